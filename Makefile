@@ -1,0 +1,29 @@
+# Build of the B200 strategy-search engine (sm_100a only) and the oracle.
+#   make            -> paper_2210_07297_b200/libamp_search.so + oracle
+#   make lib        -> the CUDA C-ABI library only
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+# -fmad=false: the reference's doubles are never FMA-contracted
+NVFLAGS := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC,-Wall,-ffp-contract=off \
+           -Xptxas -v,-warn-spills --expt-relaxed-constexpr
+PKG := paper_2210_07297_b200
+LIB := $(PKG)/libamp_search.so
+SRCS := $(PKG)/csrc/amp_search.cu $(PKG)/csrc/amp_simulate.cpp
+HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/amp_search.h
+
+all: lib oracle
+
+lib: $(LIB)
+
+$(LIB): $(SRCS) $(HDRS)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> $(PKG)/csrc/ptxas.log || (cat $(PKG)/csrc/ptxas.log; exit 1)
+	@grep -E "Compiling entry|Used|spill" $(PKG)/csrc/ptxas.log | sed 's/^ptxas info *: //' | head -40
+
+oracle:
+	$(MAKE) -f oracle/Makefile all
+
+clean:
+	rm -f $(LIB) $(PKG)/csrc/ptxas.log
+	$(MAKE) -f oracle/Makefile clean
+
+.PHONY: all lib oracle clean

@@ -1,0 +1,345 @@
+"""Benchmark of the B200 AMP strategy-search hot path.
+
+One "step" = evaluating one batch of candidate strategies end to end on the
+GPU: placement, stage-boundary bandwidths, the layer-partition DP, the cost
+estimate, and the global top-k (CTA lists -> device merge; across ranks an
+NCCL all-gather of the per-GPU top-k followed by a device merge).
+
+Workload (BASELINE.json configs[1] + configs[4]): the hetero_cluster scenario
+(30-layer GPT-2-like chain, 16 devices: 3 fast V100 nodes + 1 T4 node,
+asymmetric intra/inter bandwidth, gbs 32) swept over its 70 plan() classes
+x P placements, N_PER_GPU candidates per GPU per step
+(weak scaling).  Inputs (problem tables) are resident in HBM; the per-step
+outputs are a k-record top-k.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SCENARIO = "hetero_cluster"
+DEFAULT_N_PER_GPU = 1_000_000
+TOPK = 10
+METRIC = "candidate strategies/sec"
+UNIT = "candidates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n-per-gpu", type=int, default=DEFAULT_N_PER_GPU)
+    ap.add_argument("--cpu-sample", type=int, default=4000,
+                    help="candidates in the bounded CPU-baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def load_scenario():
+    from paper_2210_07297_b200 import problem as P
+    return P.load_scenario(os.path.join(ROOT, "tests", "golden", "scenarios", SCENARIO + ".json"))
+
+
+def workload(n_per_gpu, world):
+    n_total = n_per_gpu * world
+    n_cls = 70
+    P_ = -(-n_total // n_cls)
+    return n_total, P_
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for name, v in zip(names, r[3:7]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def cpu_sample_indices(n_total, P_, sample):
+    """Strided sample across the whole class-major range (all classes)."""
+    stride = max(1, n_total // sample)
+    return np.arange(0, n_total, stride, dtype=np.uint64)[:sample]
+
+
+def run_cpu_reference(sc, n_total, P_, sample, threads):
+    """The reference's own CPU call chain (oracle/_ref, compiled from the
+    unmodified reference sources) over a bounded strided sample."""
+    from oracle import bindings as B
+    from paper_2210_07297_b200 import problem as P
+    enc = P.EncodedProblem.from_scenario(sc)
+    idx = cpu_sample_indices(n_total, P_, sample)
+    max_pp = 16
+    if B.ref_available():
+        t0 = time.perf_counter()
+        B.ref_sweep_indices(enc, P_, 0, idx, threads, max_pp)
+        dt = time.perf_counter() - t0
+        kind = "reference"
+    else:  # the plain-C port of the same path
+        o = B.Oracle(enc, P_, 0)
+        t0 = time.perf_counter()
+        rec = np.zeros(1, dtype=__import__("paper_2210_07297_b200.planner", fromlist=["x"]).RECORD_DTYPE)
+        for i in idx:
+            o.lib.oracle_evaluate(o.h, int(i), rec.ctypes.data_as(B._recp), None, None, None)
+        dt = time.perf_counter() - t0
+        kind = "port"
+        threads = 1
+    return len(idx) / dt, dt, kind, threads, len(idx)
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sc = load_scenario()
+    n_total, P_ = workload(args.n_per_gpu, args.gpus)
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, dt, kind, th, ns = run_cpu_reference(sc, n_total, P_, args.cpu_sample, threads)
+        if i >= args.warmup:
+            vals.append(v)
+    value = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * ns / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{SCENARIO} sweep (C2 classes x placements)", "scenario": SCENARIO,
+                   "candidates_per_step": n_total, "placements_per_class": P_,
+                   "sample": f"{ns} strided candidates of the {n_total}-candidate space"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": th, "kind": kind,
+                         "sample": f"{ns} strided candidates, reference call chain "
+                                   "(heuristic/shuffled placement, optimal_assignment, estimate)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def l2_flush(buf):
+    buf.add_(1)  # write a buffer larger than L2 (126 MB)
+
+
+def our_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2210_07297_b200 import problem as P
+    from paper_2210_07297_b200.planner import RECORD_DTYPE, Searcher
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    distributed = world > 1
+    if distributed:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    sc = load_scenario()
+    n_total, P_ = workload(args.n_per_gpu, world)
+    enc = P.EncodedProblem.from_scenario(sc)
+    s = Searcher(enc, placements_per_class=P_, seed=0, device=local)
+    N_all = s.num_candidates
+    bounds = s.partition(world)
+    bounds[-1] = n_total  # truncate the class-major space to exactly n_total
+    bounds = [min(b, n_total) for b in bounds]
+    lo, hi = bounds[rank], bounds[rank + 1]
+    stream = torch.cuda.current_stream()
+    k = TOPK
+    local_top = torch.empty(k * 64, dtype=torch.uint8, device="cuda")
+    gathered = torch.empty(world * k * 64, dtype=torch.uint8, device="cuda")
+    final = torch.empty(k * 64, dtype=torch.uint8, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def step():
+        s.run_device(lo, hi, k, local_top.data_ptr(), stream.cuda_stream)
+        if distributed:
+            dist.all_gather_into_tensor(gathered, local_top)
+            s.merge_device(gathered.data_ptr(), world * k, k, final.data_ptr(), stream.cuda_stream)
+        else:
+            final.copy_(local_top)
+
+    for _ in range(args.warmup):
+        l2_flush(flush)
+        step()
+    torch.cuda.synchronize()
+    if distributed:
+        dist.barrier()
+    times = []
+    kernel_ms = []
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            l2_flush(flush)
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+            kernel_ms.append(s.stats()["kernel_ms"])  # K1+K2 events on the engine stream
+        torch.cuda.synchronize()
+    times = [a.elapsed_time(b) for a, b in ev]
+    my_ms = float(sum(times))
+    if distributed:
+        t = torch.tensor([my_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        my_ms = float(t.item())
+        dist.barrier()
+    ms_per_step = my_ms / args.steps
+    value = n_total / (ms_per_step * 1e-3)
+    st = s.stats()
+    top = np.frombuffer(final.cpu().numpy().tobytes(), dtype=RECORD_DTYPE)
+
+    # ---- roofline of the dominant kernel (K1+K2 evaluate) ---------------
+    from paper_2210_07297_b200 import _native as N
+    import ctypes as C
+    peak = C.c_double()
+    pms = C.c_double()
+    N.check(N.load().amp_fp64_peak(local, C.byref(peak), C.byref(pms)))
+    kern_ms = float(np.mean(kernel_ms))
+    achieved = st["fp64_ops"] / (kern_ms * 1e-3) / 1e12
+    peak_t = peak.value / 1e12
+
+    # ---- e2e through the C-ABI with host buffers ------------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_arm(args, enc, P_, lo, hi, n_total, world, rank, local, distributed)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{SCENARIO} sweep (C2 classes x placements)",
+                       "scenario": SCENARIO, "candidates_per_step": n_total,
+                       "candidates_per_gpu": args.n_per_gpu, "placements_per_class": P_,
+                       "topk": k, "l2": "flushed (256 MiB write) before every timed step",
+                       "parallelism": f"index-range shards x{world}, NCCL all-gather of top-k"},
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s",
+                         "frac": achieved / peak_t, "traffic": None,
+                         "kernel": "k_evaluate (K1 DP + K2 estimate)",
+                         "kernel_ms_per_step": kern_ms,
+                         "fp64_ops_per_step": st["fp64_ops"], "dp_inner_per_step": st["dp_inner"],
+                         "peak_source": "measured live: amp_fp64_peak DADD throughput (no FP64 entry "
+                                        "in MEASURED_PEAKS.json)"},
+            "gpu_launches": int(args.steps * (st["launches"] + (1 if distributed else 0))),
+            "best": {"index": int(top[0]["index"]), "total": float(top[0]["total"]),
+                     "degrees": [int(top[0]["pp"]), int(top[0]["dp"]), int(top[0]["tmp"])],
+                     "mbs": int(top[0]["mbs"])},
+            "clocks": clk.summary(),
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if world == 1 and not args.no_cpu_baseline:
+            v, dt, kind, th, ns = run_cpu_reference(sc, n_total, P_, args.cpu_sample, os.cpu_count() or 1)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": th, "kind": kind,
+                                    "sample": f"{ns} strided candidates of the same sweep, "
+                                              f"{dt:.1f} s on {th} host threads"}
+        print(json.dumps(line), flush=True)
+    s.close()
+    if distributed:
+        dist.destroy_process_group()
+
+
+def e2e_arm(args, enc, P_, lo, hi, n_total, world, rank, local, distributed):
+    """Same metric through the public C-ABI per step: amp_search_create from
+    HOST arrays (H2D of the problem), amp_search_run to a HOST top-k (D2H),
+    destroy — wall clock, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2210_07297_b200.planner import Searcher
+    k = TOPK
+    h2d = (enc.param.nbytes + enc.flops.nbytes + enc.flops_ok.nbytes + enc.act.nbytes +
+           enc.node.nbytes + enc.bw.nbytes + enc.p_layer.nbytes * 3 + enc.p_sec.nbytes)
+    d2h = k * 64
+    steps = max(1, min(args.steps, 3))
+    for i in range(1 + steps):
+        if distributed:
+            dist.barrier()
+        t0 = time.perf_counter()
+        s = Searcher(enc, placements_per_class=P_, seed=0, device=local)
+        top, _, _ = s.run(lo, hi, k=k)
+        s.close()
+        dt = time.perf_counter() - t0
+        if i == 0:
+            continue  # warm-up
+        if distributed:
+            t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        if i == 1:
+            best = dt
+        best = min(best, dt)
+    return {"value": n_total / best, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "s_per_step": best,
+            "note": "wall clock per step: amp_search_create (host arrays -> HBM, K0 tables) + "
+                    "amp_search_run (host top-k) + destroy"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        our_arm(args)
+
+
+if __name__ == "__main__":
+    main()

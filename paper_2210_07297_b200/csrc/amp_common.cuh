@@ -1,0 +1,116 @@
+// amp_common.cuh — device-side data layout shared by the kernels.
+//
+// HBM layout (all written once at amp_search_create, read-only afterwards):
+//   PairDev[n_pairs]        one entry per distinct (tmp, mbs): the layer
+//                           times, prefix sums, tolerance domain and segment
+//                           index of SegmentTimes/tolerance_domain
+//                           (reference pipeline_dp.cpp:39-91), built once
+//                           per pair instead of once per candidate.
+//   ClassDev[n_cls]         plan() candidate list (optimizer.cpp:288-293)
+//                           with gas and the pair it uses.
+//   times   [n_pairs][L]    f64 layer times (LayerTimeResolver, cost_model.cpp:74-86)
+//   prefix  [n_pairs][L+1]  f64 prefix sums, left-to-right
+//   domain  [n_pairs][nv]   f64 sorted unique segment sums (M valid)
+//   seg     [n_pairs][(L+1)^2] u16 lower_bound index of prefix[b]-prefix[a]
+//   bw      [|D|][|D|]      f64 link bandwidth, +inf diagonal
+#pragma once
+
+#include <stdint.h>
+
+#include "../../include/amp_search.h"
+
+namespace amp {
+
+constexpr int kMaxLayers = 180;        // (L(L+1)/2 + 1) <= 16384 for the smem sort
+constexpr int kSortCap = 16384;        // padded domain capacity (pow2)
+constexpr int kEvalThreads = 256;      // evaluate kernel block size
+
+struct PairDev {
+  int32_t tmp, mbs;
+  int32_t M;            // tolerance domain size
+  int32_t fail_code;    // AMP_FAIL_PROFILE_MISS / _ALLREDUCE_BANDWIDTH / 0
+  int32_t fail_layer;   // first failing layer (segment_times order)
+  int32_t pad;
+  double fail_value;
+};
+
+struct ClassDev {
+  int32_t pp, dp, tmp, mbs;
+  int32_t gas, pair;
+  int32_t pad0, pad1;
+};
+
+// Contiguous run of candidate indices of one class, handed out
+// heaviest-class-first by the persistent evaluate kernel.
+struct Segment {
+  uint64_t first;   // first candidate index
+  uint64_t count;   // number of candidates
+  uint64_t offset;  // exclusive prefix of counts in dispatch order
+  uint64_t out;     // position of `first` in the caller's output order
+};
+
+struct EvalParams {
+  // problem
+  int32_t L, D, gbs, max_pp;
+  uint64_t P, seed;
+  const double* param;      // [L]
+  const double* act;        // [L-1]
+  const double* bw;         // [D*D]
+  const int32_t* base_order;  // [D] heuristic device order
+  int32_t has_ceiling;
+  int32_t n_pairs;
+  double ceiling;
+  double bpp;
+  // tables
+  const ClassDev* cls;
+  const PairDev* pairs;
+  const double* times;
+  const double* prefix;
+  const double* domain;
+  const uint16_t* seg;
+  int32_t nv_stride;        // domain stride per pair
+  int32_t slice_in_smem;    // 1: DP stage slice in shared memory
+  // work list
+  const Segment* segs;
+  int32_t n_segs;
+  int32_t pad0;
+  uint64_t n_work;
+  const uint64_t* index_list;  // explicit indices (evaluate) or NULL
+  unsigned long long* counter;
+  // scratch (per CTA)
+  uint8_t* bp;              // backpointers, bp_stride bytes per CTA
+  uint64_t bp_stride;
+  double* slice;            // global stage slice when !slice_in_smem
+  uint64_t slice_stride;    // doubles per CTA
+  int32_t* place;           // placement, D per CTA
+  // outputs
+  amp_record* all;          // [n_work] in output order, or NULL
+  int32_t* all_cuts;        // [n_work * (max_pp+1)]
+  double* all_stage;        // [n_work * max_pp]
+  double* all_edge;         // [n_work * max_pp]
+  int32_t* all_place;       // [n_work * D]
+  amp_record* cta_topk;     // [gridDim.x * k]
+  int32_t k;
+  int32_t max_M;
+};
+
+// splitmix64; integer-only, identical on host.
+__host__ __device__ inline uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+// Ranking key of rank_records (optimizer.cpp:264-282): non-failed first,
+// then total ascending, then (pp, dp, tmp, mbs[, p]) == candidate index.
+// fail_code < 0 marks an empty slot that sorts after everything.
+__host__ __device__ inline bool rank_less(const amp_record& a, const amp_record& b) {
+  const int ca = a.fail_code < 0 ? 2 : (a.fail_code != 0 ? 1 : 0);
+  const int cb = b.fail_code < 0 ? 2 : (b.fail_code != 0 ? 1 : 0);
+  if (ca != cb) return ca < cb;
+  if (ca == 0 && a.total != b.total) return a.total < b.total;
+  return a.index < b.index;
+}
+
+}  // namespace amp

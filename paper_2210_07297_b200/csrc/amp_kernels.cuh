@@ -1,0 +1,852 @@
+// amp_kernels.cuh — sm_100a kernels of the strategy search.
+//
+//   K0 k_pair_tables   one CTA per distinct (tmp, mbs): layer times
+//                      (LayerTimeResolver, cost_model.cpp:74-86), prefix
+//                      sums, tolerance domain (bitonic sort + unique in
+//                      smem), segment index (pipeline_dp.cpp:39-91).
+//   K1+K2 k_evaluate   persistent CTAs; per candidate: placement, stage
+//                      boundary bandwidths, the tolerance-indexed DP as a
+//                      shared-memory row wavefront (pipeline_dp.cpp:70-149),
+//                      ceiling check, estimate (cost_model.cpp:176-212),
+//                      record + CTA-local top-k.
+//   K3 k_merge_topk    deterministic k-round block argmin of the CTA lists.
+//
+// Numerics: compiled with -fmad=false; every sum is evaluated in the
+// reference's order (SURVEY.md §8(a) numerics contract).  min/max
+// reductions are exact and may be reordered; argmin/argmax ties are broken
+// toward the reference's sequential winner (lowest cut / lowest replica).
+#pragma once
+
+#include <math_constants.h>
+
+#include "amp_common.cuh"
+
+namespace amp {
+
+// std::min(a, b) with the reference's argument order: (b < a) ? b : a.
+__device__ __forceinline__ double std_min(double a, double b) { return b < a ? b : a; }
+// std::max(a, b): (a < b) ? b : a.
+__device__ __forceinline__ double std_max(double a, double b) { return a < b ? b : a; }
+// std::max(0.0, x)
+__device__ __forceinline__ double max0(double x) { return 0.0 < x ? x : 0.0; }
+
+// ---------------------------------------------------------------------------
+// block helpers
+// ---------------------------------------------------------------------------
+
+// Block-wide min with std_min semantics (NaN never enters); all threads get it.
+__device__ double block_min(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = std_min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < (int)(blockDim.x >> 5) ? red[l] : CUDART_INF;
+    for (int o = 16; o > 0; o >>= 1) v = std_min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (l == 0) red[0] = v;
+  }
+  __syncthreads();
+  v = red[0];
+  __syncthreads();
+  return v;
+}
+
+// Block-wide (max value, lowest index) over candidates; NaN/-1 idx skipped.
+__device__ void block_argmax(double& v, int& idx, double* red, int* redi) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (oi >= 0 && (idx < 0 || ov > v || (ov == v && oi < idx))) {
+      v = ov;
+      idx = oi;
+    }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) {
+    red[w] = v;
+    redi[w] = idx;
+  }
+  __syncthreads();
+  if (w == 0) {
+    v = l < (int)(blockDim.x >> 5) ? red[l] : -CUDART_INF;
+    idx = l < (int)(blockDim.x >> 5) ? redi[l] : -1;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (oi >= 0 && (idx < 0 || ov > v || (ov == v && oi < idx))) {
+        v = ov;
+        idx = oi;
+      }
+    }
+    if (l == 0) {
+      red[0] = v;
+      redi[0] = idx;
+    }
+  }
+  __syncthreads();
+  v = red[0];
+  idx = redi[0];
+  __syncthreads();
+}
+
+__device__ int block_min_int(int v, int* redi) {
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) redi[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < (int)(blockDim.x >> 5) ? redi[l] : 0x7fffffff;
+    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (l == 0) redi[0] = v;
+  }
+  __syncthreads();
+  v = redi[0];
+  __syncthreads();
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// tolerance domain (pipeline_dp.cpp:55-68) + segment index (83-91)
+// ---------------------------------------------------------------------------
+
+// Builds the sorted unique domain of {0} U {P[b]-P[a]} into dom_out[0..M)
+// and seg_out[a*(L+1)+b].  `vals` is smem scratch of npow2 doubles
+// (npow2 >= 1 + L(L+1)/2, power of two).  Returns M (all threads).
+__device__ int build_domain(const double* Pf, int L, double* vals, int npow2, double* dom_out,
+                            uint16_t* seg_out, int* redi) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int nv = 1 + L * (L + 1) / 2;
+  for (int x = tid; x < npow2; x += nt) {
+    double v = CUDART_INF;
+    if (x == 0) {
+      v = 0.0;
+    } else if (x < nv) {
+      // x-1 enumerates (a, b), a < b, row-major over a (same multiset as the
+      // reference's push order; the order is irrelevant after sorting).
+      int r = x - 1, a = 0, len = L;
+      while (r >= len) {
+        r -= len;
+        ++a;
+        --len;
+      }
+      const int b = a + 1 + r;
+      v = Pf[b] - Pf[a];
+    }
+    vals[x] = v;
+  }
+  __syncthreads();
+  // bitonic sort ascending
+  for (int size = 2; size <= npow2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int x = tid; x < (npow2 >> 1); x += nt) {
+        const int lo = 2 * x - (x & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = ((lo & size) == 0);
+        const double a = vals[lo], b = vals[hi];
+        if ((a > b) == up) {
+          vals[lo] = b;
+          vals[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // unique (exact ==): chunked scan, one contiguous chunk per thread
+  const int chunk = (nv + nt - 1) / nt;
+  const int c0 = tid * chunk, c1 = min(nv, c0 + chunk);
+  int cnt = 0;
+  for (int x = c0; x < c1; ++x)
+    if (x == 0 || !(vals[x] == vals[x - 1])) ++cnt;
+  // exclusive scan of cnt over threads (warp shuffles + smem)
+  int incl = cnt;
+  const int l = tid & 31, w = tid >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (l >= o) incl += y;
+  }
+  __syncthreads();
+  if (l == 31) redi[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int s = l < (nt >> 5) ? redi[l] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (l >= o) s += y;
+    }
+    if (l < (nt >> 5)) redi[32 + l] = s;  // inclusive per warp
+  }
+  __syncthreads();
+  int pos = incl - cnt + (w > 0 ? redi[32 + w - 1] : 0);
+  const int M = redi[32 + (nt >> 5) - 1];
+  for (int x = c0; x < c1; ++x)
+    if (x == 0 || !(vals[x] == vals[x - 1])) dom_out[pos++] = vals[x];
+  __syncthreads();
+  // seg_index: lower_bound of each segment sum (exact member of the domain)
+  for (int x = tid; x < (L + 1) * (L + 1); x += nt) {
+    const int a = x / (L + 1), b = x % (L + 1);
+    int idx = 0;
+    if (a < b) {
+      const double v = Pf[b] - Pf[a];
+      int lo = 0, hi = M;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (dom_out[mid] < v) lo = mid + 1;
+        else hi = mid;
+      }
+      idx = lo;
+    }
+    seg_out[x] = (uint16_t)idx;
+  }
+  __syncthreads();
+  return M;
+}
+
+// ---------------------------------------------------------------------------
+// K1: tolerance-indexed layer-partition DP (pipeline_dp.cpp:70-149)
+// ---------------------------------------------------------------------------
+//
+// Stage slice C[i][m] (i in [0, L], m in [0, M)) lives in shared memory (or
+// in a per-CTA global buffer for large M).  Stage j is computed in place,
+// rows i descending: row i at stage j reads only rows cut < i at stage j-1,
+// which have not been overwritten yet; one barrier per row orders the
+// overwrite.  Threads own domain columns m; the cut loop runs ascending with
+// a strict '<', so the smallest cut wins ties exactly like the reference.
+// Backpointers (one byte per (j, i, m)) go to global scratch; thread 0
+// backtracks from (L, k, m = 0).
+template <class EdgeFn>
+__device__ double dp_solve(const int L, const int k, const int gas, const int M,
+                           const double* __restrict__ Pf, const double* __restrict__ Dm,
+                           const uint16_t* __restrict__ seg, const EdgeFn& edge, double* C,
+                           double* E, uint8_t* __restrict__ bp, int* cuts) {
+  const double g1 = (double)(gas - 1);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int LP = L + 1;
+  // base case j = 1 (102-107): t1 = between(0, i) = prefix[i] - prefix[0]
+  for (int x = tid; x < L * M; x += nt) {
+    const int i = 1 + x / M, m = x - (i - 1) * M;
+    const double t1 = Pf[i] - Pf[0];
+    C[(size_t)i * M + m] = g1 * max0(t1 - Dm[m]) + t1;
+  }
+  __syncthreads();
+  for (int j = 2; j <= k; ++j) {
+    for (int cut = j - 1 + tid; cut < L; cut += nt) E[cut] = edge(cut, j - 2);
+    __syncthreads();
+    uint8_t* bpj = bp + (size_t)j * LP * M;
+    for (int i = L; i >= j; --i) {
+      const double Pi = Pf[i];
+      for (int m = tid; m < M; m += nt) {
+        const double dm = Dm[m];
+        double best = CUDART_INF;
+        int bc = -1;
+        for (int cut = j - 1; cut < i; ++cut) {
+          const double t2 = Pi - Pf[cut];
+          const int s = seg[cut * LP + i];
+          const double sub = C[(size_t)cut * M + (s > m ? s : m)];
+          const double g = ((sub + g1 * max0(t2 - dm)) + t2) + E[cut];
+          if (g < best) {
+            best = g;
+            bc = cut;
+          }
+        }
+        C[(size_t)i * M + m] = best;
+        bpj[(size_t)i * M + m] = (uint8_t)bc;
+      }
+      __syncthreads();
+    }
+  }
+  double cost = 0.0;
+  if (tid == 0) {
+    cost = C[(size_t)L * M + 0];
+    cuts[k] = L;
+    int i = L, m = 0;
+    for (int j = k; j >= 2; --j) {
+      const int cut = bp[((size_t)j * LP + i) * M + m];
+      cuts[j - 1] = cut;
+      const int s = seg[cut * LP + i];
+      m = s > m ? s : m;
+      i = cut;
+    }
+    cuts[0] = 0;
+  }
+  __syncthreads();
+  return cost;
+}
+
+// ---------------------------------------------------------------------------
+// K0: per-(tmp, mbs) tables
+// ---------------------------------------------------------------------------
+
+struct TableParams {
+  int32_t L, n_pairs, npow2;
+  int32_t fallback_enabled;
+  const int32_t* pair_tmp;      // [n_pairs]
+  const int32_t* pair_mbs;      // [n_pairs]
+  const double* cube;           // [n_pairs][L] profile seconds
+  const uint8_t* cube_hit;      // [n_pairs][L]
+  const double* flops;          // [L]
+  const uint8_t* flops_ok;      // [L]
+  const double* act;            // [L-1]
+  double device_flops, tmp_bandwidth;
+  PairDev* pairs;
+  double* times;
+  double* prefix;
+  double* domain;
+  uint16_t* seg;
+  int32_t nv_stride;
+};
+
+__global__ void k_pair_tables(TableParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* vals = reinterpret_cast<double*>(smem_raw);
+  double* Pf = vals + p.npow2;
+  __shared__ int redi[64];
+  const int pr = blockIdx.x, L = p.L, tid = threadIdx.x;
+  const int tmp = p.pair_tmp[pr], mbs = p.pair_mbs[pr];
+  double* times = p.times + (size_t)pr * L;
+  // LayerTimeResolver::layer_time (cost_model.cpp:74-86): profile hit, else
+  // analytic fallback (61-68) with allreduce_time (40-52), else miss.
+  int my_fail = 0x7fffffff;  // (layer << 3) | code, min = first failing layer
+  for (int l = tid; l < L; l += blockDim.x) {
+    double t = 0.0;
+    int code = 0;
+    if (p.cube_hit[(size_t)pr * L + l]) {
+      t = p.cube[(size_t)pr * L + l];
+    } else if (!p.fallback_enabled || !p.flops_ok[l]) {
+      code = AMP_FAIL_PROFILE_MISS;
+    } else {
+      const double vol = L <= 1 ? 0.0 : (l < L - 1 ? p.act[l] : p.act[l - 1]);
+      const double message = vol * mbs;
+      const double compute = (double)mbs * p.flops[l] / ((double)tmp * p.device_flops);
+      double ar = 0.0;
+      if (tmp != 1) {
+        if (!(p.tmp_bandwidth > 0)) code = AMP_FAIL_ALLREDUCE_BANDWIDTH;
+        else ar = 2.0 * (double)(tmp - 1) * message / ((double)tmp * p.tmp_bandwidth);
+      }
+      t = compute + ar;
+    }
+    times[l] = t;
+    if (code) my_fail = min(my_fail, (l << 3) | code);
+  }
+  const int fail = block_min_int(my_fail, redi);
+  if (tid == 0) {
+    PairDev d;
+    d.tmp = tmp;
+    d.mbs = mbs;
+    d.M = 0;
+    d.fail_code = fail == 0x7fffffff ? 0 : (fail & 7);
+    d.fail_layer = fail == 0x7fffffff ? -1 : (fail >> 3);
+    d.pad = 0;
+    d.fail_value = d.fail_code == AMP_FAIL_ALLREDUCE_BANDWIDTH ? p.tmp_bandwidth : 0.0;
+    p.pairs[pr] = d;
+  }
+  __syncthreads();
+  if (fail != 0x7fffffff) return;  // every candidate of this pair fails
+  // prefix sums, strictly left to right (pipeline_dp.cpp:39-44)
+  if (tid == 0) {
+    double s = 0.0;
+    Pf[0] = 0.0;
+    for (int l = 0; l < L; ++l) {
+      s = s + times[l];
+      Pf[l + 1] = s;
+    }
+  }
+  __syncthreads();
+  for (int x = tid; x <= L; x += blockDim.x) p.prefix[(size_t)pr * (L + 1) + x] = Pf[x];
+  const int M = build_domain(Pf, L, vals, p.npow2, p.domain + (size_t)pr * p.nv_stride,
+                             p.seg + (size_t)pr * (L + 1) * (L + 1), redi);
+  if (tid == 0) p.pairs[pr].M = M;
+}
+
+// ---------------------------------------------------------------------------
+// K1+K2: persistent candidate evaluation
+// ---------------------------------------------------------------------------
+
+struct EdgeFromBandwidth {  // placement_edge_cost (optimizer.cpp:130-139)
+  const double* act;
+  const double* bwq;
+  int mbs;
+  __device__ double operator()(int cut, int q) const { return act[cut - 1] * mbs / bwq[q]; }
+};
+
+struct EvalShared {
+  int cand_t;
+  int done;
+  uint64_t index, out_pos;
+  int n_top;
+  int fail_code, fail_layer;
+  double fail_value;
+  double pipeline, dpsync;
+  int best_r;
+};
+
+__device__ void topk_insert(amp_record* list, int& n, int k, const amp_record& r) {
+  if (n == k && !rank_less(r, list[k - 1])) return;
+  int pos = n < k ? n : k - 1;
+  while (pos > 0 && rank_less(r, list[pos - 1])) {
+    list[pos] = list[pos - 1];
+    --pos;
+  }
+  list[pos] = r;
+  if (n < k) ++n;
+}
+
+__global__ void __launch_bounds__(kEvalThreads) k_evaluate(EvalParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ EvalShared sh;
+  __shared__ double red[32];
+  __shared__ int redi[64];
+  const int L = p.L, D = p.D, LP = L + 1, tid = threadIdx.x, nt = blockDim.x;
+  const int maxM = p.max_M, maxpp = p.max_pp;
+  // dynamic smem carve-up
+  unsigned char* sp = smem_raw;
+  double* C = nullptr;
+  if (p.slice_in_smem) {
+    C = reinterpret_cast<double*>(sp);
+    sp += sizeof(double) * (size_t)LP * maxM;
+  } else {
+    C = p.slice + (size_t)blockIdx.x * p.slice_stride;
+  }
+  double* Dm = reinterpret_cast<double*>(sp);
+  sp += sizeof(double) * maxM;
+  double* Pf = reinterpret_cast<double*>(sp);
+  sp += sizeof(double) * LP;
+  double* E = reinterpret_cast<double*>(sp);
+  sp += sizeof(double) * L;
+  double* bwq = reinterpret_cast<double*>(sp);
+  sp += sizeof(double) * maxpp;
+  double* st = reinterpret_cast<double*>(sp);
+  sp += sizeof(double) * maxpp;
+  int* cuts = reinterpret_cast<int*>(sp);
+  sp += sizeof(int) * (maxpp + 2);
+  int* place = reinterpret_cast<int*>(sp);
+  sp += sizeof(int) * D;
+  sp = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sp) + 15) & ~uintptr_t(15));
+  uint16_t* seg = reinterpret_cast<uint16_t*>(sp);
+
+  uint8_t* bp = p.bp + (size_t)blockIdx.x * p.bp_stride;
+  amp_record* mytop = p.cta_topk + (size_t)blockIdx.x * p.k;
+  if (tid == 0) sh.n_top = 0;
+
+  for (;;) {
+    if (tid == 0) {
+      const unsigned long long t = atomicAdd(p.counter, 1ull);
+      sh.done = t >= p.n_work;
+      if (!sh.done) {
+        if (p.index_list) {
+          sh.index = p.index_list[t];
+          sh.out_pos = t;
+        } else {
+          int lo = 0, hi = p.n_segs - 1;  // last segment with offset <= t
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (p.segs[mid].offset <= t) lo = mid;
+            else hi = mid - 1;
+          }
+          const uint64_t d = t - p.segs[lo].offset;
+          sh.index = p.segs[lo].first + d;
+          sh.out_pos = p.segs[lo].out + d;
+        }
+      }
+      sh.fail_code = 0;
+      sh.fail_layer = -1;
+      sh.fail_value = 0.0;
+    }
+    __syncthreads();
+    if (sh.done) break;
+    const uint64_t index = sh.index;
+    const int c = (int)(index / p.P);
+    const uint64_t pl = index % p.P;
+    const ClassDev cl = p.cls[c];
+    const int pp = cl.pp, dp = cl.dp, tmp = cl.tmp, mbs = cl.mbs, gas = cl.gas;
+    const PairDev pr = p.pairs[cl.pair];
+    const int M = pr.M;
+    double total = CUDART_NAN;
+    bool ok = false;
+
+    if (pp > L) {  // optimizer.cpp:149-152
+      if (tid == 0) sh.fail_code = AMP_FAIL_PP_GT_L;
+    } else if (pr.fail_code) {  // segment_times: first failing layer
+      if (tid == 0) {
+        sh.fail_code = pr.fail_code;
+        sh.fail_layer = pr.fail_layer;
+        sh.fail_value = pr.fail_value;
+      }
+    } else {
+      ok = true;
+    }
+    __syncthreads();
+    if (ok) {
+      // ---- placement: heuristic order, Fisher-Yates for p >= 1 ----------
+      for (int x = tid; x < D; x += nt) place[x] = p.base_order[x];
+      __syncthreads();
+      if (pl != 0 && tid == 0) {
+        uint64_t r = splitmix64(p.seed ^ pl);
+        for (int kk = D - 1; kk >= 1; --kk) {
+          const int jj = (int)(r % (uint64_t)(kk + 1));
+          const int t = place[kk];
+          place[kk] = place[jj];
+          place[jj] = t;
+          r = splitmix64(r);
+        }
+      }
+      // ---- DP inputs ---------------------------------------------------
+      const double* gdom = p.domain + (size_t)cl.pair * p.nv_stride;
+      for (int x = tid; x < M; x += nt) Dm[x] = gdom[x];
+      for (int x = tid; x < LP; x += nt) Pf[x] = p.prefix[(size_t)cl.pair * LP + x];
+      const uint16_t* gseg = p.seg + (size_t)cl.pair * LP * LP;
+      for (int x = tid; x < LP * LP; x += nt) seg[x] = gseg[x];
+      __syncthreads();
+      // min_edge_bandwidth per stage boundary (cost_model.cpp:164-174)
+      for (int q = tid; q < pp - 1; q += nt) {
+        double b = CUDART_INF;
+        for (int r = 0; r < dp; ++r)
+          for (int s = 0; s < tmp; ++s)
+            b = std_min(b, p.bw[(size_t)place[(q * dp + r) * tmp + s] * D +
+                                place[((q + 1) * dp + r) * tmp + s]]);
+        bwq[q] = b;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int q = 0; q + 1 < pp; ++q)
+          if (!(bwq[q] > 0)) {  // p2p_time throws inside the DP's edge fn
+            sh.fail_code = AMP_FAIL_P2P_BANDWIDTH;
+            sh.fail_value = bwq[q];
+            break;
+          }
+      }
+      __syncthreads();
+      ok = sh.fail_code == 0;
+    }
+    if (ok) {
+      EdgeFromBandwidth ef{p.act, bwq, mbs};
+      dp_solve(L, pp, gas, M, Pf, Dm, seg, ef, C, E, bp, cuts);
+      // ---- per-device parameter ceiling (optimizer.cpp:159-169) ---------
+      const double* tl = p.times + (size_t)cl.pair * L;
+      if (tid < pp) {
+        double sum = 0.0;  // stage_time (cost_model.cpp:88-98)
+        for (int l = cuts[tid]; l < cuts[tid + 1]; ++l) sum += tl[l];
+        st[tid] = sum;
+      }
+      if (tid == 0 && p.has_ceiling) {
+        double worst = 0.0;
+        for (int j = 0; j < pp; ++j) {
+          double s = 0.0;  // params_in_range (types.cpp:34-40)
+          for (int l = cuts[j]; l < cuts[j + 1]; ++l) s += p.param[l];
+          worst = std_max(worst, s / tmp);
+        }
+        if (worst > p.ceiling) sh.fail_code = AMP_FAIL_CEILING;
+      }
+      __syncthreads();
+      ok = sh.fail_code == 0;
+    }
+    if (ok) {
+      // ---- estimate: pipeline term (cost_model.cpp:176-212) -------------
+      double slowest_stage = st[0];  // std::max_element: first maximum
+      for (int j = 1; j < pp; ++j)
+        if (slowest_stage < st[j]) slowest_stage = st[j];
+      const double g1 = (double)(gas - 1);
+      double my_best = -CUDART_INF;
+      int my_r = -1;
+      for (int r = tid; r < dp; r += nt) {
+        double sum = 0.0;
+        for (int q = 0; q + 1 < pp; ++q) {  // replica_edge_times (145-162)
+          const int cut = cuts[q + 1];
+          const double volume = p.act[cut - 1] * mbs;
+          double b = CUDART_INF;
+          for (int s = 0; s < tmp; ++s)
+            b = std_min(b, p.bw[(size_t)place[(q * dp + r) * tmp + s] * D +
+                                place[((q + 1) * dp + r) * tmp + s]]);
+          sum = sum + volume / b;
+        }
+        for (int j = 0; j < pp; ++j) sum = sum + st[j];
+        const double tr = g1 * slowest_stage + sum;  // pipeline_time (100-120)
+        if (tr > my_best) {  // strict '>' over ascending r: first maximum
+          my_best = tr;
+          my_r = r;
+        }
+      }
+      block_argmax(my_best, my_r, red, redi);
+      // ---- dpsync_time (122-143) ---------------------------------------
+      double worst = 0.0;
+      int bad_group = 0x7fffffff;
+      double bad_value = 0.0;
+      if (dp != 1) {
+        const int ngroups = pp * tmp;
+        if (dp <= 8) {
+          // one thread per (stage, shard) group
+          for (int g = tid; g < ngroups; g += nt) {
+            const int j = g / tmp, s = g % tmp;
+            double sp_ = 0.0;
+            for (int l = cuts[j]; l < cuts[j + 1]; ++l) sp_ += p.param[l];
+            const double message = sp_ * p.bpp / tmp;
+            double b = CUDART_INF;  // make_comm_group (23-38)
+            for (int r1 = 0; r1 < dp; ++r1)
+              for (int r2 = r1 + 1; r2 < dp; ++r2)
+                b = std_min(b, p.bw[(size_t)place[(j * dp + r1) * tmp + s] * D +
+                                    place[(j * dp + r2) * tmp + s]]);
+            if (!(b > 0)) {
+              if (g < bad_group) {
+                bad_group = g;
+                bad_value = b;
+              }
+            } else {
+              worst = std_max(worst, 2.0 * (double)(dp - 1) * message / ((double)dp * b));
+            }
+          }
+        } else {
+          // block-cooperative pair minimum per group
+          for (int g = 0; g < ngroups; ++g) {
+            const int j = g / tmp, s = g % tmp;
+            double b = CUDART_INF;
+            for (int x = tid; x < dp * dp; x += nt) {
+              const int r1 = x / dp, r2 = x - r1 * dp;
+              if (r1 < r2)
+                b = std_min(b, p.bw[(size_t)place[(j * dp + r1) * tmp + s] * D +
+                                    place[(j * dp + r2) * tmp + s]]);
+            }
+            b = block_min(b, red);
+            if (tid == 0) {
+              double sp_ = 0.0;
+              for (int l = cuts[j]; l < cuts[j + 1]; ++l) sp_ += p.param[l];
+              const double message = sp_ * p.bpp / tmp;
+              if (!(b > 0)) {
+                if (g < bad_group) {
+                  bad_group = g;
+                  bad_value = b;
+                }
+              } else {
+                worst = std_max(worst, 2.0 * (double)(dp - 1) * message / ((double)dp * b));
+              }
+            }
+          }
+        }
+      }
+      // reduce worst (max, NaN-free) and first bad group
+      {
+        double w2 = -worst;
+        w2 = block_min(w2, red);
+        worst = -w2;
+        const int bg = block_min_int(bad_group, redi);
+        if (bg != 0x7fffffff) {
+          if (bad_group == bg) {
+            sh.fail_code = AMP_FAIL_ALLREDUCE_BANDWIDTH;
+            sh.fail_value = bad_value;
+          }
+        }
+        if (tid == 0) {
+          sh.pipeline = my_best;
+          sh.dpsync = worst;
+          sh.best_r = my_r;
+        }
+        __syncthreads();
+        ok = sh.fail_code == 0;
+        total = sh.pipeline + sh.dpsync;
+      }
+    }
+    // ---- record ---------------------------------------------------------
+    if (tid == 0) {
+      amp_record rec;
+      rec.index = index;
+      rec.pp = pp;
+      rec.dp = dp;
+      rec.tmp = tmp;
+      rec.mbs = mbs;
+      rec.fail_code = sh.fail_code;
+      rec.fail_layer = sh.fail_layer;
+      rec.fail_value = sh.fail_value;
+      if (ok) {
+        rec.total = total;
+        rec.pipeline_time = sh.pipeline;
+        rec.dpsync_time = sh.dpsync;
+      } else {
+        rec.total = rec.pipeline_time = rec.dpsync_time = CUDART_NAN;
+      }
+      topk_insert(mytop, sh.n_top, p.k, rec);
+      if (p.all) p.all[sh.out_pos] = rec;
+    }
+    if (p.all_cuts) {
+      int32_t* o = p.all_cuts + sh.out_pos * (maxpp + 1);
+      for (int q = tid; q <= maxpp; q += nt) o[q] = (ok && q <= pp) ? cuts[q] : -1;
+    }
+    if (p.all_stage) {
+      double* o = p.all_stage + sh.out_pos * maxpp;
+      for (int q = tid; q < maxpp; q += nt) o[q] = (ok && q < pp) ? st[q] : CUDART_NAN;
+    }
+    if (p.all_edge) {
+      double* o = p.all_edge + sh.out_pos * maxpp;
+      const int r = sh.best_r;
+      for (int q = tid; q < maxpp; q += nt) {
+        double v = CUDART_NAN;
+        if (ok && q + 1 < pp) {
+          const int cut = cuts[q + 1];
+          double b = CUDART_INF;
+          for (int s = 0; s < tmp; ++s)
+            b = std_min(b, p.bw[(size_t)place[(q * dp + r) * tmp + s] * D +
+                                place[((q + 1) * dp + r) * tmp + s]]);
+          v = p.act[cut - 1] * mbs / b;
+        }
+        o[q] = v;
+      }
+    }
+    if (p.all_place) {
+      int32_t* o = p.all_place + sh.out_pos * D;
+      const bool placed = ok;  // failed records keep a default placement
+      for (int x = tid; x < D; x += nt) o[x] = placed ? place[x] : -1;
+    }
+    __syncthreads();
+  }
+  // pad the CTA list to k entries
+  if (tid == 0) {
+    for (int x = sh.n_top; x < p.k; ++x) {
+      amp_record e;
+      e.index = ~0ull;
+      e.total = e.pipeline_time = e.dpsync_time = CUDART_NAN;
+      e.pp = e.dp = e.tmp = e.mbs = 0;
+      e.fail_code = -1;
+      e.fail_layer = -1;
+      e.fail_value = 0.0;
+      mytop[x] = e;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: deterministic merge (k rounds of block argmin under rank_less)
+// ---------------------------------------------------------------------------
+
+__global__ void k_merge_topk(const amp_record* in, int n, int k, amp_record* out,
+                             unsigned char* taken) {
+  __shared__ int best_idx[32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int x = tid; x < n; x += nt) taken[x] = 0;
+  __syncthreads();
+  for (int round = 0; round < k; ++round) {
+    int bi = -1;
+    for (int x = tid; x < n; x += nt)
+      if (!taken[x] && (bi < 0 || rank_less(in[x], in[bi]))) bi = x;
+    for (int o = 16; o > 0; o >>= 1) {
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (oi >= 0 && (bi < 0 || rank_less(in[oi], in[bi]))) bi = oi;
+    }
+    if ((tid & 31) == 0) best_idx[tid >> 5] = bi;
+    __syncthreads();
+    if (tid == 0) {
+      int b = -1;
+      for (int w = 0; w < (nt >> 5); ++w) {
+        const int oi = best_idx[w];
+        if (oi >= 0 && (b < 0 || rank_less(in[oi], in[b]))) b = oi;
+      }
+      if (b >= 0) {
+        out[round] = in[b];
+        taken[b] = 1;
+      } else {
+        amp_record e;
+        e.index = ~0ull;
+        e.total = e.pipeline_time = e.dpsync_time = CUDART_NAN;
+        e.pp = e.dp = e.tmp = e.mbs = 0;
+        e.fail_code = -1;
+        e.fail_layer = -1;
+        e.fail_value = 0.0;
+        out[round] = e;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// standalone DP batch (amp_dp_solve_batch)
+// ---------------------------------------------------------------------------
+
+struct DpBatchItem {
+  int32_t L, stages, gas, status;
+  const double* times;
+  const double* edges;
+};
+
+struct EdgeFromTable {
+  const double* e;
+  int L;
+  __device__ double operator()(int cut, int q) const { return e[(size_t)q * L + cut]; }
+};
+
+struct DpBatchParams {
+  const DpBatchItem* items;
+  int32_t n, max_L, max_k, npow2;
+  int32_t cut_stride;
+  int32_t* cuts_out;
+  double* cost_out;
+  uint8_t* bp;
+  uint64_t bp_stride;
+  double* slice;
+  uint64_t slice_stride;
+  double* domain;  // per-CTA scratch [npow2]
+  uint16_t* seg;   // per-CTA scratch [(max_L+1)^2]
+};
+
+__global__ void k_dp_batch(DpBatchParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int redi[64];
+  double* vals = reinterpret_cast<double*>(smem_raw);
+  const int tid = threadIdx.x;
+  double* Pf = vals + p.npow2;
+  double* E = Pf + p.max_L + 1;
+  int* cuts = reinterpret_cast<int*>(E + p.max_L);
+  double* dom = p.domain + (size_t)blockIdx.x * p.npow2;
+  uint16_t* seg = p.seg + (size_t)blockIdx.x * (p.max_L + 1) * (p.max_L + 1);
+  double* C = p.slice + (size_t)blockIdx.x * p.slice_stride;
+  uint8_t* bp = p.bp + (size_t)blockIdx.x * p.bp_stride;
+  for (int inst = blockIdx.x; inst < p.n; inst += gridDim.x) {
+    const DpBatchItem it = p.items[inst];
+    if (it.status != 0) continue;
+    const int L = it.L;
+    if (tid == 0) {
+      double s = 0.0;
+      Pf[0] = 0.0;
+      for (int l = 0; l < L; ++l) {
+        s = s + it.times[l];
+        Pf[l + 1] = s;
+      }
+    }
+    __syncthreads();
+    int np2 = 2;
+    while (np2 < 1 + L * (L + 1) / 2) np2 <<= 1;
+    const int M = build_domain(Pf, L, vals, np2, dom, seg, redi);
+    EdgeFromTable ef{it.edges, L};
+    const double cost = dp_solve(L, it.stages, it.gas, M, Pf, dom, seg, ef, C, E, bp, cuts);
+    if (tid == 0) {
+      p.cost_out[inst] = cost;
+      for (int q = 0; q <= it.stages; ++q) p.cuts_out[(size_t)inst * p.cut_stride + q] = cuts[q];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FP64 add throughput probe (roofline denominator)
+// ---------------------------------------------------------------------------
+
+__global__ void k_dadd_peak(double* out, int iters, double a) {
+  double x0 = threadIdx.x * 1e-9, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
+  double x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      x0 = x0 + a;
+      x1 = x1 + a;
+      x2 = x2 + a;
+      x3 = x3 + a;
+      x4 = x4 + a;
+      x5 = x5 + a;
+      x6 = x6 + a;
+      x7 = x7 + a;
+    }
+  }
+  const double s = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+  if (s == 1234.5) out[0] = s;
+}
+
+}  // namespace amp

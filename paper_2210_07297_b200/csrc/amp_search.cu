@@ -1,0 +1,871 @@
+// amp_search.cu — host side of the C ABI declared in include/amp_search.h.
+//
+// Owns the device tables, launches K0 (pair tables) at create time and
+// K1+K2 (evaluate) + K3 (merge) per run.  No CPU evaluation path exists:
+// every candidate is evaluated by the sm_100a kernels; the host only
+// enumerates classes (integers), encodes the profile map into a dense cube,
+// and schedules work.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "amp_common.cuh"
+#include "amp_kernels.cuh"
+
+using namespace amp;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t ensure(size_t n) {
+    if (n <= bytes && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, n ? n : 16);
+    if (e == cudaSuccess) bytes = n;
+    return e;
+  }
+  template <class T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+std::vector<int> divisors(int n) {
+  std::vector<int> out;
+  for (int d = 1; d * d <= n; ++d)
+    if (n % d == 0) {
+      out.push_back(d);
+      if (d != n / d) out.push_back(n / d);
+    }
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
+}  // namespace
+
+struct amp_ctx {
+  int device = 0;
+  std::string err;
+  int L = 0, D = 0, gbs = 0;
+  uint64_t P = 1, seed = 0;
+  int max_ctas_cfg = 0;
+  int has_ceiling = 0;
+  double ceiling = 0.0, bpp = 2.0;
+  std::vector<ClassDev> classes;
+  std::vector<PairDev> pairs;
+  std::vector<double> class_inner;  // DP inner iterations per candidate
+  std::vector<double> class_lt;     // of which m < seg(cut, i)
+  std::vector<double> class_cells;
+  int max_pp = 1, max_M = 1, nv_stride = 1, npow2 = 2;
+  size_t bp_stride = 0, slice_stride = 0;
+  int slice_in_smem = 1;
+  size_t smem_bytes = 0;
+  int n_ctas = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+  DevBuf param, act, bw, base_order, times, prefix, domain, seg, pairs_d, cls_d;
+  DevBuf bp, slice, cta_topk, topk, taken, segs, counter, index_list;
+  DevBuf o_all, o_cuts, o_stage, o_edge, o_place;
+  amp_stats stats{};
+};
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) {                                                          \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                 \
+      return e_ == cudaErrorMemoryAllocation ? AMP_E_OOM                              \
+             : (e_ == cudaErrorNoKernelImageForDevice || e_ == cudaErrorInvalidDeviceFunction \
+                    ? AMP_E_NOT_BUILT                                                 \
+                    : AMP_E_CUDA);                                                    \
+    }                                                                                 \
+  } while (0)
+
+namespace {
+
+int fail(amp_ctx* ctx, int code, const std::string& msg) {
+  ctx->err = msg;
+  return code;
+}
+
+template <class T>
+cudaError_t upload(DevBuf& b, const T* src, size_t n) {
+  cudaError_t e = b.ensure(sizeof(T) * n);
+  if (e != cudaSuccess) return e;
+  if (n) e = cudaMemcpy(b.p, src, sizeof(T) * n, cudaMemcpyHostToDevice);
+  return e;
+}
+
+int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
+  if (!p) return fail(ctx, AMP_E_INVALID, "problem is NULL");
+  const int L = p->n_layers, D = p->n_devices;
+  if (L < 1) return fail(ctx, AMP_E_INVALID, "model must have at least one layer");
+  if (L > kMaxLayers)
+    return fail(ctx, AMP_E_UNSUPPORTED, "n_layers > " + std::to_string(kMaxLayers));
+  if (D < 1) return fail(ctx, AMP_E_INVALID, "cluster must have at least one device");
+  if (D > 4096) return fail(ctx, AMP_E_UNSUPPORTED, "n_devices > 4096");
+  if (p->gbs < 1) return fail(ctx, AMP_E_INVALID, "gbs must be >= 1");
+  if (!p->param_count || !p->node_id || !p->bandwidth || (L > 1 && !p->activation_volumes))
+    return fail(ctx, AMP_E_INVALID, "missing model/cluster array");
+  if (p->n_profile_entries < 0 ||
+      (p->n_profile_entries > 0 &&
+       (!p->profile_layer || !p->profile_tmp || !p->profile_mbs || !p->profile_seconds)))
+    return fail(ctx, AMP_E_INVALID, "missing profile arrays");
+  const uint64_t P = cfg ? cfg->placements_per_class : 1;
+  if (P < 1) return fail(ctx, AMP_E_INVALID, "placements_per_class must be >= 1");
+  ctx->L = L;
+  ctx->D = D;
+  ctx->gbs = p->gbs;
+  ctx->P = P;
+  ctx->seed = cfg ? cfg->seed : 0;
+  ctx->device = cfg ? cfg->device : 0;
+  ctx->max_ctas_cfg = cfg ? cfg->max_ctas : 0;
+  ctx->has_ceiling = p->has_max_params_per_device;
+  ctx->ceiling = p->max_params_per_device;
+  ctx->bpp = p->bytes_per_param;
+
+  CK(cudaSetDevice(ctx->device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, ctx->device));
+  if (prop.major != 10)
+    return fail(ctx, AMP_E_NOT_BUILT,
+                "device is sm_" + std::to_string(prop.major * 10 + prop.minor) +
+                    "; this build contains sm_100a kernels only");
+  CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&ctx->ev0));
+  CK(cudaEventCreate(&ctx->ev1));
+  CK(cudaEventCreate(&ctx->ev2));
+
+  // ---- classes: the plan() candidate list (optimizer.cpp:288-293) -------
+  std::map<std::pair<int, int>, int> pair_of;
+  std::vector<int> pair_tmp, pair_mbs;
+  for (int pp : divisors(D))
+    for (int dp : divisors(D / pp)) {
+      const int tmp = D / (pp * dp);
+      if (p->gbs % dp != 0) continue;
+      for (int mbs : divisors(p->gbs / dp)) {
+        auto key = std::make_pair(tmp, mbs);
+        auto it = pair_of.find(key);
+        int pr;
+        if (it == pair_of.end()) {
+          pr = static_cast<int>(pair_tmp.size());
+          pair_of.emplace(key, pr);
+          pair_tmp.push_back(tmp);
+          pair_mbs.push_back(mbs);
+        } else {
+          pr = it->second;
+        }
+        ClassDev c{};
+        c.pp = pp;
+        c.dp = dp;
+        c.tmp = tmp;
+        c.mbs = mbs;
+        c.gas = p->gbs / (dp * mbs);
+        c.pair = pr;
+        ctx->classes.push_back(c);
+        ctx->max_pp = std::max(ctx->max_pp, pp);
+      }
+    }
+  if (ctx->classes.empty()) return fail(ctx, AMP_E_INVALID, "no candidates");
+  const int n_pairs = static_cast<int>(pair_tmp.size());
+
+  // ---- profile cube: ProfileTable map -> dense [pair][layer] -----------
+  std::vector<double> cube((size_t)n_pairs * L, 0.0);
+  std::vector<uint8_t> hit((size_t)n_pairs * L, 0);
+  for (int64_t e = 0; e < p->n_profile_entries; ++e) {  // later entries overwrite
+    const int l = p->profile_layer[e];
+    if (l < 0 || l >= L) continue;
+    auto it = pair_of.find({p->profile_tmp[e], p->profile_mbs[e]});
+    if (it == pair_of.end()) continue;
+    cube[(size_t)it->second * L + l] = p->profile_seconds[e];
+    hit[(size_t)it->second * L + l] = 1;
+  }
+  std::vector<double> flops(L, 0.0);
+  std::vector<uint8_t> flops_ok(L, 0);
+  for (int l = 0; l < L; ++l) {
+    flops_ok[l] = p->flops_present ? p->flops_present[l] : 0;
+    if (flops_ok[l] && p->flops_per_sample) flops[l] = p->flops_per_sample[l];
+  }
+  std::vector<double> act(std::max(1, L - 1), 0.0);
+  for (int l = 0; l + 1 < L; ++l) act[l] = p->activation_volumes[l];
+  std::vector<double> bw((size_t)D * D);
+  for (int i = 0; i < D; ++i)
+    for (int j = 0; j < D; ++j)
+      bw[(size_t)i * D + j] = i == j ? INFINITY : p->bandwidth[(size_t)i * D + j];
+  // heuristic_placement device order (placement.cpp:37-49)
+  std::vector<int> order(D);
+  for (int i = 0; i < D; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    return p->node_id[a] != p->node_id[b] ? p->node_id[a] < p->node_id[b] : a < b;
+  });
+
+  CK(upload(ctx->param, p->param_count, L));
+  CK(upload(ctx->act, act.data(), act.size()));
+  CK(upload(ctx->bw, bw.data(), bw.size()));
+  CK(upload(ctx->base_order, order.data(), order.size()));
+  CK(upload(ctx->cls_d, ctx->classes.data(), ctx->classes.size()));
+
+  // ---- K0: pair tables on the device ----------------------------------
+  const int nv = 1 + L * (L + 1) / 2;
+  int npow2 = 2;
+  while (npow2 < nv) npow2 <<= 1;
+  ctx->npow2 = npow2;
+  ctx->nv_stride = nv;
+  DevBuf d_cube, d_hit, d_flops, d_flops_ok, d_ptmp, d_pmbs;
+  CK(upload(d_cube, cube.data(), cube.size()));
+  CK(upload(d_hit, hit.data(), hit.size()));
+  CK(upload(d_flops, flops.data(), flops.size()));
+  CK(upload(d_flops_ok, flops_ok.data(), flops_ok.size()));
+  CK(upload(d_ptmp, pair_tmp.data(), pair_tmp.size()));
+  CK(upload(d_pmbs, pair_mbs.data(), pair_mbs.size()));
+  CK(ctx->pairs_d.ensure(sizeof(PairDev) * n_pairs));
+  CK(ctx->times.ensure(sizeof(double) * n_pairs * L));
+  CK(ctx->prefix.ensure(sizeof(double) * n_pairs * (L + 1)));
+  CK(ctx->domain.ensure(sizeof(double) * (size_t)n_pairs * nv));
+  CK(ctx->seg.ensure(sizeof(uint16_t) * (size_t)n_pairs * (L + 1) * (L + 1)));
+  TableParams tp{};
+  tp.L = L;
+  tp.n_pairs = n_pairs;
+  tp.npow2 = npow2;
+  tp.fallback_enabled = p->fallback_enabled;
+  tp.pair_tmp = d_ptmp.as<int32_t>();
+  tp.pair_mbs = d_pmbs.as<int32_t>();
+  tp.cube = d_cube.as<double>();
+  tp.cube_hit = d_hit.as<uint8_t>();
+  tp.flops = d_flops.as<double>();
+  tp.flops_ok = d_flops_ok.as<uint8_t>();
+  tp.act = ctx->act.as<double>();
+  tp.device_flops = p->fallback_device_flops;
+  tp.tmp_bandwidth = p->fallback_tmp_bandwidth;
+  tp.pairs = ctx->pairs_d.as<PairDev>();
+  tp.times = ctx->times.as<double>();
+  tp.prefix = ctx->prefix.as<double>();
+  tp.domain = ctx->domain.as<double>();
+  tp.seg = ctx->seg.as<uint16_t>();
+  tp.nv_stride = nv;
+  const size_t k0_smem = sizeof(double) * (npow2 + L + 1);
+  CK(cudaFuncSetAttribute(k_pair_tables, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)k0_smem));
+  k_pair_tables<<<n_pairs, 512, k0_smem, ctx->stream>>>(tp);
+  CK(cudaGetLastError());
+  ctx->pairs.resize(n_pairs);
+  std::vector<uint16_t> seg_h((size_t)n_pairs * (L + 1) * (L + 1));
+  CK(cudaMemcpyAsync(ctx->pairs.data(), ctx->pairs_d.p, sizeof(PairDev) * n_pairs,
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(seg_h.data(), ctx->seg.p, sizeof(uint16_t) * seg_h.size(),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+
+  // ---- per-class work accounting (scheduling + roofline) ---------------
+  ctx->class_inner.assign(ctx->classes.size(), 0.0);
+  ctx->class_lt.assign(ctx->classes.size(), 0.0);
+  ctx->class_cells.assign(ctx->classes.size(), 0.0);
+  size_t bp_stride = 16;
+  for (size_t c = 0; c < ctx->classes.size(); ++c) {
+    const ClassDev& cl = ctx->classes[c];
+    const PairDev& pr = ctx->pairs[cl.pair];
+    if (cl.pp > L || pr.fail_code) continue;
+    const int M = pr.M;
+    ctx->max_M = std::max(ctx->max_M, M);
+    bp_stride = std::max(bp_stride, (size_t)(cl.pp + 1) * (L + 1) * M);
+    double inner = 0, lt = 0;
+    const uint16_t* sg = seg_h.data() + (size_t)cl.pair * (L + 1) * (L + 1);
+    for (int cut = 1; cut < L; ++cut) {
+      const int w = std::min(cl.pp, cut + 1) - 1;  // stages j in [2, min(k, cut+1)]
+      if (w <= 0) continue;
+      for (int i = cut + 1; i <= L; ++i) {
+        inner += (double)w * M;
+        lt += (double)w * sg[cut * (L + 1) + i];
+      }
+    }
+    ctx->class_inner[c] = inner;
+    ctx->class_lt[c] = lt;
+    double cells = (double)L * M;
+    for (int j = 2; j <= cl.pp; ++j) cells += (double)(L - j + 1) * M;
+    ctx->class_cells[c] = cells;
+  }
+  ctx->bp_stride = (bp_stride + 255) & ~size_t(255);
+
+  // ---- evaluate kernel launch shape -------------------------------------
+  const int LP = L + 1;
+  auto smem_for = [&](bool slice) {
+    size_t b = 0;
+    if (slice) b += sizeof(double) * (size_t)LP * ctx->max_M;
+    b += sizeof(double) * ctx->max_M + sizeof(double) * LP + sizeof(double) * L +
+         2 * sizeof(double) * ctx->max_pp + sizeof(int) * (ctx->max_pp + 2) + sizeof(int) * D;
+    b = (b + 15) & ~size_t(15);
+    b += sizeof(uint16_t) * LP * LP;
+    return b;
+  };
+  const size_t smem_limit = 200 * 1024;
+  ctx->slice_in_smem = smem_for(true) <= smem_limit;
+  ctx->smem_bytes = smem_for(ctx->slice_in_smem != 0);
+  if (ctx->smem_bytes > 227 * 1024) return fail(ctx, AMP_E_UNSUPPORTED, "shared memory budget");
+  CK(cudaFuncSetAttribute(k_evaluate, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)ctx->smem_bytes));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_evaluate, kEvalThreads,
+                                                   ctx->smem_bytes));
+  if (occ < 1) return fail(ctx, AMP_E_UNSUPPORTED, "evaluate kernel does not fit on an SM");
+  int n_ctas = occ * prop.multiProcessorCount;
+  ctx->slice_stride = ctx->slice_in_smem ? 0 : (size_t)LP * ctx->max_M;
+  // keep per-CTA scratch (backpointers + global slice) within 16 GiB
+  const size_t per_cta = ctx->bp_stride + sizeof(double) * ctx->slice_stride;
+  const size_t cap = (size_t)16 << 30;
+  if ((size_t)n_ctas * per_cta > cap) n_ctas = std::max<size_t>(1, cap / per_cta);
+  if (ctx->max_ctas_cfg > 0) n_ctas = std::min(n_ctas, ctx->max_ctas_cfg);
+  ctx->n_ctas = n_ctas;
+  CK(ctx->bp.ensure(ctx->bp_stride * n_ctas));
+  if (!ctx->slice_in_smem) CK(ctx->slice.ensure(sizeof(double) * ctx->slice_stride * n_ctas));
+  CK(ctx->counter.ensure(sizeof(unsigned long long)));
+  return AMP_OK;
+}
+
+// Work list: the classes intersecting [begin, end), heaviest first.
+std::vector<Segment> make_segments(const amp_ctx* ctx, uint64_t begin, uint64_t end) {
+  std::vector<std::pair<double, Segment>> v;
+  const uint64_t P = ctx->P;
+  for (uint64_t c = begin / P; c < ctx->classes.size() && c * P < end; ++c) {
+    const uint64_t lo = std::max(begin, c * P), hi = std::min(end, (c + 1) * P);
+    if (hi <= lo) continue;
+    Segment s{};
+    s.first = lo;
+    s.count = hi - lo;
+    s.out = lo - begin;
+    v.emplace_back(ctx->class_inner[c], s);
+  }
+  std::stable_sort(v.begin(), v.end(),
+                   [](const auto& a, const auto& b) { return a.first > b.first; });
+  std::vector<Segment> out;
+  uint64_t off = 0;
+  for (auto& e : v) {
+    e.second.offset = off;
+    off += e.second.count;
+    out.push_back(e.second);
+  }
+  return out;
+}
+
+void account(amp_ctx* ctx, uint64_t begin, uint64_t end, const uint64_t* list, int32_t n) {
+  amp_stats& s = ctx->stats;
+  s.dp_inner = s.dp_inner_lt = s.dp_cells = 0;
+  s.candidates = 0;
+  s.dp_instances = 0;
+  auto add = [&](uint64_t c, double cnt) {
+    s.dp_inner += ctx->class_inner[c] * cnt;
+    s.dp_inner_lt += ctx->class_lt[c] * cnt;
+    s.dp_cells += ctx->class_cells[c] * cnt;
+    if (ctx->class_cells[c] > 0) s.dp_instances += (uint64_t)cnt;
+  };
+  if (list) {
+    for (int32_t i = 0; i < n; ++i) add(list[i] / ctx->P, 1.0);
+    s.candidates = (uint64_t)n;
+  } else {
+    const uint64_t P = ctx->P;
+    for (uint64_t c = begin / P; c < ctx->classes.size() && c * P < end; ++c) {
+      const uint64_t lo = std::max(begin, c * P), hi = std::min(end, (c + 1) * P);
+      if (hi > lo) add(c, (double)(hi - lo));
+    }
+    s.candidates = end - begin;
+  }
+  // FP64 ops the exact recurrence needs: m >= seg: 2 DADD +
+  // 1 DSETP; m < seg: DADD, DMUL, 3 DADD, DSETP.
+  const double ge = s.dp_inner - s.dp_inner_lt;
+  s.fp64_ops = 3.0 * ge + 6.0 * s.dp_inner_lt;
+  s.bytes = 0;
+}
+
+// Launch K1+K2 over either a segment list or an explicit index list.
+int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64_t* d_list,
+                    uint64_t n_work, int32_t k, bool want_all, bool want_details,
+                    bool want_place) {
+  EvalParams ep{};
+  ep.L = ctx->L;
+  ep.D = ctx->D;
+  ep.gbs = ctx->gbs;
+  ep.max_pp = ctx->max_pp;
+  ep.P = ctx->P;
+  ep.seed = ctx->seed;
+  ep.param = ctx->param.as<double>();
+  ep.act = ctx->act.as<double>();
+  ep.bw = ctx->bw.as<double>();
+  ep.base_order = ctx->base_order.as<int32_t>();
+  ep.has_ceiling = ctx->has_ceiling;
+  ep.n_pairs = static_cast<int32_t>(ctx->pairs.size());
+  ep.ceiling = ctx->ceiling;
+  ep.bpp = ctx->bpp;
+  ep.cls = ctx->cls_d.as<ClassDev>();
+  ep.pairs = ctx->pairs_d.as<PairDev>();
+  ep.times = ctx->times.as<double>();
+  ep.prefix = ctx->prefix.as<double>();
+  ep.domain = ctx->domain.as<double>();
+  ep.seg = ctx->seg.as<uint16_t>();
+  ep.nv_stride = ctx->nv_stride;
+  ep.slice_in_smem = ctx->slice_in_smem;
+  if (segs) {
+    CK(upload(ctx->segs, segs->data(), segs->size()));
+    ep.segs = ctx->segs.as<Segment>();
+    ep.n_segs = static_cast<int32_t>(segs->size());
+  }
+  ep.n_work = n_work;
+  ep.index_list = d_list;
+  ep.counter = ctx->counter.as<unsigned long long>();
+  ep.bp = ctx->bp.as<uint8_t>();
+  ep.bp_stride = ctx->bp_stride;
+  ep.slice = ctx->slice.as<double>();
+  ep.slice_stride = ctx->slice_stride;
+  if (want_all) {
+    CK(ctx->o_all.ensure(sizeof(amp_record) * n_work));
+    ep.all = ctx->o_all.as<amp_record>();
+  }
+  if (want_details) {
+    CK(ctx->o_cuts.ensure(sizeof(int32_t) * n_work * (ctx->max_pp + 1)));
+    CK(ctx->o_stage.ensure(sizeof(double) * n_work * ctx->max_pp));
+    CK(ctx->o_edge.ensure(sizeof(double) * n_work * ctx->max_pp));
+    ep.all_cuts = ctx->o_cuts.as<int32_t>();
+    ep.all_stage = ctx->o_stage.as<double>();
+    ep.all_edge = ctx->o_edge.as<double>();
+  }
+  if (want_place) {
+    CK(ctx->o_place.ensure(sizeof(int32_t) * n_work * ctx->D));
+    ep.all_place = ctx->o_place.as<int32_t>();
+  }
+  const int kk = std::max(1, k);
+  CK(ctx->cta_topk.ensure(sizeof(amp_record) * (size_t)kk * ctx->n_ctas));
+  ep.cta_topk = ctx->cta_topk.as<amp_record>();
+  ep.k = kk;
+  ep.max_M = ctx->max_M;
+  CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), ctx->stream));
+  k_evaluate<<<ctx->n_ctas, kEvalThreads, ctx->smem_bytes, ctx->stream>>>(ep);
+  CK(cudaGetLastError());
+  return AMP_OK;
+}
+
+int launch_merge(amp_ctx* ctx, const amp_record* d_in, int n_in, int k, amp_record* d_out,
+                 cudaStream_t st) {
+  CK(ctx->taken.ensure((size_t)n_in + 16));
+  k_merge_topk<<<1, 1024, 0, st>>>(d_in, n_in, k, d_out, ctx->taken.as<unsigned char>());
+  CK(cudaGetLastError());
+  return AMP_OK;
+}
+
+int copy_details(amp_ctx* ctx, uint64_t n, const amp_details* det) {
+  if (!det) return AMP_OK;
+  if (det->cuts)
+    CK(cudaMemcpyAsync(det->cuts, ctx->o_cuts.p, sizeof(int32_t) * n * (ctx->max_pp + 1),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  if (det->stage_times)
+    CK(cudaMemcpyAsync(det->stage_times, ctx->o_stage.p, sizeof(double) * n * ctx->max_pp,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  if (det->edge_times)
+    CK(cudaMemcpyAsync(det->edge_times, ctx->o_edge.p, sizeof(double) * n * ctx->max_pp,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  if (det->placement)
+    CK(cudaMemcpyAsync(det->placement, ctx->o_place.p, sizeof(int32_t) * n * ctx->D,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  return AMP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int amp_search_abi_version(void) { return AMP_SEARCH_ABI_VERSION; }
+
+const char* amp_last_error(void) { return g_last_error.c_str(); }
+
+int amp_search_create(amp_ctx** out, const amp_problem* problem,
+                      const amp_search_config* config) {
+  if (!out) {
+    g_last_error = "out is NULL";
+    return AMP_E_INVALID;
+  }
+  *out = nullptr;
+  amp_ctx* ctx = new amp_ctx();
+  const int rc = setup(ctx, problem, config);
+  if (rc != AMP_OK) {
+    g_last_error = ctx->err;
+    amp_search_destroy(ctx);
+    return rc;
+  }
+  *out = ctx;
+  return AMP_OK;
+}
+
+void amp_search_destroy(amp_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->ev2) cudaEventDestroy(ctx->ev2);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* amp_search_last_error(const amp_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_last_error.c_str();
+}
+
+uint64_t amp_search_num_candidates(const amp_ctx* ctx) {
+  return ctx ? (uint64_t)ctx->classes.size() * ctx->P : 0;
+}
+
+int32_t amp_search_num_classes(const amp_ctx* ctx) {
+  return ctx ? static_cast<int32_t>(ctx->classes.size()) : 0;
+}
+
+int32_t amp_search_max_pp(const amp_ctx* ctx) { return ctx ? ctx->max_pp : 0; }
+
+int amp_search_class(const amp_ctx* ctx, int32_t c, int32_t* pp, int32_t* dp, int32_t* tmp,
+                     int32_t* mbs) {
+  if (!ctx || c < 0 || c >= (int32_t)ctx->classes.size()) return AMP_E_INVALID;
+  const ClassDev& cl = ctx->classes[c];
+  if (pp) *pp = cl.pp;
+  if (dp) *dp = cl.dp;
+  if (tmp) *tmp = cl.tmp;
+  if (mbs) *mbs = cl.mbs;
+  return AMP_OK;
+}
+
+int amp_search_partition(const amp_ctx* ctx, int32_t n_parts, uint64_t* bounds) {
+  if (!ctx || n_parts < 1 || !bounds) return AMP_E_INVALID;
+  const uint64_t P = ctx->P, N = (uint64_t)ctx->classes.size() * P;
+  // per-candidate weight: DP inner iterations + a constant for the
+  // placement/estimate work of every candidate
+  std::vector<double> w(ctx->classes.size());
+  double total = 0;
+  for (size_t c = 0; c < w.size(); ++c) {
+    w[c] = ctx->class_inner[c] + 64.0 * ctx->D;
+    total += w[c] * (double)P;
+  }
+  bounds[0] = 0;
+  size_t c = 0;
+  double acc = 0;  // cumulative weight before class c
+  for (int32_t part = 1; part < n_parts; ++part) {
+    const double target = total * part / n_parts;
+    while (c < w.size() && acc + w[c] * (double)P < target) {
+      acc += w[c] * (double)P;
+      ++c;
+    }
+    uint64_t b = N;
+    if (c < w.size()) {
+      const double within = (target - acc) / w[c];
+      uint64_t off = (uint64_t)std::llround(within);
+      if (off > P) off = P;
+      b = (uint64_t)c * P + off;
+    }
+    bounds[part] = std::max(b, bounds[part - 1]);
+  }
+  bounds[n_parts] = N;
+  return AMP_OK;
+}
+
+int amp_search_run(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k, amp_record* topk,
+                   int32_t* n_topk, amp_record* all, const amp_details* all_details) {
+  if (!ctx) return AMP_E_INVALID;
+  const uint64_t N = amp_search_num_candidates(ctx);
+  if (begin > end || end > N) return fail(ctx, AMP_E_INVALID, "range outside [0, num_candidates)");
+  if (k < 0 || k > 4096) return fail(ctx, AMP_E_INVALID, "k must be in [0, 4096]");
+  if (k > 0 && !topk) return fail(ctx, AMP_E_INVALID, "topk is NULL");
+  CK(cudaSetDevice(ctx->device));
+  const uint64_t n = end - begin;
+  if (n_topk) *n_topk = 0;
+  if (n == 0) return AMP_OK;
+  const auto segs = make_segments(ctx, begin, end);
+  const bool det = all_details && (all_details->cuts || all_details->stage_times ||
+                                   all_details->edge_times);
+  CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  int rc = launch_evaluate(ctx, &segs, nullptr, n, k, all != nullptr, det,
+                           all_details && all_details->placement);
+  if (rc) return rc;
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  const int kk = std::max(1, k);
+  CK(ctx->topk.ensure(sizeof(amp_record) * kk));
+  rc = launch_merge(ctx, ctx->cta_topk.as<amp_record>(), kk * ctx->n_ctas, kk,
+                    ctx->topk.as<amp_record>(), ctx->stream);
+  if (rc) return rc;
+  CK(cudaEventRecord(ctx->ev2, ctx->stream));
+  std::vector<amp_record> tk(kk);
+  CK(cudaMemcpyAsync(tk.data(), ctx->topk.p, sizeof(amp_record) * kk, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  if (all)
+    CK(cudaMemcpyAsync(all, ctx->o_all.p, sizeof(amp_record) * n, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  rc = copy_details(ctx, n, all_details);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  int cnt = 0;
+  for (int i = 0; i < k; ++i)
+    if (tk[i].fail_code >= 0) topk[cnt++] = tk[i];
+  if (n_topk) *n_topk = cnt;
+  float ms1 = 0, ms2 = 0;
+  cudaEventElapsedTime(&ms1, ctx->ev0, ctx->ev1);
+  cudaEventElapsedTime(&ms2, ctx->ev0, ctx->ev2);
+  account(ctx, begin, end, nullptr, 0);
+  ctx->stats.kernel_ms = ms1;
+  ctx->stats.total_ms = ms2;
+  ctx->stats.launches = 2;
+  ctx->stats.ctas = ctx->n_ctas;
+  return AMP_OK;
+}
+
+int amp_search_evaluate(amp_ctx* ctx, const uint64_t* indices, int32_t n, amp_record* out,
+                        const amp_details* details) {
+  if (!ctx || n < 0 || (n > 0 && (!indices || !out))) return AMP_E_INVALID;
+  if (n == 0) return AMP_OK;
+  const uint64_t N = amp_search_num_candidates(ctx);
+  for (int32_t i = 0; i < n; ++i)
+    if (indices[i] >= N) return fail(ctx, AMP_E_INVALID, "index outside [0, num_candidates)");
+  CK(cudaSetDevice(ctx->device));
+  CK(upload(ctx->index_list, indices, (size_t)n));
+  const bool det = details && (details->cuts || details->stage_times || details->edge_times);
+  CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  int rc = launch_evaluate(ctx, nullptr, ctx->index_list.as<uint64_t>(), (uint64_t)n, 1, true,
+                           det, details && details->placement);
+  if (rc) return rc;
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  CK(cudaMemcpyAsync(out, ctx->o_all.p, sizeof(amp_record) * n, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  rc = copy_details(ctx, (uint64_t)n, details);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  account(ctx, 0, 0, indices, n);
+  ctx->stats.kernel_ms = ms;
+  ctx->stats.total_ms = ms;
+  ctx->stats.launches = 1;
+  ctx->stats.ctas = ctx->n_ctas;
+  return AMP_OK;
+}
+
+int amp_search_run_device(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k,
+                          amp_record* d_topk, void* stream) {
+  if (!ctx || k < 1 || k > 4096 || !d_topk) return AMP_E_INVALID;
+  const uint64_t N = amp_search_num_candidates(ctx);
+  if (begin > end || end > N) return fail(ctx, AMP_E_INVALID, "range outside [0, num_candidates)");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
+  // order the context stream after the caller's stream
+  CK(cudaEventRecord(ctx->ev0, user));
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev0, 0));
+  const auto segs = make_segments(ctx, begin, end);
+  int rc = AMP_OK;
+  if (end > begin) {
+    rc = launch_evaluate(ctx, &segs, nullptr, end - begin, k, false, false, false);
+    if (rc) return rc;
+  } else {
+    // nothing to evaluate: pad the CTA lists
+    std::vector<amp_record> pad((size_t)k * ctx->n_ctas);
+    for (auto& e : pad) {
+      std::memset(&e, 0, sizeof(e));
+      e.index = ~0ull;
+      e.fail_code = -1;
+      e.total = e.pipeline_time = e.dpsync_time = NAN;
+    }
+    CK(ctx->cta_topk.ensure(sizeof(amp_record) * pad.size()));
+    CK(cudaMemcpyAsync(ctx->cta_topk.p, pad.data(), sizeof(amp_record) * pad.size(),
+                       cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  rc = launch_merge(ctx, ctx->cta_topk.as<amp_record>(), k * ctx->n_ctas, k, d_topk, ctx->stream);
+  if (rc) return rc;
+  CK(cudaEventRecord(ctx->ev2, ctx->stream));
+  CK(cudaStreamWaitEvent(user, ctx->ev2, 0));
+  account(ctx, begin, end, nullptr, 0);
+  ctx->stats.launches = end > begin ? 2 : 1;
+  ctx->stats.ctas = ctx->n_ctas;
+  ctx->stats.kernel_ms = -1;  // resolved by amp_search_last_stats
+  ctx->stats.total_ms = -1;
+  return AMP_OK;
+}
+
+int amp_search_merge_topk_device(amp_ctx* ctx, const amp_record* d_in, int32_t n_in, int32_t k,
+                                 amp_record* d_out, void* stream) {
+  if (!ctx || !d_in || !d_out || n_in < 1 || k < 1 || k > 4096) return AMP_E_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  return launch_merge(ctx, d_in, n_in, k, d_out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int amp_search_last_stats(const amp_ctx* ctx_c, amp_stats* out) {
+  amp_ctx* ctx = const_cast<amp_ctx*>(ctx_c);
+  if (!ctx || !out) return AMP_E_INVALID;
+  if (ctx->stats.kernel_ms < 0) {  // device run: resolve the events now
+    CK(cudaEventSynchronize(ctx->ev2));
+    float ms1 = 0, ms2 = 0;
+    cudaEventElapsedTime(&ms1, ctx->ev0, ctx->ev1);
+    cudaEventElapsedTime(&ms2, ctx->ev0, ctx->ev2);
+    ctx->stats.kernel_ms = ms1;
+    ctx->stats.total_ms = ms2;
+  }
+  *out = ctx->stats;
+  return AMP_OK;
+}
+
+int amp_dp_solve_batch(int32_t device, const amp_dp_instance* inst, int32_t n, int32_t* cuts_out,
+                       int32_t cut_stride, double* cost_out, int32_t* status_out) {
+  amp_ctx tmp_ctx;  // error sink
+  amp_ctx* ctx = &tmp_ctx;
+  auto bail = [&](int rc) {
+    g_last_error = ctx->err;
+    return rc;
+  };
+  if (n < 0 || (n > 0 && (!inst || !cuts_out || !cost_out))) {
+    ctx->err = "invalid arguments";
+    return bail(AMP_E_INVALID);
+  }
+  if (n == 0) return AMP_OK;
+  int max_L = 1, max_k = 1;
+  std::vector<DpBatchItem> items(n);
+  size_t tot_times = 0, tot_edges = 0;
+  for (int i = 0; i < n; ++i) {
+    const auto& it = inst[i];
+    int status = 0;
+    if (it.n_layers < 1 || it.n_layers > kMaxLayers || it.stages < 1 || it.stages > it.n_layers ||
+        it.gas < 1 || !it.layer_times || (it.stages > 1 && !it.edge_costs))
+      status = 1;
+    if (it.stages + 1 > cut_stride) status = 1;
+    items[i] = DpBatchItem{it.n_layers, it.stages, it.gas, status, nullptr, nullptr};
+    if (status_out) status_out[i] = status;
+    if (status) continue;
+    max_L = std::max(max_L, it.n_layers);
+    max_k = std::max(max_k, it.stages);
+    tot_times += it.n_layers;
+    tot_edges += (size_t)std::max(0, it.stages - 1) * it.n_layers;
+  }
+  int rcs = cudaSetDevice(device);
+  if (rcs != cudaSuccess) {
+    ctx->err = cudaGetErrorString((cudaError_t)rcs);
+    return bail(AMP_E_CUDA);
+  }
+  std::vector<double> times(tot_times + 1), edges(tot_edges + 1);
+  std::vector<size_t> toff(n), eoff(n);
+  size_t ta = 0, ea = 0;
+  for (int i = 0; i < n; ++i) {
+    if (items[i].status) continue;
+    toff[i] = ta;
+    eoff[i] = ea;
+    std::memcpy(&times[ta], inst[i].layer_times, sizeof(double) * inst[i].n_layers);
+    ta += inst[i].n_layers;
+    const size_t ne = (size_t)std::max(0, inst[i].stages - 1) * inst[i].n_layers;
+    if (ne) std::memcpy(&edges[ea], inst[i].edge_costs, sizeof(double) * ne);
+    ea += ne;
+  }
+  DevBuf d_times, d_edges, d_items, d_cuts, d_cost, d_bp, d_slice, d_dom, d_seg;
+  int rc;
+#define CKB(call)                                                    \
+  do {                                                               \
+    cudaError_t e_ = (call);                                         \
+    if (e_ != cudaSuccess) {                                         \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_); \
+      return bail(e_ == cudaErrorMemoryAllocation ? AMP_E_OOM : AMP_E_CUDA); \
+    }                                                                \
+  } while (0)
+  CKB(upload(d_times, times.data(), times.size()));
+  CKB(upload(d_edges, edges.data(), edges.size()));
+  for (int i = 0; i < n; ++i) {
+    if (items[i].status) continue;
+    items[i].times = d_times.as<double>() + toff[i];
+    items[i].edges = d_edges.as<double>() + eoff[i];
+  }
+  CKB(upload(d_items, items.data(), items.size()));
+  CKB(d_cuts.ensure(sizeof(int32_t) * (size_t)n * cut_stride));
+  CKB(d_cost.ensure(sizeof(double) * n));
+  const int nv = 1 + max_L * (max_L + 1) / 2;
+  int npow2 = 2;
+  while (npow2 < nv) npow2 <<= 1;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const int grid = std::min(n, sms * 2);
+  const size_t bp_stride = ((size_t)(max_k + 1) * (max_L + 1) * nv + 255) & ~size_t(255);
+  const size_t slice_stride = (size_t)(max_L + 1) * nv;
+  CKB(d_bp.ensure(bp_stride * grid));
+  CKB(d_slice.ensure(sizeof(double) * slice_stride * grid));
+  CKB(d_dom.ensure(sizeof(double) * (size_t)npow2 * grid));
+  CKB(d_seg.ensure(sizeof(uint16_t) * (size_t)(max_L + 1) * (max_L + 1) * grid));
+  DpBatchParams bpp{};
+  bpp.items = d_items.as<DpBatchItem>();
+  bpp.n = n;
+  bpp.max_L = max_L;
+  bpp.max_k = max_k;
+  bpp.npow2 = npow2;
+  bpp.cut_stride = cut_stride;
+  bpp.cuts_out = d_cuts.as<int32_t>();
+  bpp.cost_out = d_cost.as<double>();
+  bpp.bp = d_bp.as<uint8_t>();
+  bpp.bp_stride = bp_stride;
+  bpp.slice = d_slice.as<double>();
+  bpp.slice_stride = slice_stride;
+  bpp.domain = d_dom.as<double>();
+  bpp.seg = d_seg.as<uint16_t>();
+  const size_t smem = sizeof(double) * (npow2 + 2 * (max_L + 1)) + sizeof(int) * (max_k + 2);
+  CKB(cudaFuncSetAttribute(k_dp_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_dp_batch<<<grid, 256, smem>>>(bpp);
+  CKB(cudaGetLastError());
+  std::vector<int32_t> cuts((size_t)n * cut_stride);
+  CKB(cudaMemcpy(cuts.data(), d_cuts.p, sizeof(int32_t) * cuts.size(), cudaMemcpyDeviceToHost));
+  CKB(cudaMemcpy(cost_out, d_cost.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n; ++i) {
+    if (items[i].status) {
+      cost_out[i] = NAN;
+      for (int q = 0; q < cut_stride; ++q) cuts_out[(size_t)i * cut_stride + q] = -1;
+      continue;
+    }
+    for (int q = 0; q < cut_stride; ++q)
+      cuts_out[(size_t)i * cut_stride + q] =
+          q <= items[i].stages ? cuts[(size_t)i * cut_stride + q] : -1;
+  }
+  (void)rc;
+#undef CKB
+  return AMP_OK;
+}
+
+int amp_fp64_peak(int32_t device, double* dadd_per_s, double* ms_out) {
+  if (cudaSetDevice(device) != cudaSuccess) return AMP_E_CUDA;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double* d = nullptr;
+  if (cudaMalloc(&d, 8) != cudaSuccess) return AMP_E_OOM;
+  const int grid = sms * 8, threads = 256, iters = 4096;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  k_dadd_peak<<<grid, threads>>>(d, 64, 1e-300);  // warm-up
+  cudaEventRecord(a);
+  k_dadd_peak<<<grid, threads>>>(d, iters, 1e-300);
+  cudaEventRecord(b);
+  cudaError_t e = cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(d);
+  if (e != cudaSuccess) {
+    g_last_error = cudaGetErrorString(e);
+    return AMP_E_CUDA;
+  }
+  const double ops = (double)grid * threads * iters * 16 * 8;
+  if (dadd_per_s) *dadd_per_s = ops / (ms * 1e-3);
+  if (ms_out) *ms_out = ms;
+  return AMP_OK;
+}
+
+}  // extern "C"
