@@ -105,11 +105,18 @@ typedef struct amp_problem {
  * With P == 1 the space is exactly the reference plan() space and index
  * order equals the reference ranking tie-break key (pp, dp, tmp, mbs).
  */
+/* amp_search_config.flags */
+/* Evaluate the reference's full tolerance-indexed DP table instead of only
+ * the cells the result depends on (same results; for comparison).          */
+#define AMP_FLAG_DENSE_DP 1
+
 typedef struct amp_search_config {
   uint64_t placements_per_class; /* P >= 1                                 */
   uint64_t seed;                 /* shuffle seed                            */
   int32_t device;                /* CUDA device ordinal                     */
   int32_t max_ctas;              /* 0 = auto (resident CTAs on all SMs)     */
+  int32_t flags;                 /* AMP_FLAG_*                              */
+  int32_t reserved;
 } amp_search_config;
 
 /* One evaluated candidate: CandidateRecord minus the vectors

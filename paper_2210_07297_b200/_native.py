@@ -64,7 +64,12 @@ class AmpSearchConfig(C.Structure):
         ("seed", C.c_uint64),
         ("device", C.c_int32),
         ("max_ctas", C.c_int32),
+        ("flags", C.c_int32),
+        ("reserved", C.c_int32),
     ]
+
+
+AMP_FLAG_DENSE_DP = 1
 
 
 class AmpRecord(C.Structure):

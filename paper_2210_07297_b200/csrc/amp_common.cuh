@@ -23,14 +23,14 @@ namespace amp {
 
 constexpr int kMaxLayers = 180;        // (L(L+1)/2 + 1) <= 16384 for the smem sort
 constexpr int kSortCap = 16384;        // padded domain capacity (pow2)
-constexpr int kEvalThreads = 256;      // evaluate kernel block size
+constexpr int kEvalThreads = 384;      // evaluate kernel max block size
 
 struct PairDev {
   int32_t tmp, mbs;
   int32_t M;            // tolerance domain size
   int32_t fail_code;    // AMP_FAIL_PROFILE_MISS / _ALLREDUCE_BANDWIDTH / 0
   int32_t fail_layer;   // first failing layer (segment_times order)
-  int32_t pad;
+  int32_t monotone;     // all layer times >= 0 (DP split-loop fast path)
   double fail_value;
 };
 
@@ -48,6 +48,9 @@ struct Segment {
   uint64_t offset;  // exclusive prefix of counts in dispatch order
   uint64_t out;     // position of `first` in the caller's output order
 };
+
+struct WEnt;     // per-stage cut table entry (amp_kernels.cuh)
+struct ProgDev;  // pruned-DP program (amp_dp_sparse.cuh)
 
 struct EvalParams {
   // problem
@@ -70,6 +73,8 @@ struct EvalParams {
   const uint16_t* seg;
   int32_t nv_stride;        // domain stride per pair
   int32_t slice_in_smem;    // 1: DP stage slice in shared memory
+  int32_t w_in_smem;        // 1: per-stage cut table in shared memory
+  int32_t pad1;
   // work list
   const Segment* segs;
   int32_t n_segs;
@@ -81,6 +86,7 @@ struct EvalParams {
   uint8_t* bp;              // backpointers, bp_stride bytes per CTA
   uint64_t bp_stride;
   double* slice;            // global stage slice when !slice_in_smem
+  WEnt* wtab;               // global cut tables when !w_in_smem
   uint64_t slice_stride;    // doubles per CTA
   int32_t* place;           // placement, D per CTA
   // outputs
@@ -92,7 +98,24 @@ struct EvalParams {
   amp_record* cta_topk;     // [gridDim.x * k]
   int32_t k;
   int32_t max_M;
+  // pruned DP (amp_dp_sparse.cuh)
+  const ProgDev* progs;
+  const int32_t* class_prog;  // [n_cls] program of each class
+  const uint32_t* cells;
+  const uint32_t* cellpred;
+  const uint16_t* preds;
+  const uint32_t* stage;
+  double* vbuf;               // global value arrays when not in smem
+  int32_t max_cells;          // max_j |N_j| over programs
+  int32_t max_prog_cells;     // max sum_j |N_j| over programs
 };
+
+// std::min(a, b) with the reference's argument order: (b < a) ? b : a.
+__device__ __forceinline__ double std_min(double a, double b) { return b < a ? b : a; }
+// std::max(a, b): (a < b) ? b : a.
+__device__ __forceinline__ double std_max(double a, double b) { return a < b ? b : a; }
+// std::max(0.0, x)
+__device__ __forceinline__ double max0(double x) { return 0.0 < x ? x : 0.0; }
 
 // splitmix64; integer-only, identical on host.
 __host__ __device__ inline uint64_t splitmix64(uint64_t x) {

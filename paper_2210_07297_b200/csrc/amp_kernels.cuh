@@ -20,15 +20,10 @@
 #include <math_constants.h>
 
 #include "amp_common.cuh"
+#include "amp_dp_sparse.cuh"
 
 namespace amp {
 
-// std::min(a, b) with the reference's argument order: (b < a) ? b : a.
-__device__ __forceinline__ double std_min(double a, double b) { return b < a ? b : a; }
-// std::max(a, b): (a < b) ? b : a.
-__device__ __forceinline__ double std_max(double a, double b) { return a < b ? b : a; }
-// std::max(0.0, x)
-__device__ __forceinline__ double max0(double x) { return 0.0 < x ? x : 0.0; }
 
 // ---------------------------------------------------------------------------
 // block helpers
@@ -209,54 +204,146 @@ __device__ int build_domain(const double* Pf, int L, double* vals, int npow2, do
 // ---------------------------------------------------------------------------
 //
 // Stage slice C[i][m] (i in [0, L], m in [0, M)) lives in shared memory (or
-// in a per-CTA global buffer for large M).  Stage j is computed in place,
-// rows i descending: row i at stage j reads only rows cut < i at stage j-1,
-// which have not been overwritten yet; one barrier per row orders the
-// overwrite.  Threads own domain columns m; the cut loop runs ascending with
-// a strict '<', so the smallest cut wins ties exactly like the reference.
+// in a per-CTA global buffer for large M).  Each thread OWNS domain columns
+// m and computes stage j of its column in place, rows i descending: row i at
+// stage j reads rows cut < i of stage j-1 which, in the thread's own column,
+// have not been overwritten yet.  The only cross-column read of the
+// recurrence is cost[cut][j-1][max(seg(cut,i), m)] when m < seg(cut,i); that
+// value, U(cut,i) = C[cut][seg(cut,i)], is uniform over m and is gathered
+// once per stage into the table W[i][cut] = {t2, edge, U} together with the
+// segment time t2 = prefix[i] - prefix[cut] and the stage's edge cost.  So a
+// stage needs two barriers (table build, column sweep) instead of one per
+// row, and the inner loop reads one uniform 32-byte entry plus (on the
+// m >= seg branch) one own-column double.
+//
+// With non-negative layer times seg(cut, i) is non-increasing in cut, so for
+// each (i, m) the cut range [j-1, i) splits at c* into an "m < seg" prefix
+// (U branch) and an "m >= seg" suffix (own-column branch); c* is walked down
+// incrementally as i decreases.  The two loops run in ascending cut order
+// with a strict '<', so the smallest cut wins ties exactly like the
+// reference (pipeline_dp.cpp:118-127).  Exactness of the branch forms:
+//   m <  seg: t2 - dom[m] > 0, so max(0, .) = t2 - dom[m];
+//   m >= seg: t2 - dom[m] <= 0, so (gas-1)*max(0, .) = +0.0 and
+//             sub + 0.0 == sub (sub is never -0.0, t2 never -0.0).
 // Backpointers (one byte per (j, i, m)) go to global scratch; thread 0
 // backtracks from (L, k, m = 0).
+struct __align__(16) WEnt {
+  double t2;  // prefix[i] - prefix[cut]
+  double e;   // edge cost at `cut` for the current stage boundary
+  double u;   // C_{j-1}[cut][seg(cut, i)]
+  double pad;
+};
+
+// Lexicographic (value, cut) argmin accumulator.  Several accumulators,
+// each fed its cuts in ascending order, combined with comb(), equal the
+// reference's single sequential strict-'<' scan (first cut attaining the
+// minimum; NaN never selected); they break the DSETP->FSEL dependency chain.
+struct ArgMin {
+  double v;
+  int c;
+};
+__device__ __forceinline__ void upd(ArgMin& a, double g, int c) {
+  if (g < a.v) {
+    a.v = g;
+    a.c = c;
+  }
+}
+__device__ __forceinline__ ArgMin comb(const ArgMin& a, const ArgMin& b) {
+  return (b.v < a.v || (b.v == a.v && b.c < a.c)) ? b : a;
+}
+
 template <class EdgeFn>
 __device__ double dp_solve(const int L, const int k, const int gas, const int M,
                            const double* __restrict__ Pf, const double* __restrict__ Dm,
                            const uint16_t* __restrict__ seg, const EdgeFn& edge, double* C,
-                           double* E, uint8_t* __restrict__ bp, int* cuts) {
+                           WEnt* W, double* E, const bool monotone, uint8_t* __restrict__ bp,
+                           int* cuts) {
   const double g1 = (double)(gas - 1);
   const int tid = threadIdx.x, nt = blockDim.x;
   const int LP = L + 1;
   // base case j = 1 (102-107): t1 = between(0, i) = prefix[i] - prefix[0]
-  for (int x = tid; x < L * M; x += nt) {
-    const int i = 1 + x / M, m = x - (i - 1) * M;
-    const double t1 = Pf[i] - Pf[0];
-    C[(size_t)i * M + m] = g1 * max0(t1 - Dm[m]) + t1;
-  }
-  __syncthreads();
-  for (int j = 2; j <= k; ++j) {
-    for (int cut = j - 1 + tid; cut < L; cut += nt) E[cut] = edge(cut, j - 2);
-    __syncthreads();
-    uint8_t* bpj = bp + (size_t)j * LP * M;
-    for (int i = L; i >= j; --i) {
-      const double Pi = Pf[i];
-      for (int m = tid; m < M; m += nt) {
-        const double dm = Dm[m];
-        double best = CUDART_INF;
-        int bc = -1;
-        for (int cut = j - 1; cut < i; ++cut) {
-          const double t2 = Pi - Pf[cut];
-          const int s = seg[cut * LP + i];
-          const double sub = C[(size_t)cut * M + (s > m ? s : m)];
-          const double g = ((sub + g1 * max0(t2 - dm)) + t2) + E[cut];
-          if (g < best) {
-            best = g;
-            bc = cut;
-          }
-        }
-        C[(size_t)i * M + m] = best;
-        bpj[(size_t)i * M + m] = (uint8_t)bc;
-      }
-      __syncthreads();
+  for (int m = tid; m < M; m += nt) {
+    const double dm = Dm[m];
+    double* col = C + m;
+    for (int i = 1; i <= L; ++i) {
+      const double t1 = Pf[i] - Pf[0];
+      col[i * M] = g1 * max0(t1 - dm) + t1;
     }
   }
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  for (int j = 2; j <= k; ++j) {
+    // ---- per-stage uniform table W[i][cut], cut in [j-1, L), i in (cut, L]
+    const int c0 = j - 1;
+    for (int c = c0 + tid; c < L; c += nt) E[c] = edge(c, j - 2);
+    __syncthreads();  // E ready; previous stage's columns complete
+    for (int i = j + warp; i <= L; i += nwarp) {  // one warp per row
+      const double Pi = Pf[i];
+      for (int c = c0 + lane; c < i; c += 32) {
+        WEnt w;
+        w.t2 = Pi - Pf[c];
+        w.e = E[c];
+        w.u = C[c * M + seg[c * LP + i]];
+        w.pad = 0.0;
+        W[i * L + c] = w;
+      }
+    }
+    __syncthreads();
+    uint8_t* bpj = bp + (size_t)j * LP * M;
+    for (int m = tid; m < M; m += nt) {
+      const double dm = Dm[m];
+      const double* Cm = C + m;
+      double* Crow = C + L * M + m;           // C[i][m], i = L, L-1, ...
+      uint8_t* brow = bpj + L * M + m;
+      const WEnt* Wi = W + L * L;             // row i of the cut table
+      const uint16_t* segi = seg + L;         // &seg[0 * LP + i]
+      int cs = L;  // c*: first cut of the m >= seg suffix (non-increasing in i)
+      for (int i = L; i >= j; --i, Crow -= M, brow -= M, Wi -= L, --segi) {
+        double best = CUDART_INF;
+        int bc = -1;
+        if (monotone) {
+          if (cs > i) cs = i;
+          while (cs > c0 && (int)segi[(cs - 1) * LP] <= m) --cs;
+          const WEnt* w = Wi + c0;
+          const WEnt* wu = Wi + cs;
+          int c = c0;
+#pragma unroll 2
+          for (; w < wu; ++w, ++c) {  // m < seg(c, i): U branch
+            const double4 x = *reinterpret_cast<const double4*>(w);  // t2, e, u
+            const double g = ((x.z + g1 * (x.x - dm)) + x.x) + x.y;
+            if (g < best) {
+              best = g;
+              bc = c;
+            }
+          }
+          const WEnt* we = Wi + i;
+          const double* cp = Cm + c * M;
+#pragma unroll 2
+          for (; w < we; ++w, ++c, cp += M) {  // m >= seg(c, i): own column
+            const double2 te = *reinterpret_cast<const double2*>(w);
+            const double g = (*cp + te.x) + te.y;
+            if (g < best) {
+              best = g;
+              bc = c;
+            }
+          }
+        } else {  // general order (negative layer times): test per cut
+          for (int c = c0; c < i; ++c) {
+            const WEnt w = Wi[c];
+            const int s = segi[c * LP];
+            const double sub = s > m ? w.u : Cm[c * M];
+            const double g = ((sub + g1 * max0(w.t2 - dm)) + w.t2) + w.e;
+            if (g < best) {
+              best = g;
+              bc = c;
+            }
+          }
+        }
+        *Crow = best;
+        *brow = (uint8_t)bc;
+      }
+    }
+  }
+  __syncthreads();
   double cost = 0.0;
   if (tid == 0) {
     cost = C[(size_t)L * M + 0];
@@ -338,7 +425,7 @@ __global__ void k_pair_tables(TableParams p) {
     d.M = 0;
     d.fail_code = fail == 0x7fffffff ? 0 : (fail & 7);
     d.fail_layer = fail == 0x7fffffff ? -1 : (fail >> 3);
-    d.pad = 0;
+    d.monotone = 1;
     d.fail_value = d.fail_code == AMP_FAIL_ALLREDUCE_BANDWIDTH ? p.tmp_bandwidth : 0.0;
     p.pairs[pr] = d;
   }
@@ -348,10 +435,13 @@ __global__ void k_pair_tables(TableParams p) {
   if (tid == 0) {
     double s = 0.0;
     Pf[0] = 0.0;
+    int mono = 1;  // non-negative layer times: seg(cut, i) monotone in cut
     for (int l = 0; l < L; ++l) {
+      if (!(times[l] >= 0.0)) mono = 0;
       s = s + times[l];
       Pf[l + 1] = s;
     }
+    p.pairs[pr].monotone = mono;
   }
   __syncthreads();
   for (int x = tid; x <= L; x += blockDim.x) p.prefix[(size_t)pr * (L + 1) + x] = Pf[x];
@@ -393,28 +483,63 @@ __device__ void topk_insert(amp_record* list, int& n, int k, const amp_record& r
   if (n < k) ++n;
 }
 
-__global__ void __launch_bounds__(kEvalThreads) k_evaluate(EvalParams p) {
+// MODE selects the DP implementation and where its working set lives
+// (compile-time so the compiler emits LDS/STS instead of generic loads):
+//   kDenseSS/SG/GS/GG  full tolerance-indexed table; stage slice / cut table
+//                      in (S)hared or (G)lobal memory
+//   kSparseS/G         pruned program (amp_dp_sparse.cuh); value arrays and
+//                      backpointers in shared / global memory
+enum : int { kDenseSS = 0, kDenseSG = 1, kDenseGS = 2, kDenseGG = 3, kSparseS = 4, kSparseG = 5 };
+
+template <int MODE>
+__global__ void __launch_bounds__(MODE >= kSparseS ? 256 : kEvalThreads, MODE >= kSparseS ? 4 : 2)
+    k_evaluate(EvalParams p) {
+  constexpr bool SPARSE = MODE >= kSparseS;
+  constexpr bool SLICE_SMEM = MODE == kDenseSS || MODE == kDenseSG;
+  constexpr bool W_SMEM = MODE == kDenseSS || MODE == kDenseGS;
+  constexpr bool V_SMEM = MODE == kSparseS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ EvalShared sh;
   __shared__ double red[32];
   __shared__ int redi[64];
   const int L = p.L, D = p.D, LP = L + 1, tid = threadIdx.x, nt = blockDim.x;
   const int maxM = p.max_M, maxpp = p.max_pp;
-  // dynamic smem carve-up
+  // dynamic smem carve-up (host mirror: eval_smem_bytes in amp_search.cu)
   unsigned char* sp = smem_raw;
   double* C = nullptr;
-  if (p.slice_in_smem) {
-    C = reinterpret_cast<double*>(sp);
-    sp += sizeof(double) * (size_t)LP * maxM;
+  WEnt* W = nullptr;
+  double *V0 = nullptr, *V1 = nullptr;
+  uint8_t* bp = p.bp + (size_t)blockIdx.x * p.bp_stride;
+  if (SPARSE) {
+    if (V_SMEM) {
+      V0 = reinterpret_cast<double*>(sp);
+      sp += sizeof(double) * 2 * (size_t)p.max_cells;
+      bp = reinterpret_cast<uint8_t*>(sp);
+      sp += (p.max_prog_cells + 15) & ~15;
+    } else {
+      V0 = p.vbuf + (size_t)blockIdx.x * 2 * p.max_cells;
+    }
+    V1 = V0 + p.max_cells;
   } else {
-    C = p.slice + (size_t)blockIdx.x * p.slice_stride;
+    if (SLICE_SMEM) {
+      C = reinterpret_cast<double*>(sp);
+      sp += sizeof(double) * (size_t)LP * maxM;
+    } else {
+      C = p.slice + (size_t)blockIdx.x * p.slice_stride;
+    }
+    if (W_SMEM) {
+      W = reinterpret_cast<WEnt*>(sp);
+      sp += sizeof(WEnt) * (size_t)LP * L;
+    } else {
+      W = p.wtab + (size_t)blockIdx.x * LP * L;
+    }
   }
   double* Dm = reinterpret_cast<double*>(sp);
   sp += sizeof(double) * maxM;
   double* Pf = reinterpret_cast<double*>(sp);
   sp += sizeof(double) * LP;
   double* E = reinterpret_cast<double*>(sp);
-  sp += sizeof(double) * L;
+  sp += sizeof(double) * 2 * L;
   double* bwq = reinterpret_cast<double*>(sp);
   sp += sizeof(double) * maxpp;
   double* st = reinterpret_cast<double*>(sp);
@@ -423,10 +548,9 @@ __global__ void __launch_bounds__(kEvalThreads) k_evaluate(EvalParams p) {
   sp += sizeof(int) * (maxpp + 2);
   int* place = reinterpret_cast<int*>(sp);
   sp += sizeof(int) * D;
-  sp = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sp) + 15) & ~uintptr_t(15));
-  uint16_t* seg = reinterpret_cast<uint16_t*>(sp);
+  // (integer offset from smem_raw keeps the shared address space visible)
+  uint16_t* seg = reinterpret_cast<uint16_t*>(smem_raw + ((sp - smem_raw + 15) & ~15));
 
-  uint8_t* bp = p.bp + (size_t)blockIdx.x * p.bp_stride;
   amp_record* mytop = p.cta_topk + (size_t)blockIdx.x * p.k;
   if (tid == 0) sh.n_top = 0;
 
@@ -496,8 +620,10 @@ __global__ void __launch_bounds__(kEvalThreads) k_evaluate(EvalParams p) {
       const double* gdom = p.domain + (size_t)cl.pair * p.nv_stride;
       for (int x = tid; x < M; x += nt) Dm[x] = gdom[x];
       for (int x = tid; x < LP; x += nt) Pf[x] = p.prefix[(size_t)cl.pair * LP + x];
-      const uint16_t* gseg = p.seg + (size_t)cl.pair * LP * LP;
-      for (int x = tid; x < LP * LP; x += nt) seg[x] = gseg[x];
+      if (!SPARSE) {
+        const uint16_t* gseg = p.seg + (size_t)cl.pair * LP * LP;
+        for (int x = tid; x < LP * LP; x += nt) seg[x] = gseg[x];
+      }
       __syncthreads();
       // min_edge_bandwidth per stage boundary (cost_model.cpp:164-174)
       for (int q = tid; q < pp - 1; q += nt) {
@@ -522,13 +648,19 @@ __global__ void __launch_bounds__(kEvalThreads) k_evaluate(EvalParams p) {
     }
     if (ok) {
       EdgeFromBandwidth ef{p.act, bwq, mbs};
-      dp_solve(L, pp, gas, M, Pf, Dm, seg, ef, C, E, bp, cuts);
+      if (SPARSE) {
+        const ProgDev pg = p.progs[p.class_prog[c]];
+        sparse_solve(L, pp, gas, Pf, Dm, pg, p.cells, p.cellpred, p.preds, p.stage, ef, V0, V1, E,
+                     E + L, bp, cuts);
+      } else {
+        dp_solve(L, pp, gas, M, Pf, Dm, seg, ef, C, W, E, pr.monotone != 0, bp, cuts);
+      }
       // ---- per-device parameter ceiling (optimizer.cpp:159-169) ---------
       const double* tl = p.times + (size_t)cl.pair * L;
-      if (tid < pp) {
+      for (int j = tid; j < pp; j += nt) {
         double sum = 0.0;  // stage_time (cost_model.cpp:88-98)
-        for (int l = cuts[tid]; l < cuts[tid + 1]; ++l) sum += tl[l];
-        st[tid] = sum;
+        for (int l = cuts[j]; l < cuts[j + 1]; ++l) sum += tl[l];
+        st[j] = sum;
       }
       if (tid == 0 && p.has_ceiling) {
         double worst = 0.0;
@@ -785,6 +917,7 @@ struct DpBatchParams {
   uint64_t slice_stride;
   double* domain;  // per-CTA scratch [npow2]
   uint16_t* seg;   // per-CTA scratch [(max_L+1)^2]
+  WEnt* wtab;      // per-CTA scratch [(max_L+1) * max_L]
 };
 
 __global__ void k_dp_batch(DpBatchParams p) {
@@ -795,6 +928,7 @@ __global__ void k_dp_batch(DpBatchParams p) {
   double* Pf = vals + p.npow2;
   double* E = Pf + p.max_L + 1;
   int* cuts = reinterpret_cast<int*>(E + p.max_L);
+  WEnt* W = p.wtab + (size_t)blockIdx.x * (p.max_L + 1) * p.max_L;
   double* dom = p.domain + (size_t)blockIdx.x * p.npow2;
   uint16_t* seg = p.seg + (size_t)blockIdx.x * (p.max_L + 1) * (p.max_L + 1);
   double* C = p.slice + (size_t)blockIdx.x * p.slice_stride;
@@ -803,10 +937,13 @@ __global__ void k_dp_batch(DpBatchParams p) {
     const DpBatchItem it = p.items[inst];
     if (it.status != 0) continue;
     const int L = it.L;
+    __shared__ int mono;
     if (tid == 0) {
       double s = 0.0;
       Pf[0] = 0.0;
+      mono = 1;
       for (int l = 0; l < L; ++l) {
+        if (!(it.times[l] >= 0.0)) mono = 0;
         s = s + it.times[l];
         Pf[l + 1] = s;
       }
@@ -816,7 +953,7 @@ __global__ void k_dp_batch(DpBatchParams p) {
     while (np2 < 1 + L * (L + 1) / 2) np2 <<= 1;
     const int M = build_domain(Pf, L, vals, np2, dom, seg, redi);
     EdgeFromTable ef{it.edges, L};
-    const double cost = dp_solve(L, it.stages, it.gas, M, Pf, dom, seg, ef, C, E, bp, cuts);
+    const double cost = dp_solve(L, it.stages, it.gas, M, Pf, dom, seg, ef, C, W, E, mono != 0, bp, cuts);
     if (tid == 0) {
       p.cost_out[inst] = cost;
       for (int q = 0; q <= it.stages; ++q) p.cuts_out[(size_t)inst * p.cut_stride + q] = cuts[q];

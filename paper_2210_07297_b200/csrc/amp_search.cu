@@ -75,13 +75,25 @@ struct amp_ctx {
   int max_pp = 1, max_M = 1, nv_stride = 1, npow2 = 2;
   size_t bp_stride = 0, slice_stride = 0;
   int slice_in_smem = 1;
+  int w_in_smem = 1;
+  const void* eval_fn = nullptr;
+  int eval_threads = kEvalThreads;
   size_t smem_bytes = 0;
   int n_ctas = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
   DevBuf param, act, bw, base_order, times, prefix, domain, seg, pairs_d, cls_d;
-  DevBuf bp, slice, cta_topk, topk, taken, segs, counter, index_list;
+  DevBuf bp, slice, wtab, cta_topk, topk, taken, segs, counter, index_list;
   DevBuf o_all, o_cuts, o_stage, o_edge, o_place;
+  // pruned DP programs
+  bool sparse = false, progs_ok = false;
+  int mode = 0;
+  std::vector<int32_t> class_prog;
+  std::vector<ProgDev> progs_h;
+  std::vector<double> prog_inner;  // inner iterations per program
+  int max_cells = 1, max_prog_cells = 1;
+  size_t v_stride = 0;
+  DevBuf progs_d, stage_d, class_prog_d, cells, cellpred, preds, vbuf;
   amp_stats stats{};
 };
 
@@ -110,6 +122,139 @@ cudaError_t upload(DevBuf& b, const T* src, size_t n) {
   if (e != cudaSuccess) return e;
   if (n) e = cudaMemcpy(b.p, src, sizeof(T) * n, cudaMemcpyHostToDevice);
   return e;
+}
+
+// K0b driver: programs for every distinct (pair, k) of the feasible classes.
+// Pass 1 counts |N_j| and predecessor entries per stage; the host lays out
+// the arrays; pass 2 writes them.  Sets ctx->progs_ok = false (dense DP)
+// when some |N_j| exceeds the u16 index range.
+int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
+  (void)seg_h;
+  const int L = ctx->L, LP = L + 1;
+  std::map<std::pair<int, int>, int> prog_of;
+  std::vector<int32_t> pk, ppair;
+  ctx->class_prog.assign(ctx->classes.size(), 0);
+  for (size_t c = 0; c < ctx->classes.size(); ++c) {
+    const ClassDev& cl = ctx->classes[c];
+    if (cl.pp > L || ctx->pairs[cl.pair].fail_code) continue;
+    auto key = std::make_pair(cl.pair, cl.pp);
+    auto it = prog_of.find(key);
+    if (it == prog_of.end()) {
+      it = prog_of.emplace(key, (int)pk.size()).first;
+      pk.push_back(cl.pp);
+      ppair.push_back(cl.pair);
+    }
+    ctx->class_prog[c] = it->second;
+  }
+  const int n = (int)pk.size();
+  ctx->progs_ok = true;
+  ctx->prog_inner.assign(n, 0.0);
+  if (n == 0) {
+    CK(upload(ctx->class_prog_d, ctx->class_prog.data(), ctx->class_prog.size()));
+    return AMP_OK;
+  }
+  DevBuf d_k, d_pair, d_scratch, d_sizes, d_preds_n, d_pstart;
+  CK(upload(d_k, pk.data(), pk.size()));
+  CK(upload(d_pair, ppair.data(), ppair.size()));
+  const uint64_t scratch_stride = 2ull * LP * ctx->max_M;
+  CK(d_scratch.ensure(sizeof(uint32_t) * scratch_stride * n));
+  CK(d_sizes.ensure(sizeof(uint32_t) * (size_t)n * LP));
+  CK(d_preds_n.ensure(sizeof(uint64_t) * (size_t)n * LP));
+  CK(cudaMemsetAsync(d_sizes.p, 0, sizeof(uint32_t) * (size_t)n * LP, ctx->stream));
+  CK(cudaMemsetAsync(d_preds_n.p, 0, sizeof(uint64_t) * (size_t)n * LP, ctx->stream));
+  ProgBuildParams bp{};
+  bp.L = L;
+  bp.n_progs = n;
+  bp.count_only = 1;
+  bp.prog_k = d_k.as<int32_t>();
+  bp.prog_pair = d_pair.as<int32_t>();
+  bp.pairs = ctx->pairs_d.as<PairDev>();
+  bp.seg = ctx->seg.as<uint16_t>();
+  bp.scratch = d_scratch.as<uint32_t>();
+  bp.scratch_stride = scratch_stride;
+  bp.stage_sizes = d_sizes.as<uint32_t>();
+  bp.stage_preds = d_preds_n.as<uint64_t>();
+  const int W = (ctx->max_M + 31) / 32;
+  const size_t smem = sizeof(uint32_t) * 2 * (size_t)LP * W + sizeof(uint16_t) * LP * LP;
+  if (smem > 227 * 1024) {
+    ctx->progs_ok = false;
+    return AMP_OK;
+  }
+  CK(cudaFuncSetAttribute(k_build_progs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_build_progs<<<n, 512, smem, ctx->stream>>>(bp);
+  CK(cudaGetLastError());
+  std::vector<uint32_t> sizes((size_t)n * LP);
+  std::vector<uint64_t> pn((size_t)n * LP);
+  CK(cudaMemcpyAsync(sizes.data(), d_sizes.p, sizeof(uint32_t) * sizes.size(),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(pn.data(), d_preds_n.p, sizeof(uint64_t) * pn.size(), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  // layout
+  std::vector<ProgDev> progs(n);
+  std::vector<uint32_t> stage;
+  std::vector<uint64_t> pstart((size_t)n * LP, 0);
+  uint64_t cell_total = 0, pred_total = 0;
+  int max_cells = 1;
+  uint64_t max_prog_cells = 1;
+  for (int g = 0; g < n; ++g) {
+    const int k = pk[g];
+    ProgDev& d = progs[g];
+    d.k = k;
+    d.pair = ppair[g];
+    d.cell_base = (uint32_t)cell_total;
+    d.stage_base = (uint32_t)stage.size();
+    d.pred_base = pred_total;
+    uint32_t acc = 0, mx = 0;
+    for (int j = 1; j <= k; ++j) {
+      stage.push_back(acc);
+      const uint32_t sz = sizes[(size_t)g * LP + j];
+      acc += sz;
+      mx = std::max(mx, sz);
+    }
+    stage.push_back(acc);
+    uint64_t pacc = 0;
+    for (int j = 2; j <= k; ++j) {
+      pstart[(size_t)g * LP + j] = pacc;
+      pacc += pn[(size_t)g * LP + j];
+    }
+    d.n_cells = acc;
+    d.max_cells = mx;
+    d.n_preds = pacc;
+    d.ok = mx <= 65536;
+    if (!d.ok) ctx->progs_ok = false;
+    cell_total += acc;
+    pred_total += pacc;
+    max_cells = std::max<int>(max_cells, (int)mx);
+    max_prog_cells = std::max<uint64_t>(max_prog_cells, acc);
+    ctx->prog_inner[g] = (double)pacc;
+  }
+  if (!ctx->progs_ok || cell_total >= (1ull << 32)) {
+    ctx->progs_ok = false;
+    return AMP_OK;
+  }
+  ctx->max_cells = max_cells;
+  ctx->max_prog_cells = (int)max_prog_cells;
+  CK(upload(ctx->progs_d, progs.data(), progs.size()));
+  CK(upload(ctx->stage_d, stage.data(), stage.size()));
+  CK(upload(ctx->class_prog_d, ctx->class_prog.data(), ctx->class_prog.size()));
+  DevBuf d_pst;
+  CK(upload(d_pst, pstart.data(), pstart.size()));
+  CK(ctx->cells.ensure(sizeof(uint32_t) * cell_total));
+  CK(ctx->cellpred.ensure(sizeof(uint32_t) * cell_total));
+  CK(ctx->preds.ensure(sizeof(uint16_t) * (pred_total + 8)));
+  bp.count_only = 0;
+  bp.progs = ctx->progs_d.as<ProgDev>();
+  bp.cells = ctx->cells.as<uint32_t>();
+  bp.cellpred = ctx->cellpred.as<uint32_t>();
+  bp.preds = ctx->preds.as<uint16_t>();
+  bp.stage = ctx->stage_d.as<uint32_t>();
+  bp.pred_start = d_pst.as<uint64_t>();
+  k_build_progs<<<n, 512, smem, ctx->stream>>>(bp);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->progs_h = progs;
+  return AMP_OK;
 }
 
 int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
@@ -302,37 +447,83 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   }
   ctx->bp_stride = (bp_stride + 255) & ~size_t(255);
 
-  // ---- evaluate kernel launch shape -------------------------------------
   const int LP = L + 1;
-  auto smem_for = [&](bool slice) {
-    size_t b = 0;
-    if (slice) b += sizeof(double) * (size_t)LP * ctx->max_M;
-    b += sizeof(double) * ctx->max_M + sizeof(double) * LP + sizeof(double) * L +
-         2 * sizeof(double) * ctx->max_pp + sizeof(int) * (ctx->max_pp + 2) + sizeof(int) * D;
-    b = (b + 15) & ~size_t(15);
-    b += sizeof(uint16_t) * LP * LP;
-    return b;
-  };
-  const size_t smem_limit = 200 * 1024;
-  ctx->slice_in_smem = smem_for(true) <= smem_limit;
-  ctx->smem_bytes = smem_for(ctx->slice_in_smem != 0);
+  // ---- K0b: pruned-DP programs, one per distinct (pair, k) ---------------
+  bool sparse = !(cfg && (cfg->flags & AMP_FLAG_DENSE_DP));
+  if (sparse) {
+    int rc = build_programs(ctx, seg_h);
+    if (rc != AMP_OK) return rc;
+    sparse = ctx->progs_ok;
+  }
+  ctx->sparse = sparse;
+  if (sparse)  // scheduling/roofline weights: executed predecessor entries
+    for (size_t c = 0; c < ctx->classes.size(); ++c)
+      if (ctx->class_inner[c] > 0) {
+        ctx->class_inner[c] = ctx->prog_inner[ctx->class_prog[c]];
+        ctx->class_lt[c] = 0;
+      }
+
+  // ---- evaluate kernel launch shape -------------------------------------
+  size_t small = sizeof(double) * ctx->max_M + sizeof(double) * LP + 2 * sizeof(double) * L +
+                 2 * sizeof(double) * ctx->max_pp + sizeof(int) * (ctx->max_pp + 2) +
+                 sizeof(int) * D;
+  small = (small + 15) & ~size_t(15);
+  const size_t w_b = sizeof(WEnt) * (size_t)LP * L;
+  int mode;
+  if (sparse) {
+    // value arrays (2 stages) + backpointers of one candidate
+    const size_t v_b = sizeof(double) * 2 * (size_t)ctx->max_cells +
+                       (((size_t)ctx->max_prog_cells + 15) & ~size_t(15));
+    const bool v_smem = small + v_b <= 64 * 1024;
+    mode = v_smem ? kSparseS : kSparseG;
+    ctx->smem_bytes = small + (v_smem ? v_b : 0);
+    ctx->eval_threads = v_smem ? 128 : 256;
+    ctx->bp_stride = v_smem ? 0 : (((size_t)ctx->max_prog_cells + 255) & ~size_t(255));
+    ctx->v_stride = v_smem ? 0 : 2 * (size_t)ctx->max_cells;
+    ctx->slice_in_smem = ctx->w_in_smem = 1;
+  } else {
+    // smem = [C slice (L+1) x max_M] [W table (L+1) x L x 32 B] + small
+    // arrays + seg table; keep whichever big one fits (slice first).
+    small += sizeof(uint16_t) * LP * LP;
+    const size_t slice_b = sizeof(double) * (size_t)LP * ctx->max_M;
+    const size_t smem_limit = 200 * 1024;
+    ctx->slice_in_smem = small + slice_b <= smem_limit;
+    ctx->w_in_smem = small + w_b + (ctx->slice_in_smem ? slice_b : 0) <= smem_limit;
+    ctx->smem_bytes = small + (ctx->slice_in_smem ? slice_b : 0) + (ctx->w_in_smem ? w_b : 0);
+    mode = ctx->slice_in_smem ? (ctx->w_in_smem ? kDenseSS : kDenseSG)
+                              : (ctx->w_in_smem ? kDenseGS : kDenseGG);
+    // one thread per domain column (threads beyond M idle in the DP sweep)
+    ctx->eval_threads = std::min(kEvalThreads, std::max(128, (ctx->max_M + 31) / 32 * 32));
+    ctx->v_stride = 0;
+  }
   if (ctx->smem_bytes > 227 * 1024) return fail(ctx, AMP_E_UNSUPPORTED, "shared memory budget");
-  CK(cudaFuncSetAttribute(k_evaluate, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static const void* const kModes[] = {(const void*)k_evaluate<kDenseSS>,
+                                       (const void*)k_evaluate<kDenseSG>,
+                                       (const void*)k_evaluate<kDenseGS>,
+                                       (const void*)k_evaluate<kDenseGG>,
+                                       (const void*)k_evaluate<kSparseS>,
+                                       (const void*)k_evaluate<kSparseG>};
+  ctx->mode = mode;
+  ctx->eval_fn = kModes[mode];
+  CK(cudaFuncSetAttribute(ctx->eval_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)ctx->smem_bytes));
   int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_evaluate, kEvalThreads,
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ctx->eval_fn, ctx->eval_threads,
                                                    ctx->smem_bytes));
   if (occ < 1) return fail(ctx, AMP_E_UNSUPPORTED, "evaluate kernel does not fit on an SM");
   int n_ctas = occ * prop.multiProcessorCount;
-  ctx->slice_stride = ctx->slice_in_smem ? 0 : (size_t)LP * ctx->max_M;
-  // keep per-CTA scratch (backpointers + global slice) within 16 GiB
-  const size_t per_cta = ctx->bp_stride + sizeof(double) * ctx->slice_stride;
+  ctx->slice_stride = (sparse || ctx->slice_in_smem) ? 0 : (size_t)LP * ctx->max_M;
+  // keep per-CTA scratch (backpointers + global slice/table/values) within 16 GiB
+  const size_t per_cta = ctx->bp_stride + sizeof(double) * (ctx->slice_stride + ctx->v_stride) +
+                         ((sparse || ctx->w_in_smem) ? 0 : w_b);
   const size_t cap = (size_t)16 << 30;
-  if ((size_t)n_ctas * per_cta > cap) n_ctas = std::max<size_t>(1, cap / per_cta);
+  if (per_cta && (size_t)n_ctas * per_cta > cap) n_ctas = std::max<size_t>(1, cap / per_cta);
   if (ctx->max_ctas_cfg > 0) n_ctas = std::min(n_ctas, ctx->max_ctas_cfg);
   ctx->n_ctas = n_ctas;
-  CK(ctx->bp.ensure(ctx->bp_stride * n_ctas));
-  if (!ctx->slice_in_smem) CK(ctx->slice.ensure(sizeof(double) * ctx->slice_stride * n_ctas));
+  CK(ctx->bp.ensure(ctx->bp_stride * n_ctas + 16));
+  if (ctx->slice_stride) CK(ctx->slice.ensure(sizeof(double) * ctx->slice_stride * n_ctas));
+  if (!sparse && !ctx->w_in_smem) CK(ctx->wtab.ensure(w_b * n_ctas));
+  if (ctx->v_stride) CK(ctx->vbuf.ensure(sizeof(double) * ctx->v_stride * n_ctas));
   CK(ctx->counter.ensure(sizeof(unsigned long long)));
   return AMP_OK;
 }
@@ -384,10 +575,11 @@ void account(amp_ctx* ctx, uint64_t begin, uint64_t end, const uint64_t* list, i
     }
     s.candidates = end - begin;
   }
-  // FP64 ops the exact recurrence needs: m >= seg: 2 DADD +
-  // 1 DSETP; m < seg: DADD, DMUL, 3 DADD, DSETP.
+  // FP64 ops of the executed recurrence.  Dense split form:
+  // m >= seg: 2 DADD + DSETP; m < seg: DADD, DMUL, 3 DADD, DSETP.  Pruned
+  // form (generic recurrence): t2 DADD, x DADD, max DSETP, DMUL, 3 DADD, DSETP.
   const double ge = s.dp_inner - s.dp_inner_lt;
-  s.fp64_ops = 3.0 * ge + 6.0 * s.dp_inner_lt;
+  s.fp64_ops = ctx->sparse ? 8.0 * s.dp_inner : 3.0 * ge + 6.0 * s.dp_inner_lt;
   s.bytes = 0;
 }
 
@@ -418,6 +610,8 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   ep.seg = ctx->seg.as<uint16_t>();
   ep.nv_stride = ctx->nv_stride;
   ep.slice_in_smem = ctx->slice_in_smem;
+  ep.w_in_smem = ctx->w_in_smem;
+  ep.wtab = ctx->wtab.as<WEnt>();
   if (segs) {
     CK(upload(ctx->segs, segs->data(), segs->size()));
     ep.segs = ctx->segs.as<Segment>();
@@ -451,8 +645,19 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   ep.cta_topk = ctx->cta_topk.as<amp_record>();
   ep.k = kk;
   ep.max_M = ctx->max_M;
+  ep.progs = ctx->progs_d.as<ProgDev>();
+  ep.class_prog = ctx->class_prog_d.as<int32_t>();
+  ep.cells = ctx->cells.as<uint32_t>();
+  ep.cellpred = ctx->cellpred.as<uint32_t>();
+  ep.preds = ctx->preds.as<uint16_t>();
+  ep.stage = ctx->stage_d.as<uint32_t>();
+  ep.vbuf = ctx->vbuf.as<double>();
+  ep.max_cells = ctx->max_cells;
+  ep.max_prog_cells = ctx->max_prog_cells;
   CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), ctx->stream));
-  k_evaluate<<<ctx->n_ctas, kEvalThreads, ctx->smem_bytes, ctx->stream>>>(ep);
+  void* args[] = {&ep};
+  CK(cudaLaunchKernel(ctx->eval_fn, dim3(ctx->n_ctas), dim3(ctx->eval_threads), args, ctx->smem_bytes,
+                      ctx->stream));
   CK(cudaGetLastError());
   return AMP_OK;
 }
@@ -769,7 +974,7 @@ int amp_dp_solve_batch(int32_t device, const amp_dp_instance* inst, int32_t n, i
     if (ne) std::memcpy(&edges[ea], inst[i].edge_costs, sizeof(double) * ne);
     ea += ne;
   }
-  DevBuf d_times, d_edges, d_items, d_cuts, d_cost, d_bp, d_slice, d_dom, d_seg;
+  DevBuf d_times, d_edges, d_items, d_cuts, d_cost, d_bp, d_slice, d_dom, d_seg, d_w;
   int rc;
 #define CKB(call)                                                    \
   do {                                                               \
@@ -801,6 +1006,7 @@ int amp_dp_solve_batch(int32_t device, const amp_dp_instance* inst, int32_t n, i
   CKB(d_slice.ensure(sizeof(double) * slice_stride * grid));
   CKB(d_dom.ensure(sizeof(double) * (size_t)npow2 * grid));
   CKB(d_seg.ensure(sizeof(uint16_t) * (size_t)(max_L + 1) * (max_L + 1) * grid));
+  CKB(d_w.ensure(sizeof(WEnt) * (size_t)(max_L + 1) * max_L * grid));
   DpBatchParams bpp{};
   bpp.items = d_items.as<DpBatchItem>();
   bpp.n = n;
@@ -816,9 +1022,10 @@ int amp_dp_solve_batch(int32_t device, const amp_dp_instance* inst, int32_t n, i
   bpp.slice_stride = slice_stride;
   bpp.domain = d_dom.as<double>();
   bpp.seg = d_seg.as<uint16_t>();
+  bpp.wtab = d_w.as<WEnt>();
   const size_t smem = sizeof(double) * (npow2 + 2 * (max_L + 1)) + sizeof(int) * (max_k + 2);
   CKB(cudaFuncSetAttribute(k_dp_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_dp_batch<<<grid, 256, smem>>>(bpp);
+  k_dp_batch<<<grid, 512, smem>>>(bpp);
   CKB(cudaGetLastError());
   std::vector<int32_t> cuts((size_t)n * cut_stride);
   CKB(cudaMemcpy(cuts.data(), d_cuts.p, sizeof(int32_t) * cuts.size(), cudaMemcpyDeviceToHost));

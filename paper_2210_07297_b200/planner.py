@@ -106,11 +106,11 @@ class Searcher:
     """One amp_ctx: problem tables resident on one GPU."""
 
     def __init__(self, problem: EncodedProblem, placements_per_class: int = 1, seed: int = 0,
-                 device: int = 0, max_ctas: int = 0):
+                 device: int = 0, max_ctas: int = 0, dense_dp: bool = False):
         self.lib = N.load()
         self.problem = problem
         cfg = N.AmpSearchConfig(int(placements_per_class), int(seed) & (2**64 - 1), int(device),
-                                int(max_ctas))
+                                int(max_ctas), N.AMP_FLAG_DENSE_DP if dense_dp else 0, 0)
         h = C.c_void_p()
         N.check(self.lib.amp_search_create(C.byref(h), problem.ref(), C.byref(cfg)))
         self.ctx = h
@@ -242,13 +242,13 @@ def rank_order(recs: np.ndarray) -> np.ndarray:
 
 
 def plan(model: ModelGraph, cluster: Cluster, profile: ProfileTable, gbs: int,
-         options: Optional[PlanOptions] = None, device: int = 0) -> PlanResult:
+         options: Optional[PlanOptions] = None, device: int = 0, dense_dp: bool = False) -> PlanResult:
     """parplan::plan on the GPU (optimizer.cpp:200-251)."""
     from . import simulator
 
     options = options or PlanOptions()
     enc = EncodedProblem(model, cluster, profile, gbs, options)
-    with Searcher(enc, placements_per_class=1, device=device) as s:
+    with Searcher(enc, placements_per_class=1, device=device, dense_dp=dense_dp) as s:
         _, allr, bufs = s.run(0, s.num_candidates, k=0, want_all=True, details=True, placement=True)
     order = rank_order(allr)
     cands = records_to_candidates(allr, bufs, model.layer_count(), rows=order)

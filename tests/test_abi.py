@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
 def test_struct_layouts():
     assert C.sizeof(N.AmpRecord) == 64
     assert planner.RECORD_DTYPE.itemsize == 64
-    assert C.sizeof(N.AmpSearchConfig) == 24
+    assert C.sizeof(N.AmpSearchConfig) == 32
     # amp_problem: 4 ints, 6 ptrs, int64, 4 ptrs, 3 doubles, 2 ints, 1 double
     assert C.sizeof(N.AmpProblem) == 16 + 48 + 8 + 32 + 24 + 8 + 8
 

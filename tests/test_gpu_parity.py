@@ -85,11 +85,12 @@ def check_plan_against_golden(res, golden):
     assert res.best_index == golden["best_index"]
 
 
+@pytest.mark.parametrize("dense", [False, True], ids=["pruned", "dense"])
 @pytest.mark.parametrize("name", ["homogeneous", "hetero_cluster", "hetero_model", "synthetic96"])
-def test_gpu_plan_matches_reference(name):
+def test_gpu_plan_matches_reference(name, dense):
     sc = scenario(name)
     golden = load_json(f"plan_{name}.json")
-    res = planner.plan(sc.model, sc.cluster, sc.profile, sc.gbs, sc.options)
+    res = planner.plan(sc.model, sc.cluster, sc.profile, sc.gbs, sc.options, dense_dp=dense)
     check_plan_against_golden(res, golden)
 
 
@@ -101,12 +102,14 @@ def test_heuristic_placement_matches_reference_order():
     assert (bufs["placement"] == np.arange(16)).all()
 
 
+@pytest.mark.parametrize("dense", [False, True], ids=["pruned", "dense"])
 @pytest.mark.parametrize("name", ["hetero_cluster", "hetero_model"])
-def test_gpu_sweep_matches_reference(name):
+def test_gpu_sweep_matches_reference(name, dense):
     g = load_json(f"sweep_{name}.json")
     sc = scenario(name)
     enc = P.EncodedProblem.from_scenario(sc)
-    with planner.Searcher(enc, placements_per_class=g["placements_per_class"], seed=g["seed"]) as s:
+    with planner.Searcher(enc, placements_per_class=g["placements_per_class"], seed=g["seed"],
+                          dense_dp=dense) as s:
         top, allr, bufs = s.run(0, g["n"], k=10, want_all=True, details=True)
     for i, e in enumerate(g["records"]):
         r = allr[i]
@@ -119,14 +122,15 @@ def test_gpu_sweep_matches_reference(name):
     assert top["index"].tolist() == allr["index"][order].tolist()
 
 
+@pytest.mark.parametrize("dense", [False, True], ids=["pruned", "dense"])
 @pytest.mark.parametrize("kind", ["plain", "miss", "ceiling", "fallback"])
-def test_gpu_failure_paths_match_oracle(kind):
+def test_gpu_failure_paths_match_oracle(kind, dense):
     from test_oracle import _variant_world
     model, cl, prof, gbs, opts = _variant_world(kind)
     enc = P.EncodedProblem(model, cl, prof, gbs, opts)
     o = B.Oracle(enc, placements_per_class=5, seed=11)
     orec, odet = o.run(threads=4)
-    with planner.Searcher(enc, placements_per_class=5, seed=11) as s:
+    with planner.Searcher(enc, placements_per_class=5, seed=11, dense_dp=dense) as s:
         _, allr, bufs = s.run(0, s.num_candidates, k=5, want_all=True, details=True)
     for f in ("index", "pp", "dp", "tmp", "mbs", "fail_code"):
         assert np.array_equal(allr[f], orec[f]), f
@@ -134,7 +138,7 @@ def test_gpu_failure_paths_match_oracle(kind):
     for f in ("total", "pipeline_time", "dpsync_time"):
         assert np.array_equal(allr[f][ok], orec[f][ok]), f
     assert np.array_equal(bufs["cuts"][ok], odet["cuts"][ok])
-    assert np.array_equal(bufs["stage_times"][ok], odet["stage_times"][ok])
+    assert np.array_equal(bufs["stage_times"][ok], odet["stage_times"][ok], equal_nan=True)
     ed_ok = ~np.isnan(odet["edge_times"])
     assert np.array_equal(bufs["edge_times"][ed_ok], odet["edge_times"][ed_ok])
     miss = orec["fail_code"] == 2
