@@ -47,6 +47,8 @@ struct Segment {
   uint64_t count;   // number of candidates
   uint64_t offset;  // exclusive prefix of counts in dispatch order
   uint64_t out;     // position of `first` in the caller's output order
+  uint64_t p0;      // placement index of `first` within its class
+  int64_t cls;      // class of the whole segment
 };
 
 struct WEnt;     // per-stage cut table entry (amp_kernels.cuh)
@@ -80,6 +82,8 @@ struct EvalParams {
   int32_t n_segs;
   int32_t pad0;
   uint64_t n_work;
+  int32_t chunk;               // work items taken per atomic fetch
+  int32_t pad2;
   const uint64_t* index_list;  // explicit indices (evaluate) or NULL
   unsigned long long* counter;
   // scratch (per CTA)
@@ -106,6 +110,7 @@ struct EvalParams {
   const uint16_t* preds;
   const uint32_t* stage;
   double* vbuf;               // global value arrays when not in smem
+  unsigned long long* phase_cycles;  // [8], AMP_PROFILE_PHASES builds only
   int32_t max_cells;          // max_j |N_j| over programs
   int32_t max_prog_cells;     // max sum_j |N_j| over programs
 };

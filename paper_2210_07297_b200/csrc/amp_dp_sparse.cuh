@@ -21,7 +21,8 @@
 //               descending then m ascending (equal cut counts are adjacent)
 //   cellpred[]  u32 per cell of N_j (j >= 2): offset of its predecessor list
 //   preds[]     u16 per (cell, cut): index of (c, max(seg(c,i), m)) within
-//               N_{j-1}, for c = j-1 .. i-1
+//               N_{j-1}, for c = j-1 .. i-1; each cell's list is padded to a
+//               multiple of 4 entries so it can be read with 8-byte loads
 //   stage[]     u32 k+1 entries: start of N_j (j = 1..k) within the program's
 //               cells, then the end
 #pragma once
@@ -136,7 +137,7 @@ __global__ void k_build_progs(ProgBuildParams p) {
     for (int x = tid; x < n; x += nt) {
       const uint32_t cell = A[x];
       const int i = cell >> 16, m = cell & 0xffff;
-      my_preds += (uint64_t)(i - j + 1);
+      my_preds += (uint64_t)((i - j + 1 + 3) & ~3);  // lists padded to 4 (8-byte loads)
       for (int c = j - 1; c < i; ++c) {
         const int s = seg[c * LP + i];
         const int mp = s > m ? s : m;
@@ -163,7 +164,7 @@ __global__ void k_build_progs(ProgBuildParams p) {
       const uint64_t pbase = pd.pred_base + p.pred_start[(size_t)pg * LP + j];
       uint32_t* cpo = p.cellpred + pd.cell_base + p.stage[pd.stage_base + j - 1];
       block_scan(
-          n, [&](int x) { return (uint64_t)((A[x] >> 16) - j + 1); },
+          n, [&](int x) { return (uint64_t)(((A[x] >> 16) - j + 1 + 3) & ~3u); },
           [&](int x, uint64_t before) {
             const uint32_t cell = A[x];
             const int i = cell >> 16, m = cell & 0xffff;
@@ -206,6 +207,25 @@ __global__ void k_build_progs(ProgBuildParams p) {
 // writes V[j & 1], one barrier per stage.  E[j & 1][c] is stage j's edge cost
 // at cut c (boundary j-2), computed one stage ahead.  bpS[x] is the argmin
 // cut of cell x (global cell index within the program).
+// One cut of the recurrence (pipeline_dp.cpp:122): with t2 = prefix[i] -
+// prefix[c] and x = t2 - dom[m], (gas-1) * max(0, x) equals
+// (t2 > dom[m]) ? (gas-1) * x : +0.0 exactly (for finite IEEE doubles
+// a - b > 0 iff a > b, and NaN compares false on both sides).
+__device__ __forceinline__ void cut_step(double sub, double Pi, double2 pe, double dm, double g1,
+                                         int c, double& best, int& bc) {
+  const double t2 = Pi - pe.x;
+  const double term = t2 > dm ? g1 * (t2 - dm) : 0.0;
+  const double g = ((sub + term) + t2) + pe.y;
+  if (g < best) {
+    best = g;
+    bc = c;
+  }
+}
+
+// V[j & 1][x] holds cost(cell x of N_j); stage j reads V[(j-1) & 1] and
+// writes V[j & 1], one barrier per stage.  PE[j & 1][c] = {prefix[c],
+// edge_j(c)} for stage j (boundary j-2), built one stage ahead.  bpS[x] is
+// the argmin cut of cell x (global cell index within the program).
 template <class EdgeFn>
 __device__ double sparse_solve(const int L, const int k, const int gas,
                                const double* __restrict__ Pf, const double* __restrict__ Dm,
@@ -213,7 +233,7 @@ __device__ double sparse_solve(const int L, const int k, const int gas,
                                const uint32_t* __restrict__ cellpred,
                                const uint16_t* __restrict__ preds,
                                const uint32_t* __restrict__ stage, const EdgeFn& edge,
-                               double* V0, double* V1, double* E0, double* E1,
+                               double* V0, double* V1, double2* PE0, double2* PE1,
                                uint8_t* __restrict__ bpS, int* cuts) {
   const double g1 = (double)(gas - 1);
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -229,36 +249,79 @@ __device__ double sparse_solve(const int L, const int k, const int gas,
     V1[x - ss[0]] = g1 * max0(t1 - Dm[m]) + t1;
   }
   if (k >= 2)
-    for (int c = 1 + tid; c < L; c += nt) E0[c] = edge(c, 0);  // stage 2 -> E[0]
+    for (int c = 1 + tid; c < L; c += nt) PE0[c] = make_double2(Pf[c], edge(c, 0));  // stage 2
   __syncthreads();
   for (int j = 2; j <= k; ++j) {
     const double* Vp = (j & 1) ? V0 : V1;
     double* Vc = (j & 1) ? V1 : V0;
-    const double* Ej = (j & 1) ? E1 : E0;
+    const double2* PE = (j & 1) ? PE1 : PE0;
     if (j < k) {
-      double* En = (j & 1) ? E0 : E1;
-      for (int c = j + tid; c < L; c += nt) En[c] = edge(c, j - 1);
+      double2* PN = (j & 1) ? PE0 : PE1;
+      for (int c = j + tid; c < L; c += nt) PN[c] = make_double2(Pf[c], edge(c, j - 1));
     }
     const uint32_t s0 = ss[j - 1], s1 = ss[j];
     const int c0 = j - 1;
-    for (uint32_t x = s0 + tid; x < s1; x += nt) {
-      const uint32_t cell = cl[x];
-      const int i = cell >> 16, m = cell & 0xffff;
-      const double dm = Dm[m], Pi = Pf[i];
-      const uint16_t* q = pd + cpd[x];
-      double best = CUDART_INF;
-      int bc = -1;
-      for (int c = c0; c < i; ++c) {
-        const double t2 = Pi - Pf[c];
-        const double sub = Vp[q[c - c0]];
-        const double g = ((sub + g1 * max0(t2 - dm)) + t2) + Ej[c];
-        if (g < best) {
-          best = g;
-          bc = c;
+    const int n = (int)(s1 - s0);
+    if (n * 2 > nt) {
+      // one thread per cell; predecessor indices read 4 at a time
+      for (uint32_t x = s0 + tid; x < s1; x += nt) {
+        const uint32_t cell = cl[x];
+        const int i = cell >> 16, m = cell & 0xffff;
+        const double dm = Dm[m], Pi = Pf[i];
+        const uint2* q = reinterpret_cast<const uint2*>(pd + cpd[x]);
+        double best = CUDART_INF;
+        int bc = -1;
+        int c = c0;
+        for (; c + 3 < i; c += 4, ++q) {
+          const uint2 w = __ldg(q);
+          cut_step(Vp[w.x & 0xffff], Pi, PE[c], dm, g1, c, best, bc);
+          cut_step(Vp[w.x >> 16], Pi, PE[c + 1], dm, g1, c + 1, best, bc);
+          cut_step(Vp[w.y & 0xffff], Pi, PE[c + 2], dm, g1, c + 2, best, bc);
+          cut_step(Vp[w.y >> 16], Pi, PE[c + 3], dm, g1, c + 3, best, bc);
+        }
+        if (c < i) {
+          const uint2 w = __ldg(q);
+          cut_step(Vp[w.x & 0xffff], Pi, PE[c], dm, g1, c, best, bc);
+          if (c + 1 < i) cut_step(Vp[w.x >> 16], Pi, PE[c + 1], dm, g1, c + 1, best, bc);
+          if (c + 2 < i) cut_step(Vp[w.y & 0xffff], Pi, PE[c + 2], dm, g1, c + 2, best, bc);
+        }
+        Vc[x - s0] = best;
+        bpS[x] = (uint8_t)bc;
+      }
+    } else {
+      // few cells (late stages): G lanes per cell split the cut loop by
+      // residue, then a lexicographic (value, cut) butterfly combine — equal
+      // to the sequential strict-'<' scan.
+      int G = 2;
+      while (G < 32 && n * G * 2 <= nt) G <<= 1;
+      const int gl = tid & (G - 1);
+      const int per = nt / G;
+      for (int base = 0; base < n; base += per) {  // uniform trip count
+        const int xi = base + tid / G;
+        double best = CUDART_INF;
+        int bc = -1;
+        if (xi < n) {
+          const uint32_t x = s0 + xi;
+          const uint32_t cell = cl[x];
+          const int i = cell >> 16, m = cell & 0xffff;
+          const double dm = Dm[m], Pi = Pf[i];
+          const uint16_t* q = pd + cpd[x] + gl;
+          for (int c = c0 + gl; c < i; c += G, q += G)
+            cut_step(Vp[__ldg(q)], Pi, PE[c], dm, g1, c, best, bc);
+        }
+        for (int o = G >> 1; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+          if (ov < best || (ov == best && oc < bc)) {
+            best = ov;
+            bc = oc;
+          }
+        }
+        if (xi < n && gl == 0) {
+          Vc[xi] = best;
+          bpS[s0 + xi] = (uint8_t)bc;
         }
       }
-      Vc[x - s0] = best;
-      bpS[x] = (uint8_t)bc;
     }
     __syncthreads();
   }

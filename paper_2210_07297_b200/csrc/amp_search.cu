@@ -93,7 +93,7 @@ struct amp_ctx {
   std::vector<double> prog_inner;  // inner iterations per program
   int max_cells = 1, max_prog_cells = 1;
   size_t v_stride = 0;
-  DevBuf progs_d, stage_d, class_prog_d, cells, cellpred, preds, vbuf;
+  DevBuf progs_d, stage_d, class_prog_d, cells, cellpred, preds, vbuf, phase;
   amp_stats stats{};
 };
 
@@ -464,7 +464,9 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
       }
 
   // ---- evaluate kernel launch shape -------------------------------------
-  size_t small = sizeof(double) * ctx->max_M + sizeof(double) * LP + 2 * sizeof(double) * L +
+  size_t small = 16 + 32 * sizeof(double) + sizeof(double) * ctx->max_pp +
+                 (D <= 32 ? sizeof(double) * D * D : 0) + sizeof(amp_record) * 32 +
+                 sizeof(double) * ctx->max_M + sizeof(double) * LP + 4 * sizeof(double) * L +
                  2 * sizeof(double) * ctx->max_pp + sizeof(int) * (ctx->max_pp + 2) +
                  sizeof(int) * D;
   small = (small + 15) & ~size_t(15);
@@ -539,6 +541,8 @@ std::vector<Segment> make_segments(const amp_ctx* ctx, uint64_t begin, uint64_t 
     s.first = lo;
     s.count = hi - lo;
     s.out = lo - begin;
+    s.p0 = lo - c * P;
+    s.cls = (int64_t)c;
     v.emplace_back(ctx->class_inner[c], s);
   }
   std::stable_sort(v.begin(), v.end(),
@@ -618,6 +622,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     ep.n_segs = static_cast<int32_t>(segs->size());
   }
   ep.n_work = n_work;
+  ep.chunk = (int)std::max<uint64_t>(1, std::min<uint64_t>(8, n_work / ((uint64_t)ctx->n_ctas * 16)));
   ep.index_list = d_list;
   ep.counter = ctx->counter.as<unsigned long long>();
   ep.bp = ctx->bp.as<uint8_t>();
@@ -653,6 +658,11 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   ep.stage = ctx->stage_d.as<uint32_t>();
   ep.vbuf = ctx->vbuf.as<double>();
   ep.max_cells = ctx->max_cells;
+#ifdef AMP_PROFILE_PHASES
+  CK(ctx->phase.ensure(sizeof(unsigned long long) * 8));
+  CK(cudaMemsetAsync(ctx->phase.p, 0, sizeof(unsigned long long) * 8, ctx->stream));
+  ep.phase_cycles = ctx->phase.as<unsigned long long>();
+#endif
   ep.max_prog_cells = ctx->max_prog_cells;
   CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), ctx->stream));
   void* args[] = {&ep};
@@ -908,6 +918,16 @@ int amp_search_merge_topk_device(amp_ctx* ctx, const amp_record* d_in, int32_t n
   if (!ctx || !d_in || !d_out || n_in < 1 || k < 1 || k > 4096) return AMP_E_INVALID;
   CK(cudaSetDevice(ctx->device));
   return launch_merge(ctx, d_in, n_in, k, d_out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// Debug: per-phase cycle totals of the last run (AMP_PROFILE_PHASES builds;
+// zeros otherwise).  Not part of the public header.
+int amp_debug_phase_cycles(const amp_ctx* ctx, unsigned long long* out8) {
+  if (!ctx || !out8) return AMP_E_INVALID;
+  std::memset(out8, 0, 8 * sizeof(unsigned long long));
+  if (ctx->phase.p)
+    cudaMemcpy(out8, ctx->phase.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return AMP_OK;
 }
 
 int amp_search_last_stats(const amp_ctx* ctx_c, amp_stats* out) {

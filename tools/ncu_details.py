@@ -10,7 +10,7 @@ h = next(r)
 ix = [h.index(x) for x in ["Section Name", "Metric Name", "Metric Unit", "Metric Value"]]
 want = sys.argv[2].split(",") if len(sys.argv) > 2 else None
 for row in r:
-    if len(row) < len(h) or not row[ix[1]]:
+    if len(row) <= max(ix) or not row[ix[1]]:
         continue
     if want and not any(w.lower() in (row[ix[0]] + row[ix[1]]).lower() for w in want):
         continue
