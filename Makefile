@@ -31,3 +31,19 @@ clean:
 	$(MAKE) -f oracle/Makefile clean
 
 .PHONY: all lib oracle clean phases
+
+# C++ drop-in shim test: parplan_gpu::plan vs the reference parplan::plan in
+# one binary (reference sources compiled where they lie; needs /root/reference
+# at build time, the binary travels to the GPU box).
+REF ?= /root/reference/proj
+DROPIN := tests/cpp/build/test_drop_in
+drop-in: $(DROPIN)
+$(DROPIN): tests/cpp/test_drop_in.cpp $(PKG)/host/parplan_plan_gpu.cpp $(PKG)/host/parplan_plan_gpu.hpp include/amp_search.h $(LIB)
+	@if [ -d "$(REF)/src" ]; then \
+	  mkdir -p tests/cpp/build && \
+	  g++ -std=c++20 -O2 -ffp-contract=off -pthread -I$(REF)/include -Iinclude -I$(PKG)/host \
+	    -o $@ tests/cpp/test_drop_in.cpp $(PKG)/host/parplan_plan_gpu.cpp \
+	    $(addprefix $(REF)/src/,types.cpp cost_model.cpp pipeline_dp.cpp placement.cpp optimizer.cpp simulator.cpp) \
+	    -L$(PKG) -lamp_search -Wl,-rpath,'$$ORIGIN/../../../$(PKG)'; \
+	else echo "drop-in: $(REF) absent, using prebuilt $@"; fi
+.PHONY: drop-in

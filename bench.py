@@ -31,7 +31,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 SCENARIO = "hetero_cluster"
-DEFAULT_N_PER_GPU = 1_000_000
+DEFAULT_N_PER_GPU = 10_000_000
 TOPK = 10
 METRIC = "candidate strategies/sec"
 UNIT = "candidates/s"
@@ -44,10 +44,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n-per-gpu", type=int, default=DEFAULT_N_PER_GPU)
-    ap.add_argument("--cpu-sample", type=int, default=4000,
+    ap.add_argument("--cpu-sample", type=int, default=300000,
                     help="candidates in the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dense", action="store_true", help="skip the dense-DP comparison leg")
     return ap.parse_args()
 
 
@@ -152,9 +153,11 @@ def reference_arm(args):
     sc = load_scenario()
     n_total, P_ = workload(args.n_per_gpu, args.gpus)
     threads = os.cpu_count() or 1
+    # keep the whole K + W run to ~1-2 minutes of CPU time
+    per_step = max(1000, min(args.cpu_sample, args.cpu_sample * 8 // max(1, args.steps + args.warmup)))
     vals = []
     for i in range(args.warmup + args.steps):
-        v, dt, kind, th, ns = run_cpu_reference(sc, n_total, P_, args.cpu_sample, threads)
+        v, dt, kind, th, ns = run_cpu_reference(sc, n_total, P_, per_step, threads)
         if i >= args.warmup:
             vals.append(v)
     value = float(np.median(vals))
@@ -261,6 +264,10 @@ def our_arm(args):
     if not args.no_e2e:
         e2e = e2e_arm(args, enc, P_, lo, hi, n_total, world, rank, local, distributed)
 
+    dense = None
+    if world == 1 and not args.no_dense:
+        dense = dense_leg(enc, local)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -286,6 +293,8 @@ def our_arm(args):
         }
         if e2e:
             line["e2e"] = e2e
+        if dense:
+            line["dense_dp"] = dense
         if world == 1 and not args.no_cpu_baseline:
             v, dt, kind, th, ns = run_cpu_reference(sc, n_total, P_, args.cpu_sample, os.cpu_count() or 1)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": th, "kind": kind,
@@ -295,6 +304,34 @@ def our_arm(args):
     s.close()
     if distributed:
         dist.destroy_process_group()
+
+
+def dense_leg(enc, local, n=1_000_000):
+    """The reference's full-table DP on the same sweep (AMP_FLAG_DENSE_DP):
+    same results, ~36x more DP work; its FP64-pipe roofline is reported
+    separately from the production (pruned) path."""
+    import ctypes as C
+
+    from paper_2210_07297_b200 import _native as N
+    from paper_2210_07297_b200.planner import Searcher
+    P_ = -(-n // 70)
+    s = Searcher(enc, placements_per_class=P_, seed=0, device=local, dense_dp=True)
+    s.run(0, n, k=TOPK)
+    ms = []
+    for _ in range(3):
+        s.run(0, n, k=TOPK)
+        ms.append(s.stats()["kernel_ms"])
+    st = s.stats()
+    s.close()
+    peak = C.c_double()
+    pms = C.c_double()
+    N.check(N.load().amp_fp64_peak(local, C.byref(peak), C.byref(pms)))
+    k_ms = float(np.median(ms))
+    ach = st["fp64_ops"] / (k_ms * 1e-3) / 1e12
+    return {"value": n / (k_ms * 1e-3), "unit": UNIT, "candidates": n, "kernel_ms": k_ms,
+            "dp_inner": st["dp_inner"],
+            "roofline": {"bound": "fp64", "achieved": ach, "peak": peak.value / 1e12,
+                         "unit": "TFLOP/s", "frac": ach / (peak.value / 1e12)}}
 
 
 def e2e_arm(args, enc, P_, lo, hi, n_total, world, rank, local, distributed):

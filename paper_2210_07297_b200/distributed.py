@@ -1,0 +1,75 @@
+"""Multi-GPU search: one process per GPU, candidates sharded by index range.
+
+SURVEY.md §8(e): candidates are independent, so each rank evaluates a
+contiguous, work-weighted slice of the class-major index space
+(amp_search_partition) and keeps its local top-k on the device; the only
+exchange is one all-gather of the k records per rank (NCCL over NVLink on
+GPUs, gloo in the CPU tests) followed by a deterministic merge under the
+reference ranking key (failed, total, index) — identical for any world size.
+
+`search()` is written against two small hooks so the exchange logic is the
+same with the CUDA engine and with the CPU oracle used by the gloo tests.
+"""
+from __future__ import annotations
+
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+from .planner import RECORD_DTYPE, rank_order
+
+
+def merge_topk_host(records: np.ndarray, k: int) -> np.ndarray:
+    """Host merge under the rank_records key; drops empty slots."""
+    records = records[records["fail_code"] >= 0]
+    return records[rank_order(records)[:k]]
+
+
+def shard_bounds(n_total: int, world: int, weights: Optional[Sequence[int]] = None) -> List[int]:
+    """Equal-count contiguous split (the engine's amp_search_partition gives
+    the work-weighted one)."""
+    if weights is not None:
+        return list(weights)
+    return [n_total * r // world for r in range(world + 1)]
+
+
+def search_gpu(searcher, k: int, bounds: Sequence[int], rank: int, world: int, group=None):
+    """Evaluate this rank's slice on the GPU; all-gather the device top-k
+    (NCCL) and merge on the device.  Returns the global top-k (host)."""
+    import torch
+    import torch.distributed as dist
+
+    stream = torch.cuda.current_stream()
+    local = torch.empty(k * RECORD_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    searcher.run_device(bounds[rank], bounds[rank + 1], k, local.data_ptr(), stream.cuda_stream)
+    if world == 1:
+        out = local
+    else:
+        gathered = torch.empty(world * k * RECORD_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+        dist.all_gather_into_tensor(gathered, local, group=group)
+        out = torch.empty_like(local)
+        searcher.merge_device(gathered.data_ptr(), world * k, k, out.data_ptr(), stream.cuda_stream)
+    recs = np.frombuffer(out.cpu().numpy().tobytes(), dtype=RECORD_DTYPE)
+    return recs[recs["fail_code"] >= 0]
+
+
+def search_host(evaluate: Callable[[int, int], np.ndarray], k: int, bounds: Sequence[int], rank: int,
+                world: int, group=None) -> np.ndarray:
+    """Same exchange with a host evaluator (tests / gloo): each rank ranks its
+    slice, all-gathers k fixed-size records and merges."""
+    import torch
+    import torch.distributed as dist
+
+    recs = evaluate(bounds[rank], bounds[rank + 1])
+    local = np.zeros(k, dtype=RECORD_DTYPE)
+    local["fail_code"] = -1
+    local["index"] = np.iinfo(np.uint64).max
+    top = merge_topk_host(recs, k)
+    local[: len(top)] = top
+    t = torch.from_numpy(np.frombuffer(local.tobytes(), dtype=np.uint8).copy())
+    if world == 1:
+        return merge_topk_host(local, k)
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t, group=group)
+    allr = np.frombuffer(b"".join(o.numpy().tobytes() for o in out), dtype=RECORD_DTYPE)
+    return merge_topk_host(allr, k)

@@ -1,0 +1,71 @@
+"""Multi-process exchange of the sharded search on CPU (gloo, world_size 2):
+each rank evaluates its index range (oracle evaluator), the k best records
+are all-gathered and merged; the result must equal the single-process top-k
+for any split (output identical for any n_gpus)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from conftest import ROOT, scenario
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, bounds, k, out_path):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch.distributed as dist
+
+    from conftest import scenario as sc_
+    from oracle import bindings as B
+    from paper_2210_07297_b200 import distributed as Dd
+    from paper_2210_07297_b200 import problem as P
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sc = sc_("hetero_model")
+    enc = P.EncodedProblem.from_scenario(sc)
+    o = B.Oracle(enc, placements_per_class=6, seed=9)
+
+    def evaluate(lo, hi):
+        recs, _ = o.run(lo, hi, threads=2, details=False)
+        return recs
+
+    top = Dd.search_host(evaluate, k, bounds, rank, world)
+    if rank == 0:
+        np.save(out_path, top)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("split", ["even", "skewed"])
+def test_gloo_two_rank_merge_matches_single_process(tmp_path, split):
+    from oracle import bindings as B
+    from paper_2210_07297_b200 import distributed as Dd
+    from paper_2210_07297_b200 import problem as P
+
+    sc = scenario("hetero_model")
+    enc = P.EncodedProblem.from_scenario(sc)
+    o = B.Oracle(enc, placements_per_class=6, seed=9)
+    n = o.num_candidates
+    recs, _ = o.run(0, n, threads=4, details=False)
+    k = 12
+    want = Dd.merge_topk_host(recs, k)
+    bounds = [0, n // 2, n] if split == "even" else [0, 37, n]
+    out = str(tmp_path / "top.npy")
+    mp.spawn(_worker, args=(2, _free_port(), bounds, k, out), nprocs=2, join=True)
+    got = np.load(out)
+    assert got["index"].tolist() == want["index"].tolist()
+    assert np.array_equal(got["total"], want["total"])
