@@ -19,10 +19,6 @@ $(LIB): $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> $(PKG)/csrc/ptxas.log || (cat $(PKG)/csrc/ptxas.log; exit 1)
 	@grep -E "Compiling entry|Used|spill" $(PKG)/csrc/ptxas.log | sed 's/^ptxas info *: //' | head -40
 
-# instrumented build: per-phase clock64 totals (amp_debug_phase_cycles)
-phases: $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -DAMP_PROFILE_PHASES -shared -o $(PKG)/libamp_search_phases.so $(SRCS) 2> /dev/null
-
 oracle:
 	$(MAKE) -f oracle/Makefile all
 
@@ -30,7 +26,7 @@ clean:
 	rm -f $(LIB) $(PKG)/csrc/ptxas.log
 	$(MAKE) -f oracle/Makefile clean
 
-.PHONY: all lib oracle clean phases
+.PHONY: all lib oracle clean
 
 # C++ drop-in shim test: parplan_gpu::plan vs the reference parplan::plan in
 # one binary (reference sources compiled where they lie; needs /root/reference

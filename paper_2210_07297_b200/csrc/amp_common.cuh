@@ -53,6 +53,7 @@ struct Segment {
 
 struct WEnt;     // per-stage cut table entry (amp_kernels.cuh)
 struct ProgDev;  // pruned-DP program (amp_dp_sparse.cuh)
+struct CandWork; // per-candidate pipeline record (amp_pipeline.cuh)
 
 struct EvalParams {
   // problem
@@ -110,7 +111,15 @@ struct EvalParams {
   const uint16_t* preds;
   const uint32_t* stage;
   double* vbuf;               // global value arrays when not in smem
-  unsigned long long* phase_cycles;  // [8], AMP_PROFILE_PHASES builds only
+  // pipeline chunk: work items [t0, t0 + n_chunk) of the run
+  uint64_t t0;
+  uint64_t n_chunk;
+  CandWork* work;             // [n_chunk]
+  int32_t* placeb;            // [n_chunk][D] rank -> device
+  double* bwqb;               // [n_chunk][max_pp] stage-boundary bandwidths
+  uint8_t* cutsb;             // [n_chunk][max_pp + 1]
+  int32_t first_chunk;        // K_est: start CTA top-k lists empty
+  int32_t pad3;
   int32_t max_cells;          // max_j |N_j| over programs
   int32_t max_prog_cells;     // max sum_j |N_j| over programs
 };

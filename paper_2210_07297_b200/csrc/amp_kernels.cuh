@@ -461,39 +461,6 @@ struct EdgeFromBandwidth {  // placement_edge_cost (optimizer.cpp:130-139)
   __device__ double operator()(int cut, int q) const { return act[cut - 1] * mbs / bwq[q]; }
 };
 
-// Optional per-phase cycle accounting (build with -DAMP_PROFILE_PHASES):
-// thread 0 of every CTA accumulates clock64 deltas into p.phase_cycles[8].
-#ifdef AMP_PROFILE_PHASES
-#define PHASE(id)                                                         \
-  do {                                                                    \
-    if (tid == 0) {                                                       \
-      const long long now_ = clock64();                                   \
-      atomicAdd(&p.phase_cycles[id], (unsigned long long)(now_ - t_mark)); \
-      t_mark = now_;                                                      \
-    }                                                                     \
-  } while (0)
-#else
-#define PHASE(id) \
-  do {            \
-  } while (0)
-#endif
-
-struct EvalShared {
-  int cand_t;
-  int done;
-  uint64_t index, out_pos, pl;
-  uint64_t t_next, t_end;  // CTA-local work chunk
-  int seg;                 // current segment (sweep mode)
-  int cls, pair;           // class/pair cached below (-1: none)
-  ClassDev cl;
-  PairDev pr;
-  int n_top;
-  int fail_code, fail_layer;
-  double fail_value;
-  double pipeline, dpsync;
-  int best_r;
-};
-
 __device__ void topk_insert(amp_record* list, int& n, int k, const amp_record& r) {
   if (n == k && !rank_less(r, list[k - 1])) return;
   int pos = n < k ? n : k - 1;
@@ -503,548 +470,6 @@ __device__ void topk_insert(amp_record* list, int& n, int k, const amp_record& r
   }
   list[pos] = r;
   if (n < k) ++n;
-}
-
-// MODE selects the DP implementation and where its working set lives
-// (compile-time so the compiler emits LDS/STS instead of generic loads):
-//   kDenseSS/SG/GS/GG  full tolerance-indexed table; stage slice / cut table
-//                      in (S)hared or (G)lobal memory
-//   kSparseS/G         pruned program (amp_dp_sparse.cuh); value arrays and
-//                      backpointers in shared / global memory
-enum : int { kDenseSS = 0, kDenseSG = 1, kDenseGS = 2, kDenseGG = 3, kSparseS = 4, kSparseG = 5 };
-
-template <int MODE>
-__global__ void __launch_bounds__(MODE >= kSparseS ? 256 : kEvalThreads, MODE >= kSparseS ? 4 : 2)
-    k_evaluate(EvalParams p) {
-  constexpr bool SPARSE = MODE >= kSparseS;
-  constexpr bool SLICE_SMEM = MODE == kDenseSS || MODE == kDenseSG;
-  constexpr bool W_SMEM = MODE == kDenseSS || MODE == kDenseGS;
-  constexpr bool V_SMEM = MODE == kSparseS;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ EvalShared sh;
-  __shared__ double red[32];
-  __shared__ int redi[64];
-  const int L = p.L, D = p.D, LP = L + 1, tid = threadIdx.x, nt = blockDim.x;
-  const int maxM = p.max_M, maxpp = p.max_pp;
-  // dynamic smem carve-up (host mirror: eval_smem_bytes in amp_search.cu)
-  unsigned char* sp = smem_raw;
-  double* C = nullptr;
-  WEnt* W = nullptr;
-  double *V0 = nullptr, *V1 = nullptr;
-  uint8_t* bp = p.bp + (size_t)blockIdx.x * p.bp_stride;
-  if (SPARSE) {
-    if (V_SMEM) {
-      V0 = reinterpret_cast<double*>(sp);
-      sp += sizeof(double) * 2 * (size_t)p.max_cells;
-      bp = reinterpret_cast<uint8_t*>(sp);
-      sp += (p.max_prog_cells + 15) & ~15;
-    } else {
-      V0 = p.vbuf + (size_t)blockIdx.x * 2 * p.max_cells;
-    }
-    V1 = V0 + p.max_cells;
-  } else {
-    if (SLICE_SMEM) {
-      C = reinterpret_cast<double*>(sp);
-      sp += sizeof(double) * (size_t)LP * maxM;
-    } else {
-      C = p.slice + (size_t)blockIdx.x * p.slice_stride;
-    }
-    if (W_SMEM) {
-      W = reinterpret_cast<WEnt*>(sp);
-      sp += sizeof(WEnt) * (size_t)LP * L;
-    } else {
-      W = p.wtab + (size_t)blockIdx.x * LP * L;
-    }
-  }
-  double* Dm = reinterpret_cast<double*>(sp);
-  sp += sizeof(double) * maxM;
-  double* Pf = reinterpret_cast<double*>(sp);
-  sp += sizeof(double) * LP;
-  sp = smem_raw + ((sp - smem_raw + 15) & ~15);
-  double* E = reinterpret_cast<double*>(sp);  // dense: E[L]; sparse: 2 x double2[L]
-  sp += sizeof(double) * 4 * L;
-  double* bwq = reinterpret_cast<double*>(sp);
-  sp += sizeof(double) * maxpp;
-  double* st = reinterpret_cast<double*>(sp);
-  sp += sizeof(double) * maxpp;
-  double* ebuf = reinterpret_cast<double*>(sp);  // warp estimate scratch
-  sp += sizeof(double) * 32;
-  double* spar = reinterpret_cast<double*>(sp);  // per-stage parameter sums
-  sp += sizeof(double) * maxpp;
-  // |D| <= 32: the bandwidth matrix lives in smem for the whole kernel
-  double* bwS = reinterpret_cast<double*>(sp);
-  if (D <= 32) sp += sizeof(double) * D * D;
-  amp_record* topS = reinterpret_cast<amp_record*>(sp);  // CTA top-k (k <= 32)
-  if (p.k <= 32) sp += sizeof(amp_record) * p.k;
-  int* cuts = reinterpret_cast<int*>(sp);
-  sp += sizeof(int) * (maxpp + 2);
-  int* place = reinterpret_cast<int*>(sp);
-  sp += sizeof(int) * D;
-  // (integer offset from smem_raw keeps the shared address space visible)
-  uint16_t* seg = reinterpret_cast<uint16_t*>(smem_raw + ((sp - smem_raw + 15) & ~15));
-
-  amp_record* const gtop = p.cta_topk + (size_t)blockIdx.x * p.k;
-  amp_record* mytop = p.k <= 32 ? topS : gtop;
-  if (tid == 0) sh.n_top = 0;
-  const double* BW = p.bw;
-  if (D <= 32) {
-    for (int x = tid; x < D * D; x += nt) bwS[x] = BW[x];
-    BW = bwS;
-  }
-
-  long long t_mark = clock64();
-  (void)t_mark;
-  if (tid == 0) {
-    sh.t_next = sh.t_end = 0;
-    sh.seg = 0;
-    sh.cls = -1;
-    sh.pair = -1;
-  }
-  for (;;) {
-    if (tid == 0) {
-      // work items are fetched `chunk` at a time to amortise the atomic
-      if (sh.t_next >= sh.t_end) {
-        const unsigned long long t0 = atomicAdd(p.counter, (unsigned long long)p.chunk);
-        sh.t_next = t0;
-        sh.t_end = t0 + p.chunk < p.n_work ? t0 + p.chunk : p.n_work;
-      }
-      const uint64_t t = sh.t_next++;
-      sh.done = t >= p.n_work;
-      if (!sh.done) {
-        int c;
-        if (p.index_list) {
-          sh.index = p.index_list[t];
-          sh.out_pos = t;
-          c = (int)(sh.index / p.P);
-          sh.pl = sh.index % p.P;
-        } else {
-          int lo = sh.seg;  // usually the same segment as the previous item
-          if (!(p.segs[lo].offset <= t && t < p.segs[lo].offset + p.segs[lo].count)) {
-            lo = 0;
-            int hi = p.n_segs - 1;  // last segment with offset <= t
-            while (lo < hi) {
-              const int mid = (lo + hi + 1) >> 1;
-              if (p.segs[mid].offset <= t) lo = mid;
-              else hi = mid - 1;
-            }
-            sh.seg = lo;
-          }
-          const Segment sg = p.segs[lo];
-          const uint64_t d = t - sg.offset;
-          sh.index = sg.first + d;
-          sh.out_pos = sg.out + d;
-          sh.pl = sg.p0 + d;
-          c = (int)sg.cls;
-        }
-        if (c != sh.cls) {  // class/pair tables change only between segments
-          sh.cls = c;
-          sh.cl = p.cls[c];
-          sh.pr = p.pairs[sh.cl.pair];
-        }
-      }
-      sh.fail_code = 0;
-      sh.fail_layer = -1;
-      sh.fail_value = 0.0;
-    }
-    __syncthreads();
-    if (sh.done) break;
-    const uint64_t index = sh.index;
-    const int c = sh.cls;
-    const uint64_t pl = sh.pl;
-    const ClassDev cl = sh.cl;
-    const int pp = cl.pp, dp = cl.dp, tmp = cl.tmp, mbs = cl.mbs, gas = cl.gas;
-    const PairDev pr = sh.pr;
-    const int M = pr.M;
-    double total = CUDART_NAN;
-    bool ok = false;
-
-    PHASE(0);  // fetch + decode (incl. barrier)
-    if (pp > L) {  // optimizer.cpp:149-152
-      if (tid == 0) sh.fail_code = AMP_FAIL_PP_GT_L;
-    } else if (pr.fail_code) {  // segment_times: first failing layer
-      if (tid == 0) {
-        sh.fail_code = pr.fail_code;
-        sh.fail_layer = pr.fail_layer;
-        sh.fail_value = pr.fail_value;
-      }
-    } else {
-      ok = true;
-    }
-    __syncthreads();
-    if (ok) {
-      // ---- placement: heuristic order, Fisher-Yates for p >= 1 ----------
-      if (D <= 32) {
-        // warp 0 keeps the device order in registers (lane r holds rank r);
-        // every lane walks the splitmix64 chain and keeps the draw of its own
-        // step k, then the D-1 swaps are applied as lane permutations.
-        if (tid < 32) {
-          int v = tid < D ? p.base_order[tid] : -1;
-          if (pl != 0) {
-            // lane kk keeps the draw of step kk, then reduces it once:
-            // r mod d == ((hi mod d) * (2^32 mod d) + (lo mod d)) mod d
-            uint64_t r = splitmix64(p.seed ^ pl), mine = 0;
-            for (int kk = D - 1; kk >= 1; --kk) {
-              mine = tid == kk ? r : mine;
-              r = splitmix64(r);
-            }
-            const uint32_t d = (uint32_t)tid + 1u;
-            const uint32_t hi = (uint32_t)(mine >> 32) % d, lo = (uint32_t)mine % d;
-            const uint32_t t32 = (uint32_t)((1ull << 32) % d);
-            const int jk = (int)((hi * t32 + lo) % d);
-            for (int kk = D - 1; kk >= 1; --kk) {
-              const int jj = __shfl_sync(0xffffffffu, jk, kk);
-              const int src = tid == kk ? jj : (tid == jj ? kk : tid);
-              v = __shfl_sync(0xffffffffu, v, src);
-            }
-          }
-          if (tid < D) place[tid] = v;
-        }
-      } else {
-        for (int x = tid; x < D; x += nt) place[x] = p.base_order[x];
-        __syncthreads();
-        if (pl != 0 && tid == 0) {
-          uint64_t r = splitmix64(p.seed ^ pl);
-          for (int kk = D - 1; kk >= 1; --kk) {
-            const int jj = (int)(r % (uint64_t)(kk + 1));
-            const int t = place[kk];
-            place[kk] = place[jj];
-            place[jj] = t;
-            r = splitmix64(r);
-          }
-        }
-      }
-      PHASE(1);  // placement
-      // ---- DP inputs ---------------------------------------------------
-      if (sh.pair != cl.pair) {  // Dm/Pf (and the dense seg table) persist in smem
-        const double* gdom = p.domain + (size_t)cl.pair * p.nv_stride;
-        for (int x = tid; x < M; x += nt) Dm[x] = gdom[x];
-        for (int x = tid; x < LP; x += nt) Pf[x] = p.prefix[(size_t)cl.pair * LP + x];
-        if (!SPARSE) {
-          const uint16_t* gseg = p.seg + (size_t)cl.pair * LP * LP;
-          for (int x = tid; x < LP * LP; x += nt) seg[x] = gseg[x];
-        }
-      }
-      __syncthreads();
-      if (tid == 0) sh.pair = cl.pair;
-      // min_edge_bandwidth per stage boundary (cost_model.cpp:164-174)
-      for (int q = tid; q < pp - 1; q += nt) {
-        double b = CUDART_INF;
-        for (int r = 0; r < dp; ++r)
-          for (int s = 0; s < tmp; ++s)
-            b = std_min(b, BW[(size_t)place[(q * dp + r) * tmp + s] * D +
-                                place[((q + 1) * dp + r) * tmp + s]]);
-        bwq[q] = b;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        for (int q = 0; q + 1 < pp; ++q)
-          if (!(bwq[q] > 0)) {  // p2p_time throws inside the DP's edge fn
-            sh.fail_code = AMP_FAIL_P2P_BANDWIDTH;
-            sh.fail_value = bwq[q];
-            break;
-          }
-      }
-      __syncthreads();
-      ok = sh.fail_code == 0;
-    }
-    if (ok) {
-      PHASE(2);  // tables, bandwidths, checks
-      EdgeFromBandwidth ef{p.act, bwq, mbs};
-      if (SPARSE) {
-        const ProgDev pg = p.progs[p.class_prog[c]];
-        sparse_solve(L, pp, gas, Pf, Dm, pg, p.cells, p.cellpred, p.preds, p.stage, ef, V0, V1,
-                     reinterpret_cast<double2*>(E), reinterpret_cast<double2*>(E) + L, bp, cuts);
-      } else {
-        dp_solve(L, pp, gas, M, Pf, Dm, seg, ef, C, W, E, pr.monotone != 0, bp, cuts);
-      }
-      PHASE(3);  // DP
-      // ---- per-device parameter ceiling (optimizer.cpp:159-169) ---------
-      const double* tl = p.times + (size_t)cl.pair * L;
-      for (int j = tid; j < pp; j += nt) {
-        double sum = 0.0, ps = 0.0;  // stage_time (cost_model.cpp:88-98),
-        for (int l = cuts[j]; l < cuts[j + 1]; ++l) {  // params_in_range (types.cpp:34-40)
-          sum += tl[l];
-          ps += p.param[l];
-        }
-        st[j] = sum;
-        spar[j] = ps;
-      }
-      __syncthreads();
-      if (tid == 0 && p.has_ceiling) {
-        double worst = 0.0;
-        for (int j = 0; j < pp; ++j) worst = std_max(worst, spar[j] / tmp);
-        if (worst > p.ceiling) sh.fail_code = AMP_FAIL_CEILING;
-      }
-      __syncthreads();
-      ok = sh.fail_code == 0;
-    }
-    if (ok) {
-      PHASE(4);  // stage times + ceiling
-      // ---- estimate: pipeline term (cost_model.cpp:176-212) -------------
-      double slowest_stage = st[0];  // std::max_element: first maximum
-      for (int j = 1; j < pp; ++j)
-        if (slowest_stage < st[j]) slowest_stage = st[j];
-      const double g1 = (double)(gas - 1);
-      if (D <= 32) {
-        // one warp: lane r = replica r (dp <= 32); lane (g, r1) = dp-group g,
-        // first member r1 (pp * tmp * dp == D <= 32)
-        if (tid < 32) {
-          double tr = -CUDART_INF;
-          int rr = -1;
-          // replica_edge_times (145-162): lane (r, q) computes edge q of replica
-          // r (dp * (pp - 1) < D <= 32), then lane r sums them in order
-          const int ne = pp - 1;
-          if (tid < dp * ne) {
-            const int r = tid / ne, q = tid - r * ne;
-            const int cut = cuts[q + 1];
-            const double volume = p.act[cut - 1] * mbs;
-            double b = CUDART_INF;
-            for (int s = 0; s < tmp; ++s)
-              b = std_min(b, BW[(size_t)place[(q * dp + r) * tmp + s] * D +
-                                  place[((q + 1) * dp + r) * tmp + s]]);
-            ebuf[tid] = volume / b;
-          }
-          __syncwarp();
-          if (tid < dp) {
-            double sum = 0.0;
-            for (int q = 0; q < ne; ++q) sum = sum + ebuf[tid * ne + q];
-            for (int j = 0; j < pp; ++j) sum = sum + st[j];
-            const double t = g1 * slowest_stage + sum;  // pipeline_time (100-120)
-            if (t > tr) {  // NaN never becomes the maximum
-              tr = t;
-              rr = tid;
-            }
-          }
-          for (int o = 16; o > 0; o >>= 1) {  // max, lowest replica on ties
-            const double ov = __shfl_xor_sync(0xffffffffu, tr, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, rr, o);
-            if (oi >= 0 && (rr < 0 || ov > tr || (ov == tr && oi < rr))) {
-              tr = ov;
-              rr = oi;
-            }
-          }
-          // dpsync_time (122-143): group g = (stage j, shard s)
-          double worst = 0.0;
-          int bad_group = 0x7fffffff;
-          double bad_value = 0.0;
-          if (dp != 1) {
-            const int ngroups = pp * tmp;
-            double b = CUDART_INF;
-            const int g = tid / dp, r1 = tid % dp;
-            if (g < ngroups) {  // make_comm_group (23-38): pairwise minimum
-              const int j = g / tmp, s = g % tmp;
-              const int d1 = place[(j * dp + r1) * tmp + s];
-              for (int r2 = r1 + 1; r2 < dp; ++r2)
-                b = std_min(b, BW[(size_t)d1 * D + place[(j * dp + r2) * tmp + s]]);
-            }
-            // minimum over the dp lanes of each group (min is exact)
-            for (int o = 1; o < dp; o <<= 1) {
-              const double ob = __shfl_down_sync(0xffffffffu, b, o);
-              if (r1 + o < dp) b = std_min(b, ob);
-            }
-            if (g < ngroups && r1 == 0) {
-              const int j = g / tmp;
-              const double message = spar[j] * p.bpp / tmp;
-              if (!(b > 0)) {
-                bad_group = g;
-                bad_value = b;
-              } else {
-                worst = 2.0 * (double)(dp - 1) * message / ((double)dp * b);
-              }
-            }
-            for (int o = 16; o > 0; o >>= 1) {
-              worst = std_max(worst, __shfl_xor_sync(0xffffffffu, worst, o));
-              const int og = __shfl_xor_sync(0xffffffffu, bad_group, o);
-              const double ov = __shfl_xor_sync(0xffffffffu, bad_value, o);
-              if (og < bad_group) {
-                bad_group = og;
-                bad_value = ov;
-              }
-            }
-          }
-          if (tid == 0) {
-            if (bad_group != 0x7fffffff) {
-              sh.fail_code = AMP_FAIL_ALLREDUCE_BANDWIDTH;
-              sh.fail_value = bad_value;
-            }
-            sh.pipeline = tr;
-            sh.dpsync = worst;
-            sh.best_r = rr;
-          }
-        }
-        __syncthreads();
-        ok = sh.fail_code == 0;
-        total = sh.pipeline + sh.dpsync;
-      } else {
-        double my_best = -CUDART_INF;
-        int my_r = -1;
-        for (int r = tid; r < dp; r += nt) {
-          double sum = 0.0;
-          for (int q = 0; q + 1 < pp; ++q) {  // replica_edge_times (145-162)
-            const int cut = cuts[q + 1];
-            const double volume = p.act[cut - 1] * mbs;
-            double b = CUDART_INF;
-            for (int s = 0; s < tmp; ++s)
-              b = std_min(b, BW[(size_t)place[(q * dp + r) * tmp + s] * D +
-                                  place[((q + 1) * dp + r) * tmp + s]]);
-            sum = sum + volume / b;
-          }
-          for (int j = 0; j < pp; ++j) sum = sum + st[j];
-          const double tr = g1 * slowest_stage + sum;  // pipeline_time (100-120)
-          if (tr > my_best) {  // strict '>' over ascending r: first maximum
-            my_best = tr;
-            my_r = r;
-          }
-        }
-        block_argmax(my_best, my_r, red, redi);
-        // ---- dpsync_time (122-143) ---------------------------------------
-        double worst = 0.0;
-        int bad_group = 0x7fffffff;
-        double bad_value = 0.0;
-        if (dp != 1) {
-          const int ngroups = pp * tmp;
-          if (dp <= 8) {
-            // one thread per (stage, shard) group
-            for (int g = tid; g < ngroups; g += nt) {
-              const int j = g / tmp, s = g % tmp;
-              double sp_ = 0.0;
-              for (int l = cuts[j]; l < cuts[j + 1]; ++l) sp_ += p.param[l];
-              const double message = sp_ * p.bpp / tmp;
-              double b = CUDART_INF;  // make_comm_group (23-38)
-              for (int r1 = 0; r1 < dp; ++r1)
-                for (int r2 = r1 + 1; r2 < dp; ++r2)
-                  b = std_min(b, BW[(size_t)place[(j * dp + r1) * tmp + s] * D +
-                                      place[(j * dp + r2) * tmp + s]]);
-              if (!(b > 0)) {
-                if (g < bad_group) {
-                  bad_group = g;
-                  bad_value = b;
-                }
-              } else {
-                worst = std_max(worst, 2.0 * (double)(dp - 1) * message / ((double)dp * b));
-              }
-            }
-          } else {
-            // block-cooperative pair minimum per group
-            for (int g = 0; g < ngroups; ++g) {
-              const int j = g / tmp, s = g % tmp;
-              double b = CUDART_INF;
-              for (int x = tid; x < dp * dp; x += nt) {
-                const int r1 = x / dp, r2 = x - r1 * dp;
-                if (r1 < r2)
-                  b = std_min(b, BW[(size_t)place[(j * dp + r1) * tmp + s] * D +
-                                      place[(j * dp + r2) * tmp + s]]);
-              }
-              b = block_min(b, red);
-              if (tid == 0) {
-                double sp_ = 0.0;
-                for (int l = cuts[j]; l < cuts[j + 1]; ++l) sp_ += p.param[l];
-                const double message = sp_ * p.bpp / tmp;
-                if (!(b > 0)) {
-                  if (g < bad_group) {
-                    bad_group = g;
-                    bad_value = b;
-                  }
-                } else {
-                  worst = std_max(worst, 2.0 * (double)(dp - 1) * message / ((double)dp * b));
-                }
-              }
-            }
-          }
-        }
-        // reduce worst (max, NaN-free) and first bad group
-        {
-          double w2 = -worst;
-          w2 = block_min(w2, red);
-          worst = -w2;
-          const int bg = block_min_int(bad_group, redi);
-          if (bg != 0x7fffffff) {
-            if (bad_group == bg) {
-              sh.fail_code = AMP_FAIL_ALLREDUCE_BANDWIDTH;
-              sh.fail_value = bad_value;
-            }
-          }
-          if (tid == 0) {
-            sh.pipeline = my_best;
-            sh.dpsync = worst;
-            sh.best_r = my_r;
-          }
-          __syncthreads();
-          ok = sh.fail_code == 0;
-          total = sh.pipeline + sh.dpsync;
-        }
-      }
-      }
-    PHASE(5);  // estimate
-    // ---- record ---------------------------------------------------------
-    if (tid == 0) {
-      amp_record rec;
-      rec.index = index;
-      rec.pp = pp;
-      rec.dp = dp;
-      rec.tmp = tmp;
-      rec.mbs = mbs;
-      rec.fail_code = sh.fail_code;
-      rec.fail_layer = sh.fail_layer;
-      rec.fail_value = sh.fail_value;
-      if (ok) {
-        rec.total = total;
-        rec.pipeline_time = sh.pipeline;
-        rec.dpsync_time = sh.dpsync;
-      } else {
-        rec.total = rec.pipeline_time = rec.dpsync_time = CUDART_NAN;
-      }
-      topk_insert(mytop, sh.n_top, p.k, rec);
-      if (p.all) p.all[sh.out_pos] = rec;
-    }
-    if (p.all_cuts) {
-      int32_t* o = p.all_cuts + sh.out_pos * (maxpp + 1);
-      for (int q = tid; q <= maxpp; q += nt) o[q] = (ok && q <= pp) ? cuts[q] : -1;
-    }
-    if (p.all_stage) {
-      double* o = p.all_stage + sh.out_pos * maxpp;
-      for (int q = tid; q < maxpp; q += nt) o[q] = (ok && q < pp) ? st[q] : CUDART_NAN;
-    }
-    if (p.all_edge) {
-      double* o = p.all_edge + sh.out_pos * maxpp;
-      const int r = sh.best_r;
-      for (int q = tid; q < maxpp; q += nt) {
-        double v = CUDART_NAN;
-        if (ok && q + 1 < pp) {
-          const int cut = cuts[q + 1];
-          double b = CUDART_INF;
-          for (int s = 0; s < tmp; ++s)
-            b = std_min(b, BW[(size_t)place[(q * dp + r) * tmp + s] * D +
-                                place[((q + 1) * dp + r) * tmp + s]]);
-          v = p.act[cut - 1] * mbs / b;
-        }
-        o[q] = v;
-      }
-    }
-    if (p.all_place) {
-      int32_t* o = p.all_place + sh.out_pos * D;
-      const bool placed = ok;  // failed records keep a default placement
-      for (int x = tid; x < D; x += nt) o[x] = placed ? place[x] : -1;
-    }
-    __syncthreads();
-    PHASE(6);  // record + top-k + barrier
-  }
-  PHASE(7);
-  // pad the CTA list to k entries
-  if (tid == 0) {
-    if (mytop != gtop)
-      for (int x = 0; x < sh.n_top; ++x) gtop[x] = mytop[x];
-    for (int x = sh.n_top; x < p.k; ++x) {
-      amp_record e;
-      e.index = ~0ull;
-      e.total = e.pipeline_time = e.dpsync_time = CUDART_NAN;
-      e.pp = e.dp = e.tmp = e.mbs = 0;
-      e.fail_code = -1;
-      e.fail_layer = -1;
-      e.fail_value = 0.0;
-      gtop[x] = e;
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------

@@ -18,6 +18,7 @@
 
 #include "amp_common.cuh"
 #include "amp_kernels.cuh"
+#include "amp_pipeline.cuh"
 
 using namespace amp;
 
@@ -93,7 +94,10 @@ struct amp_ctx {
   std::vector<double> prog_inner;  // inner iterations per program
   int max_cells = 1, max_prog_cells = 1;
   size_t v_stride = 0;
-  DevBuf progs_d, stage_d, class_prog_d, cells, cellpred, preds, vbuf, phase;
+  DevBuf progs_d, stage_d, class_prog_d, cells, cellpred, preds, vbuf;
+  DevBuf c_work, c_place, c_bwq, c_cuts;  // pipeline chunk buffers
+  uint64_t chunk = 1;
+  int est_ctas = 1, sms = 148, launches = 0;
   amp_stats stats{};
 };
 
@@ -464,11 +468,10 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
       }
 
   // ---- evaluate kernel launch shape -------------------------------------
-  size_t small = 16 + 32 * sizeof(double) + sizeof(double) * ctx->max_pp +
-                 (D <= 32 ? sizeof(double) * D * D : 0) + sizeof(amp_record) * 32 +
-                 sizeof(double) * ctx->max_M + sizeof(double) * LP + 4 * sizeof(double) * L +
-                 2 * sizeof(double) * ctx->max_pp + sizeof(int) * (ctx->max_pp + 2) +
-                 sizeof(int) * D;
+  // K_dp smem (mirror of the carve-up in amp_pipeline.cuh k_dp)
+  size_t small = 16 + sizeof(double) * ctx->max_M + sizeof(double) * LP +
+                 4 * sizeof(double) * L + sizeof(double) * ctx->max_pp +
+                 sizeof(int) * (ctx->max_pp + 2);
   small = (small + 15) & ~size_t(15);
   const size_t w_b = sizeof(WEnt) * (size_t)LP * L;
   int mode;
@@ -499,12 +502,9 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
     ctx->v_stride = 0;
   }
   if (ctx->smem_bytes > 227 * 1024) return fail(ctx, AMP_E_UNSUPPORTED, "shared memory budget");
-  static const void* const kModes[] = {(const void*)k_evaluate<kDenseSS>,
-                                       (const void*)k_evaluate<kDenseSG>,
-                                       (const void*)k_evaluate<kDenseGS>,
-                                       (const void*)k_evaluate<kDenseGG>,
-                                       (const void*)k_evaluate<kSparseS>,
-                                       (const void*)k_evaluate<kSparseG>};
+  static const void* const kModes[] = {(const void*)k_dp<kDenseSS>, (const void*)k_dp<kDenseSG>,
+                                       (const void*)k_dp<kDenseGS>, (const void*)k_dp<kDenseGG>,
+                                       (const void*)k_dp<kSparseS>, (const void*)k_dp<kSparseG>};
   ctx->mode = mode;
   ctx->eval_fn = kModes[mode];
   CK(cudaFuncSetAttribute(ctx->eval_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -522,6 +522,12 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   if (per_cta && (size_t)n_ctas * per_cta > cap) n_ctas = std::max<size_t>(1, cap / per_cta);
   if (ctx->max_ctas_cfg > 0) n_ctas = std::min(n_ctas, ctx->max_ctas_cfg);
   ctx->n_ctas = n_ctas;
+  ctx->sms = prop.multiProcessorCount;
+  ctx->est_ctas = prop.multiProcessorCount * 4;  // 32 estimate warps per SM
+  // chunk size: keep the per-chunk buffers within ~256 MB
+  const size_t per_item = sizeof(CandWork) + sizeof(int32_t) * D + sizeof(double) * ctx->max_pp +
+                          (ctx->max_pp + 1);
+  ctx->chunk = std::max<uint64_t>(1024, std::min<uint64_t>(1ull << 20, (256ull << 20) / per_item));
   CK(ctx->bp.ensure(ctx->bp_stride * n_ctas + 16));
   if (ctx->slice_stride) CK(ctx->slice.ensure(sizeof(double) * ctx->slice_stride * n_ctas));
   if (!sparse && !ctx->w_in_smem) CK(ctx->wtab.ensure(w_b * n_ctas));
@@ -588,6 +594,9 @@ void account(amp_ctx* ctx, uint64_t begin, uint64_t end, const uint64_t* list, i
 }
 
 // Launch K1+K2 over either a segment list or an explicit index list.
+// Evaluate n_work items (segment list or explicit index list) as a pipeline
+// of chunks: K_place -> K_dp -> K_est per chunk (amp_pipeline.cuh).  CTA
+// top-k lists of K_est persist across chunks in ctx->cta_topk.
 int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64_t* d_list,
                     uint64_t n_work, int32_t k, bool want_all, bool want_details,
                     bool want_place) {
@@ -622,7 +631,6 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     ep.n_segs = static_cast<int32_t>(segs->size());
   }
   ep.n_work = n_work;
-  ep.chunk = (int)std::max<uint64_t>(1, std::min<uint64_t>(8, n_work / ((uint64_t)ctx->n_ctas * 16)));
   ep.index_list = d_list;
   ep.counter = ctx->counter.as<unsigned long long>();
   ep.bp = ctx->bp.as<uint8_t>();
@@ -646,7 +654,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     ep.all_place = ctx->o_place.as<int32_t>();
   }
   const int kk = std::max(1, k);
-  CK(ctx->cta_topk.ensure(sizeof(amp_record) * (size_t)kk * ctx->n_ctas));
+  CK(ctx->cta_topk.ensure(sizeof(amp_record) * (size_t)kk * ctx->est_ctas));
   ep.cta_topk = ctx->cta_topk.as<amp_record>();
   ep.k = kk;
   ep.max_M = ctx->max_M;
@@ -658,17 +666,42 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   ep.stage = ctx->stage_d.as<uint32_t>();
   ep.vbuf = ctx->vbuf.as<double>();
   ep.max_cells = ctx->max_cells;
-#ifdef AMP_PROFILE_PHASES
-  CK(ctx->phase.ensure(sizeof(unsigned long long) * 8));
-  CK(cudaMemsetAsync(ctx->phase.p, 0, sizeof(unsigned long long) * 8, ctx->stream));
-  ep.phase_cycles = ctx->phase.as<unsigned long long>();
-#endif
   ep.max_prog_cells = ctx->max_prog_cells;
-  CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), ctx->stream));
-  void* args[] = {&ep};
-  CK(cudaLaunchKernel(ctx->eval_fn, dim3(ctx->n_ctas), dim3(ctx->eval_threads), args, ctx->smem_bytes,
-                      ctx->stream));
-  CK(cudaGetLastError());
+  // chunk buffers (sized once per context for ctx->chunk items)
+  const uint64_t C = ctx->chunk;
+  CK(ctx->c_work.ensure(sizeof(CandWork) * C));
+  CK(ctx->c_place.ensure(sizeof(int32_t) * C * ctx->D));
+  CK(ctx->c_bwq.ensure(sizeof(double) * C * ctx->max_pp));
+  CK(ctx->c_cuts.ensure((size_t)C * (ctx->max_pp + 1)));
+  ep.work = ctx->c_work.as<CandWork>();
+  ep.placeb = ctx->c_place.as<int32_t>();
+  ep.bwqb = ctx->c_bwq.as<double>();
+  ep.cutsb = ctx->c_cuts.as<uint8_t>();
+  const int D = ctx->D, mp = ctx->max_pp;
+  const size_t place_smem = (D <= 32 ? sizeof(double) * D * D : 0) + sizeof(int) * 32 * 8;
+  size_t est_smem = (D <= 32 ? sizeof(double) * D * D : 0) +
+                    sizeof(double) * 2 * mp * kEstWarps + sizeof(int) * (mp + 2) * kEstWarps;
+  est_smem = ((est_smem + 15) & ~size_t(15)) + sizeof(EstWarp) * kEstWarps +
+             (kk <= 32 ? sizeof(amp_record) * kk : 0);
+  if (est_smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(k_est, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)est_smem));
+  for (uint64_t t0 = 0; t0 < n_work; t0 += C) {
+    ep.t0 = t0;
+    ep.n_chunk = std::min<uint64_t>(C, n_work - t0);
+    ep.first_chunk = t0 == 0;
+    const uint64_t warps = ep.n_chunk;
+    const int place_grid = (int)std::min<uint64_t>((warps + 7) / 8, (uint64_t)ctx->sms * 16);
+    k_place<<<place_grid, 256, place_smem, ctx->stream>>>(ep);
+    CK(cudaGetLastError());
+    CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), ctx->stream));
+    void* args[] = {&ep};
+    CK(cudaLaunchKernel(ctx->eval_fn, dim3(ctx->n_ctas), dim3(ctx->eval_threads), args,
+                        ctx->smem_bytes, ctx->stream));
+    CK(cudaGetLastError());
+    k_est<<<ctx->est_ctas, kEstWarps * 32, est_smem, ctx->stream>>>(ep);
+    CK(cudaGetLastError());
+    ctx->launches += 3;
+  }
   return AMP_OK;
 }
 
@@ -807,13 +840,14 @@ int amp_search_run(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k, amp_re
   const bool det = all_details && (all_details->cuts || all_details->stage_times ||
                                    all_details->edge_times);
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  ctx->launches = 0;
   int rc = launch_evaluate(ctx, &segs, nullptr, n, k, all != nullptr, det,
                            all_details && all_details->placement);
   if (rc) return rc;
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
   const int kk = std::max(1, k);
   CK(ctx->topk.ensure(sizeof(amp_record) * kk));
-  rc = launch_merge(ctx, ctx->cta_topk.as<amp_record>(), kk * ctx->n_ctas, kk,
+  rc = launch_merge(ctx, ctx->cta_topk.as<amp_record>(), kk * ctx->est_ctas, kk,
                     ctx->topk.as<amp_record>(), ctx->stream);
   if (rc) return rc;
   CK(cudaEventRecord(ctx->ev2, ctx->stream));
@@ -836,7 +870,7 @@ int amp_search_run(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k, amp_re
   account(ctx, begin, end, nullptr, 0);
   ctx->stats.kernel_ms = ms1;
   ctx->stats.total_ms = ms2;
-  ctx->stats.launches = 2;
+  ctx->stats.launches = ctx->launches + 1;
   ctx->stats.ctas = ctx->n_ctas;
   return AMP_OK;
 }
@@ -852,6 +886,7 @@ int amp_search_evaluate(amp_ctx* ctx, const uint64_t* indices, int32_t n, amp_re
   CK(upload(ctx->index_list, indices, (size_t)n));
   const bool det = details && (details->cuts || details->stage_times || details->edge_times);
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  ctx->launches = 0;
   int rc = launch_evaluate(ctx, nullptr, ctx->index_list.as<uint64_t>(), (uint64_t)n, 1, true,
                            det, details && details->placement);
   if (rc) return rc;
@@ -866,7 +901,7 @@ int amp_search_evaluate(amp_ctx* ctx, const uint64_t* indices, int32_t n, amp_re
   account(ctx, 0, 0, indices, n);
   ctx->stats.kernel_ms = ms;
   ctx->stats.total_ms = ms;
-  ctx->stats.launches = 1;
+  ctx->stats.launches = ctx->launches;
   ctx->stats.ctas = ctx->n_ctas;
   return AMP_OK;
 }
@@ -883,12 +918,13 @@ int amp_search_run_device(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k,
   CK(cudaStreamWaitEvent(ctx->stream, ctx->ev0, 0));
   const auto segs = make_segments(ctx, begin, end);
   int rc = AMP_OK;
+  ctx->launches = 0;
   if (end > begin) {
     rc = launch_evaluate(ctx, &segs, nullptr, end - begin, k, false, false, false);
     if (rc) return rc;
   } else {
     // nothing to evaluate: pad the CTA lists
-    std::vector<amp_record> pad((size_t)k * ctx->n_ctas);
+    std::vector<amp_record> pad((size_t)k * ctx->est_ctas);
     for (auto& e : pad) {
       std::memset(&e, 0, sizeof(e));
       e.index = ~0ull;
@@ -901,12 +937,12 @@ int amp_search_run_device(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k,
     CK(cudaStreamSynchronize(ctx->stream));
   }
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
-  rc = launch_merge(ctx, ctx->cta_topk.as<amp_record>(), k * ctx->n_ctas, k, d_topk, ctx->stream);
+  rc = launch_merge(ctx, ctx->cta_topk.as<amp_record>(), k * ctx->est_ctas, k, d_topk, ctx->stream);
   if (rc) return rc;
   CK(cudaEventRecord(ctx->ev2, ctx->stream));
   CK(cudaStreamWaitEvent(user, ctx->ev2, 0));
   account(ctx, begin, end, nullptr, 0);
-  ctx->stats.launches = end > begin ? 2 : 1;
+  ctx->stats.launches = ctx->launches + 1;
   ctx->stats.ctas = ctx->n_ctas;
   ctx->stats.kernel_ms = -1;  // resolved by amp_search_last_stats
   ctx->stats.total_ms = -1;
@@ -918,16 +954,6 @@ int amp_search_merge_topk_device(amp_ctx* ctx, const amp_record* d_in, int32_t n
   if (!ctx || !d_in || !d_out || n_in < 1 || k < 1 || k > 4096) return AMP_E_INVALID;
   CK(cudaSetDevice(ctx->device));
   return launch_merge(ctx, d_in, n_in, k, d_out, reinterpret_cast<cudaStream_t>(stream));
-}
-
-// Debug: per-phase cycle totals of the last run (AMP_PROFILE_PHASES builds;
-// zeros otherwise).  Not part of the public header.
-int amp_debug_phase_cycles(const amp_ctx* ctx, unsigned long long* out8) {
-  if (!ctx || !out8) return AMP_E_INVALID;
-  std::memset(out8, 0, 8 * sizeof(unsigned long long));
-  if (ctx->phase.p)
-    cudaMemcpy(out8, ctx->phase.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-  return AMP_OK;
 }
 
 int amp_search_last_stats(const amp_ctx* ctx_c, amp_stats* out) {
