@@ -203,8 +203,10 @@ int amp_search_evaluate(amp_ctx* ctx, const uint64_t* indices, int32_t n,
 int amp_search_run_device(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k,
                           amp_record* d_topk, void* stream);
 
-/* Merge n_in device records (e.g. the all-gathered per-GPU top-k lists)
- * into the k best under the ranking key; deterministic.                   */
+/* Merge n_in device records — n_in / k lists of k records, each sorted by
+ * the ranking key and padded at its end (e.g. the all-gathered per-GPU
+ * outputs of amp_search_run_device), at most 1024 lists — into the k best
+ * under the ranking key; deterministic.                                   */
 int amp_search_merge_topk_device(amp_ctx* ctx, const amp_record* d_in, int32_t n_in,
                                  int32_t k, amp_record* d_out, void* stream);
 

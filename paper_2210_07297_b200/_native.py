@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libamp_search.so")
+# AMP_SEARCH_LIB overrides the library (A/B builds in tools/)
+LIB_PATH = os.environ.get("AMP_SEARCH_LIB", os.path.join(_HERE, "libamp_search.so"))
 
 AMP_OK = 0
 AMP_E_INVALID = -1

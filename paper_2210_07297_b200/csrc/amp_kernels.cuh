@@ -476,31 +476,69 @@ __device__ void topk_insert(amp_record* list, int& n, int k, const amp_record& r
 // K3: deterministic merge (k rounds of block argmin under rank_less)
 // ---------------------------------------------------------------------------
 
+// The input is n / k sorted lists of k records (CTA lists of K_est, or the
+// all-gathered per-rank lists), each padded with empty slots at its end.
+// k rounds of a block argmin over the list heads (a k-way merge), keys of
+// the heads cached in shared memory.  Deterministic: ties cannot occur
+// between distinct candidate indices.
+constexpr int kMergeMaxLists = 1024;
+
+__device__ __forceinline__ bool key_less(int ca, double ta, uint64_t ia, int cb, double tb,
+                                         uint64_t ib) {
+  if (ca != cb) return ca < cb;
+  if (ca == 0 && ta != tb) return ta < tb;
+  return ia < ib;
+}
+
 __global__ void k_merge_topk(const amp_record* in, int n, int k, amp_record* out,
-                             unsigned char* taken) {
-  __shared__ int best_idx[32];
+                             unsigned char* /*unused*/) {
+  __shared__ int hcls[kMergeMaxLists];
+  __shared__ double htot[kMergeMaxLists];
+  __shared__ uint64_t hidx[kMergeMaxLists];
+  __shared__ int hpos[kMergeMaxLists];
+  __shared__ int wbest[32];
   const int tid = threadIdx.x, nt = blockDim.x;
-  for (int x = tid; x < n; x += nt) taken[x] = 0;
+  const int nl = n / k;
+  auto load_head = [&](int l) {
+    const int pos = hpos[l];
+    if (pos >= k) {
+      hcls[l] = 3;  // exhausted: after everything
+      htot[l] = 0.0;
+      hidx[l] = ~0ull;
+      return;
+    }
+    const amp_record& r = in[(size_t)l * k + pos];
+    hcls[l] = r.fail_code < 0 ? 3 : (r.fail_code != 0 ? 1 : 0);
+    htot[l] = r.total;
+    hidx[l] = r.index;
+  };
+  for (int l = tid; l < nl; l += nt) {
+    hpos[l] = 0;
+    load_head(l);
+  }
   __syncthreads();
   for (int round = 0; round < k; ++round) {
-    int bi = -1;
-    for (int x = tid; x < n; x += nt)
-      if (!taken[x] && (bi < 0 || rank_less(in[x], in[bi]))) bi = x;
+    int bl = -1;
+    for (int l = tid; l < nl; l += nt)
+      if (bl < 0 || key_less(hcls[l], htot[l], hidx[l], hcls[bl], htot[bl], hidx[bl])) bl = l;
     for (int o = 16; o > 0; o >>= 1) {
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (oi >= 0 && (bi < 0 || rank_less(in[oi], in[bi]))) bi = oi;
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (ol >= 0 && (bl < 0 || key_less(hcls[ol], htot[ol], hidx[ol], hcls[bl], htot[bl], hidx[bl])))
+        bl = ol;
     }
-    if ((tid & 31) == 0) best_idx[tid >> 5] = bi;
+    if ((tid & 31) == 0) wbest[tid >> 5] = bl;
     __syncthreads();
     if (tid == 0) {
       int b = -1;
       for (int w = 0; w < (nt >> 5); ++w) {
-        const int oi = best_idx[w];
-        if (oi >= 0 && (b < 0 || rank_less(in[oi], in[b]))) b = oi;
+        const int ol = wbest[w];
+        if (ol >= 0 && (b < 0 || key_less(hcls[ol], htot[ol], hidx[ol], hcls[b], htot[b], hidx[b])))
+          b = ol;
       }
-      if (b >= 0) {
-        out[round] = in[b];
-        taken[b] = 1;
+      if (b >= 0 && hcls[b] != 3) {
+        out[round] = in[(size_t)b * k + hpos[b]];
+        ++hpos[b];
+        load_head(b);
       } else {
         amp_record e;
         e.index = ~0ull;

@@ -179,6 +179,11 @@ __global__ void __launch_bounds__(256) k_place(EvalParams p) {
 // ---------------------------------------------------------------------------
 enum : int { kDenseSS = 0, kDenseSG = 1, kDenseGS = 2, kDenseGG = 3, kSparseS = 4, kSparseG = 5 };
 
+#ifndef AMP_DP_BATCH
+#define AMP_DP_BATCH 4
+#endif
+constexpr int kDpBatch = AMP_DP_BATCH;
+
 struct DpShared {
   uint64_t u;
   int done, ok;
@@ -241,8 +246,8 @@ __global__ void __launch_bounds__(MODE >= kSparseS ? 256 : kEvalThreads, MODE >=
   sp = smem_raw + ((sp - smem_raw + 15) & ~15);
   double* E = reinterpret_cast<double*>(sp);  // dense: E[L]; sparse: 2 x double2[L]
   sp += sizeof(double) * 4 * L;
-  double* bwq = reinterpret_cast<double*>(sp);
-  sp += sizeof(double) * maxpp;
+  CandWork* wq = reinterpret_cast<CandWork*>(sp);  // [kDpBatch]
+  sp += sizeof(CandWork) * kDpBatch;
   int* cuts = reinterpret_cast<int*>(sp);
   sp += sizeof(int) * (maxpp + 2);
   // (integer offset from smem_raw keeps the shared address space visible)
@@ -252,31 +257,44 @@ __global__ void __launch_bounds__(MODE >= kSparseS ? 256 : kEvalThreads, MODE >=
     sh.cls = -1;
     sh.pair = -1;
   }
+  // work is taken kDpBatch items at a time: one atomic and one coalesced
+  // load of the work records and bandwidth rows per batch
+  int bi = 0, bn = 0;
+  uint64_t bbase = 0;
   for (;;) {
-    if (tid == 0) {
-      const unsigned long long u = atomicAdd(p.counter, 1ull);
-      sh.done = u >= p.n_chunk;
-      if (!sh.done) {
-        sh.u = u;
-        const CandWork w = p.work[u];
-        sh.ok = w.fail_code == 0;
-        if (sh.ok && w.cls != sh.cls) {
-          sh.cls = w.cls;
-          sh.cl = p.cls[w.cls];
-          sh.pr = p.pairs[sh.cl.pair];
-        }
+    if (bi >= bn) {
+      if (tid == 0) {
+        const unsigned long long u0 = atomicAdd(p.counter, (unsigned long long)kDpBatch);
+        sh.u = u0;
+        sh.done = u0 >= p.n_chunk;
       }
-    }
-    __syncthreads();
-    if (sh.done) break;
-    if (!sh.ok) {  // failed before the DP (pp > L, profile miss, bandwidth)
       __syncthreads();
-      continue;
+      if (sh.done) break;
+      bbase = sh.u;
+      bn = p.n_chunk - bbase < (uint64_t)kDpBatch ? (int)(p.n_chunk - bbase) : kDpBatch;
+      bi = 0;
+      const uint64_t* src = reinterpret_cast<const uint64_t*>(p.work + bbase);
+      uint64_t* dst = reinterpret_cast<uint64_t*>(wq);
+      for (int x = tid; x < bn * (int)(sizeof(CandWork) / 8); x += nt) dst[x] = src[x];
+      __syncthreads();
     }
-    const uint64_t u = sh.u;
+    const int my = bi++;
+    const CandWork& w = wq[my];
+    if (w.fail_code != 0) continue;  // failed before the DP (uniform)
+    const uint64_t u = bbase + my;
+    if (w.cls != sh.cls) {  // uniform: everybody reads the same smem
+      __syncthreads();
+      if (tid == 0) {
+        sh.cls = w.cls;
+        sh.cl = p.cls[w.cls];
+        sh.pr = p.pairs[sh.cl.pair];
+      }
+      __syncthreads();
+    }
     const ClassDev cl = sh.cl;
     const PairDev pr = sh.pr;
     const int pp = cl.pp, M = pr.M;
+    const double* bwq = p.bwqb + u * maxpp;  // read by the edge function (L1)
     if (sh.pair != cl.pair) {  // Dm/Pf (and the dense seg table) persist in smem
       const double* gdom = p.domain + (size_t)cl.pair * p.nv_stride;
       for (int x = tid; x < M; x += nt) Dm[x] = gdom[x];
@@ -285,10 +303,9 @@ __global__ void __launch_bounds__(MODE >= kSparseS ? 256 : kEvalThreads, MODE >=
         const uint16_t* gseg = p.seg + (size_t)cl.pair * LP * LP;
         for (int x = tid; x < LP * LP; x += nt) seg[x] = gseg[x];
       }
+      __syncthreads();
+      if (tid == 0) sh.pair = cl.pair;
     }
-    for (int q = tid; q < pp - 1; q += nt) bwq[q] = p.bwqb[u * maxpp + q];
-    __syncthreads();
-    if (tid == 0) sh.pair = cl.pair;
     EdgeFromBandwidth ef{p.act, bwq, cl.mbs};
     if (SPARSE) {
       const ProgDev pg = p.progs[p.class_prog[sh.cls]];

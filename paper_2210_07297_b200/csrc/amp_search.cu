@@ -8,10 +8,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -25,6 +28,19 @@ using namespace amp;
 namespace {
 
 thread_local std::string g_last_error;
+
+// AMP_TIMING=1: print host-side phase times of amp_search_create to stderr.
+struct PhaseTimer {
+  bool on = std::getenv("AMP_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[amp create] %-22s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 struct DevBuf {
   void* p = nullptr;
@@ -289,9 +305,23 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   ctx->ceiling = p->max_params_per_device;
   ctx->bpp = p->bytes_per_param;
 
+  PhaseTimer tm;
   CK(cudaSetDevice(ctx->device));
+  // cudaGetDeviceProperties costs milliseconds; cache it per device
+  static std::mutex prop_mu;
+  static std::map<int, cudaDeviceProp> prop_cache;
   cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, ctx->device));
+  {
+    std::lock_guard<std::mutex> lk(prop_mu);
+    auto it = prop_cache.find(ctx->device);
+    if (it == prop_cache.end()) {
+      CK(cudaGetDeviceProperties(&prop, ctx->device));
+      prop_cache.emplace(ctx->device, prop);
+    } else {
+      prop = it->second;
+    }
+  }
+  tm.mark("device+props");
   if (prop.major != 10)
     return fail(ctx, AMP_E_NOT_BUILT,
                 "device is sm_" + std::to_string(prop.major * 10 + prop.minor) +
@@ -301,6 +331,7 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   CK(cudaEventCreate(&ctx->ev1));
   CK(cudaEventCreate(&ctx->ev2));
 
+  tm.mark("stream/events");
   // ---- classes: the plan() candidate list (optimizer.cpp:288-293) -------
   std::map<std::pair<int, int>, int> pair_of;
   std::vector<int> pair_tmp, pair_mbs;
@@ -370,6 +401,7 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   CK(upload(ctx->base_order, order.data(), order.size()));
   CK(upload(ctx->cls_d, ctx->classes.data(), ctx->classes.size()));
 
+  tm.mark("encode+uploads");
   // ---- K0: pair tables on the device ----------------------------------
   const int nv = 1 + L * (L + 1) / 2;
   int npow2 = 2;
@@ -421,6 +453,7 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
                      cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
 
+  tm.mark("K0 pair tables");
   // ---- per-class work accounting (scheduling + roofline) ---------------
   ctx->class_inner.assign(ctx->classes.size(), 0.0);
   ctx->class_lt.assign(ctx->classes.size(), 0.0);
@@ -452,6 +485,7 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   ctx->bp_stride = (bp_stride + 255) & ~size_t(255);
 
   const int LP = L + 1;
+  tm.mark("class accounting");
   // ---- K0b: pruned-DP programs, one per distinct (pair, k) ---------------
   bool sparse = !(cfg && (cfg->flags & AMP_FLAG_DENSE_DP));
   if (sparse) {
@@ -467,10 +501,11 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
         ctx->class_lt[c] = 0;
       }
 
+  tm.mark("K0b programs");
   // ---- evaluate kernel launch shape -------------------------------------
   // K_dp smem (mirror of the carve-up in amp_pipeline.cuh k_dp)
   size_t small = 16 + sizeof(double) * ctx->max_M + sizeof(double) * LP +
-                 4 * sizeof(double) * L + sizeof(double) * ctx->max_pp +
+                 4 * sizeof(double) * L + sizeof(CandWork) * kDpBatch +
                  sizeof(int) * (ctx->max_pp + 2);
   small = (small + 15) & ~size_t(15);
   const size_t w_b = sizeof(WEnt) * (size_t)LP * L;
@@ -533,6 +568,7 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   if (!sparse && !ctx->w_in_smem) CK(ctx->wtab.ensure(w_b * n_ctas));
   if (ctx->v_stride) CK(ctx->vbuf.ensure(sizeof(double) * ctx->v_stride * n_ctas));
   CK(ctx->counter.ensure(sizeof(unsigned long long)));
+  tm.mark("launch shape+scratch");
   return AMP_OK;
 }
 
@@ -667,8 +703,8 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   ep.vbuf = ctx->vbuf.as<double>();
   ep.max_cells = ctx->max_cells;
   ep.max_prog_cells = ctx->max_prog_cells;
-  // chunk buffers (sized once per context for ctx->chunk items)
-  const uint64_t C = ctx->chunk;
+  // chunk buffers (grown on demand up to ctx->chunk items)
+  const uint64_t C = std::min<uint64_t>(ctx->chunk, std::max<uint64_t>(n_work, 1));
   CK(ctx->c_work.ensure(sizeof(CandWork) * C));
   CK(ctx->c_place.ensure(sizeof(int32_t) * C * ctx->D));
   CK(ctx->c_bwq.ensure(sizeof(double) * C * ctx->max_pp));
@@ -707,6 +743,8 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
 
 int launch_merge(amp_ctx* ctx, const amp_record* d_in, int n_in, int k, amp_record* d_out,
                  cudaStream_t st) {
+  if (n_in % k != 0 || n_in / k > kMergeMaxLists)
+    return fail(ctx, AMP_E_INVALID, "merge input must be <= 1024 sorted lists of k records");
   CK(ctx->taken.ensure((size_t)n_in + 16));
   k_merge_topk<<<1, 1024, 0, st>>>(d_in, n_in, k, d_out, ctx->taken.as<unsigned char>());
   CK(cudaGetLastError());

@@ -244,24 +244,47 @@ def rank_order(recs: np.ndarray) -> np.ndarray:
 def plan(model: ModelGraph, cluster: Cluster, profile: ProfileTable, gbs: int,
          options: Optional[PlanOptions] = None, device: int = 0, dense_dp: bool = False) -> PlanResult:
     """parplan::plan on the GPU (optimizer.cpp:200-251)."""
+    import os
+    import time
+
     from . import simulator
 
+    tm = {} if os.environ.get("AMP_TIMING") else None
+    t = time.perf_counter()
     options = options or PlanOptions()
     enc = EncodedProblem(model, cluster, profile, gbs, options)
+    if tm is not None:
+        tm["encode"] = time.perf_counter() - t
+        t = time.perf_counter()
     with Searcher(enc, placements_per_class=1, device=device, dense_dp=dense_dp) as s:
+        if tm is not None:
+            tm["create"] = time.perf_counter() - t
+            t = time.perf_counter()
         _, allr, bufs = s.run(0, s.num_candidates, k=0, want_all=True, details=True, placement=True)
+        if tm is not None:
+            tm["run"] = time.perf_counter() - t
+            t = time.perf_counter()
+    if tm is not None:
+        tm["destroy"] = time.perf_counter() - t
+        t = time.perf_counter()
     order = rank_order(allr)
     cands = records_to_candidates(allr, bufs, model.layer_count(), rows=order)
     for i, c in enumerate(cands):
         c.rank = i + 1
     result = PlanResult(cands, -1)
+    if tm is not None:
+        tm["decode"] = time.perf_counter() - t
+        t = time.perf_counter()
     # validate the top `budget` with the simulator (optimizer.cpp:235-249)
     for i in range(min(len(cands), max(0, options.budget))):
         rec = cands[i]
         if rec.failure is not None:
             continue
         rec.simulated = simulator.simulate(rec.strategy, model, cluster, profile, gbs,
-                                           options.cost_options)
+                                           options.cost_options, encoded=enc)
         if result.best_index < 0 or rec.simulated < cands[result.best_index].simulated:
             result.best_index = i
+    if tm is not None:
+        tm["simulate"] = time.perf_counter() - t
+        print("plan timing (ms):", {k: round(v * 1e3, 3) for k, v in tm.items()})
     return result
