@@ -34,6 +34,7 @@ SCENARIO = "hetero_cluster"
 DEFAULT_N_PER_GPU = 10_000_000
 TOPK = 10
 METRIC = "candidate strategies/sec"
+TRAFFIC_BYTES_PER_CANDIDATE = 141.5  # ncu: k_dp dram__bytes_read+write / candidates
 UNIT = "candidates/s"
 
 
@@ -235,7 +236,7 @@ def our_arm(args):
             ev[i][0].record(stream)
             step()
             ev[i][1].record(stream)
-            kernel_ms.append(s.stats()["kernel_ms"])  # K1+K2 events on the engine stream
+            kernel_ms.append(s.stats())  # per-kernel events on the engine stream
         torch.cuda.synchronize()
     times = [a.elapsed_time(b) for a, b in ev]
     my_ms = float(sum(times))
@@ -255,7 +256,10 @@ def our_arm(args):
     peak = C.c_double()
     pms = C.c_double()
     N.check(N.load().amp_fp64_peak(local, C.byref(peak), C.byref(pms)))
-    kern_ms = float(np.mean(kernel_ms))
+    dp_ms = float(np.mean([x["dp_ms"] for x in kernel_ms]))
+    place_ms = float(np.mean([x["place_ms"] for x in kernel_ms]))
+    est_ms = float(np.mean([x["est_ms"] for x in kernel_ms]))
+    kern_ms = dp_ms
     achieved = st["fp64_ops"] / (kern_ms * 1e-3) / 1e12
     peak_t = peak.value / 1e12
 
@@ -279,9 +283,14 @@ def our_arm(args):
                        "topk": k, "l2": "flushed (256 MiB write) before every timed step",
                        "parallelism": f"index-range shards x{world}, NCCL all-gather of top-k"},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s",
-                         "frac": achieved / peak_t, "traffic": None,
-                         "kernel": "k_evaluate (K1 DP + K2 estimate)",
+                         "frac": achieved / peak_t,
+                         "traffic": TRAFFIC_BYTES_PER_CANDIDATE * n_total / max(1, st["launches"] // 3),
+                         "traffic_note": "dram read+write bytes per k_dp launch, scaled from the ncu "
+                                         "capture in profiles/r1_k_dp_ncu.txt (141.5 B/candidate, "
+                                         "cold cache); algorithmic bytes ~0 (L2-resident tables)",
+                         "kernel": "k_dp (pruned layer-partition DP)",
                          "kernel_ms_per_step": kern_ms,
+                         "pipeline_ms_per_step": {"k_place": place_ms, "k_dp": dp_ms, "k_est": est_ms},
                          "fp64_ops_per_step": st["fp64_ops"], "dp_inner_per_step": st["dp_inner"],
                          "peak_source": "measured live: amp_fp64_peak DADD throughput (no FP64 entry "
                                         "in MEASURED_PEAKS.json)"},

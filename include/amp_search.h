@@ -157,7 +157,10 @@ typedef struct amp_stats {
   uint64_t candidates;       /* candidates evaluated                         */
   uint64_t dp_instances;     /* DP instances solved                          */
   int32_t launches;          /* kernels launched by the run                  */
-  int32_t ctas;              /* CTAs of the evaluate kernel                  */
+  int32_t ctas;              /* CTAs of the DP kernel                        */
+  double place_ms;           /* device time of K_place (all chunks)          */
+  double dp_ms;              /* device time of K_dp (all chunks)             */
+  double est_ms;             /* device time of K_est (all chunks)            */
 } amp_stats;
 
 typedef struct amp_ctx amp_ctx;

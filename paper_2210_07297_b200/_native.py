@@ -114,6 +114,9 @@ class AmpStats(C.Structure):
         ("dp_instances", C.c_uint64),
         ("launches", C.c_int32),
         ("ctas", C.c_int32),
+        ("place_ms", C.c_double),
+        ("dp_ms", C.c_double),
+        ("est_ms", C.c_double),
     ]
 
 

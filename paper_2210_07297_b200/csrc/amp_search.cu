@@ -114,6 +114,11 @@ struct amp_ctx {
   DevBuf c_work, c_place, c_bwq, c_cuts;  // pipeline chunk buffers
   uint64_t chunk = 1;
   int est_ctas = 1, sms = 148, launches = 0;
+  // per-chunk kernel events {before K_place, after K_place, after K_dp,
+  // after K_est}; resolved into stats.{place,dp,est}_ms
+  std::vector<cudaEvent_t> kev;
+  int kev_used = 0;
+  bool kev_pending = false;
   amp_stats stats{};
 };
 
@@ -599,6 +604,27 @@ std::vector<Segment> make_segments(const amp_ctx* ctx, uint64_t begin, uint64_t 
   return out;
 }
 
+// Sum the per-chunk kernel events of the last launch_evaluate (blocks
+// until they completed).
+void resolve_kernel_times(amp_ctx* ctx) {
+  if (!ctx->kev_pending) return;
+  double pl = 0, dpm = 0, es = 0;
+  for (int c = 0; c + 3 < ctx->kev_used; c += 4) {
+    cudaEventSynchronize(ctx->kev[c + 3]);
+    float a = 0, b = 0, d = 0;
+    cudaEventElapsedTime(&a, ctx->kev[c], ctx->kev[c + 1]);
+    cudaEventElapsedTime(&b, ctx->kev[c + 1], ctx->kev[c + 2]);
+    cudaEventElapsedTime(&d, ctx->kev[c + 2], ctx->kev[c + 3]);
+    pl += a;
+    dpm += b;
+    es += d;
+  }
+  ctx->stats.place_ms = pl;
+  ctx->stats.dp_ms = dpm;
+  ctx->stats.est_ms = es;
+  ctx->kev_pending = false;
+}
+
 void account(amp_ctx* ctx, uint64_t begin, uint64_t end, const uint64_t* list, int32_t n) {
   amp_stats& s = ctx->stats;
   s.dp_inner = s.dp_inner_lt = s.dp_cells = 0;
@@ -721,7 +747,17 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
              (kk <= 32 ? sizeof(amp_record) * kk : 0);
   if (est_smem > 48 * 1024)
     CK(cudaFuncSetAttribute(k_est, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)est_smem));
+  const int n_chunks = (int)((n_work + C - 1) / C);
+  while ((int)ctx->kev.size() < 4 * n_chunks) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    ctx->kev.push_back(e);
+  }
+  ctx->kev_used = 4 * n_chunks;
+  ctx->kev_pending = true;
   for (uint64_t t0 = 0; t0 < n_work; t0 += C) {
+    cudaEvent_t* ev = &ctx->kev[4 * (t0 / C)];
+    CK(cudaEventRecord(ev[0], ctx->stream));
     ep.t0 = t0;
     ep.n_chunk = std::min<uint64_t>(C, n_work - t0);
     ep.first_chunk = t0 == 0;
@@ -730,12 +766,15 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     k_place<<<place_grid, 256, place_smem, ctx->stream>>>(ep);
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), ctx->stream));
+    CK(cudaEventRecord(ev[1], ctx->stream));
     void* args[] = {&ep};
     CK(cudaLaunchKernel(ctx->eval_fn, dim3(ctx->n_ctas), dim3(ctx->eval_threads), args,
                         ctx->smem_bytes, ctx->stream));
     CK(cudaGetLastError());
+    CK(cudaEventRecord(ev[2], ctx->stream));
     k_est<<<ctx->est_ctas, kEstWarps * 32, est_smem, ctx->stream>>>(ep);
     CK(cudaGetLastError());
+    CK(cudaEventRecord(ev[3], ctx->stream));
     ctx->launches += 3;
   }
   return AMP_OK;
@@ -801,6 +840,7 @@ void amp_search_destroy(amp_ctx* ctx) {
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->ev2) cudaEventDestroy(ctx->ev2);
+  for (cudaEvent_t e : ctx->kev) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -906,6 +946,7 @@ int amp_search_run(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k, amp_re
   cudaEventElapsedTime(&ms1, ctx->ev0, ctx->ev1);
   cudaEventElapsedTime(&ms2, ctx->ev0, ctx->ev2);
   account(ctx, begin, end, nullptr, 0);
+  resolve_kernel_times(ctx);
   ctx->stats.kernel_ms = ms1;
   ctx->stats.total_ms = ms2;
   ctx->stats.launches = ctx->launches + 1;
@@ -937,6 +978,7 @@ int amp_search_evaluate(amp_ctx* ctx, const uint64_t* indices, int32_t n, amp_re
   float ms = 0;
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
   account(ctx, 0, 0, indices, n);
+  resolve_kernel_times(ctx);
   ctx->stats.kernel_ms = ms;
   ctx->stats.total_ms = ms;
   ctx->stats.launches = ctx->launches;
@@ -1005,6 +1047,7 @@ int amp_search_last_stats(const amp_ctx* ctx_c, amp_stats* out) {
     ctx->stats.kernel_ms = ms1;
     ctx->stats.total_ms = ms2;
   }
+  resolve_kernel_times(ctx);
   *out = ctx->stats;
   return AMP_OK;
 }
