@@ -198,8 +198,11 @@ struct DpShared {
 //                      in (S)hared or (G)lobal memory
 //   kSparseS/G         pruned program (amp_dp_sparse.cuh); value arrays and
 //                      backpointers in shared / global memory
+// kSparseG (large L, e.g. 96 layers x 1024 GPUs): few, very uneven DP
+// instances, so each candidate gets a full 1024-thread CTA.
 template <int MODE>
-__global__ void __launch_bounds__(MODE >= kSparseS ? 256 : kEvalThreads, MODE >= kSparseS ? 4 : 2)
+__global__ void __launch_bounds__(MODE == kSparseG ? 1024 : (MODE == kSparseS ? 256 : kEvalThreads),
+                                  MODE == kSparseG ? 1 : (MODE == kSparseS ? 4 : 2))
     k_dp(EvalParams p) {
   constexpr bool SPARSE = MODE >= kSparseS;
   constexpr bool SLICE_SMEM = MODE == kDenseSS || MODE == kDenseSG;

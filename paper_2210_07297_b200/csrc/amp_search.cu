@@ -522,7 +522,7 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
     const bool v_smem = small + v_b <= 64 * 1024;
     mode = v_smem ? kSparseS : kSparseG;
     ctx->smem_bytes = small + (v_smem ? v_b : 0);
-    ctx->eval_threads = v_smem ? 128 : 256;
+    ctx->eval_threads = v_smem ? 128 : 1024;
     ctx->bp_stride = v_smem ? 0 : (((size_t)ctx->max_prog_cells + 255) & ~size_t(255));
     ctx->v_stride = v_smem ? 0 : 2 * (size_t)ctx->max_cells;
     ctx->slice_in_smem = ctx->w_in_smem = 1;
