@@ -122,6 +122,17 @@ struct EvalParams {
   int32_t pad3;
   int32_t max_cells;          // max_j |N_j| over programs
   int32_t max_prog_cells;     // max sum_j |N_j| over programs
+  // K_dp multi (amp_dp_multi.cuh)
+  int32_t max_n1;             // max |N_1|
+  int32_t max_v;              // max_{j >= 2} |N_j|
+  int32_t max_rest;           // max sum_{j >= 2} |N_j| (backpointer bytes per candidate)
+  int32_t n_codes;            // distinct link bandwidths (0: codes disabled)
+  const uint8_t* bwcode;      // [D*D] rank of each link's bandwidth among bwval, or NULL
+  const double* bwval;        // [n_codes] distinct bandwidths, ascending
+  const double* qtab;         // [n_cls][n_codes][L] edge cost act[c-1]*mbs / bwval[code]
+  uint8_t* bwcb;              // [n_chunk][max_pp] stage-boundary bandwidth codes
+  const uint2* cellrec;       // [cells] {cell, cellpred} (K_dp multi)
+  uint64_t n_dp;              // chunk items [0, n_dp) may need K_dp (pp >= 3 first)
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

@@ -22,7 +22,8 @@
 //   cellpred[]  u32 per cell of N_j (j >= 2): offset of its predecessor list
 //   preds[]     u16 per (cell, cut): index of (c, max(seg(c,i), m)) within
 //               N_{j-1}, for c = j-1 .. i-1; each cell's list is padded to a
-//               multiple of 4 entries so it can be read with 8-byte loads
+//               multiple of 4 entries so it can be read with 8-byte loads;
+//               padding entries hold |N_{j-1}| (sentinel slot)
 //   stage[]     u32 k+1 entries: start of N_j (j = 1..k) within the program's
 //               cells, then the end
 #pragma once
@@ -53,7 +54,8 @@ struct ProgBuildParams {
   uint64_t scratch_stride;
   // count pass outputs
   uint32_t* stage_sizes;     // [n_progs][L+1]  |N_j| at [j]
-  uint64_t* stage_preds;     // [n_progs][L+1]  predecessor entries of stage j
+  uint64_t* stage_preds;     // [n_progs][L+1]  predecessor entries of stage j (padded)
+  uint64_t* stage_inner;     // [n_progs][L+1]  inner iterations of stage j (unpadded)
   // build pass inputs/outputs
   const ProgDev* progs;
   uint32_t* cells;
@@ -133,11 +135,12 @@ __global__ void k_build_progs(ProgBuildParams p) {
     // ---- mark N_{j-1} ----------------------------------------------------
     for (int x = tid; x < nw; x += nt) bm[x] = 0;
     __syncthreads();
-    uint64_t my_preds = 0;
+    uint64_t my_preds = 0, my_inner = 0;
     for (int x = tid; x < n; x += nt) {
       const uint32_t cell = A[x];
       const int i = cell >> 16, m = cell & 0xffff;
       my_preds += (uint64_t)((i - j + 1 + 3) & ~3);  // lists padded to 4 (8-byte loads)
+      my_inner += (uint64_t)(i - j + 1);
       for (int c = j - 1; c < i; ++c) {
         const int s = seg[c * LP + i];
         const int mp = s > m ? s : m;
@@ -145,13 +148,25 @@ __global__ void k_build_progs(ProgBuildParams p) {
       }
     }
     // total predecessor entries of stage j
-    for (int o = 16; o > 0; o >>= 1) my_preds += __shfl_xor_sync(0xffffffffu, my_preds, o);
-    if ((tid & 31) == 0) red64[tid >> 5] = my_preds;
+    for (int o = 16; o > 0; o >>= 1) {
+      my_preds += __shfl_xor_sync(0xffffffffu, my_preds, o);
+      my_inner += __shfl_xor_sync(0xffffffffu, my_inner, o);
+    }
+    if ((tid & 31) == 0) {
+      red64[tid >> 5] = my_preds;
+      red64[16 + (tid >> 5)] = my_inner;
+    }
     __syncthreads();
     if (tid == 0) {
-      uint64_t t = 0;
-      for (int w = 0; w < (nt >> 5); ++w) t += red64[w];
-      if (p.count_only) p.stage_preds[(size_t)pg * LP + j] = t;
+      uint64_t t = 0, ti = 0;
+      for (int w = 0; w < (nt >> 5); ++w) {
+        t += red64[w];
+        ti += red64[16 + w];
+      }
+      if (p.count_only) {
+        p.stage_preds[(size_t)pg * LP + j] = t;
+        p.stage_inner[(size_t)pg * LP + j] = ti;
+      }
     }
     // ---- rank structure: words in row-descending order ------------------
     // scan position o = (L - row) * W + w
@@ -177,6 +192,10 @@ __global__ void k_build_progs(ProgBuildParams p) {
               const uint32_t below = bm[wi] & ((1u << (mp & 31)) - 1u);
               q[c - (j - 1)] = (uint16_t)(wpre[wi] + __popc(below));
             }
+            // padding entries name the sentinel slot |N_{j-1}| (a +inf
+            // value in K_dp multi, so padded cuts never win)
+            for (int t = i - (j - 1); t < (((i - j + 1) + 3) & ~3); ++t)
+              q[t] = (uint16_t)n_next;
           },
           scan_sm);
     }

@@ -64,13 +64,20 @@ __device__ __forceinline__ void decode_item(const EvalParams& p, uint64_t t, uin
 __global__ void __launch_bounds__(256) k_place(EvalParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int D = p.D, lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  // |D| <= 32: bandwidth matrix and one rank->device row per warp in smem
+  // |D| <= 32: bandwidth matrix (or its code matrix) and one rank->device
+  // row per warp in smem
   double* bwS = reinterpret_cast<double*>(smem_raw);
   int* placeS = reinterpret_cast<int*>(bwS + (D <= 32 ? D * D : 0)) + wib * 32;
+  uint8_t* codeS = reinterpret_cast<uint8_t*>(placeS - wib * 32 + 32 * (blockDim.x >> 5));
   const double* BW = p.bw;
+  const uint8_t* CODE = p.bwcode;
   if (D <= 32) {
-    for (int x = threadIdx.x; x < D * D; x += blockDim.x) bwS[x] = p.bw[x];
+    for (int x = threadIdx.x; x < D * D; x += blockDim.x) {
+      bwS[x] = p.bw[x];
+      if (p.bwcode) codeS[x] = p.bwcode[x];
+    }
     BW = bwS;
+    if (p.bwcode) CODE = codeS;
     __syncthreads();
   }
   const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
@@ -140,10 +147,24 @@ __global__ void __launch_bounds__(256) k_place(EvalParams p) {
         const int q = q0 + lane;
         double b = CUDART_INF;
         if (q < pp - 1) {
-          for (int r = 0; r < dp; ++r)
-            for (int s = 0; s < tmp; ++s)
-              b = std_min(b, BW[(size_t)PL[(q * dp + r) * tmp + s] * D +
-                                PL[((q + 1) * dp + r) * tmp + s]]);
+          if (CODE) {
+            // codes rank the distinct bandwidths, so the minimum code is the
+            // code of the minimum bandwidth (no NaN: checked at create)
+            int cm = 255;
+            for (int r = 0; r < dp; ++r)
+              for (int s = 0; s < tmp; ++s) {
+                const int cc = CODE[(size_t)PL[(q * dp + r) * tmp + s] * D +
+                                    PL[((q + 1) * dp + r) * tmp + s]];
+                cm = cc < cm ? cc : cm;
+              }
+            b = p.bwval[cm];
+            p.bwcb[u * p.max_pp + q] = (uint8_t)cm;
+          } else {
+            for (int r = 0; r < dp; ++r)
+              for (int s = 0; s < tmp; ++s)
+                b = std_min(b, BW[(size_t)PL[(q * dp + r) * tmp + s] * D +
+                                  PL[((q + 1) * dp + r) * tmp + s]]);
+          }
           p.bwqb[u * p.max_pp + q] = b;
         }
         // p2p_time throws on the first invalid boundary inside the DP's
@@ -269,12 +290,12 @@ __global__ void __launch_bounds__(MODE == kSparseG ? 1024 : (MODE == kSparseS ? 
       if (tid == 0) {
         const unsigned long long u0 = atomicAdd(p.counter, (unsigned long long)kDpBatch);
         sh.u = u0;
-        sh.done = u0 >= p.n_chunk;
+        sh.done = u0 >= p.n_dp;  // items [n_dp, n_chunk) are pp <= 2 (K_est)
       }
       __syncthreads();
       if (sh.done) break;
       bbase = sh.u;
-      bn = p.n_chunk - bbase < (uint64_t)kDpBatch ? (int)(p.n_chunk - bbase) : kDpBatch;
+      bn = p.n_dp - bbase < (uint64_t)kDpBatch ? (int)(p.n_dp - bbase) : kDpBatch;
       bi = 0;
       const uint64_t* src = reinterpret_cast<const uint64_t*>(p.work + bbase);
       uint64_t* dst = reinterpret_cast<uint64_t*>(wq);
@@ -327,6 +348,45 @@ __global__ void __launch_bounds__(MODE == kSparseG ? 1024 : (MODE == kSparseS ? 
 // K_est
 // ---------------------------------------------------------------------------
 constexpr int kEstWarps = 8;
+
+// The layer-partition DP for k = 2 stages (pipeline_dp.cpp:70-149): stage 2
+// has the single cell (L, 0); its cut c reads stage-1 cell
+// (c, max(seg(c, L), 0)) = (c, seg(c, L)).  Lane-strided cuts, each lane
+// keeps its first strict minimum, then a lexicographic (value, cut)
+// butterfly — the sequential strict-'<' scan.  Same operations and operand
+// order as sparse_solve / the reference.
+__device__ int light_cut2(const EvalParams& p, const ClassDev& cl, uint64_t u, int lane) {
+  const int L = p.L, LP = L + 1;
+  const double* Pf = p.prefix + (size_t)cl.pair * LP;
+  const double* Dm = p.domain + (size_t)cl.pair * p.nv_stride;
+  const uint16_t* sg = p.seg + (size_t)cl.pair * LP * LP;
+  const double g1 = (double)(cl.gas - 1);
+  const double bq = p.bwqb[u * p.max_pp];
+  const double dm0 = Dm[0], PL = Pf[L], P0 = Pf[0];
+  double best = CUDART_INF;
+  int bc = -1;
+  for (int c = 1 + lane; c < L; c += 32) {
+    const double t1 = Pf[c] - P0;
+    const double sub = g1 * max0(t1 - Dm[sg[c * LP + L]]) + t1;  // cost(c, 1, seg(c, L))
+    const double t2 = PL - Pf[c];
+    const double term = t2 > dm0 ? g1 * (t2 - dm0) : 0.0;
+    const double e = p.act[c - 1] * cl.mbs / bq;  // placement_edge_cost
+    const double g = ((sub + term) + t2) + e;
+    if (g < best) {
+      best = g;
+      bc = c;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+    if (ov < best || (ov == best && oc < bc)) {
+      best = ov;
+      bc = oc;
+    }
+  }
+  return bc;
+}
 
 // Per-warp smem scratch of K_est.
 struct EstWarp {
@@ -393,8 +453,19 @@ __global__ void __launch_bounds__(kEstWarps * 32) k_est(EvalParams p) {
     int best_r = -1;
     const int* PL = ew->place;
     if (fc == 0) {
-      const uint8_t* ci = p.cutsb + u * (maxpp + 1);
-      for (int q = lane; q <= pp; q += 32) cutsW[q] = ci[q];
+      if (pp >= 3) {
+        const uint8_t* ci = p.cutsb + u * (maxpp + 1);
+        for (int q = lane; q <= pp; q += 32) cutsW[q] = ci[q];
+      } else {
+        // pp <= 2 never reaches K_dp: single stage, or the two-stage DP
+        // solved here by the warp (light_cut2)
+        const int c1 = pp == 2 ? light_cut2(p, cl, u, lane) : p.L;
+        if (lane == 0) {
+          cutsW[0] = 0;
+          cutsW[1] = pp == 2 ? (int)(uint8_t)c1 : p.L;
+          if (pp == 2) cutsW[2] = p.L;
+        }
+      }
       const int32_t* prow = p.placeb + u * D;
       if (D <= 32) {
         if (lane < D) ew->place[lane] = prow[lane];

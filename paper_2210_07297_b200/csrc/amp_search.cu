@@ -22,6 +22,7 @@
 #include "amp_common.cuh"
 #include "amp_kernels.cuh"
 #include "amp_pipeline.cuh"
+#include "amp_dp_multi.cuh"
 
 using namespace amp;
 
@@ -109,9 +110,17 @@ struct amp_ctx {
   std::vector<ProgDev> progs_h;
   std::vector<double> prog_inner;  // inner iterations per program
   int max_cells = 1, max_prog_cells = 1;
+  int max_n1 = 1, max_v = 1, max_rest = 1;
+  int multi_b = 0;                 // K_dp multi: candidates per group (0: per-candidate k_dp)
+  std::vector<double> prog_inner_raw;  // unpadded inner iterations per program
   size_t v_stride = 0;
   DevBuf progs_d, stage_d, class_prog_d, cells, cellpred, preds, vbuf;
-  DevBuf c_work, c_place, c_bwq, c_cuts;  // pipeline chunk buffers
+  DevBuf c_work, c_place, c_bwq, c_cuts, c_bwc;  // pipeline chunk buffers
+  // bandwidth codes (ranks of the distinct link bandwidths) and per-class
+  // edge-cost tables; n_codes = 0 when disabled
+  int n_codes = 0;
+  DevBuf bwcode, bwval, qtab, cellrec;
+  uint64_t n_heavy = 0;  // items of pp >= 3 classes in the current run's dispatch order
   uint64_t chunk = 1;
   int est_ctas = 1, sms = 148, launches = 0;
   // per-chunk kernel events {before K_place, after K_place, after K_dp,
@@ -178,15 +187,17 @@ int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
     CK(upload(ctx->class_prog_d, ctx->class_prog.data(), ctx->class_prog.size()));
     return AMP_OK;
   }
-  DevBuf d_k, d_pair, d_scratch, d_sizes, d_preds_n, d_pstart;
+  DevBuf d_k, d_pair, d_scratch, d_sizes, d_preds_n, d_inner_n, d_pstart;
   CK(upload(d_k, pk.data(), pk.size()));
   CK(upload(d_pair, ppair.data(), ppair.size()));
   const uint64_t scratch_stride = 2ull * LP * ctx->max_M;
   CK(d_scratch.ensure(sizeof(uint32_t) * scratch_stride * n));
   CK(d_sizes.ensure(sizeof(uint32_t) * (size_t)n * LP));
   CK(d_preds_n.ensure(sizeof(uint64_t) * (size_t)n * LP));
+  CK(d_inner_n.ensure(sizeof(uint64_t) * (size_t)n * LP));
   CK(cudaMemsetAsync(d_sizes.p, 0, sizeof(uint32_t) * (size_t)n * LP, ctx->stream));
   CK(cudaMemsetAsync(d_preds_n.p, 0, sizeof(uint64_t) * (size_t)n * LP, ctx->stream));
+  CK(cudaMemsetAsync(d_inner_n.p, 0, sizeof(uint64_t) * (size_t)n * LP, ctx->stream));
   ProgBuildParams bp{};
   bp.L = L;
   bp.n_progs = n;
@@ -199,6 +210,7 @@ int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
   bp.scratch_stride = scratch_stride;
   bp.stage_sizes = d_sizes.as<uint32_t>();
   bp.stage_preds = d_preds_n.as<uint64_t>();
+  bp.stage_inner = d_inner_n.as<uint64_t>();
   const int W = (ctx->max_M + 31) / 32;
   const size_t smem = sizeof(uint32_t) * 2 * (size_t)LP * W + sizeof(uint16_t) * LP * LP;
   if (smem > 227 * 1024) {
@@ -209,12 +221,15 @@ int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
   k_build_progs<<<n, 512, smem, ctx->stream>>>(bp);
   CK(cudaGetLastError());
   std::vector<uint32_t> sizes((size_t)n * LP);
-  std::vector<uint64_t> pn((size_t)n * LP);
+  std::vector<uint64_t> pn((size_t)n * LP), pin((size_t)n * LP);
   CK(cudaMemcpyAsync(sizes.data(), d_sizes.p, sizeof(uint32_t) * sizes.size(),
                      cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(pn.data(), d_preds_n.p, sizeof(uint64_t) * pn.size(), cudaMemcpyDeviceToHost,
                      ctx->stream));
+  CK(cudaMemcpyAsync(pin.data(), d_inner_n.p, sizeof(uint64_t) * pin.size(),
+                     cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  ctx->prog_inner_raw.assign(n, 0.0);
   // layout
   std::vector<ProgDev> progs(n);
   std::vector<uint32_t> stage;
@@ -238,15 +253,24 @@ int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
       mx = std::max(mx, sz);
     }
     stage.push_back(acc);
-    uint64_t pacc = 0;
+    uint64_t pacc = 0, iacc = 0;
+    uint32_t mxv = 1;
     for (int j = 2; j <= k; ++j) {
       pstart[(size_t)g * LP + j] = pacc;
       pacc += pn[(size_t)g * LP + j];
+      iacc += pin[(size_t)g * LP + j];
+      mxv = std::max(mxv, sizes[(size_t)g * LP + j]);
+    }
+    ctx->prog_inner_raw[g] = (double)iacc;
+    ctx->max_n1 = std::max<int>(ctx->max_n1, (int)sizes[(size_t)g * LP + 1]);
+    if (k >= 2) {
+      ctx->max_v = std::max<int>(ctx->max_v, (int)mxv);
+      ctx->max_rest = std::max<int>(ctx->max_rest, (int)(acc - sizes[(size_t)g * LP + 1]));
     }
     d.n_cells = acc;
     d.max_cells = mx;
     d.n_preds = pacc;
-    d.ok = mx <= 65536;
+    d.ok = mx < 65536;  // u16 indices plus the sentinel slot |N_j|
     if (!d.ok) ctx->progs_ok = false;
     cell_total += acc;
     pred_total += pacc;
@@ -280,6 +304,14 @@ int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->progs_h = progs;
   return AMP_OK;
+}
+
+// Dynamic smem of k_dp_multi<b> (mirror of its carve-up).
+size_t multi_smem_bytes(const amp_ctx* ctx, int b) {
+  const int L = ctx->L;
+  size_t d = sizeof(double) * (2 * (size_t)(ctx->max_v + 1) * b + 2 * (size_t)(L + 3) * b +
+                               (ctx->max_n1 + 1) + ctx->max_M + (L + 4));
+  return d + 2 * (size_t)b * ctx->max_rest + 16;  // two backpointer buffers
 }
 
 int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
@@ -400,6 +432,36 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
     return p->node_id[a] != p->node_id[b] ? p->node_id[a] < p->node_id[b] : a < b;
   });
 
+  // ---- bandwidth codes: rank of each link among the distinct bandwidths --
+  // (used by K_place and the K_dp edge tables; disabled with NaN links or
+  // more than 255 distinct values)
+  {
+    std::vector<double> vals(bw.begin(), bw.end());
+    bool nan = false;
+    for (double v : vals) nan |= std::isnan(v);
+    std::sort(vals.begin(), vals.end());
+    vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
+    ctx->n_codes = 0;
+    if (!nan && vals.size() <= 255 && std::getenv("AMP_NO_CODES") == nullptr) {
+      std::vector<uint8_t> code((size_t)D * D);
+      for (size_t x = 0; x < code.size(); ++x)
+        code[x] = (uint8_t)(std::lower_bound(vals.begin(), vals.end(), bw[x]) - vals.begin());
+      const int U = (int)vals.size();
+      // qtab[cls][code][c] = act[c-1] * mbs / vals[code] (optimizer.cpp:130-139)
+      const size_t qn = ctx->classes.size() * (size_t)U * L;
+      if (qn * sizeof(double) <= ((size_t)256 << 20)) {
+        std::vector<double> q(qn, 0.0);
+        for (size_t c = 0; c < ctx->classes.size(); ++c)
+          for (int u = 0; u < U; ++u)
+            for (int cut = 1; cut < L; ++cut)
+              q[(c * U + u) * L + cut] = act[cut - 1] * ctx->classes[c].mbs / vals[u];
+        CK(upload(ctx->bwcode, code.data(), code.size()));
+        CK(upload(ctx->bwval, vals.data(), vals.size()));
+        CK(upload(ctx->qtab, q.data(), q.size()));
+        ctx->n_codes = U;
+      }
+    }
+  }
   CK(upload(ctx->param, p->param_count, L));
   CK(upload(ctx->act, act.data(), act.size()));
   CK(upload(ctx->bw, bw.data(), bw.size()));
@@ -502,7 +564,7 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   if (sparse)  // scheduling/roofline weights: executed predecessor entries
     for (size_t c = 0; c < ctx->classes.size(); ++c)
       if (ctx->class_inner[c] > 0) {
-        ctx->class_inner[c] = ctx->prog_inner[ctx->class_prog[c]];
+        ctx->class_inner[c] = ctx->prog_inner_raw[ctx->class_prog[c]];
         ctx->class_lt[c] = 0;
       }
 
@@ -541,12 +603,45 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
     ctx->eval_threads = std::min(kEvalThreads, std::max(128, (ctx->max_M + 31) / 32 * 32));
     ctx->v_stride = 0;
   }
+  // K_dp multi (amp_dp_multi.cuh): B candidates of one class per group when
+  // B value arrays + backpointers fit two CTAs per SM.  AMP_DP_B=0 selects
+  // the per-candidate kernel (comparison runs).
+  ctx->multi_b = 0;
+  if (sparse) {
+    const char* eb = std::getenv("AMP_DP_B");
+    const int want = eb ? std::atoi(eb) : 4;
+    for (int b : {8, 4, 2}) {
+      if (b > want) continue;
+      const size_t sb = multi_smem_bytes(ctx, b);
+      if (sb <= 113 * 1024) {
+        ctx->multi_b = b;
+        ctx->smem_bytes = sb;
+        ctx->eval_threads = 256;
+        ctx->bp_stride = 0;
+        ctx->v_stride = 0;
+        break;
+      }
+    }
+  }
   if (ctx->smem_bytes > 227 * 1024) return fail(ctx, AMP_E_UNSUPPORTED, "shared memory budget");
   static const void* const kModes[] = {(const void*)k_dp<kDenseSS>, (const void*)k_dp<kDenseSG>,
                                        (const void*)k_dp<kDenseGS>, (const void*)k_dp<kDenseGG>,
                                        (const void*)k_dp<kSparseS>, (const void*)k_dp<kSparseG>};
   ctx->mode = mode;
   ctx->eval_fn = kModes[mode];
+  if (ctx->multi_b) {  // {cell, cellpred} records of every program
+    uint64_t cell_total = 0;
+    for (const ProgDev& d : ctx->progs_h) cell_total = std::max<uint64_t>(cell_total, d.cell_base + d.n_cells);
+    CK(ctx->cellrec.ensure(sizeof(uint2) * (cell_total + 1)));
+    if (cell_total) {
+      k_pack_cells<<<(int)std::min<uint64_t>((cell_total + 255) / 256, 4096), 256, 0, ctx->stream>>>(
+          ctx->cells.as<uint32_t>(), ctx->cellpred.as<uint32_t>(), ctx->cellrec.as<uint2>(), cell_total);
+      CK(cudaGetLastError());
+    }
+  }
+  if (ctx->multi_b == 2) ctx->eval_fn = (const void*)k_dp_multi<2>;
+  if (ctx->multi_b == 4) ctx->eval_fn = (const void*)k_dp_multi<4>;
+  if (ctx->multi_b == 8) ctx->eval_fn = (const void*)k_dp_multi<8>;
   CK(cudaFuncSetAttribute(ctx->eval_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)ctx->smem_bytes));
   int occ = 0;
@@ -578,6 +673,11 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
 }
 
 // Work list: the classes intersecting [begin, end), heaviest first.
+// Classes whose candidates go through K_dp (pp <= 2 is solved in K_est).
+bool is_heavy(const amp_ctx* ctx, uint64_t c) {
+  return ctx->classes[c].pp >= 3 && ctx->class_inner[c] > 0;
+}
+
 std::vector<Segment> make_segments(const amp_ctx* ctx, uint64_t begin, uint64_t end) {
   std::vector<std::pair<double, Segment>> v;
   const uint64_t P = ctx->P;
@@ -590,7 +690,9 @@ std::vector<Segment> make_segments(const amp_ctx* ctx, uint64_t begin, uint64_t 
     s.out = lo - begin;
     s.p0 = lo - c * P;
     s.cls = (int64_t)c;
-    v.emplace_back(ctx->class_inner[c], s);
+    // pp >= 3 classes (the only ones K_dp solves) lead the dispatch order
+    const double w = ctx->class_inner[c] + (is_heavy(ctx, c) ? 1e30 : 0.0);
+    v.emplace_back(w, s);
   }
   std::stable_sort(v.begin(), v.end(),
                    [](const auto& a, const auto& b) { return a.first > b.first; });
@@ -649,9 +751,10 @@ void account(amp_ctx* ctx, uint64_t begin, uint64_t end, const uint64_t* list, i
   }
   // FP64 ops of the executed recurrence.  Dense split form:
   // m >= seg: 2 DADD + DSETP; m < seg: DADD, DMUL, 3 DADD, DSETP.  Pruned
-  // form (generic recurrence): t2 DADD, x DADD, max DSETP, DMUL, 3 DADD, DSETP.
+  // form: the SURVEY §8(d) count of 7 FP64 ops per inner iteration (t2-dom,
+  // max, DMUL, 3 DADD, DSETP) over the executed (unpadded) iterations.
   const double ge = s.dp_inner - s.dp_inner_lt;
-  s.fp64_ops = ctx->sparse ? 8.0 * s.dp_inner : 3.0 * ge + 6.0 * s.dp_inner_lt;
+  s.fp64_ops = ctx->sparse ? 7.0 * s.dp_inner : 3.0 * ge + 6.0 * s.dp_inner_lt;
   s.bytes = 0;
 }
 
@@ -729,6 +832,9 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   ep.vbuf = ctx->vbuf.as<double>();
   ep.max_cells = ctx->max_cells;
   ep.max_prog_cells = ctx->max_prog_cells;
+  ep.max_n1 = ctx->max_n1;
+  ep.max_v = ctx->max_v;
+  ep.max_rest = ctx->max_rest;
   // chunk buffers (grown on demand up to ctx->chunk items)
   const uint64_t C = std::min<uint64_t>(ctx->chunk, std::max<uint64_t>(n_work, 1));
   CK(ctx->c_work.ensure(sizeof(CandWork) * C));
@@ -739,8 +845,24 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   ep.placeb = ctx->c_place.as<int32_t>();
   ep.bwqb = ctx->c_bwq.as<double>();
   ep.cutsb = ctx->c_cuts.as<uint8_t>();
+  CK(ctx->c_bwc.ensure((size_t)C * ctx->max_pp));
+  ep.bwcb = ctx->c_bwc.as<uint8_t>();
+  ep.n_codes = ctx->n_codes;
+  ep.bwcode = ctx->n_codes ? ctx->bwcode.as<uint8_t>() : nullptr;
+  ep.bwval = ctx->bwval.as<double>();
+  ep.qtab = ctx->n_codes ? ctx->qtab.as<double>() : nullptr;
+  ep.cellrec = ctx->cellrec.as<uint2>();
+  // items of pp >= 3 classes lead the dispatch order of a segment list
+  uint64_t n_heavy = n_work;
+  if (segs) {
+    n_heavy = 0;
+    for (const Segment& sg : *segs) {
+      if (!is_heavy(ctx, (uint64_t)sg.cls)) break;
+      n_heavy += sg.count;
+    }
+  }
   const int D = ctx->D, mp = ctx->max_pp;
-  const size_t place_smem = (D <= 32 ? sizeof(double) * D * D : 0) + sizeof(int) * 32 * 8;
+  const size_t place_smem = (D <= 32 ? (sizeof(double) + 1) * D * D : 0) + sizeof(int) * 32 * 8;
   size_t est_smem = (D <= 32 ? sizeof(double) * D * D : 0) +
                     sizeof(double) * 2 * mp * kEstWarps + sizeof(int) * (mp + 2) * kEstWarps;
   est_smem = ((est_smem + 15) & ~size_t(15)) + sizeof(EstWarp) * kEstWarps +
@@ -760,6 +882,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     CK(cudaEventRecord(ev[0], ctx->stream));
     ep.t0 = t0;
     ep.n_chunk = std::min<uint64_t>(C, n_work - t0);
+    ep.n_dp = n_heavy > t0 ? std::min<uint64_t>(ep.n_chunk, n_heavy - t0) : 0;
     ep.first_chunk = t0 == 0;
     const uint64_t warps = ep.n_chunk;
     const int place_grid = (int)std::min<uint64_t>((warps + 7) / 8, (uint64_t)ctx->sms * 16);
@@ -767,15 +890,18 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), ctx->stream));
     CK(cudaEventRecord(ev[1], ctx->stream));
-    void* args[] = {&ep};
-    CK(cudaLaunchKernel(ctx->eval_fn, dim3(ctx->n_ctas), dim3(ctx->eval_threads), args,
-                        ctx->smem_bytes, ctx->stream));
-    CK(cudaGetLastError());
+    if (ep.n_dp > 0) {
+      void* args[] = {&ep};
+      CK(cudaLaunchKernel(ctx->eval_fn, dim3(ctx->n_ctas), dim3(ctx->eval_threads), args,
+                          ctx->smem_bytes, ctx->stream));
+      CK(cudaGetLastError());
+      ctx->launches += 1;
+    }
     CK(cudaEventRecord(ev[2], ctx->stream));
     k_est<<<ctx->est_ctas, kEstWarps * 32, est_smem, ctx->stream>>>(ep);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev[3], ctx->stream));
-    ctx->launches += 3;
+    ctx->launches += 2;
   }
   return AMP_OK;
 }

@@ -22,5 +22,5 @@ with Searcher(enc, placements_per_class=Pp, seed=0, dense_dp=dense) as s:
         top, _, _ = s.run(0, n, k=10)
         st = s.stats()
         print(f"run {it}: {n} candidates in {st['kernel_ms']:.3f} ms kernel, "
-              f"{(time.perf_counter()-t0)*1e3:.1f} ms wall, inner={st['dp_inner']:.3e} "
+              f"{(time.perf_counter()-t0)*1e3:.1f} ms wall, place/dp/est {st['place_ms']:.2f}/{st['dp_ms']:.2f}/{st['est_ms']:.2f} ms, inner={st['dp_inner']:.3e} "
               f"fp64={st['fp64_ops']:.3e} best={top[0]['total']!r}")
