@@ -34,7 +34,9 @@ SCENARIO = "hetero_cluster"
 DEFAULT_N_PER_GPU = 10_000_000
 TOPK = 10
 METRIC = "candidate strategies/sec"
-TRAFFIC_BYTES_PER_CANDIDATE = 141.5  # ncu: k_dp dram__bytes_read+write / candidates
+# ncu --set full of one k_dp_multi launch (profiles/r1b_k_dp_multi_ncu.txt):
+# dram__bytes_read.sum + dram__bytes_write.sum / candidates of that launch
+TRAFFIC_BYTES_PER_DP_ITEM = 66.5  # 66.54 MB over the 1,000,000 items of launch 3
 UNIT = "candidates/s"
 
 
@@ -284,11 +286,15 @@ def our_arm(args):
                        "parallelism": f"index-range shards x{world}, NCCL all-gather of top-k"},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s",
                          "frac": achieved / peak_t,
-                         "traffic": TRAFFIC_BYTES_PER_CANDIDATE * n_total / max(1, st["launches"] // 3),
-                         "traffic_note": "dram read+write bytes per k_dp launch, scaled from the ncu "
-                                         "capture in profiles/r1_k_dp_ncu.txt (141.5 B/candidate, "
-                                         "cold cache); algorithmic bytes ~0 (L2-resident tables)",
-                         "kernel": "k_dp (pruned layer-partition DP)",
+                         "traffic": TRAFFIC_BYTES_PER_DP_ITEM * st["dp_items"] / max(1, st["dp_launches"]),
+                         "traffic_note": "dram read+write bytes per k_dp launch: ncu per-item figure "
+                                         "(profiles/r1b_k_dp_multi_ncu.txt) x items per launch; the "
+                                         "kernel is FP64/issue-bound, its tables are L2/L1-resident",
+                         "kernel": f"k_dp_multi<{st['dp_group']}> (pruned layer-partition DP, "
+                                   f"{st['dp_group']} candidates of one class per CTA group)",
+                         "fp64_ops_def": "7 per executed inner iteration (SURVEY.md 8(d)) over the "
+                                         "pruned program's iterations, per candidate",
+                         "dp_items_per_step": st["dp_items"], "dp_launches_per_step": st["dp_launches"],
                          "kernel_ms_per_step": kern_ms,
                          "pipeline_ms_per_step": {"k_place": place_ms, "k_dp": dp_ms, "k_est": est_ms},
                          "fp64_ops_per_step": st["fp64_ops"], "dp_inner_per_step": st["dp_inner"],

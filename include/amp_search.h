@@ -161,6 +161,9 @@ typedef struct amp_stats {
   double place_ms;           /* device time of K_place (all chunks)          */
   double dp_ms;              /* device time of K_dp (all chunks)             */
   double est_ms;             /* device time of K_est (all chunks)            */
+  uint64_t dp_items;         /* candidates that went through K_dp (pp >= 3)  */
+  int32_t dp_launches;       /* K_dp launches of the run                     */
+  int32_t dp_group;          /* K_dp candidates per group (0: one at a time) */
 } amp_stats;
 
 typedef struct amp_ctx amp_ctx;

@@ -117,6 +117,9 @@ class AmpStats(C.Structure):
         ("place_ms", C.c_double),
         ("dp_ms", C.c_double),
         ("est_ms", C.c_double),
+        ("dp_items", C.c_uint64),
+        ("dp_launches", C.c_int32),
+        ("dp_group", C.c_int32),
     ]
 
 

@@ -208,7 +208,7 @@ __device__ __forceinline__ void multi_stage(const int j, const uint32_t s0, cons
 // group is deferred into stage 2 of the next group (double-buffered
 // backpointers), where it overlaps with the other warps' cells.
 template <int B>
-__global__ void __launch_bounds__(256, 2) k_dp_multi(EvalParams p) {
+__global__ void __launch_bounds__(B >= 8 ? 512 : 256, (B <= 2 ? 3 : (B >= 8 ? 1 : 2))) k_dp_multi(EvalParams p) {
   static_assert(B % 2 == 0 && B <= 16, "B must be even (16-byte value/edge loads)");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int WW = sizeof(CandWork) / 8;  // 8-byte words per work record

@@ -355,13 +355,16 @@ constexpr int kEstWarps = 8;
 // keeps its first strict minimum, then a lexicographic (value, cut)
 // butterfly — the sequential strict-'<' scan.  Same operations and operand
 // order as sparse_solve / the reference.
-__device__ int light_cut2(const EvalParams& p, const ClassDev& cl, uint64_t u, int lane) {
+__device__ int light_cut2(const EvalParams& p, const ClassDev& cl, int cls, uint64_t u, int lane) {
   const int L = p.L, LP = L + 1;
   const double* Pf = p.prefix + (size_t)cl.pair * LP;
   const double* Dm = p.domain + (size_t)cl.pair * p.nv_stride;
   const uint16_t* sg = p.seg + (size_t)cl.pair * LP * LP;
   const double g1 = (double)(cl.gas - 1);
   const double bq = p.bwqb[u * p.max_pp];
+  // edge costs: the class's table of the same quotients when coded
+  const double* qt = p.qtab ? p.qtab + ((size_t)cls * p.n_codes + p.bwcb[u * p.max_pp]) * L
+                            : nullptr;
   const double dm0 = Dm[0], PL = Pf[L], P0 = Pf[0];
   double best = CUDART_INF;
   int bc = -1;
@@ -370,7 +373,7 @@ __device__ int light_cut2(const EvalParams& p, const ClassDev& cl, uint64_t u, i
     const double sub = g1 * max0(t1 - Dm[sg[c * LP + L]]) + t1;  // cost(c, 1, seg(c, L))
     const double t2 = PL - Pf[c];
     const double term = t2 > dm0 ? g1 * (t2 - dm0) : 0.0;
-    const double e = p.act[c - 1] * cl.mbs / bq;  // placement_edge_cost
+    const double e = qt ? qt[c] : p.act[c - 1] * cl.mbs / bq;  // placement_edge_cost
     const double g = ((sub + term) + t2) + e;
     if (g < best) {
       best = g;
@@ -394,7 +397,7 @@ struct EstWarp {
   int place[32];
 };
 
-__global__ void __launch_bounds__(kEstWarps * 32) k_est(EvalParams p) {
+__global__ void __launch_bounds__(kEstWarps * 32, 3) k_est(EvalParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int lock;
   __shared__ int n_top;
@@ -459,7 +462,7 @@ __global__ void __launch_bounds__(kEstWarps * 32) k_est(EvalParams p) {
       } else {
         // pp <= 2 never reaches K_dp: single stage, or the two-stage DP
         // solved here by the warp (light_cut2)
-        const int c1 = pp == 2 ? light_cut2(p, cl, u, lane) : p.L;
+        const int c1 = pp == 2 ? light_cut2(p, cl, w.cls, u, lane) : p.L;
         if (lane == 0) {
           cutsW[0] = 0;
           cutsW[1] = pp == 2 ? (int)(uint8_t)c1 : p.L;

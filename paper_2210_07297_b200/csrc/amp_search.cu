@@ -613,10 +613,10 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
     for (int b : {8, 4, 2}) {
       if (b > want) continue;
       const size_t sb = multi_smem_bytes(ctx, b);
-      if (sb <= 113 * 1024) {
+      if (sb <= (b <= 2 ? 75 : (b >= 8 ? 226 : 113)) * 1024) {
         ctx->multi_b = b;
         ctx->smem_bytes = sb;
-        ctx->eval_threads = 256;
+        ctx->eval_threads = b >= 8 ? 512 : 256;
         ctx->bp_stride = 0;
         ctx->v_stride = 0;
         break;
@@ -658,7 +658,7 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   if (ctx->max_ctas_cfg > 0) n_ctas = std::min(n_ctas, ctx->max_ctas_cfg);
   ctx->n_ctas = n_ctas;
   ctx->sms = prop.multiProcessorCount;
-  ctx->est_ctas = prop.multiProcessorCount * 4;  // 32 estimate warps per SM
+  ctx->est_ctas = prop.multiProcessorCount * 3;  // 3 x 8 estimate warps per SM (launch bounds)
   // chunk size: keep the per-chunk buffers within ~256 MB
   const size_t per_item = sizeof(CandWork) + sizeof(int32_t) * D + sizeof(double) * ctx->max_pp +
                           (ctx->max_pp + 1);
@@ -869,6 +869,9 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
              (kk <= 32 ? sizeof(amp_record) * kk : 0);
   if (est_smem > 48 * 1024)
     CK(cudaFuncSetAttribute(k_est, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)est_smem));
+  ctx->stats.dp_items = 0;
+  ctx->stats.dp_launches = 0;
+  ctx->stats.dp_group = ctx->multi_b;
   const int n_chunks = (int)((n_work + C - 1) / C);
   while ((int)ctx->kev.size() < 4 * n_chunks) {
     cudaEvent_t e;
@@ -890,7 +893,9 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), ctx->stream));
     CK(cudaEventRecord(ev[1], ctx->stream));
+    ctx->stats.dp_items += ep.n_dp;
     if (ep.n_dp > 0) {
+      ctx->stats.dp_launches += 1;
       void* args[] = {&ep};
       CK(cudaLaunchKernel(ctx->eval_fn, dim3(ctx->n_ctas), dim3(ctx->eval_threads), args,
                           ctx->smem_bytes, ctx->stream));

@@ -1,0 +1,90 @@
+"""Summarise a gpu_round.sh capture (gpurun_out/) into profiles/<tag>_*.
+
+usage: python tools/summarize_profiles.py <tag> [gpurun_out]
+
+  <tag>_launches_summary.csv  per-kernel launches / total time / share of the
+                              ncu launch list (gpu__time_duration.sum,
+                              --clock-control none: cold-cache, serialised —
+                              compare shares, not absolutes)
+  <tag>_k_dp_multi_ncu.txt    selected details + raw counters of the one
+                              `ncu --set full` capture, and the hottest source
+                              lines (tools/ncu_lines.py)
+"""
+import collections
+import csv
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+tag = sys.argv[1]
+src = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out")
+out = os.path.join(ROOT, "profiles")
+
+
+def rows(path):
+    with open(path) as f:
+        lines = [l for l in f if l.startswith('"')]
+    return list(csv.DictReader(lines))
+
+
+# ---- launch list ---------------------------------------------------------
+L = rows(os.path.join(src, "launches.csv"))
+agg = collections.OrderedDict()
+for r in L:
+    if r["Metric Name"] != "gpu__time_duration.sum":
+        continue
+    a = agg.setdefault(r["Kernel Name"], [0, 0.0])
+    a[0] += 1
+    a[1] += float(r["Metric Value"]) / 1e3
+tot = sum(v[1] for v in agg.values())
+with open(os.path.join(out, f"{tag}_launches_summary.csv"), "w") as f:
+    f.write("# ncu launch list: python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-dense "
+            "--no-e2e (tools/gpu_round.sh)\n")
+    f.write("# metric gpu__time_duration.sum, --clock-control none (cold-cache, serialised; compare "
+            "shares, not absolutes)\n")
+    f.write("kernel,launches,total_us,share\n")
+    for k, (n, us) in sorted(agg.items(), key=lambda t: -t[1][1]):
+        f.write(f'"{k}",{n},{us:.1f},{us / tot:.4f}\n')
+
+# ---- full capture --------------------------------------------------------
+want_details = ["Duration", "Compute (SM) Throughput", "Memory Throughput", "DRAM Throughput",
+                "Executed Ipc Active", "Issue Slots Busy", "Eligible Warps Per Scheduler",
+                "No Eligible", "Warp Cycles Per Issued Instruction", "Registers Per Thread",
+                "Dynamic Shared Memory Per Block", "Block Size", "Grid Size",
+                "Theoretical Occupancy", "Achieved Occupancy", "L1/TEX Hit Rate", "L2 Hit Rate"]
+det = rows(os.path.join(src, "kdp_full_details.csv"))
+raw = list(csv.reader(open(os.path.join(src, "kdp_full_raw.csv"))))
+raw = [r for r in raw if r and not r[0].startswith("==")]
+hdr, unit, val = raw[0], raw[1], raw[2]
+want_raw = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+            "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
+            "launch__grid_size", "launch__block_size"]
+kname = det[0]["Kernel Name"] if det else "?"
+lines_txt = ""
+try:
+    lib = os.path.join(ROOT, "paper_2210_07297_b200", "libamp_search.so")
+    mangled = "_ZN3amp10k_dp_multiILi4EEEvNS_10EvalParamsE"
+    lines_txt = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"),
+                                os.path.join(src, "kdp_full_sass.csv"), lib, mangled, "25"],
+                               capture_output=True, text=True).stdout
+except Exception as e:  # noqa: BLE001
+    lines_txt = f"(ncu_lines failed: {e})"
+with open(os.path.join(out, f"{tag}_k_dp_multi_ncu.txt"), "w") as f:
+    f.write("# ncu --set full --clock-control none --import-source on -k regex:k_dp_multi -s 2 -c 1 "
+            "python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-dense --no-e2e\n")
+    f.write(f"# kernel: {kname} (3rd K_dp launch of the bench workload: a heavy chunk)\n\n## details\n")
+    for r in det:
+        if r["Metric Name"] in want_details:
+            f.write(f'{r["Section Name"]} | {r["Metric Name"]} | {r["Metric Unit"]} | '
+                    f'{r["Metric Value"]}\n')
+    f.write("\n## raw\n")
+    for name in want_raw:
+        if name in hdr:
+            i = hdr.index(name)
+            f.write(f"{name} {unit[i]} {val[i]}\n")
+    f.write("\n## hottest source lines (tools/ncu_lines.py)\n")
+    f.write(lines_txt)
+print("wrote", tag)
