@@ -202,11 +202,11 @@ def our_arm(args):
     n_total, P_ = workload(args.n_per_gpu, world)
     enc = P.EncodedProblem.from_scenario(sc)
     s = Searcher(enc, placements_per_class=P_, seed=0, device=local)
-    N_all = s.num_candidates
-    bounds = s.partition(world)
-    bounds[-1] = n_total  # truncate the class-major space to exactly n_total
-    bounds = [min(b, n_total) for b in bounds]
-    lo, hi = bounds[rank], bounds[rank + 1]
+    # the whole class-major space (70 classes x P_ placements, >= n_total);
+    # rank r evaluates placements [P*r/N, P*(r+1)/N) of every class
+    # (amp_search_run_device_shard): every rank gets the same class mix
+    n_total = s.num_candidates
+    n_mine = s.shard_size(rank, world)
     stream = torch.cuda.current_stream()
     k = TOPK
     local_top = torch.empty(k * 64, dtype=torch.uint8, device="cuda")
@@ -215,7 +215,7 @@ def our_arm(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def step():
-        s.run_device(lo, hi, k, local_top.data_ptr(), stream.cuda_stream)
+        s.run_device_shard(rank, world, k, local_top.data_ptr(), stream.cuda_stream)
         if distributed:
             dist.all_gather_into_tensor(gathered, local_top)
             s.merge_device(gathered.data_ptr(), world * k, k, final.data_ptr(), stream.cuda_stream)
@@ -268,7 +268,7 @@ def our_arm(args):
     # ---- e2e through the C-ABI with host buffers ------------------------
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_arm(args, enc, P_, lo, hi, n_total, world, rank, local, distributed)
+        e2e = e2e_arm(args, enc, P_, n_total, world, rank, local, distributed)
 
     dense = None
     if world == 1 and not args.no_dense:
@@ -283,7 +283,10 @@ def our_arm(args):
                        "scenario": SCENARIO, "candidates_per_step": n_total,
                        "candidates_per_gpu": args.n_per_gpu, "placements_per_class": P_,
                        "topk": k, "l2": "flushed (256 MiB write) before every timed step",
-                       "parallelism": f"index-range shards x{world}, NCCL all-gather of top-k"},
+                       "candidates_this_rank": n_mine,
+                       "parallelism": f"per-class placement-slice shards x{world} "
+                                      "(amp_search_run_device_shard), NCCL all-gather of the "
+                                      "k-record top-k + device merge"},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s",
                          "frac": achieved / peak_t,
                          "traffic": TRAFFIC_BYTES_PER_DP_ITEM * st["dp_items"] / max(1, st["dp_launches"]),
@@ -349,13 +352,15 @@ def dense_leg(enc, local, n=1_000_000):
                          "unit": "TFLOP/s", "frac": ach / (peak.value / 1e12)}}
 
 
-def e2e_arm(args, enc, P_, lo, hi, n_total, world, rank, local, distributed):
-    """Same metric through the public C-ABI per step: amp_search_create from
-    HOST arrays (H2D of the problem), amp_search_run to a HOST top-k (D2H),
-    destroy — wall clock, max over ranks."""
+def e2e_arm(args, enc, P_, n_total, world, rank, local, distributed):
+    """Same metric through the public API per step, from HOST arrays to a
+    HOST top-k: amp_search_create (H2D of the problem, K0 tables), the
+    sharded run + NCCL all-gather + device merge (distributed.search_gpu_sharded),
+    the D2H of the k-record result, destroy — wall clock, max over ranks."""
     import torch
     import torch.distributed as dist
 
+    from paper_2210_07297_b200 import distributed as Dd
     from paper_2210_07297_b200.planner import Searcher
     k = TOPK
     h2d = (enc.param.nbytes + enc.flops.nbytes + enc.flops_ok.nbytes + enc.act.nbytes +
@@ -367,7 +372,7 @@ def e2e_arm(args, enc, P_, lo, hi, n_total, world, rank, local, distributed):
             dist.barrier()
         t0 = time.perf_counter()
         s = Searcher(enc, placements_per_class=P_, seed=0, device=local)
-        top, _, _ = s.run(lo, hi, k=k)
+        top = Dd.search_gpu_sharded(s, k, rank, world)
         s.close()
         dt = time.perf_counter() - t0
         if i == 0:
@@ -381,8 +386,9 @@ def e2e_arm(args, enc, P_, lo, hi, n_total, world, rank, local, distributed):
         best = min(best, dt)
     return {"value": n_total / best, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "s_per_step": best,
+            "best_index": int(top[0]["index"]) if len(top) else None,
             "note": "wall clock per step: amp_search_create (host arrays -> HBM, K0 tables) + "
-                    "amp_search_run (host top-k) + destroy"}
+                    "sharded run + all-gather/merge + host top-k + destroy"}
 
 
 def main():

@@ -208,6 +208,14 @@ int amp_search_evaluate(amp_ctx* ctx, const uint64_t* indices, int32_t n,
  * host synchronisation.                                                   */
 int amp_search_run_device(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k,
                           amp_record* d_topk, void* stream);
+/* Shard `shard` of n_shards (multi-GPU): placements
+ * [P*shard/n, P*(shard+1)/n) of EVERY class, so all shards carry the same
+ * class mix; the union over shards is the whole space and the merged top-k
+ * equals the single-GPU one.  Device-resident like amp_search_run_device.  */
+int amp_search_run_device_shard(amp_ctx* ctx, int32_t shard, int32_t n_shards, int32_t k,
+                                amp_record* d_topk, void* stream);
+/* Candidates in shard `shard` of n_shards. */
+uint64_t amp_search_shard_size(const amp_ctx* ctx, int32_t shard, int32_t n_shards);
 
 /* Merge n_in device records — n_in / k lists of k records, each sorted by
  * the ranking key and padded at its end (e.g. the all-gathered per-GPU

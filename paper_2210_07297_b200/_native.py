@@ -152,6 +152,9 @@ SIGNATURES = [
                                       C.POINTER(AmpDetails)]),
     ("amp_search_run_device", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int32, C.c_void_p,
                                         C.c_void_p]),
+    ("amp_search_run_device_shard", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                              C.c_void_p, C.c_void_p]),
+    ("amp_search_shard_size", C.c_uint64, [C.c_void_p, C.c_int32, C.c_int32]),
     ("amp_search_merge_topk_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                                C.c_void_p, C.c_void_p]),
     ("amp_search_last_stats", C.c_int, [C.c_void_p, C.POINTER(AmpStats)]),

@@ -1,8 +1,12 @@
-"""Multi-GPU search: one process per GPU, candidates sharded by index range.
+"""Multi-GPU search: one process per GPU, candidates sharded across ranks.
 
-SURVEY.md §8(e): candidates are independent, so each rank evaluates a
-contiguous, work-weighted slice of the class-major index space
-(amp_search_partition) and keeps its local top-k on the device; the only
+SURVEY.md §8(e): candidates are independent, so each rank evaluates its own
+part of the class-major index space and keeps its local top-k on the
+device.  Two splits: the per-class placement slice (`search_gpu_sharded`,
+amp_search_run_device_shard: rank r takes placements [P*r/n, P*(r+1)/n) of
+EVERY class, so every rank gets the same class mix — the bench's split) and
+the contiguous work-weighted index range (`search_gpu`,
+amp_search_partition).  The only
 exchange is one all-gather of the k records per rank (NCCL over NVLink on
 GPUs, gloo in the CPU tests) followed by a deterministic merge under the
 reference ranking key (failed, total, index) — identical for any world size.
@@ -53,6 +57,34 @@ def search_gpu(searcher, k: int, bounds: Sequence[int], rank: int, world: int, g
     return recs[recs["fail_code"] >= 0]
 
 
+def search_gpu_sharded(searcher, k: int, rank: int, world: int, group=None):
+    """Evaluate this rank's per-class placement slice on the GPU, all-gather
+    the device top-k (NCCL) and merge on the device.  Returns the global
+    top-k (host)."""
+    import torch
+    import torch.distributed as dist
+
+    stream = torch.cuda.current_stream()
+    local = torch.empty(k * RECORD_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    searcher.run_device_shard(rank, world, k, local.data_ptr(), stream.cuda_stream)
+    if world == 1:
+        out = local
+    else:
+        gathered = torch.empty(world * k * RECORD_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+        dist.all_gather_into_tensor(gathered, local, group=group)
+        out = torch.empty_like(local)
+        searcher.merge_device(gathered.data_ptr(), world * k, k, out.data_ptr(), stream.cuda_stream)
+    recs = np.frombuffer(out.cpu().numpy().tobytes(), dtype=RECORD_DTYPE)
+    return recs[recs["fail_code"] >= 0]
+
+
+def class_slice_ranges(n_classes: int, P: int, shard: int, n_shards: int) -> List[tuple]:
+    """Index ranges of shard `shard` in the per-class placement split (mirror
+    of amp_search_run_device_shard): [c*P + P*shard/n, c*P + P*(shard+1)/n)."""
+    p0, p1 = P * shard // n_shards, P * (shard + 1) // n_shards
+    return [(c * P + p0, c * P + p1) for c in range(n_classes) if p1 > p0]
+
+
 def search_host(evaluate: Callable[[int, int], np.ndarray], k: int, bounds: Sequence[int], rank: int,
                 world: int, group=None) -> np.ndarray:
     """Same exchange with a host evaluator (tests / gloo): each rank ranks its
@@ -60,7 +92,11 @@ def search_host(evaluate: Callable[[int, int], np.ndarray], k: int, bounds: Sequ
     import torch
     import torch.distributed as dist
 
-    recs = evaluate(bounds[rank], bounds[rank + 1])
+    if isinstance(bounds[0], (list, tuple)):  # a list of ranges per rank (class slices)
+        parts = [evaluate(lo, hi) for lo, hi in bounds[rank]]
+        recs = np.concatenate(parts) if parts else np.zeros(0, dtype=RECORD_DTYPE)
+    else:
+        recs = evaluate(bounds[rank], bounds[rank + 1])
     local = np.zeros(k, dtype=RECORD_DTYPE)
     local["fail_code"] = -1
     local["index"] = np.iinfo(np.uint64).max

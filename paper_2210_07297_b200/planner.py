@@ -189,6 +189,16 @@ class Searcher:
         N.check(self.lib.amp_search_run_device(self.ctx, begin, end, k, C.c_void_p(d_topk_ptr),
                                                C.c_void_p(stream_ptr)), self.ctx)
 
+    def run_device_shard(self, shard: int, n_shards: int, k: int, d_topk_ptr: int,
+                         stream_ptr: int = 0):
+        """Placements [P*shard/n, P*(shard+1)/n) of every class (multi-GPU shard)."""
+        N.check(self.lib.amp_search_run_device_shard(self.ctx, shard, n_shards, k,
+                                                     C.c_void_p(d_topk_ptr), C.c_void_p(stream_ptr)),
+                self.ctx)
+
+    def shard_size(self, shard: int, n_shards: int) -> int:
+        return int(self.lib.amp_search_shard_size(self.ctx, shard, n_shards))
+
     def merge_device(self, d_in_ptr: int, n_in: int, k: int, d_out_ptr: int, stream_ptr: int = 0):
         N.check(self.lib.amp_search_merge_topk_device(self.ctx, C.c_void_p(d_in_ptr), n_in, k,
                                                       C.c_void_p(d_out_ptr), C.c_void_p(stream_ptr)),

@@ -50,7 +50,7 @@ def _worker(rank, world, port, bounds, k, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("split", ["even", "skewed"])
+@pytest.mark.parametrize("split", ["even", "skewed", "class-slice"])
 def test_gloo_two_rank_merge_matches_single_process(tmp_path, split):
     from oracle import bindings as B
     from paper_2210_07297_b200 import distributed as Dd
@@ -63,7 +63,10 @@ def test_gloo_two_rank_merge_matches_single_process(tmp_path, split):
     recs, _ = o.run(0, n, threads=4, details=False)
     k = 12
     want = Dd.merge_topk_host(recs, k)
-    bounds = [0, n // 2, n] if split == "even" else [0, 37, n]
+    if split == "class-slice":  # the bench's split (amp_search_run_device_shard)
+        bounds = [Dd.class_slice_ranges(n // 6, 6, r, 2) for r in range(2)]
+    else:
+        bounds = [0, n // 2, n] if split == "even" else [0, 37, n]
     out = str(tmp_path / "top.npy")
     mp.spawn(_worker, args=(2, _free_port(), bounds, k, out), nprocs=2, join=True)
     got = np.load(out)

@@ -220,3 +220,29 @@ def test_simulator_matches_reference():
             mine = simulator.simulate(s, sc.model, sc.cluster, sc.profile, sc.gbs, sc.options.cost_options, enc)
             ref = B.ref_simulate(enc, s.pp, s.dp, s.tmp, s.mbs, s.placement, s.cut_boundaries)
             assert mine == ref
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_shards", [2, 3, 8])
+def test_class_slice_shards_merge_to_single_run(n_shards):
+    """Per-class placement-slice shards (amp_search_run_device_shard, the
+    bench's multi-GPU split) cover the space exactly once and merge to the
+    single-run top-k."""
+    import torch
+    sc = scenario("hetero_cluster")
+    enc = P.EncodedProblem.from_scenario(sc)
+    k = 12
+    with planner.Searcher(enc, placements_per_class=101, seed=5) as s:
+        N_ = s.num_candidates
+        whole, _, _ = s.run(0, N_, k=k)
+        assert sum(s.shard_size(r, n_shards) for r in range(n_shards)) == N_
+        st = torch.cuda.current_stream().cuda_stream
+        parts = torch.empty((n_shards, k * 64), dtype=torch.uint8, device="cuda")
+        for r in range(n_shards):
+            s.run_device_shard(r, n_shards, k, parts[r].data_ptr(), st)
+        out = torch.empty(k * 64, dtype=torch.uint8, device="cuda")
+        s.merge_device(parts.data_ptr(), n_shards * k, k, out.data_ptr(), st)
+        torch.cuda.synchronize()
+        merged = np.frombuffer(out.cpu().numpy().tobytes(), dtype=planner.RECORD_DTYPE)
+    assert merged["index"].tolist() == whole["index"].tolist()
+    assert np.array_equal(merged["total"], whole["total"])
