@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense-DP comparison leg")
+    ap.add_argument("--no-wall-time", action="store_true",
+                    help="skip the C1-C4 plan() wall-time leg (ours vs the reference)")
     return ap.parse_args()
 
 
@@ -178,6 +180,48 @@ def reference_arm(args):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def search_wall_time(budget=10):
+    """The metric's second half: AMP search wall time of plan() for C1-C4 —
+    the drop-in (planner.plan: create from host arrays, K0/K0b, evaluate,
+    rank, simulate the top `budget`) vs the reference parplan::plan
+    (oracle/_ref, all host threads), same inputs; the argmin and the whole
+    ranking must be identical."""
+    from oracle import bindings as B
+    from paper_2210_07297_b200 import planner, problem as P
+    out = {}
+    names = {"C1": "homogeneous", "C2": "hetero_cluster", "C3": "hetero_model", "C4": "synthetic96"}
+    for tag, name in names.items():
+        sc = P.synthetic_c4() if name == "synthetic96" else P.load_scenario(
+            os.path.join(ROOT, "tests", "golden", "scenarios", name + ".json"))
+        opts = P.PlanOptions(budget=budget, cost_options=sc.options.cost_options,
+                             max_params_per_device=sc.options.max_params_per_device)
+        planner.plan(sc.model, sc.cluster, sc.profile, sc.gbs, opts)  # warm-up
+        ts = []
+        for _ in range(5 if tag != "C4" else 3):
+            t0 = time.perf_counter()
+            res = planner.plan(sc.model, sc.cluster, sc.profile, sc.gbs, opts)
+            ts.append(time.perf_counter() - t0)
+        e = {"workload": name, "candidates": len(res.candidates), "budget": budget,
+             "ours_s": min(ts), "best": list(res.candidates[res.best_index].strategy.degrees)
+             if res.best_index >= 0 else None}
+        if B.ref_available():
+            enc = P.EncodedProblem.from_scenario(sc, opts)
+            max_pp = max(c[0] for c in P.candidate_classes(sc.cluster.device_count(), sc.gbs))
+            rs = []
+            for _ in range(3 if tag != "C4" else 1):
+                t0 = time.perf_counter()
+                r = B.ref_plan(enc, max_pp, budget=budget, workers=os.cpu_count() or 1)
+                rs.append(time.perf_counter() - t0)
+            e["reference_s"] = min(rs)
+            e["reference_threads"] = os.cpu_count()
+            e["same_argmin"] = bool(r["best_index"] == res.best_index)
+            e["same_ranking"] = bool([int(x) for x in r["records"]["index"]] ==
+                                     [c.index for c in res.candidates])
+            e["speedup"] = e["reference_s"] / e["ours_s"]
+        out[tag] = e
+    return out
 
 
 def l2_flush(buf):
@@ -313,6 +357,8 @@ def our_arm(args):
             line["e2e"] = e2e
         if dense:
             line["dense_dp"] = dense
+        if world == 1 and not args.no_wall_time:
+            line["search_wall_time"] = search_wall_time()
         if world == 1 and not args.no_cpu_baseline:
             v, dt, kind, th, ns = run_cpu_reference(sc, n_total, P_, args.cpu_sample, os.cpu_count() or 1)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": th, "kind": kind,

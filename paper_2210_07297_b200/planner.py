@@ -285,15 +285,27 @@ def plan(model: ModelGraph, cluster: Cluster, profile: ProfileTable, gbs: int,
     if tm is not None:
         tm["decode"] = time.perf_counter() - t
         t = time.perf_counter()
-    # validate the top `budget` with the simulator (optimizer.cpp:235-249)
-    for i in range(min(len(cands), max(0, options.budget))):
-        rec = cands[i]
-        if rec.failure is not None:
-            continue
-        rec.simulated = simulator.simulate(rec.strategy, model, cluster, profile, gbs,
-                                           options.cost_options, encoded=enc)
-        if result.best_index < 0 or rec.simulated < cands[result.best_index].simulated:
-            result.best_index = i
+    # validate the top `budget` with the simulator (optimizer.cpp:235-249):
+    # the simulations are independent (ctypes releases the GIL), so they run
+    # on a thread pool; best_index is then the first strict minimum in rank
+    # order, as in the reference's sequential loop
+    todo = [i for i in range(min(len(cands), max(0, options.budget))) if cands[i].failure is None]
+    if todo:
+        from concurrent.futures import ThreadPoolExecutor
+
+        def sim(i):
+            return simulator.simulate(cands[i].strategy, model, cluster, profile, gbs,
+                                      options.cost_options, encoded=enc)
+        workers = min(len(todo), options.workers or (os.cpu_count() or 1))
+        if workers > 1:
+            with ThreadPoolExecutor(max_workers=workers) as ex:
+                sims = list(ex.map(sim, todo))
+        else:
+            sims = [sim(i) for i in todo]
+        for i, v in zip(todo, sims):
+            cands[i].simulated = v
+            if result.best_index < 0 or v < cands[result.best_index].simulated:
+                result.best_index = i
     if tm is not None:
         tm["simulate"] = time.perf_counter() - t
         print("plan timing (ms):", {k: round(v * 1e3, 3) for k, v in tm.items()})
