@@ -1,0 +1,60 @@
+// gen_report.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// Writes the reference's own report.json for a plan() run
+// (report.cpp:28-53 write_report, the CLI `plan` path of
+// parplan_main.cpp:196-216), so tests/golden/report_*.json pin the drop-in
+// CLI's report byte for byte.  Built by oracle/Makefile (_ref/gen_report)
+// from the reference sources where they lie, with nlohmann/json 3.11.3 from
+// the venv (the reference's vendored copy is absent).
+//
+//   gen_report <model> <cluster> <profile> <gbs> <budget> <out.json>
+//              [fallback_device_flops fallback_tmp_bw] [max_params]
+// Exit codes follow the CLI: 1 error, 3 all candidates failed on a profile
+// miss (parplan_main.cpp:73-82).
+#include <cstdlib>
+#include <iostream>
+#include <string>
+
+#include "parplan/json_io.hpp"
+#include "parplan/optimizer.hpp"
+#include "parplan/report.hpp"
+
+int main(int argc, char** argv) {
+  if (argc < 7) {
+    std::cerr << "usage: gen_report model cluster profile gbs budget out [flops tmp_bw] [max]\n";
+    return 1;
+  }
+  try {
+    const parplan::ModelGraph model = parplan::load_model(argv[1]);
+    const parplan::Cluster cluster = parplan::load_cluster(argv[2]);
+    const parplan::ProfileTable profile = parplan::load_profile(argv[3]);
+    parplan::PlanOptions opts;
+    opts.budget = std::atoi(argv[5]);
+    opts.workers = 0;
+    if (argc >= 9) {
+      const double flops = std::atof(argv[7]), bw = std::atof(argv[8]);
+      if (flops > 0) {
+        opts.cost_options.fallback.enabled = true;
+        opts.cost_options.fallback.device_flops = flops;
+        if (bw > 0) opts.cost_options.fallback.tmp_bandwidth = bw;
+      }
+    }
+    if (argc >= 10 && std::atof(argv[9]) > 0) opts.max_params_per_device = std::atof(argv[9]);
+    const parplan::PlanResult r = parplan::plan(model, cluster, profile, std::atoi(argv[4]), opts);
+    bool any_ok = false;
+    for (const auto& c : r.candidates) any_ok |= !c.failure;
+    if (!any_ok) {
+      const std::string why = r.candidates.empty() ? "no candidates" : *r.candidates.front().failure;
+      std::cerr << "error: every candidate failed; first failure: " << why << "\n";
+      return why.find("profile miss") != std::string::npos ? 3 : 1;
+    }
+    parplan::write_report(r.candidates, argv[6]);
+    parplan::print_candidate_table(std::cout, r.candidates);
+    if (r.best_index >= 0)
+      std::cout << "best by simulation: rank " << r.candidates[r.best_index].rank << "\n";
+  } catch (const std::exception& e) {
+    std::cerr << "error: " << e.what() << "\n";
+    return 1;
+  }
+  return 0;
+}

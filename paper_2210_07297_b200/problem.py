@@ -83,6 +83,14 @@ class ProfileTable:
     def __len__(self) -> int:
         return len(self.layer)
 
+    def entries(self):
+        """std::map<ProfileKey, double> view: last set() wins, ordered by
+        (layer, tmp, mbs) (types.hpp:81-100)."""
+        d = {}
+        for l, t, m, v in zip(self.layer, self.tmp, self.mbs, self.seconds):
+            d[(l, t, m)] = v
+        return sorted(d.items())
+
 
 @dataclass
 class AnalyticFallback:
@@ -199,6 +207,72 @@ def profile_from_json(j: dict) -> ProfileTable:
             raise ValidationError(f"entries[{i}].seconds: profile times must be >= 0")
         t.set(int(e["layer"]), int(e["tmp"]), int(e["mbs"]), seconds)
     return t
+
+
+def model_to_json(model: ModelGraph) -> dict:
+    """json_io.cpp:177-187"""
+    layers = []
+    for l in model.layers:
+        e = {"id": int(l.id), "kind": l.kind, "param_count": float(l.param_count)}
+        if l.flops_per_sample is not None:
+            e["flops_per_sample"] = float(l.flops_per_sample)
+        layers.append(e)
+    return {"layers": layers, "activation_volumes": [float(v) for v in model.activation_volumes]}
+
+
+def cluster_to_json(cluster: Cluster) -> dict:
+    """json_io.cpp:189-199: the +inf self-link is written as 0.0."""
+    bw = np.array(cluster.bandwidth, dtype=np.float64).copy()
+    for i in range(min(bw.shape)):
+        bw[i, i] = 0.0
+    return {"devices": [{"id": d.id, "node_id": d.node_id, "device_type": d.device_type}
+                        for d in cluster.devices],
+            "bandwidth": [[float(x) for x in row] for row in bw]}
+
+
+def profile_to_json(profile: ProfileTable) -> dict:
+    """json_io.cpp:201-208"""
+    return {"entries": [{"layer": l, "tmp": t, "mbs": m, "seconds": float(v)}
+                        for (l, t, m), v in profile.entries()]}
+
+
+def write_json_file(obj, path: str) -> None:
+    """write_file (json_io.cpp:49-55): nlohmann dump(2) + newline."""
+    from .jsonfmt import dumps
+    try:
+        with open(path, "w") as f:
+            f.write(dumps(obj) + "\n")
+    except OSError:
+        raise ParseError(f"cannot open file for writing: {path}")
+
+
+def layer_activation_volume(model: ModelGraph, layer: int) -> float:
+    """ModelGraph::layer_activation_volume (types.cpp:42-50)."""
+    n = model.layer_count()
+    if n <= 1:
+        return 0.0
+    return float(model.activation_volumes[layer if layer < n - 1 else layer - 1])
+
+
+def allreduce_time(workers: int, message_size: float, bandwidth: float) -> float:
+    """cost_model.cpp:40-52: ((2.0*(n-1))*M)/(n*B)."""
+    if workers < 1:
+        raise ValidationError("all-reduce needs at least one worker")
+    if workers == 1:
+        return 0.0
+    if not bandwidth > 0:
+        raise ValidationError(f"invalid bandwidth {bandwidth:f} in all-reduce group")
+    return 2.0 * (workers - 1) * message_size / (workers * bandwidth)
+
+
+def analytic_layer_time(layer: LayerSpec, tmp: int, mbs: int, device_flops: float,
+                        message_size: float, bandwidth: float) -> float:
+    """cost_model.cpp:61-68 (raises ProfileMissError-like ValidationError
+    when the layer has no flops)."""
+    if layer.flops_per_sample is None:
+        raise ValidationError(f"profile miss: layer={layer.id} tmp={tmp} mbs={mbs}")
+    compute = mbs * layer.flops_per_sample / (tmp * device_flops)
+    return compute + allreduce_time(tmp, message_size, bandwidth)
 
 
 def load_model(path: str) -> ModelGraph:
