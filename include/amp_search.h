@@ -143,6 +143,9 @@ typedef struct amp_details {
   double* stage_times;
   double* edge_times;
   int32_t* placement;
+  double* simulated;   /* [n] simulate() iteration time (simulator.cpp:140-198),
+                          NaN for failed candidates; runs the batched
+                          simulator on the device      */
 } amp_details;
 
 /* Counters of the last amp_search_run* call (roofline accounting). */
@@ -206,6 +209,13 @@ int amp_search_evaluate(amp_ctx* ctx, const uint64_t* indices, int32_t n,
  * (padded with fail_code = -1, index = UINT64_MAX) to device memory
  * d_topk on `stream` (cudaStream_t, NULL = legacy default stream).  No
  * host synchronisation.                                                   */
+/* Estimate only (K_place -> K_est, no DP): candidates `indices` with the
+ * caller's layer cuts cuts[i * (max_pp + 1) + 0 .. pp] (0 = c_0 < ... <
+ * c_pp = n_layers).  The Megatron baseline path (optimizer.cpp:253-279:
+ * uniform / parameter-balanced cuts through estimate(),
+ * cost_model.cpp:176-212).  Host buffers, records in input order.          */
+int amp_search_estimate(amp_ctx* ctx, const uint64_t* indices, const int32_t* cuts, int32_t n,
+                        amp_record* out, const amp_details* details);
 int amp_search_run_device(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k,
                           amp_record* d_topk, void* stream);
 /* Shard `shard` of n_shards (multi-GPU): placements

@@ -9,9 +9,12 @@
 //
 //   gen_report <model> <cluster> <profile> <gbs> <budget> <out.json>
 //              [fallback_device_flops fallback_tmp_bw] [max_params]
+//   GEN_MODE=layer-balance|param-balance: the CLI `baseline` path instead
+//   (megatron_baseline, optimizer.cpp:253-279; parplan_main.cpp:285-296)
 // Exit codes follow the CLI: 1 error, 3 all candidates failed on a profile
 // miss (parplan_main.cpp:73-82).
 #include <cstdlib>
+#include <cstring>
 #include <iostream>
 #include <string>
 
@@ -40,6 +43,22 @@ int main(int argc, char** argv) {
       }
     }
     if (argc >= 10 && std::atof(argv[9]) > 0) opts.max_params_per_device = std::atof(argv[9]);
+    if (const char* mode = std::getenv("GEN_MODE")) {
+      const auto bal = std::strcmp(mode, "param-balance") == 0 ? parplan::BalanceMode::kParamBalance
+                                                               : parplan::BalanceMode::kLayerBalance;
+      const auto cands = parplan::megatron_baseline(model, cluster, profile, std::atoi(argv[4]), bal,
+                                                    opts.cost_options);
+      bool ok = false;
+      for (const auto& c : cands) ok |= !c.failure;
+      if (!ok) {
+        const std::string why = cands.empty() ? "no candidates" : *cands.front().failure;
+        std::cerr << "error: every candidate failed; first failure: " << why << "\n";
+        return why.find("profile miss") != std::string::npos ? 3 : 1;
+      }
+      parplan::write_report(cands, argv[6]);
+      parplan::print_candidate_table(std::cout, cands);
+      return 0;
+    }
     const parplan::PlanResult r = parplan::plan(model, cluster, profile, std::atoi(argv[4]), opts);
     bool any_ok = false;
     for (const auto& c : r.candidates) any_ok |= !c.failure;

@@ -98,6 +98,7 @@ class AmpDetails(C.Structure):
         ("stage_times", _dp),
         ("edge_times", _dp),
         ("placement", _ip),
+        ("simulated", _dp),
     ]
 
 
@@ -149,6 +150,8 @@ SIGNATURES = [
     ("amp_search_run", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int32,
                                  C.POINTER(AmpRecord), _ip, C.POINTER(AmpRecord), C.POINTER(AmpDetails)]),
     ("amp_search_evaluate", C.c_int, [C.c_void_p, _u64p, C.c_int32, C.POINTER(AmpRecord),
+                                      C.POINTER(AmpDetails)]),
+    ("amp_search_estimate", C.c_int, [C.c_void_p, _u64p, _ip, C.c_int32, C.POINTER(AmpRecord),
                                       C.POINTER(AmpDetails)]),
     ("amp_search_run_device", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int32, C.c_void_p,
                                         C.c_void_p]),

@@ -96,6 +96,11 @@ def _parser() -> argparse.ArgumentParser:
     p.add_argument("--max-params-per-device", type=float, default=0.0,
                    help="fail candidates whose per-device parameter count exceeds this")
     p.add_argument("--device", type=int, default=0, help="CUDA device (engine option)")
+    b = sub.add_parser("baseline", help="Megatron-style heuristic candidates")
+    _add_common(b)
+    b.add_argument("--mode", default="layer-balance", choices=["layer-balance", "param-balance"])
+    b.add_argument("--report", default="report.json", help="output report path")
+    b.add_argument("--device", type=int, default=0, help="CUDA device (engine option)")
     g = sub.add_parser("gen-profile", help="generate a synthetic profile table from per-layer flops")
     g.add_argument("--model", required=True)
     g.add_argument("--device-flops", required=True, type=_positive_float)
@@ -125,6 +130,22 @@ def cmd_plan(a) -> int:
     return 0
 
 
+def cmd_baseline(a) -> int:
+    """parplan_main.cpp:285-296 over baseline.megatron_baseline."""
+    from . import baseline
+    model = P.load_model(a.model)
+    cluster = P.load_cluster(a.cluster)
+    profile = P.load_profile(a.profile)
+    cands = baseline.megatron_baseline(model, cluster, profile, a.gbs, a.mode, _cost_options(a),
+                                       device=a.device)
+    st = _abort_if_all_failed(cands)
+    if st:
+        return st
+    R.write_report(cands, a.report)
+    R.print_candidate_table(sys.stdout, cands)
+    return 0
+
+
 def cmd_gen_profile(a) -> int:
     """parplan_main.cpp:170-188 with analytic_layer_time (cost_model.cpp:61-68)."""
     model = P.load_model(a.model)
@@ -146,6 +167,8 @@ def main(argv: Optional[List[str]] = None) -> int:
     try:
         if a.cmd == "plan":
             return cmd_plan(a)
+        if a.cmd == "baseline":
+            return cmd_baseline(a)
         if a.cmd == "gen-profile":
             return cmd_gen_profile(a)
     except ProfileMissError as e:

@@ -133,6 +133,10 @@ struct EvalParams {
   uint8_t* bwcb;              // [n_chunk][max_pp] stage-boundary bandwidth codes
   const uint2* cellrec;       // [cells] {cell, cellpred} (K_dp multi)
   uint64_t n_dp;              // chunk items [0, n_dp) may need K_dp (pp >= 3 first)
+  int32_t cuts_given;         // 1: cutsb holds caller cuts for every item (estimate only)
+  int32_t pad5;
+  double* all_sim;            // [n_work] simulated iteration time (simulator.cpp:140-198) or NULL
+  double* simbuf;             // per-warp scratch [gbs] for the pp > 32 simulation path
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

@@ -349,6 +349,75 @@ __global__ void __launch_bounds__(MODE == kSparseG ? 1024 : (MODE == kSparseS ? 
 // ---------------------------------------------------------------------------
 constexpr int kEstWarps = 8;
 
+// simulate() (reference simulator.cpp:140-198) for one candidate, by its
+// warp.  run_replica's event loop (75-136) keeps every stage in micro-batch
+// order and every link FIFO, so its event times obey
+//     C[j][u]  = max(C[j][u-1], TE[j-1][u]) + t_j      (compute end)
+//     TE[j][u] = max(TE[j][u-1], C[j][u]) + e_j(r)     (transfer end)
+// with C[j][-1] = TE[j][-1] = 0 and TE[-1][u] = 0: the start of an event is
+// the time of the later of its two triggers, and each end time is one DADD
+// of that start, exactly as the event loop pushes `now + duration`.
+// finish = C[pp-1][gas-1]; makespan = max over replicas (std::max order);
+// iteration time = makespan + dpsync.  pp <= 32: lane j owns stage j and the
+// warp sweeps the (stage, micro-batch) wavefront (TE passed by shfl_up);
+// pp > 32: lane 0 sweeps stage by stage over a per-warp array of the
+// incoming ready times.
+__device__ double sim_iteration(const EvalParams& p, const ClassDev& cl, const int* PL,
+                                const int* cutsW, const double* stW, double dpsync, int lane,
+                                double* scratch) {
+  const int pp = cl.pp, dp = cl.dp, tmp = cl.tmp, gas = cl.gas, D = p.D;
+  auto edge = [&](int q, int r) {  // replica_edge_times (cost_model.cpp:145-162)
+    const double volume = p.act[cutsW[q + 1] - 1] * cl.mbs;
+    double b = CUDART_INF;
+    for (int s = 0; s < tmp; ++s)
+      b = std_min(b, p.bw[(size_t)PL[(q * dp + r) * tmp + s] * D + PL[((q + 1) * dp + r) * tmp + s]]);
+    return volume / b;
+  };
+  double makespan = 0.0;
+  for (int r = 0; r < dp; ++r) {
+    double fin = 0.0;
+    if (pp <= 32) {
+      const int j = lane;
+      const double t = j < pp ? stW[j] : 0.0;
+      const double e = j < pp - 1 ? edge(j, r) : 0.0;
+      double C = 0.0, TE = 0.0;
+      for (int step = 0; step < gas + pp - 1; ++step) {
+        const double Rin = __shfl_up_sync(0xffffffffu, TE, 1);  // TE[j-1][step-j]
+        const int u = step - j;
+        if (j < pp && u >= 0 && u < gas) {
+          const double R = j == 0 ? 0.0 : Rin;
+          C = (C < R ? R : C) + t;
+          if (j < pp - 1) TE = (TE < C ? C : TE) + e;
+        }
+      }
+      fin = __shfl_sync(0xffffffffu, C, pp - 1);
+    } else {
+      if (lane == 0) {
+        for (int u = 0; u < gas; ++u) scratch[u] = 0.0;
+        double C = 0.0;
+        for (int j = 0; j < pp; ++j) {
+          const double t = stW[j];
+          const double e = j < pp - 1 ? edge(j, r) : 0.0;
+          double TE = 0.0;
+          C = 0.0;
+          for (int u = 0; u < gas; ++u) {
+            const double R = scratch[u];
+            C = (C < R ? R : C) + t;
+            if (j < pp - 1) {
+              TE = (TE < C ? C : TE) + e;
+              scratch[u] = TE;
+            }
+          }
+        }
+        fin = C;
+      }
+      fin = __shfl_sync(0xffffffffu, fin, 0);
+    }
+    makespan = makespan < fin ? fin : makespan;  // std::max(makespan, run_replica(...))
+  }
+  return makespan + dpsync;
+}
+
 // The layer-partition DP for k = 2 stages (pipeline_dp.cpp:70-149): stage 2
 // has the single cell (L, 0); its cut c reads stage-1 cell
 // (c, max(seg(c, L), 0)) = (c, seg(c, L)).  Lane-strided cuts, each lane
@@ -456,7 +525,7 @@ __global__ void __launch_bounds__(kEstWarps * 32, 3) k_est(EvalParams p) {
     int best_r = -1;
     const int* PL = ew->place;
     if (fc == 0) {
-      if (pp >= 3) {
+      if (pp >= 3 || p.cuts_given) {
         const uint8_t* ci = p.cutsb + u * (maxpp + 1);
         for (int q = lane; q <= pp; q += 32) cutsW[q] = ci[q];
       } else {
@@ -627,6 +696,12 @@ __global__ void __launch_bounds__(kEstWarps * 32, 3) k_est(EvalParams p) {
         best_r = rr;
       }
     }
+    // ---- batched simulator ---------------------------
+    double simv = CUDART_NAN;
+    if (p.all_sim && fc == 0)  // fc is warp-uniform
+      simv = sim_iteration(p, cl, PL, cutsW, stW, dpsync, lane,
+                           p.simbuf + ((size_t)blockIdx.x * kEstWarps + wib) * p.gbs);
+    if (p.all_sim && lane == 0) p.all_sim[w.out] = simv;
     // ---- record ---------------------------------------------------------
     amp_record rec;
     rec.index = w.index;

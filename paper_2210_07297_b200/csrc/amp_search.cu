@@ -102,7 +102,7 @@ struct amp_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
   DevBuf param, act, bw, base_order, times, prefix, domain, seg, pairs_d, cls_d;
   DevBuf bp, slice, wtab, cta_topk, topk, taken, segs, counter, index_list;
-  DevBuf o_all, o_cuts, o_stage, o_edge, o_place;
+  DevBuf o_all, o_cuts, o_stage, o_edge, o_place, o_sim, simbuf;
   // pruned DP programs
   bool sparse = false, progs_ok = false;
   int mode = 0;
@@ -770,7 +770,8 @@ void account(amp_ctx* ctx, uint64_t begin, uint64_t end, const uint64_t* list, i
 // top-k lists of K_est persist across chunks in ctx->cta_topk.
 int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64_t* d_list,
                     uint64_t n_work, int32_t k, bool want_all, bool want_details,
-                    bool want_place) {
+                    bool want_place, const uint8_t* d_given_cuts = nullptr,
+                    bool want_sim = false) {
   EvalParams ep{};
   ep.L = ctx->L;
   ep.D = ctx->D;
@@ -823,6 +824,14 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   if (want_place) {
     CK(ctx->o_place.ensure(sizeof(int32_t) * n_work * ctx->D));
     ep.all_place = ctx->o_place.as<int32_t>();
+  }
+  if (want_sim) {
+    CK(ctx->o_sim.ensure(sizeof(double) * n_work));
+    ep.all_sim = ctx->o_sim.as<double>();
+    if (ctx->max_pp > 32) {  // per-warp ready-time array of the pp > 32 path
+      CK(ctx->simbuf.ensure(sizeof(double) * (size_t)ctx->est_ctas * kEstWarps * ctx->gbs));
+      ep.simbuf = ctx->simbuf.as<double>();
+    }
   }
   const int kk = std::max(1, k);
   CK(ctx->cta_topk.ensure(sizeof(amp_record) * (size_t)kk * ctx->est_ctas));
@@ -892,6 +901,12 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     ep.t0 = t0;
     ep.n_chunk = std::min<uint64_t>(C, n_work - t0);
     ep.n_dp = n_heavy > t0 ? std::min<uint64_t>(ep.n_chunk, n_heavy - t0) : 0;
+    ep.cuts_given = d_given_cuts != nullptr;
+    if (d_given_cuts) {  // estimate only: the caller's cuts replace K_dp
+      ep.n_dp = 0;
+      CK(cudaMemcpyAsync(ctx->c_cuts.p, d_given_cuts + t0 * (ctx->max_pp + 1),
+                         ep.n_chunk * (ctx->max_pp + 1), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
     ep.first_chunk = t0 == 0;
     const uint64_t warps = ep.n_chunk;
     const int place_grid = (int)std::min<uint64_t>((warps + 7) / 8, (uint64_t)ctx->sms * 16);
@@ -941,6 +956,9 @@ int copy_details(amp_ctx* ctx, uint64_t n, const amp_details* det) {
   if (det->placement)
     CK(cudaMemcpyAsync(det->placement, ctx->o_place.p, sizeof(int32_t) * n * ctx->D,
                        cudaMemcpyDeviceToHost, ctx->stream));
+  if (det->simulated)
+    CK(cudaMemcpyAsync(det->simulated, ctx->o_sim.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                       ctx->stream));
   return AMP_OK;
 }
 
@@ -1136,7 +1154,8 @@ int amp_search_run(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k, amp_re
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
   ctx->launches = 0;
   int rc = launch_evaluate(ctx, &segs, nullptr, n, k, all != nullptr, det,
-                           all_details && all_details->placement);
+                           all_details && all_details->placement, nullptr,
+                           all != nullptr && all_details && all_details->simulated);
   if (rc) return rc;
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
   const int kk = std::max(1, k);
@@ -1183,7 +1202,8 @@ int amp_search_evaluate(amp_ctx* ctx, const uint64_t* indices, int32_t n, amp_re
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
   ctx->launches = 0;
   int rc = launch_evaluate(ctx, nullptr, ctx->index_list.as<uint64_t>(), (uint64_t)n, 1, true,
-                           det, details && details->placement);
+                           det, details && details->placement, nullptr,
+                           details && details->simulated);
   if (rc) return rc;
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
   CK(cudaMemcpyAsync(out, ctx->o_all.p, sizeof(amp_record) * n, cudaMemcpyDeviceToHost,
@@ -1199,6 +1219,56 @@ int amp_search_evaluate(amp_ctx* ctx, const uint64_t* indices, int32_t n, amp_re
   ctx->stats.total_ms = ms;
   ctx->stats.launches = ctx->launches;
   ctx->stats.ctas = ctx->n_ctas;
+  return AMP_OK;
+}
+
+int amp_search_estimate(amp_ctx* ctx, const uint64_t* indices, const int32_t* cuts, int32_t n,
+                        amp_record* out, const amp_details* details) {
+  if (!ctx || n < 0 || (n > 0 && (!indices || !cuts || !out))) return AMP_E_INVALID;
+  if (n == 0) return AMP_OK;
+  const uint64_t N = amp_search_num_candidates(ctx);
+  const int W = ctx->max_pp + 1;
+  std::vector<uint8_t> c8((size_t)n * W, 0);
+  for (int32_t i = 0; i < n; ++i) {
+    if (indices[i] >= N) return fail(ctx, AMP_E_INVALID, "index outside [0, num_candidates)");
+    const int pp = ctx->classes[indices[i] / ctx->P].pp;
+    const int32_t* c = cuts + (size_t)i * W;
+    if (pp <= ctx->L) {  // (pp > L fails in K_place before the cuts are read)
+      bool ok = c[0] == 0 && c[pp] == ctx->L;
+      for (int j = 0; j < pp && ok; ++j) ok = c[j] < c[j + 1];
+      if (!ok)
+        return fail(ctx, AMP_E_INVALID,
+                    "cuts of candidate " + std::to_string(i) +
+                        " must rise strictly from 0 to n_layers over pp stages");
+    }
+    for (int j = 0; j <= pp && j < W; ++j) c8[(size_t)i * W + j] = (uint8_t)c[j];
+  }
+  CK(cudaSetDevice(ctx->device));
+  CK(upload(ctx->index_list, indices, (size_t)n));
+  DevBuf d_cuts;
+  CK(upload(d_cuts, c8.data(), c8.size()));
+  const bool det = details && (details->cuts || details->stage_times || details->edge_times);
+  CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  ctx->launches = 0;
+  int rc = launch_evaluate(ctx, nullptr, ctx->index_list.as<uint64_t>(), (uint64_t)n, 1, true,
+                           det, details && details->placement, d_cuts.as<uint8_t>(),
+                           details && details->simulated);
+  if (rc) return rc;
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  CK(cudaMemcpyAsync(out, ctx->o_all.p, sizeof(amp_record) * n, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  rc = copy_details(ctx, (uint64_t)n, details);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  resolve_kernel_times(ctx);
+  ctx->stats.kernel_ms = ms;
+  ctx->stats.total_ms = ms;
+  ctx->stats.launches = ctx->launches;
+  ctx->stats.ctas = ctx->n_ctas;
+  ctx->stats.candidates = (uint64_t)n;
+  ctx->stats.dp_inner = ctx->stats.fp64_ops = 0;
   return AMP_OK;
 }
 

@@ -100,6 +100,7 @@ class CandidateRecord:
 class PlanResult:
     candidates: List[CandidateRecord]
     best_index: int = -1
+    simulated_all: Optional[List[Optional[float]]] = None  # plan(simulate_all=True)
 
 
 class Searcher:
@@ -142,8 +143,8 @@ class Searcher:
         return {f: getattr(s, f) for f, _ in N.AmpStats._fields_}
 
     # -- evaluation --------------------------------------------------------
-    def _details(self, n: int, details: bool, placement: bool):
-        if not (details or placement):
+    def _details(self, n: int, details: bool, placement: bool, simulate: bool = False):
+        if not (details or placement or simulate):
             return None, None
         mp = self.max_pp
         bufs = {}
@@ -158,31 +159,52 @@ class Searcher:
         if placement:
             bufs["placement"] = np.full((n, self.n_devices), -1, dtype=np.int32)
             d.placement = bufs["placement"].ctypes.data_as(N._ip)
+        if simulate:  # batched device simulator (simulator.cpp:140-198)
+            bufs["simulated"] = np.full(n, np.nan)
+            d.simulated = bufs["simulated"].ctypes.data_as(N._dp)
         return d, bufs
 
     def run(self, begin: int = 0, end: Optional[int] = None, k: int = 10, want_all: bool = False,
-            details: bool = False, placement: bool = False):
+            details: bool = False, placement: bool = False, simulate: bool = False):
         """Evaluate [begin, end); returns (topk records, all records | None, detail arrays)."""
         end = self.num_candidates if end is None else int(end)
         n = end - begin
         top = np.zeros(max(k, 1), dtype=RECORD_DTYPE)
         ntop = C.c_int32(0)
         allr = np.zeros(n, dtype=RECORD_DTYPE) if want_all else None
-        d, bufs = self._details(n, details and want_all, placement and want_all)
+        d, bufs = self._details(n, details and want_all, placement and want_all,
+                                simulate and want_all)
         N.check(self.lib.amp_search_run(
             self.ctx, begin, end, k, top.ctypes.data_as(C.POINTER(N.AmpRecord)), C.byref(ntop),
             allr.ctypes.data_as(C.POINTER(N.AmpRecord)) if allr is not None else None,
             C.byref(d) if d is not None else None), self.ctx)
         return top[:ntop.value], allr, bufs or {}
 
-    def evaluate(self, indices: Sequence[int], details: bool = True, placement: bool = True):
+    def evaluate(self, indices: Sequence[int], details: bool = True, placement: bool = True,
+                 simulate: bool = False):
         idx = np.ascontiguousarray(indices, dtype=np.uint64)
         n = len(idx)
         out = np.zeros(n, dtype=RECORD_DTYPE)
-        d, bufs = self._details(n, details, placement)
+        d, bufs = self._details(n, details, placement, simulate)
         N.check(self.lib.amp_search_evaluate(
             self.ctx, idx.ctypes.data_as(N._u64p), n, out.ctypes.data_as(C.POINTER(N.AmpRecord)),
             C.byref(d) if d is not None else None), self.ctx)
+        return out, bufs or {}
+
+    def estimate(self, indices: Sequence[int], cuts: np.ndarray, details: bool = True,
+                 placement: bool = True, simulate: bool = False):
+        """Estimate only, with the caller's cuts ([n][max_pp+1]); no DP."""
+        idx = np.ascontiguousarray(indices, dtype=np.uint64)
+        n = len(idx)
+        c = np.full((n, self.max_pp + 1), -1, dtype=np.int32)
+        for i, row in enumerate(cuts):
+            c[i, :len(row)] = row
+        out = np.zeros(n, dtype=RECORD_DTYPE)
+        d, bufs = self._details(n, details, placement, simulate)
+        N.check(self.lib.amp_search_estimate(
+            self.ctx, idx.ctypes.data_as(N._u64p), c.ctypes.data_as(N._ip), n,
+            out.ctypes.data_as(C.POINTER(N.AmpRecord)), C.byref(d) if d is not None else None),
+            self.ctx)
         return out, bufs or {}
 
     def run_device(self, begin: int, end: int, k: int, d_topk_ptr: int, stream_ptr: int = 0):
@@ -252,8 +274,11 @@ def rank_order(recs: np.ndarray) -> np.ndarray:
 
 
 def plan(model: ModelGraph, cluster: Cluster, profile: ProfileTable, gbs: int,
-         options: Optional[PlanOptions] = None, device: int = 0, dense_dp: bool = False) -> PlanResult:
-    """parplan::plan on the GPU (optimizer.cpp:200-251)."""
+         options: Optional[PlanOptions] = None, device: int = 0, dense_dp: bool = False,
+         simulate_all: bool = False) -> PlanResult:
+    """parplan::plan on the GPU (optimizer.cpp:200-251).  simulate_all: also
+    return every candidate's simulated time (result.simulated_all, in rank
+    order) — acceptance criterion 5's rank agreement in one pass."""
     import os
     import time
 
@@ -270,7 +295,10 @@ def plan(model: ModelGraph, cluster: Cluster, profile: ProfileTable, gbs: int,
         if tm is not None:
             tm["create"] = time.perf_counter() - t
             t = time.perf_counter()
-        _, allr, bufs = s.run(0, s.num_candidates, k=0, want_all=True, details=True, placement=True)
+        # the batched device simulator runs in the same pass (K_est), so the
+        # top-`budget` validation needs no host simulation
+        _, allr, bufs = s.run(0, s.num_candidates, k=0, want_all=True, details=True, placement=True,
+                              simulate=options.budget > 0 or simulate_all)
         if tm is not None:
             tm["run"] = time.perf_counter() - t
             t = time.perf_counter()
@@ -286,26 +314,20 @@ def plan(model: ModelGraph, cluster: Cluster, profile: ProfileTable, gbs: int,
         tm["decode"] = time.perf_counter() - t
         t = time.perf_counter()
     # validate the top `budget` with the simulator (optimizer.cpp:235-249):
-    # the simulations are independent (ctypes releases the GIL), so they run
-    # on a thread pool; best_index is then the first strict minimum in rank
-    # order, as in the reference's sequential loop
-    todo = [i for i in range(min(len(cands), max(0, options.budget))) if cands[i].failure is None]
-    if todo:
-        from concurrent.futures import ThreadPoolExecutor
-
-        def sim(i):
-            return simulator.simulate(cands[i].strategy, model, cluster, profile, gbs,
-                                      options.cost_options, encoded=enc)
-        workers = min(len(todo), options.workers or (os.cpu_count() or 1))
-        if workers > 1:
-            with ThreadPoolExecutor(max_workers=workers) as ex:
-                sims = list(ex.map(sim, todo))
-        else:
-            sims = [sim(i) for i in todo]
-        for i, v in zip(todo, sims):
-            cands[i].simulated = v
-            if result.best_index < 0 or v < cands[result.best_index].simulated:
-                result.best_index = i
+    # values from the device simulator (bit-identical to simulate(),
+    # tests/test_gpu_parity.py); best_index is the first strict minimum in
+    # rank order, as in the reference's sequential loop
+    sims = bufs.get("simulated")
+    for i in range(min(len(cands), max(0, options.budget))):
+        if cands[i].failure is not None:
+            continue
+        v = float(sims[order[i]])
+        cands[i].simulated = v
+        if result.best_index < 0 or v < cands[result.best_index].simulated:
+            result.best_index = i
+    if simulate_all and sims is not None:
+        result.simulated_all = [None if c.failure is not None else float(sims[order[i]])
+                                for i, c in enumerate(cands)]
     if tm is not None:
         tm["simulate"] = time.perf_counter() - t
         print("plan timing (ms):", {k: round(v * 1e3, 3) for k, v in tm.items()})

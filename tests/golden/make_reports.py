@@ -29,6 +29,12 @@ CASES = {
     "C3_b10": ("hetero_model", 64, 10, None),
     "C1_partial_b3": ("homogeneous", 32, 3, "partial"),  # test_cli.cpp:131-160
     "C1_allmiss_b1": ("homogeneous", 32, 1, "empty"),    # test_cli.cpp:100-115
+    # CLI `baseline` (megatron_baseline), test_cli.cpp:267-281
+    "C1_baseline_layer": ("homogeneous", 32, 1, None),
+    "C1_baseline_param": ("homogeneous", 32, 1, None),
+    "C2_baseline_layer": ("hetero_cluster", 32, 1, None),
+    "C3_baseline_param": ("hetero_model", 64, 1, None),
+    "C1_partial_baseline_layer": ("homogeneous", 32, 1, "partial"),
 }
 
 
@@ -56,8 +62,11 @@ def main():
         rep = os.path.join(OUT, case + ".json")
         if os.path.exists(rep):
             os.remove(rep)
+        env = dict(os.environ)
+        if "baseline" in case:
+            env["GEN_MODE"] = "param-balance" if case.endswith("param") else "layer-balance"
         r = subprocess.run([BIN, os.path.join(d, "model.json"), os.path.join(d, "cluster.json"), prof,
-                            str(gbs), str(budget), rep], capture_output=True, text=True)
+                            str(gbs), str(budget), rep], capture_output=True, text=True, env=env)
         with open(os.path.join(OUT, case + ".txt"), "w") as f:
             f.write(r.stdout)
         with open(os.path.join(OUT, case + ".rc"), "w") as f:

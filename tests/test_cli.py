@@ -23,6 +23,11 @@ CASES = {
     "C2_b10": ("hetero_cluster", 32, 10, None),
     "C3_b10": ("hetero_model", 64, 10, None),
     "C1_partial_b3": ("homogeneous", 32, 3, "partial"),
+    "C1_baseline_layer": ("homogeneous", 32, "layer-balance", None),
+    "C1_baseline_param": ("homogeneous", 32, "param-balance", None),
+    "C2_baseline_layer": ("hetero_cluster", 32, "layer-balance", None),
+    "C3_baseline_param": ("hetero_model", 64, "param-balance", None),
+    "C1_partial_baseline_layer": ("homogeneous", 32, "layer-balance", "partial"),
 }
 
 
@@ -99,8 +104,12 @@ def test_cli_plan_matches_reference_report_bytes(case, tmp_path):
     name, gbs, budget, variant = CASES[case]
     p = _write_inputs(tmp_path, name, variant)
     rep = str(tmp_path / "report.json")
-    r = _cli(["plan", "--model", p["model"], "--cluster", p["cluster"], "--profile", p["profile"],
-              "--gbs", str(gbs), "--budget", str(budget), "--report", rep], ROOT)
+    common = ["--model", p["model"], "--cluster", p["cluster"], "--profile", p["profile"],
+              "--gbs", str(gbs), "--report", rep]
+    if "baseline" in case:  # CLI `baseline` (megatron_baseline through amp_search_estimate)
+        r = _cli(["baseline"] + common + ["--mode", budget], ROOT)
+    else:
+        r = _cli(["plan"] + common + ["--budget", str(budget)], ROOT)
     assert r.returncode == 0, r.stderr
     with open(rep) as f:
         assert f.read() == _read(case + ".json")
@@ -118,3 +127,22 @@ def test_cli_all_profile_miss_exits_3(tmp_path):
     assert r.returncode == int(_read("C1_allmiss_b1.rc"))
     assert r.stderr == _read("C1_allmiss_b1.err")
     assert not os.path.exists(rep)
+
+
+def test_megatron_host_rules_match_reference_unit_cases():
+    """test_optimizer.cpp:126-155 (degree rule) and the assignment helpers."""
+    from paper_2210_07297_b200 import baseline as Bl, problem as P
+    sc = scenario("homogeneous")  # 4 nodes x 4 devices
+    # largest dp that fits: tmp*pp minimal -> (1, 16, 1) for mbs 1
+    assert Bl.megatron_degree_choice(sc.cluster, 32, 1, 24) == (1, 16, 1)
+    # mbs 4: dp must divide 32/4*... -> gbs/dp % 4 == 0 -> dp <= 8
+    assert Bl.megatron_degree_choice(sc.cluster, 32, 4, 24) == (2, 8, 1)
+    for mbs in (1, 2, 4, 8):
+        pp, dp, tmp = Bl.megatron_degree_choice(sc.cluster, 32, mbs, 4)
+        assert tmp <= Bl.min_node_size(sc.cluster) and pp <= 4
+    assert Bl.uniform_assignment(30, 4) == [0, 8, 16, 23, 30]
+    assert Bl.uniform_assignment(24, 1) == [0, 24]
+    with pytest.raises(P.ValidationError):
+        Bl.uniform_assignment(3, 4)
+    m = scenario("hetero_model").model
+    assert Bl.param_balance_assignment(m, 4) == [0, 3, 6, 9, 24]

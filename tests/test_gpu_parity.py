@@ -246,3 +246,57 @@ def test_class_slice_shards_merge_to_single_run(n_shards):
         merged = np.frombuffer(out.cpu().numpy().tobytes(), dtype=planner.RECORD_DTYPE)
     assert merged["index"].tolist() == whole["index"].tolist()
     assert np.array_equal(merged["total"], whole["total"])
+
+
+@pytest.mark.parametrize("name,P_", [("homogeneous", 1), ("hetero_cluster", 1), ("hetero_model", 1),
+                                     ("hetero_cluster", 40), ("synthetic96", 1)])
+def test_batched_simulator_matches_reference_simulate(name, P_):
+    """the device simulator (amp_details.simulated, K_est)
+    equals the reference simulate() (simulator.cpp:140-198, oracle/_ref)
+    bit for bit on every candidate — the plan() spaces, shuffled placements,
+    and C4's pp up to 64 (the > 32-stage path)."""
+    if not B.ref_available():
+        pytest.skip("oracle/_ref not built")
+    sc = scenario(name)
+    enc = P.EncodedProblem.from_scenario(sc)
+    with planner.Searcher(enc, placements_per_class=P_, seed=7) as s:
+        n = s.num_candidates
+        idx = np.arange(n) if n <= 3000 else np.random.default_rng(3).choice(n, 3000, replace=False)
+        recs, bufs = s.evaluate(idx, details=True, placement=True, simulate=True)
+    checked = 0
+    for i in range(len(idx)):
+        r = recs[i]
+        if r["fail_code"] != 0:
+            assert np.isnan(bufs["simulated"][i])
+            continue
+        pp, dp, tmp, mbs = int(r["pp"]), int(r["dp"]), int(r["tmp"]), int(r["mbs"])
+        ref = B.ref_simulate(enc, pp, dp, tmp, mbs, bufs["placement"][i][: pp * dp * tmp],
+                             bufs["cuts"][i][: pp + 1])
+        assert bufs["simulated"][i] == ref, (name, i, pp, dp, tmp, mbs)
+        checked += 1
+    assert checked > 0
+
+
+@pytest.mark.parametrize("name", ["homogeneous", "hetero_cluster", "hetero_model"])
+def test_acceptance_rank_agreement_one_pass(name):
+    """acceptance_main.cpp:236-267 (criterion 5): Spearman(estimate,
+    simulation) over every feasible candidate >= 0.5, here from one plan()
+    pass with the device simulator; the simulated values equal the
+    reference's simulate() on the reference's own plan() strategies."""
+    if not B.ref_available():
+        pytest.skip("oracle/_ref not built")
+    from paper_2210_07297_b200 import simulator
+    sc = scenario(name)
+    enc = P.EncodedProblem.from_scenario(sc)
+    res = planner.plan(sc.model, sc.cluster, sc.profile, sc.gbs, P.PlanOptions(budget=1),
+                       simulate_all=True)
+    est, sim = [], []
+    for c, v in zip(res.candidates, res.simulated_all):
+        if c.failure is not None:
+            continue
+        s = c.strategy
+        assert v == B.ref_simulate(enc, s.pp, s.dp, s.tmp, s.mbs, s.placement, s.cut_boundaries)
+        est.append(c.estimated.total)
+        sim.append(v)
+    rho = simulator.rank_correlation(est, sim)
+    assert len(est) >= 20 and rho >= 0.5
