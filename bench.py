@@ -314,9 +314,10 @@ def our_arm(args):
     if not args.no_e2e:
         e2e = e2e_arm(args, enc, P_, n_total, world, rank, local, distributed)
 
-    dense = None
+    dense = per_cand = None
     if world == 1 and not args.no_dense:
         dense = dense_leg(enc, local)
+        per_cand = per_candidate_leg(enc, local, P_, n_total)
 
     if rank == 0:
         line = {
@@ -340,7 +341,11 @@ def our_arm(args):
                          "kernel": f"k_dp_multi<{st['dp_group']}> (pruned layer-partition DP, "
                                    f"{st['dp_group']} candidates of one class per CTA group)",
                          "fp64_ops_def": "7 per executed inner iteration (SURVEY.md 8(d)) over the "
-                                         "pruned program's iterations, per candidate",
+                                         "pruned program's iterations of the DP instances "
+                                         "actually solved (memoised by signature: one per "
+                                         "distinct (class, boundary-bandwidth codes))",
+                         "dp_memoisation": {"candidates": n_total,
+                                            "dp_instances_solved": st["dp_instances"]},
                          "dp_items_per_step": st["dp_items"], "dp_launches_per_step": st["dp_launches"],
                          "kernel_ms_per_step": kern_ms,
                          "pipeline_ms_per_step": {"k_place": place_ms, "k_dp": dp_ms, "k_est": est_ms},
@@ -355,6 +360,8 @@ def our_arm(args):
         }
         if e2e:
             line["e2e"] = e2e
+        if per_cand:
+            line["per_candidate_dp"] = per_cand
         if dense:
             line["dense_dp"] = dense
         if world == 1 and not args.no_wall_time:
@@ -368,6 +375,36 @@ def our_arm(args):
     s.close()
     if distributed:
         dist.destroy_process_group()
+
+
+def per_candidate_leg(enc, local, P_, n):
+    """The same sweep with one DP per candidate (AMP_FLAG_NO_DEDUP): the
+    K_dp kernel's own efficiency without memoisation (identical results,
+    tests/test_gpu_parity.py::test_memoised_dp_equals_per_candidate_dp)."""
+    import ctypes as C
+
+    from paper_2210_07297_b200 import _native as N
+    from paper_2210_07297_b200.planner import Searcher
+    s = Searcher(enc, placements_per_class=P_, seed=0, device=local, dedup=False)
+    s.run(0, n, k=TOPK)
+    sts = []
+    for _ in range(3):
+        s.run(0, n, k=TOPK)
+        sts.append(s.stats())
+    s.close()
+    peak = C.c_double()
+    pms = C.c_double()
+    N.check(N.load().amp_fp64_peak(local, C.byref(peak), C.byref(pms)))
+    tot = float(np.median([x["total_ms"] for x in sts]))
+    dp_ms = float(np.median([x["dp_ms"] for x in sts]))
+    ach = sts[-1]["fp64_ops"] / (dp_ms * 1e-3) / 1e12
+    return {"value": n / (tot * 1e-3), "unit": UNIT, "candidates": n, "ms_per_step": tot,
+            "pipeline_ms": {"k_place": float(np.median([x["place_ms"] for x in sts])),
+                            "k_dp": dp_ms, "k_est": float(np.median([x["est_ms"] for x in sts]))},
+            "dp_inner": sts[-1]["dp_inner"],
+            "roofline": {"bound": "fp64", "kernel": f"k_dp_multi<{sts[-1]['dp_group']}>",
+                         "achieved": ach, "peak": peak.value / 1e12, "unit": "TFLOP/s",
+                         "frac": ach / (peak.value / 1e12)}}
 
 
 def dense_leg(enc, local, n=1_000_000):

@@ -109,6 +109,11 @@ typedef struct amp_problem {
 /* Evaluate the reference's full tolerance-indexed DP table instead of only
  * the cells the result depends on (same results; for comparison).          */
 #define AMP_FLAG_DENSE_DP 1
+/* Solve one DP per candidate even when candidates share a signature (class,
+ * per-boundary bandwidth codes).  By default the engine memoises the DP by
+ * signature (exact: optimal_assignment is a pure function of it; SURVEY
+ * §8(d)); this flag is for comparison runs.                                 */
+#define AMP_FLAG_NO_DEDUP 2
 
 typedef struct amp_search_config {
   uint64_t placements_per_class; /* P >= 1                                 */

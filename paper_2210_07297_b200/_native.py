@@ -71,6 +71,7 @@ class AmpSearchConfig(C.Structure):
 
 
 AMP_FLAG_DENSE_DP = 1
+AMP_FLAG_NO_DEDUP = 2
 
 
 class AmpRecord(C.Structure):

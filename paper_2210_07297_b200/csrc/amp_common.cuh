@@ -137,6 +137,12 @@ struct EvalParams {
   int32_t pad5;
   double* all_sim;            // [n_work] simulated iteration time (simulator.cpp:140-198) or NULL
   double* simbuf;             // per-warp scratch [gbs] for the pp > 32 simulation path
+  // DP memoisation by signature (amp_dedup.cuh); NULL when off
+  const uint32_t* rep_list;   // [n_rep] chunk items whose DP K_dp solves
+  const uint32_t* rep_of;     // [n_dp] representative of every heavy item
+  const uint64_t* n_rep;      // device count of representatives
+  const double* prog_inner;   // [n_progs] unpadded inner iterations per program
+  unsigned long long* exec_counters;  // [2]: DP instances solved, inner iterations executed
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

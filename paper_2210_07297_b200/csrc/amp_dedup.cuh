@@ -1,0 +1,81 @@
+// amp_dedup.cuh — exact DP memoisation by signature.
+//
+// optimal_assignment (pipeline_dp.cpp:70-149) is a pure function of the
+// class (pp, dp, tmp, mbs: layer times, gas, k) and the edge function
+// e(cut, q) = act[cut-1]*mbs / bw[q] (optimizer.cpp:130-139).  With coded
+// bandwidths (K_place) the edge function is fixed by the per-boundary codes,
+// so candidates with the same (class, code vector) have bit-identical cuts.
+// Per chunk:
+//   K_key    key[u] = class << (nq * cb) | codes, value u   (heavy items)
+//   radix sort (cub::DeviceRadixSort) of (key, u)
+//   K_heads  head flag of every run of equal keys
+//   scan     run id of every sorted position (cub::DeviceScan)
+//   K_reps   run heads -> rep_list[run] = u;  then rep_of[u] = rep_list[run]
+// K_dp solves only rep_list[0 .. n_rep) (class-contiguous: the class is in
+// the key's high bits), K_est reads each candidate's cuts at rep_of[u].
+// Failed and pp <= 2 items get the all-ones key (never a real signature:
+// keys use at most 63 bits); K_dp skips them as before.
+#pragma once
+
+#include "amp_common.cuh"
+
+namespace amp {
+
+struct DedupParams {
+  const CandWork* work;
+  const ClassDev* cls;
+  const uint8_t* bwcb;  // [n][max_pp] boundary codes
+  uint64_t n;           // heavy prefix of the chunk
+  int32_t max_pp, code_bits, pad0, pad1;
+  uint64_t* keys;       // [n]
+  uint32_t* vals;       // [n]
+  const uint64_t* skeys;  // sorted
+  const uint32_t* svals;
+  uint32_t* flags;      // [n] head flags -> (scan) run ids (inclusive)
+  const uint32_t* runid;
+  uint32_t* rep_list;   // [n] representative item of each run
+  uint32_t* rep_of;     // [n] representative of every item
+  uint64_t* n_rep;      // device count of runs
+};
+
+__global__ void k_dedup_keys(DedupParams p) {
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < p.n;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const CandWork& w = p.work[u];
+    uint64_t key = ~0ull;
+    if (w.fail_code == 0) {
+      const ClassDev cl = p.cls[w.cls];
+      if (cl.pp >= 3) {
+        key = (uint64_t)w.cls;
+        const uint8_t* c = p.bwcb + u * p.max_pp;
+        for (int q = 0; q < p.max_pp - 1; ++q)
+          key = (key << p.code_bits) | (q < cl.pp - 1 ? (uint64_t)c[q] : 0ull);
+      }
+    }
+    p.keys[u] = key;
+    p.vals[u] = (uint32_t)u;
+  }
+}
+
+__global__ void k_dedup_heads(DedupParams p) {
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < p.n;
+       s += (uint64_t)gridDim.x * blockDim.x)
+    p.flags[s] = (s == 0 || p.skeys[s] != p.skeys[s - 1]) ? 1u : 0u;
+}
+
+__global__ void k_dedup_reps(DedupParams p) {
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < p.n;
+       s += (uint64_t)gridDim.x * blockDim.x) {
+    const bool head = s == 0 || p.skeys[s] != p.skeys[s - 1];
+    if (head) p.rep_list[p.runid[s] - 1] = p.svals[s];
+    if (s + 1 == p.n) *p.n_rep = p.runid[s];
+  }
+}
+
+__global__ void k_dedup_scatter(DedupParams p) {
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < p.n;
+       s += (uint64_t)gridDim.x * blockDim.x)
+    p.rep_of[p.svals[s]] = p.rep_list[p.runid[s] - 1];
+}
+
+}  // namespace amp

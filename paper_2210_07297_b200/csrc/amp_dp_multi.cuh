@@ -230,13 +230,16 @@ __global__ void __launch_bounds__(B >= 8 ? 512 : 256, (B <= 2 ? 3 : (B >= 8 ? 1 
   double* Pf = Dm + p.max_M;
   uint8_t* const bpb = reinterpret_cast<uint8_t*>(Pf + LP + 3);  // [2][max_rest][B]
 
-  const uint64_t n_items = p.n_dp;  // chunk items that may need the DP (pp >= 3 first)
+  // slots: chunk items that may need the DP (pp >= 3 first), or with
+  // memoisation the representatives of the distinct signatures
+  const uint64_t n_items = p.rep_list ? *p.n_rep : p.n_dp;
+  auto item_of = [&](uint64_t slot) -> uint64_t { return p.rep_list ? p.rep_list[slot] : slot; };
   const uint64_t nbatch = (n_items + B - 1) / B;
   uint64_t bi = blockIdx.x;
   if (bi >= nbatch) return;
   auto word = [&](uint64_t batch, int w) -> uint64_t {
-    const uint64_t item = batch * B + w / WW;
-    return item < n_items ? reinterpret_cast<const uint64_t*>(p.work + item)[w % WW] : 0;
+    const uint64_t slot = batch * B + w / WW;
+    return slot < n_items ? reinterpret_cast<const uint64_t*>(p.work + item_of(slot))[w % WW] : 0;
   };
   if (tid < B * WW) reinterpret_cast<uint64_t*>(wq[0])[tid] = word(bi, tid);
   if (tid < 3 * B) {  // edge padding (cuts L .. L+2), never rewritten
@@ -289,12 +292,17 @@ __global__ void __launch_bounds__(B >= 8 ? 512 : 256, (B <= 2 ? 3 : (B >= 8 ? 1 
       auto member = [&](int r) -> uint64_t {  // r >= ng repeats member 0
         unsigned m = gm;
         for (int q = r < ng ? r : 0; q > 0; --q) m &= m - 1;
-        return ubase + (uint64_t)(__ffs(m) - 1);
+        return item_of(ubase + (uint64_t)(__ffs(m) - 1));
       };
       const ClassDev cl = p.cls[gcls];
       const int k = cl.pp;
       if (k <= 2) continue;  // solved in K_est (light_cut2)
       const ProgDev pg = p.progs[p.class_prog[gcls]];
+      if (p.exec_counters && tid == 0) {  // executed work (roofline accounting)
+        atomicAdd(&p.exec_counters[0], (unsigned long long)ng);
+        atomicAdd(&p.exec_counters[1],
+                  (unsigned long long)(p.prog_inner[p.class_prog[gcls]] * ng));
+      }
       const uint32_t* cl_ = p.cells + pg.cell_base;
       const uint2* cr = p.cellrec + pg.cell_base;
       const uint16_t* pd = p.preds + pg.pred_base;

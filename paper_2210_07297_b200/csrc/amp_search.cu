@@ -23,6 +23,10 @@
 #include "amp_kernels.cuh"
 #include "amp_pipeline.cuh"
 #include "amp_dp_multi.cuh"
+#include "amp_dedup.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 using namespace amp;
 
@@ -121,6 +125,12 @@ struct amp_ctx {
   int n_codes = 0;
   DevBuf bwcode, bwval, qtab, cellrec;
   uint64_t n_heavy = 0;  // items of pp >= 3 classes in the current run's dispatch order
+  // DP memoisation by signature (amp_dedup.cuh)
+  bool dedup = false;
+  int code_bits = 0, key_bits = 0;
+  DevBuf dd_keys, dd_vals, dd_skeys, dd_svals, dd_flags, dd_runid, dd_rep_list, dd_rep_of;
+  DevBuf dd_nrep, dd_temp, dd_counters, prog_inner_d;
+  size_t dd_temp_bytes = 0;
   uint64_t chunk = 1;
   int est_ctas = 1, sms = 148, launches = 0;
   // per-chunk kernel events {before K_place, after K_place, after K_dp,
@@ -128,6 +138,7 @@ struct amp_ctx {
   std::vector<cudaEvent_t> kev;
   int kev_used = 0;
   bool kev_pending = false;
+  bool stats_exec_pending = false;  // exec counters of a memoised run to read back
   amp_stats stats{};
 };
 
@@ -639,6 +650,26 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
       CK(cudaGetLastError());
     }
   }
+  // ---- DP memoisation by signature: key = class | codes ------
+  ctx->dedup = false;
+  if (ctx->multi_b && ctx->n_codes > 0 && !(cfg && (cfg->flags & AMP_FLAG_NO_DEDUP)) &&
+      std::getenv("AMP_NO_DEDUP") == nullptr) {
+    int cb = 1;
+    while ((1 << cb) < ctx->n_codes) ++cb;
+    int clsb = 1;
+    while ((1ull << clsb) < ctx->classes.size()) ++clsb;
+    const int kb = clsb + (ctx->max_pp - 1) * cb;
+    if (kb <= 63) {
+      ctx->dedup = true;
+      ctx->code_bits = cb;
+      ctx->key_bits = kb;
+      std::vector<double> pin(ctx->prog_inner_raw.begin(), ctx->prog_inner_raw.end());
+      if (pin.empty()) pin.push_back(0.0);
+      CK(upload(ctx->prog_inner_d, pin.data(), pin.size()));
+      CK(ctx->dd_nrep.ensure(sizeof(uint64_t)));
+      CK(ctx->dd_counters.ensure(2 * sizeof(unsigned long long)));
+    }
+  }
   if (ctx->multi_b == 2) ctx->eval_fn = (const void*)k_dp_multi<2>;
   if (ctx->multi_b == 4) ctx->eval_fn = (const void*)k_dp_multi<4>;
   if (ctx->multi_b == 8) ctx->eval_fn = (const void*)k_dp_multi<8>;
@@ -725,6 +756,16 @@ void resolve_kernel_times(amp_ctx* ctx) {
   ctx->stats.dp_ms = dpm;
   ctx->stats.est_ms = es;
   ctx->kev_pending = false;
+  if (ctx->stats_exec_pending) {  // memoised run: executed DP instances / iterations
+    unsigned long long c[2] = {0, 0};
+    if (cudaMemcpy(c, ctx->dd_counters.p, sizeof c, cudaMemcpyDeviceToHost) == cudaSuccess) {
+      ctx->stats.dp_items = c[0];
+      ctx->stats.dp_instances = c[0];
+      ctx->stats.dp_inner = (double)c[1];
+      ctx->stats.fp64_ops = 7.0 * (double)c[1];
+    }
+    ctx->stats_exec_pending = false;
+  }
 }
 
 void account(amp_ctx* ctx, uint64_t begin, uint64_t end, const uint64_t* list, int32_t n,
@@ -867,6 +908,28 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   ep.bwval = ctx->bwval.as<double>();
   ep.qtab = ctx->n_codes ? ctx->qtab.as<double>() : nullptr;
   ep.cellrec = ctx->cellrec.as<uint2>();
+  if (ctx->dedup && !d_given_cuts) {
+    CK(ctx->dd_keys.ensure(sizeof(uint64_t) * C));
+    CK(ctx->dd_skeys.ensure(sizeof(uint64_t) * C));
+    CK(ctx->dd_vals.ensure(sizeof(uint32_t) * C));
+    CK(ctx->dd_svals.ensure(sizeof(uint32_t) * C));
+    CK(ctx->dd_flags.ensure(sizeof(uint32_t) * C));
+    CK(ctx->dd_runid.ensure(sizeof(uint32_t) * C));
+    CK(ctx->dd_rep_list.ensure(sizeof(uint32_t) * C));
+    CK(ctx->dd_rep_of.ensure(sizeof(uint32_t) * C));
+    size_t t1 = 0, t2 = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, t1, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                       (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)C, 0,
+                                       ctx->key_bits, ctx->stream));
+    CK(cub::DeviceScan::InclusiveSum(nullptr, t2, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                     (int)C, ctx->stream));
+    ctx->dd_temp_bytes = std::max(t1, t2);
+    CK(ctx->dd_temp.ensure(ctx->dd_temp_bytes + 16));
+    CK(cudaMemsetAsync(ctx->dd_counters.p, 0, 2 * sizeof(unsigned long long), ctx->stream));
+    ep.exec_counters = ctx->dd_counters.as<unsigned long long>();
+    ep.prog_inner = ctx->prog_inner_d.as<double>();
+  }
+  ctx->stats_exec_pending = ctx->dedup && !d_given_cuts;
   // items of pp >= 3 classes lead the dispatch order of a segment list
   uint64_t n_heavy = n_work;
   if (segs) {
@@ -914,6 +977,45 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), ctx->stream));
     CK(cudaEventRecord(ev[1], ctx->stream));
+    ep.rep_list = nullptr;
+    ep.rep_of = nullptr;
+    ep.n_rep = nullptr;
+    if (ctx->dedup && !d_given_cuts && ep.n_dp > 0) {
+      // ---- memoisation: sort signatures, one DP per distinct key --------
+      DedupParams dp{};
+      dp.work = ep.work;
+      dp.cls = ep.cls;
+      dp.bwcb = ep.bwcb;
+      dp.n = ep.n_dp;
+      dp.max_pp = ctx->max_pp;
+      dp.code_bits = ctx->code_bits;
+      dp.keys = ctx->dd_keys.as<uint64_t>();
+      dp.vals = ctx->dd_vals.as<uint32_t>();
+      dp.skeys = ctx->dd_skeys.as<uint64_t>();
+      dp.svals = ctx->dd_svals.as<uint32_t>();
+      dp.flags = ctx->dd_flags.as<uint32_t>();
+      dp.runid = ctx->dd_runid.as<uint32_t>();
+      dp.rep_list = ctx->dd_rep_list.as<uint32_t>();
+      dp.rep_of = ctx->dd_rep_of.as<uint32_t>();
+      dp.n_rep = ctx->dd_nrep.as<uint64_t>();
+      const int g = (int)std::min<uint64_t>((ep.n_dp + 255) / 256, (uint64_t)ctx->sms * 8);
+      k_dedup_keys<<<g, 256, 0, ctx->stream>>>(dp);
+      size_t tb = ctx->dd_temp_bytes;
+      CK(cub::DeviceRadixSort::SortPairs(ctx->dd_temp.p, tb, dp.keys, ctx->dd_skeys.as<uint64_t>(),
+                                         dp.vals, ctx->dd_svals.as<uint32_t>(), (int)ep.n_dp, 0,
+                                         ctx->key_bits, ctx->stream));
+      k_dedup_heads<<<g, 256, 0, ctx->stream>>>(dp);
+      tb = ctx->dd_temp_bytes;
+      CK(cub::DeviceScan::InclusiveSum(ctx->dd_temp.p, tb, dp.flags, ctx->dd_runid.as<uint32_t>(),
+                                       (int)ep.n_dp, ctx->stream));
+      k_dedup_reps<<<g, 256, 0, ctx->stream>>>(dp);
+      k_dedup_scatter<<<g, 256, 0, ctx->stream>>>(dp);
+      CK(cudaGetLastError());
+      ctx->launches += 6;  // 4 kernels + 2 CUB passes (sort, scan) of ours
+      ep.rep_list = dp.rep_list;
+      ep.rep_of = dp.rep_of;
+      ep.n_rep = dp.n_rep;
+    }
     ctx->stats.dp_items += ep.n_dp;
     if (ep.n_dp > 0) {
       ctx->stats.dp_launches += 1;

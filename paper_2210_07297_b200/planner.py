@@ -107,11 +107,14 @@ class Searcher:
     """One amp_ctx: problem tables resident on one GPU."""
 
     def __init__(self, problem: EncodedProblem, placements_per_class: int = 1, seed: int = 0,
-                 device: int = 0, max_ctas: int = 0, dense_dp: bool = False):
+                 device: int = 0, max_ctas: int = 0, dense_dp: bool = False,
+                 dedup: bool = True):
         self.lib = N.load()
         self.problem = problem
         cfg = N.AmpSearchConfig(int(placements_per_class), int(seed) & (2**64 - 1), int(device),
-                                int(max_ctas), N.AMP_FLAG_DENSE_DP if dense_dp else 0, 0)
+                                int(max_ctas),
+                                (N.AMP_FLAG_DENSE_DP if dense_dp else 0) |
+                                (0 if dedup else N.AMP_FLAG_NO_DEDUP), 0)
         h = C.c_void_p()
         N.check(self.lib.amp_search_create(C.byref(h), problem.ref(), C.byref(cfg)))
         self.ctx = h

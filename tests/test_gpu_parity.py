@@ -300,3 +300,23 @@ def test_acceptance_rank_agreement_one_pass(name):
         sim.append(v)
     rho = simulator.rank_correlation(est, sim)
     assert len(est) >= 20 and rho >= 0.5
+
+
+@pytest.mark.parametrize("name", ["hetero_cluster", "hetero_model", "homogeneous"])
+def test_memoised_dp_equals_per_candidate_dp(name):
+    """DP memoisation by signature (amp_dedup.cuh) changes no output: every
+    record and every cut of a shuffled-placement sweep equals the
+    one-DP-per-candidate run (AMP_FLAG_NO_DEDUP), and the top-k matches."""
+    sc = scenario(name)
+    enc = P.EncodedProblem.from_scenario(sc)
+    outs = []
+    for dedup in (True, False):
+        with planner.Searcher(enc, placements_per_class=3000, seed=11, dedup=dedup) as s:
+            top, allr, bufs = s.run(0, s.num_candidates, k=20, want_all=True, details=True)
+            st = s.stats()
+        outs.append((top, allr, bufs["cuts"], st))
+    (t1, a1, c1, s1), (t2, a2, c2, s2) = outs
+    assert np.array_equal(a1.view(np.uint8), a2.view(np.uint8))
+    assert np.array_equal(c1, c2)
+    assert t1["index"].tolist() == t2["index"].tolist()
+    assert s1["dp_instances"] < s2["dp_instances"]  # memoisation did skip repeats
