@@ -24,6 +24,7 @@
 #include "amp_pipeline.cuh"
 #include "amp_dp_multi.cuh"
 #include "amp_dedup.cuh"
+#include "amp_thread.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -950,6 +951,10 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   ctx->stats.dp_items = 0;
   ctx->stats.dp_launches = 0;
   ctx->stats.dp_group = ctx->multi_b;
+  // thread-per-candidate K_place / K_est (amp_thread.cuh): |D| <= 16 with
+  // coded bandwidths; AMP_NO_THREAD=1 keeps the warp kernels
+  const bool thread_mode = ctx->D <= kThreadMaxD && ctx->n_codes > 0 && ctx->max_pp <= kThreadMaxD &&
+                           std::getenv("AMP_NO_THREAD") == nullptr;
   const int n_chunks = (int)((n_work + C - 1) / C);
   while ((int)ctx->kev.size() < 4 * n_chunks) {
     cudaEvent_t e;
@@ -973,7 +978,12 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     ep.first_chunk = t0 == 0;
     const uint64_t warps = ep.n_chunk;
     const int place_grid = (int)std::min<uint64_t>((warps + 7) / 8, (uint64_t)ctx->sms * 16);
-    k_place<<<place_grid, 256, place_smem, ctx->stream>>>(ep);
+    if (thread_mode) {
+      const int tg = (int)std::min<uint64_t>((ep.n_chunk + 255) / 256, (uint64_t)ctx->sms * 16);
+      k_place_t<<<tg, 256, 0, ctx->stream>>>(ep);
+    } else {
+      k_place<<<place_grid, 256, place_smem, ctx->stream>>>(ep);
+    }
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), ctx->stream));
     CK(cudaEventRecord(ev[1], ctx->stream));
@@ -1026,7 +1036,10 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
       ctx->launches += 1;
     }
     CK(cudaEventRecord(ev[2], ctx->stream));
-    k_est<<<ctx->est_ctas, kEstWarps * 32, est_smem, ctx->stream>>>(ep);
+    if (thread_mode && !want_sim && kk <= 32)
+      k_est_t<<<ctx->est_ctas, kEstTWarps * 32, 0, ctx->stream>>>(ep);
+    else
+      k_est<<<ctx->est_ctas, kEstWarps * 32, est_smem, ctx->stream>>>(ep);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev[3], ctx->stream));
     ctx->launches += 2;

@@ -1,0 +1,392 @@
+// amp_thread.cuh — K_place / K_est with one THREAD per candidate for
+// clusters of at most 16 devices with coded bandwidths.
+//
+// The warp-per-candidate kernels (amp_pipeline.cuh) spread one candidate's
+// few dozen sequential steps over 32 lanes; at |D| <= 16 most lanes idle or
+// repeat the same scalar work (the splitmix64 chain, the stage loops).  Here
+// a thread runs the reference's sequential code for its own candidate:
+//  * the placement is a 16 x 4-bit nibble vector in one register;
+//  * the Fisher–Yates draw r mod (k+1) uses a 32-bit Barrett step;
+//  * the bandwidths are per-link u8 codes with integer minima (the
+//    distinct-value table is sorted, so min code == code of the min);
+//  * the edge costs come from the per-class tables of IEEE quotients.
+// Every floating-point value is produced by the same operations in the
+// same order as the warp kernels and the reference (sequential sums,
+// strict comparisons), so records, cuts and the top-k are bit-identical
+// (the GPU parity tests run both paths).
+#pragma once
+
+#include "amp_common.cuh"
+#include "amp_pipeline.cuh"
+
+namespace amp {
+
+constexpr int kThreadMaxD = 16;
+
+__device__ __forceinline__ int nib(uint64_t v, int i) { return (int)((v >> (4 * i)) & 0xf); }
+
+// r mod d for d in [2, 32]: (hi mod d) * (2^32 mod d) + (lo mod d), each
+// 32-bit mod by a Barrett step with m = floor(2^32 / d) (quotient off by at
+// most one, fixed by one conditional subtraction).
+__device__ __forceinline__ uint32_t mod32(uint32_t x, uint32_t d, uint32_t m) {
+  uint32_t r = x - __umulhi(x, m) * d;
+  return r >= d ? r - d : r;
+}
+__device__ __forceinline__ uint32_t mod64_small(uint64_t r, uint32_t d) {
+  const uint32_t m = (uint32_t)(0x100000000ull / d);
+  const uint32_t t32 = (uint32_t)(0x100000000ull % d);
+  const uint32_t a = mod32((uint32_t)(r >> 32), d, m), b = mod32((uint32_t)r, d, m);
+  return mod32(a * t32 + b, d, m);  // < d*d + d <= 1056
+}
+
+// ---------------------------------------------------------------------------
+// K_place (thread per candidate)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
+  __shared__ uint8_t codeS[kThreadMaxD * kThreadMaxD];
+  __shared__ uint64_t base_perm;
+  const int D = p.D;
+  for (int x = threadIdx.x; x < D * D; x += blockDim.x) codeS[x] = p.bwcode[x];
+  if (threadIdx.x == 0) {
+    uint64_t v = 0;
+    for (int x = 0; x < D; ++x) v |= (uint64_t)p.base_order[x] << (4 * x);
+    base_perm = v;
+  }
+  __syncthreads();
+  const int maxpp = p.max_pp;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < p.n_chunk; u += stride) {
+    uint64_t index, out, pl;
+    int c;
+    decode_item(p, p.t0 + u, index, out, c, pl);
+    const ClassDev cl = p.cls[c];
+    const PairDev pr = p.pairs[cl.pair];
+    const int pp = cl.pp, dp = cl.dp, tmp = cl.tmp;
+    int fc = 0, flayer = -1;
+    double fval = 0.0;
+    if (pp > p.L) {  // optimizer.cpp:149-152
+      fc = AMP_FAIL_PP_GT_L;
+    } else if (pr.fail_code) {  // segment_times: first failing layer
+      fc = pr.fail_code;
+      flayer = pr.fail_layer;
+      fval = pr.fail_value;
+    }
+    if (fc == 0) {
+      // ---- placement: heuristic order (placement.cpp:37-49); p >= 1:
+      //      Fisher-Yates driven by splitmix64(seed ^ p) --------------------
+      uint64_t perm = base_perm;
+      if (pl != 0) {
+        uint64_t r = splitmix64(p.seed ^ pl);
+        for (int kk = D - 1; kk >= 1; --kk) {
+          const int jj = (int)mod64_small(r, (uint32_t)kk + 1u);
+          const uint64_t a = (perm >> (4 * kk)) & 0xf, b = (perm >> (4 * jj)) & 0xf;
+          perm &= ~((0xfull << (4 * kk)) | (0xfull << (4 * jj)));
+          perm |= (b << (4 * kk)) | (a << (4 * jj));
+          r = splitmix64(r);
+        }
+      }
+      int32_t* prow = p.placeb + u * D;
+      for (int x = 0; x < D; ++x) prow[x] = nib(perm, x);
+      // ---- stage-boundary bandwidths: min over all replicas and shards
+      //      (cost_model.cpp:164-174), as codes; the first invalid boundary
+      //      fails like p2p_time in the DP's edge function ---------------
+      int first_bad = -1;
+      double bad_val = 0.0;
+      for (int q = 0; q < pp - 1; ++q) {
+        int cm = 255;
+        for (int r = 0; r < dp; ++r)
+          for (int s = 0; s < tmp; ++s) {
+            const int cc = codeS[nib(perm, (q * dp + r) * tmp + s) * D +
+                                 nib(perm, ((q + 1) * dp + r) * tmp + s)];
+            cm = cc < cm ? cc : cm;
+          }
+        const double b = p.bwval[cm];
+        p.bwcb[u * maxpp + q] = (uint8_t)cm;
+        p.bwqb[u * maxpp + q] = b;
+        if (first_bad < 0 && !(b > 0)) {
+          first_bad = q;
+          bad_val = b;
+        }
+      }
+      if (first_bad >= 0) {
+        fc = AMP_FAIL_P2P_BANDWIDTH;
+        fval = bad_val;
+      }
+    }
+    CandWork w;
+    w.index = index;
+    w.out = out;
+    w.cls = c;
+    w.fail_code = fc;
+    w.fail_layer = flayer;
+    w.pad = 0;
+    w.fail_value = fval;
+    p.work[u] = w;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K_est (thread per candidate)
+// ---------------------------------------------------------------------------
+constexpr int kEstTWarps = 8;
+
+__global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
+  __shared__ uint8_t codeS[kThreadMaxD * kThreadMaxD];
+  __shared__ int lock;
+  __shared__ int n_top;
+  __shared__ double kth_total;
+  __shared__ int kth_failed;
+  __shared__ amp_record stage_rec[kEstTWarps][32];  // records handed to the warp leader
+  __shared__ amp_record topS[32];
+  const int D = p.D, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, maxpp = p.max_pp;
+  const int L = p.L, LP = L + 1;
+  amp_record* const gtop = p.cta_topk + (size_t)blockIdx.x * p.k;
+  amp_record* mytop = p.k <= 32 ? topS : gtop;
+  for (int x = threadIdx.x; x < D * D; x += blockDim.x) codeS[x] = p.bwcode[x];
+  if (threadIdx.x == 0) {
+    lock = 0;
+    n_top = 0;
+    kth_total = CUDART_INF;
+    kth_failed = 2;
+    if (!p.first_chunk) {  // CTA lists persist across chunks
+      for (int x = 0; x < p.k; ++x) {
+        if (gtop[x].fail_code < 0) break;
+        if (mytop != gtop) mytop[x] = gtop[x];
+        ++n_top;
+      }
+      if (p.k > 0 && n_top == p.k) {
+        kth_failed = mytop[p.k - 1].fail_code != 0;
+        kth_total = mytop[p.k - 1].total;
+      }
+    }
+  }
+  __syncthreads();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  // uniform trip count per warp (the top-k hand-off is warp-synchronous)
+  const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+  for (uint64_t wbase = first; wbase < p.n_chunk; wbase += stride) {
+    const uint64_t u = wbase + lane;
+    const bool live = u < p.n_chunk;
+    amp_record rec;
+    int cuts[kThreadMaxD + 1];
+    double st[kThreadMaxD], spar[kThreadMaxD];
+    int pp = 0, best_r = -1;
+    bool ok = false;
+    if (live) {
+      const CandWork w = p.work[u];
+      const ClassDev cl = p.cls[w.cls];
+      pp = cl.pp;
+      const int dp = cl.dp, tmp = cl.tmp, mbs = cl.mbs;
+      int fc = w.fail_code;
+      double fval = w.fail_value;
+      double pipeline = CUDART_NAN, dpsync = CUDART_NAN;
+      const int32_t* PL = p.placeb + u * D;
+      uint64_t perm = 0;
+      if (fc == 0) {
+        for (int x = 0; x < D; ++x) perm |= (uint64_t)PL[x] << (4 * x);
+        // ---- cuts: K_dp (memoised: its signature's representative), or
+        //      the k <= 2 DP here (light_cut2's operations, sequential) ---
+        if (pp >= 3 || p.cuts_given) {
+          const uint64_t src = (p.rep_of && !p.cuts_given && u < p.n_dp) ? p.rep_of[u] : u;
+          const uint8_t* ci = p.cutsb + src * (maxpp + 1);
+          for (int q = 0; q <= pp; ++q) cuts[q] = ci[q];
+        } else if (pp == 2) {
+          const double* Pf = p.prefix + (size_t)cl.pair * LP;
+          const double* Dm = p.domain + (size_t)cl.pair * p.nv_stride;
+          const uint16_t* sg = p.seg + (size_t)cl.pair * LP * LP;
+          const double g1 = (double)(cl.gas - 1);
+          const double* qt = p.qtab + ((size_t)w.cls * p.n_codes + p.bwcb[u * maxpp]) * L;
+          const double dm0 = Dm[0], PLL = Pf[L], P0 = Pf[0];
+          double best = CUDART_INF;
+          int bc = -1;
+          for (int c = 1; c < L; ++c) {
+            const double t1 = Pf[c] - P0;
+            const double sub = g1 * max0(t1 - Dm[sg[c * LP + L]]) + t1;
+            const double t2 = PLL - Pf[c];
+            const double term = t2 > dm0 ? g1 * (t2 - dm0) : 0.0;
+            const double g = ((sub + term) + t2) + qt[c];
+            if (g < best) {
+              best = g;
+              bc = c;
+            }
+          }
+          cuts[0] = 0;
+          cuts[1] = (int)(uint8_t)bc;
+          cuts[2] = L;
+        } else {
+          cuts[0] = 0;
+          cuts[1] = L;
+        }
+        // ---- stage_time (cost_model.cpp:88-98), params_in_range
+        //      (types.cpp:34-40), per-device parameter ceiling -----------
+        const double* tl = p.times + (size_t)cl.pair * L;
+        double worst_p = 0.0;
+        for (int j = 0; j < pp; ++j) {
+          double sum = 0.0, ps = 0.0;
+          for (int l = cuts[j]; l < cuts[j + 1]; ++l) {
+            sum += tl[l];
+            ps += p.param[l];
+          }
+          st[j] = sum;
+          spar[j] = ps;
+          worst_p = std_max(worst_p, ps / tmp);
+        }
+        if (p.has_ceiling && worst_p > p.ceiling) fc = AMP_FAIL_CEILING;
+      }
+      if (fc == 0) {
+        // ---- pipeline term (cost_model.cpp:100-120, 145-162, 176-212) ---
+        double slowest = st[0];  // std::max_element: first maximum
+        for (int j = 1; j < pp; ++j)
+          if (slowest < st[j]) slowest = st[j];
+        const double g1 = (double)(cl.gas - 1);
+        const double* qt = p.qtab + (size_t)w.cls * p.n_codes * L;
+        double tr = -CUDART_INF;
+        int rr = -1;
+        for (int r = 0; r < dp; ++r) {
+          double sum = 0.0;
+          for (int q = 0; q < pp - 1; ++q) {
+            int cm = 255;
+            for (int s = 0; s < tmp; ++s) {
+              const int cc = codeS[nib(perm, (q * dp + r) * tmp + s) * D +
+                                   nib(perm, ((q + 1) * dp + r) * tmp + s)];
+              cm = cc < cm ? cc : cm;
+            }
+            sum = sum + qt[(size_t)cm * L + cuts[q + 1]];  // (act[cut-1]*mbs) / b
+          }
+          for (int j = 0; j < pp; ++j) sum = sum + st[j];
+          const double t = g1 * slowest + sum;
+          if (t > tr) {  // strict '>' over ascending r: first maximum
+            tr = t;
+            rr = r;
+          }
+        }
+        // ---- dpsync_time (cost_model.cpp:122-143): groups (stage, shard) -
+        double worst = 0.0;
+        int bad_group = -1;
+        double bad_value = 0.0;
+        if (dp != 1) {
+          for (int g = 0; g < pp * tmp; ++g) {
+            const int j = g / tmp, s = g % tmp;
+            int cm = 255;
+            for (int r1 = 0; r1 < dp; ++r1) {
+              const int d1 = nib(perm, (j * dp + r1) * tmp + s);
+              for (int r2 = r1 + 1; r2 < dp; ++r2) {
+                const int cc = codeS[d1 * D + nib(perm, (j * dp + r2) * tmp + s)];
+                cm = cc < cm ? cc : cm;
+              }
+            }
+            const double b = p.bwval[cm];
+            if (!(b > 0)) {
+              if (bad_group < 0) {
+                bad_group = g;
+                bad_value = b;
+              }
+            } else {
+              const double message = spar[j] * p.bpp / tmp;
+              worst = std_max(worst, 2.0 * (double)(dp - 1) * message / ((double)dp * b));
+            }
+          }
+        }
+        if (bad_group >= 0) {
+          fc = AMP_FAIL_ALLREDUCE_BANDWIDTH;
+          fval = bad_value;
+        } else {
+          pipeline = tr;
+          dpsync = worst;
+          best_r = rr;
+        }
+      }
+      rec.index = w.index;
+      rec.pp = pp;
+      rec.dp = dp;
+      rec.tmp = tmp;
+      rec.mbs = mbs;
+      rec.fail_code = fc;
+      rec.fail_layer = fc == AMP_FAIL_PROFILE_MISS ? w.fail_layer : -1;
+      rec.fail_value = fc == AMP_FAIL_P2P_BANDWIDTH || fc == AMP_FAIL_ALLREDUCE_BANDWIDTH ? fval : 0.0;
+      ok = fc == 0;
+      rec.pipeline_time = ok ? pipeline : CUDART_NAN;
+      rec.dpsync_time = ok ? dpsync : CUDART_NAN;
+      rec.total = ok ? pipeline + dpsync : CUDART_NAN;
+      if (p.all) p.all[w.out] = rec;
+      if (p.all_cuts) {
+        int32_t* o = p.all_cuts + w.out * (maxpp + 1);
+        for (int q = 0; q <= maxpp; ++q) o[q] = (ok && q <= pp) ? cuts[q] : -1;
+      }
+      if (p.all_stage) {
+        double* o = p.all_stage + w.out * maxpp;
+        for (int q = 0; q < maxpp; ++q) o[q] = (ok && q < pp) ? st[q] : CUDART_NAN;
+      }
+      if (p.all_edge) {  // edges of the slowest replica (cost_model.cpp:203-207)
+        double* o = p.all_edge + w.out * maxpp;
+        for (int q = 0; q < maxpp; ++q) {
+          double v = CUDART_NAN;
+          if (ok && q + 1 < pp) {
+            int cm = 255;
+            for (int s = 0; s < tmp; ++s) {
+              const int cc = codeS[nib(perm, (q * dp + best_r) * tmp + s) * D +
+                                   nib(perm, ((q + 1) * dp + best_r) * tmp + s)];
+              cm = cc < cm ? cc : cm;
+            }
+            v = p.act[cuts[q + 1] - 1] * mbs / p.bwval[cm];
+          }
+          o[q] = v;
+        }
+      }
+      if (p.all_place) {
+        int32_t* o = p.all_place + w.out * D;
+        for (int x = 0; x < D; ++x) o[x] = ok ? nib(perm, x) : -1;
+      }
+    }
+    // ---- CTA top-k (rank_records key): lanes that pass the cheap check
+    //      against the current k-th entry hand their record to the leader --
+    if (p.k > 0) {
+      bool cand = false;
+      if (live) {
+        const int kf = *(volatile int*)&kth_failed;
+        const double kt = *(volatile double*)&kth_total;
+        const int rf = ok ? 0 : 1;
+        cand = !(rf > kf || (rf == 0 && kf == 0 && rec.total > kt));
+        if (cand) stage_rec[wib][lane] = rec;
+      }
+      unsigned m = __ballot_sync(0xffffffffu, cand);
+      __syncwarp();
+      if (lane == 0 && m) {
+        while (atomicCAS(&lock, 0, 1) != 0) __nanosleep(32);
+        __threadfence_block();
+        int n = *(volatile int*)&n_top;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          topk_insert(mytop, n, p.k, stage_rec[wib][b]);
+        }
+        *(volatile int*)&n_top = n;
+        if (n == p.k) {
+          *(volatile int*)&kth_failed = mytop[p.k - 1].fail_code != 0;
+          *(volatile double*)&kth_total = mytop[p.k - 1].total;
+        }
+        __threadfence_block();
+        atomicExch(&lock, 0);
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // store the CTA list (padded to k) for the next chunk / the merge
+  if (threadIdx.x == 0 && p.k > 0) {
+    if (mytop != gtop)
+      for (int x = 0; x < n_top; ++x) gtop[x] = mytop[x];
+    for (int x = n_top; x < p.k; ++x) {
+      amp_record e;
+      e.index = ~0ull;
+      e.total = e.pipeline_time = e.dpsync_time = CUDART_NAN;
+      e.pp = e.dp = e.tmp = e.mbs = 0;
+      e.fail_code = -1;
+      e.fail_layer = -1;
+      e.fail_value = 0.0;
+      gtop[x] = e;
+    }
+  }
+}
+
+}  // namespace amp

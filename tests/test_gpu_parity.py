@@ -320,3 +320,27 @@ def test_memoised_dp_equals_per_candidate_dp(name):
     assert np.array_equal(c1, c2)
     assert t1["index"].tolist() == t2["index"].tolist()
     assert s1["dp_instances"] < s2["dp_instances"]  # memoisation did skip repeats
+
+
+@pytest.mark.parametrize("name", ["hetero_cluster", "hetero_model"])
+def test_thread_and_warp_kernels_agree(name, monkeypatch):
+    """Thread-per-candidate K_place/K_est (amp_thread.cuh, |D| <= 16) and the
+    warp-per-candidate kernels produce identical records, cuts, edges,
+    placements and top-k on a shuffled sweep."""
+    sc = scenario(name)
+    enc = P.EncodedProblem.from_scenario(sc)
+    outs = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("AMP_NO_THREAD", env)
+        else:
+            monkeypatch.delenv("AMP_NO_THREAD", raising=False)
+        with planner.Searcher(enc, placements_per_class=700, seed=13) as s:
+            top, allr, bufs = s.run(0, s.num_candidates, k=24, want_all=True, details=True,
+                                    placement=True)
+        outs.append((top, allr, bufs))
+    (t1, a1, b1), (t2, a2, b2) = outs
+    assert np.array_equal(a1.view(np.uint8), a2.view(np.uint8))
+    for key in ("cuts", "stage_times", "edge_times", "placement"):
+        assert np.array_equal(b1[key], b2[key], equal_nan=True), key
+    assert t1.view(np.uint8).tobytes() == t2.view(np.uint8).tobytes()
