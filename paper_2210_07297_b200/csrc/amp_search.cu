@@ -48,25 +48,58 @@ struct PhaseTimer {
   }
 };
 
+// Device buffers come from the device's stream-ordered memory pool, kept
+// warm across contexts (release threshold = max), so a create/run/destroy
+// cycle does not pay cudaMalloc/cudaFree.  Allocation and free are ordered
+// on the stream of the API call in flight (g_alloc_stream: the context's
+// stream); a fresh allocation is synchronised once so synchronous copies on
+// other streams may use it.
+thread_local cudaStream_t g_alloc_stream = nullptr;
+
+void warm_pool(int device) {
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (std::find(done.begin(), done.end(), device) != done.end()) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done.push_back(device);
+}
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
-  ~DevBuf() {
-    if (p) cudaFree(p);
+  cudaStream_t s = nullptr;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    bytes = 0;
   }
   cudaError_t ensure(size_t n) {
     if (n <= bytes && p) return cudaSuccess;
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-    cudaError_t e = cudaMalloc(&p, n ? n : 16);
+    release();
+    s = g_alloc_stream;
+    cudaError_t e = cudaMallocAsync(&p, n ? n : 16, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e == cudaSuccess) bytes = n;
+    else p = nullptr;
     return e;
   }
   template <class T>
   T* as() const {
     return reinterpret_cast<T*>(p);
   }
+};
+
+// Sets the allocation stream for the duration of an API call.
+struct AllocStream {
+  cudaStream_t prev;
+  explicit AllocStream(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
+  ~AllocStream() { g_alloc_stream = prev; }
 };
 
 std::vector<int> divisors(int n) {
@@ -375,7 +408,9 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
     return fail(ctx, AMP_E_NOT_BUILT,
                 "device is sm_" + std::to_string(prop.major * 10 + prop.minor) +
                     "; this build contains sm_100a kernels only");
+  warm_pool(ctx->device);
   CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  g_alloc_stream = ctx->stream;
   CK(cudaEventCreate(&ctx->ev0));
   CK(cudaEventCreate(&ctx->ev1));
   CK(cudaEventCreate(&ctx->ev2));
@@ -1166,6 +1201,7 @@ const char* amp_last_error(void) { return g_last_error.c_str(); }
 
 int amp_search_create(amp_ctx** out, const amp_problem* problem,
                       const amp_search_config* config) {
+  AllocStream alloc_guard(nullptr);  // setup() points it at the new stream
   if (!out) {
     g_last_error = "out is NULL";
     return AMP_E_INVALID;
@@ -1190,8 +1226,9 @@ void amp_search_destroy(amp_ctx* ctx) {
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->ev2) cudaEventDestroy(ctx->ev2);
   for (cudaEvent_t e : ctx->kev) cudaEventDestroy(e);
-  if (ctx->stream) cudaStreamDestroy(ctx->stream);
-  delete ctx;
+  cudaStream_t st = ctx->stream;
+  delete ctx;  // buffers return to the pool, ordered on the context stream
+  if (st) cudaStreamDestroy(st);
 }
 
 const char* amp_search_last_error(const amp_ctx* ctx) {
@@ -1254,6 +1291,7 @@ int amp_search_partition(const amp_ctx* ctx, int32_t n_parts, uint64_t* bounds) 
 
 int amp_search_run(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k, amp_record* topk,
                    int32_t* n_topk, amp_record* all, const amp_details* all_details) {
+  AllocStream alloc_guard(ctx ? ctx->stream : nullptr);
   if (!ctx) return AMP_E_INVALID;
   const uint64_t N = amp_search_num_candidates(ctx);
   if (begin > end || end > N) return fail(ctx, AMP_E_INVALID, "range outside [0, num_candidates)");
@@ -1306,6 +1344,7 @@ int amp_search_run(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k, amp_re
 
 int amp_search_evaluate(amp_ctx* ctx, const uint64_t* indices, int32_t n, amp_record* out,
                         const amp_details* details) {
+  AllocStream alloc_guard(ctx ? ctx->stream : nullptr);
   if (!ctx || n < 0 || (n > 0 && (!indices || !out))) return AMP_E_INVALID;
   if (n == 0) return AMP_OK;
   const uint64_t N = amp_search_num_candidates(ctx);
@@ -1339,6 +1378,7 @@ int amp_search_evaluate(amp_ctx* ctx, const uint64_t* indices, int32_t n, amp_re
 
 int amp_search_estimate(amp_ctx* ctx, const uint64_t* indices, const int32_t* cuts, int32_t n,
                         amp_record* out, const amp_details* details) {
+  AllocStream alloc_guard(ctx ? ctx->stream : nullptr);
   if (!ctx || n < 0 || (n > 0 && (!indices || !cuts || !out))) return AMP_E_INVALID;
   if (n == 0) return AMP_OK;
   const uint64_t N = amp_search_num_candidates(ctx);
@@ -1389,6 +1429,7 @@ int amp_search_estimate(amp_ctx* ctx, const uint64_t* indices, const int32_t* cu
 
 int amp_search_run_device(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k,
                           amp_record* d_topk, void* stream) {
+  AllocStream alloc_guard(ctx ? ctx->stream : nullptr);
   if (!ctx || k < 1 || k > 4096 || !d_topk) return AMP_E_INVALID;
   const uint64_t N = amp_search_num_candidates(ctx);
   if (begin > end || end > N) return fail(ctx, AMP_E_INVALID, "range outside [0, num_candidates)");
@@ -1397,6 +1438,7 @@ int amp_search_run_device(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k,
 
 int amp_search_run_device_shard(amp_ctx* ctx, int32_t shard, int32_t n_shards, int32_t k,
                                 amp_record* d_topk, void* stream) {
+  AllocStream alloc_guard(ctx ? ctx->stream : nullptr);
   if (!ctx || k < 1 || k > 4096 || !d_topk) return AMP_E_INVALID;
   if (n_shards < 1 || shard < 0 || shard >= n_shards)
     return fail(ctx, AMP_E_INVALID, "shard must be in [0, n_shards)");
@@ -1412,6 +1454,7 @@ uint64_t amp_search_shard_size(const amp_ctx* ctx, int32_t shard, int32_t n_shar
 
 int amp_search_merge_topk_device(amp_ctx* ctx, const amp_record* d_in, int32_t n_in, int32_t k,
                                  amp_record* d_out, void* stream) {
+  AllocStream alloc_guard(ctx ? ctx->stream : nullptr);
   if (!ctx || !d_in || !d_out || n_in < 1 || k < 1 || k > 4096) return AMP_E_INVALID;
   CK(cudaSetDevice(ctx->device));
   return launch_merge(ctx, d_in, n_in, k, d_out, reinterpret_cast<cudaStream_t>(stream));
