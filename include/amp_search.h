@@ -44,6 +44,9 @@ extern "C" {
 #define AMP_E_OOM (-3)         /* device allocation failed                  */
 #define AMP_E_UNSUPPORTED (-4) /* problem outside the supported envelope    */
 #define AMP_E_NOT_BUILT (-5)   /* no sm_100a device / kernels unavailable   */
+#define AMP_E_CANDIDATE (-6)   /* a strategy the search must evaluate failed
+                                  (the reference throws there); the failing
+                                  record is returned to the caller         */
 
 /* ---- per-candidate failure codes (data) ------------------------------- */
 /* Message texts the host rebuilds verbatim (reference file:line):          */
@@ -221,6 +224,15 @@ int amp_search_evaluate(amp_ctx* ctx, const uint64_t* indices, int32_t n,
  * cost_model.cpp:176-212).  Host buffers, records in input order.          */
 int amp_search_estimate(amp_ctx* ctx, const uint64_t* indices, const int32_t* cuts, int32_t n,
                         amp_record* out, const amp_details* details);
+/* Evaluate caller placements: candidate i is class classes[i] with the
+ * placement placements[i * |D| .. +|D|) (rank -> device id, a permutation)
+ * instead of one of the P generated ones; with cuts == NULL the layer
+ * partition is solved (DP), else the caller's cuts are estimated.  Used by
+ * the annealing search (its domino-tiling proposals, placement.cpp:299-398)
+ * and by any caller with its own placements.  Host buffers.                */
+int amp_search_evaluate_placed(amp_ctx* ctx, const int32_t* classes, const int32_t* placements,
+                               const int32_t* cuts, int32_t n, amp_record* out,
+                               const amp_details* details);
 int amp_search_run_device(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k,
                           amp_record* d_topk, void* stream);
 /* Shard `shard` of n_shards (multi-GPU): placements
@@ -240,6 +252,41 @@ int amp_search_merge_topk_device(amp_ctx* ctx, const amp_record* d_in, int32_t n
                                  int32_t k, amp_record* d_out, void* stream);
 
 int amp_search_last_stats(const amp_ctx* ctx, amp_stats* out);
+
+/* ---- annealing search (placement.cpp:299-398, Algorithm 2) ------------ */
+typedef struct amp_anneal_config {
+  int32_t iterations;          /* >= 1                                      */
+  int32_t budget;              /* top strategies ranked                     */
+  uint64_t seed;               /* std::mt19937_64 seed                      */
+  double initial_temperature;  /* reference default 1.0                     */
+  double cooling;              /* 0.97                                      */
+  double min_temperature;      /* 1e-3                                      */
+  int32_t record_all;          /* record rejected evaluated states too      */
+  int32_t neighbor_retries;    /* 20                                        */
+} amp_anneal_config;
+
+typedef struct amp_anneal_entry {
+  amp_record estimated;        /* degrees, mbs, total / pipeline / dpsync    */
+  int32_t iteration;           /* 0 = initial state                          */
+  int32_t accepted;
+  int32_t reserved[2];
+} amp_anneal_entry;
+
+/* The reference's annealing chain, bit for bit (same mt19937_64 draws,
+ * domino tilings, temperatures and acceptances), with every proposal's DP
+ * and estimate evaluated on the GPU (amp_search_evaluate_placed).  `record`
+ * receives the recorded states in visit order ([cap]; cap >= iterations+1
+ * always suffices), record_place [cap][|D|] and record_cuts
+ * [cap][max_pp + 1] their placements and cuts (nullable); top[budget] the
+ * record indices of the best `budget` states by (total, pp, dp, tmp, mbs)
+ * (the reference's std::sort).  AMP_E_CANDIDATE: a strategy failed to
+ * evaluate (profile miss ...) — the reference aborts there; `failed`
+ * (nullable) receives its record.  The problem must be the one the context
+ * was created from.                                                        */
+int amp_search_anneal(amp_ctx* ctx, const amp_problem* problem, const amp_anneal_config* cfg,
+                      amp_anneal_entry* record, int32_t* record_place, int32_t* record_cuts,
+                      int32_t cap, int32_t* n_record, int32_t* top, int32_t* n_top,
+                      double* initial_cost, amp_record* failed);
 
 /* ---- standalone layer-partition DP (pipeline_dp.cpp:70-149) ----------- */
 /* One instance: SegmentTimes over layer_times[L], `stages` stages, gas,

@@ -18,9 +18,14 @@
 #include <iostream>
 #include <string>
 
+#include <cstdio>
+#include <fstream>
+
 #include "parplan/json_io.hpp"
 #include "parplan/optimizer.hpp"
+#include "parplan/placement.hpp"
 #include "parplan/report.hpp"
+#include "parplan/simulator.hpp"
 
 int main(int argc, char** argv) {
   if (argc < 7) {
@@ -43,6 +48,45 @@ int main(int argc, char** argv) {
       }
     }
     if (argc >= 10 && std::atof(argv[9]) > 0) opts.max_params_per_device = std::atof(argv[9]);
+    if (const char* mode = std::getenv("GEN_MODE"); mode && std::strncmp(mode, "anneal", 6) == 0) {
+      // CLI `anneal` (parplan_main.cpp:219-256): GEN_MODE=anneal:<iters>:<seed>[:trace]
+      parplan::AnnealOptions ao;
+      ao.budget = opts.budget;
+      ao.cost_options = opts.cost_options;
+      int iters = 200;
+      unsigned long long seed = 0;
+      char tr[16] = {0};
+      std::sscanf(mode, "anneal:%d:%llu:%15s", &iters, &seed, tr);
+      ao.iterations = iters;
+      ao.seed = seed;
+      parplan::AnnealResult result =
+          parplan::anneal(model, cluster, profile, std::atoi(argv[4]), ao);
+      std::vector<parplan::CandidateRecord> candidates;
+      for (size_t i = 0; i < result.top.size(); ++i) {
+        parplan::CandidateRecord record;
+        record.strategy = result.top[i].strategy;
+        record.estimated = result.top[i].estimated;
+        record.rank = static_cast<int>(i) + 1;
+        parplan::SimOptions sim_options;
+        sim_options.cost_options = opts.cost_options;
+        record.simulated = parplan::simulate(record.strategy, model, cluster, profile,
+                                             std::atoi(argv[4]), sim_options).iteration_time;
+        candidates.push_back(std::move(record));
+      }
+      parplan::write_report(candidates, argv[6]);
+      parplan::print_candidate_table(std::cout, candidates);
+      if (tr[0]) {
+        std::ofstream out(std::string(argv[6]) + ".trace");
+        for (const auto& entry : result.record) {
+          nlohmann::json line = parplan::strategy_to_json(entry.strategy);
+          line["iteration"] = entry.iteration;
+          line["accepted"] = entry.accepted;
+          line["estimated_total"] = entry.estimated.total;
+          out << line.dump() << "\n";
+        }
+      }
+      return 0;
+    }
     if (const char* mode = std::getenv("GEN_MODE")) {
       const auto bal = std::strcmp(mode, "param-balance") == 0 ? parplan::BalanceMode::kParamBalance
                                                                : parplan::BalanceMode::kLayerBalance;

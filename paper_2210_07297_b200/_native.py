@@ -19,6 +19,7 @@ AMP_E_CUDA = -2
 AMP_E_OOM = -3
 AMP_E_UNSUPPORTED = -4
 AMP_E_NOT_BUILT = -5
+AMP_E_CANDIDATE = -6
 
 AMP_FAIL_NONE = 0
 AMP_FAIL_PP_GT_L = 1
@@ -93,6 +94,28 @@ class AmpRecord(C.Structure):
 assert C.sizeof(AmpRecord) == 64
 
 
+class AmpAnnealConfig(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int32),
+        ("budget", C.c_int32),
+        ("seed", C.c_uint64),
+        ("initial_temperature", C.c_double),
+        ("cooling", C.c_double),
+        ("min_temperature", C.c_double),
+        ("record_all", C.c_int32),
+        ("neighbor_retries", C.c_int32),
+    ]
+
+
+class AmpAnnealEntry(C.Structure):
+    _fields_ = [
+        ("estimated", AmpRecord),
+        ("iteration", C.c_int32),
+        ("accepted", C.c_int32),
+        ("reserved", C.c_int32 * 2),
+    ]
+
+
 class AmpDetails(C.Structure):
     _fields_ = [
         ("cuts", _ip),
@@ -154,6 +177,11 @@ SIGNATURES = [
                                       C.POINTER(AmpDetails)]),
     ("amp_search_estimate", C.c_int, [C.c_void_p, _u64p, _ip, C.c_int32, C.POINTER(AmpRecord),
                                       C.POINTER(AmpDetails)]),
+    ("amp_search_evaluate_placed", C.c_int, [C.c_void_p, _ip, _ip, _ip, C.c_int32,
+                                             C.POINTER(AmpRecord), C.POINTER(AmpDetails)]),
+    ("amp_search_anneal", C.c_int, [C.c_void_p, C.POINTER(AmpProblem), C.POINTER(AmpAnnealConfig),
+                                    C.POINTER(AmpAnnealEntry), _ip, _ip, C.c_int32, _ip, _ip, _ip,
+                                    _dp, C.POINTER(AmpRecord)]),
     ("amp_search_run_device", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int32, C.c_void_p,
                                         C.c_void_p]),
     ("amp_search_run_device_shard", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32,

@@ -101,6 +101,16 @@ def _parser() -> argparse.ArgumentParser:
     b.add_argument("--mode", default="layer-balance", choices=["layer-balance", "param-balance"])
     b.add_argument("--report", default="report.json", help="output report path")
     b.add_argument("--device", type=int, default=0, help="CUDA device (engine option)")
+    an = sub.add_parser("anneal", help="simulated-annealing search over domino-tiling placements")
+    _add_common(an)
+    an.add_argument("--iterations", type=_positive_int, default=200, help="annealing iterations")
+    an.add_argument("--seed", type=int, default=0, help="random seed")
+    an.add_argument("--budget", type=_positive_int, default=10,
+                    help="top recorded strategies to keep and simulate")
+    an.add_argument("--report", default="report.json", help="output report path")
+    an.add_argument("--trace", default="", help="dump accepted states as JSON lines")
+    an.add_argument("--record-all", action="store_true", help="record rejected evaluated states too")
+    an.add_argument("--device", type=int, default=0, help="CUDA device (engine option)")
     g = sub.add_parser("gen-profile", help="generate a synthetic profile table from per-layer flops")
     g.add_argument("--model", required=True)
     g.add_argument("--device-flops", required=True, type=_positive_float)
@@ -146,6 +156,38 @@ def cmd_baseline(a) -> int:
     return 0
 
 
+def cmd_anneal(a) -> int:
+    """parplan_main.cpp:219-256 over anneal.anneal (chain on the engine)."""
+    from . import anneal as A
+    from .jsonfmt import dumps_compact
+    model = P.load_model(a.model)
+    cluster = P.load_cluster(a.cluster)
+    profile = P.load_profile(a.profile)
+    opts = A.AnnealOptions(iterations=a.iterations, seed=a.seed, budget=a.budget,
+                           record_all=a.record_all, cost_options=_cost_options(a))
+    try:
+        res = A.anneal(model, cluster, profile, a.gbs, opts, device=a.device)
+    except A.ProfileMissError as e:
+        raise ProfileMissError(str(e))
+    cands = []
+    for i, t in enumerate(res.top):
+        cands.append(planner.CandidateRecord(t.strategy, t.estimated, i + 1, t.simulated))
+    R.write_report(cands, a.report)
+    R.print_candidate_table(sys.stdout, cands)
+    if a.trace:
+        try:
+            with open(a.trace, "w") as f:
+                for e in res.record:
+                    line = R.strategy_to_json(e.strategy)
+                    line["iteration"] = e.iteration
+                    line["accepted"] = e.accepted
+                    line["estimated_total"] = float(e.estimated.total)
+                    f.write(dumps_compact(line) + "\n")
+        except OSError:
+            raise P.ParseError(f"cannot open trace file for writing: {a.trace}")
+    return 0
+
+
 def cmd_gen_profile(a) -> int:
     """parplan_main.cpp:170-188 with analytic_layer_time (cost_model.cpp:61-68)."""
     model = P.load_model(a.model)
@@ -167,6 +209,8 @@ def main(argv: Optional[List[str]] = None) -> int:
     try:
         if a.cmd == "plan":
             return cmd_plan(a)
+        if a.cmd == "anneal":
+            return cmd_anneal(a)
         if a.cmd == "baseline":
             return cmd_baseline(a)
         if a.cmd == "gen-profile":

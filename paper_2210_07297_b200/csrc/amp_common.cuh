@@ -143,6 +143,7 @@ struct EvalParams {
   const uint64_t* n_rep;      // device count of representatives
   const double* prog_inner;   // [n_progs] unpadded inner iterations per program
   unsigned long long* exec_counters;  // [2]: DP instances solved, inner iterations executed
+  const int32_t* given_place;  // [n_work][D] caller placements (rank -> device) or NULL
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

@@ -101,7 +101,12 @@ __global__ void __launch_bounds__(256) k_place(EvalParams p) {
     if (fc == 0) {
       // ---- placement: heuristic order (placement.cpp:37-49); p >= 1:
       //      Fisher-Yates driven by splitmix64(seed ^ p) ------------------
-      if (D <= 32) {
+      if (p.given_place) {  // caller placement (anneal proposals, evaluate_placed)
+        const int32_t* g = p.given_place + (p.t0 + u) * D;
+        for (int x = lane; x < D; x += 32) prow[x] = g[x];
+        if (D <= 32) placeS[lane] = lane < D ? g[lane] : -1;
+        __syncwarp();
+      } else if (D <= 32) {
         int v = lane < D ? p.base_order[lane] : -1;
         if (pl != 0) {
           // lane kk keeps the draw of step kk, then reduces it once:

@@ -848,7 +848,7 @@ void account(amp_ctx* ctx, uint64_t begin, uint64_t end, const uint64_t* list, i
 int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64_t* d_list,
                     uint64_t n_work, int32_t k, bool want_all, bool want_details,
                     bool want_place, const uint8_t* d_given_cuts = nullptr,
-                    bool want_sim = false) {
+                    bool want_sim = false, const int32_t* d_given_place = nullptr) {
   EvalParams ep{};
   ep.L = ctx->L;
   ep.D = ctx->D;
@@ -881,6 +881,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   }
   ep.n_work = n_work;
   ep.index_list = d_list;
+  ep.given_place = d_given_place;
   ep.counter = ctx->counter.as<unsigned long long>();
   ep.bp = ctx->bp.as<uint8_t>();
   ep.bp_stride = ctx->bp_stride;
@@ -1424,6 +1425,72 @@ int amp_search_estimate(amp_ctx* ctx, const uint64_t* indices, const int32_t* cu
   ctx->stats.ctas = ctx->n_ctas;
   ctx->stats.candidates = (uint64_t)n;
   ctx->stats.dp_inner = ctx->stats.fp64_ops = 0;
+  return AMP_OK;
+}
+
+int amp_search_evaluate_placed(amp_ctx* ctx, const int32_t* classes, const int32_t* placements,
+                               const int32_t* cuts, int32_t n, amp_record* out,
+                               const amp_details* details) {
+  AllocStream alloc_guard(ctx ? ctx->stream : nullptr);
+  if (!ctx || n < 0 || (n > 0 && (!classes || !placements || !out))) return AMP_E_INVALID;
+  if (n == 0) return AMP_OK;
+  const int D = ctx->D, W = ctx->max_pp + 1;
+  std::vector<uint64_t> idx(n);
+  std::vector<uint8_t> c8;
+  if (cuts) c8.assign((size_t)n * W, 0);
+  std::vector<char> seen(D);
+  for (int32_t i = 0; i < n; ++i) {
+    if (classes[i] < 0 || classes[i] >= (int32_t)ctx->classes.size())
+      return fail(ctx, AMP_E_INVALID, "class outside [0, num_classes)");
+    idx[i] = (uint64_t)classes[i] * ctx->P;  // placement slot 0, overridden
+    std::fill(seen.begin(), seen.end(), 0);
+    for (int x = 0; x < D; ++x) {
+      const int d = placements[(size_t)i * D + x];
+      if (d < 0 || d >= D || seen[d])
+        return fail(ctx, AMP_E_INVALID,
+                    "placement " + std::to_string(i) + " is not a permutation of the devices");
+      seen[d] = 1;
+    }
+    if (cuts) {
+      const int pp = ctx->classes[classes[i]].pp;
+      const int32_t* c = cuts + (size_t)i * W;
+      if (pp <= ctx->L) {
+        bool ok = c[0] == 0 && c[pp] == ctx->L;
+        for (int j = 0; j < pp && ok; ++j) ok = c[j] < c[j + 1];
+        if (!ok)
+          return fail(ctx, AMP_E_INVALID,
+                      "cuts of candidate " + std::to_string(i) +
+                          " must rise strictly from 0 to n_layers over pp stages");
+      }
+      for (int j = 0; j <= pp && j < W; ++j) c8[(size_t)i * W + j] = (uint8_t)c[j];
+    }
+  }
+  CK(cudaSetDevice(ctx->device));
+  CK(upload(ctx->index_list, idx.data(), idx.size()));
+  DevBuf d_place, d_cuts;
+  CK(upload(d_place, placements, (size_t)n * D));
+  if (cuts) CK(upload(d_cuts, c8.data(), c8.size()));
+  const bool det = details && (details->cuts || details->stage_times || details->edge_times);
+  CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  ctx->launches = 0;
+  int rc = launch_evaluate(ctx, nullptr, ctx->index_list.as<uint64_t>(), (uint64_t)n, 1, true, det,
+                           details && details->placement, cuts ? d_cuts.as<uint8_t>() : nullptr,
+                           details && details->simulated, d_place.as<int32_t>());
+  if (rc) return rc;
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  CK(cudaMemcpyAsync(out, ctx->o_all.p, sizeof(amp_record) * n, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  rc = copy_details(ctx, (uint64_t)n, details);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  account(ctx, 0, 0, idx.data(), n);
+  resolve_kernel_times(ctx);
+  ctx->stats.kernel_ms = ms;
+  ctx->stats.total_ms = ms;
+  ctx->stats.launches = ctx->launches;
+  ctx->stats.ctas = ctx->n_ctas;
   return AMP_OK;
 }
 

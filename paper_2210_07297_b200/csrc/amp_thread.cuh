@@ -75,7 +75,11 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
       // ---- placement: heuristic order (placement.cpp:37-49); p >= 1:
       //      Fisher-Yates driven by splitmix64(seed ^ p) --------------------
       uint64_t perm = base_perm;
-      if (pl != 0) {
+      if (p.given_place) {  // caller placement (anneal proposals, evaluate_placed)
+        const int32_t* g = p.given_place + (p.t0 + u) * D;
+        perm = 0;
+        for (int x = 0; x < D; ++x) perm |= (uint64_t)g[x] << (4 * x);
+      } else if (pl != 0) {
         uint64_t r = splitmix64(p.seed ^ pl);
         for (int kk = D - 1; kk >= 1; --kk) {
           const int jj = (int)mod64_small(r, (uint32_t)kk + 1u);

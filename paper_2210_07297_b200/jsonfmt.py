@@ -26,3 +26,9 @@ def _clean(o):
 def dumps(obj) -> str:
     return json.dumps(_clean(obj), indent=2, sort_keys=True, ensure_ascii=False,
                       separators=(",", ": "), allow_nan=False)
+
+
+def dumps_compact(obj) -> str:
+    """nlohmann::json::dump() without indent."""
+    return json.dumps(_clean(obj), sort_keys=True, ensure_ascii=False, separators=(",", ":"),
+                      allow_nan=False)

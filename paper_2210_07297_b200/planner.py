@@ -210,6 +210,23 @@ class Searcher:
             self.ctx)
         return out, bufs or {}
 
+    def evaluate_placed(self, classes: Sequence[int], placements: np.ndarray,
+                        cuts: Optional[np.ndarray] = None, details: bool = True,
+                        placement: bool = True, simulate: bool = False):
+        """Caller placements ([n][|D|]) of classes[i]; DP when cuts is None."""
+        ci = np.ascontiguousarray(classes, dtype=np.int32)
+        n = len(ci)
+        pl = np.ascontiguousarray(placements, dtype=np.int32).reshape(n, self.n_devices)
+        cu = None if cuts is None else np.ascontiguousarray(cuts, dtype=np.int32)
+        out = np.zeros(n, dtype=RECORD_DTYPE)
+        d, bufs = self._details(n, details, placement, simulate)
+        N.check(self.lib.amp_search_evaluate_placed(
+            self.ctx, ci.ctypes.data_as(N._ip), pl.ctypes.data_as(N._ip),
+            cu.ctypes.data_as(N._ip) if cu is not None else None, n,
+            out.ctypes.data_as(C.POINTER(N.AmpRecord)), C.byref(d) if d is not None else None),
+            self.ctx)
+        return out, bufs or {}
+
     def run_device(self, begin: int, end: int, k: int, d_topk_ptr: int, stream_ptr: int = 0):
         N.check(self.lib.amp_search_run_device(self.ctx, begin, end, k, C.c_void_p(d_topk_ptr),
                                                C.c_void_p(stream_ptr)), self.ctx)

@@ -35,6 +35,10 @@ CASES = {
     "C2_baseline_layer": ("hetero_cluster", 32, 1, None),
     "C3_baseline_param": ("hetero_model", 64, 1, None),
     "C1_partial_baseline_layer": ("homogeneous", 32, 1, "partial"),
+    # CLI `anneal` (acceptance criterion 9: --budget 5 --iterations 60 --seed 17)
+    "C1_anneal_i60_s17": ("homogeneous", 32, 5, None),
+    "C2_anneal_i200_s3": ("hetero_cluster", 32, 10, None),
+    "C3_anneal_i120_s11": ("hetero_model", 64, 10, None),
 }
 
 
@@ -65,6 +69,9 @@ def main():
         env = dict(os.environ)
         if "baseline" in case:
             env["GEN_MODE"] = "param-balance" if case.endswith("param") else "layer-balance"
+        if "anneal" in case:  # C?_anneal_i<iters>_s<seed>, with the trace
+            it, sd = case.split("_i")[1].split("_s")
+            env["GEN_MODE"] = f"anneal:{it}:{sd}:trace"
         r = subprocess.run([BIN, os.path.join(d, "model.json"), os.path.join(d, "cluster.json"), prof,
                             str(gbs), str(budget), rep], capture_output=True, text=True, env=env)
         with open(os.path.join(OUT, case + ".txt"), "w") as f:

@@ -146,3 +146,29 @@ def test_megatron_host_rules_match_reference_unit_cases():
         Bl.uniform_assignment(3, 4)
     m = scenario("hetero_model").model
     assert Bl.param_balance_assignment(m, 4) == [0, 3, 6, 9, 24]
+
+
+ANNEAL = {"C1_anneal_i60_s17": ("homogeneous", 32, 5, 60, 17),
+          "C2_anneal_i200_s3": ("hetero_cluster", 32, 10, 200, 3),
+          "C3_anneal_i120_s11": ("hetero_model", 64, 10, 120, 11)}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", sorted(ANNEAL))
+def test_cli_anneal_reproduces_reference_chain(case, tmp_path):
+    """`anneal` (placement.cpp:299-398) with every
+    proposal's DP + estimate on the GPU reproduces the reference chain bit
+    for bit: the same report.json (top states, estimates, simulated times),
+    table and the whole recorded trace (JSON lines)."""
+    name, gbs, budget, iters, seed = ANNEAL[case]
+    p = _write_inputs(tmp_path, name)
+    rep, trace = str(tmp_path / "anneal.json"), str(tmp_path / "anneal.trace")
+    r = _cli(["anneal", "--model", p["model"], "--cluster", p["cluster"], "--profile", p["profile"],
+              "--gbs", str(gbs), "--budget", str(budget), "--iterations", str(iters),
+              "--seed", str(seed), "--report", rep, "--trace", trace], ROOT)
+    assert r.returncode == 0, r.stderr
+    with open(rep) as f:
+        assert f.read() == _read(case + ".json")
+    assert r.stdout == _read(case + ".txt")
+    with open(trace) as f:
+        assert f.read() == _read(case + ".json.trace")
