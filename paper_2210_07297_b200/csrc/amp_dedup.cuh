@@ -36,6 +36,7 @@ struct DedupParams {
   uint32_t* rep_list;   // [n] representative item of each run
   uint32_t* rep_of;     // [n] representative of every item
   uint64_t* n_rep;      // device count of runs
+  uint64_t* rep_key;    // [n] key of each run (NULL: not needed)
 };
 
 __global__ void k_dedup_keys(DedupParams p) {
@@ -67,7 +68,10 @@ __global__ void k_dedup_reps(DedupParams p) {
   for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < p.n;
        s += (uint64_t)gridDim.x * blockDim.x) {
     const bool head = s == 0 || p.skeys[s] != p.skeys[s - 1];
-    if (head) p.rep_list[p.runid[s] - 1] = p.svals[s];
+    if (head) {
+      p.rep_list[p.runid[s] - 1] = p.svals[s];
+      if (p.rep_key) p.rep_key[p.runid[s] - 1] = p.skeys[s];
+    }
     if (s + 1 == p.n) *p.n_rep = p.runid[s];
   }
 }

@@ -25,6 +25,7 @@
 #include "amp_dp_multi.cuh"
 #include "amp_dedup.cuh"
 #include "amp_thread.cuh"
+#include "amp_trie.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -165,6 +166,11 @@ struct amp_ctx {
   DevBuf dd_keys, dd_vals, dd_skeys, dd_svals, dd_flags, dd_runid, dd_rep_list, dd_rep_of;
   DevBuf dd_nrep, dd_temp, dd_counters, prog_inner_d;
   size_t dd_temp_bytes = 0;
+  // DP shared across signature prefixes (amp_trie.cuh)
+  bool trie = false;
+  std::vector<uint32_t> stage_h;  // host copy of the program stage starts
+  DevBuf v1off_d, v1g_d, dd_rep_key, tr_nid, tr_first, tr_voff, tr_flags, tr_size, tr_vals0,
+      tr_vals1, tr_bp, tr_bbase;
   uint64_t chunk = 1;
   int est_ctas = 1, sms = 148, launches = 0;
   // per-chunk kernel events {before K_place, after K_place, after K_dp,
@@ -331,6 +337,7 @@ int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
   ctx->max_prog_cells = (int)max_prog_cells;
   CK(upload(ctx->progs_d, progs.data(), progs.size()));
   CK(upload(ctx->stage_d, stage.data(), stage.size()));
+  ctx->stage_h = stage;
   CK(upload(ctx->class_prog_d, ctx->class_prog.data(), ctx->class_prog.size()));
   DevBuf d_pst;
   CK(upload(d_pst, pstart.data(), pstart.size()));
@@ -350,6 +357,8 @@ int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
   ctx->progs_h = progs;
   return AMP_OK;
 }
+
+bool is_heavy(const amp_ctx* ctx, uint64_t c);
 
 // Dynamic smem of k_dp_multi<b> (mirror of its carve-up).
 size_t multi_smem_bytes(const amp_ctx* ctx, int b) {
@@ -706,6 +715,33 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
       CK(ctx->dd_counters.ensure(2 * sizeof(unsigned long long)));
     }
   }
+  // ---- prefix-shared DP (amp_trie.cuh): class stage-1 tables, once -------
+  ctx->trie = ctx->dedup && std::getenv("AMP_NO_TRIE") == nullptr;
+  if (ctx->trie) {
+    std::vector<uint64_t> v1off(ctx->classes.size(), 0);
+    std::vector<int32_t> heavy;
+    uint64_t acc = 0;
+    for (size_t c = 0; c < ctx->classes.size(); ++c) {
+      if (!is_heavy(ctx, c)) continue;
+      const ProgDev& pg = ctx->progs_h[ctx->class_prog[c]];
+      v1off[c] = acc;
+      acc += ctx->stage_h[pg.stage_base + 1] - ctx->stage_h[pg.stage_base];
+      heavy.push_back((int32_t)c);
+    }
+    CK(upload(ctx->v1off_d, v1off.data(), v1off.size()));
+    CK(ctx->v1g_d.ensure(sizeof(double) * (acc + 1)));
+    if (!heavy.empty()) {
+      DevBuf d_heavy;
+      CK(upload(d_heavy, heavy.data(), heavy.size()));
+      k_trie_v1<<<(int)heavy.size(), 256, 0, ctx->stream>>>(
+          ctx->cls_d.as<ClassDev>(), ctx->class_prog_d.as<int32_t>(), ctx->progs_d.as<ProgDev>(),
+          ctx->stage_d.as<uint32_t>(), ctx->cells.as<uint32_t>(), ctx->prefix.as<double>(),
+          ctx->domain.as<double>(), ctx->nv_stride, L, d_heavy.as<int32_t>(), (int)heavy.size(),
+          ctx->v1off_d.as<uint64_t>(), ctx->v1g_d.as<double>());
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
+  }
   if (ctx->multi_b == 2) ctx->eval_fn = (const void*)k_dp_multi<2>;
   if (ctx->multi_b == 4) ctx->eval_fn = (const void*)k_dp_multi<4>;
   if (ctx->multi_b == 8) ctx->eval_fn = (const void*)k_dp_multi<8>;
@@ -846,6 +882,102 @@ void account(amp_ctx* ctx, uint64_t begin, uint64_t end, const uint64_t* list, i
   s.bytes = 0;
 }
 
+// Prefix-shared DP over the sorted signatures of the chunk (amp_trie.cuh):
+// node ids per depth (flag + scan), first signatures and stage table sizes
+// (+ scan), one host read of the counts, then one launch per stage and the
+// backtrack.  Writes the cuts of every representative into ep.cutsb.
+int run_trie(amp_ctx* ctx, const EvalParams& ep) {
+  uint64_t n_rep = 0;
+  CK(cudaMemcpyAsync(&n_rep, ctx->dd_nrep.p, sizeof n_rep, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (n_rep == 0) return AMP_OK;
+  const int nq = ctx->max_pp - 1, D1 = nq + 1;
+  const uint64_t S = n_rep;
+  CK(ctx->tr_nid.ensure(sizeof(uint32_t) * D1 * S));
+  CK(ctx->tr_first.ensure(sizeof(uint32_t) * D1 * S));
+  CK(ctx->tr_voff.ensure(sizeof(uint64_t) * D1 * (S + 1)));
+  CK(ctx->tr_flags.ensure(sizeof(uint32_t) * S));
+  CK(ctx->tr_size.ensure(sizeof(uint64_t) * (S + 1)));
+  TrieParams tp{};
+  tp.n_rep = ctx->dd_nrep.as<uint64_t>();
+  tp.rep_key = ctx->dd_rep_key.as<uint64_t>();
+  tp.rep_list = ctx->dd_rep_list.as<uint32_t>();
+  tp.nq = nq;
+  tp.cb = ctx->code_bits;
+  tp.L = ctx->L;
+  tp.max_pp = ctx->max_pp;
+  tp.stride = S;
+  tp.nid = ctx->tr_nid.as<uint32_t>();
+  tp.first = ctx->tr_first.as<uint32_t>();
+  tp.voff = ctx->tr_voff.as<uint64_t>();
+  tp.flags = ctx->tr_flags.as<uint32_t>();
+  tp.cls = ctx->cls_d.as<ClassDev>();
+  tp.class_prog = ctx->class_prog_d.as<int32_t>();
+  tp.progs = ctx->progs_d.as<ProgDev>();
+  tp.stage = ctx->stage_d.as<uint32_t>();
+  tp.cellrec = ctx->cellrec.as<uint2>();
+  tp.preds = ctx->preds.as<uint16_t>();
+  tp.prefix = ctx->prefix.as<double>();
+  tp.domain = ctx->domain.as<double>();
+  tp.nv_stride = ctx->nv_stride;
+  tp.n_codes = ctx->n_codes;
+  tp.qtab = ctx->qtab.as<double>();
+  tp.v1g = ctx->v1g_d.as<double>();
+  tp.v1off = ctx->v1off_d.as<uint64_t>();
+  tp.cutsb = ep.cutsb;
+  const int g = (int)std::min<uint64_t>((S + 255) / 256, (uint64_t)ctx->sms * 8);
+  const int g1 = (int)std::min<uint64_t>((S + 256) / 256, (uint64_t)ctx->sms * 8);
+  for (int d = 1; d <= nq; ++d) {
+    k_trie_flag<<<g, 256, 0, ctx->stream>>>(tp, d);
+    size_t tb = ctx->dd_temp_bytes;
+    CK(cub::DeviceScan::InclusiveSum(ctx->dd_temp.p, tb, tp.flags, tp.nid + (size_t)d * S, (int)S,
+                                     ctx->stream));
+    k_trie_first<<<g, 256, 0, ctx->stream>>>(tp, d);
+    k_trie_size<<<g1, 256, 0, ctx->stream>>>(tp, d, ctx->tr_size.as<uint64_t>());
+    tb = ctx->dd_temp_bytes;
+    CK(cub::DeviceScan::ExclusiveSum(ctx->dd_temp.p, tb, ctx->tr_size.as<uint64_t>(),
+                                     tp.voff + (size_t)d * (S + 1), (int)S + 1, ctx->stream));
+  }
+  CK(cudaGetLastError());
+  ctx->launches += 5 * nq;
+  // stage table totals (voff_d[S], d = 1..nq): stage j = d + 1
+  std::vector<uint64_t> tot(D1, 0);
+  for (int d = 1; d <= nq; ++d)
+    CK(cudaMemcpyAsync(&tot[d], tp.voff + (size_t)d * (S + 1) + S, sizeof(uint64_t),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  std::vector<uint64_t> bbase(ctx->max_pp + 1, 0);
+  uint64_t acc = 0, mx = 1;
+  for (int j = 2; j <= ctx->max_pp; ++j) {
+    bbase[j] = acc;
+    acc += tot[j - 1];
+    mx = std::max<uint64_t>(mx, tot[j - 1]);
+  }
+  CK(ctx->tr_vals0.ensure(sizeof(double) * mx));
+  CK(ctx->tr_vals1.ensure(sizeof(double) * mx));
+  CK(ctx->tr_bp.ensure(acc + 16));
+  CK(upload(ctx->tr_bbase, bbase.data(), bbase.size()));
+  tp.vals[0] = ctx->tr_vals0.as<double>();
+  tp.vals[1] = ctx->tr_vals1.as<double>();
+  tp.bp = ctx->tr_bp.as<uint8_t>();
+  tp.bbase = ctx->tr_bbase.as<uint64_t>();
+  unsigned long long* exec = ep.exec_counters ? ep.exec_counters + 1 : nullptr;
+  for (int j = 2; j <= ctx->max_pp; ++j) {
+    const uint64_t total = tot[j - 1];
+    if (!total) continue;
+    const int gs = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)ctx->sms * 16);
+    k_trie_stage<<<gs, 256, 0, ctx->stream>>>(tp, j, total, exec);
+    ctx->launches += 1;
+  }
+  k_trie_back<<<g, 256, 0, ctx->stream>>>(tp);
+  CK(cudaGetLastError());
+  ctx->launches += 1;
+  if (ep.exec_counters)  // DP instances solved: one per signature
+    CK(cudaMemcpyAsync(ep.exec_counters, ctx->dd_nrep.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+  return AMP_OK;
+}
+
 // Launch K1+K2 over either a segment list or an explicit index list.
 // Evaluate n_work items (segment list or explicit index list) as a pipeline
 // of chunks: K_place -> K_dp -> K_est per chunk (amp_pipeline.cuh).  CTA
@@ -959,13 +1091,17 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     CK(ctx->dd_runid.ensure(sizeof(uint32_t) * C));
     CK(ctx->dd_rep_list.ensure(sizeof(uint32_t) * C));
     CK(ctx->dd_rep_of.ensure(sizeof(uint32_t) * C));
+    if (ctx->trie) CK(ctx->dd_rep_key.ensure(sizeof(uint64_t) * C));
     size_t t1 = 0, t2 = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, t1, (const uint64_t*)nullptr, (uint64_t*)nullptr,
                                        (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)C, 0,
                                        ctx->key_bits, ctx->stream));
     CK(cub::DeviceScan::InclusiveSum(nullptr, t2, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                      (int)C, ctx->stream));
-    ctx->dd_temp_bytes = std::max(t1, t2);
+    size_t t3 = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, t3, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                     (int)C + 1, ctx->stream));
+    ctx->dd_temp_bytes = std::max(std::max(t1, t2), t3);
     CK(ctx->dd_temp.ensure(ctx->dd_temp_bytes + 16));
     CK(cudaMemsetAsync(ctx->dd_counters.p, 0, 2 * sizeof(unsigned long long), ctx->stream));
     ep.exec_counters = ctx->dd_counters.as<unsigned long long>();
@@ -1031,6 +1167,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     ep.rep_list = nullptr;
     ep.rep_of = nullptr;
     ep.n_rep = nullptr;
+    bool skip_dp = false;
     if (ctx->dedup && !d_given_cuts && ep.n_dp > 0) {
       // ---- memoisation: sort signatures, one DP per distinct key --------
       DedupParams dp{};
@@ -1049,6 +1186,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
       dp.rep_list = ctx->dd_rep_list.as<uint32_t>();
       dp.rep_of = ctx->dd_rep_of.as<uint32_t>();
       dp.n_rep = ctx->dd_nrep.as<uint64_t>();
+      dp.rep_key = ctx->trie ? ctx->dd_rep_key.as<uint64_t>() : nullptr;
       const int g = (int)std::min<uint64_t>((ep.n_dp + 255) / 256, (uint64_t)ctx->sms * 8);
       k_dedup_keys<<<g, 256, 0, ctx->stream>>>(dp);
       size_t tb = ctx->dd_temp_bytes;
@@ -1066,9 +1204,14 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
       ep.rep_list = dp.rep_list;
       ep.rep_of = dp.rep_of;
       ep.n_rep = dp.n_rep;
+      if (ctx->trie) {
+        const int rc = run_trie(ctx, ep);
+        if (rc != AMP_OK) return rc;
+        skip_dp = true;  // K_dp's work is done (K_est reads the cuts via rep_of)
+      }
     }
     ctx->stats.dp_items += ep.n_dp;
-    if (ep.n_dp > 0) {
+    if (ep.n_dp > 0 && !skip_dp) {
       ctx->stats.dp_launches += 1;
       void* args[] = {&ep};
       CK(cudaLaunchKernel(ctx->eval_fn, dim3(ctx->n_ctas), dim3(ctx->eval_threads), args,
