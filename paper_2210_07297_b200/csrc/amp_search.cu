@@ -169,8 +169,8 @@ struct amp_ctx {
   // DP shared across signature prefixes (amp_trie.cuh)
   bool trie = false;
   std::vector<uint32_t> stage_h;  // host copy of the program stage starts
-  DevBuf v1off_d, v1g_d, dd_rep_key, tr_nid, tr_first, tr_voff, tr_flags, tr_size, tr_vals0,
-      tr_vals1, tr_bp, tr_bbase;
+  DevBuf v1off_d, v1g_d, dd_rep_key, tr_nid, tr_first, tr_parent, tr_flags, tr_range, tr_vals0,
+      tr_vals1, tr_bp, tr_vbase, tr_bbase, tr_stcls, tr_stitem, tr_stn;
   uint64_t chunk = 1;
   int est_ctas = 1, sms = 148, launches = 0;
   // per-chunk kernel events {before K_place, after K_place, after K_dp,
@@ -891,13 +891,14 @@ int run_trie(amp_ctx* ctx, const EvalParams& ep) {
   CK(cudaMemcpyAsync(&n_rep, ctx->dd_nrep.p, sizeof n_rep, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   if (n_rep == 0) return AMP_OK;
-  const int nq = ctx->max_pp - 1, D1 = nq + 1;
+  const int nq = ctx->max_pp - 1, D1 = nq + 1, NC = (int)ctx->classes.size();
   const uint64_t S = n_rep;
   CK(ctx->tr_nid.ensure(sizeof(uint32_t) * D1 * S));
   CK(ctx->tr_first.ensure(sizeof(uint32_t) * D1 * S));
-  CK(ctx->tr_voff.ensure(sizeof(uint64_t) * D1 * (S + 1)));
+  CK(ctx->tr_parent.ensure(sizeof(uint32_t) * D1 * S));
   CK(ctx->tr_flags.ensure(sizeof(uint32_t) * S));
-  CK(ctx->tr_size.ensure(sizeof(uint64_t) * (S + 1)));
+  CK(ctx->tr_range.ensure(sizeof(uint32_t) * D1 * NC * 2));
+  CK(cudaMemsetAsync(ctx->tr_range.p, 0, sizeof(uint32_t) * D1 * NC * 2, ctx->stream));
   TrieParams tp{};
   tp.n_rep = ctx->dd_nrep.as<uint64_t>();
   tp.rep_key = ctx->dd_rep_key.as<uint64_t>();
@@ -906,11 +907,13 @@ int run_trie(amp_ctx* ctx, const EvalParams& ep) {
   tp.cb = ctx->code_bits;
   tp.L = ctx->L;
   tp.max_pp = ctx->max_pp;
+  tp.n_cls = NC;
   tp.stride = S;
   tp.nid = ctx->tr_nid.as<uint32_t>();
   tp.first = ctx->tr_first.as<uint32_t>();
-  tp.voff = ctx->tr_voff.as<uint64_t>();
+  tp.parent = ctx->tr_parent.as<uint32_t>();
   tp.flags = ctx->tr_flags.as<uint32_t>();
+  tp.range = ctx->tr_range.as<uint32_t>();
   tp.cls = ctx->cls_d.as<ClassDev>();
   tp.class_prog = ctx->class_prog_d.as<int32_t>();
   tp.progs = ctx->progs_d.as<ProgDev>();
@@ -926,47 +929,68 @@ int run_trie(amp_ctx* ctx, const EvalParams& ep) {
   tp.v1off = ctx->v1off_d.as<uint64_t>();
   tp.cutsb = ep.cutsb;
   const int g = (int)std::min<uint64_t>((S + 255) / 256, (uint64_t)ctx->sms * 8);
-  const int g1 = (int)std::min<uint64_t>((S + 256) / 256, (uint64_t)ctx->sms * 8);
   for (int d = 1; d <= nq; ++d) {
     k_trie_flag<<<g, 256, 0, ctx->stream>>>(tp, d);
     size_t tb = ctx->dd_temp_bytes;
     CK(cub::DeviceScan::InclusiveSum(ctx->dd_temp.p, tb, tp.flags, tp.nid + (size_t)d * S, (int)S,
                                      ctx->stream));
-    k_trie_first<<<g, 256, 0, ctx->stream>>>(tp, d);
-    k_trie_size<<<g1, 256, 0, ctx->stream>>>(tp, d, ctx->tr_size.as<uint64_t>());
-    tb = ctx->dd_temp_bytes;
-    CK(cub::DeviceScan::ExclusiveSum(ctx->dd_temp.p, tb, ctx->tr_size.as<uint64_t>(),
-                                     tp.voff + (size_t)d * (S + 1), (int)S + 1, ctx->stream));
+    k_trie_nodes<<<g, 256, 0, ctx->stream>>>(tp, d);
   }
   CK(cudaGetLastError());
-  ctx->launches += 5 * nq;
-  // stage table totals (voff_d[S], d = 1..nq): stage j = d + 1
-  std::vector<uint64_t> tot(D1, 0);
-  for (int d = 1; d <= nq; ++d)
-    CK(cudaMemcpyAsync(&tot[d], tp.voff + (size_t)d * (S + 1) + S, sizeof(uint64_t),
-                       cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->launches += 3 * nq;
+  // node ranges of every class at every depth -> table bases, stage lists
+  std::vector<uint32_t> range((size_t)D1 * NC * 2);
+  CK(cudaMemcpyAsync(range.data(), ctx->tr_range.p, sizeof(uint32_t) * range.size(),
+                     cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  std::vector<uint64_t> bbase(ctx->max_pp + 1, 0);
-  uint64_t acc = 0, mx = 1;
+  const int P1 = ctx->max_pp + 1;
+  std::vector<uint64_t> vbase((size_t)D1 * NC, 0), bbase((size_t)D1 * NC, 0);
+  std::vector<int32_t> stcls((size_t)P1 * NC, 0), stn(P1, 0);
+  std::vector<uint64_t> stitem((size_t)P1 * (NC + 1), 0), total(P1, 0);
+  uint64_t bacc = 0, vmax = 1;
   for (int j = 2; j <= ctx->max_pp; ++j) {
-    bbase[j] = acc;
-    acc += tot[j - 1];
-    mx = std::max<uint64_t>(mx, tot[j - 1]);
+    const int d = j - 1;
+    uint64_t vacc = 0;
+    for (int c = 0; c < NC; ++c) {
+      const uint32_t nb = range[((size_t)d * NC + c) * 2], ne = range[((size_t)d * NC + c) * 2 + 1];
+      if (ne <= nb || !is_heavy(ctx, c) || ctx->classes[c].pp < j) continue;
+      const ProgDev& pg = ctx->progs_h[ctx->class_prog[c]];
+      const uint64_t cells = ctx->stage_h[pg.stage_base + j] - ctx->stage_h[pg.stage_base + j - 1];
+      const uint64_t sz = cells * (ne - nb);
+      vbase[(size_t)d * NC + c] = vacc;
+      bbase[(size_t)d * NC + c] = bacc;
+      stcls[(size_t)j * NC + stn[j]] = c;
+      stitem[(size_t)j * (NC + 1) + stn[j]] = vacc;
+      ++stn[j];
+      vacc += sz;
+      bacc += sz;
+    }
+    stitem[(size_t)j * (NC + 1) + stn[j]] = vacc;
+    total[j] = vacc;
+    vmax = std::max<uint64_t>(vmax, vacc);
   }
-  CK(ctx->tr_vals0.ensure(sizeof(double) * mx));
-  CK(ctx->tr_vals1.ensure(sizeof(double) * mx));
-  CK(ctx->tr_bp.ensure(acc + 16));
+  if (NC > kTrieMaxCls) return fail(ctx, AMP_E_UNSUPPORTED, "too many classes for the trie DP");
+  CK(upload(ctx->tr_vbase, vbase.data(), vbase.size()));
   CK(upload(ctx->tr_bbase, bbase.data(), bbase.size()));
+  CK(upload(ctx->tr_stcls, stcls.data(), stcls.size()));
+  CK(upload(ctx->tr_stitem, stitem.data(), stitem.size()));
+  CK(upload(ctx->tr_stn, stn.data(), stn.size()));
+  CK(ctx->tr_vals0.ensure(sizeof(double) * vmax));
+  CK(ctx->tr_vals1.ensure(sizeof(double) * vmax));
+  CK(ctx->tr_bp.ensure(bacc + 16));
+  tp.vbase = ctx->tr_vbase.as<uint64_t>();
+  tp.bbase = ctx->tr_bbase.as<uint64_t>();
+  tp.st_cls = ctx->tr_stcls.as<int32_t>();
+  tp.st_item = ctx->tr_stitem.as<uint64_t>();
+  tp.st_n = ctx->tr_stn.as<int32_t>();
   tp.vals[0] = ctx->tr_vals0.as<double>();
   tp.vals[1] = ctx->tr_vals1.as<double>();
   tp.bp = ctx->tr_bp.as<uint8_t>();
-  tp.bbase = ctx->tr_bbase.as<uint64_t>();
   unsigned long long* exec = ep.exec_counters ? ep.exec_counters + 1 : nullptr;
   for (int j = 2; j <= ctx->max_pp; ++j) {
-    const uint64_t total = tot[j - 1];
-    if (!total) continue;
-    const int gs = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)ctx->sms * 16);
-    k_trie_stage<<<gs, 256, 0, ctx->stream>>>(tp, j, total, exec);
+    if (!total[j]) continue;
+    const int gs = (int)std::min<uint64_t>((total[j] + 255) / 256, (uint64_t)ctx->sms * 16);
+    k_trie_stage<<<gs, 256, 0, ctx->stream>>>(tp, j, total[j], exec);
     ctx->launches += 1;
   }
   k_trie_back<<<g, 256, 0, ctx->stream>>>(tp);

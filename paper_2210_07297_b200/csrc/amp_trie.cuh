@@ -1,32 +1,37 @@
 // amp_trie.cuh — the layer-partition DP shared across signature prefixes.
 //
 // Stage j of the DP (pipeline_dp.cpp:114-131) reads stage j-1 and the edge
-// costs of boundary j-2 only, so the values and argmins of stage j are a
+// costs of boundary j-2 only.  So the values and argmins of stage j are a
 // function of the class and of the boundary codes c_0 .. c_{j-2}: every
 // signature (class, c_0 .. c_{k-2}) with the same first j-1 codes has the
 // same stage-j table.  After the signature sort (amp_dedup.cuh) the
 // representatives are in key order, i.e. lexicographic in (class, c_0,
-// c_1, ...), so the signatures sharing a prefix of length d are a run: the
-// runs are the nodes of a trie, and stage j is solved once per node of
-// depth j-1 instead of once per signature.  The operations per cell and cut
-// are those of the per-candidate kernels (same operands, same order, same
-// strict '<'), so every cut is bit-identical (tested against
+// c_1, ...).  The signatures sharing a prefix of length d therefore form a
+// run; the runs are the nodes of a trie, and stage j is solved once per node
+// of depth j-1 instead of once per signature.  The operations per cell and
+// cut are those of the per-candidate kernels (same operands, same order,
+// same strict '<'), so every cut is bit-identical (tested against
 // AMP_FLAG_NO_DEDUP).
 //
-//   K_flag(d)   head flag of each depth-d run        -> scan -> nid_d (1-based)
-//   K_first     first representative of every node, per depth
-//   K_size(d)   |N_{d+1}| of each depth-d node (0 when the class has pp <= d)
-//               -> exclusive scan -> voff_d (values / backpointer offsets)
-//   K_stage(j)  one thread per (node of depth j-1, cell of N_j): the cut loop
-//               over the parent node's stage-(j-1) values (stage 1 from the
-//               class table V1g); writes values (ping-pong) + u8 argmins
-//   K_back      one thread per signature: walk its trie path, write its cuts
+// Layout: the nodes of one depth are class-contiguous.  The stage-j table of
+// class c is cell-major over its K nodes — value / argmin of (cell x, node
+// n) at base_c + x*K + (n - nb_c) — so the threads of a warp share a cell
+// (program record, predecessor list, prefix, domain: broadcast loads, no
+// divergence in the cut loop) and touch consecutive nodes (coalesced).
+//
+//   K_flag(d)    head flags of the depth-d runs        -> scan -> nid_d (1-based)
+//   K_nodes(d)   first signature and parent of every node, class node ranges
+//   (host)       one read of the ranges; table bases, per-stage item lists
+//   K_stage(j)   one thread per (class, cell of N_j, node of depth j-1)
+//   K_back       one thread per signature: walk its trie path, write its cuts
 #pragma once
 
 #include "amp_common.cuh"
 #include "amp_dp_sparse.cuh"
 
 namespace amp {
+
+constexpr int kTrieMaxCls = 1024;  // classes per stage list held in smem
 
 struct TrieParams {
   // signatures (run heads of the sorted keys)
@@ -35,11 +40,19 @@ struct TrieParams {
   const uint32_t* rep_list;   // [n_rep] chunk item of each signature
   int32_t nq, cb;             // codes per key, bits per code
   int32_t L, max_pp;
+  int32_t n_cls, pad0;
   uint64_t stride;            // n_rep (row stride of the per-depth arrays)
   uint32_t* nid;              // [nq + 1][stride]  node id (1-based) at depth d
   uint32_t* first;            // [nq + 1][stride]  first signature of each node
-  uint64_t* voff;             // [nq + 1][stride + 1] offsets of stage d+1 tables
+  uint32_t* parent;           // [nq + 1][stride]  node of depth d-1 it extends
   uint32_t* flags;            // [stride] scratch
+  uint32_t* range;            // [nq + 1][n_cls][2]  node range [nb, ne) of each class
+  // host-computed tables (after one read of `range`)
+  const uint64_t* vbase;      // [nq + 1][n_cls]  value-table base of (depth, class)
+  const uint64_t* bbase;      // [nq + 1][n_cls]  argmin-table base of (depth, class)
+  const int32_t* st_cls;      // [max_pp + 1][n_cls]  classes of stage j's item list
+  const uint64_t* st_item;    // [max_pp + 1][n_cls + 1]  exclusive item bases
+  const int32_t* st_n;        // [max_pp + 1]  classes in stage j's list
   // problem tables
   const ClassDev* cls;
   const int32_t* class_prog;
@@ -55,8 +68,7 @@ struct TrieParams {
   const uint64_t* v1off;      // [n_cls]
   // stage storage
   double* vals[2];            // ping-pong by stage parity
-  uint8_t* bp;                // all stages: bp[bbase_j + voff_{j-1}[node] + x]
-  const uint64_t* bbase;      // [max_pp + 1] host-computed stage bases
+  uint8_t* bp;                // argmins of all stages
   uint8_t* cutsb;             // [n_chunk][max_pp + 1]
 };
 
@@ -76,67 +88,63 @@ __global__ void k_trie_flag(TrieParams p, int d) {
     p.flags[r] = (r == 0 || (p.rep_key[r] >> sh) != (p.rep_key[r - 1] >> sh)) ? 1u : 0u;
 }
 
-// first signature of every depth-d node
-__global__ void k_trie_first(TrieParams p, int d) {
+// first signature and parent of every depth-d node; node range of each
+// class (the failed / pp <= 2 run, key ~0, belongs to no class)
+__global__ void k_trie_nodes(TrieParams p, int d) {
   const uint64_t n = *p.n_rep;
   const uint32_t* nid = p.nid + (size_t)d * p.stride;
   uint32_t* first = p.first + (size_t)d * p.stride;
+  uint32_t* parent = p.parent + (size_t)d * p.stride;
+  uint32_t* range = p.range + (size_t)d * p.n_cls * 2;
   for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
-       r += (uint64_t)gridDim.x * blockDim.x)
-    if (r == 0 || nid[r] != nid[r - 1]) first[nid[r] - 1] = (uint32_t)r;
-}
-
-// stage-(d+1) table size of every depth-d node; 0 beyond the depth's node
-// count, for classes with pp <= d and for the failed / pp <= 2 run
-__global__ void k_trie_size(TrieParams p, int d, uint64_t* size) {
-  const uint64_t n = *p.n_rep;
-  const uint32_t* nid = p.nid + (size_t)d * p.stride;
-  const uint32_t* first = p.first + (size_t)d * p.stride;
-  const uint32_t n_nodes = n ? nid[n - 1] : 0;
-  const int j = d + 1;  // the stage these nodes solve
-  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= p.stride;
-       x += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t s = 0;
-    const uint64_t key = x < n_nodes ? p.rep_key[first[x]] : ~0ull;
-    const int c = key == ~0ull ? 0 : key_cls(p, key);
-    if (key != ~0ull && p.cls[c].pp >= j) {
-      const ProgDev pg = p.progs[p.class_prog[c]];
-      const uint32_t* ss = p.stage + pg.stage_base;
-      s = ss[j] - ss[j - 1];
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t node = nid[r] - 1;
+    if (r == 0 || nid[r] != nid[r - 1]) {  // node head
+      first[node] = (uint32_t)r;
+      parent[node] = d >= 2 ? p.nid[(size_t)(d - 1) * p.stride + r] - 1 : 0;
     }
-    size[x] = s;
+    const uint64_t key = p.rep_key[r];
+    if (key == ~0ull) continue;
+    const int c = key_cls(p, key);
+    // the class's first signature opens its node range, its last closes it
+    if (r == 0 || key_cls(p, p.rep_key[r - 1]) != c) range[2 * c] = node;
+    if (r + 1 == n || p.rep_key[r + 1] == ~0ull || key_cls(p, p.rep_key[r + 1]) != c)
+      range[2 * c + 1] = node + 1;
   }
 }
 
-// Stage j: one thread per (node of depth j-1, cell of N_j).
+// Stage j: one thread per (class, cell x of N_j, node n of depth j-1), node
+// fastest.
 __global__ void __launch_bounds__(256) k_trie_stage(TrieParams p, int j, uint64_t total,
                                                     unsigned long long* exec) {
+  __shared__ uint64_t ibase[kTrieMaxCls + 1];
+  __shared__ int32_t icls[kTrieMaxCls];
   __shared__ unsigned long long cnt;
+  const int nc = p.st_n[j];
+  for (int x = threadIdx.x; x <= nc; x += blockDim.x) {
+    ibase[x] = p.st_item[(size_t)j * (p.n_cls + 1) + x];
+    if (x < nc) icls[x] = p.st_cls[(size_t)j * p.n_cls + x];
+  }
   if (threadIdx.x == 0) cnt = 0;
   __syncthreads();
   unsigned long long mine = 0;
   const int d = j - 1, L = p.L, LP = L + 1;
-  const uint64_t n = *p.n_rep;
-  const uint32_t* nid = p.nid + (size_t)d * p.stride;
-  const uint32_t* first = p.first + (size_t)d * p.stride;
-  const uint64_t* voff = p.voff + (size_t)d * (p.stride + 1);
-  const uint32_t n_nodes = n ? nid[n - 1] : 0;
   const double* Vprev = p.vals[(j - 1) & 1];
   double* Vcur = p.vals[j & 1];
-  uint8_t* bpj = p.bp + p.bbase[j];
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (uint64_t)gridDim.x * blockDim.x) {
-    // node: last x with voff[x] <= t (voff is an exclusive scan of sizes)
-    uint32_t lo = 0, hi = n_nodes - 1;
+    int lo = 0, hi = nc - 1;  // class slot: last with ibase <= t
     while (lo < hi) {
-      const uint32_t mid = (lo + hi + 1) >> 1;
-      if (voff[mid] <= t) lo = mid;
+      const int mid = (lo + hi + 1) >> 1;
+      if (ibase[mid] <= t) lo = mid;
       else hi = mid - 1;
     }
-    const uint32_t node = lo;
-    const uint32_t x = (uint32_t)(t - voff[node]);
-    const uint64_t key = p.rep_key[first[node]];
-    const int c = key_cls(p, key);
+    const int c = icls[lo];
+    const uint32_t* rg = p.range + ((size_t)d * p.n_cls + c) * 2;
+    const uint32_t nb = rg[0], K = rg[1] - rg[0];
+    const uint64_t off = t - ibase[lo];
+    const uint32_t x = (uint32_t)(off / K), nl = (uint32_t)(off % K);
+    const uint32_t node = nb + nl;
     const ClassDev cl = p.cls[c];
     const ProgDev pg = p.progs[p.class_prog[c]];
     const uint32_t* ss = p.stage + pg.stage_base;
@@ -147,29 +155,34 @@ __global__ void __launch_bounds__(256) k_trie_stage(TrieParams p, int j, uint64_
     const double dm = p.domain[(size_t)cl.pair * p.nv_stride + m];
     const double Pi = Pf[i];
     const double g1 = (double)(cl.gas - 1);
+    const uint64_t key = p.rep_key[p.first[(size_t)d * p.stride + node]];
     const double* E = p.qtab + ((size_t)c * p.n_codes + key_code(p, key, j - 2)) * L;
     // the parent's stage-(j-1) values: the class's stage-1 table, or the
-    // depth-(j-2) node this node extends
+    // depth-(j-2) node this node extends (cell-major table of its class)
     const double* Vp;
+    uint32_t Kp = 1;
     if (j == 2) {
       Vp = p.v1g + p.v1off[c];
     } else {
-      const uint32_t pn = p.nid[(size_t)(d - 1) * p.stride + first[node]] - 1;
-      Vp = Vprev + p.voff[(size_t)(d - 1) * (p.stride + 1) + pn];
+      const uint32_t* rgp = p.range + ((size_t)(d - 1) * p.n_cls + c) * 2;
+      Kp = rgp[1] - rgp[0];
+      const uint32_t pn = p.parent[(size_t)d * p.stride + node] - rgp[0];
+      Vp = Vprev + p.vbase[(size_t)(d - 1) * p.n_cls + c] + pn;
     }
     double best = CUDART_INF;
     int bc = -1;
     for (int cut = j - 1; cut < i; ++cut) {  // pipeline_dp.cpp:114-131
       const double t2 = Pi - Pf[cut];
       const double term = t2 > dm ? g1 * (t2 - dm) : 0.0;
-      const double g = ((Vp[q[cut - (j - 1)]] + term) + t2) + E[cut];
+      const double g = ((Vp[(size_t)q[cut - (j - 1)] * Kp] + term) + t2) + E[cut];
       if (g < best) {
         best = g;
         bc = cut;
       }
     }
-    Vcur[voff[node] + x] = best;
-    bpj[voff[node] + x] = (uint8_t)bc;
+    const uint64_t o = (uint64_t)x * K + nl;
+    Vcur[p.vbase[(size_t)d * p.n_cls + c] + o] = best;
+    p.bp[p.bbase[(size_t)d * p.n_cls + c] + o] = (uint8_t)bc;
     mine += (unsigned long long)(i - (j - 1));
   }
   if (exec) {  // executed inner iterations (roofline accounting)
@@ -198,9 +211,10 @@ __global__ void k_trie_back(TrieParams p) {
     uint32_t x = ss[k - 1];  // N_k = {(L, 0)}
     for (int j = k; j >= 2; --j) {
       const int d = j - 1;
+      const uint32_t* rg = p.range + ((size_t)d * p.n_cls + c) * 2;
       const uint32_t node = p.nid[(size_t)d * p.stride + r] - 1;
-      const uint64_t off = p.voff[(size_t)d * (p.stride + 1) + node];
-      const int cut = p.bp[p.bbase[j] + off + (x - ss[j - 1])];
+      const uint64_t o = (uint64_t)(x - ss[j - 1]) * (rg[1] - rg[0]) + (node - rg[0]);
+      const int cut = p.bp[p.bbase[(size_t)d * p.n_cls + c] + o];
       co[j - 1] = (uint8_t)cut;
       const uint2 rec = p.cellrec[pg.cell_base + x];
       x = ss[j - 2] + p.preds[pg.pred_base + rec.y + (cut - (j - 1))];
