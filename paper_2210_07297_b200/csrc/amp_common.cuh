@@ -144,6 +144,10 @@ struct EvalParams {
   const double* prog_inner;   // [n_progs] unpadded inner iterations per program
   unsigned long long* exec_counters;  // [2]: DP instances solved, inner iterations executed
   const int32_t* given_place;  // [n_work][D] caller placements (rank -> device) or NULL
+  // thread-mode traffic trims (amp_thread.cuh)
+  uint64_t* placep;           // [n_chunk] placement as 16 x 4-bit nibbles, or NULL
+  int32_t need_place_rows;    // K_place must also write placeb (warp K_est reads it)
+  int32_t need_bwq;           // K_place must also write bwqb (kernels without edge tables)
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

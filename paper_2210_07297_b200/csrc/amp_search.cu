@@ -154,7 +154,7 @@ struct amp_ctx {
   std::vector<double> prog_inner_raw;  // unpadded inner iterations per program
   size_t v_stride = 0;
   DevBuf progs_d, stage_d, class_prog_d, cells, cellpred, preds, vbuf;
-  DevBuf c_work, c_place, c_bwq, c_cuts, c_bwc;  // pipeline chunk buffers
+  DevBuf c_work, c_place, c_bwq, c_cuts, c_bwc, c_placep;  // pipeline chunk buffers
   // bandwidth codes (ranks of the distinct link bandwidths) and per-class
   // edge-cost tables; n_codes = 0 when disabled
   int n_codes = 0;
@@ -1156,6 +1156,17 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   // coded bandwidths; AMP_NO_THREAD=1 keeps the warp kernels
   const bool thread_mode = ctx->D <= kThreadMaxD && ctx->n_codes > 0 && ctx->max_pp <= kThreadMaxD &&
                            std::getenv("AMP_NO_THREAD") == nullptr;
+  // thread-mode traffic trims: packed placements (8 B instead of |D| ints)
+  // when K_est_t reads them; bandwidth values only for kernels without the
+  // edge tables
+  const bool est_thread = thread_mode && !want_sim && kk <= 32;
+  ep.need_place_rows = !est_thread;
+  ep.need_bwq = !(thread_mode && ctx->multi_b);
+  ep.placep = nullptr;
+  if (thread_mode) {
+    CK(ctx->c_placep.ensure(sizeof(uint64_t) * C));
+    ep.placep = ctx->c_placep.as<uint64_t>();
+  }
   const int n_chunks = (int)((n_work + C - 1) / C);
   while ((int)ctx->kev.size() < 4 * n_chunks) {
     cudaEvent_t e;
@@ -1244,7 +1255,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
       ctx->launches += 1;
     }
     CK(cudaEventRecord(ev[2], ctx->stream));
-    if (thread_mode && !want_sim && kk <= 32)
+    if (est_thread)
       k_est_t<<<ctx->est_ctas, kEstTWarps * 32, 0, ctx->stream>>>(ep);
     else
       k_est<<<ctx->est_ctas, kEstWarps * 32, est_smem, ctx->stream>>>(ep);

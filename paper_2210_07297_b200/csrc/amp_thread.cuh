@@ -89,8 +89,11 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
           r = splitmix64(r);
         }
       }
-      int32_t* prow = p.placeb + u * D;
-      for (int x = 0; x < D; ++x) prow[x] = nib(perm, x);
+      if (p.placep) p.placep[u] = perm;
+      if (p.need_place_rows) {
+        int32_t* prow = p.placeb + u * D;
+        for (int x = 0; x < D; ++x) prow[x] = nib(perm, x);
+      }
       // ---- stage-boundary bandwidths: min over all replicas and shards
       //      (cost_model.cpp:164-174), as codes; the first invalid boundary
       //      fails like p2p_time in the DP's edge function ---------------
@@ -106,7 +109,7 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
           }
         const double b = p.bwval[cm];
         p.bwcb[u * maxpp + q] = (uint8_t)cm;
-        p.bwqb[u * maxpp + q] = b;
+        if (p.need_bwq) p.bwqb[u * maxpp + q] = b;
         if (first_bad < 0 && !(b > 0)) {
           first_bad = q;
           bad_val = b;
@@ -184,10 +187,14 @@ __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
       int fc = w.fail_code;
       double fval = w.fail_value;
       double pipeline = CUDART_NAN, dpsync = CUDART_NAN;
-      const int32_t* PL = p.placeb + u * D;
       uint64_t perm = 0;
       if (fc == 0) {
-        for (int x = 0; x < D; ++x) perm |= (uint64_t)PL[x] << (4 * x);
+        if (p.placep) {
+          perm = p.placep[u];
+        } else {
+          const int32_t* PL = p.placeb + u * D;
+          for (int x = 0; x < D; ++x) perm |= (uint64_t)PL[x] << (4 * x);
+        }
         // ---- cuts: K_dp (memoised: its signature's representative), or
         //      the k <= 2 DP here (light_cut2's operations, sequential) ---
         if (pp >= 3 || p.cuts_given) {

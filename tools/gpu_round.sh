@@ -9,7 +9,7 @@ python bench.py > $O/bench.log 2>&1; echo bench=$?
 python bench.py --impl reference > $O/bench_ref.log 2>&1; echo ref=$?
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-dense --no-e2e --no-wall-time > $O/ncu_launch.log 2>&1; echo launches=$?
-ncu --set full --clock-control none --import-source on -k regex:k_dp_multi -s 2 -c 1 -o $O/kdp_full -f \
+ncu --set full --clock-control none --import-source on -k regex:k_trie_stage -s 25 -c 1 -o $O/kdp_full -f \
     python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-dense --no-e2e --no-wall-time > $O/ncu_full.log 2>&1; echo full=$?
 ncu -i $O/kdp_full.ncu-rep --page raw --csv > $O/kdp_full_raw.csv 2>/dev/null
 ncu -i $O/kdp_full.ncu-rep --page details --csv > $O/kdp_full_details.csv 2>/dev/null

@@ -19,6 +19,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag = sys.argv[1]
 src = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out")
+mangled = sys.argv[3] if len(sys.argv) > 3 else "_ZN3amp12k_trie_stageENS_10TrieParamsEimPy"
+kname_short = sys.argv[4] if len(sys.argv) > 4 else "k_trie_stage"
 out = os.path.join(ROOT, "profiles")
 
 
@@ -66,16 +68,16 @@ kname = det[0]["Kernel Name"] if det else "?"
 lines_txt = ""
 try:
     lib = os.path.join(ROOT, "paper_2210_07297_b200", "libamp_search.so")
-    mangled = "_ZN3amp10k_dp_multiILi4EEEvNS_10EvalParamsE"
     lines_txt = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"),
                                 os.path.join(src, "kdp_full_sass.csv"), lib, mangled, "25"],
                                capture_output=True, text=True).stdout
 except Exception as e:  # noqa: BLE001
     lines_txt = f"(ncu_lines failed: {e})"
-with open(os.path.join(out, f"{tag}_k_dp_multi_ncu.txt"), "w") as f:
-    f.write("# ncu --set full --clock-control none --import-source on -k regex:k_dp_multi -s 2 -c 1 "
-            "python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-dense --no-e2e\n")
-    f.write(f"# kernel: {kname} (3rd K_dp launch of the bench workload: a heavy chunk)\n\n## details\n")
+with open(os.path.join(out, f"{tag}_{kname_short}_ncu.txt"), "w") as f:
+    f.write(f"# ncu --set full --clock-control none --import-source on -k regex:{kname_short} "
+            "(tools/gpu_round.sh) python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-dense "
+            "--no-e2e --no-wall-time\n")
+    f.write(f"# kernel: {kname}\n\n## details\n")
     for r in det:
         if r["Metric Name"] in want_details:
             f.write(f'{r["Section Name"]} | {r["Metric Name"]} | {r["Metric Unit"]} | '
