@@ -32,11 +32,11 @@ __device__ __forceinline__ uint32_t mod32(uint32_t x, uint32_t d, uint32_t m) {
   uint32_t r = x - __umulhi(x, m) * d;
   return r >= d ? r - d : r;
 }
-__device__ __forceinline__ uint32_t mod64_small(uint64_t r, uint32_t d) {
-  const uint32_t m = (uint32_t)(0x100000000ull / d);
-  const uint32_t t32 = (uint32_t)(0x100000000ull % d);
-  const uint32_t a = mod32((uint32_t)(r >> 32), d, m), b = mod32((uint32_t)r, d, m);
-  return mod32(a * t32 + b, d, m);  // < d*d + d <= 1056
+// (m, t32) = (floor(2^32 / d), 2^32 mod d) come from a per-CTA table: a
+// 64-bit division by a runtime divisor is a ~100-instruction routine.
+__device__ __forceinline__ uint32_t mod64_small(uint64_t r, uint32_t d, uint2 mt) {
+  const uint32_t a = mod32((uint32_t)(r >> 32), d, mt.x), b = mod32((uint32_t)r, d, mt.x);
+  return mod32(a * mt.y + b, d, mt.x);  // < d*d + d <= 1056
 }
 
 // ---------------------------------------------------------------------------
@@ -45,8 +45,12 @@ __device__ __forceinline__ uint32_t mod64_small(uint64_t r, uint32_t d) {
 __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
   __shared__ uint8_t codeS[kThreadMaxD * kThreadMaxD];
   __shared__ uint64_t base_perm;
+  __shared__ uint2 magic[kThreadMaxD + 1];  // d -> (floor(2^32/d), 2^32 mod d)
   const int D = p.D;
   for (int x = threadIdx.x; x < D * D; x += blockDim.x) codeS[x] = p.bwcode[x];
+  if (threadIdx.x >= 2 && threadIdx.x <= kThreadMaxD)
+    magic[threadIdx.x] = make_uint2((uint32_t)(0x100000000ull / threadIdx.x),
+                                    (uint32_t)(0x100000000ull % threadIdx.x));
   if (threadIdx.x == 0) {
     uint64_t v = 0;
     for (int x = 0; x < D; ++x) v |= (uint64_t)p.base_order[x] << (4 * x);
@@ -82,7 +86,7 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
       } else if (pl != 0) {
         uint64_t r = splitmix64(p.seed ^ pl);
         for (int kk = D - 1; kk >= 1; --kk) {
-          const int jj = (int)mod64_small(r, (uint32_t)kk + 1u);
+          const int jj = (int)mod64_small(r, (uint32_t)kk + 1u, magic[kk + 1]);
           const uint64_t a = (perm >> (4 * kk)) & 0xf, b = (perm >> (4 * jj)) & 0xf;
           perm &= ~((0xfull << (4 * kk)) | (0xfull << (4 * jj)));
           perm |= (b << (4 * kk)) | (a << (4 * jj));
