@@ -718,6 +718,11 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   // ---- prefix-shared DP (amp_trie.cuh): class stage-1 tables, once -------
   ctx->trie = ctx->dedup && std::getenv("AMP_NO_TRIE") == nullptr;
   if (ctx->trie) {
+    int n_heavy = 0;
+    for (size_t c = 0; c < ctx->classes.size(); ++c) n_heavy += is_heavy(ctx, c) ? 1 : 0;
+    ctx->trie = n_heavy <= kTrieMaxCls;
+  }
+  if (ctx->trie) {
     std::vector<uint64_t> v1off(ctx->classes.size(), 0);
     std::vector<int32_t> heavy;
     uint64_t acc = 0;
@@ -950,7 +955,7 @@ int run_trie(amp_ctx* ctx, const EvalParams& ep) {
   uint64_t bacc = 0, vmax = 1;
   for (int j = 2; j <= ctx->max_pp; ++j) {
     const int d = j - 1;
-    uint64_t vacc = 0;
+    uint64_t vacc = 0, iacc = 0;
     for (int c = 0; c < NC; ++c) {
       const uint32_t nb = range[((size_t)d * NC + c) * 2], ne = range[((size_t)d * NC + c) * 2 + 1];
       if (ne <= nb || !is_heavy(ctx, c) || ctx->classes[c].pp < j) continue;
@@ -960,16 +965,17 @@ int run_trie(amp_ctx* ctx, const EvalParams& ep) {
       vbase[(size_t)d * NC + c] = vacc;
       bbase[(size_t)d * NC + c] = bacc;
       stcls[(size_t)j * NC + stn[j]] = c;
-      stitem[(size_t)j * (NC + 1) + stn[j]] = vacc;
+      stitem[(size_t)j * (NC + 1) + stn[j]] = iacc;  // items: (cell, chunk of kTrieNB nodes)
       ++stn[j];
       vacc += sz;
       bacc += sz;
+      iacc += cells * ((ne - nb + kTrieNB - 1) / kTrieNB);
     }
-    stitem[(size_t)j * (NC + 1) + stn[j]] = vacc;
-    total[j] = vacc;
+    if (stn[j] > kTrieMaxCls) return fail(ctx, AMP_E_UNSUPPORTED, "too many classes for the trie DP");
+    stitem[(size_t)j * (NC + 1) + stn[j]] = iacc;
+    total[j] = iacc;
     vmax = std::max<uint64_t>(vmax, vacc);
   }
-  if (NC > kTrieMaxCls) return fail(ctx, AMP_E_UNSUPPORTED, "too many classes for the trie DP");
   CK(upload(ctx->tr_vbase, vbase.data(), vbase.size()));
   CK(upload(ctx->tr_bbase, bbase.data(), bbase.size()));
   CK(upload(ctx->tr_stcls, stcls.data(), stcls.size()));

@@ -31,7 +31,7 @@
 
 namespace amp {
 
-constexpr int kTrieMaxCls = 1024;  // classes per stage list held in smem
+constexpr int kTrieMaxCls = 256;  // classes per stage list held in smem
 
 struct TrieParams {
   // signatures (run heads of the sorted keys)
@@ -113,22 +113,66 @@ __global__ void k_trie_nodes(TrieParams p, int d) {
   }
 }
 
-// Stage j: one thread per (class, cell x of N_j, node n of depth j-1), node
-// fastest.
+// Per-class facts of one stage, cached in shared memory.
+struct TrieSlot {
+  uint64_t ibase;      // first item of the class in the stage
+  uint64_t vbase, bbase, vbase_p;  // table bases at depth d, d (argmins), d-1
+  uint64_t v1off;
+  uint32_t nb, K, nb_p, K_p;       // node ranges at depth d and d-1
+  uint32_t cell0, pred_base_lo, pred_base_hi, pad;  // program: first cell of N_j, preds
+  int32_t c, pair, gas, chunks;    // class, its (tmp, mbs) pair, gas, node chunks
+};
+
+constexpr int kTrieNB = 4;  // nodes per thread: they share the cell's work
+
+// Stage j: one thread per (class, cell x of N_j, chunk of kTrieNB nodes of
+// depth j-1).  Per cut the predecessor index, t2 and the tolerance term are
+// shared by the thread's nodes; each node adds its parent's value and its
+// own edge (the per-candidate kernels' operations and order).
 __global__ void __launch_bounds__(256) k_trie_stage(TrieParams p, int j, uint64_t total,
                                                     unsigned long long* exec) {
+  __shared__ TrieSlot slot[kTrieMaxCls];
   __shared__ uint64_t ibase[kTrieMaxCls + 1];
-  __shared__ int32_t icls[kTrieMaxCls];
   __shared__ unsigned long long cnt;
   const int nc = p.st_n[j];
+  const int d = j - 1, L = p.L, LP = L + 1;
   for (int x = threadIdx.x; x <= nc; x += blockDim.x) {
     ibase[x] = p.st_item[(size_t)j * (p.n_cls + 1) + x];
-    if (x < nc) icls[x] = p.st_cls[(size_t)j * p.n_cls + x];
+    if (x == nc) continue;
+    TrieSlot t;
+    const int c = p.st_cls[(size_t)j * p.n_cls + x];
+    const ClassDev cl = p.cls[c];
+    const ProgDev pg = p.progs[p.class_prog[c]];
+    const uint32_t* rg = p.range + ((size_t)d * p.n_cls + c) * 2;
+    t.ibase = ibase[x];
+    t.c = c;
+    t.pair = cl.pair;
+    t.gas = cl.gas;
+    t.nb = rg[0];
+    t.K = rg[1] - rg[0];
+    t.chunks = (t.K + kTrieNB - 1) / kTrieNB;
+    t.vbase = p.vbase[(size_t)d * p.n_cls + c];
+    t.bbase = p.bbase[(size_t)d * p.n_cls + c];
+    if (j > 2) {
+      const uint32_t* rgp = p.range + ((size_t)(d - 1) * p.n_cls + c) * 2;
+      t.nb_p = rgp[0];
+      t.K_p = rgp[1] - rgp[0];
+      t.vbase_p = p.vbase[(size_t)(d - 1) * p.n_cls + c];
+    } else {
+      t.nb_p = 0;
+      t.K_p = 1;
+      t.vbase_p = 0;
+    }
+    t.v1off = p.v1off[c];
+    t.cell0 = pg.cell_base + p.stage[pg.stage_base + j - 1];
+    t.pred_base_lo = (uint32_t)pg.pred_base;
+    t.pred_base_hi = (uint32_t)(pg.pred_base >> 32);
+    t.pad = 0;
+    slot[x] = t;
   }
   if (threadIdx.x == 0) cnt = 0;
   __syncthreads();
   unsigned long long mine = 0;
-  const int d = j - 1, L = p.L, LP = L + 1;
   const double* Vprev = p.vals[(j - 1) & 1];
   double* Vcur = p.vals[j & 1];
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
@@ -139,51 +183,58 @@ __global__ void __launch_bounds__(256) k_trie_stage(TrieParams p, int j, uint64_
       if (ibase[mid] <= t) lo = mid;
       else hi = mid - 1;
     }
-    const int c = icls[lo];
-    const uint32_t* rg = p.range + ((size_t)d * p.n_cls + c) * 2;
-    const uint32_t nb = rg[0], K = rg[1] - rg[0];
-    const uint64_t off = t - ibase[lo];
-    const uint32_t x = (uint32_t)(off / K), nl = (uint32_t)(off % K);
-    const uint32_t node = nb + nl;
-    const ClassDev cl = p.cls[c];
-    const ProgDev pg = p.progs[p.class_prog[c]];
-    const uint32_t* ss = p.stage + pg.stage_base;
-    const uint2 rec = p.cellrec[pg.cell_base + ss[j - 1] + x];
+    const TrieSlot& S = slot[lo];
+    const uint64_t off = t - S.ibase;
+    const uint32_t x = (uint32_t)(off / (uint32_t)S.chunks);
+    const uint32_t n0 = (uint32_t)(off % (uint32_t)S.chunks) * kTrieNB;  // local node
+    const int nn = (int)min((uint32_t)kTrieNB, S.K - n0);
+    const uint2 rec = p.cellrec[S.cell0 + x];
     const int i = rec.x >> 16, m = rec.x & 0xffff;
-    const uint16_t* q = p.preds + pg.pred_base + rec.y;
-    const double* Pf = p.prefix + (size_t)cl.pair * LP;
-    const double dm = p.domain[(size_t)cl.pair * p.nv_stride + m];
+    const uint16_t* q = p.preds + (((uint64_t)S.pred_base_hi << 32) | S.pred_base_lo) + rec.y;
+    const double* Pf = p.prefix + (size_t)S.pair * LP;
+    const double dm = p.domain[(size_t)S.pair * p.nv_stride + m];
     const double Pi = Pf[i];
-    const double g1 = (double)(cl.gas - 1);
-    const uint64_t key = p.rep_key[p.first[(size_t)d * p.stride + node]];
-    const double* E = p.qtab + ((size_t)c * p.n_codes + key_code(p, key, j - 2)) * L;
-    // the parent's stage-(j-1) values: the class's stage-1 table, or the
-    // depth-(j-2) node this node extends (cell-major table of its class)
-    const double* Vp;
-    uint32_t Kp = 1;
-    if (j == 2) {
-      Vp = p.v1g + p.v1off[c];
-    } else {
-      const uint32_t* rgp = p.range + ((size_t)(d - 1) * p.n_cls + c) * 2;
-      Kp = rgp[1] - rgp[0];
-      const uint32_t pn = p.parent[(size_t)d * p.stride + node] - rgp[0];
-      Vp = Vprev + p.vbase[(size_t)(d - 1) * p.n_cls + c] + pn;
+    const double g1 = (double)(S.gas - 1);
+    const double* Vp[kTrieNB];
+    const double* E[kTrieNB];
+    double best[kTrieNB];
+    int bc[kTrieNB];
+#pragma unroll
+    for (int b = 0; b < kTrieNB; ++b) {
+      const uint32_t node = S.nb + n0 + (b < nn ? b : 0);  // pad with the first node
+      const uint64_t key = p.rep_key[p.first[(size_t)d * p.stride + node]];
+      E[b] = p.qtab + ((size_t)S.c * p.n_codes + key_code(p, key, j - 2)) * L;
+      if (j == 2) {
+        Vp[b] = p.v1g + S.v1off;
+      } else {
+        const uint32_t pn = p.parent[(size_t)d * p.stride + node] - S.nb_p;
+        Vp[b] = Vprev + S.vbase_p + pn;
+      }
+      best[b] = CUDART_INF;
+      bc[b] = -1;
     }
-    double best = CUDART_INF;
-    int bc = -1;
+    const uint32_t Kp = S.K_p;
     for (int cut = j - 1; cut < i; ++cut) {  // pipeline_dp.cpp:114-131
       const double t2 = Pi - Pf[cut];
       const double term = t2 > dm ? g1 * (t2 - dm) : 0.0;
-      const double g = ((Vp[(size_t)q[cut - (j - 1)] * Kp] + term) + t2) + E[cut];
-      if (g < best) {
-        best = g;
-        bc = cut;
+      const size_t idx = (size_t)q[cut - (j - 1)] * Kp;
+#pragma unroll
+      for (int b = 0; b < kTrieNB; ++b) {
+        const double g = ((Vp[b][idx] + term) + t2) + E[b][cut];
+        if (g < best[b]) {
+          best[b] = g;
+          bc[b] = cut;
+        }
       }
     }
-    const uint64_t o = (uint64_t)x * K + nl;
-    Vcur[p.vbase[(size_t)d * p.n_cls + c] + o] = best;
-    p.bp[p.bbase[(size_t)d * p.n_cls + c] + o] = (uint8_t)bc;
-    mine += (unsigned long long)(i - (j - 1));
+#pragma unroll
+    for (int b = 0; b < kTrieNB; ++b) {
+      if (b >= nn) break;
+      const uint64_t o = (uint64_t)x * S.K + n0 + b;
+      Vcur[S.vbase + o] = best[b];
+      p.bp[S.bbase + o] = (uint8_t)bc[b];
+    }
+    mine += (unsigned long long)(i - (j - 1)) * nn;
   }
   if (exec) {  // executed inner iterations (roofline accounting)
     atomicAdd(&cnt, mine);
