@@ -148,6 +148,9 @@ struct EvalParams {
   uint64_t* placep;           // [n_chunk] placement as 16 x 4-bit nibbles, or NULL
   int32_t need_place_rows;    // K_place must also write placeb (warp K_est reads it)
   int32_t need_bwq;           // K_place must also write bwqb (kernels without edge tables)
+  const uint8_t* cut2tab;     // [n_cls][n_codes] cut of the 2-stage DP (pp == 2 classes) or NULL
+  int32_t n_cls_total;        // classes in the plan() list
+  int32_t pad6;
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

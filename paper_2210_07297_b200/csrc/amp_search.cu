@@ -158,7 +158,7 @@ struct amp_ctx {
   // bandwidth codes (ranks of the distinct link bandwidths) and per-class
   // edge-cost tables; n_codes = 0 when disabled
   int n_codes = 0;
-  DevBuf bwcode, bwval, qtab, cellrec;
+  DevBuf bwcode, bwval, qtab, cellrec, cut2tab;
   uint64_t n_heavy = 0;  // items of pp >= 3 classes in the current run's dispatch order
   // DP memoisation by signature (amp_dedup.cuh)
   bool dedup = false;
@@ -715,6 +715,23 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
       CK(ctx->dd_counters.ensure(2 * sizeof(unsigned long long)));
     }
   }
+  // ---- 2-stage DP table (pp == 2 classes x boundary codes), once ----------
+  if (ctx->n_codes > 0) {
+    EvalParams tp{};
+    tp.L = L;
+    tp.cls = ctx->cls_d.as<ClassDev>();
+    tp.prefix = ctx->prefix.as<double>();
+    tp.domain = ctx->domain.as<double>();
+    tp.seg = ctx->seg.as<uint16_t>();
+    tp.nv_stride = ctx->nv_stride;
+    tp.qtab = ctx->qtab.as<double>();
+    tp.n_codes = ctx->n_codes;
+    tp.n_cls_total = (int)ctx->classes.size();
+    const size_t nt = ctx->classes.size() * (size_t)ctx->n_codes;
+    CK(ctx->cut2tab.ensure(nt + 16));
+    k_cut2_table<<<(int)((nt + 127) / 128), 128, 0, ctx->stream>>>(tp, ctx->cut2tab.as<uint8_t>());
+    CK(cudaGetLastError());
+  }
   // ---- prefix-shared DP (amp_trie.cuh): class stage-1 tables, once -------
   ctx->trie = ctx->dedup && std::getenv("AMP_NO_TRIE") == nullptr;
   if (ctx->trie) {
@@ -1112,6 +1129,8 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   ep.bwval = ctx->bwval.as<double>();
   ep.qtab = ctx->n_codes ? ctx->qtab.as<double>() : nullptr;
   ep.cellrec = ctx->cellrec.as<uint2>();
+  ep.cut2tab = ctx->n_codes ? ctx->cut2tab.as<uint8_t>() : nullptr;
+  ep.n_cls_total = (int)ctx->classes.size();
   if (ctx->dedup && !d_given_cuts) {
     CK(ctx->dd_keys.ensure(sizeof(uint64_t) * C));
     CK(ctx->dd_skeys.ensure(sizeof(uint64_t) * C));

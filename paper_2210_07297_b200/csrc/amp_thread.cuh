@@ -104,9 +104,9 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
       int first_bad = -1;
       double bad_val = 0.0;
       for (int q = 0; q < pp - 1; ++q) {
-        int cm = 255;
-        for (int r = 0; r < dp; ++r)
-          for (int s = 0; s < tmp; ++s) {
+        int cm = 255;  // (code 0 is the smallest bandwidth: nothing can go lower)
+        for (int r = 0; r < dp && cm; ++r)
+          for (int s = 0; s < tmp && cm; ++s) {
             const int cc = codeS[nib(perm, (q * dp + r) * tmp + s) * D +
                                  nib(perm, ((q + 1) * dp + r) * tmp + s)];
             cm = cc < cm ? cc : cm;
@@ -205,6 +205,12 @@ __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
           const uint64_t src = (p.rep_of && !p.cuts_given && u < p.n_dp) ? p.rep_of[u] : u;
           const uint8_t* ci = p.cutsb + src * (maxpp + 1);
           for (int q = 0; q <= pp; ++q) cuts[q] = ci[q];
+        } else if (pp == 2 && p.cut2tab) {
+          // the 2-stage DP depends on (class, boundary-0 code) only: tabulated
+          // once per context by k_cut2_table (the same operations)
+          cuts[0] = 0;
+          cuts[1] = p.cut2tab[(size_t)w.cls * p.n_codes + p.bwcb[u * maxpp]];
+          cuts[2] = L;
         } else if (pp == 2) {
           const double* Pf = p.prefix + (size_t)cl.pair * LP;
           const double* Dm = p.domain + (size_t)cl.pair * p.nv_stride;
@@ -261,7 +267,7 @@ __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
           double sum = 0.0;
           for (int q = 0; q < pp - 1; ++q) {
             int cm = 255;
-            for (int s = 0; s < tmp; ++s) {
+            for (int s = 0; s < tmp && cm; ++s) {
               const int cc = codeS[nib(perm, (q * dp + r) * tmp + s) * D +
                                    nib(perm, ((q + 1) * dp + r) * tmp + s)];
               cm = cc < cm ? cc : cm;
@@ -283,9 +289,9 @@ __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
           for (int g = 0; g < pp * tmp; ++g) {
             const int j = g / tmp, s = g % tmp;
             int cm = 255;
-            for (int r1 = 0; r1 < dp; ++r1) {
+            for (int r1 = 0; r1 < dp && cm; ++r1) {
               const int d1 = nib(perm, (j * dp + r1) * tmp + s);
-              for (int r2 = r1 + 1; r2 < dp; ++r2) {
+              for (int r2 = r1 + 1; r2 < dp && cm; ++r2) {
                 const int cc = codeS[d1 * D + nib(perm, (j * dp + r2) * tmp + s)];
                 cm = cc < cm ? cc : cm;
               }
@@ -401,6 +407,40 @@ __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
       e.fail_value = 0.0;
       gtop[x] = e;
     }
+  }
+}
+
+// The 2-stage DP (pipeline_dp.cpp:70-149 at k = 2; light_cut2's operations
+// in order) for every pp == 2 class and every boundary code, once per
+// context: its inputs are the class's tables and the code's edge row only.
+__global__ void k_cut2_table(const EvalParams p, uint8_t* tab) {
+  const int n = p.n_codes;
+  const int L = p.L, LP = L + 1;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < p.n_cls_total * n;
+       t += gridDim.x * blockDim.x) {
+    const int c = t / n, code = t % n;
+    const ClassDev cl = p.cls[c];
+    if (cl.pp != 2 || cl.pp > L) continue;
+    const double* Pf = p.prefix + (size_t)cl.pair * LP;
+    const double* Dm = p.domain + (size_t)cl.pair * p.nv_stride;
+    const uint16_t* sg = p.seg + (size_t)cl.pair * LP * LP;
+    const double g1 = (double)(cl.gas - 1);
+    const double* qt = p.qtab + ((size_t)c * n + code) * L;
+    const double dm0 = Dm[0], PLL = Pf[L], P0 = Pf[0];
+    double best = CUDART_INF;
+    int bc = -1;
+    for (int cut = 1; cut < L; ++cut) {
+      const double t1 = Pf[cut] - P0;
+      const double sub = g1 * max0(t1 - Dm[sg[cut * LP + L]]) + t1;
+      const double t2 = PLL - Pf[cut];
+      const double term = t2 > dm0 ? g1 * (t2 - dm0) : 0.0;
+      const double g = ((sub + term) + t2) + qt[cut];
+      if (g < best) {
+        best = g;
+        bc = cut;
+      }
+    }
+    tab[t] = (uint8_t)bc;
   }
 }
 

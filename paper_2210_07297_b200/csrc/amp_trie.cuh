@@ -133,7 +133,6 @@ __global__ void __launch_bounds__(256) k_trie_stage(TrieParams p, int j, uint64_
                                                     unsigned long long* exec) {
   __shared__ TrieSlot slot[kTrieMaxCls];
   __shared__ uint64_t ibase[kTrieMaxCls + 1];
-  __shared__ unsigned long long cnt;
   const int nc = p.st_n[j];
   const int d = j - 1, L = p.L, LP = L + 1;
   for (int x = threadIdx.x; x <= nc; x += blockDim.x) {
@@ -170,7 +169,6 @@ __global__ void __launch_bounds__(256) k_trie_stage(TrieParams p, int j, uint64_
     t.pad = 0;
     slot[x] = t;
   }
-  if (threadIdx.x == 0) cnt = 0;
   __syncthreads();
   unsigned long long mine = 0;
   const double* Vprev = p.vals[(j - 1) & 1];
@@ -236,10 +234,10 @@ __global__ void __launch_bounds__(256) k_trie_stage(TrieParams p, int j, uint64_
     }
     mine += (unsigned long long)(i - (j - 1)) * nn;
   }
-  if (exec) {  // executed inner iterations (roofline accounting)
-    atomicAdd(&cnt, mine);
-    __syncthreads();
-    if (threadIdx.x == 0) atomicAdd(exec, cnt);
+  if (exec) {  // executed inner iterations (roofline accounting): one
+               // global atomic per warp (a 64-bit smem atomicAdd is a CAS loop)
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(exec, mine);
   }
 }
 
