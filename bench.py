@@ -31,7 +31,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 SCENARIO = "hetero_cluster"
-DEFAULT_N_PER_GPU = 10_000_000
+DEFAULT_N_PER_GPU = 100_000_000
 TOPK = 10
 METRIC = "candidate strategies/sec"
 # ncu --set full of one k_dp_multi launch (profiles/r1b_k_dp_multi_ncu.txt):

@@ -787,12 +787,12 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   // chunk size: keep the per-chunk buffers within ~256 MB
   const size_t per_item = sizeof(CandWork) + sizeof(int32_t) * D + sizeof(double) * ctx->max_pp +
                           (ctx->max_pp + 1);
-  // (+ the dedup buffers, ~40 B/item) — up to 16 M items (~5 GB) per chunk
-  // so a 10 M step is one pass: fewer launch tails and dedup over the whole
-  // step; AMP_CHUNK overrides (tests of the multi-chunk path)
+  // (+ the dedup buffers, ~40 B/item) — up to 64 M items (~20 GB of the
+  // 180 GB HBM) per chunk, so a 100 M step is two passes: fewer launch tails
+  // and dedup over most of the step; AMP_CHUNK overrides (multi-chunk tests)
   const uint64_t chunk_cap = std::getenv("AMP_CHUNK") ? std::strtoull(std::getenv("AMP_CHUNK"), nullptr, 10)
-                                                : (16ull << 20);
-  ctx->chunk = std::max<uint64_t>(1024, std::min<uint64_t>(chunk_cap, (4ull << 30) / per_item));
+                                                : (64ull << 20);
+  ctx->chunk = std::max<uint64_t>(1024, std::min<uint64_t>(chunk_cap, (24ull << 30) / per_item));
   CK(ctx->bp.ensure(ctx->bp_stride * n_ctas + 16));
   if (ctx->slice_stride) CK(ctx->slice.ensure(sizeof(double) * ctx->slice_stride * n_ctas));
   if (!sparse && !ctx->w_in_smem) CK(ctx->wtab.ensure(w_b * n_ctas));
