@@ -151,6 +151,11 @@ struct EvalParams {
   const uint8_t* cut2tab;     // [n_cls][n_codes] cut of the 2-stage DP (pp == 2 classes) or NULL
   int32_t n_cls_total;        // classes in the plan() list
   int32_t pad6;
+  // stage_time / params_in_range over every layer range [a, b), summed from
+  // 0.0 in layer order (the reference's loops, tabulated once per context)
+  const double* rsum_t;       // [n_pairs][(L+1)^2] layer-time range sums, or NULL
+  const double* rsum_p;       // [(L+1)^2] parameter range sums
+  uint8_t* repcuts;           // [n_rep][max_pp + 1] cuts per signature run (memoised runs)
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

@@ -34,7 +34,7 @@ struct DedupParams {
   uint32_t* flags;      // [n] head flags -> (scan) run ids (inclusive)
   const uint32_t* runid;
   uint32_t* rep_list;   // [n] representative item of each run
-  uint32_t* rep_of;     // [n] representative of every item
+  uint32_t* rep_of;     // [n] signature run of every item
   uint64_t* n_rep;      // device count of runs
   uint64_t* rep_key;    // [n] key of each run (NULL: not needed)
 };
@@ -79,7 +79,7 @@ __global__ void k_dedup_reps(DedupParams p) {
 __global__ void k_dedup_scatter(DedupParams p) {
   for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < p.n;
        s += (uint64_t)gridDim.x * blockDim.x)
-    p.rep_of[p.svals[s]] = p.rep_list[p.runid[s] - 1];
+    p.rep_of[p.svals[s]] = p.runid[s] - 1;  // the signature's run (index into repcuts)
 }
 
 }  // namespace amp

@@ -252,14 +252,16 @@ __global__ void __launch_bounds__(B >= 8 ? 512 : 256, (B <= 2 ? 3 : (B >= 8 ? 1 
   // deferred backtrack (uniform except pend_u, the member of this lane)
   int pend_n = 0, pend_k = 0, pend_buf = 0;
   uint32_t pend_cell = 0, pend_stage = 0;
-  uint64_t pend_pred = 0, pend_u = 0;
+  uint64_t pend_pred = 0, pend_u = 0, pend_slot = 0;
   int bpsel = 0;
   auto backtrack = [&]() {  // pipeline_dp.cpp:134-148, lane r < pend_n
     const uint32_t* cpd = p.cellpred + pend_cell;
     const uint16_t* pd = p.preds + pend_pred;
     const uint32_t* ss = p.stage + pend_stage;
     const uint32_t rest0 = ss[1];
-    uint8_t* co = p.cutsb + pend_u * (maxpp + 1);
+    // memoised runs write the signature's cuts at its run index (compact,
+    // L2-resident for K_est); otherwise at the chunk item
+    uint8_t* co = p.repcuts ? p.repcuts + pend_slot * (maxpp + 1) : p.cutsb + pend_u * (maxpp + 1);
     const uint8_t* bpr = bpb + (size_t)pend_buf * B * max_rest + lane;
     co[pend_k] = (uint8_t)L;
     uint32_t x = ss[pend_k - 1];  // N_k = {(L, 0)}
@@ -289,6 +291,11 @@ __global__ void __launch_bounds__(B >= 8 ? 512 : 256, (B <= 2 ? 3 : (B >= 8 ? 1 
         if (((todo >> b) & 1u) && wq[cur][b].cls == gcls) gm |= 1u << b;
       todo &= ~gm;
       const int ng = __popc(gm);
+      auto slot_of = [&](int r) -> uint64_t {  // r >= ng repeats member 0
+        unsigned m = gm;
+        for (int q = r < ng ? r : 0; q > 0; --q) m &= m - 1;
+        return ubase + (uint64_t)(__ffs(m) - 1);
+      };
       auto member = [&](int r) -> uint64_t {  // r >= ng repeats member 0
         unsigned m = gm;
         for (int q = r < ng ? r : 0; q > 0; --q) m &= m - 1;
@@ -377,6 +384,7 @@ __global__ void __launch_bounds__(B >= 8 ? 512 : 256, (B <= 2 ? 3 : (B >= 8 ? 1 
       pend_pred = pg.pred_base;
       pend_stage = pg.stage_base;
       pend_u = member(lane);
+      pend_slot = slot_of(lane);
       bpsel ^= 1;
     }
     if (bnext >= nbatch) break;

@@ -532,8 +532,10 @@ __global__ void __launch_bounds__(kEstWarps * 32, 3) k_est(EvalParams p) {
     if (fc == 0) {
       if (pp >= 3 || p.cuts_given) {
         // (memoised DP: the cuts of this candidate's signature representative)
-        const uint64_t src = (p.rep_of && !p.cuts_given && u < p.n_dp) ? p.rep_of[u] : u;
-        const uint8_t* ci = p.cutsb + src * (maxpp + 1);
+        // (memoised DP: the cuts of this candidate's signature run)
+        const uint8_t* ci = (p.rep_of && !p.cuts_given && u < p.n_dp)
+                                ? p.repcuts + (uint64_t)p.rep_of[u] * (maxpp + 1)
+                                : p.cutsb + u * (maxpp + 1);
         for (int q = lane; q <= pp; q += 32) cutsW[q] = ci[q];
       } else {
         // pp <= 2 never reaches K_dp: single stage, or the two-stage DP

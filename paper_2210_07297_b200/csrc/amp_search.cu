@@ -158,13 +158,13 @@ struct amp_ctx {
   // bandwidth codes (ranks of the distinct link bandwidths) and per-class
   // edge-cost tables; n_codes = 0 when disabled
   int n_codes = 0;
-  DevBuf bwcode, bwval, qtab, cellrec, cut2tab;
+  DevBuf bwcode, bwval, qtab, cellrec, cut2tab, rsum_t, rsum_p;
   uint64_t n_heavy = 0;  // items of pp >= 3 classes in the current run's dispatch order
   // DP memoisation by signature (amp_dedup.cuh)
   bool dedup = false;
   int code_bits = 0, key_bits = 0;
   DevBuf dd_keys, dd_vals, dd_skeys, dd_svals, dd_flags, dd_runid, dd_rep_list, dd_rep_of;
-  DevBuf dd_nrep, dd_temp, dd_counters, prog_inner_d;
+  DevBuf dd_nrep, dd_temp, dd_counters, prog_inner_d, dd_repcuts;
   size_t dd_temp_bytes = 0;
   // DP shared across signature prefixes (amp_trie.cuh)
   bool trie = false;
@@ -715,6 +715,15 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
       CK(ctx->dd_counters.ensure(2 * sizeof(unsigned long long)));
     }
   }
+  // ---- stage-time / parameter range sums (thread K_est), once ------------
+  if ((size_t)(L + 1) * (L + 1) * (n_pairs + 1) * sizeof(double) <= ((size_t)256 << 20)) {
+    CK(ctx->rsum_t.ensure(sizeof(double) * (size_t)n_pairs * (L + 1) * (L + 1)));
+    CK(ctx->rsum_p.ensure(sizeof(double) * (size_t)(L + 1) * (L + 1)));
+    k_range_sums<<<n_pairs + 1, 128, 0, ctx->stream>>>(ctx->times.as<double>(), ctx->param.as<double>(),
+                                                      L, n_pairs, ctx->rsum_t.as<double>(),
+                                                      ctx->rsum_p.as<double>());
+    CK(cudaGetLastError());
+  }
   // ---- 2-stage DP table (pp == 2 classes x boundary codes), once ----------
   if (ctx->n_codes > 0) {
     EvalParams tp{};
@@ -949,7 +958,7 @@ int run_trie(amp_ctx* ctx, const EvalParams& ep) {
   tp.qtab = ctx->qtab.as<double>();
   tp.v1g = ctx->v1g_d.as<double>();
   tp.v1off = ctx->v1off_d.as<uint64_t>();
-  tp.cutsb = ep.cutsb;
+  tp.repcuts = ep.repcuts;
   const int g = (int)std::min<uint64_t>((S + 255) / 256, (uint64_t)ctx->sms * 8);
   for (int d = 1; d <= nq; ++d) {
     k_trie_flag<<<g, 256, 0, ctx->stream>>>(tp, d);
@@ -1130,6 +1139,8 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   ep.qtab = ctx->n_codes ? ctx->qtab.as<double>() : nullptr;
   ep.cellrec = ctx->cellrec.as<uint2>();
   ep.cut2tab = ctx->n_codes ? ctx->cut2tab.as<uint8_t>() : nullptr;
+  ep.rsum_t = ctx->rsum_t.as<double>();
+  ep.rsum_p = ctx->rsum_p.as<double>();
   ep.n_cls_total = (int)ctx->classes.size();
   if (ctx->dedup && !d_given_cuts) {
     CK(ctx->dd_keys.ensure(sizeof(uint64_t) * C));
@@ -1141,6 +1152,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     CK(ctx->dd_rep_list.ensure(sizeof(uint32_t) * C));
     CK(ctx->dd_rep_of.ensure(sizeof(uint32_t) * C));
     if (ctx->trie) CK(ctx->dd_rep_key.ensure(sizeof(uint64_t) * C));
+    CK(ctx->dd_repcuts.ensure((size_t)C * (ctx->max_pp + 1)));
     size_t t1 = 0, t2 = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, t1, (const uint64_t*)nullptr, (uint64_t*)nullptr,
                                        (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)C, 0,
@@ -1227,6 +1239,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     ep.rep_list = nullptr;
     ep.rep_of = nullptr;
     ep.n_rep = nullptr;
+    ep.repcuts = nullptr;
     bool skip_dp = false;
     if (ctx->dedup && !d_given_cuts && ep.n_dp > 0) {
       // ---- memoisation: sort signatures, one DP per distinct key --------
@@ -1264,6 +1277,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
       ep.rep_list = dp.rep_list;
       ep.rep_of = dp.rep_of;
       ep.n_rep = dp.n_rep;
+      ep.repcuts = ctx->dd_repcuts.as<uint8_t>();
       if (ctx->trie) {
         const int rc = run_trie(ctx, ep);
         if (rc != AMP_OK) return rc;

@@ -143,11 +143,9 @@ constexpr int kEstTWarps = 8;
 
 __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
   __shared__ uint8_t codeS[kThreadMaxD * kThreadMaxD];
-  __shared__ int lock;
   __shared__ int n_top;
-  __shared__ double kth_total;
-  __shared__ int kth_failed;
   __shared__ amp_record stage_rec[kEstTWarps][32];  // records handed to the warp leader
+  __shared__ amp_record wtop[kEstTWarps][32];       // per-warp top-k (no lock)
   __shared__ amp_record topS[32];
   const int D = p.D, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, maxpp = p.max_pp;
   const int L = p.L, LP = L + 1;
@@ -155,23 +153,19 @@ __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
   amp_record* mytop = p.k <= 32 ? topS : gtop;
   for (int x = threadIdx.x; x < D * D; x += blockDim.x) codeS[x] = p.bwcode[x];
   if (threadIdx.x == 0) {
-    lock = 0;
     n_top = 0;
-    kth_total = CUDART_INF;
-    kth_failed = 2;
     if (!p.first_chunk) {  // CTA lists persist across chunks
       for (int x = 0; x < p.k; ++x) {
         if (gtop[x].fail_code < 0) break;
         if (mytop != gtop) mytop[x] = gtop[x];
         ++n_top;
       }
-      if (p.k > 0 && n_top == p.k) {
-        kth_failed = mytop[p.k - 1].fail_code != 0;
-        kth_total = mytop[p.k - 1].total;
-      }
     }
   }
   __syncthreads();
+  __shared__ int wcount[kEstTWarps];
+  int w_n = 0, w_kf = 2;  // warp list size, k-th entry (failed flag, total)
+  double w_kt = CUDART_INF;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   // uniform trip count per warp (the top-k hand-off is warp-synchronous)
   const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
@@ -202,8 +196,10 @@ __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
         // ---- cuts: K_dp (memoised: its signature's representative), or
         //      the k <= 2 DP here (light_cut2's operations, sequential) ---
         if (pp >= 3 || p.cuts_given) {
-          const uint64_t src = (p.rep_of && !p.cuts_given && u < p.n_dp) ? p.rep_of[u] : u;
-          const uint8_t* ci = p.cutsb + src * (maxpp + 1);
+          // (memoised DP: the cuts of this candidate's signature run)
+          const uint8_t* ci = (p.rep_of && !p.cuts_given && u < p.n_dp)
+                                  ? p.repcuts + (uint64_t)p.rep_of[u] * (maxpp + 1)
+                                  : p.cutsb + u * (maxpp + 1);
           for (int q = 0; q <= pp; ++q) cuts[q] = ci[q];
         } else if (pp == 2 && p.cut2tab) {
           // the 2-stage DP depends on (class, boundary-0 code) only: tabulated
@@ -242,15 +238,24 @@ __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
         //      (types.cpp:34-40), per-device parameter ceiling -----------
         const double* tl = p.times + (size_t)cl.pair * L;
         double worst_p = 0.0;
-        for (int j = 0; j < pp; ++j) {
-          double sum = 0.0, ps = 0.0;
-          for (int l = cuts[j]; l < cuts[j + 1]; ++l) {
-            sum += tl[l];
-            ps += p.param[l];
+        if (p.rsum_t) {  // the same sums, tabulated per layer range
+          const double* rt = p.rsum_t + (size_t)cl.pair * LP * LP;
+          for (int j = 0; j < pp; ++j) {
+            st[j] = rt[cuts[j] * LP + cuts[j + 1]];
+            spar[j] = p.rsum_p[cuts[j] * LP + cuts[j + 1]];
+            worst_p = std_max(worst_p, spar[j] / tmp);
           }
-          st[j] = sum;
-          spar[j] = ps;
-          worst_p = std_max(worst_p, ps / tmp);
+        } else {
+          for (int j = 0; j < pp; ++j) {
+            double sum = 0.0, ps = 0.0;
+            for (int l = cuts[j]; l < cuts[j + 1]; ++l) {
+              sum += tl[l];
+              ps += p.param[l];
+            }
+            st[j] = sum;
+            spar[j] = ps;
+            worst_p = std_max(worst_p, ps / tmp);
+          }
         }
         if (p.has_ceiling && worst_p > p.ceiling) fc = AMP_FAIL_CEILING;
       }
@@ -359,38 +364,41 @@ __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
         for (int x = 0; x < D; ++x) o[x] = ok ? nib(perm, x) : -1;
       }
     }
-    // ---- CTA top-k (rank_records key): lanes that pass the cheap check
-    //      against the current k-th entry hand their record to the leader --
+    // ---- warp top-k (rank_records key): lanes that pass the cheap check
+    //      against the warp list's k-th entry hand their record to the
+    //      leader; the warp lists merge into the CTA list at the end --------
     if (p.k > 0) {
       bool cand = false;
       if (live) {
-        const int kf = *(volatile int*)&kth_failed;
-        const double kt = *(volatile double*)&kth_total;
         const int rf = ok ? 0 : 1;
-        cand = !(rf > kf || (rf == 0 && kf == 0 && rec.total > kt));
+        cand = !(rf > w_kf || (rf == 0 && w_kf == 0 && rec.total > w_kt));
         if (cand) stage_rec[wib][lane] = rec;
       }
       unsigned m = __ballot_sync(0xffffffffu, cand);
       __syncwarp();
       if (lane == 0 && m) {
-        while (atomicCAS(&lock, 0, 1) != 0) __nanosleep(32);
-        __threadfence_block();
-        int n = *(volatile int*)&n_top;
         while (m) {
           const int b = __ffs(m) - 1;
           m &= m - 1;
-          topk_insert(mytop, n, p.k, stage_rec[wib][b]);
+          topk_insert(wtop[wib], w_n, p.k, stage_rec[wib][b]);
         }
-        *(volatile int*)&n_top = n;
-        if (n == p.k) {
-          *(volatile int*)&kth_failed = mytop[p.k - 1].fail_code != 0;
-          *(volatile double*)&kth_total = mytop[p.k - 1].total;
+        if (w_n == p.k) {
+          w_kf = wtop[wib][p.k - 1].fail_code != 0;
+          w_kt = wtop[wib][p.k - 1].total;
         }
-        __threadfence_block();
-        atomicExch(&lock, 0);
       }
-      __syncwarp();
+      w_n = __shfl_sync(0xffffffffu, w_n, 0);
+      w_kf = __shfl_sync(0xffffffffu, w_kf, 0);
+      w_kt = __shfl_sync(0xffffffffu, w_kt, 0);
     }
+  }
+  if (lane == 0) wcount[wib] = w_n;
+  __syncthreads();
+  if (threadIdx.x == 0 && p.k > 0) {  // CTA list (+ the persisted one) <- warp lists
+    int n = n_top;
+    for (int w = 0; w < kEstTWarps; ++w)
+      for (int x = 0; x < wcount[w]; ++x) topk_insert(mytop, n, p.k, wtop[w][x]);
+    n_top = n;
   }
   __syncthreads();
   // store the CTA list (padded to k) for the next chunk / the merge
@@ -406,6 +414,25 @@ __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
       e.fail_layer = -1;
       e.fail_value = 0.0;
       gtop[x] = e;
+    }
+  }
+}
+
+// Range sums of stage_time / params_in_range (cost_model.cpp:88-98,
+// types.cpp:34-40): out[a*(L+1) + b] = ((0.0 + v[a]) + v[a+1]) + ... + v[b-1],
+// the reference's loop order, for every range; block n_pairs is the params.
+__global__ void k_range_sums(const double* times, const double* param, int L, int n_pairs,
+                             double* rt, double* rp) {
+  const int LP = L + 1;
+  const int pr = blockIdx.x;
+  const double* v = pr < n_pairs ? times + (size_t)pr * L : param;
+  double* out = pr < n_pairs ? rt + (size_t)pr * LP * LP : rp;
+  for (int a = threadIdx.x; a <= L; a += blockDim.x) {
+    double sum = 0.0;
+    out[a * LP + a] = 0.0;
+    for (int b = a + 1; b <= L; ++b) {
+      sum += v[b - 1];
+      out[a * LP + b] = sum;
     }
   }
 }

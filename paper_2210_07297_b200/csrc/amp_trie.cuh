@@ -69,7 +69,7 @@ struct TrieParams {
   // stage storage
   double* vals[2];            // ping-pong by stage parity
   uint8_t* bp;                // argmins of all stages
-  uint8_t* cutsb;             // [n_chunk][max_pp + 1]
+  uint8_t* repcuts;           // [n_rep][max_pp + 1] cuts per signature run
 };
 
 __device__ __forceinline__ int key_cls(const TrieParams& p, uint64_t k) {
@@ -255,7 +255,7 @@ __global__ void k_trie_back(TrieParams p) {
     const int k = cl.pp;
     const ProgDev pg = p.progs[p.class_prog[c]];
     const uint32_t* ss = p.stage + pg.stage_base;
-    uint8_t* co = p.cutsb + (uint64_t)p.rep_list[r] * (p.max_pp + 1);
+    uint8_t* co = p.repcuts + r * (p.max_pp + 1);  // compact, by signature run
     co[k] = (uint8_t)L;
     uint32_t x = ss[k - 1];  // N_k = {(L, 0)}
     for (int j = k; j >= 2; --j) {
