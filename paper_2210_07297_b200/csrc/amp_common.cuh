@@ -156,6 +156,8 @@ struct EvalParams {
   const double* rsum_t;       // [n_pairs][(L+1)^2] layer-time range sums, or NULL
   const double* rsum_p;       // [(L+1)^2] parameter range sums
   uint8_t* repcuts;           // [n_rep][max_pp + 1] cuts per signature run (memoised runs)
+  int32_t bw_positive;        // every link bandwidth > 0 (coded): no all-reduce group can fail
+  int32_t pad7;
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

@@ -158,6 +158,7 @@ struct amp_ctx {
   // bandwidth codes (ranks of the distinct link bandwidths) and per-class
   // edge-cost tables; n_codes = 0 when disabled
   int n_codes = 0;
+  bool bw_positive = false;  // smallest distinct bandwidth > 0
   DevBuf bwcode, bwval, qtab, cellrec, cut2tab, rsum_t, rsum_p;
   uint64_t n_heavy = 0;  // items of pp >= 3 classes in the current run's dispatch order
   // DP memoisation by signature (amp_dedup.cuh)
@@ -515,6 +516,7 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
         CK(upload(ctx->bwval, vals.data(), vals.size()));
         CK(upload(ctx->qtab, q.data(), q.size()));
         ctx->n_codes = U;
+        ctx->bw_positive = vals[0] > 0;
       }
     }
   }
@@ -1140,6 +1142,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   ep.cellrec = ctx->cellrec.as<uint2>();
   ep.cut2tab = ctx->n_codes ? ctx->cut2tab.as<uint8_t>() : nullptr;
   ep.rsum_t = ctx->rsum_t.as<double>();
+  ep.bw_positive = ctx->n_codes > 0 && ctx->bw_positive;
   ep.rsum_p = ctx->rsum_p.as<double>();
   ep.n_cls_total = (int)ctx->classes.size();
   if (ctx->dedup && !d_given_cuts) {

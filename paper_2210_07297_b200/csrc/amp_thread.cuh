@@ -268,7 +268,9 @@ __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
         const double* qt = p.qtab + (size_t)w.cls * p.n_codes * L;
         double tr = -CUDART_INF;
         int rr = -1;
-        for (int r = 0; r < dp; ++r) {
+        // (pp == 1: no edges, every replica computes the same t, so the
+        //  strict-'>' scan keeps replica 0: one evaluation)
+        for (int r = 0; r < (pp == 1 ? 1 : dp); ++r) {
           double sum = 0.0;
           for (int q = 0; q < pp - 1; ++q) {
             int cm = 255;
@@ -290,28 +292,47 @@ __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
         double worst = 0.0;
         int bad_group = -1;
         double bad_value = 0.0;
-        if (dp != 1) {
-          for (int g = 0; g < pp * tmp; ++g) {
-            const int j = g / tmp, s = g % tmp;
+        if (dp != 1 && p.bw_positive) {
+          // no group can fail; within a stage every shard group carries the
+          // same message, and the rounded time is non-increasing in b, so the
+          // stage's maximum is the time of its minimum-bandwidth group: one
+          // division per stage (same expression)
+          for (int j = 0; j < pp; ++j) {
             int cm = 255;
-            for (int r1 = 0; r1 < dp && cm; ++r1) {
-              const int d1 = nib(perm, (j * dp + r1) * tmp + s);
-              for (int r2 = r1 + 1; r2 < dp && cm; ++r2) {
-                const int cc = codeS[d1 * D + nib(perm, (j * dp + r2) * tmp + s)];
-                cm = cc < cm ? cc : cm;
+            for (int s = 0; s < tmp && cm; ++s)
+              for (int r1 = 0; r1 < dp && cm; ++r1) {
+                const int d1 = nib(perm, (j * dp + r1) * tmp + s);
+                for (int r2 = r1 + 1; r2 < dp && cm; ++r2) {
+                  const int cc = codeS[d1 * D + nib(perm, (j * dp + r2) * tmp + s)];
+                  cm = cc < cm ? cc : cm;
+                }
               }
-            }
             const double b = p.bwval[cm];
-            if (!(b > 0)) {
-              if (bad_group < 0) {
-                bad_group = g;
-                bad_value = b;
-              }
-            } else {
-              const double message = spar[j] * p.bpp / tmp;
-              worst = std_max(worst, 2.0 * (double)(dp - 1) * message / ((double)dp * b));
-            }
+            const double message = spar[j] * p.bpp / tmp;
+            worst = std_max(worst, 2.0 * (double)(dp - 1) * message / ((double)dp * b));
           }
+        } else if (dp != 1) {
+          for (int j = 0, g = 0; j < pp; ++j)
+            for (int s = 0; s < tmp; ++s, ++g) {
+              int cm = 255;
+              for (int r1 = 0; r1 < dp && cm; ++r1) {
+                const int d1 = nib(perm, (j * dp + r1) * tmp + s);
+                for (int r2 = r1 + 1; r2 < dp && cm; ++r2) {
+                  const int cc = codeS[d1 * D + nib(perm, (j * dp + r2) * tmp + s)];
+                  cm = cc < cm ? cc : cm;
+                }
+              }
+              const double b = p.bwval[cm];
+              if (!(b > 0)) {
+                if (bad_group < 0) {
+                  bad_group = g;
+                  bad_value = b;
+                }
+              } else {
+                const double message = spar[j] * p.bpp / tmp;
+                worst = std_max(worst, 2.0 * (double)(dp - 1) * message / ((double)dp * b));
+              }
+            }
         }
         if (bad_group >= 0) {
           fc = AMP_FAIL_ALLREDUCE_BANDWIDTH;
