@@ -157,7 +157,7 @@ struct EvalParams {
   const double* rsum_p;       // [(L+1)^2] parameter range sums
   uint8_t* repcuts;           // [n_rep][max_pp + 1] cuts per signature run (memoised runs)
   int32_t bw_positive;        // every link bandwidth > 0 (coded): no all-reduce group can fail
-  int32_t pad7;
+  int32_t fuse_light;         // thread K_est places items [n_dp, n_chunk) itself (pp <= 2)
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

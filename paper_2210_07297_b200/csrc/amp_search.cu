@@ -1201,6 +1201,9 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   // edge tables
   const bool est_thread = thread_mode && !want_sim && kk <= 32;
   ep.need_place_rows = !est_thread;
+  // K_est_t places the pp <= 2 tail of a segment list itself (never in K_dp)
+  ep.fuse_light = est_thread && segs != nullptr && d_given_cuts == nullptr &&
+                  std::getenv("AMP_NO_FUSE") == nullptr;
   ep.need_bwq = !(thread_mode && ctx->multi_b);
   ep.placep = nullptr;
   if (thread_mode) {

@@ -42,96 +42,121 @@ __device__ __forceinline__ uint32_t mod64_small(uint64_t r, uint32_t d, uint2 mt
 // ---------------------------------------------------------------------------
 // K_place (thread per candidate)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
-  __shared__ uint8_t codeS[kThreadMaxD * kThreadMaxD];
-  __shared__ uint64_t base_perm;
-  __shared__ uint2 magic[kThreadMaxD + 1];  // d -> (floor(2^32/d), 2^32 mod d)
+// Shared state of the thread kernels' placement step (per CTA).
+struct PlaceSmem {
+  uint8_t code[kThreadMaxD * kThreadMaxD];
+  uint64_t base_perm;
+  uint2 magic[kThreadMaxD + 1];  // d -> (floor(2^32/d), 2^32 mod d)
+};
+
+__device__ void place_smem_init(const EvalParams& p, PlaceSmem& S) {
   const int D = p.D;
-  for (int x = threadIdx.x; x < D * D; x += blockDim.x) codeS[x] = p.bwcode[x];
+  for (int x = threadIdx.x; x < D * D; x += blockDim.x) S.code[x] = p.bwcode[x];
   if (threadIdx.x >= 2 && threadIdx.x <= kThreadMaxD)
-    magic[threadIdx.x] = make_uint2((uint32_t)(0x100000000ull / threadIdx.x),
-                                    (uint32_t)(0x100000000ull % threadIdx.x));
+    S.magic[threadIdx.x] = make_uint2((uint32_t)(0x100000000ull / threadIdx.x),
+                                      (uint32_t)(0x100000000ull % threadIdx.x));
   if (threadIdx.x == 0) {
     uint64_t v = 0;
     for (int x = 0; x < D; ++x) v |= (uint64_t)p.base_order[x] << (4 * x);
-    base_perm = v;
+    S.base_perm = v;
   }
-  __syncthreads();
-  const int maxpp = p.max_pp;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < p.n_chunk; u += stride) {
-    uint64_t index, out, pl;
-    int c;
-    decode_item(p, p.t0 + u, index, out, c, pl);
-    const ClassDev cl = p.cls[c];
-    const PairDev pr = p.pairs[cl.pair];
-    const int pp = cl.pp, dp = cl.dp, tmp = cl.tmp;
-    int fc = 0, flayer = -1;
-    double fval = 0.0;
-    if (pp > p.L) {  // optimizer.cpp:149-152
-      fc = AMP_FAIL_PP_GT_L;
-    } else if (pr.fail_code) {  // segment_times: first failing layer
-      fc = pr.fail_code;
-      flayer = pr.fail_layer;
-      fval = pr.fail_value;
+}
+
+// K_place's work for chunk item u: decode, early failures, placement,
+// boundary codes.  `store`: write placement / codes / values for the later
+// kernels (K_dp, K_est); else only return them (fused light path).
+__device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& S, uint64_t u,
+                                          bool store, CandWork& w, uint64_t& perm, int& code0) {
+  const int D = p.D, maxpp = p.max_pp;
+  uint64_t index, out, pl;
+  int c;
+  decode_item(p, p.t0 + u, index, out, c, pl);
+  const ClassDev cl = p.cls[c];
+  const PairDev pr = p.pairs[cl.pair];
+  const int pp = cl.pp, dp = cl.dp, tmp = cl.tmp;
+  int fc = 0, flayer = -1;
+  double fval = 0.0;
+  code0 = 0;
+  perm = S.base_perm;
+  if (pp > p.L) {  // optimizer.cpp:149-152
+    fc = AMP_FAIL_PP_GT_L;
+  } else if (pr.fail_code) {  // segment_times: first failing layer
+    fc = pr.fail_code;
+    flayer = pr.fail_layer;
+    fval = pr.fail_value;
+  }
+  if (fc == 0) {
+    // ---- placement: heuristic order (placement.cpp:37-49); p >= 1:
+    //      Fisher-Yates driven by splitmix64(seed ^ p) ----------------------
+    if (p.given_place) {  // caller placement (anneal proposals, evaluate_placed)
+      const int32_t* g = p.given_place + (p.t0 + u) * D;
+      perm = 0;
+      for (int x = 0; x < D; ++x) perm |= (uint64_t)g[x] << (4 * x);
+    } else if (pl != 0) {
+      uint64_t r = splitmix64(p.seed ^ pl);
+      for (int kk = D - 1; kk >= 1; --kk) {
+        const int jj = (int)mod64_small(r, (uint32_t)kk + 1u, S.magic[kk + 1]);
+        const uint64_t a = (perm >> (4 * kk)) & 0xf, b = (perm >> (4 * jj)) & 0xf;
+        perm &= ~((0xfull << (4 * kk)) | (0xfull << (4 * jj)));
+        perm |= (b << (4 * kk)) | (a << (4 * jj));
+        r = splitmix64(r);
+      }
     }
-    if (fc == 0) {
-      // ---- placement: heuristic order (placement.cpp:37-49); p >= 1:
-      //      Fisher-Yates driven by splitmix64(seed ^ p) --------------------
-      uint64_t perm = base_perm;
-      if (p.given_place) {  // caller placement (anneal proposals, evaluate_placed)
-        const int32_t* g = p.given_place + (p.t0 + u) * D;
-        perm = 0;
-        for (int x = 0; x < D; ++x) perm |= (uint64_t)g[x] << (4 * x);
-      } else if (pl != 0) {
-        uint64_t r = splitmix64(p.seed ^ pl);
-        for (int kk = D - 1; kk >= 1; --kk) {
-          const int jj = (int)mod64_small(r, (uint32_t)kk + 1u, magic[kk + 1]);
-          const uint64_t a = (perm >> (4 * kk)) & 0xf, b = (perm >> (4 * jj)) & 0xf;
-          perm &= ~((0xfull << (4 * kk)) | (0xfull << (4 * jj)));
-          perm |= (b << (4 * kk)) | (a << (4 * jj));
-          r = splitmix64(r);
+    if (store && p.placep) p.placep[u] = perm;
+    if (store && p.need_place_rows) {
+      int32_t* prow = p.placeb + u * D;
+      for (int x = 0; x < D; ++x) prow[x] = nib(perm, x);
+    }
+    // ---- stage-boundary bandwidths: min over all replicas and shards
+    //      (cost_model.cpp:164-174), as codes; the first invalid boundary
+    //      fails like p2p_time in the DP's edge function -----------------
+    int first_bad = -1;
+    double bad_val = 0.0;
+    for (int q = 0; q < pp - 1; ++q) {
+      int cm = 255;  // (code 0 is the smallest bandwidth: nothing can go lower)
+      for (int r = 0; r < dp && cm; ++r)
+        for (int s = 0; s < tmp && cm; ++s) {
+          const int cc = S.code[nib(perm, (q * dp + r) * tmp + s) * D +
+                                nib(perm, ((q + 1) * dp + r) * tmp + s)];
+          cm = cc < cm ? cc : cm;
         }
-      }
-      if (p.placep) p.placep[u] = perm;
-      if (p.need_place_rows) {
-        int32_t* prow = p.placeb + u * D;
-        for (int x = 0; x < D; ++x) prow[x] = nib(perm, x);
-      }
-      // ---- stage-boundary bandwidths: min over all replicas and shards
-      //      (cost_model.cpp:164-174), as codes; the first invalid boundary
-      //      fails like p2p_time in the DP's edge function ---------------
-      int first_bad = -1;
-      double bad_val = 0.0;
-      for (int q = 0; q < pp - 1; ++q) {
-        int cm = 255;  // (code 0 is the smallest bandwidth: nothing can go lower)
-        for (int r = 0; r < dp && cm; ++r)
-          for (int s = 0; s < tmp && cm; ++s) {
-            const int cc = codeS[nib(perm, (q * dp + r) * tmp + s) * D +
-                                 nib(perm, ((q + 1) * dp + r) * tmp + s)];
-            cm = cc < cm ? cc : cm;
-          }
-        const double b = p.bwval[cm];
+      const double b = p.bwval[cm];
+      if (q == 0) code0 = cm;
+      if (store) {
         p.bwcb[u * maxpp + q] = (uint8_t)cm;
         if (p.need_bwq) p.bwqb[u * maxpp + q] = b;
-        if (first_bad < 0 && !(b > 0)) {
-          first_bad = q;
-          bad_val = b;
-        }
       }
-      if (first_bad >= 0) {
-        fc = AMP_FAIL_P2P_BANDWIDTH;
-        fval = bad_val;
+      if (first_bad < 0 && !(b > 0)) {
+        first_bad = q;
+        bad_val = b;
       }
     }
+    if (first_bad >= 0) {
+      fc = AMP_FAIL_P2P_BANDWIDTH;
+      fval = bad_val;
+    }
+  }
+  w.index = index;
+  w.out = out;
+  w.cls = c;
+  w.fail_code = fc;
+  w.fail_layer = flayer;
+  w.pad = 0;
+  w.fail_value = fval;
+}
+
+__global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
+  __shared__ PlaceSmem S;
+  place_smem_init(p, S);
+  __syncthreads();
+  // fused light path: K_est_t places the pp <= 2 tail itself
+  const uint64_t n = p.fuse_light ? p.n_dp : p.n_chunk;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
     CandWork w;
-    w.index = index;
-    w.out = out;
-    w.cls = c;
-    w.fail_code = fc;
-    w.fail_layer = flayer;
-    w.pad = 0;
-    w.fail_value = fval;
+    uint64_t perm;
+    int code0;
+    place_one(p, S, u, true, w, perm, code0);
     p.work[u] = w;
   }
 }
@@ -142,7 +167,8 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
 constexpr int kEstTWarps = 8;
 
 __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
-  __shared__ uint8_t codeS[kThreadMaxD * kThreadMaxD];
+  __shared__ PlaceSmem PS;
+  const uint8_t* codeS = PS.code;
   __shared__ int n_top;
   __shared__ amp_record stage_rec[kEstTWarps][32];  // records handed to the warp leader
   __shared__ amp_record wtop[kEstTWarps][32];       // per-warp top-k (no lock)
@@ -151,7 +177,7 @@ __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
   const int L = p.L, LP = L + 1;
   amp_record* const gtop = p.cta_topk + (size_t)blockIdx.x * p.k;
   amp_record* mytop = p.k <= 32 ? topS : gtop;
-  for (int x = threadIdx.x; x < D * D; x += blockDim.x) codeS[x] = p.bwcode[x];
+  place_smem_init(p, PS);
   if (threadIdx.x == 0) {
     n_top = 0;
     if (!p.first_chunk) {  // CTA lists persist across chunks
@@ -178,16 +204,22 @@ __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
     int pp = 0, best_r = -1;
     bool ok = false;
     if (live) {
-      const CandWork w = p.work[u];
+      // fused light path: the pp <= 2 tail (never in K_dp) is placed here
+      const bool fused = p.fuse_light && u >= p.n_dp;
+      CandWork w;
+      uint64_t perm = 0;
+      int code0 = 0;
+      if (fused) place_one(p, PS, u, false, w, perm, code0);
+      else w = p.work[u];
       const ClassDev cl = p.cls[w.cls];
       pp = cl.pp;
       const int dp = cl.dp, tmp = cl.tmp, mbs = cl.mbs;
       int fc = w.fail_code;
       double fval = w.fail_value;
       double pipeline = CUDART_NAN, dpsync = CUDART_NAN;
-      uint64_t perm = 0;
       if (fc == 0) {
-        if (p.placep) {
+        if (fused) {
+        } else if (p.placep) {
           perm = p.placep[u];
         } else {
           const int32_t* PL = p.placeb + u * D;
@@ -205,14 +237,15 @@ __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
           // the 2-stage DP depends on (class, boundary-0 code) only: tabulated
           // once per context by k_cut2_table (the same operations)
           cuts[0] = 0;
-          cuts[1] = p.cut2tab[(size_t)w.cls * p.n_codes + p.bwcb[u * maxpp]];
+          cuts[1] = p.cut2tab[(size_t)w.cls * p.n_codes + (fused ? code0 : p.bwcb[u * maxpp])];
           cuts[2] = L;
         } else if (pp == 2) {
           const double* Pf = p.prefix + (size_t)cl.pair * LP;
           const double* Dm = p.domain + (size_t)cl.pair * p.nv_stride;
           const uint16_t* sg = p.seg + (size_t)cl.pair * LP * LP;
           const double g1 = (double)(cl.gas - 1);
-          const double* qt = p.qtab + ((size_t)w.cls * p.n_codes + p.bwcb[u * maxpp]) * L;
+          const double* qt =
+              p.qtab + ((size_t)w.cls * p.n_codes + (fused ? code0 : p.bwcb[u * maxpp])) * L;
           const double dm0 = Dm[0], PLL = Pf[L], P0 = Pf[0];
           double best = CUDART_INF;
           int bc = -1;
