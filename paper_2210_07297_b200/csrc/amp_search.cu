@@ -1235,7 +1235,10 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     const int place_grid = (int)std::min<uint64_t>((warps + 7) / 8, (uint64_t)ctx->sms * 16);
     if (thread_mode) {
       const int tg = (int)std::min<uint64_t>((ep.n_chunk + 255) / 256, (uint64_t)ctx->sms * 16);
-      k_place_t<<<tg, 256, 0, ctx->stream>>>(ep);
+      if (ctx->D == 16)
+        k_place_t<16><<<tg, 256, 0, ctx->stream>>>(ep);
+      else
+        k_place_t<0><<<tg, 256, 0, ctx->stream>>>(ep);
     } else {
       k_place<<<place_grid, 256, place_smem, ctx->stream>>>(ep);
     }
@@ -1300,8 +1303,10 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
       ctx->launches += 1;
     }
     CK(cudaEventRecord(ev[2], ctx->stream));
-    if (est_thread)
-      k_est_t<<<ctx->est_ctas, kEstTWarps * 32, 0, ctx->stream>>>(ep);
+    if (est_thread && ctx->D == 16)
+      k_est_t<16><<<ctx->est_ctas, kEstTWarps * 32, 0, ctx->stream>>>(ep);
+    else if (est_thread)
+      k_est_t<0><<<ctx->est_ctas, kEstTWarps * 32, 0, ctx->stream>>>(ep);
     else
       k_est<<<ctx->est_ctas, kEstWarps * 32, est_smem, ctx->stream>>>(ep);
     CK(cudaGetLastError());

@@ -65,9 +65,12 @@ __device__ void place_smem_init(const EvalParams& p, PlaceSmem& S) {
 // K_place's work for chunk item u: decode, early failures, placement,
 // boundary codes.  `store`: write placement / codes / values for the later
 // kernels (K_dp, K_est); else only return them (fused light path).
+// DT > 0: the device count as a compile-time constant (the Fisher-Yates
+// loop unrolls: constant shifts, constant-divisor modulo).
+template <int DT>
 __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& S, uint64_t u,
                                           bool store, CandWork& w, uint64_t& perm, int& code0) {
-  const int D = p.D, maxpp = p.max_pp;
+  const int D = DT > 0 ? DT : p.D, maxpp = p.max_pp;
   uint64_t index, out, pl;
   int c;
   decode_item(p, p.t0 + u, index, out, c, pl);
@@ -94,12 +97,25 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
       for (int x = 0; x < D; ++x) perm |= (uint64_t)g[x] << (4 * x);
     } else if (pl != 0) {
       uint64_t r = splitmix64(p.seed ^ pl);
-      for (int kk = D - 1; kk >= 1; --kk) {
-        const int jj = (int)mod64_small(r, (uint32_t)kk + 1u, S.magic[kk + 1]);
-        const uint64_t a = (perm >> (4 * kk)) & 0xf, b = (perm >> (4 * jj)) & 0xf;
-        perm &= ~((0xfull << (4 * kk)) | (0xfull << (4 * jj)));
-        perm |= (b << (4 * kk)) | (a << (4 * jj));
-        r = splitmix64(r);
+      if (DT > 0) {
+#pragma unroll
+        for (int kk = DT - 1; kk >= 1; --kk) {
+          const uint32_t d = (uint32_t)kk + 1u;  // constant: the compiler's divide-by-constant
+          const uint32_t t32 = (uint32_t)(0x100000000ull % d);
+          const uint32_t jj = (uint32_t)((((uint32_t)(r >> 32) % d) * t32 + ((uint32_t)r % d)) % d);
+          const uint64_t a = (perm >> (4 * kk)) & 0xf, b = (perm >> (4 * jj)) & 0xf;
+          perm &= ~((0xfull << (4 * kk)) | (0xfull << (4 * jj)));
+          perm |= (b << (4 * kk)) | (a << (4 * jj));
+          r = splitmix64(r);
+        }
+      } else {
+        for (int kk = D - 1; kk >= 1; --kk) {
+          const int jj = (int)mod64_small(r, (uint32_t)kk + 1u, S.magic[kk + 1]);
+          const uint64_t a = (perm >> (4 * kk)) & 0xf, b = (perm >> (4 * jj)) & 0xf;
+          perm &= ~((0xfull << (4 * kk)) | (0xfull << (4 * jj)));
+          perm |= (b << (4 * kk)) | (a << (4 * jj));
+          r = splitmix64(r);
+        }
       }
     }
     if (store && p.placep) p.placep[u] = perm;
@@ -145,6 +161,7 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
   w.fail_value = fval;
 }
 
+template <int DT>
 __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
   __shared__ PlaceSmem S;
   place_smem_init(p, S);
@@ -156,7 +173,7 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
     CandWork w;
     uint64_t perm;
     int code0;
-    place_one(p, S, u, true, w, perm, code0);
+    place_one<DT>(p, S, u, true, w, perm, code0);
     p.work[u] = w;
   }
 }
@@ -166,6 +183,7 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
 // ---------------------------------------------------------------------------
 constexpr int kEstTWarps = 8;
 
+template <int DT>
 __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
   __shared__ PlaceSmem PS;
   const uint8_t* codeS = PS.code;
@@ -209,7 +227,7 @@ __global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
       CandWork w;
       uint64_t perm = 0;
       int code0 = 0;
-      if (fused) place_one(p, PS, u, false, w, perm, code0);
+      if (fused) place_one<DT>(p, PS, u, false, w, perm, code0);
       else w = p.work[u];
       const ClassDev cl = p.cls[w.cls];
       pp = cl.pp;
