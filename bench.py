@@ -37,6 +37,9 @@ METRIC = "candidate strategies/sec"
 # ncu --set full of one k_dp_multi launch (profiles/r1b_k_dp_multi_ncu.txt):
 # dram__bytes_read.sum + dram__bytes_write.sum / candidates of that launch
 TRAFFIC_BYTES_PER_DP_ITEM = 66.5  # 66.54 MB over the 1,000,000 items of launch 3
+# ncu instructions / DRAM bytes per item of the per-candidate kernels on this
+# workload (tools/gpu_round.sh -> tools/summarize_profiles.py)
+KERNEL_COUNTS = os.path.join(ROOT, "profiles", "r1e_kernel_counts.json")
 UNIT = "candidates/s"
 
 
@@ -334,6 +337,37 @@ def our_arm(args):
         dense = dense_leg(enc, local)
         per_cand = per_candidate_leg(enc, local, P_, n_total)
 
+    # ---- rooflines of the three kernels of a step ---------------------------
+    #   k_dp: FP64 pipe (algorithmic ops of the DP instances solved);
+    #   k_est / k_place: instruction issue (thread per candidate, integer and
+    #   FP64 mix) — ncu instructions per item x items / measured time, against
+    #   148 SMs x 4 warp-instructions/clk at the sampled SM clock
+    rooflines = {"k_dp": {"bound": "fp64", "achieved": achieved, "peak": peak_t,
+                          "unit": "TFLOP/s", "frac": achieved / peak_t, "ms_per_step": dp_ms}}
+    try:
+        with open(KERNEL_COUNTS) as f:
+            kc = json.load(f)
+    except OSError:
+        kc = {}
+    import torch
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    csum = clk.summary() if hasattr(clk, "summary") else {}
+    mhz = csum.get("sm_mhz") or csum.get("sm_max_mhz") or 1965.0
+    issue_peak = sms * 4 * mhz * 1e6
+    # K_place_t covers the pp >= 3 classes (the pp <= 2 tail is placed in K_est)
+    cls_list = s.classes()
+    heavy = sum(1 for c in cls_list if c[0] >= 3) * (n_mine // len(cls_list))
+    for name, ms, items in (("k_est", est_ms, n_mine), ("k_place", place_ms, heavy)):
+        c = kc.get(name + "_t")
+        if not c or not items:
+            continue
+        ach = c["warp_inst_per_item"] * items / (ms * 1e-3)
+        rooflines[name] = {"bound": "issue", "achieved": ach, "peak": issue_peak,
+                           "unit": "warp-inst/s", "frac": ach / issue_peak, "ms_per_step": ms,
+                           "traffic": c["dram_bytes_per_item"] * items / max(1, st["dp_launches"]),
+                           "counts": os.path.relpath(KERNEL_COUNTS, ROOT)}
+    dominant = max(("k_dp", dp_ms), ("k_est", est_ms), ("k_place", place_ms), key=lambda t: t[1])[0]
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -347,26 +381,24 @@ def our_arm(args):
                        "parallelism": f"per-class placement-slice shards x{world} "
                                       "(amp_search_run_device_shard), NCCL all-gather of the "
                                       "k-record top-k + device merge"},
-            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s",
-                         "frac": achieved / peak_t,
-                         "traffic": TRAFFIC_BYTES_PER_DP_ITEM * st["dp_items"] / max(1, st["dp_launches"]),
-                         "traffic_note": "dram read+write bytes per k_dp launch: ncu per-item figure "
-                                         "(profiles/r1b_k_dp_multi_ncu.txt) x items per launch; the "
-                                         "kernel is FP64/issue-bound, its tables are L2/L1-resident",
-                         "kernel": f"k_dp_multi<{st['dp_group']}> (pruned layer-partition DP, "
-                                   f"{st['dp_group']} candidates of one class per CTA group)",
-                         "fp64_ops_def": "7 per executed inner iteration (SURVEY.md 8(d)) over the "
-                                         "pruned program's iterations of the DP instances "
-                                         "actually solved (memoised by signature: one per "
-                                         "distinct (class, boundary-bandwidth codes))",
-                         "dp_memoisation": {"candidates": n_total,
-                                            "dp_instances_solved": st["dp_instances"]},
-                         "dp_items_per_step": st["dp_items"], "dp_launches_per_step": st["dp_launches"],
-                         "kernel_ms_per_step": kern_ms,
-                         "pipeline_ms_per_step": {"k_place": place_ms, "k_dp": dp_ms, "k_est": est_ms},
-                         "fp64_ops_per_step": st["fp64_ops"], "dp_inner_per_step": st["dp_inner"],
-                         "peak_source": "measured live: amp_fp64_peak DADD throughput (no FP64 entry "
-                                        "in MEASURED_PEAKS.json)"},
+            "roofline": dict(rooflines[dominant], kernel={
+                "k_est": "k_est_t (thread per candidate: pp<=2 placement + estimate, "
+                         "replica edges, dpsync, CTA top-k)",
+                "k_place": "k_place_t (thread per candidate: Fisher-Yates placement, "
+                           "boundary bandwidth codes)",
+                "k_dp": "memoised + prefix-shared layer-partition DP (dedup sort, trie stages)",
+            }[dominant], dominant_of=["k_place", "k_dp", "k_est"]),
+            "rooflines": rooflines,
+            "dp_detail": {
+                "traffic": TRAFFIC_BYTES_PER_DP_ITEM * st["dp_items"] / max(1, st["dp_launches"]),
+                "fp64_ops_def": "7 per executed inner iteration (SURVEY.md 8(d)) over the pruned "
+                                "program's iterations actually executed (memoised by signature, "
+                                "stage tables shared by code prefix)",
+                "dp_memoisation": {"candidates": n_total, "dp_instances_solved": st["dp_instances"]},
+                "pipeline_ms_per_step": {"k_place": place_ms, "k_dp": dp_ms, "k_est": est_ms},
+                "fp64_ops_per_step": st["fp64_ops"], "dp_inner_per_step": st["dp_inner"],
+                "peak_source": "measured live: amp_fp64_peak DADD throughput (no FP64 entry "
+                               "in MEASURED_PEAKS.json)"},
             "gpu_launches": int(args.steps * (st["launches"] + (1 if distributed else 0))),
             "best": {"index": int(top[0]["index"]), "total": float(top[0]["total"]),
                      "degrees": [int(top[0]["pp"]), int(top[0]["dp"]), int(top[0]["tmp"])],

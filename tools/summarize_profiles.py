@@ -90,3 +90,34 @@ with open(os.path.join(out, f"{tag}_{kname_short}_ncu.txt"), "w") as f:
     f.write("\n## hottest source lines (tools/ncu_lines.py)\n")
     f.write(lines_txt)
 print("wrote", tag)
+
+# ---- per-candidate kernels: instructions and DRAM bytes per item ----------
+# (tools/gpu_round.sh's pe_full capture: the first chunk of the measured run
+#  of prof_eval.py 100000000 — 67,108,864 items, of which the 45,714,304 of
+#  the pp >= 3 classes go through K_place; K_est covers the whole chunk)
+pe = os.path.join(src, "pe_full_raw.csv")
+if os.path.exists(pe):
+    import json
+    raw = [r for r in csv.reader(open(pe)) if r and not r[0].startswith("==")]
+    hdr, unit = raw[0], raw[1]
+    n_cls, P = 70, -(-100_000_000 // 70)
+    chunk = 64 << 20
+    heavy = min(chunk, 32 * P)
+    items = {"k_place_t": heavy, "k_est_t": chunk}
+    out_j = {"source": f"profiles/{tag}_kernel_counts.json from ncu --set full (tools/gpu_round.sh)",
+             "workload": "hetero_cluster sweep, 100M candidates, first 64M-item chunk"}
+    for row in raw[2:]:
+        d = dict(zip(hdr, row))
+        name = d["Kernel Name"].split("(")[0].split("<")[0].split("::")[-1].split()[-1]
+        n = items.get(name)
+        if not n:
+            continue
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+        rd = float(d["dram__bytes_read.sum"]) * scale[unit[hdr.index("dram__bytes_read.sum")]]
+        wr = float(d["dram__bytes_write.sum"]) * scale[unit[hdr.index("dram__bytes_write.sum")]]
+        out_j[name] = {"items": n, "warp_inst_per_item": float(d["smsp__inst_executed.sum"]) / n,
+                       "dram_bytes_per_item": (rd + wr) / n,
+                       "duration_ms": float(d["gpu__time_duration.sum"])}
+    with open(os.path.join(out, f"{tag}_kernel_counts.json"), "w") as f:
+        json.dump(out_j, f, indent=1)
+    print("kernel counts", out_j)
