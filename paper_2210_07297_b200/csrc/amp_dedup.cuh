@@ -83,3 +83,107 @@ __global__ void k_dedup_scatter(DedupParams p) {
 }
 
 }  // namespace amp
+
+namespace amp {
+
+// ---- hash-based signature runs (replaces the full radix sort) -------------
+//
+// Each heavy item inserts its key into an open-addressing table (linear
+// probing, load <= 1/2): an item reads the slot first and only the first
+// writer of a key CASes it in, so the many items of a hot signature cost one
+// L2 read each.  The first writer appends the slot to the list of distinct
+// keys.  Only those (a few hundred thousand) are then sorted: the run order
+// (class, c_0, c_1, ...) that K_dp / the trie need.  Which item becomes a
+// signature's representative does not matter: all its items have identical
+// DP inputs.
+constexpr uint64_t kHashEmpty = ~0ull;
+
+struct HashParams {
+  const CandWork* work;
+  const ClassDev* cls;
+  const uint8_t* bwcb;
+  uint64_t n;              // heavy items
+  int32_t max_pp, code_bits;
+  uint64_t mask;           // table size - 1
+  unsigned long long* tkey;  // [T] keys (kHashEmpty = free)
+  uint32_t* tval;          // [T] first item, then run index
+  uint32_t* slot_of;       // [n] slot of every item (~0u: no signature)
+  uint32_t* uniq;          // [n] slots of the distinct keys
+  unsigned long long* n_uniq;
+  // after the host sorted the distinct keys
+  const uint64_t* skeys;   // [n_uniq] sorted keys
+  const uint32_t* sslots;  // [n_uniq] their slots
+  uint64_t* rep_key;       // [n_uniq] (NULL: not needed)
+  uint32_t* rep_list;      // [n_uniq] representative item of each run
+  uint32_t* rep_of;        // [n] run of every item
+  uint64_t* n_rep;         // device count of runs
+};
+
+__device__ __forceinline__ uint64_t sig_key(const CandWork& w, const ClassDev* cls,
+                                            const uint8_t* codes, int max_pp, int cb) {
+  if (w.fail_code != 0) return kHashEmpty;
+  const ClassDev cl = cls[w.cls];
+  if (cl.pp < 3) return kHashEmpty;
+  uint64_t key = (uint64_t)w.cls;
+  for (int q = 0; q < max_pp - 1; ++q) key = (key << cb) | (q < cl.pp - 1 ? (uint64_t)codes[q] : 0ull);
+  return key;
+}
+
+__global__ void k_hash_insert(HashParams p) {
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < p.n;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = sig_key(p.work[u], p.cls, p.bwcb + u * p.max_pp, p.max_pp, p.code_bits);
+    uint32_t slot = ~0u;
+    if (key != kHashEmpty) {
+      uint64_t h = splitmix64(key) & p.mask;
+      for (;;) {
+        const unsigned long long k = *(volatile unsigned long long*)&p.tkey[h];
+        if (k == key) break;
+        if (k == kHashEmpty) {
+          const unsigned long long old = atomicCAS(&p.tkey[h], kHashEmpty, key);
+          if (old == kHashEmpty) {  // first writer of this key
+            p.tval[h] = (uint32_t)u;
+            p.uniq[atomicAdd(p.n_uniq, 1ull)] = (uint32_t)h;
+            break;
+          }
+          if (old == key) break;
+        }
+        h = (h + 1) & p.mask;
+      }
+      slot = (uint32_t)h;
+    }
+    p.slot_of[u] = slot;
+  }
+}
+
+__global__ void k_hash_gather(HashParams p, uint64_t* keys, uint32_t* slots) {
+  const uint64_t n = *p.n_uniq;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = p.uniq[i];
+    keys[i] = p.tkey[s];
+    slots[i] = s;
+  }
+}
+
+__global__ void k_hash_runs(HashParams p) {
+  const uint64_t n = *p.n_uniq;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = p.sslots[r];
+    p.rep_list[r] = p.tval[s];
+    if (p.rep_key) p.rep_key[r] = p.skeys[r];
+    p.tval[s] = (uint32_t)r;  // slot -> run
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *p.n_rep = n;
+}
+
+__global__ void k_hash_scatter(HashParams p) {
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < p.n;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = p.slot_of[u];
+    p.rep_of[u] = s == ~0u ? 0u : p.tval[s];
+  }
+}
+
+}  // namespace amp

@@ -166,6 +166,7 @@ struct amp_ctx {
   int code_bits = 0, key_bits = 0;
   DevBuf dd_keys, dd_vals, dd_skeys, dd_svals, dd_flags, dd_runid, dd_rep_list, dd_rep_of;
   DevBuf dd_nrep, dd_temp, dd_counters, prog_inner_d, dd_repcuts;
+  DevBuf dd_tkey, dd_tval, dd_slot, dd_uniq, dd_nuniq;  // hash dedup
   size_t dd_temp_bytes = 0;
   // DP shared across signature prefixes (amp_trie.cuh)
   bool trie = false;
@@ -1251,38 +1252,89 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     ep.repcuts = nullptr;
     bool skip_dp = false;
     if (ctx->dedup && !d_given_cuts && ep.n_dp > 0) {
-      // ---- memoisation: sort signatures, one DP per distinct key --------
+      // ---- memoisation: one DP per distinct signature ---------------------
+      const int g = (int)std::min<uint64_t>((ep.n_dp + 255) / 256, (uint64_t)ctx->sms * 8);
       DedupParams dp{};
-      dp.work = ep.work;
-      dp.cls = ep.cls;
-      dp.bwcb = ep.bwcb;
-      dp.n = ep.n_dp;
-      dp.max_pp = ctx->max_pp;
-      dp.code_bits = ctx->code_bits;
-      dp.keys = ctx->dd_keys.as<uint64_t>();
-      dp.vals = ctx->dd_vals.as<uint32_t>();
-      dp.skeys = ctx->dd_skeys.as<uint64_t>();
-      dp.svals = ctx->dd_svals.as<uint32_t>();
-      dp.flags = ctx->dd_flags.as<uint32_t>();
-      dp.runid = ctx->dd_runid.as<uint32_t>();
       dp.rep_list = ctx->dd_rep_list.as<uint32_t>();
       dp.rep_of = ctx->dd_rep_of.as<uint32_t>();
       dp.n_rep = ctx->dd_nrep.as<uint64_t>();
-      dp.rep_key = ctx->trie ? ctx->dd_rep_key.as<uint64_t>() : nullptr;
-      const int g = (int)std::min<uint64_t>((ep.n_dp + 255) / 256, (uint64_t)ctx->sms * 8);
-      k_dedup_keys<<<g, 256, 0, ctx->stream>>>(dp);
-      size_t tb = ctx->dd_temp_bytes;
-      CK(cub::DeviceRadixSort::SortPairs(ctx->dd_temp.p, tb, dp.keys, ctx->dd_skeys.as<uint64_t>(),
-                                         dp.vals, ctx->dd_svals.as<uint32_t>(), (int)ep.n_dp, 0,
-                                         ctx->key_bits, ctx->stream));
-      k_dedup_heads<<<g, 256, 0, ctx->stream>>>(dp);
-      tb = ctx->dd_temp_bytes;
-      CK(cub::DeviceScan::InclusiveSum(ctx->dd_temp.p, tb, dp.flags, ctx->dd_runid.as<uint32_t>(),
-                                       (int)ep.n_dp, ctx->stream));
-      k_dedup_reps<<<g, 256, 0, ctx->stream>>>(dp);
-      k_dedup_scatter<<<g, 256, 0, ctx->stream>>>(dp);
-      CK(cudaGetLastError());
-      ctx->launches += 6;  // 4 kernels + 2 CUB passes (sort, scan) of ours
+      if (std::getenv("AMP_DEDUP_SORT")) {
+        // full radix sort of the item keys (comparison path)
+        dp.work = ep.work;
+        dp.cls = ep.cls;
+        dp.bwcb = ep.bwcb;
+        dp.n = ep.n_dp;
+        dp.max_pp = ctx->max_pp;
+        dp.code_bits = ctx->code_bits;
+        dp.keys = ctx->dd_keys.as<uint64_t>();
+        dp.vals = ctx->dd_vals.as<uint32_t>();
+        dp.skeys = ctx->dd_skeys.as<uint64_t>();
+        dp.svals = ctx->dd_svals.as<uint32_t>();
+        dp.flags = ctx->dd_flags.as<uint32_t>();
+        dp.runid = ctx->dd_runid.as<uint32_t>();
+        dp.rep_key = ctx->trie ? ctx->dd_rep_key.as<uint64_t>() : nullptr;
+        k_dedup_keys<<<g, 256, 0, ctx->stream>>>(dp);
+        size_t tb = ctx->dd_temp_bytes;
+        CK(cub::DeviceRadixSort::SortPairs(ctx->dd_temp.p, tb, dp.keys, ctx->dd_skeys.as<uint64_t>(),
+                                           dp.vals, ctx->dd_svals.as<uint32_t>(), (int)ep.n_dp, 0,
+                                           ctx->key_bits, ctx->stream));
+        k_dedup_heads<<<g, 256, 0, ctx->stream>>>(dp);
+        tb = ctx->dd_temp_bytes;
+        CK(cub::DeviceScan::InclusiveSum(ctx->dd_temp.p, tb, dp.flags, ctx->dd_runid.as<uint32_t>(),
+                                         (int)ep.n_dp, ctx->stream));
+        k_dedup_reps<<<g, 256, 0, ctx->stream>>>(dp);
+        k_dedup_scatter<<<g, 256, 0, ctx->stream>>>(dp);
+        CK(cudaGetLastError());
+        ctx->launches += 6;
+      } else {
+        // hash the item keys (amp_dedup.cuh), sort only the distinct ones
+        uint64_t T = 1024;
+        while (T < 2 * ep.n_dp) T <<= 1;
+        CK(ctx->dd_tkey.ensure(sizeof(uint64_t) * T));
+        CK(ctx->dd_tval.ensure(sizeof(uint32_t) * T));
+        CK(ctx->dd_slot.ensure(sizeof(uint32_t) * C));
+        CK(ctx->dd_uniq.ensure(sizeof(uint32_t) * C));
+        CK(ctx->dd_nuniq.ensure(sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(ctx->dd_tkey.p, 0xff, sizeof(uint64_t) * T, ctx->stream));
+        CK(cudaMemsetAsync(ctx->dd_nuniq.p, 0, sizeof(unsigned long long), ctx->stream));
+        HashParams hp{};
+        hp.work = ep.work;
+        hp.cls = ep.cls;
+        hp.bwcb = ep.bwcb;
+        hp.n = ep.n_dp;
+        hp.max_pp = ctx->max_pp;
+        hp.code_bits = ctx->code_bits;
+        hp.mask = T - 1;
+        hp.tkey = ctx->dd_tkey.as<unsigned long long>();
+        hp.tval = ctx->dd_tval.as<uint32_t>();
+        hp.slot_of = ctx->dd_slot.as<uint32_t>();
+        hp.uniq = ctx->dd_uniq.as<uint32_t>();
+        hp.n_uniq = ctx->dd_nuniq.as<unsigned long long>();
+        hp.skeys = ctx->dd_skeys.as<uint64_t>();
+        hp.sslots = ctx->dd_svals.as<uint32_t>();
+        hp.rep_key = ctx->trie ? ctx->dd_rep_key.as<uint64_t>() : nullptr;
+        hp.rep_list = dp.rep_list;
+        hp.rep_of = dp.rep_of;
+        hp.n_rep = dp.n_rep;
+        k_hash_insert<<<g, 256, 0, ctx->stream>>>(hp);
+        unsigned long long nu = 0;
+        CK(cudaMemcpyAsync(&nu, ctx->dd_nuniq.p, sizeof nu, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        const int gu = (int)std::min<uint64_t>((nu + 255) / 256 + 1, (uint64_t)ctx->sms * 8);
+        k_hash_gather<<<gu, 256, 0, ctx->stream>>>(hp, ctx->dd_keys.as<uint64_t>(),
+                                                    ctx->dd_vals.as<uint32_t>());
+        if (nu > 0) {
+          size_t tb = ctx->dd_temp_bytes;
+          CK(cub::DeviceRadixSort::SortPairs(ctx->dd_temp.p, tb, ctx->dd_keys.as<uint64_t>(),
+                                             ctx->dd_skeys.as<uint64_t>(), ctx->dd_vals.as<uint32_t>(),
+                                             ctx->dd_svals.as<uint32_t>(), (int)nu, 0, ctx->key_bits,
+                                             ctx->stream));
+        }
+        k_hash_runs<<<gu, 256, 0, ctx->stream>>>(hp);
+        k_hash_scatter<<<g, 256, 0, ctx->stream>>>(hp);
+        CK(cudaGetLastError());
+        ctx->launches += 5;
+      }
       ep.rep_list = dp.rep_list;
       ep.rep_of = dp.rep_of;
       ep.n_rep = dp.n_rep;
