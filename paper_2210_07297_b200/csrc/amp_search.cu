@@ -795,7 +795,8 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   if (ctx->max_ctas_cfg > 0) n_ctas = std::min(n_ctas, ctx->max_ctas_cfg);
   ctx->n_ctas = n_ctas;
   ctx->sms = prop.multiProcessorCount;
-  ctx->est_ctas = prop.multiProcessorCount * 3;  // 3 x 8 estimate warps per SM (launch bounds)
+  const char* ec = std::getenv("AMP_EST_CTAS_PER_SM");
+  ctx->est_ctas = prop.multiProcessorCount * (ec ? std::atoi(ec) : 4);  // 8-warp estimate CTAs per SM
   // chunk size: keep the per-chunk buffers within ~256 MB
   const size_t per_item = sizeof(CandWork) + sizeof(int32_t) * D + sizeof(double) * ctx->max_pp +
                           (ctx->max_pp + 1);

@@ -184,7 +184,10 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
 constexpr int kEstTWarps = 8;
 
 template <int DT>
-__global__ void __launch_bounds__(kEstTWarps * 32) k_est_t(EvalParams p) {
+#ifndef AMP_EST_MINB
+#define AMP_EST_MINB 4
+#endif
+__global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalParams p) {
   __shared__ PlaceSmem PS;
   const uint8_t* codeS = PS.code;
   __shared__ int n_top;
