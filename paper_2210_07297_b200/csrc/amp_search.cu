@@ -17,6 +17,7 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <unordered_set>
 #include <vector>
 
 #include "amp_common.cuh"
@@ -494,16 +495,36 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   // (used by K_place and the K_dp edge tables; disabled with NaN links or
   // more than 255 distinct values)
   {
-    std::vector<double> vals(bw.begin(), bw.end());
+    // distinct values: a hash set (|D|^2 entries, few distinct), then sort
+    std::vector<double> vals;
     bool nan = false;
-    for (double v : vals) nan |= std::isnan(v);
+    {
+      std::unordered_set<uint64_t> seen;
+      for (double v : bw) {
+        if (std::isnan(v)) {
+          nan = true;
+          break;
+        }
+        uint64_t bits;
+        std::memcpy(&bits, &v, sizeof bits);
+        if (v == 0.0) bits = 0;  // +0 / -0 are one value
+        if (seen.insert(bits).second) vals.push_back(v == 0.0 ? 0.0 : v);
+        if (vals.size() > 255) break;  // codes disabled anyway
+      }
+    }
     std::sort(vals.begin(), vals.end());
-    vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
     ctx->n_codes = 0;
     if (!nan && vals.size() <= 255 && std::getenv("AMP_NO_CODES") == nullptr) {
       std::vector<uint8_t> code((size_t)D * D);
-      for (size_t x = 0; x < code.size(); ++x)
-        code[x] = (uint8_t)(std::lower_bound(vals.begin(), vals.end(), bw[x]) - vals.begin());
+      double last = NAN;
+      uint8_t last_c = 0;
+      for (size_t x = 0; x < code.size(); ++x) {  // (runs of equal values are common)
+        if (!(bw[x] == last)) {
+          last = bw[x];
+          last_c = (uint8_t)(std::lower_bound(vals.begin(), vals.end(), bw[x]) - vals.begin());
+        }
+        code[x] = last_c;
+      }
       const int U = (int)vals.size();
       // qtab[cls][code][c] = act[c-1] * mbs / vals[code] (optimizer.cpp:130-139)
       const size_t qn = ctx->classes.size() * (size_t)U * L;

@@ -274,14 +274,14 @@ def records_to_candidates(recs: np.ndarray, bufs: dict, n_layers: int,
         fail = failure_text(r, n_layers)
         st = Strategy(pp, dp, tmp, mbs)
         est = CostBreakdown()
-        if fail is None:
+        if fail is None:  # (ndarray.tolist: C-speed conversion of the detail rows)
             if "placement" in bufs:
-                st.placement = [int(x) for x in bufs["placement"][i][: pp * dp * tmp]]
+                st.placement = bufs["placement"][i][: pp * dp * tmp].tolist()
             if "cuts" in bufs:
-                st.cut_boundaries = [int(x) for x in bufs["cuts"][i][: pp + 1]]
+                st.cut_boundaries = bufs["cuts"][i][: pp + 1].tolist()
             est = CostBreakdown(float(r["pipeline_time"]), float(r["dpsync_time"]), float(r["total"]),
-                                [float(x) for x in bufs.get("stage_times", np.zeros((len(recs), 0)))[i][:pp]],
-                                [float(x) for x in bufs.get("edge_times", np.zeros((len(recs), 0)))[i][:pp - 1]])
+                                bufs["stage_times"][i][:pp].tolist() if "stage_times" in bufs else [],
+                                bufs["edge_times"][i][:pp - 1].tolist() if "edge_times" in bufs else [])
         out.append(CandidateRecord(st, est, 0, None, fail, int(r["index"])))
     return out
 
