@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
           for (int j = 0; j < pp; ++j) {
             st[j] = rt[cuts[j] * LP + cuts[j + 1]];
             spar[j] = p.rsum_p[cuts[j] * LP + cuts[j + 1]];
-            worst_p = std_max(worst_p, spar[j] / tmp);
+            if (p.has_ceiling) worst_p = std_max(worst_p, spar[j] / tmp);  // (only for the ceiling)
           }
         } else {
           for (int j = 0; j < pp; ++j) {
@@ -322,9 +322,33 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
         const double* qt = p.qtab + (size_t)w.cls * p.n_codes * L;
         double tr = -CUDART_INF;
         int rr = -1;
-        // (pp == 1: no edges, every replica computes the same t, so the
-        //  strict-'>' scan keeps replica 0: one evaluation)
-        for (int r = 0; r < (pp == 1 ? 1 : dp); ++r) {
+        // Without per-candidate edge details the slowest replica's value is
+        // enough: t_r = g1*slowest + (((E_r + st_0) + st_1) + ...) is
+        // non-decreasing in its edge sum E_r (IEEE additions round
+        // monotonically), so max_r t_r = t at max_r E_r — one stage-sum chain
+        // instead of one per replica.  (pp == 1: no edges, every replica
+        // computes the same t; the strict-'>' scan keeps replica 0.)
+        if (!p.all_edge) {
+          double emax = -CUDART_INF;
+          for (int r = 0; r < (pp == 1 ? 1 : dp); ++r) {
+            double esum = 0.0;
+            for (int q = 0; q < pp - 1; ++q) {
+              int cm = 255;
+              for (int s = 0; s < tmp && cm; ++s) {
+                const int cc = codeS[nib(perm, (q * dp + r) * tmp + s) * D +
+                                     nib(perm, ((q + 1) * dp + r) * tmp + s)];
+                cm = cc < cm ? cc : cm;
+              }
+              esum = esum + qt[(size_t)cm * L + cuts[q + 1]];  // (act[cut-1]*mbs) / b
+            }
+            emax = emax < esum ? esum : emax;
+          }
+          double sum = emax;
+          for (int j = 0; j < pp; ++j) sum = sum + st[j];
+          tr = g1 * slowest + sum;
+          rr = 0;  // (not reported without edge details)
+        }
+        for (int r = 0; p.all_edge && r < (pp == 1 ? 1 : dp); ++r) {
           double sum = 0.0;
           for (int q = 0; q < pp - 1; ++q) {
             int cm = 255;
