@@ -158,6 +158,9 @@ struct EvalParams {
   uint8_t* repcuts;           // [n_rep][max_pp + 1] cuts per signature run (memoised runs)
   int32_t bw_positive;        // every link bandwidth > 0 (coded): no all-reduce group can fail
   int32_t fuse_light;         // thread K_est places items [n_dp, n_chunk) itself (pp <= 2)
+  uint64_t* sigkey;           // [n_chunk] DP signature key written by K_place_t, or NULL
+  int32_t sig_code_bits;      // bits per boundary code in the key
+  int32_t pad8;
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

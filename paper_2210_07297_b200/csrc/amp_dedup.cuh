@@ -105,6 +105,9 @@ struct HashParams {
   uint64_t n;              // heavy items
   int32_t max_pp, code_bits;
   uint64_t mask;           // table size - 1
+  uint64_t epoch;          // this run's tag (> 0)
+  int32_t epoch_shift, pad0;  // key bits (tag above them), 64: no tag
+  const uint64_t* sigkey;  // [n] keys written by K_place, or NULL (computed here)
   unsigned long long* tkey;  // [T] keys (kHashEmpty = free)
   uint32_t* tval;          // [T] first item, then run index
   uint32_t* slot_of;       // [n] slot of every item (~0u: no signature)
@@ -129,24 +132,37 @@ __device__ __forceinline__ uint64_t sig_key(const CandWork& w, const ClassDev* c
   return key;
 }
 
+// Table entries carry the run's epoch above the key bits (epoch_shift), so
+// a slot of an older epoch reads as free and the table is never cleared
+// between chunks (epoch_shift = 64: no tag, the table is cleared instead).
+__device__ __forceinline__ bool slot_free(unsigned long long k, uint64_t epoch, int sh) {
+  return sh >= 64 ? k == kHashEmpty : (k >> sh) != epoch;
+}
+
 __global__ void k_hash_insert(HashParams p) {
+  const int sh = p.epoch_shift;
+  const uint64_t tag = sh >= 64 ? 0 : (p.epoch << sh);
   for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < p.n;
        u += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t key = sig_key(p.work[u], p.cls, p.bwcb + u * p.max_pp, p.max_pp, p.code_bits);
+    const uint64_t key = p.sigkey ? p.sigkey[u]
+                                  : sig_key(p.work[u], p.cls, p.bwcb + u * p.max_pp, p.max_pp,
+                                            p.code_bits);
     uint32_t slot = ~0u;
     if (key != kHashEmpty) {
+      const unsigned long long want = key | tag;
       uint64_t h = splitmix64(key) & p.mask;
       for (;;) {
-        const unsigned long long k = *(volatile unsigned long long*)&p.tkey[h];
-        if (k == key) break;
-        if (k == kHashEmpty) {
-          const unsigned long long old = atomicCAS(&p.tkey[h], kHashEmpty, key);
-          if (old == kHashEmpty) {  // first writer of this key
+        unsigned long long k = *(volatile unsigned long long*)&p.tkey[h];
+        if (k == want) break;
+        if (slot_free(k, p.epoch, sh)) {
+          const unsigned long long old = atomicCAS(&p.tkey[h], k, want);
+          if (old == k) {  // first writer of this key in this epoch
             p.tval[h] = (uint32_t)u;
             p.uniq[atomicAdd(p.n_uniq, 1ull)] = (uint32_t)h;
             break;
           }
-          if (old == key) break;
+          if (old == want) break;
+          k = old;  // lost to another key: probe on
         }
         h = (h + 1) & p.mask;
       }
@@ -161,7 +177,8 @@ __global__ void k_hash_gather(HashParams p, uint64_t* keys, uint32_t* slots) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t s = p.uniq[i];
-    keys[i] = p.tkey[s];
+    const unsigned long long k = p.tkey[s];
+    keys[i] = p.epoch_shift >= 64 ? k : (k & ((1ull << p.epoch_shift) - 1));  // drop the tag
     slots[i] = s;
   }
 }

@@ -167,7 +167,8 @@ struct amp_ctx {
   int code_bits = 0, key_bits = 0;
   DevBuf dd_keys, dd_vals, dd_skeys, dd_svals, dd_flags, dd_runid, dd_rep_list, dd_rep_of;
   DevBuf dd_nrep, dd_temp, dd_counters, prog_inner_d, dd_repcuts;
-  DevBuf dd_tkey, dd_tval, dd_slot, dd_uniq, dd_nuniq;  // hash dedup
+  DevBuf dd_tkey, dd_tval, dd_slot, dd_uniq, dd_nuniq, dd_sigkey;  // hash dedup
+  uint64_t hash_epoch = 0, hash_T = 0;
   size_t dd_temp_bytes = 0;
   // DP shared across signature prefixes (amp_trie.cuh)
   bool trie = false;
@@ -1229,9 +1230,15 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
                   std::getenv("AMP_NO_FUSE") == nullptr;
   ep.need_bwq = !(thread_mode && ctx->multi_b);
   ep.placep = nullptr;
+  ep.sigkey = nullptr;
   if (thread_mode) {
     CK(ctx->c_placep.ensure(sizeof(uint64_t) * C));
     ep.placep = ctx->c_placep.as<uint64_t>();
+    if (ctx->dedup && !d_given_cuts) {  // K_place_t writes the DP signature keys
+      CK(ctx->dd_sigkey.ensure(sizeof(uint64_t) * C));
+      ep.sigkey = ctx->dd_sigkey.as<uint64_t>();
+      ep.sig_code_bits = ctx->code_bits;
+    }
   }
   const int n_chunks = (int)((n_work + C - 1) / C);
   while ((int)ctx->kev.size() < 4 * n_chunks) {
@@ -1312,12 +1319,26 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
         // hash the item keys (amp_dedup.cuh), sort only the distinct ones
         uint64_t T = 1024;
         while (T < 2 * ep.n_dp) T <<= 1;
+        const bool grown = ctx->dd_tkey.bytes < sizeof(uint64_t) * T;
         CK(ctx->dd_tkey.ensure(sizeof(uint64_t) * T));
         CK(ctx->dd_tval.ensure(sizeof(uint32_t) * T));
         CK(ctx->dd_slot.ensure(sizeof(uint32_t) * C));
         CK(ctx->dd_uniq.ensure(sizeof(uint32_t) * C));
         CK(ctx->dd_nuniq.ensure(sizeof(unsigned long long)));
-        CK(cudaMemsetAsync(ctx->dd_tkey.p, 0xff, sizeof(uint64_t) * T, ctx->stream));
+        // epoch tags above the key bits: the table is cleared only when it
+        // is (re)allocated or the tag wraps (amp_dedup.cuh slot_free)
+        const int esh = 64 - ctx->key_bits >= 8 ? ctx->key_bits : 64;
+        if (esh >= 64) {
+          CK(cudaMemsetAsync(ctx->dd_tkey.p, 0xff, sizeof(uint64_t) * T, ctx->stream));
+        } else {
+          const uint64_t max_epoch = (1ull << (64 - esh)) - 1;
+          if (grown || ctx->hash_T != T || ctx->hash_epoch >= max_epoch) {
+            CK(cudaMemsetAsync(ctx->dd_tkey.p, 0, sizeof(uint64_t) * T, ctx->stream));
+            ctx->hash_epoch = 0;
+          }
+          ++ctx->hash_epoch;
+        }
+        ctx->hash_T = T;
         CK(cudaMemsetAsync(ctx->dd_nuniq.p, 0, sizeof(unsigned long long), ctx->stream));
         HashParams hp{};
         hp.work = ep.work;
@@ -1327,6 +1348,9 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
         hp.max_pp = ctx->max_pp;
         hp.code_bits = ctx->code_bits;
         hp.mask = T - 1;
+        hp.epoch = ctx->hash_epoch;
+        hp.epoch_shift = esh;
+        hp.sigkey = ep.sigkey;
         hp.tkey = ctx->dd_tkey.as<unsigned long long>();
         hp.tval = ctx->dd_tval.as<uint32_t>();
         hp.slot_of = ctx->dd_slot.as<uint32_t>();

@@ -128,6 +128,7 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
     //      fails like p2p_time in the DP's edge function -----------------
     int first_bad = -1;
     double bad_val = 0.0;
+    uint64_t key = (uint64_t)c;  // DP signature (amp_dedup.cuh sig_key)
     for (int q = 0; q < pp - 1; ++q) {
       int cm = 255;  // (code 0 is the smallest bandwidth: nothing can go lower)
       for (int r = 0; r < dp && cm; ++r)
@@ -138,6 +139,7 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
         }
       const double b = p.bwval[cm];
       if (q == 0) code0 = cm;
+      key = (key << p.sig_code_bits) | (uint64_t)cm;
       if (store) {
         p.bwcb[u * maxpp + q] = (uint8_t)cm;
         if (p.need_bwq) p.bwqb[u * maxpp + q] = b;
@@ -151,6 +153,12 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
       fc = AMP_FAIL_P2P_BANDWIDTH;
       fval = bad_val;
     }
+    if (store && p.sigkey) {  // zero codes pad the unused boundaries
+      key <<= (uint64_t)p.sig_code_bits * (uint64_t)(maxpp - (pp > 0 ? pp : 1));
+      p.sigkey[u] = (fc == 0 && pp >= 3) ? key : ~0ull;
+    }
+  } else if (store && p.sigkey) {
+    p.sigkey[u] = ~0ull;
   }
   w.index = index;
   w.out = out;
