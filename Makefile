@@ -5,7 +5,7 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 # -fmad=false: the reference's doubles are never FMA-contracted
 NVFLAGS := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC,-Wall,-ffp-contract=off \
-           -Xptxas -v,-warn-spills --expt-relaxed-constexpr
+           -Xptxas -v,-warn-spills --expt-relaxed-constexpr $(EXTRA)
 PKG := paper_2210_07297_b200
 LIB := $(PKG)/libamp_search.so
 SRCS := $(PKG)/csrc/amp_search.cu $(PKG)/csrc/amp_simulate.cpp $(PKG)/csrc/amp_anneal.cpp

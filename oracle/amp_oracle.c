@@ -449,8 +449,97 @@ static double params_in_range(const oracle_ctx* c, int first, int last) {
   return sum;
 }
 
+/* ------------------------------------------------------------------ */
+/* DP memo (SURVEY.md §8(d) "full-N memoized CPU oracle"): optimal_assignment
+ * is a pure function of the class (layer times, gas, stage count) and the
+ * boundary bandwidths (the edge function), so a per-worker table keyed by
+ * (class, bws bits) returns the cuts the DP would compute.                */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  int nb;           /* bandwidth slots per key (max_pp - 1, >= 1) */
+  int nc;           /* cut slots per value (max_pp + 1) */
+  uint64_t cap, n;  /* power of two; entries */
+  uint8_t* used;
+  int32_t* cls;
+  double* bws;      /* [cap][nb] */
+  int32_t* cuts;    /* [cap][nc] */
+  pthread_mutex_t* mu; /* shared by the run's workers (DPs run outside it) */
+} dp_memo;
+
+static void memo_init(dp_memo* m, int max_pp, uint64_t cap) {
+  m->nb = max_pp > 1 ? max_pp - 1 : 1;
+  m->nc = max_pp + 1;
+  m->cap = cap;
+  m->n = 0;
+  m->used = (uint8_t*)calloc(cap, 1);
+  m->cls = (int32_t*)malloc(sizeof(int32_t) * cap);
+  m->bws = (double*)calloc(cap * m->nb, sizeof(double));
+  m->cuts = (int32_t*)malloc(sizeof(int32_t) * cap * m->nc);
+  m->mu = NULL;
+}
+
+static void memo_free(dp_memo* m) {
+  free(m->used);
+  free(m->cls);
+  free(m->bws);
+  free(m->cuts);
+}
+
+static uint64_t memo_hash(int k, const double* bws, int nb) {
+  uint64_t h = oracle_splitmix64((uint64_t)k);
+  for (int q = 0; q < nb; ++q) {
+    uint64_t v;
+    memcpy(&v, &bws[q], 8);
+    h = oracle_splitmix64(h ^ v);
+  }
+  return h;
+}
+
+/* slot of (k, bws) (bws padded with zeros to nb): found or the free slot */
+static uint64_t memo_slot(const dp_memo* m, int k, const double* bws) {
+  uint64_t h = memo_hash(k, bws, m->nb) & (m->cap - 1);
+  while (m->used[h] &&
+         !(m->cls[h] == k && memcmp(m->bws + h * m->nb, bws, sizeof(double) * m->nb) == 0))
+    h = (h + 1) & (m->cap - 1);
+  return h;
+}
+
+static void memo_put(dp_memo* m, int k, const double* bws, const int32_t* cuts, int pp) {
+  if (2 * (m->n + 1) > m->cap) { /* grow x2, re-insert */
+    dp_memo g;
+    memo_init(&g, m->nc - 1, m->cap * 2);
+    for (uint64_t i = 0; i < m->cap; ++i)
+      if (m->used[i]) {
+        const uint64_t t = memo_slot(&g, m->cls[i], m->bws + i * m->nb);
+        g.used[t] = 1;
+        g.cls[t] = m->cls[i];
+        memcpy(g.bws + t * g.nb, m->bws + i * m->nb, sizeof(double) * m->nb);
+        memcpy(g.cuts + t * g.nc, m->cuts + i * m->nc, sizeof(int32_t) * m->nc);
+      }
+    g.n = m->n;
+    g.mu = m->mu;
+    memo_free(m);
+    *m = g;
+  }
+  const uint64_t h = memo_slot(m, k, bws);
+  if (m->used[h]) return; /* another worker solved it meanwhile */
+  m->used[h] = 1;
+  m->cls[h] = k;
+  memcpy(m->bws + h * m->nb, bws, sizeof(double) * m->nb);
+  memcpy(m->cuts + h * m->nc, cuts, sizeof(int32_t) * (pp + 1));
+  ++m->n;
+}
+
+static void evaluate_impl(const oracle_ctx* c, uint64_t index, amp_record* rec, int32_t* cuts_out,
+                          double* stage_out, double* edge_out, dp_memo* memo);
+
 void oracle_evaluate(const oracle_ctx* c, uint64_t index, amp_record* rec, int32_t* cuts_out,
                      double* stage_out, double* edge_out) {
+  evaluate_impl(c, index, rec, cuts_out, stage_out, edge_out, NULL);
+}
+
+static void evaluate_impl(const oracle_ctx* c, uint64_t index, amp_record* rec, int32_t* cuts_out,
+                          double* stage_out, double* edge_out, dp_memo* memo) {
   const int L = c->L;
   const int k = (int)(index / c->P);
   const int pp = c->cls[k][0], dp = c->cls[k][1], tmp = c->cls[k][2], mbs = c->cls[k][3];
@@ -481,7 +570,7 @@ void oracle_evaluate(const oracle_ctx* c, uint64_t index, amp_record* rec, int32
 
   /* placement_edge_cost (optimizer.cpp:130-139) via min_edge_bandwidth
    * (cost_model.cpp:164-174). */
-  double* bws = (double*)malloc(sizeof(double) * (pp > 1 ? pp - 1 : 1));
+  double* bws = (double*)calloc(maxpp > 1 ? maxpp - 1 : 1, sizeof(double)); /* (memo key pad) */
   for (int q = 0; q + 1 < pp; ++q) {
     double b = INFINITY;
     for (int r = 0; r < dp; ++r)
@@ -519,7 +608,22 @@ void oracle_evaluate(const oracle_ctx* c, uint64_t index, amp_record* rec, int32
     }
     int32_t* cuts = (int32_t*)malloc(sizeof(int32_t) * (pp + 1));
     double dpcost;
-    oracle_optimal_assignment(t, L, pp, gas, edges, cuts, &dpcost, NULL, NULL);
+    int hit = 0;
+    if (memo) {
+      pthread_mutex_lock(memo->mu);
+      const uint64_t slot = memo_slot(memo, k, bws);
+      if ((hit = memo->used[slot]))
+        memcpy(cuts, memo->cuts + slot * memo->nc, sizeof(int32_t) * (pp + 1));
+      pthread_mutex_unlock(memo->mu);
+    }
+    if (!hit) {
+      oracle_optimal_assignment(t, L, pp, gas, edges, cuts, &dpcost, NULL, NULL);
+      if (memo) {
+        pthread_mutex_lock(memo->mu);
+        memo_put(memo, k, bws, cuts, pp);
+        pthread_mutex_unlock(memo->mu);
+      }
+    }
     free(edges);
 
     /* per-device parameter ceiling (optimizer.cpp:159-169). */
@@ -621,6 +725,7 @@ typedef struct {
   int32_t* cuts;
   double* stage;
   double* edge;
+  dp_memo* memo;
 } run_state;
 
 static void* run_worker(void* arg) {
@@ -629,16 +734,39 @@ static void* run_worker(void* arg) {
   for (;;) {
     uint64_t i = atomic_fetch_add(&s->next, 1);
     if (i >= s->end - s->begin) break;
-    oracle_evaluate(s->c, s->begin + i, &s->records[i], s->cuts ? s->cuts + i * (maxpp + 1) : NULL,
-                    s->stage ? s->stage + i * maxpp : NULL, s->edge ? s->edge + i * maxpp : NULL);
+    evaluate_impl(s->c, s->begin + i, &s->records[i], s->cuts ? s->cuts + i * (maxpp + 1) : NULL,
+                  s->stage ? s->stage + i * maxpp : NULL, s->edge ? s->edge + i * maxpp : NULL,
+                  s->memo);
   }
   return NULL;
 }
 
+static void run_impl(const oracle_ctx* c, uint64_t begin, uint64_t end, int32_t threads,
+                     amp_record* records, int32_t* cuts, double* stage_times, double* edge_times,
+                     int memo);
+
 void oracle_run(const oracle_ctx* c, uint64_t begin, uint64_t end, int32_t threads,
                 amp_record* records, int32_t* cuts, double* stage_times, double* edge_times) {
+  run_impl(c, begin, end, threads, records, cuts, stage_times, edge_times, 0);
+}
+
+void oracle_run_memo(const oracle_ctx* c, uint64_t begin, uint64_t end, int32_t threads,
+                     amp_record* records, int32_t* cuts, double* stage_times, double* edge_times) {
+  run_impl(c, begin, end, threads, records, cuts, stage_times, edge_times, 1);
+}
+
+static void run_impl(const oracle_ctx* c, uint64_t begin, uint64_t end, int32_t threads,
+                     amp_record* records, int32_t* cuts, double* stage_times, double* edge_times,
+                     int memo) {
   if (end <= begin) return;
   run_state s;
+  dp_memo m;
+  pthread_mutex_t mu = PTHREAD_MUTEX_INITIALIZER;
+  if (memo) {
+    memo_init(&m, c->max_pp, 1u << 12);
+    m.mu = &mu;
+  }
+  s.memo = memo ? &m : NULL;
   s.c = c;
   s.begin = begin;
   s.end = end;
@@ -654,6 +782,7 @@ void oracle_run(const oracle_ctx* c, uint64_t begin, uint64_t end, int32_t threa
   run_worker(&s);
   for (int w = 1; w < threads; ++w) pthread_join(tid[w], NULL);
   free(tid);
+  if (memo) memo_free(&m);
 }
 
 static const amp_record* g_rank_records;

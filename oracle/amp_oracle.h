@@ -60,6 +60,12 @@ void oracle_evaluate(const oracle_ctx* ctx, uint64_t index, amp_record* rec, int
 void oracle_run(const oracle_ctx* ctx, uint64_t begin, uint64_t end, int32_t threads,
                 amp_record* records, int32_t* cuts, double* stage_times, double* edge_times);
 
+/* oracle_run with the DP memoised per worker by (class, boundary
+ * bandwidths): the same records, cuts and times (SURVEY.md §8(d) full-N
+ * memoised CPU oracle for large-N parity). */
+void oracle_run_memo(const oracle_ctx* ctx, uint64_t begin, uint64_t end, int32_t threads,
+                     amp_record* records, int32_t* cuts, double* stage_times, double* edge_times);
+
 /* rank_records key (optimizer.cpp:178-196): writes the permutation that
  * sorts records by (failed, total, index). */
 void oracle_rank(const amp_record* records, int64_t n, int64_t* order);

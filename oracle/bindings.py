@@ -50,6 +50,7 @@ def load_oracle() -> C.CDLL:
             "oracle_placement": (None, [C.c_void_p, C.c_uint64, _ip]),
             "oracle_evaluate": (None, [C.c_void_p, C.c_uint64, _recp, _ip, _dp, _dp]),
             "oracle_run": (None, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int32, _recp, _ip, _dp, _dp]),
+            "oracle_run_memo": (None, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int32, _recp, _ip, _dp, _dp]),
             "oracle_rank": (None, [_recp, C.c_int64, _i64p]),
             "oracle_splitmix64": (C.c_uint64, [C.c_uint64]),
         }
@@ -119,7 +120,9 @@ class Oracle:
             out.append((a.value, b.value, c.value, d.value))
         return out
 
-    def run(self, begin=0, end=None, threads=1, details=True):
+    def run(self, begin=0, end=None, threads=1, details=True, memo=False):
+        """Evaluate [begin, end); memo=True memoises the DP per worker by
+        (class, boundary bandwidths) — identical outputs, for large N."""
         end = self.num_candidates if end is None else end
         n = end - begin
         recs, rp = _recs(n)
@@ -127,7 +130,8 @@ class Oracle:
         cuts = np.full((n, mp + 1), -1, dtype=np.int32) if details else None
         st = np.full((n, mp), np.nan) if details else None
         ed = np.full((n, mp), np.nan) if details else None
-        self.lib.oracle_run(self.h, begin, end, threads, rp,
+        fn = self.lib.oracle_run_memo if memo else self.lib.oracle_run
+        fn(self.h, begin, end, threads, rp,
                             cuts.ctypes.data_as(_ip) if details else None,
                             st.ctypes.data_as(_dp) if details else None,
                             ed.ctypes.data_as(_dp) if details else None)

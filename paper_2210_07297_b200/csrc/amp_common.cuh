@@ -170,6 +170,10 @@ __device__ __forceinline__ double std_max(double a, double b) { return a < b ? b
 // std::max(0.0, x)
 __device__ __forceinline__ double max0(double x) { return 0.0 < x ? x : 0.0; }
 
+__device__ __forceinline__ void prefetch_l2(const void* a) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+}
+
 // splitmix64; integer-only, identical on host.
 __host__ __device__ inline uint64_t splitmix64(uint64_t x) {
   x += 0x9e3779b97f4a7c15ULL;

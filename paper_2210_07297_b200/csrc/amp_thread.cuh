@@ -190,6 +190,9 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
 // K_est (thread per candidate)
 // ---------------------------------------------------------------------------
 constexpr int kEstTWarps = 8;
+#ifndef AMP_EST_PREFETCH
+#define AMP_EST_PREFETCH 1
+#endif
 
 template <int DT>
 #ifndef AMP_EST_MINB
@@ -227,6 +230,16 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
   for (uint64_t wbase = first; wbase < p.n_chunk; wbase += stride) {
     const uint64_t u = wbase + lane;
     const bool live = u < p.n_chunk;
+#if AMP_EST_PREFETCH
+    {  // the next iteration's streamed inputs into L2 (no registers held)
+      const uint64_t un = u + stride;
+      if (un < p.n_chunk && !(p.fuse_light && un >= p.n_dp)) {
+        prefetch_l2(p.work + un);
+        if (p.placep) prefetch_l2(p.placep + un);
+        if (p.rep_of && un < p.n_dp) prefetch_l2(p.rep_of + un);
+      }
+    }
+#endif
     amp_record rec;
     int cuts[kThreadMaxD + 1];
     double st[kThreadMaxD], spar[kThreadMaxD];

@@ -344,3 +344,28 @@ def test_thread_and_warp_kernels_agree(name, monkeypatch):
     for key in ("cuts", "stage_times", "edge_times", "placement"):
         assert np.array_equal(b1[key], b2[key], equal_nan=True), key
     assert t1.view(np.uint8).tobytes() == t2.view(np.uint8).tobytes()
+
+
+def test_full_sweep_1m_equals_memoised_oracle():
+    """SURVEY §8(d) large-N parity: a 1.05 M-candidate hetero_cluster sweep
+    (the bench scenario and seed, its production path: thread kernels,
+    signature memoisation, prefix-shared DP) equals the full-N memoised CPU
+    oracle record for record, and the device top-k is the oracle's ranking."""
+    import os
+    sc = scenario("hetero_cluster")
+    enc = P.EncodedProblem.from_scenario(sc)
+    P_ = 15000
+    with planner.Searcher(enc, placements_per_class=P_, seed=0) as s:
+        top, allr, _ = s.run(0, s.num_candidates, k=32, want_all=True, details=False)
+        n = s.num_candidates
+    o = B.Oracle(enc, P_, 0)
+    orec, _ = o.run(threads=os.cpu_count() or 4, details=False, memo=True)
+    assert len(orec) == n == 70 * P_
+    for f in ("index", "pp", "dp", "tmp", "mbs", "fail_code"):
+        assert np.array_equal(allr[f], orec[f]), f
+    ok = orec["fail_code"] == 0
+    assert ok.sum() > n // 2
+    for f in ("total", "pipeline_time", "dpsync_time"):
+        assert np.array_equal(allr[f][ok], orec[f][ok]), f
+    order = B.oracle_rank(orec)
+    assert top["index"].tolist() == orec["index"][order[:32]].tolist()
