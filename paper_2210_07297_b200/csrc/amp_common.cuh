@@ -160,7 +160,7 @@ struct EvalParams {
   int32_t fuse_light;         // thread K_est places items [n_dp, n_chunk) itself (pp <= 2)
   uint64_t* sigkey;           // [n_chunk] DP signature key written by K_place_t, or NULL
   int32_t sig_code_bits;      // bits per boundary code in the key
-  int32_t pad8;
+  int32_t est_fast;           // K_est_t uses the unrolled shape kernels (amp_thread.cuh est_shape)
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

@@ -1240,6 +1240,17 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
       ep.sig_code_bits = ctx->code_bits;
     }
   }
+  // unrolled shape kernels in K_est_t: |D| == 16, every class a full
+  // pp * dp * tmp == 16 shape, positive coded bandwidths, the range / 2-stage
+  // tables, records only (AMP_NO_SHAPE=1 keeps the generic body)
+  ep.est_fast = 0;
+  if (est_thread && ctx->D == 16 && ep.bw_positive && ep.cut2tab && ep.rsum_t && !ep.all_cuts &&
+      !ep.all_stage && !ep.all_edge && !ep.all_place && !d_given_cuts &&
+      std::getenv("AMP_NO_SHAPE") == nullptr) {
+    bool shapes = true;
+    for (const auto& c : ctx->classes) shapes = shapes && c.pp * c.dp * c.tmp == 16;
+    ep.est_fast = shapes;
+  }
   const int n_chunks = (int)((n_work + C - 1) / C);
   while ((int)ctx->kev.size() < 4 * n_chunks) {
     cudaEvent_t e;
@@ -1401,7 +1412,9 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
       ctx->launches += 1;
     }
     CK(cudaEventRecord(ev[2], ctx->stream));
-    if (est_thread && ctx->D == 16)
+    if (ep.est_fast)
+      k_est_t<16, true><<<ctx->est_ctas, kEstTWarps * 32, 0, ctx->stream>>>(ep);
+    else if (est_thread && ctx->D == 16)
       k_est_t<16><<<ctx->est_ctas, kEstTWarps * 32, 0, ctx->stream>>>(ep);
     else if (est_thread)
       k_est_t<0><<<ctx->est_ctas, kEstTWarps * 32, 0, ctx->stream>>>(ep);

@@ -187,6 +187,148 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// K_est shape kernels: the estimate of one candidate of class shape
+// (PP, DPn, TMP) (pp * dp * tmp == 16) with every loop unrolled — nibble
+// extractions become constant shifts, the cut / stage values live in
+// registers (the generic body indexes them at run time: local memory), and
+// the replicas' independent table loads overlap.  The same operations in the
+// same order as the generic body (which still serves detail outputs, given
+// cuts and non-positive bandwidth tables), so results are bit-identical.
+// The stage loop fuses stage_time, the first-maximum scan, the stage-sum
+// chain of the slowest replica, the parameter ceiling and dpsync_time: each
+// keeps its own sequential order, they only share the stage's two loads.
+template <int PP, int DPn, int TMP>
+__device__ __forceinline__ void est_shape(const EvalParams& p, const uint8_t* codeS, const CandWork& w,
+                                          const ClassDev& cl, uint64_t u, bool fused, uint64_t perm,
+                                          int code0, int& fc, double& pipeline, double& dpsync) {
+  constexpr int D = 16;
+  const int L = p.L, LP = L + 1, maxpp = p.max_pp;
+  int cuts[PP + 1];
+  if (PP >= 3) {  // the signature run's cuts (memoised DP) or this item's
+    const uint8_t* ci = p.rep_of ? p.repcuts + (uint64_t)p.rep_of[u] * (maxpp + 1)
+                                 : p.cutsb + u * (maxpp + 1);
+#pragma unroll
+    for (int q = 0; q <= PP; ++q) cuts[q] = ci[q];
+  } else if (PP == 2) {
+    cuts[0] = 0;
+    cuts[1] = p.cut2tab[(size_t)w.cls * p.n_codes + (fused ? code0 : p.bwcb[u * maxpp])];
+    cuts[PP] = L;
+  } else {
+    cuts[0] = 0;
+    cuts[PP] = L;
+  }
+  // slowest replica's edge sum (edge-sum monotonicity, see the generic body)
+  const double* qt = p.qtab + (size_t)w.cls * p.n_codes * L;
+  double emax = -CUDART_INF;
+#pragma unroll
+  for (int r = 0; r < (PP == 1 ? 1 : DPn); ++r) {
+    double esum = 0.0;
+#pragma unroll
+    for (int q = 0; q < PP - 1; ++q) {
+      int cm = 255;
+#pragma unroll
+      for (int s = 0; s < TMP; ++s) {
+        const int cc = codeS[nib(perm, (q * DPn + r) * TMP + s) * D + nib(perm, ((q + 1) * DPn + r) * TMP + s)];
+        cm = cc < cm ? cc : cm;
+      }
+      esum = esum + qt[(size_t)cm * L + cuts[q + 1]];
+    }
+    emax = emax < esum ? esum : emax;
+  }
+#ifdef AMP_EST_DEBUG
+  for (int q = 0; q <= PP; ++q)
+    if (cuts[q] < 0 || cuts[q] > L || (q && cuts[q] < cuts[q - 1]))
+      printf("est_fast: PP %d u=%llu bad cuts q=%d %d rep=%u\n", PP, (unsigned long long)u, q, cuts[q],
+             p.rep_of ? p.rep_of[u] : 0u);
+#endif
+  const double* rt = p.rsum_t + (size_t)cl.pair * LP * LP;
+  double slowest = 0.0, sum = emax, worst_p = 0.0, worst = 0.0;
+#pragma unroll
+  for (int j = 0; j < PP; ++j) {
+    const int a = cuts[j] * LP + cuts[j + 1];
+    const double stj = rt[a], spj = p.rsum_p[a];
+    slowest = (j == 0 || slowest < stj) ? stj : slowest;  // std::max_element: first maximum
+    sum = sum + stj;
+    if (p.has_ceiling) worst_p = std_max(worst_p, spj / TMP);
+    if (DPn != 1) {  // dpsync: the stage's minimum-bandwidth group (bw_positive)
+      int cm = 255;
+#pragma unroll
+      for (int s = 0; s < TMP && cm; ++s)
+#pragma unroll
+        for (int r1 = 0; r1 < DPn && cm; ++r1)
+#pragma unroll
+          for (int r2 = r1 + 1; r2 < DPn && cm; ++r2) {
+            const int cc = codeS[nib(perm, (j * DPn + r1) * TMP + s) * D + nib(perm, (j * DPn + r2) * TMP + s)];
+            cm = cc < cm ? cc : cm;
+          }
+      const double b = p.bwval[cm];
+      const double message = spj * p.bpp / TMP;
+      worst = std_max(worst, 2.0 * (double)(DPn - 1) * message / ((double)DPn * b));
+    }
+  }
+  if (p.has_ceiling && worst_p > p.ceiling) {
+    fc = AMP_FAIL_CEILING;
+    return;
+  }
+  pipeline = (double)(cl.gas - 1) * slowest + sum;
+  dpsync = worst;
+}
+
+// One candidate through the shape kernels (p.est_fast: |D| == 16, every class
+// with pp * dp * tmp == 16, positive bandwidths, range and 2-stage tables, no
+// detail outputs, no given cuts).
+template <int DT>
+__device__ __forceinline__ void est_fast_item(const EvalParams& p, const PlaceSmem& PS, uint64_t u,
+                                              amp_record& rec, bool& ok) {
+  const bool fused = p.fuse_light && u >= p.n_dp;
+  CandWork w;
+  uint64_t perm = 0;
+  int code0 = 0;
+  if (fused) place_one<DT>(p, PS, u, false, w, perm, code0);
+  else w = p.work[u];
+  const ClassDev cl = p.cls[w.cls];
+  int fc = w.fail_code;
+  double pipeline = CUDART_NAN, dpsync = CUDART_NAN;
+  if (fc == 0) {
+    if (!fused) perm = p.placep[u];
+    switch (cl.pp * 1024 + cl.dp * 32 + cl.tmp) {
+#define AMP_SHAPE(a, b, c)                                                                  \
+  case a * 1024 + b * 32 + c:                                                               \
+    est_shape<a, b, c>(p, PS.code, w, cl, u, fused, perm, code0, fc, pipeline, dpsync); \
+    break;
+      AMP_SHAPE(1, 1, 16) AMP_SHAPE(1, 2, 8) AMP_SHAPE(1, 4, 4) AMP_SHAPE(1, 8, 2) AMP_SHAPE(1, 16, 1)
+      AMP_SHAPE(2, 1, 8) AMP_SHAPE(2, 2, 4) AMP_SHAPE(2, 4, 2) AMP_SHAPE(2, 8, 1)
+      AMP_SHAPE(4, 1, 4) AMP_SHAPE(4, 2, 2) AMP_SHAPE(4, 4, 1)
+      AMP_SHAPE(8, 1, 2) AMP_SHAPE(8, 2, 1)
+      AMP_SHAPE(16, 1, 1)
+#undef AMP_SHAPE
+      default:
+#ifdef AMP_EST_DEBUG
+        printf("est_fast: shape %d %d %d u=%llu cls=%d fused=%d\n", cl.pp, cl.dp, cl.tmp,
+               (unsigned long long)u, w.cls, (int)fused);
+        fc = 99;
+        break;
+#else
+        __trap();  // (the host enables est_fast only for these shapes)
+#endif
+    }
+  }
+  rec.index = w.index;
+  rec.pp = cl.pp;
+  rec.dp = cl.dp;
+  rec.tmp = cl.tmp;
+  rec.mbs = cl.mbs;
+  rec.fail_code = fc;
+  rec.fail_layer = fc == AMP_FAIL_PROFILE_MISS ? w.fail_layer : -1;
+  rec.fail_value = fc == AMP_FAIL_P2P_BANDWIDTH ? w.fail_value : 0.0;
+  ok = fc == 0;
+  rec.pipeline_time = ok ? pipeline : CUDART_NAN;
+  rec.dpsync_time = ok ? dpsync : CUDART_NAN;
+  rec.total = ok ? pipeline + dpsync : CUDART_NAN;
+  if (p.all) p.all[w.out] = rec;
+}
+
+// ---------------------------------------------------------------------------
 // K_est (thread per candidate)
 // ---------------------------------------------------------------------------
 constexpr int kEstTWarps = 8;
@@ -194,7 +336,7 @@ constexpr int kEstTWarps = 8;
 #define AMP_EST_PREFETCH 1
 #endif
 
-template <int DT>
+template <int DT, bool FAST = false>
 #ifndef AMP_EST_MINB
 #define AMP_EST_MINB 4
 #endif
@@ -245,7 +387,9 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
     double st[kThreadMaxD], spar[kThreadMaxD];
     int pp = 0, best_r = -1;
     bool ok = false;
-    if (live) {
+    if constexpr (FAST) {
+      if (live) est_fast_item<DT>(p, PS, u, rec, ok);
+    } else if (live) {
       // fused light path: the pp <= 2 tail (never in K_dp) is placed here
       const bool fused = p.fuse_light && u >= p.n_dp;
       CandWork w;

@@ -369,3 +369,42 @@ def test_full_sweep_1m_equals_memoised_oracle():
         assert np.array_equal(allr[f][ok], orec[f][ok]), f
     order = B.oracle_rank(orec)
     assert top["index"].tolist() == orec["index"][order[:32]].tolist()
+
+
+@pytest.mark.parametrize("name", ["hetero_cluster", "hetero_model", "homogeneous"])
+def test_shape_kernels_equal_generic_estimate(name, monkeypatch):
+    """K_est_t's unrolled per-shape estimate (est_shape, records-only runs)
+    equals the generic body (AMP_NO_SHAPE=1) record for record, top-k too."""
+    sc = scenario(name)
+    enc = P.EncodedProblem.from_scenario(sc)
+    outs = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("AMP_NO_SHAPE", env)
+        else:
+            monkeypatch.delenv("AMP_NO_SHAPE", raising=False)
+        with planner.Searcher(enc, placements_per_class=2000, seed=5) as s:
+            top, allr, _ = s.run(0, s.num_candidates, k=24, want_all=True, details=False)
+        outs.append((top, allr))
+    (t1, a1), (t2, a2) = outs
+    assert np.array_equal(a1.view(np.uint8), a2.view(np.uint8))
+    assert np.array_equal(t1.view(np.uint8), t2.view(np.uint8))
+
+
+@pytest.mark.parametrize("kind", ["plain", "miss", "ceiling", "fallback"])
+def test_records_only_failure_paths_match_oracle(kind):
+    """Records-only runs (the shape kernels where they apply) on the failure
+    variants equal the oracle field by field."""
+    from test_oracle import _variant_world
+    model, cl, prof, gbs, opts = _variant_world(kind)
+    enc = P.EncodedProblem(model, cl, prof, gbs, opts)
+    o = B.Oracle(enc, placements_per_class=7, seed=3)
+    orec, _ = o.run(threads=4, details=False)
+    with planner.Searcher(enc, placements_per_class=7, seed=3) as s:
+        top, allr, _ = s.run(0, s.num_candidates, k=5, want_all=True, details=False)
+    for f in ("index", "pp", "dp", "tmp", "mbs", "fail_code", "fail_layer", "fail_value"):
+        assert np.array_equal(allr[f], orec[f]), f
+    ok = orec["fail_code"] == 0
+    for f in ("total", "pipeline_time", "dpsync_time"):
+        assert np.array_equal(allr[f][ok], orec[f][ok]), f
+    assert top["index"].tolist() == orec["index"][B.oracle_rank(orec)[:5]].tolist()
