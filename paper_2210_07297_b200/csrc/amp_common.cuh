@@ -161,6 +161,8 @@ struct EvalParams {
   uint64_t* sigkey;           // [n_chunk] DP signature key written by K_place_t, or NULL
   int32_t sig_code_bits;      // bits per boundary code in the key
   int32_t est_fast;           // K_est_t uses the unrolled shape kernels (amp_thread.cuh est_shape)
+  int32_t need_bwcb;          // K_place stores the boundary codes (bwcb)
+  int32_t pad9;
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

@@ -1243,14 +1243,14 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   // unrolled shape kernels in K_est_t: |D| == 16, every class a full
   // pp * dp * tmp == 16 shape, positive coded bandwidths, the range / 2-stage
   // tables, records only (AMP_NO_SHAPE=1 keeps the generic body)
-  ep.est_fast = 0;
-  if (est_thread && ctx->D == 16 && ep.bw_positive && ep.cut2tab && ep.rsum_t && !ep.all_cuts &&
-      !ep.all_stage && !ep.all_edge && !ep.all_place && !d_given_cuts &&
-      std::getenv("AMP_NO_SHAPE") == nullptr) {
-    bool shapes = true;
-    for (const auto& c : ctx->classes) shapes = shapes && c.pp * c.dp * c.tmp == 16;
-    ep.est_fast = shapes;
-  }
+  bool shape16 = thread_mode && ctx->D == 16 && ep.bw_positive && std::getenv("AMP_NO_SHAPE") == nullptr;
+  for (const auto& c : ctx->classes) shape16 = shape16 && c.pp * c.dp * c.tmp == 16;
+  ep.est_fast = shape16 && est_thread && ep.cut2tab && ep.rsum_t && !ep.all_cuts && !ep.all_stage &&
+                !ep.all_edge && !ep.all_place && !d_given_cuts;
+  // the boundary codes are read by K_dp without the trie, the sort dedup
+  // path and K_est's pp == 2 items placed by K_place; with the hash dedup on
+  // K_place's signature keys, the trie and the fused light path, nothing
+  ep.need_bwcb = !(ep.sigkey && ctx->trie && ep.fuse_light && std::getenv("AMP_DEDUP_SORT") == nullptr);
   const int n_chunks = (int)((n_work + C - 1) / C);
   while ((int)ctx->kev.size() < 4 * n_chunks) {
     cudaEvent_t e;
@@ -1276,7 +1276,9 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     const int place_grid = (int)std::min<uint64_t>((warps + 7) / 8, (uint64_t)ctx->sms * 16);
     if (thread_mode) {
       const int tg = (int)std::min<uint64_t>((ep.n_chunk + 255) / 256, (uint64_t)ctx->sms * 16);
-      if (ctx->D == 16)
+      if (shape16)
+        k_place_t<16, true><<<tg, 256, 0, ctx->stream>>>(ep);
+      else if (ctx->D == 16)
         k_place_t<16><<<tg, 256, 0, ctx->stream>>>(ep);
       else
         k_place_t<0><<<tg, 256, 0, ctx->stream>>>(ep);

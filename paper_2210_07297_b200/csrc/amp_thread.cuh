@@ -62,12 +62,39 @@ __device__ void place_smem_init(const EvalParams& p, PlaceSmem& S) {
   }
 }
 
+// Boundary codes of a full-shape class (PP, DPn, TMP), loops unrolled
+// (constant nibble shifts): the min over replicas and shards of each stage
+// boundary's link codes (cost_model.cpp:164-174), appended to the DP
+// signature key.  Positive bandwidths only (no boundary can fail).
+template <int PP, int DPn, int TMP>
+__device__ __forceinline__ uint64_t codes_shape(const EvalParams& p, const uint8_t* code, uint64_t perm,
+                                                uint64_t u, bool store, uint64_t key, int& code0) {
+#pragma unroll
+  for (int q = 0; q < PP - 1; ++q) {
+    int cm = 255;
+#pragma unroll
+    for (int r = 0; r < DPn && cm; ++r)
+#pragma unroll
+      for (int s = 0; s < TMP && cm; ++s) {
+        const int cc = code[nib(perm, (q * DPn + r) * TMP + s) * 16 + nib(perm, ((q + 1) * DPn + r) * TMP + s)];
+        cm = cc < cm ? cc : cm;
+      }
+    if (q == 0) code0 = cm;
+    key = (key << p.sig_code_bits) | (uint64_t)cm;
+    if (store) {
+      if (p.need_bwcb) p.bwcb[u * p.max_pp + q] = (uint8_t)cm;
+      if (p.need_bwq) p.bwqb[u * p.max_pp + q] = p.bwval[cm];
+    }
+  }
+  return key;
+}
+
 // K_place's work for chunk item u: decode, early failures, placement,
 // boundary codes.  `store`: write placement / codes / values for the later
 // kernels (K_dp, K_est); else only return them (fused light path).
 // DT > 0: the device count as a compile-time constant (the Fisher-Yates
 // loop unrolls: constant shifts, constant-divisor modulo).
-template <int DT>
+template <int DT, bool FAST = false>
 __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& S, uint64_t u,
                                           bool store, CandWork& w, uint64_t& perm, int& code0) {
   const int D = DT > 0 ? DT : p.D, maxpp = p.max_pp;
@@ -129,7 +156,23 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
     int first_bad = -1;
     double bad_val = 0.0;
     uint64_t key = (uint64_t)c;  // DP signature (amp_dedup.cuh sig_key)
-    for (int q = 0; q < pp - 1; ++q) {
+    if constexpr (FAST) {  // p.shape16: every class a full 16-device shape, bandwidths > 0
+      switch (pp * 1024 + dp * 32 + tmp) {
+#define AMP_SHAPE(a, b, c)                                                        \
+  case a * 1024 + b * 32 + c:                                                     \
+    key = codes_shape<a, b, c>(p, S.code, perm, u, store, key, code0); \
+    break;
+        AMP_SHAPE(1, 1, 16) AMP_SHAPE(1, 2, 8) AMP_SHAPE(1, 4, 4) AMP_SHAPE(1, 8, 2) AMP_SHAPE(1, 16, 1)
+        AMP_SHAPE(2, 1, 8) AMP_SHAPE(2, 2, 4) AMP_SHAPE(2, 4, 2) AMP_SHAPE(2, 8, 1)
+        AMP_SHAPE(4, 1, 4) AMP_SHAPE(4, 2, 2) AMP_SHAPE(4, 4, 1)
+        AMP_SHAPE(8, 1, 2) AMP_SHAPE(8, 2, 1)
+        AMP_SHAPE(16, 1, 1)
+#undef AMP_SHAPE
+        default:
+          __trap();  // (the host sets shape16 only for these shapes)
+      }
+    }
+    for (int q = 0; !FAST && q < pp - 1; ++q) {
       int cm = 255;  // (code 0 is the smallest bandwidth: nothing can go lower)
       for (int r = 0; r < dp && cm; ++r)
         for (int s = 0; s < tmp && cm; ++s) {
@@ -141,7 +184,7 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
       if (q == 0) code0 = cm;
       key = (key << p.sig_code_bits) | (uint64_t)cm;
       if (store) {
-        p.bwcb[u * maxpp + q] = (uint8_t)cm;
+        if (p.need_bwcb) p.bwcb[u * maxpp + q] = (uint8_t)cm;
         if (p.need_bwq) p.bwqb[u * maxpp + q] = b;
       }
       if (first_bad < 0 && !(b > 0)) {
@@ -169,7 +212,7 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
   w.fail_value = fval;
 }
 
-template <int DT>
+template <int DT, bool FAST = false>
 __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
   __shared__ PlaceSmem S;
   place_smem_init(p, S);
@@ -181,7 +224,7 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
     CandWork w;
     uint64_t perm;
     int code0;
-    place_one<DT>(p, S, u, true, w, perm, code0);
+    place_one<DT, FAST>(p, S, u, true, w, perm, code0);
     p.work[u] = w;
   }
 }
@@ -284,7 +327,7 @@ __device__ __forceinline__ void est_fast_item(const EvalParams& p, const PlaceSm
   CandWork w;
   uint64_t perm = 0;
   int code0 = 0;
-  if (fused) place_one<DT>(p, PS, u, false, w, perm, code0);
+  if (fused) place_one<DT, true>(p, PS, u, false, w, perm, code0);
   else w = p.work[u];
   const ClassDev cl = p.cls[w.cls];
   int fc = w.fail_code;
