@@ -139,16 +139,27 @@ __device__ __forceinline__ bool slot_free(unsigned long long k, uint64_t epoch, 
   return sh >= 64 ? k == kHashEmpty : (k >> sh) != epoch;
 }
 
+// Lanes of a warp holding the same key (neighbouring placements of a class
+// often share a signature) elect one prober (__match_any_sync): a hot
+// signature's slot is read once per warp, not once per item, so the L2
+// line holding it does not serialise the whole grid.  The loop trip count is
+// uniform per warp for the warp-wide match / shuffle.
 __global__ void k_hash_insert(HashParams p) {
-  const int sh = p.epoch_shift;
+  const int sh = p.epoch_shift, lane = threadIdx.x & 31;
   const uint64_t tag = sh >= 64 ? 0 : (p.epoch << sh);
-  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < p.n;
-       u += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t key = p.sigkey ? p.sigkey[u]
-                                  : sig_key(p.work[u], p.cls, p.bwcb + u * p.max_pp, p.max_pp,
-                                            p.code_bits);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < p.n;
+       base += stride) {
+    const uint64_t u = base + lane;
+    const bool live = u < p.n;
+    const uint64_t key = !live ? kHashEmpty
+                         : p.sigkey ? p.sigkey[u]
+                                    : sig_key(p.work[u], p.cls, p.bwcb + u * p.max_pp, p.max_pp,
+                                              p.code_bits);
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(peers) - 1;
     uint32_t slot = ~0u;
-    if (key != kHashEmpty) {
+    if (lane == leader && key != kHashEmpty) {
       const unsigned long long want = key | tag;
       uint64_t h = splitmix64(key) & p.mask;
       for (;;) {
@@ -168,7 +179,8 @@ __global__ void k_hash_insert(HashParams p) {
       }
       slot = (uint32_t)h;
     }
-    p.slot_of[u] = slot;
+    slot = __shfl_sync(0xffffffffu, slot, leader);
+    if (live) p.slot_of[u] = slot;
   }
 }
 
@@ -196,10 +208,19 @@ __global__ void k_hash_runs(HashParams p) {
 }
 
 __global__ void k_hash_scatter(HashParams p) {
-  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < p.n;
-       u += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t s = p.slot_of[u];
-    p.rep_of[u] = s == ~0u ? 0u : p.tval[s];
+  const int lane = threadIdx.x & 31;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < p.n;
+       base += stride) {
+    const uint64_t u = base + lane;
+    const bool live = u < p.n;
+    const uint32_t s = live ? p.slot_of[u] : ~0u;
+    const unsigned peers = __match_any_sync(0xffffffffu, s);  // one table read per distinct slot
+    const int leader = __ffs(peers) - 1;
+    uint32_t r = 0u;
+    if (lane == leader && s != ~0u) r = p.tval[s];
+    r = __shfl_sync(0xffffffffu, r, leader);
+    if (live) p.rep_of[u] = r;
   }
 }
 

@@ -129,7 +129,14 @@ constexpr int kTrieNB = 4;  // nodes per thread: they share the cell's work
 // depth j-1).  Per cut the predecessor index, t2 and the tolerance term are
 // shared by the thread's nodes; each node adds its parent's value and its
 // own edge (the per-candidate kernels' operations and order).
-__global__ void __launch_bounds__(256) k_trie_stage(TrieParams p, int j, uint64_t total,
+#ifndef AMP_TRIE_UNROLL
+#define AMP_TRIE_UNROLL 2
+#endif
+#ifndef AMP_TRIE_MINB
+#define AMP_TRIE_MINB 2
+#endif
+constexpr int kTrieUnroll = AMP_TRIE_UNROLL;
+__global__ void __launch_bounds__(256, AMP_TRIE_MINB) k_trie_stage(TrieParams p, int j, uint64_t total,
                                                     unsigned long long* exec) {
   __shared__ TrieSlot slot[kTrieMaxCls];
   __shared__ uint64_t ibase[kTrieMaxCls + 1];
@@ -212,6 +219,7 @@ __global__ void __launch_bounds__(256) k_trie_stage(TrieParams p, int j, uint64_
       bc[b] = -1;
     }
     const uint32_t Kp = S.K_p;
+#pragma unroll kTrieUnroll
     for (int cut = j - 1; cut < i; ++cut) {  // pipeline_dp.cpp:114-131
       const double t2 = Pi - Pf[cut];
       const double term = t2 > dm ? g1 * (t2 - dm) : 0.0;
