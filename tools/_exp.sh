@@ -1,6 +1,9 @@
 O=gpurun_out
 rm -f $O/exp.log
-python -m pytest tests/test_gpu_parity.py -q -x > $O/t.log 2>&1; echo t=$? >> $O/exp.log; tail -1 $O/t.log >> $O/exp.log
-AMP_CHUNK=3000000 python -m pytest tests/test_gpu_parity.py -q -x -k "full_sweep_1m or shape_kernels or memoised" > $O/t2.log 2>&1; echo t2=$? >> $O/exp.log; tail -1 $O/t2.log >> $O/exp.log
-python tools/prof_eval.py 100000000 >> $O/exp.log 2>&1
-AMP_DEDUP_SORT=1 python tools/prof_eval.py 100000000 >> $O/exp.log 2>&1
+run() { echo "== $*" >> $O/exp.log; env "$@" python tools/prof_eval.py 100000000 2>&1 | tail -1 >> $O/exp.log; }
+run AMP_X=0
+run AMP_EST_CARVEOUT=100
+run AMP_SEARCH_LIB=$PWD/variants/est_m5.so AMP_EST_CTAS_PER_SM=5 AMP_EST_CARVEOUT=100
+run AMP_SEARCH_LIB=$PWD/variants/est_m5.so AMP_EST_CTAS_PER_SM=5
+run AMP_SEARCH_LIB=$PWD/variants/est_m6.so AMP_EST_CTAS_PER_SM=6 AMP_EST_CARVEOUT=100
+run AMP_SEARCH_LIB=$PWD/variants/est_m6.so AMP_EST_CTAS_PER_SM=6

@@ -121,3 +121,45 @@ if os.path.exists(pe):
     with open(os.path.join(out, f"{tag}_kernel_counts.json"), "w") as f:
         json.dump(out_j, f, indent=1)
     print("kernel counts", out_j)
+
+# ---- per-candidate kernels: details + hottest source lines ---------------
+rep = os.path.join(src, "pe_full.ncu-rep")
+if os.path.exists(rep):
+    import re
+    pdet = rows(os.path.join(src, "pe_full_details.csv"))
+    syms = subprocess.run(["cuobjdump", "-symbols", os.path.join(ROOT, "paper_2210_07297_b200",
+                                                               "libamp_search.so")],
+                          capture_output=True, text=True).stdout
+    for short in ("k_est_t", "k_place_t"):
+        mine = [r for r in pdet if re.search(rf"\b{short}<", r["Kernel Name"])]
+        if not mine:
+            continue
+        kname = mine[0]["Kernel Name"]
+        sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                               "-k", f"regex:{short}", "--launch-count", "1"],
+                              capture_output=True, text=True).stdout.splitlines()
+        heads = [i for i, l in enumerate(sass) if l.startswith('"Kernel Name"')]
+        block = sass[heads[0]:heads[1] if len(heads) > 1 else len(sass)] if heads else []
+        tmpf = os.path.join(src, f"{short}_sass.csv")
+        with open(tmpf, "w") as f:
+            f.write("\n".join(block) + "\n")
+        # the launched instantiation (FAST shape kernels when present)
+        cands = re.findall(rf"_ZN3amp\d+{short}ILi16ELb[01]EEEvNS_10EvalParamsE", syms)
+        fast = "true" in kname or ", 1>" in kname
+        mang = next((c for c in cands if ("Lb1" in c) == fast), cands[0] if cands else "")
+        lines_txt = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), tmpf,
+                                    os.path.join(ROOT, "paper_2210_07297_b200", "libamp_search.so"),
+                                    mang, "25"], capture_output=True, text=True).stdout
+        with open(os.path.join(out, f"{tag}_{short}_ncu.txt"), "w") as f:
+            f.write(f"# ncu --set full --clock-control none --import-source on -k regex:'k_est_t|k_place_t' "
+                    f"(tools/gpu_round.sh) python tools/prof_eval.py 100000000 — first 64M-item chunk of "
+                    f"the measured run\n# kernel: {kname}\n\n## details\n")
+            seen = set()
+            for r in mine:
+                if r["Metric Name"] in want_details and r["Metric Name"] not in seen:
+                    seen.add(r["Metric Name"])
+                    f.write(f'{r["Section Name"]} | {r["Metric Name"]} | {r["Metric Unit"]} | '
+                            f'{r["Metric Value"]}\n')
+            f.write("\n## hottest source lines (tools/ncu_lines.py)\n")
+            f.write(lines_txt)
+        print("wrote", f"{tag}_{short}_ncu.txt")
