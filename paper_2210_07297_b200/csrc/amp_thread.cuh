@@ -407,8 +407,21 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
   }
   __syncthreads();
   __shared__ int wcount[kEstTWarps];
-  int w_n = 0, w_kf = 2;  // warp list size, k-th entry (failed flag, total)
+  // Warp top-k threshold: the rank key (failed flag, total, index) an item
+  // must beat (rank_less) to be handed to the leader — the warp list's k-th
+  // entry once it is full, before that the CTA list's k-th entry persisted
+  // from the previous chunk (an item that cannot beat it cannot reach the
+  // CTA's top-k), else nothing (w_kf = 2).  The exact key (index included)
+  // matters: a chunk of failing candidates would otherwise pass every item.
+  int w_n = 0, w_kf = 2;
   double w_kt = CUDART_INF;
+  uint64_t w_ki = ~0ull;
+  if (p.k > 0 && n_top == p.k) {
+    const amp_record& e = mytop[p.k - 1];
+    w_kf = e.fail_code < 0 ? 2 : (e.fail_code != 0 ? 1 : 0);
+    w_kt = e.total;
+    w_ki = e.index;
+  }
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   // uniform trip count per warp (the top-k hand-off is warp-synchronous)
   const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
@@ -678,7 +691,7 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
       bool cand = false;
       if (live) {
         const int rf = ok ? 0 : 1;
-        cand = !(rf > w_kf || (rf == 0 && w_kf == 0 && rec.total > w_kt));
+        cand = rf != w_kf ? rf < w_kf : (rf == 0 && rec.total != w_kt ? rec.total < w_kt : rec.index < w_ki);
         if (cand) stage_rec[wib][lane] = rec;
       }
       unsigned m = __ballot_sync(0xffffffffu, cand);
@@ -692,11 +705,13 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
         if (w_n == p.k) {
           w_kf = wtop[wib][p.k - 1].fail_code != 0;
           w_kt = wtop[wib][p.k - 1].total;
+          w_ki = wtop[wib][p.k - 1].index;
         }
       }
       w_n = __shfl_sync(0xffffffffu, w_n, 0);
       w_kf = __shfl_sync(0xffffffffu, w_kf, 0);
       w_kt = __shfl_sync(0xffffffffu, w_kt, 0);
+      w_ki = __shfl_sync(0xffffffffu, w_ki, 0);
     }
   }
   if (lane == 0) wcount[wib] = w_n;

@@ -1,9 +1,8 @@
 O=gpurun_out
 rm -f $O/exp.log
+python -m pytest tests/test_gpu_parity.py -q -x > $O/t.log 2>&1; echo t=$? >> $O/exp.log; tail -1 $O/t.log >> $O/exp.log
+AMP_CHUNK=3000000 python -m pytest tests/test_gpu_parity.py -q -x > $O/t2.log 2>&1; echo t2=$? >> $O/exp.log; tail -1 $O/t2.log >> $O/exp.log
 run() { echo "== $*" >> $O/exp.log; env "$@" python tools/prof_eval.py 100000000 2>&1 | tail -1 >> $O/exp.log; }
-run AMP_X=0
-run AMP_EST_CARVEOUT=100
-run AMP_SEARCH_LIB=$PWD/variants/est_m5.so AMP_EST_CTAS_PER_SM=5 AMP_EST_CARVEOUT=100
-run AMP_SEARCH_LIB=$PWD/variants/est_m5.so AMP_EST_CTAS_PER_SM=5
-run AMP_SEARCH_LIB=$PWD/variants/est_m6.so AMP_EST_CTAS_PER_SM=6 AMP_EST_CARVEOUT=100
-run AMP_SEARCH_LIB=$PWD/variants/est_m6.so AMP_EST_CTAS_PER_SM=6
+run PE_K=10
+run PE_K=10 AMP_CHUNK=100000000
+run PE_K=10 AMP_CHUNK=50000000

@@ -19,8 +19,8 @@ Pp = -(-n // n_cls)
 with Searcher(enc, placements_per_class=Pp, seed=0, dense_dp=dense) as s:
     for it in range(2):
         t0 = time.perf_counter()
-        top, _, _ = s.run(0, n, k=10)
+        top, _, _ = s.run(0, n, k=int(os.environ.get("PE_K", "10")))
         st = s.stats()
         print(f"run {it}: {n} candidates in {st['kernel_ms']:.3f} ms kernel, "
               f"{(time.perf_counter()-t0)*1e3:.1f} ms wall, place/dp/est {st['place_ms']:.2f}/{st['dp_ms']:.2f}/{st['est_ms']:.2f} ms, inner={st['dp_inner']:.3e} "
-              f"fp64={st['fp64_ops']:.3e} best={top[0]['total']!r}")
+              f"fp64={st['fp64_ops']:.3e} best={(top[0]['total'] if len(top) else None)!r}")
