@@ -479,6 +479,7 @@ __global__ void __launch_bounds__(kEstWarps * 32, 3) k_est(EvalParams p) {
   // as a conservative reject filter
   __shared__ double kth_total;
   __shared__ int kth_failed;
+  __shared__ unsigned long long kth_index;  // (failed k-th: failed items order by index)
   const int D = p.D, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, maxpp = p.max_pp;
   // smem: [bw matrix if |D| <= 32] [st, spar per warp: 2 * maxpp] [cuts per warp]
   //       [EstWarp per warp] [CTA top-k, k <= 32]
@@ -506,6 +507,7 @@ __global__ void __launch_bounds__(kEstWarps * 32, 3) k_est(EvalParams p) {
     n_top = 0;
     kth_total = CUDART_INF;
     kth_failed = 2;
+    kth_index = ~0ull;
     if (!p.first_chunk) {  // CTA lists persist across chunks
       for (int x = 0; x < p.k; ++x) {
         if (gtop[x].fail_code < 0) break;
@@ -515,6 +517,7 @@ __global__ void __launch_bounds__(kEstWarps * 32, 3) k_est(EvalParams p) {
       if (p.k > 0 && n_top == p.k) {
         kth_failed = mytop[p.k - 1].fail_code != 0;
         kth_total = mytop[p.k - 1].total;
+        kth_index = mytop[p.k - 1].index;
       }
     }
   }
@@ -733,7 +736,11 @@ __global__ void __launch_bounds__(kEstWarps * 32, 3) k_est(EvalParams p) {
         const int kf = *(volatile int*)&kth_failed;
         const double kt = *(volatile double*)&kth_total;
         const int rf = ok ? 0 : 1;
-        const bool reject = rf > kf || (rf == 0 && kf == 0 && rec.total > kt);
+        // (failed items: the index decides; the k-th only improves, so a
+        // stale read is looser, never stricter)
+        const unsigned long long ki = *(volatile unsigned long long*)&kth_index;
+        const bool reject = rf > kf || (rf == 0 && kf == 0 && rec.total > kt) ||
+                            (rf == 1 && kf == 1 && rec.index > ki);
         if (!reject) {
           while (atomicCAS(&lock, 0, 1) != 0) __nanosleep(32);
           __threadfence_block();
@@ -743,6 +750,7 @@ __global__ void __launch_bounds__(kEstWarps * 32, 3) k_est(EvalParams p) {
           if (n == p.k) {
             *(volatile int*)&kth_failed = mytop[p.k - 1].fail_code != 0;
             *(volatile double*)&kth_total = mytop[p.k - 1].total;
+            *(volatile unsigned long long*)&kth_index = mytop[p.k - 1].index;
           }
           __threadfence_block();
           atomicExch(&lock, 0);
