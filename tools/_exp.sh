@@ -1,8 +1,6 @@
 O=gpurun_out
 rm -f $O/exp.log
-python -m pytest tests/test_gpu_parity.py -q -x > $O/t.log 2>&1; echo t=$? >> $O/exp.log; tail -1 $O/t.log >> $O/exp.log
-AMP_CHUNK=3000000 python -m pytest tests/test_gpu_parity.py -q -x > $O/t2.log 2>&1; echo t2=$? >> $O/exp.log; tail -1 $O/t2.log >> $O/exp.log
-run() { echo "== $*" >> $O/exp.log; env "$@" python tools/prof_eval.py 100000000 2>&1 | tail -1 >> $O/exp.log; }
-run PE_K=10
-run PE_K=10 AMP_CHUNK=100000000
-run PE_K=10 AMP_CHUNK=50000000
+ncu --set full --clock-control none --import-source on -k regex:"k_est_t|k_place_t" -s 4 -c 4 -o $O/pe_full -f \
+    python tools/prof_eval.py 100000000 > $O/ncu_pe.log 2>&1; echo pe=$? >> $O/exp.log
+ncu -i $O/pe_full.ncu-rep --page raw --csv > $O/pe_full_raw.csv 2>/dev/null
+ncu -i $O/pe_full.ncu-rep --page details --csv > $O/pe_full_details.csv 2>/dev/null

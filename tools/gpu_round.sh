@@ -16,7 +16,7 @@ ncu -i $O/kdp_full.ncu-rep --page details --csv > $O/kdp_full_details.csv 2>/dev
 ncu -i $O/kdp_full.ncu-rep --page source --csv --print-source sass > $O/kdp_full_sass.csv 2>/dev/null
 # the per-candidate kernels (thread K_place / K_est) on the bench workload:
 # one launch each of the measured run (100M candidates: chunks of 64M + 36M)
-ncu --set full --clock-control none --import-source on -k regex:"k_est_t|k_place_t" -s 4 -c 2 -o $O/pe_full -f \
+ncu --set full --clock-control none --import-source on -k regex:"k_est_t|k_place_t" -s 4 -c 4 -o $O/pe_full -f \
     python tools/prof_eval.py 100000000 > $O/ncu_pe.log 2>&1; echo pe=$?
 ncu -i $O/pe_full.ncu-rep --page raw --csv > $O/pe_full_raw.csv 2>/dev/null
 ncu -i $O/pe_full.ncu-rep --page details --csv > $O/pe_full_details.csv 2>/dev/null

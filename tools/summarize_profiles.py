@@ -101,23 +101,31 @@ if os.path.exists(pe):
     raw = [r for r in csv.reader(open(pe)) if r and not r[0].startswith("==")]
     hdr, unit = raw[0], raw[1]
     n_cls, P = 70, -(-100_000_000 // 70)
-    chunk = 64 << 20
-    heavy = min(chunk, 32 * P)
-    items = {"k_place_t": heavy, "k_est_t": chunk}
+    heavy = 32 * P  # pp >= 3 items: K_place's work (K_est: every item)
+    items = {"k_place_t": heavy, "k_est_t": 100_000_000}
     out_j = {"source": f"profiles/{tag}_kernel_counts.json from ncu --set full (tools/gpu_round.sh)",
-             "workload": "hetero_cluster sweep, 100M candidates, first 64M-item chunk"}
+             "workload": "hetero_cluster sweep, 100M candidates: every launch of one measured run "
+                         "(2 chunks), summed per kernel"}
+    scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+    acc = {}
     for row in raw[2:]:
         d = dict(zip(hdr, row))
         name = d["Kernel Name"].split("(")[0].split("<")[0].split("::")[-1].split()[-1]
-        n = items.get(name)
-        if not n:
+        if name not in items:
             continue
-        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
         rd = float(d["dram__bytes_read.sum"]) * scale[unit[hdr.index("dram__bytes_read.sum")]]
         wr = float(d["dram__bytes_write.sum"]) * scale[unit[hdr.index("dram__bytes_write.sum")]]
-        out_j[name] = {"items": n, "warp_inst_per_item": float(d["smsp__inst_executed.sum"]) / n,
-                       "dram_bytes_per_item": (rd + wr) / n,
-                       "duration_ms": float(d["gpu__time_duration.sum"])}
+        tu = unit[hdr.index("gpu__time_duration.sum")]
+        ms = float(d["gpu__time_duration.sum"]) * {"ms": 1.0, "us": 1e-3, "ns": 1e-6}.get(tu, 1.0)
+        a = acc.setdefault(name, [0.0, 0.0, 0.0, 0])
+        a[0] += float(d["smsp__inst_executed.sum"])
+        a[1] += rd + wr
+        a[2] += ms
+        a[3] += 1
+    for name, (inst, byts, ms, nl) in acc.items():
+        n = items[name]
+        out_j[name] = {"items": n, "launches": nl, "warp_inst_per_item": inst / n,
+                       "dram_bytes_per_item": byts / n, "duration_ms": ms}
     with open(os.path.join(out, f"{tag}_kernel_counts.json"), "w") as f:
         json.dump(out_j, f, indent=1)
     print("kernel counts", out_j)
