@@ -408,3 +408,42 @@ def test_records_only_failure_paths_match_oracle(kind):
     for f in ("total", "pipeline_time", "dpsync_time"):
         assert np.array_equal(allr[f][ok], orec[f][ok]), f
     assert top["index"].tolist() == orec["index"][B.oracle_rank(orec)[:5]].tolist()
+
+
+def test_sweep_1e9_topk_and_sample_vs_oracle():
+    """SURVEY §8(d) parity at N > 1e6: a 10^9-candidate hetero_cluster sweep
+    (16 chunks through the production path) — every top-k entry equals the
+    oracle's evaluation of that index, the top-k is sorted under the rank
+    key, and 20,000 seeded random indices evaluated on the device are
+    bit-equal to the oracle with none beating the k-th entry."""
+    sc = scenario("hetero_cluster")
+    enc = P.EncodedProblem.from_scenario(sc)
+    n = 10 ** 9
+    P_ = -(-n // 70)
+    k = 32
+    with planner.Searcher(enc, placements_per_class=P_, seed=0) as s:
+        top, _, _ = s.run(0, n, k=k)
+        rng = np.random.default_rng(2022)
+        sample = np.unique(rng.integers(0, n, 20000).astype(np.uint64))
+        srec, _ = s.evaluate(sample, details=False, placement=False)
+    o = B.Oracle(enc, P_, 0)
+
+    def oracle_rec(i):
+        rec = np.zeros(1, dtype=planner.RECORD_DTYPE)
+        o.lib.oracle_evaluate(o.h, int(i), rec.ctypes.data_as(B._recp), None, None, None)
+        return rec[0]
+
+    assert len(top) == k
+    for r in top:
+        e = oracle_rec(r["index"])
+        assert int(e["fail_code"]) == int(r["fail_code"]) == 0
+        assert e["total"] == r["total"] and e["pipeline_time"] == r["pipeline_time"]
+    key = [(float(r["total"]), int(r["index"])) for r in top]
+    assert key == sorted(key)
+    kth = key[-1]
+    for i, r in zip(sample, srec):
+        e = oracle_rec(i)
+        assert int(e["fail_code"]) == int(r["fail_code"]), int(i)
+        if e["fail_code"] == 0:
+            assert e["total"] == r["total"], int(i)
+            assert (float(r["total"]), int(i)) >= kth or int(i) in set(top["index"].tolist())
