@@ -162,7 +162,15 @@ struct EvalParams {
   int32_t sig_code_bits;      // bits per boundary code in the key
   int32_t est_fast;           // K_est_t uses the unrolled shape kernels (amp_thread.cuh est_shape)
   int32_t need_bwcb;          // K_place stores the boundary codes (bwcb)
-  int32_t pad9;
+  int32_t fuse_hash;          // K_place_t inserts the signature keys itself (amp_dedup.cuh)
+  // the signature hash table of this chunk (fuse_hash; see HashParams)
+  unsigned long long* h_tkey;
+  uint32_t* h_tval;
+  uint32_t* h_slot_of;
+  uint32_t* h_uniq;
+  unsigned long long* h_nuniq;
+  uint64_t h_mask, h_epoch;
+  int32_t h_eshift, pad10;
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

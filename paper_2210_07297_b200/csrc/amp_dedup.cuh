@@ -144,6 +144,39 @@ __device__ __forceinline__ bool slot_free(unsigned long long k, uint64_t epoch, 
 // signature's slot is read once per warp, not once per item, so the L2
 // line holding it does not serialise the whole grid.  The loop trip count is
 // uniform per warp for the warp-wide match / shuffle.
+// Warp-cooperative insert (all 32 lanes call it): lanes with equal keys
+// elect one prober; returns the key's slot (~0u for kHashEmpty).
+__device__ __forceinline__ uint32_t hash_insert_warp(uint64_t key, uint64_t u, int lane,
+                                                     unsigned long long* tkey, uint32_t* tval,
+                                                     uint32_t* uniq, unsigned long long* n_uniq,
+                                                     uint64_t mask, uint64_t tag, uint64_t epoch,
+                                                     int sh) {
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const int leader = __ffs(peers) - 1;
+  uint32_t slot = ~0u;
+  if (lane == leader && key != kHashEmpty) {
+    const unsigned long long want = key | tag;
+    uint64_t h = splitmix64(key) & mask;
+    for (;;) {
+      unsigned long long k = *(volatile unsigned long long*)&tkey[h];
+      if (k == want) break;
+      if (slot_free(k, epoch, sh)) {
+        const unsigned long long old = atomicCAS(&tkey[h], k, want);
+        if (old == k) {  // first writer of this key in this epoch
+          tval[h] = (uint32_t)u;
+          uniq[atomicAdd(n_uniq, 1ull)] = (uint32_t)h;
+          break;
+        }
+        if (old == want) break;
+        k = old;  // lost to another key: probe on
+      }
+      h = (h + 1) & mask;
+    }
+    slot = (uint32_t)h;
+  }
+  return __shfl_sync(0xffffffffu, slot, leader);
+}
+
 __global__ void k_hash_insert(HashParams p) {
   const int sh = p.epoch_shift, lane = threadIdx.x & 31;
   const uint64_t tag = sh >= 64 ? 0 : (p.epoch << sh);
@@ -156,30 +189,8 @@ __global__ void k_hash_insert(HashParams p) {
                          : p.sigkey ? p.sigkey[u]
                                     : sig_key(p.work[u], p.cls, p.bwcb + u * p.max_pp, p.max_pp,
                                               p.code_bits);
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    const int leader = __ffs(peers) - 1;
-    uint32_t slot = ~0u;
-    if (lane == leader && key != kHashEmpty) {
-      const unsigned long long want = key | tag;
-      uint64_t h = splitmix64(key) & p.mask;
-      for (;;) {
-        unsigned long long k = *(volatile unsigned long long*)&p.tkey[h];
-        if (k == want) break;
-        if (slot_free(k, p.epoch, sh)) {
-          const unsigned long long old = atomicCAS(&p.tkey[h], k, want);
-          if (old == k) {  // first writer of this key in this epoch
-            p.tval[h] = (uint32_t)u;
-            p.uniq[atomicAdd(p.n_uniq, 1ull)] = (uint32_t)h;
-            break;
-          }
-          if (old == want) break;
-          k = old;  // lost to another key: probe on
-        }
-        h = (h + 1) & p.mask;
-      }
-      slot = (uint32_t)h;
-    }
-    slot = __shfl_sync(0xffffffffu, slot, leader);
+    const uint32_t slot = hash_insert_warp(key, u, lane, p.tkey, p.tval, p.uniq, p.n_uniq, p.mask,
+                                           tag, p.epoch, sh);
     if (live) p.slot_of[u] = slot;
   }
 }

@@ -1259,6 +1259,57 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   }
   ctx->kev_used = 4 * n_chunks;
   ctx->kev_pending = true;
+  // signature hash table of a chunk (amp_dedup.cuh): sized for ep.n_dp
+  // items at load <= 1/2; entries carry an epoch tag above the key bits, so
+  // the table is cleared only when it is (re)allocated or the tag wraps
+  auto prepare_hash = [&](HashParams& hp) -> int {
+    uint64_t T = 1024;
+    while (T < 2 * ep.n_dp) T <<= 1;
+    const bool grown = ctx->dd_tkey.bytes < sizeof(uint64_t) * T;
+    CK(ctx->dd_tkey.ensure(sizeof(uint64_t) * T));
+    CK(ctx->dd_tval.ensure(sizeof(uint32_t) * T));
+    CK(ctx->dd_slot.ensure(sizeof(uint32_t) * C));
+    CK(ctx->dd_uniq.ensure(sizeof(uint32_t) * C));
+    CK(ctx->dd_nuniq.ensure(sizeof(unsigned long long)));
+    const int esh = 64 - ctx->key_bits >= 8 ? ctx->key_bits : 64;
+    if (esh >= 64) {
+      CK(cudaMemsetAsync(ctx->dd_tkey.p, 0xff, sizeof(uint64_t) * T, ctx->stream));
+    } else {
+      const uint64_t max_epoch = (1ull << (64 - esh)) - 1;
+      if (grown || ctx->hash_T != T || ctx->hash_epoch >= max_epoch) {
+        CK(cudaMemsetAsync(ctx->dd_tkey.p, 0, sizeof(uint64_t) * T, ctx->stream));
+        ctx->hash_epoch = 0;
+      }
+      ++ctx->hash_epoch;
+    }
+    ctx->hash_T = T;
+    CK(cudaMemsetAsync(ctx->dd_nuniq.p, 0, sizeof(unsigned long long), ctx->stream));
+    hp = HashParams{};
+    hp.work = ep.work;
+    hp.cls = ep.cls;
+    hp.bwcb = ep.bwcb;
+    hp.n = ep.n_dp;
+    hp.max_pp = ctx->max_pp;
+    hp.code_bits = ctx->code_bits;
+    hp.mask = T - 1;
+    hp.epoch = ctx->hash_epoch;
+    hp.epoch_shift = esh;
+    hp.sigkey = ep.sigkey;
+    hp.tkey = ctx->dd_tkey.as<unsigned long long>();
+    hp.tval = ctx->dd_tval.as<uint32_t>();
+    hp.slot_of = ctx->dd_slot.as<uint32_t>();
+    hp.uniq = ctx->dd_uniq.as<uint32_t>();
+    hp.n_uniq = ctx->dd_nuniq.as<unsigned long long>();
+    hp.skeys = ctx->dd_skeys.as<uint64_t>();
+    hp.sslots = ctx->dd_svals.as<uint32_t>();
+    hp.rep_key = ctx->trie ? ctx->dd_rep_key.as<uint64_t>() : nullptr;
+    return AMP_OK;
+  };
+  // K_place_t inserts the keys itself (no key round trip, one launch less)
+  const bool fuse_hash_ok = thread_mode && ep.sigkey && ctx->dedup && !d_given_cuts &&
+                            std::getenv("AMP_DEDUP_SORT") == nullptr &&
+                            std::getenv("AMP_NO_FUSE_HASH") == nullptr;
+  HashParams fused_hp{};
   for (uint64_t t0 = 0; t0 < n_work; t0 += C) {
     cudaEvent_t* ev = &ctx->kev[4 * (t0 / C)];
     CK(cudaEventRecord(ev[0], ctx->stream));
@@ -1272,6 +1323,20 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
                          ep.n_chunk * (ctx->max_pp + 1), cudaMemcpyDeviceToDevice, ctx->stream));
     }
     ep.first_chunk = t0 == 0;
+    ep.fuse_hash = 0;
+    if (fuse_hash_ok && ep.n_dp > 0) {
+      const int rc = prepare_hash(fused_hp);
+      if (rc != AMP_OK) return rc;
+      ep.fuse_hash = 1;
+      ep.h_tkey = fused_hp.tkey;
+      ep.h_tval = fused_hp.tval;
+      ep.h_slot_of = fused_hp.slot_of;
+      ep.h_uniq = fused_hp.uniq;
+      ep.h_nuniq = fused_hp.n_uniq;
+      ep.h_mask = fused_hp.mask;
+      ep.h_epoch = fused_hp.epoch;
+      ep.h_eshift = fused_hp.epoch_shift;
+    }
     const uint64_t warps = ep.n_chunk;
     const int place_grid = (int)std::min<uint64_t>((warps + 7) / 8, (uint64_t)ctx->sms * 16);
     if (thread_mode) {
@@ -1330,52 +1395,17 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
         ctx->launches += 6;
       } else {
         // hash the item keys (amp_dedup.cuh), sort only the distinct ones
-        uint64_t T = 1024;
-        while (T < 2 * ep.n_dp) T <<= 1;
-        const bool grown = ctx->dd_tkey.bytes < sizeof(uint64_t) * T;
-        CK(ctx->dd_tkey.ensure(sizeof(uint64_t) * T));
-        CK(ctx->dd_tval.ensure(sizeof(uint32_t) * T));
-        CK(ctx->dd_slot.ensure(sizeof(uint32_t) * C));
-        CK(ctx->dd_uniq.ensure(sizeof(uint32_t) * C));
-        CK(ctx->dd_nuniq.ensure(sizeof(unsigned long long)));
-        // epoch tags above the key bits: the table is cleared only when it
-        // is (re)allocated or the tag wraps (amp_dedup.cuh slot_free)
-        const int esh = 64 - ctx->key_bits >= 8 ? ctx->key_bits : 64;
-        if (esh >= 64) {
-          CK(cudaMemsetAsync(ctx->dd_tkey.p, 0xff, sizeof(uint64_t) * T, ctx->stream));
-        } else {
-          const uint64_t max_epoch = (1ull << (64 - esh)) - 1;
-          if (grown || ctx->hash_T != T || ctx->hash_epoch >= max_epoch) {
-            CK(cudaMemsetAsync(ctx->dd_tkey.p, 0, sizeof(uint64_t) * T, ctx->stream));
-            ctx->hash_epoch = 0;
-          }
-          ++ctx->hash_epoch;
-        }
-        ctx->hash_T = T;
-        CK(cudaMemsetAsync(ctx->dd_nuniq.p, 0, sizeof(unsigned long long), ctx->stream));
         HashParams hp{};
-        hp.work = ep.work;
-        hp.cls = ep.cls;
-        hp.bwcb = ep.bwcb;
-        hp.n = ep.n_dp;
-        hp.max_pp = ctx->max_pp;
-        hp.code_bits = ctx->code_bits;
-        hp.mask = T - 1;
-        hp.epoch = ctx->hash_epoch;
-        hp.epoch_shift = esh;
-        hp.sigkey = ep.sigkey;
-        hp.tkey = ctx->dd_tkey.as<unsigned long long>();
-        hp.tval = ctx->dd_tval.as<uint32_t>();
-        hp.slot_of = ctx->dd_slot.as<uint32_t>();
-        hp.uniq = ctx->dd_uniq.as<uint32_t>();
-        hp.n_uniq = ctx->dd_nuniq.as<unsigned long long>();
-        hp.skeys = ctx->dd_skeys.as<uint64_t>();
-        hp.sslots = ctx->dd_svals.as<uint32_t>();
-        hp.rep_key = ctx->trie ? ctx->dd_rep_key.as<uint64_t>() : nullptr;
+        if (ep.fuse_hash) {
+          hp = fused_hp;  // table prepared before K_place_t, which inserted the keys
+        } else {
+          const int rc = prepare_hash(hp);
+          if (rc != AMP_OK) return rc;
+        }
         hp.rep_list = dp.rep_list;
         hp.rep_of = dp.rep_of;
         hp.n_rep = dp.n_rep;
-        k_hash_insert<<<g, 256, 0, ctx->stream>>>(hp);
+        if (!ep.fuse_hash) k_hash_insert<<<g, 256, 0, ctx->stream>>>(hp);
         unsigned long long nu = 0;
         CK(cudaMemcpyAsync(&nu, ctx->dd_nuniq.p, sizeof nu, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));

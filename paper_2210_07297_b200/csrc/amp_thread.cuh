@@ -17,6 +17,7 @@
 #pragma once
 
 #include "amp_common.cuh"
+#include "amp_dedup.cuh"
 #include "amp_pipeline.cuh"
 
 namespace amp {
@@ -96,7 +97,9 @@ __device__ __forceinline__ uint64_t codes_shape(const EvalParams& p, const uint8
 // loop unrolls: constant shifts, constant-divisor modulo).
 template <int DT, bool FAST = false>
 __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& S, uint64_t u,
-                                          bool store, CandWork& w, uint64_t& perm, int& code0) {
+                                          bool store, CandWork& w, uint64_t& perm, int& code0,
+                                          uint64_t* sig = nullptr) {
+  if (sig) *sig = ~0ull;
   const int D = DT > 0 ? DT : p.D, maxpp = p.max_pp;
   uint64_t index, out, pl;
   int c;
@@ -196,11 +199,13 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
       fc = AMP_FAIL_P2P_BANDWIDTH;
       fval = bad_val;
     }
-    if (store && p.sigkey) {  // zero codes pad the unused boundaries
+    if (store && (p.sigkey || sig)) {  // zero codes pad the unused boundaries
       key <<= (uint64_t)p.sig_code_bits * (uint64_t)(maxpp - (pp > 0 ? pp : 1));
-      p.sigkey[u] = (fc == 0 && pp >= 3) ? key : ~0ull;
+      key = (fc == 0 && pp >= 3) ? key : ~0ull;
+      if (sig) *sig = key;
+      else p.sigkey[u] = key;
     }
-  } else if (store && p.sigkey) {
+  } else if (store && p.sigkey && !sig) {
     p.sigkey[u] = ~0ull;
   }
   w.index = index;
@@ -220,6 +225,29 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
   // fused light path: K_est_t places the pp <= 2 tail itself
   const uint64_t n = p.fuse_light ? p.n_dp : p.n_chunk;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  if (p.fuse_hash) {
+    // the signature hash insert (amp_dedup.cuh k_hash_insert) fused: the key
+    // goes from registers into the table; warp-uniform trip count for the
+    // warp-cooperative probe
+    const int lane = threadIdx.x & 31, sh = p.h_eshift;
+    const uint64_t tag = sh >= 64 ? 0 : (p.h_epoch << sh);
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n;
+         base += stride) {
+      const uint64_t u = base + lane;
+      uint64_t key = kHashEmpty;
+      if (u < n) {
+        CandWork w;
+        uint64_t perm;
+        int code0;
+        place_one<DT, FAST>(p, S, u, true, w, perm, code0, &key);
+        p.work[u] = w;
+      }
+      const uint32_t slot = hash_insert_warp(key, u, lane, p.h_tkey, p.h_tval, p.h_uniq, p.h_nuniq,
+                                             p.h_mask, tag, p.h_epoch, sh);
+      if (u < n) p.h_slot_of[u] = slot;
+    }
+    return;
+  }
   for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
     CandWork w;
     uint64_t perm;

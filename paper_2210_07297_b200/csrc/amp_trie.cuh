@@ -123,7 +123,10 @@ struct TrieSlot {
   int32_t c, pair, gas, chunks;    // class, its (tmp, mbs) pair, gas, node chunks
 };
 
-constexpr int kTrieNB = 4;  // nodes per thread: they share the cell's work
+#ifndef AMP_TRIE_NB
+#define AMP_TRIE_NB 4
+#endif
+constexpr int kTrieNB = AMP_TRIE_NB;  // nodes per thread: they share the cell's work
 
 // Stage j: one thread per (class, cell x of N_j, chunk of kTrieNB nodes of
 // depth j-1).  Per cut the predecessor index, t2 and the tolerance term are
