@@ -171,6 +171,10 @@ struct EvalParams {
   unsigned long long* h_nuniq;
   uint64_t h_mask, h_epoch;
   int32_t h_eshift, pad10;
+  // K_est shape kernels: signature run of item u = run_of_slot[run_slot[u]]
+  // (the hash table after k_hash_runs) instead of the scattered rep_of[u]
+  const uint32_t* run_slot;
+  const uint32_t* run_of_slot;
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

@@ -1357,6 +1357,8 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     ep.rep_of = nullptr;
     ep.n_rep = nullptr;
     ep.repcuts = nullptr;
+    ep.run_slot = nullptr;
+    ep.run_of_slot = nullptr;
     bool skip_dp = false;
     if (ctx->dedup && !d_given_cuts && ep.n_dp > 0) {
       // ---- memoisation: one DP per distinct signature ---------------------
@@ -1420,7 +1422,14 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
                                              ctx->stream));
         }
         k_hash_runs<<<gu, 256, 0, ctx->stream>>>(hp);
-        k_hash_scatter<<<g, 256, 0, ctx->stream>>>(hp);
+        // the shape kernels look the run up through the table themselves
+        // (the trie reads rep_list / rep_key only); others need rep_of
+        if (ep.est_fast && ctx->trie && std::getenv("AMP_NO_RUN_SLOT") == nullptr) {
+          ep.run_slot = hp.slot_of;
+          ep.run_of_slot = hp.tval;
+        } else {
+          k_hash_scatter<<<g, 256, 0, ctx->stream>>>(hp);
+        }
         CK(cudaGetLastError());
         ctx->launches += 5;
       }

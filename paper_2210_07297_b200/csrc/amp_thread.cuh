@@ -276,8 +276,9 @@ __device__ __forceinline__ void est_shape(const EvalParams& p, const uint8_t* co
   const int L = p.L, LP = L + 1, maxpp = p.max_pp;
   int cuts[PP + 1];
   if (PP >= 3) {  // the signature run's cuts (memoised DP) or this item's
-    const uint8_t* ci = p.rep_of ? p.repcuts + (uint64_t)p.rep_of[u] * (maxpp + 1)
-                                 : p.cutsb + u * (maxpp + 1);
+    const uint8_t* ci = p.run_slot ? p.repcuts + (uint64_t)p.run_of_slot[p.run_slot[u]] * (maxpp + 1)
+                        : p.rep_of ? p.repcuts + (uint64_t)p.rep_of[u] * (maxpp + 1)
+                                   : p.cutsb + u * (maxpp + 1);
 #pragma unroll
     for (int q = 0; q <= PP; ++q) cuts[q] = ci[q];
   } else if (PP == 2) {
@@ -462,7 +463,8 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
       if (un < p.n_chunk && !(p.fuse_light && un >= p.n_dp)) {
         prefetch_l2(p.work + un);
         if (p.placep) prefetch_l2(p.placep + un);
-        if (p.rep_of && un < p.n_dp) prefetch_l2(p.rep_of + un);
+        if (p.run_slot && un < p.n_dp) prefetch_l2(p.run_slot + un);
+        else if (p.rep_of && un < p.n_dp) prefetch_l2(p.rep_of + un);
       }
     }
 #endif
