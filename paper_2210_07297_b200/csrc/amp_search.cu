@@ -184,6 +184,11 @@ struct amp_ctx {
   bool kev_pending = false;
   bool stats_exec_pending = false;  // exec counters of a memoised run to read back
   amp_stats stats{};
+  // light-tail overlap: K_est of the pp <= 2 items on a second stream while
+  // the heavy items go through K_place -> K_dp -> K_est
+  cudaStream_t aux = nullptr;
+  cudaEvent_t aux_start = nullptr, aux_done = nullptr;
+  int n_topk_lists = 0;  // CTA lists of the last launch_evaluate (main + aux)
 };
 
 #define CK(call)                                                                      \
@@ -1251,7 +1256,30 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   // path and K_est's pp == 2 items placed by K_place; with the hash dedup on
   // K_place's signature keys, the trie and the fused light path, nothing
   ep.need_bwcb = !(ep.sigkey && ctx->trie && ep.fuse_light && std::getenv("AMP_DEDUP_SORT") == nullptr);
-  const int n_chunks = (int)((n_work + C - 1) / C);
+  // ---- light tail on the aux stream -------------------------------------
+  // The pp <= 2 items [n_heavy, n_work) of a segment run need no K_place /
+  // K_dp (K_est places them itself), so their K_est runs on a second stream
+  // with its own CTA lists (after the main ones in cta_topk, merged with
+  // them) and a smaller grid, overlapping the heavy items' latency-bound
+  // K_dp.  Opt-in (AMP_OVERLAP=1): measured on the bench sweep it does not
+  // pay — K_place slows 2.1 -> 4.9 ms sharing the SMs, step 8.13 -> 8.32 ms.
+  const char* ax = std::getenv("AMP_AUX_CTAS_PER_SM");
+  const int aux_ctas = std::min(kMergeMaxLists - ctx->est_ctas, ctx->sms * (ax ? std::atoi(ax) : 2));
+  const bool overlap = ep.est_fast && ep.fuse_light && segs && n_heavy > 0 && n_heavy < n_work &&
+                       aux_ctas >= 1 && std::getenv("AMP_OVERLAP") != nullptr;
+  const uint64_t n_main = overlap ? n_heavy : n_work;
+  const int n_aux_chunks = overlap ? (int)((n_work - n_heavy + C - 1) / C) : 0;
+  ctx->n_topk_lists = ctx->est_ctas + (overlap ? aux_ctas : 0);
+  if (overlap) {
+    CK(ctx->cta_topk.ensure(sizeof(amp_record) * (size_t)kk * ctx->n_topk_lists));
+    ep.cta_topk = ctx->cta_topk.as<amp_record>();
+    if (!ctx->aux) {
+      CK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ctx->aux_start, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->aux_done, cudaEventDisableTiming));
+    }
+  }
+  const int n_chunks = (int)((n_main + C - 1) / C) + n_aux_chunks;
   while ((int)ctx->kev.size() < 4 * n_chunks) {
     cudaEvent_t e;
     CK(cudaEventCreate(&e));
@@ -1310,11 +1338,34 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
                             std::getenv("AMP_DEDUP_SORT") == nullptr &&
                             std::getenv("AMP_NO_FUSE_HASH") == nullptr;
   HashParams fused_hp{};
-  for (uint64_t t0 = 0; t0 < n_work; t0 += C) {
+  if (overlap) {
+    CK(cudaEventRecord(ctx->aux_start, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->aux, ctx->aux_start, 0));
+    EvalParams ea = ep;
+    ea.cta_topk = ep.cta_topk + (size_t)kk * ctx->est_ctas;
+    ea.n_dp = 0;
+    ea.fuse_hash = 0;
+    int a = 0;
+    for (uint64_t t0 = n_heavy; t0 < n_work; t0 += C, ++a) {
+      cudaEvent_t* ev = &ctx->kev[4 * ((n_main + C - 1) / C + a)];
+      CK(cudaEventRecord(ev[0], ctx->aux));
+      CK(cudaEventRecord(ev[1], ctx->aux));
+      CK(cudaEventRecord(ev[2], ctx->aux));
+      ea.t0 = t0;
+      ea.n_chunk = std::min<uint64_t>(C, n_work - t0);
+      ea.first_chunk = t0 == n_heavy;
+      k_est_t<16, true><<<aux_ctas, kEstTWarps * 32, 0, ctx->aux>>>(ea);
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(ev[3], ctx->aux));
+      ctx->launches += 1;
+    }
+    CK(cudaEventRecord(ctx->aux_done, ctx->aux));
+  }
+  for (uint64_t t0 = 0; t0 < n_main; t0 += C) {
     cudaEvent_t* ev = &ctx->kev[4 * (t0 / C)];
     CK(cudaEventRecord(ev[0], ctx->stream));
     ep.t0 = t0;
-    ep.n_chunk = std::min<uint64_t>(C, n_work - t0);
+    ep.n_chunk = std::min<uint64_t>(C, n_main - t0);
     ep.n_dp = n_heavy > t0 ? std::min<uint64_t>(ep.n_chunk, n_heavy - t0) : 0;
     ep.cuts_given = d_given_cuts != nullptr;
     if (d_given_cuts) {  // estimate only: the caller's cuts replace K_dp
@@ -1465,6 +1516,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     CK(cudaEventRecord(ev[3], ctx->stream));
     ctx->launches += 2;
   }
+  if (overlap) CK(cudaStreamWaitEvent(ctx->stream, ctx->aux_done, 0));
   return AMP_OK;
 }
 
@@ -1533,7 +1585,8 @@ int run_device_segs(amp_ctx* ctx, const std::vector<Segment>& segs, int32_t k, a
     CK(cudaStreamSynchronize(ctx->stream));
   }
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
-  rc = launch_merge(ctx, ctx->cta_topk.as<amp_record>(), k * ctx->est_ctas, k, d_topk, ctx->stream);
+  rc = launch_merge(ctx, ctx->cta_topk.as<amp_record>(),
+                    k * (n_work > 0 ? ctx->n_topk_lists : ctx->est_ctas), k, d_topk, ctx->stream);
   if (rc) return rc;
   CK(cudaEventRecord(ctx->ev2, ctx->stream));
   CK(cudaStreamWaitEvent(user, ctx->ev2, 0));
@@ -1612,6 +1665,10 @@ void amp_search_destroy(amp_ctx* ctx) {
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->ev2) cudaEventDestroy(ctx->ev2);
   for (cudaEvent_t e : ctx->kev) cudaEventDestroy(e);
+  if (ctx->aux) cudaStreamSynchronize(ctx->aux);
+  if (ctx->aux_start) cudaEventDestroy(ctx->aux_start);
+  if (ctx->aux_done) cudaEventDestroy(ctx->aux_done);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
   cudaStream_t st = ctx->stream;
   delete ctx;  // buffers return to the pool, ordered on the context stream
   if (st) cudaStreamDestroy(st);
@@ -1699,7 +1756,7 @@ int amp_search_run(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k, amp_re
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
   const int kk = std::max(1, k);
   CK(ctx->topk.ensure(sizeof(amp_record) * kk));
-  rc = launch_merge(ctx, ctx->cta_topk.as<amp_record>(), kk * ctx->est_ctas, kk,
+  rc = launch_merge(ctx, ctx->cta_topk.as<amp_record>(), kk * ctx->n_topk_lists, kk,
                     ctx->topk.as<amp_record>(), ctx->stream);
   if (rc) return rc;
   CK(cudaEventRecord(ctx->ev2, ctx->stream));

@@ -447,3 +447,22 @@ def test_sweep_1e9_topk_and_sample_vs_oracle():
         if e["fail_code"] == 0:
             assert e["total"] == r["total"], int(i)
             assert (float(r["total"]), int(i)) >= kth or int(i) in set(top["index"].tolist())
+
+
+def test_light_tail_overlap_equals_single_stream(monkeypatch):
+    """The opt-in light-tail overlap (AMP_OVERLAP=1: the pp <= 2 items' K_est
+    on a second stream with its own CTA lists) gives the same top-k and
+    records as the single-stream run."""
+    sc = scenario("hetero_cluster")
+    enc = P.EncodedProblem.from_scenario(sc)
+    outs = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("AMP_OVERLAP", env)
+        else:
+            monkeypatch.delenv("AMP_OVERLAP", raising=False)
+        with planner.Searcher(enc, placements_per_class=3000, seed=9) as s:
+            top, allr, _ = s.run(0, s.num_candidates, k=40, want_all=True, details=False)
+        outs.append((top, allr))
+    assert np.array_equal(outs[0][0].view(np.uint8), outs[1][0].view(np.uint8))
+    assert np.array_equal(outs[0][1].view(np.uint8), outs[1][1].view(np.uint8))
