@@ -133,17 +133,16 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
           const uint32_t d = (uint32_t)kk + 1u;  // constant: the compiler's divide-by-constant
           const uint32_t t32 = (uint32_t)(0x100000000ull % d);
           const uint32_t jj = (uint32_t)((((uint32_t)(r >> 32) % d) * t32 + ((uint32_t)r % d)) % d);
-          const uint64_t a = (perm >> (4 * kk)) & 0xf, b = (perm >> (4 * jj)) & 0xf;
-          perm &= ~((0xfull << (4 * kk)) | (0xfull << (4 * jj)));
-          perm |= (b << (4 * kk)) | (a << (4 * jj));
+          // swap nibbles kk and jj: x = a ^ b flips both (x = 0 when jj == kk)
+          const uint64_t x = ((perm >> (4 * kk)) ^ (perm >> (4 * jj))) & 0xf;
+          perm ^= (x << (4 * kk)) | (x << (4 * jj));
           r = splitmix64(r);
         }
       } else {
         for (int kk = D - 1; kk >= 1; --kk) {
           const int jj = (int)mod64_small(r, (uint32_t)kk + 1u, S.magic[kk + 1]);
-          const uint64_t a = (perm >> (4 * kk)) & 0xf, b = (perm >> (4 * jj)) & 0xf;
-          perm &= ~((0xfull << (4 * kk)) | (0xfull << (4 * jj)));
-          perm |= (b << (4 * kk)) | (a << (4 * jj));
+          const uint64_t x = ((perm >> (4 * kk)) ^ (perm >> (4 * jj))) & 0xf;  // (nibble swap)
+          perm ^= (x << (4 * kk)) | (x << (4 * jj));
           r = splitmix64(r);
         }
       }
