@@ -1,6 +1,4 @@
 O=gpurun_out
 rm -f $O/exp.log
-python -m pytest tests/test_gpu_parity.py -q -x > $O/t.log 2>&1; echo t=$? >> $O/exp.log; tail -1 $O/t.log >> $O/exp.log
-run() { echo "== $*" >> $O/exp.log; env "$@" python tools/prof_eval.py 100000000 2>&1 | tail -1 | sed 's/inner.*//' >> $O/exp.log; }
-run AMP_X=0
-run AMP_X=1
+python tools/plan_phases.py synthetic96 > $O/ph_sparse.log 2>&1; echo a=$? >> $O/exp.log
+PLAN_DENSE=1 python tools/plan_phases.py synthetic96 > $O/ph_dense.log 2>&1; echo b=$? >> $O/exp.log

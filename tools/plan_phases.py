@@ -16,5 +16,6 @@ for name in sys.argv[1:] or ["hetero_cluster", "synthetic96"]:
                          max_params_per_device=sc.options.max_params_per_device)
     for it in range(3):
         print(f"== {name} {it}", flush=True)
-        planner.plan(sc.model, sc.cluster, sc.profile, sc.gbs, opts)
+        planner.plan(sc.model, sc.cluster, sc.profile, sc.gbs, opts,
+                     dense_dp=os.environ.get("PLAN_DENSE") == "1")
         sys.stdout.flush()
