@@ -466,3 +466,24 @@ def test_light_tail_overlap_equals_single_stream(monkeypatch):
         outs.append((top, allr))
     assert np.array_equal(outs[0][0].view(np.uint8), outs[1][0].view(np.uint8))
     assert np.array_equal(outs[0][1].view(np.uint8), outs[1][1].view(np.uint8))
+
+
+@pytest.mark.parametrize("name", ["hetero_cluster", "hetero_model"])
+def test_multi_chunk_equals_single_chunk(name, monkeypatch):
+    """A sweep cut into many chunks (AMP_CHUNK: per-chunk hash epochs, CTA
+    top-k lists persisted across launches, pure-light chunks) gives the same
+    records and top-k as one chunk."""
+    sc = scenario(name)
+    enc = P.EncodedProblem.from_scenario(sc)
+    outs = []
+    for chunk in (None, "700000"):
+        if chunk:
+            monkeypatch.setenv("AMP_CHUNK", chunk)
+        else:
+            monkeypatch.delenv("AMP_CHUNK", raising=False)
+        with planner.Searcher(enc, placements_per_class=60000, seed=4) as s:
+            top, allr, _ = s.run(0, s.num_candidates, k=16, want_all=True, details=False)
+        outs.append((top, allr))
+    assert len(outs[1][1]) > 4 * 700000
+    assert np.array_equal(outs[0][0].view(np.uint8), outs[1][0].view(np.uint8))
+    assert np.array_equal(outs[0][1].view(np.uint8), outs[1][1].view(np.uint8))
