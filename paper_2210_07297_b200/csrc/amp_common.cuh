@@ -175,6 +175,9 @@ struct EvalParams {
   // (the hash table after k_hash_runs) instead of the scattered rep_of[u]
   const uint32_t* run_slot;
   const uint32_t* run_of_slot;
+  // per signature run of a dp == 1, pp >= 3 class: its pipeline time (the
+  // whole estimate: one replica, no dpsync; NaN = parameter ceiling fails)
+  const double* run_pipe;
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

@@ -166,6 +166,7 @@ struct amp_ctx {
   bool dedup = false;
   int code_bits = 0, key_bits = 0;
   DevBuf dd_keys, dd_vals, dd_skeys, dd_svals, dd_flags, dd_runid, dd_rep_list, dd_rep_of;
+  DevBuf dd_runpipe;  // per-run pipeline time of dp == 1 classes (k_run_pipe)
   DevBuf dd_nrep, dd_temp, dd_counters, prog_inner_d, dd_repcuts;
   DevBuf dd_tkey, dd_tval, dd_slot, dd_uniq, dd_nuniq, dd_sigkey;  // hash dedup
   uint64_t hash_epoch = 0, hash_T = 0;
@@ -1410,6 +1411,8 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     ep.repcuts = nullptr;
     ep.run_slot = nullptr;
     ep.run_of_slot = nullptr;
+    ep.run_pipe = nullptr;
+    uint64_t n_runs_host = 0;  // distinct signatures of the chunk (hash path)
     bool skip_dp = false;
     if (ctx->dedup && !d_given_cuts && ep.n_dp > 0) {
       // ---- memoisation: one DP per distinct signature ---------------------
@@ -1462,6 +1465,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
         unsigned long long nu = 0;
         CK(cudaMemcpyAsync(&nu, ctx->dd_nuniq.p, sizeof nu, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
+        n_runs_host = nu;
         const int gu = (int)std::min<uint64_t>((nu + 255) / 256 + 1, (uint64_t)ctx->sms * 8);
         k_hash_gather<<<gu, 256, 0, ctx->stream>>>(hp, ctx->dd_keys.as<uint64_t>(),
                                                     ctx->dd_vals.as<uint32_t>());
@@ -1492,6 +1496,15 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
         const int rc = run_trie(ctx, ep);
         if (rc != AMP_OK) return rc;
         skip_dp = true;  // K_dp's work is done (K_est reads the cuts via rep_of)
+        if (ep.est_fast && n_runs_host > 0 && std::getenv("AMP_NO_RUN_PIPE") == nullptr) {
+          CK(ctx->dd_runpipe.ensure(sizeof(double) * n_runs_host));
+          const int gr = (int)std::min<uint64_t>((n_runs_host + 255) / 256, (uint64_t)ctx->sms * 8);
+          k_run_pipe<<<gr, 256, 0, ctx->stream>>>(ep, ctx->dd_rep_key.as<uint64_t>(), n_runs_host,
+                                                   ctx->dd_runpipe.as<double>());
+          CK(cudaGetLastError());
+          ctx->launches += 1;
+          ep.run_pipe = ctx->dd_runpipe.as<double>();
+        }
       }
     }
     ctx->stats.dp_items += ep.n_dp;

@@ -275,9 +275,20 @@ __device__ __forceinline__ void est_shape(const EvalParams& p, const uint8_t* co
   const int L = p.L, LP = L + 1, maxpp = p.max_pp;
   int cuts[PP + 1];
   if (PP >= 3) {  // the signature run's cuts (memoised DP) or this item's
-    const uint8_t* ci = p.run_slot ? p.repcuts + (uint64_t)p.run_of_slot[p.run_slot[u]] * (maxpp + 1)
-                        : p.rep_of ? p.repcuts + (uint64_t)p.rep_of[u] * (maxpp + 1)
-                                   : p.cutsb + u * (maxpp + 1);
+    const uint64_t run = p.run_slot ? p.run_of_slot[p.run_slot[u]] : p.rep_of ? p.rep_of[u] : ~0ull;
+    if (DPn == 1 && p.run_pipe) {
+      // one replica whose boundary codes are the signature's: the whole
+      // estimate is a function of the run (k_run_pipe, same operations)
+      const double v = p.run_pipe[run];
+      if (v != v) {
+        fc = AMP_FAIL_CEILING;
+      } else {
+        pipeline = v;
+        dpsync = 0.0;
+      }
+      return;
+    }
+    const uint8_t* ci = run != ~0ull ? p.repcuts + run * (maxpp + 1) : p.cutsb + u * (maxpp + 1);
 #pragma unroll
     for (int q = 0; q <= PP; ++q) cuts[q] = ci[q];
   } else if (PP == 2) {
@@ -343,6 +354,42 @@ __device__ __forceinline__ void est_shape(const EvalParams& p, const uint8_t* co
   }
   pipeline = (double)(cl.gas - 1) * slowest + sum;
   dpsync = worst;
+}
+
+// Per signature run of a dp == 1, pp >= 3 class: est_shape's estimate with
+// one replica (its edge codes are the signature's boundary codes — the
+// K_place minimum over replicas x shards with a single replica), so K_est
+// reads one value per item.  Same operations and order as est_shape.
+__global__ void k_run_pipe(EvalParams p, const uint64_t* rep_key, uint64_t n_runs, double* out) {
+  const int nq = p.max_pp - 1, cb = p.sig_code_bits, L = p.L, LP = L + 1, maxpp = p.max_pp;
+  const uint64_t cmask = (1ull << cb) - 1;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_runs;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = rep_key[r];
+    const int c = (int)(key >> (nq * cb));
+    const ClassDev cl = p.cls[c];
+    if (cl.dp != 1 || cl.pp < 3) continue;
+    const uint8_t* ci = p.repcuts + r * (maxpp + 1);
+    const double* qt = p.qtab + (size_t)c * p.n_codes * L;
+    double esum = 0.0;
+    for (int q = 0; q < cl.pp - 1; ++q) {
+      const int code = (int)((key >> ((nq - 1 - q) * cb)) & cmask);
+      esum = esum + qt[(size_t)code * L + ci[q + 1]];
+    }
+    double emax = -CUDART_INF;
+    emax = emax < esum ? esum : emax;
+    const double* rt = p.rsum_t + (size_t)cl.pair * LP * LP;
+    double slowest = 0.0, sum = emax, worst_p = 0.0;
+    for (int j = 0; j < cl.pp; ++j) {
+      const int a = ci[j] * LP + ci[j + 1];
+      const double stj = rt[a], spj = p.rsum_p[a];
+      slowest = (j == 0 || slowest < stj) ? stj : slowest;
+      sum = sum + stj;
+      if (p.has_ceiling) worst_p = std_max(worst_p, spj / cl.tmp);
+    }
+    out[r] = (p.has_ceiling && worst_p > p.ceiling) ? CUDART_NAN
+                                                    : (double)(cl.gas - 1) * slowest + sum;
+  }
 }
 
 // One candidate through the shape kernels (p.est_fast: |D| == 16, every class

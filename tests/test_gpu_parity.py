@@ -487,3 +487,33 @@ def test_multi_chunk_equals_single_chunk(name, monkeypatch):
     assert len(outs[1][1]) > 4 * 700000
     assert np.array_equal(outs[0][0].view(np.uint8), outs[1][0].view(np.uint8))
     assert np.array_equal(outs[0][1].view(np.uint8), outs[1][1].view(np.uint8))
+
+
+@pytest.mark.parametrize("ceiling", [None, 1.5e8, 5e7])
+def test_run_pipe_with_parameter_ceiling_matches_oracle(ceiling, monkeypatch):
+    """The per-run estimate of dp == 1 classes (k_run_pipe) and the shape
+    kernels under a per-device parameter ceiling (some candidates fail it):
+    records equal the oracle and the AMP_NO_RUN_PIPE=1 run, 16 devices."""
+    sc = scenario("hetero_cluster")
+    opts = P.PlanOptions(cost_options=sc.options.cost_options, max_params_per_device=ceiling)
+    enc = P.EncodedProblem(sc.model, sc.cluster, sc.profile, sc.gbs, opts)
+    outs = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("AMP_NO_RUN_PIPE", env)
+        else:
+            monkeypatch.delenv("AMP_NO_RUN_PIPE", raising=False)
+        with planner.Searcher(enc, placements_per_class=400, seed=21) as s:
+            top, allr, _ = s.run(0, s.num_candidates, k=12, want_all=True, details=False)
+        outs.append((top, allr))
+    assert np.array_equal(outs[0][1].view(np.uint8), outs[1][1].view(np.uint8))
+    assert np.array_equal(outs[0][0].view(np.uint8), outs[1][0].view(np.uint8))
+    o = B.Oracle(enc, 400, 21)
+    orec, _ = o.run(threads=8, details=False, memo=True)
+    allr = outs[0][1]
+    for f in ("index", "fail_code"):
+        assert np.array_equal(allr[f], orec[f]), f
+    ok = orec["fail_code"] == 0
+    assert np.array_equal(allr["total"][ok], orec["total"][ok])
+    if ceiling is not None:
+        assert (orec["fail_code"] == 3).any() and ok.any()  # AMP_FAIL_CEILING, some pass
