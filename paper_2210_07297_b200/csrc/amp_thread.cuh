@@ -125,7 +125,10 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
       const int32_t* g = p.given_place + (p.t0 + u) * D;
       perm = 0;
       for (int x = 0; x < D; ++x) perm |= (uint64_t)g[x] << (4 * x);
-    } else if (pl != 0) {
+    } else if (pl != 0 && (store || !FAST || pp != 1 || dp != 1)) {
+      // (a fused pp = dp = 1 item's estimate does not depend on where its
+      //  single stage sits: no edges, no all-reduce group — the shuffle is
+      //  skipped when nothing stores the placement)
       uint64_t r = splitmix64(p.seed ^ pl);
       if (DT > 0) {
 #pragma unroll
