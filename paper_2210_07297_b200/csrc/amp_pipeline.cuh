@@ -35,8 +35,13 @@ struct CandWork {
 // ---------------------------------------------------------------------------
 // work decode: item t of the run -> candidate
 // ---------------------------------------------------------------------------
+// hint (optional): the segment of this thread's previous item.  Grid-stride
+// loops visit increasing t, and a stride is shorter than a class segment, so
+// the segment is found by stepping forward from the hint (usually zero or
+// one step) instead of a dependent-load binary search per item.
 __device__ __forceinline__ void decode_item(const EvalParams& p, uint64_t t, uint64_t& index,
-                                            uint64_t& out, int& cls, uint64_t& pl) {
+                                            uint64_t& out, int& cls, uint64_t& pl,
+                                            int* hint = nullptr) {
   if (p.index_list) {
     index = p.index_list[t];
     out = t;
@@ -44,12 +49,20 @@ __device__ __forceinline__ void decode_item(const EvalParams& p, uint64_t t, uin
     pl = index % p.P;
     return;
   }
-  int lo = 0, hi = p.n_segs - 1;  // last segment with offset <= t
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(&p.segs[mid].offset) <= t) lo = mid;
-    else hi = mid - 1;
+  int lo;
+  if (hint && *hint >= 0 && __ldg(&p.segs[*hint].offset) <= t) {
+    lo = *hint;
+    while (lo + 1 < p.n_segs && __ldg(&p.segs[lo + 1].offset) <= t) ++lo;
+  } else {
+    lo = 0;
+    int hi = p.n_segs - 1;  // last segment with offset <= t
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(&p.segs[mid].offset) <= t) lo = mid;
+      else hi = mid - 1;
+    }
   }
+  if (hint) *hint = lo;
   const Segment& sg = p.segs[lo];
   const uint64_t d = t - sg.offset;
   index = sg.first + d;

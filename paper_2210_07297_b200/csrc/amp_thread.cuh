@@ -98,12 +98,12 @@ __device__ __forceinline__ uint64_t codes_shape(const EvalParams& p, const uint8
 template <int DT, bool FAST = false>
 __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& S, uint64_t u,
                                           bool store, CandWork& w, uint64_t& perm, int& code0,
-                                          uint64_t* sig = nullptr) {
+                                          uint64_t* sig = nullptr, int* seg_hint = nullptr) {
   if (sig) *sig = ~0ull;
   const int D = DT > 0 ? DT : p.D, maxpp = p.max_pp;
   uint64_t index, out, pl;
   int c;
-  decode_item(p, p.t0 + u, index, out, c, pl);
+  decode_item(p, p.t0 + u, index, out, c, pl, seg_hint);
   const ClassDev cl = p.cls[c];
   const PairDev pr = p.pairs[cl.pair];
   const int pp = cl.pp, dp = cl.dp, tmp = cl.tmp;
@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
     // warp-cooperative probe
     const int lane = threadIdx.x & 31, sh = p.h_eshift;
     const uint64_t tag = sh >= 64 ? 0 : (p.h_epoch << sh);
+    int hint = -1;
     for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n;
          base += stride) {
       const uint64_t u = base + lane;
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
         CandWork w;
         uint64_t perm;
         int code0;
-        place_one<DT, FAST>(p, S, u, true, w, perm, code0, &key);
+        place_one<DT, FAST>(p, S, u, true, w, perm, code0, &key, &hint);
         p.work[u] = w;
       }
       const uint32_t slot = hash_insert_warp(key, u, lane, p.h_tkey, p.h_tval, p.h_uniq, p.h_nuniq,
@@ -250,11 +251,12 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
     }
     return;
   }
+  int hint = -1;
   for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
     CandWork w;
     uint64_t perm;
     int code0;
-    place_one<DT, FAST>(p, S, u, true, w, perm, code0);
+    place_one<DT, FAST>(p, S, u, true, w, perm, code0, nullptr, &hint);
     p.work[u] = w;
   }
 }
@@ -400,12 +402,12 @@ __global__ void k_run_pipe(EvalParams p, const uint64_t* rep_key, uint64_t n_run
 // detail outputs, no given cuts).
 template <int DT>
 __device__ __forceinline__ void est_fast_item(const EvalParams& p, const PlaceSmem& PS, uint64_t u,
-                                              amp_record& rec, bool& ok) {
+                                              amp_record& rec, bool& ok, int* seg_hint) {
   const bool fused = p.fuse_light && u >= p.n_dp;
   CandWork w;
   uint64_t perm = 0;
   int code0 = 0;
-  if (fused) place_one<DT, true>(p, PS, u, false, w, perm, code0);
+  if (fused) place_one<DT, true>(p, PS, u, false, w, perm, code0, nullptr, seg_hint);
   else w = p.work[u];
   const ClassDev cl = p.cls[w.cls];
   int fc = w.fail_code;
@@ -501,6 +503,7 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
     w_ki = e.index;
   }
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  int seg_hint = -1;  // (decode_item: this thread's previous segment)
   // uniform trip count per warp (the top-k hand-off is warp-synchronous)
   const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
   for (uint64_t wbase = first; wbase < p.n_chunk; wbase += stride) {
@@ -523,7 +526,7 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
     int pp = 0, best_r = -1;
     bool ok = false;
     if constexpr (FAST) {
-      if (live) est_fast_item<DT>(p, PS, u, rec, ok);
+      if (live) est_fast_item<DT>(p, PS, u, rec, ok, &seg_hint);
     } else if (live) {
       // fused light path: the pp <= 2 tail (never in K_dp) is placed here
       const bool fused = p.fuse_light && u >= p.n_dp;
