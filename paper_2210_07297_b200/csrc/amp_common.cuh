@@ -178,6 +178,9 @@ struct EvalParams {
   // per signature run of a dp == 1, pp >= 3 class: its pipeline time (the
   // whole estimate: one replica, no dpsync; NaN = parameter ceiling fails)
   const double* run_pipe;
+  // K_place_t writes no work records: the shape K_est re-decodes its items
+  // (nothing else reads them with the trie and the fused hash insert)
+  int32_t skip_work, pad11;
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

@@ -1339,6 +1339,8 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
                             std::getenv("AMP_DEDUP_SORT") == nullptr &&
                             std::getenv("AMP_NO_FUSE_HASH") == nullptr;
   HashParams fused_hp{};
+  ep.skip_work = ep.est_fast && ctx->dedup && ctx->trie && fuse_hash_ok && ep.fuse_light &&
+                 std::getenv("AMP_KEEP_WORK") == nullptr;
   if (overlap) {
     CK(cudaEventRecord(ctx->aux_start, ctx->stream));
     CK(cudaStreamWaitEvent(ctx->aux, ctx->aux_start, 0));

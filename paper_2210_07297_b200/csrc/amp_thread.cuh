@@ -95,7 +95,9 @@ __device__ __forceinline__ uint64_t codes_shape(const EvalParams& p, const uint8
 // kernels (K_dp, K_est); else only return them (fused light path).
 // DT > 0: the device count as a compile-time constant (the Fisher-Yates
 // loop unrolls: constant shifts, constant-divisor modulo).
-template <int DT, bool FAST = false>
+// DECODE_ONLY: decode and the early failures only (K_est re-deriving a
+// K_place item's work record: the placement comes from placep).
+template <int DT, bool FAST = false, bool DECODE_ONLY = false>
 __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& S, uint64_t u,
                                           bool store, CandWork& w, uint64_t& perm, int& code0,
                                           uint64_t* sig = nullptr, int* seg_hint = nullptr) {
@@ -118,7 +120,7 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
     flayer = pr.fail_layer;
     fval = pr.fail_value;
   }
-  if (fc == 0) {
+  if (fc == 0 && !DECODE_ONLY) {
     // ---- placement: heuristic order (placement.cpp:37-49); p >= 1:
     //      Fisher-Yates driven by splitmix64(seed ^ p) ----------------------
     if (p.given_place) {  // caller placement (anneal proposals, evaluate_placed)
@@ -243,7 +245,7 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
         uint64_t perm;
         int code0;
         place_one<DT, FAST>(p, S, u, true, w, perm, code0, &key, &hint);
-        p.work[u] = w;
+        if (!p.skip_work) p.work[u] = w;
       }
       const uint32_t slot = hash_insert_warp(key, u, lane, p.h_tkey, p.h_tval, p.h_uniq, p.h_nuniq,
                                              p.h_mask, tag, p.h_epoch, sh);
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
     uint64_t perm;
     int code0;
     place_one<DT, FAST>(p, S, u, true, w, perm, code0, nullptr, &hint);
-    p.work[u] = w;
+    if (!p.skip_work) p.work[u] = w;
   }
 }
 
@@ -408,6 +410,7 @@ __device__ __forceinline__ void est_fast_item(const EvalParams& p, const PlaceSm
   uint64_t perm = 0;
   int code0 = 0;
   if (fused) place_one<DT, true>(p, PS, u, false, w, perm, code0, nullptr, seg_hint);
+  else if (p.skip_work) place_one<DT, true, true>(p, PS, u, false, w, perm, code0, nullptr, seg_hint);
   else w = p.work[u];
   const ClassDev cl = p.cls[w.cls];
   int fc = w.fail_code;
@@ -513,7 +516,7 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
     {  // the next iteration's streamed inputs into L2 (no registers held)
       const uint64_t un = u + stride;
       if (un < p.n_chunk && !(p.fuse_light && un >= p.n_dp)) {
-        prefetch_l2(p.work + un);
+        if (!p.skip_work) prefetch_l2(p.work + un);
         if (p.placep) prefetch_l2(p.placep + un);
         if (p.run_slot && un < p.n_dp) prefetch_l2(p.run_slot + un);
         else if (p.rep_of && un < p.n_dp) prefetch_l2(p.rep_of + un);
