@@ -169,7 +169,7 @@ struct EvalParams {
   uint32_t* h_slot_of;
   uint32_t* h_uniq;
   unsigned long long* h_nuniq;
-  uint64_t h_mask, h_epoch;
+  uint64_t h_mask, h_epoch, h_max_probe;
   int32_t h_eshift, pad10;
   // K_est shape kernels: signature run of item u = run_of_slot[run_slot[u]]
   // (the hash table after k_hash_runs) instead of the scattered rep_of[u]

@@ -105,6 +105,7 @@ struct HashParams {
   uint64_t n;              // heavy items
   int32_t max_pp, code_bits;
   uint64_t mask;           // table size - 1
+  uint64_t max_probe;      // probe bound (hash_insert_warp)
   uint64_t epoch;          // this run's tag (> 0)
   int32_t epoch_shift, pad0;  // key bits (tag above them), 64: no tag
   const uint64_t* sigkey;  // [n] keys written by K_place, or NULL (computed here)
@@ -146,18 +147,26 @@ __device__ __forceinline__ bool slot_free(unsigned long long k, uint64_t epoch, 
 // uniform per warp for the warp-wide match / shuffle.
 // Warp-cooperative insert (all 32 lanes call it): lanes with equal keys
 // elect one prober; returns the key's slot (~0u for kHashEmpty).
+// The table may be sized from the previous chunk's distinct-key count: a
+// probe sequence longer than max_probe (such a table far above half full)
+// gives up and raises n_uniq[1]; the host then redoes the chunk's inserts
+// with a table sized for every item (max_probe = its size: never hit).
 __device__ __forceinline__ uint32_t hash_insert_warp(uint64_t key, uint64_t u, int lane,
                                                      unsigned long long* tkey, uint32_t* tval,
                                                      uint32_t* uniq, unsigned long long* n_uniq,
                                                      uint64_t mask, uint64_t tag, uint64_t epoch,
-                                                     int sh) {
+                                                     int sh, uint64_t max_probe) {
   const unsigned peers = __match_any_sync(0xffffffffu, key);
   const int leader = __ffs(peers) - 1;
   uint32_t slot = ~0u;
   if (lane == leader && key != kHashEmpty) {
     const unsigned long long want = key | tag;
     uint64_t h = splitmix64(key) & mask;
-    for (;;) {
+    for (uint64_t probe = 0;; ++probe) {
+      if (probe == max_probe) {
+        atomicOr(&n_uniq[1], 1ull);
+        break;
+      }
       unsigned long long k = *(volatile unsigned long long*)&tkey[h];
       if (k == want) break;
       if (slot_free(k, epoch, sh)) {
@@ -190,7 +199,7 @@ __global__ void k_hash_insert(HashParams p) {
                                     : sig_key(p.work[u], p.cls, p.bwcb + u * p.max_pp, p.max_pp,
                                               p.code_bits);
     const uint32_t slot = hash_insert_warp(key, u, lane, p.tkey, p.tval, p.uniq, p.n_uniq, p.mask,
-                                           tag, p.epoch, sh);
+                                           tag, p.epoch, sh, p.max_probe);
     if (live) p.slot_of[u] = slot;
   }
 }

@@ -169,7 +169,7 @@ struct amp_ctx {
   DevBuf dd_runpipe;  // per-run pipeline time of dp == 1 classes (k_run_pipe)
   DevBuf dd_nrep, dd_temp, dd_counters, prog_inner_d, dd_repcuts;
   DevBuf dd_tkey, dd_tval, dd_slot, dd_uniq, dd_nuniq, dd_sigkey;  // hash dedup
-  uint64_t hash_epoch = 0, hash_T = 0;
+  uint64_t hash_epoch = 0, hash_T = 0, hash_last_uniq = 0;
   size_t dd_temp_bytes = 0;
   // DP shared across signature prefixes (amp_trie.cuh)
   bool trie = false;
@@ -190,6 +190,7 @@ struct amp_ctx {
   cudaStream_t aux = nullptr;
   cudaEvent_t aux_start = nullptr, aux_done = nullptr;
   int n_topk_lists = 0;  // CTA lists of the last launch_evaluate (main + aux)
+  uint64_t stats_hash_redo = 0;  // chunks whose hash inserts were redone (table overflow)
 };
 
 #define CK(call)                                                                      \
@@ -1291,15 +1292,25 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   // signature hash table of a chunk (amp_dedup.cuh): sized for ep.n_dp
   // items at load <= 1/2; entries carry an epoch tag above the key bits, so
   // the table is cleared only when it is (re)allocated or the tag wraps
-  auto prepare_hash = [&](HashParams& hp) -> int {
+  // full = false: sized for 4x the previous chunk's distinct keys (at least
+  // 2^22 slots, AMP_HASH_MIN_LOG2) instead of for every item, so a fresh
+  // table costs a 32 MB clear, not 1 GB; an overflow (n_uniq[1]) or a load
+  // above 1/2 redoes the chunk's inserts with the full-size table
+  auto prepare_hash = [&](HashParams& hp, bool full) -> int {
     uint64_t T = 1024;
     while (T < 2 * ep.n_dp) T <<= 1;
+    if (!full) {
+      const char* ml = std::getenv("AMP_HASH_MIN_LOG2");
+      uint64_t t = 1ull << (ml ? std::atoi(ml) : 22);
+      while (t < 4 * ctx->hash_last_uniq) t <<= 1;
+      T = std::min(T, t);
+    }
     const bool grown = ctx->dd_tkey.bytes < sizeof(uint64_t) * T;
     CK(ctx->dd_tkey.ensure(sizeof(uint64_t) * T));
     CK(ctx->dd_tval.ensure(sizeof(uint32_t) * T));
     CK(ctx->dd_slot.ensure(sizeof(uint32_t) * C));
     CK(ctx->dd_uniq.ensure(sizeof(uint32_t) * C));
-    CK(ctx->dd_nuniq.ensure(sizeof(unsigned long long)));
+    CK(ctx->dd_nuniq.ensure(2 * sizeof(unsigned long long)));
     const int esh = 64 - ctx->key_bits >= 8 ? ctx->key_bits : 64;
     if (esh >= 64) {
       CK(cudaMemsetAsync(ctx->dd_tkey.p, 0xff, sizeof(uint64_t) * T, ctx->stream));
@@ -1312,7 +1323,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
       ++ctx->hash_epoch;
     }
     ctx->hash_T = T;
-    CK(cudaMemsetAsync(ctx->dd_nuniq.p, 0, sizeof(unsigned long long), ctx->stream));
+    CK(cudaMemsetAsync(ctx->dd_nuniq.p, 0, 2 * sizeof(unsigned long long), ctx->stream));
     hp = HashParams{};
     hp.work = ep.work;
     hp.cls = ep.cls;
@@ -1321,6 +1332,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     hp.max_pp = ctx->max_pp;
     hp.code_bits = ctx->code_bits;
     hp.mask = T - 1;
+    hp.max_probe = full ? T : std::min<uint64_t>(T, 4096);
     hp.epoch = ctx->hash_epoch;
     hp.epoch_shift = esh;
     hp.sigkey = ep.sigkey;
@@ -1379,7 +1391,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     ep.first_chunk = t0 == 0;
     ep.fuse_hash = 0;
     if (fuse_hash_ok && ep.n_dp > 0) {
-      const int rc = prepare_hash(fused_hp);
+      const int rc = prepare_hash(fused_hp, false);
       if (rc != AMP_OK) return rc;
       ep.fuse_hash = 1;
       ep.h_tkey = fused_hp.tkey;
@@ -1388,6 +1400,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
       ep.h_uniq = fused_hp.uniq;
       ep.h_nuniq = fused_hp.n_uniq;
       ep.h_mask = fused_hp.mask;
+      ep.h_max_probe = fused_hp.max_probe;
       ep.h_epoch = fused_hp.epoch;
       ep.h_eshift = fused_hp.epoch_shift;
     }
@@ -1457,16 +1470,52 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
         if (ep.fuse_hash) {
           hp = fused_hp;  // table prepared before K_place_t, which inserted the keys
         } else {
-          const int rc = prepare_hash(hp);
+          const int rc = prepare_hash(hp, false);
           if (rc != AMP_OK) return rc;
         }
         hp.rep_list = dp.rep_list;
         hp.rep_of = dp.rep_of;
         hp.n_rep = dp.n_rep;
         if (!ep.fuse_hash) k_hash_insert<<<g, 256, 0, ctx->stream>>>(hp);
-        unsigned long long nu = 0;
-        CK(cudaMemcpyAsync(&nu, ctx->dd_nuniq.p, sizeof nu, cudaMemcpyDeviceToHost, ctx->stream));
+        unsigned long long nuo[2] = {0, 0};
+        CK(cudaMemcpyAsync(nuo, ctx->dd_nuniq.p, sizeof nuo, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
+        if (nuo[1] || 2 * nuo[0] > hp.mask + 1) {
+          // the table sized from the last chunk overflowed: redo with the
+          // full-size one (fused: K_place again — same work, new keys' slots)
+          ctx->stats_hash_redo += 1;
+          const int rc = prepare_hash(hp, true);
+          if (rc != AMP_OK) return rc;
+          hp.rep_list = dp.rep_list;
+          hp.rep_of = dp.rep_of;
+          hp.n_rep = dp.n_rep;
+          if (ep.fuse_hash) {
+            ep.h_tkey = hp.tkey;
+            ep.h_tval = hp.tval;
+            ep.h_slot_of = hp.slot_of;
+            ep.h_uniq = hp.uniq;
+            ep.h_nuniq = hp.n_uniq;
+            ep.h_mask = hp.mask;
+            ep.h_max_probe = hp.max_probe;
+            ep.h_epoch = hp.epoch;
+            ep.h_eshift = hp.epoch_shift;
+            const int tg = (int)std::min<uint64_t>((ep.n_chunk + 255) / 256, (uint64_t)ctx->sms * 16);
+            if (shape16)
+              k_place_t<16, true><<<tg, 256, 0, ctx->stream>>>(ep);
+            else if (ctx->D == 16)
+              k_place_t<16><<<tg, 256, 0, ctx->stream>>>(ep);
+            else
+              k_place_t<0><<<tg, 256, 0, ctx->stream>>>(ep);
+          } else {
+            k_hash_insert<<<g, 256, 0, ctx->stream>>>(hp);
+          }
+          CK(cudaGetLastError());
+          CK(cudaMemcpyAsync(nuo, ctx->dd_nuniq.p, sizeof nuo, cudaMemcpyDeviceToHost, ctx->stream));
+          CK(cudaStreamSynchronize(ctx->stream));
+          if (nuo[1]) return fail(ctx, AMP_E_CUDA, "signature hash table overflow");
+        }
+        const unsigned long long nu = nuo[0];
+        ctx->hash_last_uniq = nu;
         n_runs_host = nu;
         const int gu = (int)std::min<uint64_t>((nu + 255) / 256 + 1, (uint64_t)ctx->sms * 8);
         k_hash_gather<<<gu, 256, 0, ctx->stream>>>(hp, ctx->dd_keys.as<uint64_t>(),

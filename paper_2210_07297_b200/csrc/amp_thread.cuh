@@ -248,7 +248,8 @@ __global__ void __launch_bounds__(256) k_place_t(EvalParams p) {
         if (!p.skip_work) p.work[u] = w;
       }
       const uint32_t slot = hash_insert_warp(key, u, lane, p.h_tkey, p.h_tval, p.h_uniq, p.h_nuniq,
-                                             p.h_mask, tag, p.h_epoch, sh);
+                                             p.h_mask, tag, p.h_epoch, sh,
+                                             p.h_max_probe);
       if (u < n) p.h_slot_of[u] = slot;
     }
     return;

@@ -517,3 +517,28 @@ def test_run_pipe_with_parameter_ceiling_matches_oracle(ceiling, monkeypatch):
     assert np.array_equal(allr["total"][ok], orec["total"][ok])
     if ceiling is not None:
         assert (orec["fail_code"] == 3).any() and ok.any()  # AMP_FAIL_CEILING, some pass
+
+
+@pytest.mark.parametrize("min_log2", ["10", "12"])
+def test_small_hash_table_overflow_redo(min_log2, monkeypatch):
+    """The signature table sized from the previous chunk (here forced tiny,
+    AMP_HASH_MIN_LOG2) overflows on a sweep with thousands of signatures:
+    the chunk's inserts are redone with the full-size table (K_place again)
+    and records / top-k equal the default run, also across chunks."""
+    sc = scenario("hetero_cluster")
+    enc = P.EncodedProblem.from_scenario(sc)
+    outs = []
+    for env in (None, min_log2):
+        if env:
+            monkeypatch.setenv("AMP_HASH_MIN_LOG2", env)
+            monkeypatch.setenv("AMP_CHUNK", "1000000")
+        else:
+            monkeypatch.delenv("AMP_HASH_MIN_LOG2", raising=False)
+            monkeypatch.delenv("AMP_CHUNK", raising=False)
+        with planner.Searcher(enc, placements_per_class=40000, seed=6) as s:
+            top, allr, _ = s.run(0, s.num_candidates, k=16, want_all=True, details=False)
+            st = s.stats()
+        outs.append((top, allr, st))
+    assert outs[0][2]["dp_instances"] > 2 ** int(min_log2)  # more signatures than slots
+    assert np.array_equal(outs[0][1].view(np.uint8), outs[1][1].view(np.uint8))
+    assert np.array_equal(outs[0][0].view(np.uint8), outs[1][0].view(np.uint8))
