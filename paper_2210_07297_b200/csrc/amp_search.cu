@@ -950,10 +950,14 @@ void account(amp_ctx* ctx, uint64_t begin, uint64_t end, const uint64_t* list, i
 // node ids per depth (flag + scan), first signatures and stage table sizes
 // (+ scan), one host read of the counts, then one launch per stage and the
 // backtrack.  Writes the cuts of every representative into ep.cutsb.
-int run_trie(amp_ctx* ctx, const EvalParams& ep) {
-  uint64_t n_rep = 0;
-  CK(cudaMemcpyAsync(&n_rep, ctx->dd_nrep.p, sizeof n_rep, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
+// n_rep_known: the run count when the host already has it (hash path),
+// else 0 (read back from the device).
+int run_trie(amp_ctx* ctx, const EvalParams& ep, uint64_t n_rep_known) {
+  uint64_t n_rep = n_rep_known;
+  if (n_rep == 0) {
+    CK(cudaMemcpyAsync(&n_rep, ctx->dd_nrep.p, sizeof n_rep, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
   if (n_rep == 0) return AMP_OK;
   const int nq = ctx->max_pp - 1, D1 = nq + 1, NC = (int)ctx->classes.size();
   const uint64_t S = n_rep;
@@ -1544,7 +1548,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
       ep.n_rep = dp.n_rep;
       ep.repcuts = ctx->dd_repcuts.as<uint8_t>();
       if (ctx->trie) {
-        const int rc = run_trie(ctx, ep);
+        const int rc = run_trie(ctx, ep, n_runs_host);
         if (rc != AMP_OK) return rc;
         skip_dp = true;  // K_dp's work is done (K_est reads the cuts via rep_of)
         if (ep.est_fast && n_runs_host > 0 && std::getenv("AMP_NO_RUN_PIPE") == nullptr) {
