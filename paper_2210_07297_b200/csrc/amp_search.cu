@@ -1552,10 +1552,13 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
         if (rc != AMP_OK) return rc;
         skip_dp = true;  // K_dp's work is done (K_est reads the cuts via rep_of)
         if (ep.est_fast && n_runs_host > 0 && std::getenv("AMP_NO_RUN_PIPE") == nullptr) {
-          CK(ctx->dd_runpipe.ensure(sizeof(double) * n_runs_host));
+          // by hash slot when K_est looks runs up by slot, else by run
+          const bool by_slot = ep.run_slot != nullptr;
+          CK(ctx->dd_runpipe.ensure(sizeof(double) * (by_slot ? ctx->hash_T : n_runs_host)));
           const int gr = (int)std::min<uint64_t>((n_runs_host + 255) / 256, (uint64_t)ctx->sms * 8);
           k_run_pipe<<<gr, 256, 0, ctx->stream>>>(ep, ctx->dd_rep_key.as<uint64_t>(), n_runs_host,
-                                                   ctx->dd_runpipe.as<double>());
+                                                   ctx->dd_runpipe.as<double>(),
+                                                   by_slot ? ctx->dd_svals.as<uint32_t>() : nullptr);
           CK(cudaGetLastError());
           ctx->launches += 1;
           ep.run_pipe = ctx->dd_runpipe.as<double>();

@@ -283,11 +283,12 @@ __device__ __forceinline__ void est_shape(const EvalParams& p, const uint8_t* co
   const int L = p.L, LP = L + 1, maxpp = p.max_pp;
   int cuts[PP + 1];
   if (PP >= 3) {  // the signature run's cuts (memoised DP) or this item's
-    const uint64_t run = p.run_slot ? p.run_of_slot[p.run_slot[u]] : p.rep_of ? p.rep_of[u] : ~0ull;
     if (DPn == 1 && p.run_pipe) {
       // one replica whose boundary codes are the signature's: the whole
-      // estimate is a function of the run (k_run_pipe, same operations)
-      const double v = p.run_pipe[run];
+      // estimate is a function of the run (k_run_pipe, same operations),
+      // stored by hash slot when the shape kernels look runs up by slot
+      const double v = p.run_slot ? p.run_pipe[p.run_slot[u]]
+                                  : p.run_pipe[p.rep_of ? p.rep_of[u] : 0u];
       if (v != v) {
         fc = AMP_FAIL_CEILING;
       } else {
@@ -296,6 +297,7 @@ __device__ __forceinline__ void est_shape(const EvalParams& p, const uint8_t* co
       }
       return;
     }
+    const uint64_t run = p.run_slot ? p.run_of_slot[p.run_slot[u]] : p.rep_of ? p.rep_of[u] : ~0ull;
     const uint8_t* ci = run != ~0ull ? p.repcuts + run * (maxpp + 1) : p.cutsb + u * (maxpp + 1);
 #pragma unroll
     for (int q = 0; q <= PP; ++q) cuts[q] = ci[q];
@@ -368,7 +370,10 @@ __device__ __forceinline__ void est_shape(const EvalParams& p, const uint8_t* co
 // one replica (its edge codes are the signature's boundary codes — the
 // K_place minimum over replicas x shards with a single replica), so K_est
 // reads one value per item.  Same operations and order as est_shape.
-__global__ void k_run_pipe(EvalParams p, const uint64_t* rep_key, uint64_t n_runs, double* out) {
+// out is indexed by run, or by the run's hash slot when slot_of_run is given
+// (K_est then reads it through the item's slot: one dependent load less).
+__global__ void k_run_pipe(EvalParams p, const uint64_t* rep_key, uint64_t n_runs, double* out,
+                           const uint32_t* slot_of_run) {
   const int nq = p.max_pp - 1, cb = p.sig_code_bits, L = p.L, LP = L + 1, maxpp = p.max_pp;
   const uint64_t cmask = (1ull << cb) - 1;
   for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_runs;
@@ -395,8 +400,8 @@ __global__ void k_run_pipe(EvalParams p, const uint64_t* rep_key, uint64_t n_run
       sum = sum + stj;
       if (p.has_ceiling) worst_p = std_max(worst_p, spj / cl.tmp);
     }
-    out[r] = (p.has_ceiling && worst_p > p.ceiling) ? CUDART_NAN
-                                                    : (double)(cl.gas - 1) * slowest + sum;
+    out[slot_of_run ? (uint64_t)slot_of_run[r] : r] =
+        (p.has_ceiling && worst_p > p.ceiling) ? CUDART_NAN : (double)(cl.gas - 1) * slowest + sum;
   }
 }
 
@@ -417,7 +422,8 @@ __device__ __forceinline__ void est_fast_item(const EvalParams& p, const PlaceSm
   int fc = w.fail_code;
   double pipeline = CUDART_NAN, dpsync = CUDART_NAN;
   if (fc == 0) {
-    if (!fused) perm = p.placep[u];
+    // (a dp == 1, pp >= 3 item with the per-run estimate needs no placement)
+    if (!fused && !(p.run_pipe && cl.dp == 1 && cl.pp >= 3)) perm = p.placep[u];
     switch (cl.pp * 1024 + cl.dp * 32 + cl.tmp) {
 #define AMP_SHAPE(a, b, c)                                                                  \
   case a * 1024 + b * 32 + c:                                                               \
