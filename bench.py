@@ -39,7 +39,7 @@ METRIC = "candidate strategies/sec"
 TRAFFIC_BYTES_PER_DP_ITEM = 66.5  # 66.54 MB over the 1,000,000 items of launch 3
 # ncu instructions / DRAM bytes per item of the per-candidate kernels on this
 # workload (tools/gpu_round.sh -> tools/summarize_profiles.py)
-KERNEL_COUNTS = os.path.join(ROOT, "profiles", "r1j_kernel_counts.json")
+KERNEL_COUNTS = os.path.join(ROOT, "profiles", "r1k_kernel_counts.json")
 UNIT = "candidates/s"
 
 
