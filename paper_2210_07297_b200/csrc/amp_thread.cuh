@@ -221,12 +221,15 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
   w.fail_value = fval;
 }
 
-// 256 threads; AMP_PLACE_MINB CTAs/SM bounds the registers (1 = no bound).
-#ifndef AMP_PLACE_MINB
-#define AMP_PLACE_MINB 1
+// 256 threads; -DAMP_PLACE_MINB=n caps the registers for n CTAs/SM (8
+// measured slower).  Without it ptxas picks the count (40).
+#ifdef AMP_PLACE_MINB
+#define AMP_PLACE_BOUNDS __launch_bounds__(256, AMP_PLACE_MINB)
+#else
+#define AMP_PLACE_BOUNDS __launch_bounds__(256)
 #endif
 template <int DT, bool FAST = false>
-__global__ void __launch_bounds__(256, AMP_PLACE_MINB) k_place_t(EvalParams p) {
+__global__ void AMP_PLACE_BOUNDS k_place_t(EvalParams p) {
   __shared__ PlaceSmem S;
   place_smem_init(p, S);
   __syncthreads();
