@@ -175,6 +175,12 @@ typedef struct amp_stats {
   uint64_t dp_items;         /* candidates that went through K_dp (pp >= 3)  */
   int32_t dp_launches;       /* K_dp launches of the run                     */
   int32_t dp_group;          /* K_dp candidates per group (0: one at a time) */
+  double dp_stage_ms;        /* device time of the DP stage kernels alone
+                                (K_trie_tiles launches; CUDA events)        */
+  int32_t dp_stage_launches; /* their launches                               */
+  int32_t dp_fallback;       /* chunks whose trie capacity overflowed (their
+                                signatures went through the per-signature
+                                K_dp instead)                               */
 } amp_stats;
 
 typedef struct amp_ctx amp_ctx;

@@ -145,6 +145,9 @@ class AmpStats(C.Structure):
         ("dp_items", C.c_uint64),
         ("dp_launches", C.c_int32),
         ("dp_group", C.c_int32),
+        ("dp_stage_ms", C.c_double),
+        ("dp_stage_launches", C.c_int32),
+        ("dp_fallback", C.c_int32),
     ]
 
 

@@ -179,8 +179,12 @@ struct EvalParams {
   // whole estimate: one replica, no dpsync; NaN = parameter ceiling fails)
   const double* run_pipe;
   // K_place_t writes no work records: the shape K_est re-decodes its items
-  // (nothing else reads them with the trie and the fused hash insert)
+  // (nothing else reads them with the memoised DP and the fused hash insert)
   int32_t skip_work, pad11;
+  // signature-mode K_dp (amp_dp_multi.cuh): the chunk's distinct signature
+  // keys [*n_rep]; run only while *sig_guard != 0 (NULL: always)
+  const uint64_t* sig_keys;
+  const uint32_t* sig_guard;
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

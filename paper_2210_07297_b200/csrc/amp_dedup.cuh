@@ -4,98 +4,28 @@
 // class (pp, dp, tmp, mbs: layer times, gas, k) and the edge function
 // e(cut, q) = act[cut-1]*mbs / bw[q] (optimizer.cpp:130-139).  With coded
 // bandwidths (K_place) the edge function is fixed by the per-boundary codes,
-// so candidates with the same (class, code vector) have bit-identical cuts.
-// Per chunk:
-//   K_key    key[u] = class << (nq * cb) | codes, value u   (heavy items)
-//   radix sort (cub::DeviceRadixSort) of (key, u)
-//   K_heads  head flag of every run of equal keys
-//   scan     run id of every sorted position (cub::DeviceScan)
-//   K_reps   run heads -> rep_list[run] = u;  then rep_of[u] = rep_list[run]
-// K_dp solves only rep_list[0 .. n_rep) (class-contiguous: the class is in
-// the key's high bits), K_est reads each candidate's cuts at rep_of[u].
-// Failed and pp <= 2 items get the all-ones key (never a real signature:
-// keys use at most 63 bits); K_dp skips them as before.
+// so candidates with the same signature key = class << (nq * cb) | codes
+// have bit-identical cuts.  Per chunk the heavy items insert their keys into
+// a hash table (fused into K_place_t, or k_hash_insert); its distinct keys
+// become the signature list (amp_trie.cuh K_sig_init) whose DP is solved
+// once; K_est reads each item's cuts at its signature.  Failed and pp <= 2
+// items carry the all-ones key (never a real signature: keys use at most 63
+// bits) and are not inserted.
 #pragma once
 
 #include "amp_common.cuh"
 
 namespace amp {
 
-struct DedupParams {
-  const CandWork* work;
-  const ClassDev* cls;
-  const uint8_t* bwcb;  // [n][max_pp] boundary codes
-  uint64_t n;           // heavy prefix of the chunk
-  int32_t max_pp, code_bits, pad0, pad1;
-  uint64_t* keys;       // [n]
-  uint32_t* vals;       // [n]
-  const uint64_t* skeys;  // sorted
-  const uint32_t* svals;
-  uint32_t* flags;      // [n] head flags -> (scan) run ids (inclusive)
-  const uint32_t* runid;
-  uint32_t* rep_list;   // [n] representative item of each run
-  uint32_t* rep_of;     // [n] signature run of every item
-  uint64_t* n_rep;      // device count of runs
-  uint64_t* rep_key;    // [n] key of each run (NULL: not needed)
-};
-
-__global__ void k_dedup_keys(DedupParams p) {
-  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < p.n;
-       u += (uint64_t)gridDim.x * blockDim.x) {
-    const CandWork& w = p.work[u];
-    uint64_t key = ~0ull;
-    if (w.fail_code == 0) {
-      const ClassDev cl = p.cls[w.cls];
-      if (cl.pp >= 3) {
-        key = (uint64_t)w.cls;
-        const uint8_t* c = p.bwcb + u * p.max_pp;
-        for (int q = 0; q < p.max_pp - 1; ++q)
-          key = (key << p.code_bits) | (q < cl.pp - 1 ? (uint64_t)c[q] : 0ull);
-      }
-    }
-    p.keys[u] = key;
-    p.vals[u] = (uint32_t)u;
-  }
-}
-
-__global__ void k_dedup_heads(DedupParams p) {
-  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < p.n;
-       s += (uint64_t)gridDim.x * blockDim.x)
-    p.flags[s] = (s == 0 || p.skeys[s] != p.skeys[s - 1]) ? 1u : 0u;
-}
-
-__global__ void k_dedup_reps(DedupParams p) {
-  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < p.n;
-       s += (uint64_t)gridDim.x * blockDim.x) {
-    const bool head = s == 0 || p.skeys[s] != p.skeys[s - 1];
-    if (head) {
-      p.rep_list[p.runid[s] - 1] = p.svals[s];
-      if (p.rep_key) p.rep_key[p.runid[s] - 1] = p.skeys[s];
-    }
-    if (s + 1 == p.n) *p.n_rep = p.runid[s];
-  }
-}
-
-__global__ void k_dedup_scatter(DedupParams p) {
-  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < p.n;
-       s += (uint64_t)gridDim.x * blockDim.x)
-    p.rep_of[p.svals[s]] = p.runid[s] - 1;  // the signature's run (index into repcuts)
-}
-
-}  // namespace amp
-
-namespace amp {
-
-// ---- hash-based signature runs (replaces the full radix sort) -------------
+// ---- signature hash table --------------------------------------------------
 //
 // Each heavy item inserts its key into an open-addressing table (linear
 // probing, load <= 1/2): an item reads the slot first and only the first
 // writer of a key CASes it in, so the many items of a hot signature cost one
 // L2 read each.  The first writer appends the slot to the list of distinct
-// keys.  Only those (a few hundred thousand) are then sorted: the run order
-// (class, c_0, c_1, ...) that K_dp / the trie need.  Which item becomes a
-// signature's representative does not matter: all its items have identical
-// DP inputs.
+// keys (the signature list, in insertion order: the trie orders nothing by
+// sorting).  Which item becomes a signature's representative does not
+// matter: all its items have identical DP inputs.
 constexpr uint64_t kHashEmpty = ~0ull;
 
 struct HashParams {
@@ -114,13 +44,7 @@ struct HashParams {
   uint32_t* slot_of;       // [n] slot of every item (~0u: no signature)
   uint32_t* uniq;          // [n] slots of the distinct keys
   unsigned long long* n_uniq;
-  // after the host sorted the distinct keys
-  const uint64_t* skeys;   // [n_uniq] sorted keys
-  const uint32_t* sslots;  // [n_uniq] their slots
-  uint64_t* rep_key;       // [n_uniq] (NULL: not needed)
-  uint32_t* rep_list;      // [n_uniq] representative item of each run
-  uint32_t* rep_of;        // [n] run of every item
-  uint64_t* n_rep;         // device count of runs
+  uint32_t* rep_of;        // [n] signature of every item (k_hash_scatter)
 };
 
 __device__ __forceinline__ uint64_t sig_key(const CandWork& w, const ClassDev* cls,
@@ -146,11 +70,9 @@ __device__ __forceinline__ bool slot_free(unsigned long long k, uint64_t epoch, 
 // line holding it does not serialise the whole grid.  The loop trip count is
 // uniform per warp for the warp-wide match / shuffle.
 // Warp-cooperative insert (all 32 lanes call it): lanes with equal keys
-// elect one prober; returns the key's slot (~0u for kHashEmpty).
-// The table may be sized from the previous chunk's distinct-key count: a
-// probe sequence longer than max_probe (such a table far above half full)
-// gives up and raises n_uniq[1]; the host then redoes the chunk's inserts
-// with a table sized for every item (max_probe = its size: never hit).
+// elect one prober; returns the key's slot (~0u for kHashEmpty).  The table
+// is sized for every heavy item at load <= 1/2, so a probe always ends; the
+// max_probe bound (= the table size) only guards the loop (n_uniq[1]).
 __device__ __forceinline__ uint32_t hash_insert_warp(uint64_t key, uint64_t u, int lane,
                                                      unsigned long long* tkey, uint32_t* tval,
                                                      uint32_t* uniq, unsigned long long* n_uniq,
@@ -202,29 +124,6 @@ __global__ void k_hash_insert(HashParams p) {
                                            tag, p.epoch, sh, p.max_probe);
     if (live) p.slot_of[u] = slot;
   }
-}
-
-__global__ void k_hash_gather(HashParams p, uint64_t* keys, uint32_t* slots) {
-  const uint64_t n = *p.n_uniq;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t s = p.uniq[i];
-    const unsigned long long k = p.tkey[s];
-    keys[i] = p.epoch_shift >= 64 ? k : (k & ((1ull << p.epoch_shift) - 1));  // drop the tag
-    slots[i] = s;
-  }
-}
-
-__global__ void k_hash_runs(HashParams p) {
-  const uint64_t n = *p.n_uniq;
-  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
-       r += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t s = p.sslots[r];
-    p.rep_list[r] = p.tval[s];
-    if (p.rep_key) p.rep_key[r] = p.skeys[r];
-    p.tval[s] = (uint32_t)r;  // slot -> run
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *p.n_rep = n;
 }
 
 __global__ void k_hash_scatter(HashParams p) {

@@ -231,15 +231,23 @@ __global__ void __launch_bounds__(B >= 8 ? 512 : 256, (B <= 2 ? 3 : (B >= 8 ? 1 
   uint8_t* const bpb = reinterpret_cast<uint8_t*>(Pf + LP + 3);  // [2][max_rest][B]
 
   // slots: chunk items that may need the DP (pp >= 3 first), or with
-  // memoisation the representatives of the distinct signatures
-  const uint64_t n_items = p.rep_list ? *p.n_rep : p.n_dp;
-  auto item_of = [&](uint64_t slot) -> uint64_t { return p.rep_list ? p.rep_list[slot] : slot; };
+  // memoisation the distinct signatures (signature mode: class and boundary
+  // codes come from the key, amp_trie.cuh K_sig_init; only when the trie is
+  // off, or — sig_guard — when its device capacity was exceeded)
+  if (p.sig_guard && *p.sig_guard == 0) return;
+  const bool sigm = p.sig_keys != nullptr;
+  const int sig_nq = maxpp - 1, sig_cb = p.sig_code_bits;
+  const uint64_t n_items = (p.rep_list || sigm) ? *p.n_rep : p.n_dp;
+  auto item_of = [&](uint64_t slot) -> uint64_t { return (p.rep_list && !sigm) ? p.rep_list[slot] : slot; };
   const uint64_t nbatch = (n_items + B - 1) / B;
   uint64_t bi = blockIdx.x;
   if (bi >= nbatch) return;
   auto word = [&](uint64_t batch, int w) -> uint64_t {
     const uint64_t slot = batch * B + w / WW;
-    return slot < n_items ? reinterpret_cast<const uint64_t*>(p.work + item_of(slot))[w % WW] : 0;
+    if (slot >= n_items) return 0;
+    if (sigm)  // a CandWork of class key >> codes, fail_code 0 (word 2: cls | fail_code << 32)
+      return (w % WW) == 2 ? (p.sig_keys[slot] >> (sig_nq * sig_cb)) : 0;
+    return reinterpret_cast<const uint64_t*>(p.work + item_of(slot))[w % WW];
   };
   if (tid < B * WW) reinterpret_cast<uint64_t*>(wq[0])[tid] = word(bi, tid);
   if (tid < 3 * B) {  // edge padding (cuts L .. L+2), never rewritten
@@ -340,6 +348,8 @@ __global__ void __launch_bounds__(B >= 8 ? 512 : 256, (B <= 2 ? 3 : (B >= 8 ? 1 
       // quotients when the bandwidths are coded, else the division
       const double* qt = p.qtab ? p.qtab + (size_t)gcls * p.n_codes * L : nullptr;
       auto edge = [&](uint64_t uu, int c, int q) -> double {
+        if (sigm)
+          return qt[(size_t)((p.sig_keys[uu] >> ((sig_nq - 1 - q) * sig_cb)) & ((1ull << sig_cb) - 1)) * L + c];
         if (qt) return qt[(size_t)p.bwcb[uu * maxpp + q] * L + c];
         return p.act[c - 1] * mbs / p.bwqb[uu * maxpp + q];
       };

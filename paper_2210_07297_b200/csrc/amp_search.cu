@@ -165,17 +165,25 @@ struct amp_ctx {
   // DP memoisation by signature (amp_dedup.cuh)
   bool dedup = false;
   int code_bits = 0, key_bits = 0;
-  DevBuf dd_keys, dd_vals, dd_skeys, dd_svals, dd_flags, dd_runid, dd_rep_list, dd_rep_of;
+  DevBuf dd_rep_list, dd_rep_of;
   DevBuf dd_runpipe;  // per-run pipeline time of dp == 1 classes (k_run_pipe)
-  DevBuf dd_nrep, dd_temp, dd_counters, prog_inner_d, dd_repcuts;
+  DevBuf dd_counters, prog_inner_d, dd_repcuts;
   DevBuf dd_tkey, dd_tval, dd_slot, dd_uniq, dd_nuniq, dd_sigkey;  // hash dedup
-  uint64_t hash_epoch = 0, hash_T = 0, hash_last_uniq = 0;
-  size_t dd_temp_bytes = 0;
+  uint64_t hash_epoch = 0, hash_T = 0;
   // DP shared across signature prefixes (amp_trie.cuh)
   bool trie = false;
+  int trie_nq = 0, trie_U = 0;
   std::vector<uint32_t> stage_h;  // host copy of the program stage starts
-  DevBuf v1off_d, v1g_d, dd_rep_key, tr_nid, tr_first, tr_parent, tr_flags, tr_range, tr_vals0,
-      tr_vals1, tr_bp, tr_vbase, tr_bbase, tr_stcls, tr_stitem, tr_stn;
+  std::vector<uint64_t> prog_stage_inner;  // [prog][L+1] unpadded (cell, cut) pairs of stage j
+  std::vector<int32_t> root_cls_h;         // heavy classes (trie roots) in class order
+  DevBuf v1off_d, v1g_d, dd_rep_key, dd_nid, tr_state, tr_pres, tr_cid, tr_partial, tr_npar,
+      tr_ncls, tr_ncode, tr_nb, tr_nK, tr_vbase, tr_bbase, tr_tbase, tr_tstage, tr_v0, tr_v1, tr_bp,
+      tr_rank, tr_rcls;
+  uint64_t tr_pres_cap = 0, tr_node_cap = 0, tr_vcap = 0, tr_bpcap = 0;
+  std::vector<cudaEvent_t> tev;  // {before, after} every K_trie_tiles launch of the last run
+  int tev_used = 0;
+  DevBuf ovf_log;                // trie capacity flag of every chunk of the last run
+  int ovf_used = 0;
   uint64_t chunk = 1;
   int est_ctas = 1, sms = 148, launches = 0;
   // per-chunk kernel events {before K_place, after K_place, after K_dp,
@@ -190,7 +198,6 @@ struct amp_ctx {
   cudaStream_t aux = nullptr;
   cudaEvent_t aux_start = nullptr, aux_done = nullptr;
   int n_topk_lists = 0;  // CTA lists of the last launch_evaluate (main + aux)
-  uint64_t stats_hash_redo = 0;  // chunks whose hash inserts were redone (table overflow)
 };
 
 #define CK(call)                                                                      \
@@ -203,6 +210,21 @@ struct amp_ctx {
                     ? AMP_E_NOT_BUILT                                                 \
                     : AMP_E_CUDA);                                                    \
     }                                                                                 \
+  } while (0)
+
+// AMP_DEBUG_SYNC=1: synchronise after every kernel of a run and name the
+// kernel that faulted (debugging aid; off in normal runs).
+static const bool g_debug_sync = std::getenv("AMP_DEBUG_SYNC") != nullptr;
+#define DBG_SYNC(name)                                                                   \
+  do {                                                                                   \
+    if (g_debug_sync) {                                                                  \
+      cudaError_t e_ = cudaStreamSynchronize(ctx->stream);                               \
+      if (e_ == cudaSuccess) e_ = cudaGetLastError();                                    \
+      if (e_ != cudaSuccess) {                                                           \
+        ctx->err = std::string(name) + ": " + cudaGetErrorString(e_);                    \
+        return AMP_E_CUDA;                                                               \
+      }                                                                                  \
+    }                                                                                    \
   } while (0)
 
 namespace {
@@ -292,6 +314,7 @@ int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
                      cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->prog_inner_raw.assign(n, 0.0);
+  ctx->prog_stage_inner = pin;
   // layout
   std::vector<ProgDev> progs(n);
   std::vector<uint32_t> stage;
@@ -743,7 +766,6 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
       std::vector<double> pin(ctx->prog_inner_raw.begin(), ctx->prog_inner_raw.end());
       if (pin.empty()) pin.push_back(0.0);
       CK(upload(ctx->prog_inner_d, pin.data(), pin.size()));
-      CK(ctx->dd_nrep.ensure(sizeof(uint64_t)));
       CK(ctx->dd_counters.ensure(2 * sizeof(unsigned long long)));
     }
   }
@@ -773,27 +795,63 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
     k_cut2_table<<<(int)((nt + 127) / 128), 128, 0, ctx->stream>>>(tp, ctx->cut2tab.as<uint8_t>());
     CK(cudaGetLastError());
   }
-  // ---- prefix-shared DP (amp_trie.cuh): class stage-1 tables, once -------
-  ctx->trie = ctx->dedup && std::getenv("AMP_NO_TRIE") == nullptr;
+  // ---- prefix-shared DP (amp_trie.cuh): static per-class stage facts ------
+  ctx->trie = ctx->dedup && (1 << ctx->code_bits) <= 16 && std::getenv("AMP_NO_TRIE") == nullptr;
   if (ctx->trie) {
-    int n_heavy = 0;
-    for (size_t c = 0; c < ctx->classes.size(); ++c) n_heavy += is_heavy(ctx, c) ? 1 : 0;
-    ctx->trie = n_heavy <= kTrieMaxCls;
-  }
-  if (ctx->trie) {
-    std::vector<uint64_t> v1off(ctx->classes.size(), 0);
-    std::vector<int32_t> heavy;
+    const int NC = (int)ctx->classes.size(), P1 = ctx->max_pp + 1;
+    const size_t budget = kTrieSmem / sizeof(double);
+    std::vector<TrieStage> ts((size_t)NC * P1, TrieStage{0, 0, 0, 1});
+    std::vector<int32_t> rank(NC, -1), heavy;
+    std::vector<uint64_t> v1off(NC, 0);
     uint64_t acc = 0;
-    for (size_t c = 0; c < ctx->classes.size(); ++c) {
+    int nq = 1;
+    for (int c = 0; c < NC && ctx->trie; ++c) {
       if (!is_heavy(ctx, c)) continue;
-      const ProgDev& pg = ctx->progs_h[ctx->class_prog[c]];
+      const int g = ctx->class_prog[c];
+      const ProgDev& pg = ctx->progs_h[g];
+      const uint32_t* sh = ctx->stage_h.data() + pg.stage_base;
+      rank[c] = (int32_t)heavy.size();
+      heavy.push_back(c);
       v1off[c] = acc;
-      acc += ctx->stage_h[pg.stage_base + 1] - ctx->stage_h[pg.stage_base];
-      heavy.push_back((int32_t)c);
+      acc += sh[1] - sh[0];
+      nq = std::max(nq, ctx->classes[c].pp - 1);
+      for (int j = 1; j <= ctx->classes[c].pp; ++j) {
+        TrieStage& t = ts[(size_t)c * P1 + j];
+        t.cell0 = pg.cell_base + sh[j - 1];
+        t.n = sh[j] - sh[j - 1];
+        t.iters = (uint32_t)ctx->prog_stage_inner[(size_t)g * LP + j];
+        if (j == 1) continue;
+        // tile nodes: parents' tables + edge rows + prefix + node words in
+        // the smem budget; >= 2 (cell, node group) items per thread
+        const double np = ts[(size_t)c * P1 + j - 1].n;
+        const double fixed = (double)ctx->n_codes * L + LP + np;
+        const double per = j == 2 ? 0.5 : np + 0.5;
+        const double room = (double)budget - fixed;
+        int tn = room <= per ? 0 : (int)std::floor(room / per);
+        const int want = kTrieNB * (int)std::ceil(2.0 * kTrieThreads / std::max(1u, t.n));
+        tn = std::min({tn, std::max(kTrieNB, want), 4096});
+        if (tn >= kTrieNB) tn -= tn % kTrieNB;
+        if (tn < 1) ctx->trie = false;  // a parent table does not fit: signature-mode K_dp
+        t.tn = (uint32_t)std::max(tn, 1);
+      }
     }
-    CK(upload(ctx->v1off_d, v1off.data(), v1off.size()));
-    CK(ctx->v1g_d.ensure(sizeof(double) * (acc + 1)));
-    if (!heavy.empty()) {
+    if (ctx->trie && heavy.empty()) ctx->trie = false;
+    if (ctx->trie) {
+      ctx->trie_nq = nq;
+      ctx->trie_U = 1 << ctx->code_bits;
+      ctx->root_cls_h = heavy;
+      CK(upload(ctx->tr_tstage, ts.data(), ts.size()));
+      CK(upload(ctx->tr_rank, rank.data(), rank.size()));
+      CK(upload(ctx->tr_rcls, heavy.data(), heavy.size()));
+      CK(ctx->tr_state.ensure(sizeof(TrieState)));
+      CK(ctx->tr_partial.ensure(sizeof(uint32_t) * kScanGrid));
+      CK(ctx->tr_nb.ensure(sizeof(uint32_t) * kTrieMaxD1 * NC));
+      CK(ctx->tr_nK.ensure(sizeof(uint32_t) * kTrieMaxD1 * NC));
+      CK(ctx->tr_vbase.ensure(sizeof(uint64_t) * kTrieMaxD1 * NC));
+      CK(ctx->tr_bbase.ensure(sizeof(uint64_t) * kTrieMaxD1 * NC));
+      CK(ctx->tr_tbase.ensure(sizeof(uint32_t) * kTrieMaxD1 * (NC + 1)));
+      CK(upload(ctx->v1off_d, v1off.data(), v1off.size()));
+      CK(ctx->v1g_d.ensure(sizeof(double) * (acc + 1)));
       DevBuf d_heavy;
       CK(upload(d_heavy, heavy.data(), heavy.size()));
       k_trie_v1<<<(int)heavy.size(), 256, 0, ctx->stream>>>(
@@ -802,6 +860,7 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
           ctx->domain.as<double>(), ctx->nv_stride, L, d_heavy.as<int32_t>(), (int)heavy.size(),
           ctx->v1off_d.as<uint64_t>(), ctx->v1g_d.as<double>());
       CK(cudaGetLastError());
+      CK(cudaFuncSetAttribute(k_trie_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrieSmem));
       CK(cudaStreamSynchronize(ctx->stream));
     }
   }
@@ -896,6 +955,21 @@ void resolve_kernel_times(amp_ctx* ctx) {
   ctx->stats.place_ms = pl;
   ctx->stats.dp_ms = dpm;
   ctx->stats.est_ms = es;
+  double st_ms = 0;
+  for (int c = 0; c + 1 < ctx->tev_used; c += 2) {
+    float a = 0;
+    cudaEventElapsedTime(&a, ctx->tev[c], ctx->tev[c + 1]);
+    st_ms += a;
+  }
+  ctx->stats.dp_stage_ms = st_ms;
+  ctx->stats.dp_stage_launches = ctx->tev_used / 2;
+  ctx->stats.dp_fallback = 0;
+  if (ctx->ovf_used > 0) {
+    std::vector<uint32_t> o(ctx->ovf_used);
+    if (cudaMemcpy(o.data(), ctx->ovf_log.p, sizeof(uint32_t) * o.size(), cudaMemcpyDeviceToHost) ==
+        cudaSuccess)
+      for (uint32_t v : o) ctx->stats.dp_fallback += v ? 1 : 0;
+  }
   ctx->kev_pending = false;
   if (ctx->stats_exec_pending) {  // memoised run: executed DP instances / iterations
     unsigned long long c[2] = {0, 0};
@@ -946,128 +1020,155 @@ void account(amp_ctx* ctx, uint64_t begin, uint64_t end, const uint64_t* list, i
   s.bytes = 0;
 }
 
-// Prefix-shared DP over the sorted signatures of the chunk (amp_trie.cuh):
-// node ids per depth (flag + scan), first signatures and stage table sizes
-// (+ scan), one host read of the counts, then one launch per stage and the
-// backtrack.  Writes the cuts of every representative into ep.cutsb.
-// n_rep_known: the run count when the host already has it (hash path),
-// else 0 (read back from the device).
-int run_trie(amp_ctx* ctx, const EvalParams& ep, uint64_t n_rep_known) {
-  uint64_t n_rep = n_rep_known;
-  if (n_rep == 0) {
-    CK(cudaMemcpyAsync(&n_rep, ctx->dd_nrep.p, sizeof n_rep, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-  }
-  if (n_rep == 0) return AMP_OK;
-  const int nq = ctx->max_pp - 1, D1 = nq + 1, NC = (int)ctx->classes.size();
-  const uint64_t S = n_rep;
-  CK(ctx->tr_nid.ensure(sizeof(uint32_t) * D1 * S));
-  CK(ctx->tr_first.ensure(sizeof(uint32_t) * D1 * S));
-  CK(ctx->tr_parent.ensure(sizeof(uint32_t) * D1 * S));
-  CK(ctx->tr_flags.ensure(sizeof(uint32_t) * S));
-  CK(ctx->tr_range.ensure(sizeof(uint32_t) * D1 * NC * 2));
-  CK(cudaMemsetAsync(ctx->tr_range.p, 0, sizeof(uint32_t) * D1 * NC * 2, ctx->stream));
+// DP of the chunk's distinct signatures, after the hash insert: the
+// signature list (K_sig_init), then the prefix-shared trie DP (amp_trie.cuh)
+// or — trie off, or its device capacity exceeded — the signature-mode K_dp
+// (k_dp_multi over the keys).  Every count stays on the device: no host
+// synchronisation.  Writes the cuts of signature i at ep.repcuts[i].
+int run_sig_dp(amp_ctx* ctx, EvalParams& ep, const HashParams& hp) {
+  const uint64_t C = std::max<uint64_t>(ep.n_dp, 1);  // signatures <= heavy items
+  const int L = ctx->L, NC = (int)ctx->classes.size();
+  CK(ctx->dd_rep_key.ensure(sizeof(uint64_t) * C));
+  CK(ctx->dd_rep_list.ensure(sizeof(uint32_t) * C));
+  CK(ctx->dd_repcuts.ensure((size_t)C * (ctx->max_pp + 1)));
   TrieParams tp{};
-  tp.n_rep = ctx->dd_nrep.as<uint64_t>();
-  tp.rep_key = ctx->dd_rep_key.as<uint64_t>();
-  tp.rep_list = ctx->dd_rep_list.as<uint32_t>();
-  tp.nq = nq;
+  tp.n_sig = hp.n_uniq;
+  tp.uniq = hp.uniq;
+  tp.tkey = hp.tkey;
+  tp.tval = hp.tval;
+  tp.key_shift = hp.epoch_shift;
+  tp.nq = ctx->max_pp - 1;
   tp.cb = ctx->code_bits;
-  tp.L = ctx->L;
+  tp.U = 1 << ctx->code_bits;
+  tp.L = L;
   tp.max_pp = ctx->max_pp;
   tp.n_cls = NC;
-  tp.stride = S;
-  tp.nid = ctx->tr_nid.as<uint32_t>();
-  tp.first = ctx->tr_first.as<uint32_t>();
-  tp.parent = ctx->tr_parent.as<uint32_t>();
-  tp.flags = ctx->tr_flags.as<uint32_t>();
-  tp.range = ctx->tr_range.as<uint32_t>();
+  tp.n_roots = (int)ctx->root_cls_h.size();
+  tp.sig_key = ctx->dd_rep_key.as<uint64_t>();
+  tp.rep_item = ctx->dd_rep_list.as<uint32_t>();
   tp.cls = ctx->cls_d.as<ClassDev>();
-  tp.class_prog = ctx->class_prog_d.as<int32_t>();
-  tp.progs = ctx->progs_d.as<ProgDev>();
-  tp.stage = ctx->stage_d.as<uint32_t>();
-  tp.cellrec = ctx->cellrec.as<uint2>();
-  tp.preds = ctx->preds.as<uint16_t>();
-  tp.prefix = ctx->prefix.as<double>();
-  tp.domain = ctx->domain.as<double>();
-  tp.nv_stride = ctx->nv_stride;
-  tp.n_codes = ctx->n_codes;
-  tp.qtab = ctx->qtab.as<double>();
-  tp.v1g = ctx->v1g_d.as<double>();
-  tp.v1off = ctx->v1off_d.as<uint64_t>();
-  tp.repcuts = ep.repcuts;
-  const int g = (int)std::min<uint64_t>((S + 255) / 256, (uint64_t)ctx->sms * 8);
-  for (int d = 1; d <= nq; ++d) {
-    k_trie_flag<<<g, 256, 0, ctx->stream>>>(tp, d);
-    size_t tb = ctx->dd_temp_bytes;
-    CK(cub::DeviceScan::InclusiveSum(ctx->dd_temp.p, tb, tp.flags, tp.nid + (size_t)d * S, (int)S,
-                                     ctx->stream));
-    k_trie_nodes<<<g, 256, 0, ctx->stream>>>(tp, d);
-  }
-  CK(cudaGetLastError());
-  ctx->launches += 3 * nq;
-  // node ranges of every class at every depth -> table bases, stage lists
-  std::vector<uint32_t> range((size_t)D1 * NC * 2);
-  CK(cudaMemcpyAsync(range.data(), ctx->tr_range.p, sizeof(uint32_t) * range.size(),
-                     cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  const int P1 = ctx->max_pp + 1;
-  std::vector<uint64_t> vbase((size_t)D1 * NC, 0), bbase((size_t)D1 * NC, 0);
-  std::vector<int32_t> stcls((size_t)P1 * NC, 0), stn(P1, 0);
-  std::vector<uint64_t> stitem((size_t)P1 * (NC + 1), 0), total(P1, 0);
-  uint64_t bacc = 0, vmax = 1;
-  for (int j = 2; j <= ctx->max_pp; ++j) {
-    const int d = j - 1;
-    uint64_t vacc = 0, iacc = 0;
-    for (int c = 0; c < NC; ++c) {
-      const uint32_t nb = range[((size_t)d * NC + c) * 2], ne = range[((size_t)d * NC + c) * 2 + 1];
-      if (ne <= nb || !is_heavy(ctx, c) || ctx->classes[c].pp < j) continue;
-      const ProgDev& pg = ctx->progs_h[ctx->class_prog[c]];
-      const uint64_t cells = ctx->stage_h[pg.stage_base + j] - ctx->stage_h[pg.stage_base + j - 1];
-      const uint64_t sz = cells * (ne - nb);
-      vbase[(size_t)d * NC + c] = vacc;
-      bbase[(size_t)d * NC + c] = bacc;
-      stcls[(size_t)j * NC + stn[j]] = c;
-      stitem[(size_t)j * (NC + 1) + stn[j]] = iacc;  // items: (cell, chunk of kTrieNB nodes)
-      ++stn[j];
-      vacc += sz;
-      bacc += sz;
-      iacc += cells * ((ne - nb + kTrieNB - 1) / kTrieNB);
+  tp.repcuts = ctx->dd_repcuts.as<uint8_t>();
+  tp.exec = ep.exec_counters;
+  const int g = (int)std::min<uint64_t>((C + 255) / 256, (uint64_t)ctx->sms * 8);
+  if (ctx->trie) {
+    // capacities of the device-side trie (exceeding one raises ovf and the
+    // signature-mode K_dp solves the chunk): nodes per level <= signatures
+    // <= heavy items, and <= roots * U^d
+    const uint64_t U = tp.U;
+    uint64_t node_b = 0, lvl_b = (uint64_t)tp.n_roots, w = (uint64_t)tp.n_roots;  // parents of depth 1: the roots
+    for (int d = 1; d <= ctx->trie_nq; ++d) {
+      w = std::min<uint64_t>(w * U, C);
+      node_b += w;
+      lvl_b = std::max(lvl_b, w);
     }
-    if (stn[j] > kTrieMaxCls) return fail(ctx, AMP_E_UNSUPPORTED, "too many classes for the trie DP");
-    stitem[(size_t)j * (NC + 1) + stn[j]] = iacc;
-    total[j] = iacc;
-    vmax = std::max<uint64_t>(vmax, vacc);
+    const uint64_t node_cap = std::min<uint64_t>(node_b, 16ull << 20);
+    const uint64_t pres_cap = std::min<uint64_t>(lvl_b, 16ull << 20) * U;
+    if (ctx->tr_pres.bytes < pres_cap) {  // marks must start clear (then kept clear)
+      CK(ctx->tr_pres.ensure(pres_cap));
+      CK(cudaMemsetAsync(ctx->tr_pres.p, 0, pres_cap, ctx->stream));
+    }
+    CK(ctx->tr_cid.ensure(sizeof(uint32_t) * pres_cap));
+    CK(ctx->tr_npar.ensure(sizeof(uint32_t) * node_cap));
+    CK(ctx->tr_ncls.ensure(sizeof(uint16_t) * node_cap));
+    CK(ctx->tr_ncode.ensure(node_cap));
+    // value arenas: one level each (64 M doubles; AMP_TRIE_VCAP shrinks them
+    // to exercise the capacity fallback in the tests)
+    const char* vc = std::getenv("AMP_TRIE_VCAP");
+    const uint64_t vcap = vc ? std::strtoull(vc, nullptr, 10) : (64ull << 20), bpcap = 512ull << 20;
+    CK(ctx->tr_v0.ensure(sizeof(double) * vcap));
+    CK(ctx->tr_v1.ensure(sizeof(double) * vcap));
+    CK(ctx->tr_bp.ensure(bpcap));
+    CK(ctx->dd_nid.ensure(sizeof(uint32_t) * C));
+    tp.nid = ctx->dd_nid.as<uint32_t>();
+    tp.root_rank = ctx->tr_rank.as<int32_t>();
+    tp.root_cls = ctx->tr_rcls.as<int32_t>();
+    tp.st = ctx->tr_state.as<TrieState>();
+    tp.pres = ctx->tr_pres.as<uint8_t>();
+    tp.cid = ctx->tr_cid.as<uint32_t>();
+    tp.pres_cap = pres_cap;
+    tp.partial = ctx->tr_partial.as<uint32_t>();
+    tp.npar = ctx->tr_npar.as<uint32_t>();
+    tp.ncls = ctx->tr_ncls.as<uint16_t>();
+    tp.ncode = ctx->tr_ncode.as<uint8_t>();
+    tp.node_cap = node_cap;
+    tp.nb = ctx->tr_nb.as<uint32_t>();
+    tp.nK = ctx->tr_nK.as<uint32_t>();
+    tp.vbase = ctx->tr_vbase.as<uint64_t>();
+    tp.bbase = ctx->tr_bbase.as<uint64_t>();
+    tp.tbase = ctx->tr_tbase.as<uint32_t>();
+    tp.tstage = ctx->tr_tstage.as<TrieStage>();
+    tp.varena[0] = ctx->tr_v0.as<double>();
+    tp.varena[1] = ctx->tr_v1.as<double>();
+    tp.vcap = vcap;
+    tp.bparena = ctx->tr_bp.as<uint8_t>();
+    tp.bpcap = bpcap;
+    tp.cellrec = ctx->cellrec.as<uint2>();
+    tp.preds = ctx->preds.as<uint16_t>();
+    tp.progs = ctx->progs_d.as<ProgDev>();
+    tp.class_prog = ctx->class_prog_d.as<int32_t>();
+    tp.prefix = ctx->prefix.as<double>();
+    tp.domain = ctx->domain.as<double>();
+    tp.nv_stride = ctx->nv_stride;
+    tp.n_codes = ctx->n_codes;
+    tp.qtab = ctx->qtab.as<double>();
+    tp.v1g = ctx->v1g_d.as<double>();
+    tp.v1off = ctx->v1off_d.as<uint64_t>();
   }
-  CK(upload(ctx->tr_vbase, vbase.data(), vbase.size()));
-  CK(upload(ctx->tr_bbase, bbase.data(), bbase.size()));
-  CK(upload(ctx->tr_stcls, stcls.data(), stcls.size()));
-  CK(upload(ctx->tr_stitem, stitem.data(), stitem.size()));
-  CK(upload(ctx->tr_stn, stn.data(), stn.size()));
-  CK(ctx->tr_vals0.ensure(sizeof(double) * vmax));
-  CK(ctx->tr_vals1.ensure(sizeof(double) * vmax));
-  CK(ctx->tr_bp.ensure(bacc + 16));
-  tp.vbase = ctx->tr_vbase.as<uint64_t>();
-  tp.bbase = ctx->tr_bbase.as<uint64_t>();
-  tp.st_cls = ctx->tr_stcls.as<int32_t>();
-  tp.st_item = ctx->tr_stitem.as<uint64_t>();
-  tp.st_n = ctx->tr_stn.as<int32_t>();
-  tp.vals[0] = ctx->tr_vals0.as<double>();
-  tp.vals[1] = ctx->tr_vals1.as<double>();
-  tp.bp = ctx->tr_bp.as<uint8_t>();
-  unsigned long long* exec = ep.exec_counters ? ep.exec_counters + 1 : nullptr;
-  for (int j = 2; j <= ctx->max_pp; ++j) {
-    if (!total[j]) continue;
-    const int gs = (int)std::min<uint64_t>((total[j] + 255) / 256, (uint64_t)ctx->sms * 16);
-    k_trie_stage<<<gs, 256, 0, ctx->stream>>>(tp, j, total[j], exec);
-    ctx->launches += 1;
-  }
-  k_trie_back<<<g, 256, 0, ctx->stream>>>(tp);
+  k_sig_init<<<g, 256, 0, ctx->stream>>>(tp);
+  DBG_SYNC("k_sig_init");
   CK(cudaGetLastError());
   ctx->launches += 1;
-  if (ep.exec_counters)  // DP instances solved: one per signature
-    CK(cudaMemcpyAsync(ep.exec_counters, ctx->dd_nrep.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice,
-                       ctx->stream));
+  if (ctx->trie) {
+    const int tg = ctx->sms * 4;
+    for (int d = 1; d <= ctx->trie_nq; ++d) {
+      k_level_up<<<kScanGrid, kScanThreads, 0, ctx->stream>>>(tp, d);
+      DBG_SYNC("k_level_up");
+      k_level_down<<<kScanGrid, kScanThreads, 0, ctx->stream>>>(tp, d);
+      DBG_SYNC("k_level_down");
+      k_level_assign<<<g, 256, 0, ctx->stream>>>(tp, d);
+      DBG_SYNC("k_level_assign");
+      while ((int)ctx->tev.size() < ctx->tev_used + 2) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        ctx->tev.push_back(e);
+      }
+      CK(cudaEventRecord(ctx->tev[ctx->tev_used++], ctx->stream));
+      k_trie_tiles<<<tg, kTrieThreads, kTrieSmem, ctx->stream>>>(tp, d);
+      DBG_SYNC("k_trie_tiles");
+      CK(cudaEventRecord(ctx->tev[ctx->tev_used++], ctx->stream));
+      CK(cudaGetLastError());
+      ctx->launches += 4;
+    }
+    k_trie_back<<<g, 256, 0, ctx->stream>>>(tp);
+    DBG_SYNC("k_trie_back");
+    CK(cudaGetLastError());
+    ctx->launches += 1;
+    if ((size_t)(ctx->ovf_used + 1) * sizeof(uint32_t) > ctx->ovf_log.bytes) {
+      // (grows between runs only: a run's chunk count is bounded by the first)
+      CK(ctx->ovf_log.ensure(sizeof(uint32_t) * std::max(64, 2 * (ctx->ovf_used + 1))));
+    }
+    CK(cudaMemcpyAsync(ctx->ovf_log.as<uint32_t>() + ctx->ovf_used,
+                       reinterpret_cast<const char*>(tp.st) + offsetof(TrieState, ovf), sizeof(uint32_t),
+                       cudaMemcpyDeviceToDevice, ctx->stream));
+    ++ctx->ovf_used;
+  }
+  // signature-mode K_dp: the whole DP when the trie is off; with the trie
+  // only if its capacity was exceeded on the device (it exits otherwise)
+  EvalParams es = ep;
+  es.sig_keys = ctx->dd_rep_key.as<uint64_t>();
+  es.sig_guard = ctx->trie ? reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(tp.st) +
+                                                               offsetof(TrieState, ovf))
+                          : nullptr;
+  es.n_rep = reinterpret_cast<const uint64_t*>(hp.n_uniq);
+  es.rep_list = nullptr;
+  es.repcuts = ctx->dd_repcuts.as<uint8_t>();
+  es.sig_code_bits = ctx->code_bits;
+  void* args[] = {&es};
+  CK(cudaLaunchKernel(ctx->eval_fn, dim3(ctx->n_ctas), dim3(ctx->eval_threads), args, ctx->smem_bytes,
+                      ctx->stream));
+  CK(cudaGetLastError());
+  DBG_SYNC("k_dp_multi (signatures)");
+  ctx->launches += 1;
   return AMP_OK;
 }
 
@@ -1181,27 +1282,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   ep.rsum_p = ctx->rsum_p.as<double>();
   ep.n_cls_total = (int)ctx->classes.size();
   if (ctx->dedup && !d_given_cuts) {
-    CK(ctx->dd_keys.ensure(sizeof(uint64_t) * C));
-    CK(ctx->dd_skeys.ensure(sizeof(uint64_t) * C));
-    CK(ctx->dd_vals.ensure(sizeof(uint32_t) * C));
-    CK(ctx->dd_svals.ensure(sizeof(uint32_t) * C));
-    CK(ctx->dd_flags.ensure(sizeof(uint32_t) * C));
-    CK(ctx->dd_runid.ensure(sizeof(uint32_t) * C));
-    CK(ctx->dd_rep_list.ensure(sizeof(uint32_t) * C));
     CK(ctx->dd_rep_of.ensure(sizeof(uint32_t) * C));
-    if (ctx->trie) CK(ctx->dd_rep_key.ensure(sizeof(uint64_t) * C));
-    CK(ctx->dd_repcuts.ensure((size_t)C * (ctx->max_pp + 1)));
-    size_t t1 = 0, t2 = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, t1, (const uint64_t*)nullptr, (uint64_t*)nullptr,
-                                       (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)C, 0,
-                                       ctx->key_bits, ctx->stream));
-    CK(cub::DeviceScan::InclusiveSum(nullptr, t2, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                     (int)C, ctx->stream));
-    size_t t3 = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, t3, (const uint64_t*)nullptr, (uint64_t*)nullptr,
-                                     (int)C + 1, ctx->stream));
-    ctx->dd_temp_bytes = std::max(std::max(t1, t2), t3);
-    CK(ctx->dd_temp.ensure(ctx->dd_temp_bytes + 16));
     CK(cudaMemsetAsync(ctx->dd_counters.p, 0, 2 * sizeof(unsigned long long), ctx->stream));
     ep.exec_counters = ctx->dd_counters.as<unsigned long long>();
     ep.prog_inner = ctx->prog_inner_d.as<double>();
@@ -1226,6 +1307,8 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     CK(cudaFuncSetAttribute(k_est, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)est_smem));
   ctx->stats.dp_items = 0;
   ctx->stats.dp_launches = 0;
+  ctx->tev_used = 0;
+  ctx->ovf_used = 0;
   ctx->stats.dp_group = ctx->multi_b;
   // thread-per-candidate K_place / K_est (amp_thread.cuh): |D| <= 16 with
   // coded bandwidths; AMP_NO_THREAD=1 keeps the warp kernels
@@ -1261,7 +1344,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   // the boundary codes are read by K_dp without the trie, the sort dedup
   // path and K_est's pp == 2 items placed by K_place; with the hash dedup on
   // K_place's signature keys, the trie and the fused light path, nothing
-  ep.need_bwcb = !(ep.sigkey && ctx->trie && ep.fuse_light && std::getenv("AMP_DEDUP_SORT") == nullptr);
+  ep.need_bwcb = !(ep.sigkey && ctx->dedup && ep.fuse_light);
   // ---- light tail on the aux stream -------------------------------------
   // The pp <= 2 items [n_heavy, n_work) of a segment run need no K_place /
   // K_dp (K_est places them itself), so their K_est runs on a second stream
@@ -1293,22 +1376,15 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   }
   ctx->kev_used = 4 * n_chunks;
   ctx->kev_pending = true;
-  // signature hash table of a chunk (amp_dedup.cuh): sized for ep.n_dp
-  // items at load <= 1/2; entries carry an epoch tag above the key bits, so
-  // the table is cleared only when it is (re)allocated or the tag wraps
-  // full = false: sized for 4x the previous chunk's distinct keys (at least
-  // 2^22 slots, AMP_HASH_MIN_LOG2) instead of for every item, so a fresh
-  // table costs a 32 MB clear, not 1 GB; an overflow (n_uniq[1]) or a load
-  // above 1/2 redoes the chunk's inserts with the full-size table
-  auto prepare_hash = [&](HashParams& hp, bool full) -> int {
+  // signature hash table of a chunk (amp_dedup.cuh): sized for every heavy
+  // item at load <= 1/2, so every insert finds its slot (no overflow, no
+  // host check); entries carry an epoch tag above the key bits, so the table
+  // is cleared only when it is (re)allocated or the tag wraps.  Only the
+  // slots of distinct keys are touched (L2-resident), whatever the size.
+  auto prepare_hash = [&](HashParams& hp) -> int {
     uint64_t T = 1024;
     while (T < 2 * ep.n_dp) T <<= 1;
-    if (!full) {
-      const char* ml = std::getenv("AMP_HASH_MIN_LOG2");
-      uint64_t t = 1ull << (ml ? std::atoi(ml) : 22);
-      while (t < 4 * ctx->hash_last_uniq) t <<= 1;
-      T = std::min(T, t);
-    }
+    T = std::max<uint64_t>(T, ctx->hash_T);  // keep a larger table (and its epoch)
     const bool grown = ctx->dd_tkey.bytes < sizeof(uint64_t) * T;
     CK(ctx->dd_tkey.ensure(sizeof(uint64_t) * T));
     CK(ctx->dd_tval.ensure(sizeof(uint32_t) * T));
@@ -1336,7 +1412,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     hp.max_pp = ctx->max_pp;
     hp.code_bits = ctx->code_bits;
     hp.mask = T - 1;
-    hp.max_probe = full ? T : std::min<uint64_t>(T, 4096);
+    hp.max_probe = T;
     hp.epoch = ctx->hash_epoch;
     hp.epoch_shift = esh;
     hp.sigkey = ep.sigkey;
@@ -1345,17 +1421,13 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     hp.slot_of = ctx->dd_slot.as<uint32_t>();
     hp.uniq = ctx->dd_uniq.as<uint32_t>();
     hp.n_uniq = ctx->dd_nuniq.as<unsigned long long>();
-    hp.skeys = ctx->dd_skeys.as<uint64_t>();
-    hp.sslots = ctx->dd_svals.as<uint32_t>();
-    hp.rep_key = ctx->trie ? ctx->dd_rep_key.as<uint64_t>() : nullptr;
     return AMP_OK;
   };
   // K_place_t inserts the keys itself (no key round trip, one launch less)
   const bool fuse_hash_ok = thread_mode && ep.sigkey && ctx->dedup && !d_given_cuts &&
-                            std::getenv("AMP_DEDUP_SORT") == nullptr &&
                             std::getenv("AMP_NO_FUSE_HASH") == nullptr;
   HashParams fused_hp{};
-  ep.skip_work = ep.est_fast && ctx->dedup && ctx->trie && fuse_hash_ok && ep.fuse_light &&
+  ep.skip_work = ep.est_fast && ctx->dedup && fuse_hash_ok && ep.fuse_light &&
                  std::getenv("AMP_KEEP_WORK") == nullptr;
   if (overlap) {
     CK(cudaEventRecord(ctx->aux_start, ctx->stream));
@@ -1374,6 +1446,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
       ea.n_chunk = std::min<uint64_t>(C, n_work - t0);
       ea.first_chunk = t0 == n_heavy;
       k_est_t<16, true><<<aux_ctas, kEstTWarps * 32, 0, ctx->aux>>>(ea);
+      DBG_SYNC("k_est_t");
       CK(cudaGetLastError());
       CK(cudaEventRecord(ev[3], ctx->aux));
       ctx->launches += 1;
@@ -1395,7 +1468,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     ep.first_chunk = t0 == 0;
     ep.fuse_hash = 0;
     if (fuse_hash_ok && ep.n_dp > 0) {
-      const int rc = prepare_hash(fused_hp, false);
+      const int rc = prepare_hash(fused_hp);
       if (rc != AMP_OK) return rc;
       ep.fuse_hash = 1;
       ep.h_tkey = fused_hp.tkey;
@@ -1418,8 +1491,10 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
         k_place_t<16><<<tg, 256, 0, ctx->stream>>>(ep);
       else
         k_place_t<0><<<tg, 256, 0, ctx->stream>>>(ep);
+      DBG_SYNC("k_place_t");
     } else {
       k_place<<<place_grid, 256, place_smem, ctx->stream>>>(ep);
+      DBG_SYNC("k_place");
     }
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), ctx->stream));
@@ -1431,139 +1506,49 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     ep.run_slot = nullptr;
     ep.run_of_slot = nullptr;
     ep.run_pipe = nullptr;
-    uint64_t n_runs_host = 0;  // distinct signatures of the chunk (hash path)
     bool skip_dp = false;
     if (ctx->dedup && !d_given_cuts && ep.n_dp > 0) {
-      // ---- memoisation: one DP per distinct signature ---------------------
+      // ---- memoisation: one DP per distinct signature (amp_dedup.cuh) ------
       const int g = (int)std::min<uint64_t>((ep.n_dp + 255) / 256, (uint64_t)ctx->sms * 8);
-      DedupParams dp{};
-      dp.rep_list = ctx->dd_rep_list.as<uint32_t>();
-      dp.rep_of = ctx->dd_rep_of.as<uint32_t>();
-      dp.n_rep = ctx->dd_nrep.as<uint64_t>();
-      if (std::getenv("AMP_DEDUP_SORT")) {
-        // full radix sort of the item keys (comparison path)
-        dp.work = ep.work;
-        dp.cls = ep.cls;
-        dp.bwcb = ep.bwcb;
-        dp.n = ep.n_dp;
-        dp.max_pp = ctx->max_pp;
-        dp.code_bits = ctx->code_bits;
-        dp.keys = ctx->dd_keys.as<uint64_t>();
-        dp.vals = ctx->dd_vals.as<uint32_t>();
-        dp.skeys = ctx->dd_skeys.as<uint64_t>();
-        dp.svals = ctx->dd_svals.as<uint32_t>();
-        dp.flags = ctx->dd_flags.as<uint32_t>();
-        dp.runid = ctx->dd_runid.as<uint32_t>();
-        dp.rep_key = ctx->trie ? ctx->dd_rep_key.as<uint64_t>() : nullptr;
-        k_dedup_keys<<<g, 256, 0, ctx->stream>>>(dp);
-        size_t tb = ctx->dd_temp_bytes;
-        CK(cub::DeviceRadixSort::SortPairs(ctx->dd_temp.p, tb, dp.keys, ctx->dd_skeys.as<uint64_t>(),
-                                           dp.vals, ctx->dd_svals.as<uint32_t>(), (int)ep.n_dp, 0,
-                                           ctx->key_bits, ctx->stream));
-        k_dedup_heads<<<g, 256, 0, ctx->stream>>>(dp);
-        tb = ctx->dd_temp_bytes;
-        CK(cub::DeviceScan::InclusiveSum(ctx->dd_temp.p, tb, dp.flags, ctx->dd_runid.as<uint32_t>(),
-                                         (int)ep.n_dp, ctx->stream));
-        k_dedup_reps<<<g, 256, 0, ctx->stream>>>(dp);
-        k_dedup_scatter<<<g, 256, 0, ctx->stream>>>(dp);
-        CK(cudaGetLastError());
-        ctx->launches += 6;
+      HashParams hp{};
+      if (ep.fuse_hash) {
+        hp = fused_hp;  // table prepared before K_place_t, which inserted the keys
       } else {
-        // hash the item keys (amp_dedup.cuh), sort only the distinct ones
-        HashParams hp{};
-        if (ep.fuse_hash) {
-          hp = fused_hp;  // table prepared before K_place_t, which inserted the keys
-        } else {
-          const int rc = prepare_hash(hp, false);
-          if (rc != AMP_OK) return rc;
-        }
-        hp.rep_list = dp.rep_list;
-        hp.rep_of = dp.rep_of;
-        hp.n_rep = dp.n_rep;
-        if (!ep.fuse_hash) k_hash_insert<<<g, 256, 0, ctx->stream>>>(hp);
-        unsigned long long nuo[2] = {0, 0};
-        CK(cudaMemcpyAsync(nuo, ctx->dd_nuniq.p, sizeof nuo, cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-        if (nuo[1] || 2 * nuo[0] > hp.mask + 1) {
-          // the table sized from the last chunk overflowed: redo with the
-          // full-size one (fused: K_place again — same work, new keys' slots)
-          ctx->stats_hash_redo += 1;
-          const int rc = prepare_hash(hp, true);
-          if (rc != AMP_OK) return rc;
-          hp.rep_list = dp.rep_list;
-          hp.rep_of = dp.rep_of;
-          hp.n_rep = dp.n_rep;
-          if (ep.fuse_hash) {
-            ep.h_tkey = hp.tkey;
-            ep.h_tval = hp.tval;
-            ep.h_slot_of = hp.slot_of;
-            ep.h_uniq = hp.uniq;
-            ep.h_nuniq = hp.n_uniq;
-            ep.h_mask = hp.mask;
-            ep.h_max_probe = hp.max_probe;
-            ep.h_epoch = hp.epoch;
-            ep.h_eshift = hp.epoch_shift;
-            const int tg = (int)std::min<uint64_t>((ep.n_chunk + 255) / 256, (uint64_t)ctx->sms * 16);
-            if (shape16)
-              k_place_t<16, true><<<tg, 256, 0, ctx->stream>>>(ep);
-            else if (ctx->D == 16)
-              k_place_t<16><<<tg, 256, 0, ctx->stream>>>(ep);
-            else
-              k_place_t<0><<<tg, 256, 0, ctx->stream>>>(ep);
-          } else {
-            k_hash_insert<<<g, 256, 0, ctx->stream>>>(hp);
-          }
-          CK(cudaGetLastError());
-          CK(cudaMemcpyAsync(nuo, ctx->dd_nuniq.p, sizeof nuo, cudaMemcpyDeviceToHost, ctx->stream));
-          CK(cudaStreamSynchronize(ctx->stream));
-          if (nuo[1]) return fail(ctx, AMP_E_CUDA, "signature hash table overflow");
-        }
-        const unsigned long long nu = nuo[0];
-        ctx->hash_last_uniq = nu;
-        n_runs_host = nu;
-        const int gu = (int)std::min<uint64_t>((nu + 255) / 256 + 1, (uint64_t)ctx->sms * 8);
-        k_hash_gather<<<gu, 256, 0, ctx->stream>>>(hp, ctx->dd_keys.as<uint64_t>(),
-                                                    ctx->dd_vals.as<uint32_t>());
-        if (nu > 0) {
-          size_t tb = ctx->dd_temp_bytes;
-          CK(cub::DeviceRadixSort::SortPairs(ctx->dd_temp.p, tb, ctx->dd_keys.as<uint64_t>(),
-                                             ctx->dd_skeys.as<uint64_t>(), ctx->dd_vals.as<uint32_t>(),
-                                             ctx->dd_svals.as<uint32_t>(), (int)nu, 0, ctx->key_bits,
-                                             ctx->stream));
-        }
-        k_hash_runs<<<gu, 256, 0, ctx->stream>>>(hp);
-        // the shape kernels look the run up through the table themselves
-        // (the trie reads rep_list / rep_key only); others need rep_of
-        if (ep.est_fast && ctx->trie && std::getenv("AMP_NO_RUN_SLOT") == nullptr) {
-          ep.run_slot = hp.slot_of;
-          ep.run_of_slot = hp.tval;
-        } else {
-          k_hash_scatter<<<g, 256, 0, ctx->stream>>>(hp);
-        }
-        CK(cudaGetLastError());
-        ctx->launches += 5;
-      }
-      ep.rep_list = dp.rep_list;
-      ep.rep_of = dp.rep_of;
-      ep.n_rep = dp.n_rep;
-      ep.repcuts = ctx->dd_repcuts.as<uint8_t>();
-      if (ctx->trie) {
-        const int rc = run_trie(ctx, ep, n_runs_host);
+        const int rc = prepare_hash(hp);
         if (rc != AMP_OK) return rc;
-        skip_dp = true;  // K_dp's work is done (K_est reads the cuts via rep_of)
-        if (ep.est_fast && n_runs_host > 0 && std::getenv("AMP_NO_RUN_PIPE") == nullptr) {
-          // by hash slot when K_est looks runs up by slot, else by run
-          const bool by_slot = ep.run_slot != nullptr;
-          CK(ctx->dd_runpipe.ensure(sizeof(double) * (by_slot ? ctx->hash_T : n_runs_host)));
-          const int gr = (int)std::min<uint64_t>((n_runs_host + 255) / 256, (uint64_t)ctx->sms * 8);
-          k_run_pipe<<<gr, 256, 0, ctx->stream>>>(ep, ctx->dd_rep_key.as<uint64_t>(), n_runs_host,
-                                                   ctx->dd_runpipe.as<double>(),
-                                                   by_slot ? ctx->dd_svals.as<uint32_t>() : nullptr);
-          CK(cudaGetLastError());
-          ctx->launches += 1;
-          ep.run_pipe = ctx->dd_runpipe.as<double>();
-        }
+        k_hash_insert<<<g, 256, 0, ctx->stream>>>(hp);
+        DBG_SYNC("k_hash_insert");
+        ctx->launches += 1;
       }
+      const int rc = run_sig_dp(ctx, ep, hp);
+      if (rc != AMP_OK) return rc;
+      hp.rep_of = ctx->dd_rep_of.as<uint32_t>();
+      // K_est finds an item's signature through its hash slot (tval: slot ->
+      // signature after K_sig_init); the generic bodies read rep_of
+      if (ep.est_fast && std::getenv("AMP_NO_RUN_SLOT") == nullptr) {
+        ep.run_slot = hp.slot_of;
+        ep.run_of_slot = hp.tval;
+      } else {
+        k_hash_scatter<<<g, 256, 0, ctx->stream>>>(hp);
+        DBG_SYNC("k_hash_scatter");
+        ctx->launches += 1;
+        ep.rep_of = hp.rep_of;
+      }
+      ep.repcuts = ctx->dd_repcuts.as<uint8_t>();
+      if (ep.est_fast && std::getenv("AMP_NO_RUN_PIPE") == nullptr) {
+        // dp == 1 classes: the whole estimate per signature, by hash slot when
+        // K_est looks signatures up by slot
+        const bool by_slot = ep.run_slot != nullptr;
+        CK(ctx->dd_runpipe.ensure(sizeof(double) * (by_slot ? ctx->hash_T : ep.n_dp)));
+        k_run_pipe<<<g, 256, 0, ctx->stream>>>(ep, ctx->dd_rep_key.as<uint64_t>(), hp.n_uniq,
+                                                 ctx->dd_runpipe.as<double>(),
+                                                 by_slot ? hp.uniq : nullptr);
+        DBG_SYNC("k_run_pipe");
+        CK(cudaGetLastError());
+        ctx->launches += 1;
+        ep.run_pipe = ctx->dd_runpipe.as<double>();
+      }
+      skip_dp = true;  // K_dp's work is done (K_est reads the cuts by signature)
     }
     ctx->stats.dp_items += ep.n_dp;
     if (ep.n_dp > 0 && !skip_dp) {
@@ -1583,6 +1568,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
       k_est_t<0><<<ctx->est_ctas, kEstTWarps * 32, 0, ctx->stream>>>(ep);
     else
       k_est<<<ctx->est_ctas, kEstWarps * 32, est_smem, ctx->stream>>>(ep);
+    DBG_SYNC("k_est");
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev[3], ctx->stream));
     ctx->launches += 2;

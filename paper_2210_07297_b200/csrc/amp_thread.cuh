@@ -379,10 +379,11 @@ __device__ __forceinline__ void est_shape(const EvalParams& p, const uint8_t* co
 // reads one value per item.  Same operations and order as est_shape.
 // out is indexed by run, or by the run's hash slot when slot_of_run is given
 // (K_est then reads it through the item's slot: one dependent load less).
-__global__ void k_run_pipe(EvalParams p, const uint64_t* rep_key, uint64_t n_runs, double* out,
-                           const uint32_t* slot_of_run) {
+__global__ void k_run_pipe(EvalParams p, const uint64_t* rep_key, const unsigned long long* n_runs_d,
+                           double* out, const uint32_t* slot_of_run) {
   const int nq = p.max_pp - 1, cb = p.sig_code_bits, L = p.L, LP = L + 1, maxpp = p.max_pp;
   const uint64_t cmask = (1ull << cb) - 1;
+  const uint64_t n_runs = *n_runs_d;
   for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_runs;
        r += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t key = rep_key[r];

@@ -1,29 +1,40 @@
 // amp_trie.cuh — the layer-partition DP shared across signature prefixes.
 //
 // Stage j of the DP (pipeline_dp.cpp:114-131) reads stage j-1 and the edge
-// costs of boundary j-2 only.  So the values and argmins of stage j are a
-// function of the class and of the boundary codes c_0 .. c_{j-2}: every
-// signature (class, c_0 .. c_{k-2}) with the same first j-1 codes has the
-// same stage-j table.  After the signature sort (amp_dedup.cuh) the
-// representatives are in key order, i.e. lexicographic in (class, c_0,
-// c_1, ...).  The signatures sharing a prefix of length d therefore form a
-// run; the runs are the nodes of a trie, and stage j is solved once per node
-// of depth j-1 instead of once per signature.  The operations per cell and
-// cut are those of the per-candidate kernels (same operands, same order,
-// same strict '<'), so every cut is bit-identical (tested against
-// AMP_FLAG_NO_DEDUP).
+// costs of boundary j-2 only, so the stage-j table of a candidate is a
+// function of its class and of its boundary codes c_0 .. c_{j-2}.  The
+// distinct signatures (class, c_0 .. c_{pp-2}) of a chunk (amp_dedup.cuh)
+// are the leaves of a trie whose depth-d nodes are the distinct prefixes
+// (class, c_0 .. c_{d-1}); stage j is solved once per node of depth j-1
+// instead of once per signature.  Per cell and cut the operations are those
+// of pipeline_dp.cpp:118-127 (same operands, same order, same strict '<'),
+// so every cut is bit-identical to the reference (tested against the
+// one-DP-per-candidate kernel).
 //
-// Layout: the nodes of one depth are class-contiguous.  The stage-j table of
-// class c is cell-major over its K nodes — value / argmin of (cell x, node
-// n) at base_c + x*K + (n - nb_c) — so the threads of a warp share a cell
-// (program record, predecessor list, prefix, domain: broadcast loads, no
-// divergence in the cut loop) and touch consecutive nodes (coalesced).
-//
-//   K_flag(d)    head flags of the depth-d runs        -> scan -> nid_d (1-based)
-//   K_nodes(d)   first signature and parent of every node, class node ranges
-//   (host)       one read of the ranges; table bases, per-stage item lists
-//   K_stage(j)   one thread per (class, cell of N_j, node of depth j-1)
-//   K_back       one thread per signature: walk its trie path, write its cuts
+// Everything is built and scheduled on the device — no host round trip:
+//   K_sig_init     the hash table's distinct keys -> signature list (hash
+//                  order), slot -> signature map, root of each signature,
+//                  depth-1 child marks
+//   per depth d = 1 .. nq:
+//     K_level_up   per-CTA sums of the child marks          (fixed grid)
+//     K_level_down exclusive scan -> depth-d node ids in (parent, code)
+//                  order: lexicographic, class-contiguous, children of a
+//                  parent adjacent.  The last CTA plans the level: per
+//                  class node range, tiles, value / argmin table bases
+//                  (device bump allocation; capacity overflow raises `ovf`
+//                  and the signature-mode K_dp (amp_dp_multi.cuh) solves the
+//                  chunk instead)
+//     K_level_assign each signature's depth-d node; marks for depth d+1
+//     K_trie_tiles   stage j = d+1.  One CTA per tile = (class, run of <= TN
+//                  consecutive depth-d nodes).  The tile's parents are
+//                  consecutive depth-(d-1) nodes; their stage-(j-1) tables
+//                  are staged in shared memory (transposed, odd stride: the
+//                  lanes of a warp read distinct banks), with the class's
+//                  edge rows and prefix sums.  Thread = (cell of N_j, group
+//                  of 4 nodes): per cut the predecessor index, t2 and the
+//                  tolerance term are shared by the 4 nodes.
+//   K_trie_back    one thread per signature: backtrack (pipeline_dp.cpp:
+//                  134-148) along its trie path, write its cuts.
 #pragma once
 
 #include "amp_common.cuh"
@@ -31,256 +42,405 @@
 
 namespace amp {
 
-constexpr int kTrieMaxCls = 256;  // classes per stage list held in smem
+constexpr int kTrieMaxD1 = 64;       // depths 0 .. nq (keys are <= 63 bits, >= 1 bit per code)
+constexpr int kTrieThreads = 256;    // K_trie_tiles block
+constexpr int kTrieNB = 4;           // nodes per thread (share the cell's work)
+constexpr int kScanGrid = 296;       // CTAs of the level scans
+constexpr int kScanThreads = 512;
+constexpr int kTrieSmem = 46 * 1024; // K_trie_tiles dynamic smem budget (4 CTAs / SM)
+
+// Level state, in device memory (reset by K_sig_init every chunk).
+struct TrieState {
+  uint32_t cnt[kTrieMaxD1];        // nodes per depth (depth 0: the heavy classes)
+  uint64_t node_off[kTrieMaxD1];   // start of depth d's nodes in the node arrays
+  uint32_t ntiles[kTrieMaxD1];     // tiles of stage d+1
+  unsigned long long bp_bump;      // argmin bytes allocated
+  uint32_t ovf;                    // capacity exceeded: signature-mode K_dp instead
+  uint32_t ticket;                 // last-CTA election of K_level_down
+};
+
+// Per (class, stage j) facts of the class's pruned program (host-built).
+struct TrieStage {
+  uint32_t cell0;   // first cell of N_j in cellrec (absolute)
+  uint32_t n;       // |N_j|
+  uint32_t iters;   // (cell, cut) pairs of stage j (unpadded)
+  uint32_t tn;      // nodes per K_trie_tiles tile
+};
 
 struct TrieParams {
-  // signatures (run heads of the sorted keys)
-  const uint64_t* n_rep;      // device count
-  const uint64_t* rep_key;    // [n_rep]
-  const uint32_t* rep_list;   // [n_rep] chunk item of each signature
-  int32_t nq, cb;             // codes per key, bits per code
-  int32_t L, max_pp;
-  int32_t n_cls, pad0;
-  uint64_t stride;            // n_rep (row stride of the per-depth arrays)
-  uint32_t* nid;              // [nq + 1][stride]  node id (1-based) at depth d
-  uint32_t* first;            // [nq + 1][stride]  first signature of each node
-  uint32_t* parent;           // [nq + 1][stride]  node of depth d-1 it extends
-  uint32_t* flags;            // [stride] scratch
-  uint32_t* range;            // [nq + 1][n_cls][2]  node range [nb, ne) of each class
-  // host-computed tables (after one read of `range`)
-  const uint64_t* vbase;      // [nq + 1][n_cls]  value-table base of (depth, class)
-  const uint64_t* bbase;      // [nq + 1][n_cls]  argmin-table base of (depth, class)
-  const int32_t* st_cls;      // [max_pp + 1][n_cls]  classes of stage j's item list
-  const uint64_t* st_item;    // [max_pp + 1][n_cls + 1]  exclusive item bases
-  const int32_t* st_n;        // [max_pp + 1]  classes in stage j's list
+  // signatures: the distinct keys of the chunk's hash table
+  const unsigned long long* n_sig;  // device count
+  const uint32_t* uniq;             // [n_sig] slots
+  const unsigned long long* tkey;
+  uint32_t* tval;                   // slot -> first item, rewritten to slot -> signature
+  int32_t key_shift;                // epoch tag position (64: none)
+  int32_t nq, cb, U, L, max_pp, n_cls, n_roots;
+  uint64_t* sig_key;                // [n] class | codes
+  uint32_t* rep_item;               // [n] first item of each signature
+  uint32_t* nid;                    // [n] node at the current depth (local id)
+  const int32_t* root_rank;         // [n_cls] rank among the roots (-1: not heavy)
+  const int32_t* root_cls;          // [n_roots] class of each root
+  TrieState* st;
+  uint8_t* pres;                    // child marks [cnt[d-1] * U]
+  uint32_t* cid;                    // their scan: child node id
+  uint64_t pres_cap;
+  uint32_t* partial;                // [kScanGrid]
+  uint32_t* npar;                   // node arrays (absolute index node_off[d] + id)
+  uint16_t* ncls;
+  uint8_t* ncode;
+  uint64_t node_cap;
+  // level plans [kTrieMaxD1][n_cls] (tbase: [kTrieMaxD1][n_cls + 1])
+  uint32_t* nb;
+  uint32_t* nK;
+  uint64_t* vbase;
+  uint64_t* bbase;
+  uint32_t* tbase;
+  const TrieStage* tstage;          // [n_cls][max_pp + 1]
+  double* varena[2];                // values of depth d in varena[d & 1]
+  uint64_t vcap;                    // doubles per arena
+  uint8_t* bparena;                 // argmins of every depth
+  uint64_t bpcap;
   // problem tables
   const ClassDev* cls;
-  const int32_t* class_prog;
-  const ProgDev* progs;
-  const uint32_t* stage;
   const uint2* cellrec;
   const uint16_t* preds;
+  const ProgDev* progs;
+  const int32_t* class_prog;
   const double* prefix;
   const double* domain;
   int32_t nv_stride, n_codes;
-  const double* qtab;         // [n_cls][n_codes][L]
-  const double* v1g;          // stage-1 values per class (v1off)
-  const uint64_t* v1off;      // [n_cls]
-  // stage storage
-  double* vals[2];            // ping-pong by stage parity
-  uint8_t* bp;                // argmins of all stages
-  uint8_t* repcuts;           // [n_rep][max_pp + 1] cuts per signature run
+  const double* qtab;               // [n_cls][n_codes][L]
+  const double* v1g;                // stage-1 values per class (v1off)
+  const uint64_t* v1off;
+  uint8_t* repcuts;                 // [n_sig][max_pp + 1] cuts per signature
+  unsigned long long* exec;         // [2]: DP instances, inner iterations (or NULL)
 };
 
-__device__ __forceinline__ int key_cls(const TrieParams& p, uint64_t k) {
-  return (int)(k >> (p.nq * p.cb));
-}
-__device__ __forceinline__ int key_code(const TrieParams& p, uint64_t k, int q) {
-  return (int)((k >> ((p.nq - 1 - q) * p.cb)) & ((1ull << p.cb) - 1));
+__device__ __forceinline__ int trie_cls(const TrieParams& p, uint64_t k) { return (int)(k >> (p.nq * p.cb)); }
+__device__ __forceinline__ int trie_code(const TrieParams& p, uint64_t k, int q) {
+  return (int)((k >> ((p.nq - 1 - q) * p.cb)) & (uint64_t)(p.U - 1));
 }
 
-// head flags of the depth-d runs (d codes + the class)
-__global__ void k_trie_flag(TrieParams p, int d) {
-  const uint64_t n = *p.n_rep;
-  const int sh = (p.nq - d) * p.cb;
-  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
-       r += (uint64_t)gridDim.x * blockDim.x)
-    p.flags[r] = (r == 0 || (p.rep_key[r] >> sh) != (p.rep_key[r - 1] >> sh)) ? 1u : 0u;
-}
-
-// first signature and parent of every depth-d node; node range of each
-// class (the failed / pp <= 2 run, key ~0, belongs to no class)
-__global__ void k_trie_nodes(TrieParams p, int d) {
-  const uint64_t n = *p.n_rep;
-  const uint32_t* nid = p.nid + (size_t)d * p.stride;
-  uint32_t* first = p.first + (size_t)d * p.stride;
-  uint32_t* parent = p.parent + (size_t)d * p.stride;
-  uint32_t* range = p.range + (size_t)d * p.n_cls * 2;
-  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
-       r += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t node = nid[r] - 1;
-    if (r == 0 || nid[r] != nid[r - 1]) {  // node head
-      first[node] = (uint32_t)r;
-      parent[node] = d >= 2 ? p.nid[(size_t)(d - 1) * p.stride + r] - 1 : 0;
+// signature list, slot -> signature, roots, depth-1 marks; resets the state
+__global__ void k_sig_init(TrieParams p) {
+  const uint64_t n = *p.n_sig;
+  if (p.st && blockIdx.x == 0 && threadIdx.x == 0) {  // (no state: trie off)
+    p.st->cnt[0] = (uint32_t)p.n_roots;
+    p.st->node_off[0] = 0;
+    p.st->bp_bump = 0;
+    p.st->ovf = 0;
+    p.st->ticket = 0;
+  }
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = p.uniq[i];
+    const unsigned long long k = p.tkey[s];
+    const uint64_t key = p.key_shift >= 64 ? k : (k & ((1ull << p.key_shift) - 1));
+    p.sig_key[i] = key;
+    p.rep_item[i] = p.tval[s];
+    p.tval[s] = (uint32_t)i;
+    if (p.pres) {
+      const int c = trie_cls(p, key);
+      const int r = p.root_rank[c];
+      p.nid[i] = (uint32_t)r;
+      if (p.cls[c].pp - 1 >= 1) p.pres[(uint64_t)r * p.U + trie_code(p, key, 0)] = 1;
     }
-    const uint64_t key = p.rep_key[r];
-    if (key == ~0ull) continue;
-    const int c = key_cls(p, key);
-    // the class's first signature opens its node range, its last closes it
-    if (r == 0 || key_cls(p, p.rep_key[r - 1]) != c) range[2 * c] = node;
-    if (r + 1 == n || p.rep_key[r + 1] == ~0ull || key_cls(p, p.rep_key[r + 1]) != c)
-      range[2 * c + 1] = node + 1;
   }
 }
 
-// Per-class facts of one stage, cached in shared memory.
-struct TrieSlot {
-  uint64_t ibase;      // first item of the class in the stage
-  uint64_t vbase, bbase, vbase_p;  // table bases at depth d, d (argmins), d-1
-  uint64_t v1off;
-  uint32_t nb, K, nb_p, K_p;       // node ranges at depth d and d-1
-  uint32_t cell0, pred_base_lo, pred_base_hi, pad;  // program: first cell of N_j, preds
-  int32_t c, pair, gas, chunks;    // class, its (tmp, mbs) pair, gas, node chunks
-};
+__device__ __forceinline__ uint32_t block_sum_u32(uint32_t v, uint32_t* sm) {
+  const int l = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (l == 0) sm[w] = v;
+  __syncthreads();
+  uint32_t t = 0;
+  for (int x = 0; x < nw; ++x) t += sm[x];
+  return t;
+}
 
-#ifndef AMP_TRIE_NB
-#define AMP_TRIE_NB 4
-#endif
-constexpr int kTrieNB = AMP_TRIE_NB;  // nodes per thread: they share the cell's work
+__device__ __forceinline__ uint64_t level_entries(const TrieParams& p, int d) {
+  const uint64_t n = (uint64_t)p.st->cnt[d - 1] * (uint64_t)p.U;
+  return n < p.pres_cap ? n : p.pres_cap;
+}
 
-// Stage j: one thread per (class, cell x of N_j, chunk of kTrieNB nodes of
-// depth j-1).  Per cut the predecessor index, t2 and the tolerance term are
-// shared by the thread's nodes; each node adds its parent's value and its
-// own edge (the per-candidate kernels' operations and order).
-#ifndef AMP_TRIE_UNROLL
-#define AMP_TRIE_UNROLL 2
-#endif
-#ifndef AMP_TRIE_MINB
-#define AMP_TRIE_MINB 2
-#endif
-constexpr int kTrieUnroll = AMP_TRIE_UNROLL;
-__global__ void __launch_bounds__(256, AMP_TRIE_MINB) k_trie_stage(TrieParams p, int j, uint64_t total,
-                                                    unsigned long long* exec) {
-  __shared__ TrieSlot slot[kTrieMaxCls];
-  __shared__ uint64_t ibase[kTrieMaxCls + 1];
-  const int nc = p.st_n[j];
-  const int d = j - 1, L = p.L, LP = L + 1;
-  for (int x = threadIdx.x; x <= nc; x += blockDim.x) {
-    ibase[x] = p.st_item[(size_t)j * (p.n_cls + 1) + x];
-    if (x == nc) continue;
-    TrieSlot t;
-    const int c = p.st_cls[(size_t)j * p.n_cls + x];
-    const ClassDev cl = p.cls[c];
-    const ProgDev pg = p.progs[p.class_prog[c]];
-    const uint32_t* rg = p.range + ((size_t)d * p.n_cls + c) * 2;
-    t.ibase = ibase[x];
-    t.c = c;
-    t.pair = cl.pair;
-    t.gas = cl.gas;
-    t.nb = rg[0];
-    t.K = rg[1] - rg[0];
-    t.chunks = (t.K + kTrieNB - 1) / kTrieNB;
-    t.vbase = p.vbase[(size_t)d * p.n_cls + c];
-    t.bbase = p.bbase[(size_t)d * p.n_cls + c];
-    if (j > 2) {
-      const uint32_t* rgp = p.range + ((size_t)(d - 1) * p.n_cls + c) * 2;
-      t.nb_p = rgp[0];
-      t.K_p = rgp[1] - rgp[0];
-      t.vbase_p = p.vbase[(size_t)(d - 1) * p.n_cls + c];
-    } else {
-      t.nb_p = 0;
-      t.K_p = 1;
-      t.vbase_p = 0;
+__global__ void __launch_bounds__(kScanThreads) k_level_up(TrieParams p, int d) {
+  __shared__ uint32_t sm[32];
+  if (p.st->ovf) return;
+  const uint64_t n = level_entries(p, d);
+  const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const uint64_t b = (uint64_t)blockIdx.x * per, e = b + per < n ? b + per : n;
+  uint32_t s = 0;
+  for (uint64_t x = b + threadIdx.x; x < e; x += blockDim.x) s += p.pres[x];
+  s = block_sum_u32(s, sm);
+  if (threadIdx.x == 0) p.partial[blockIdx.x] = s;
+}
+
+// Scan of the child marks -> depth-d nodes; clears the marks it reads; the
+// last CTA plans the level.
+__global__ void __launch_bounds__(kScanThreads) k_level_down(TrieParams p, int d) {
+  __shared__ uint32_t sm[32], wsum[32];
+  __shared__ uint64_t s_off;
+  __shared__ int s_last;
+  const int tid = threadIdx.x, l = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+  const uint64_t n = level_entries(p, d);
+  const uint64_t noff = d == 1 ? 0 : p.st->node_off[d - 1] + p.st->cnt[d - 1];
+  const bool ovf = p.st->ovf || noff + n > p.node_cap;
+  const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const uint64_t b = (uint64_t)blockIdx.x * per, e = b + per < n ? b + per : n;
+  uint32_t base = 0;
+  if (!ovf) {
+    uint32_t s = 0;
+    for (int x = tid; x < (int)blockIdx.x; x += blockDim.x) s += p.partial[x];
+    base = block_sum_u32(s, sm);
+  }
+  const uint64_t poff = d == 1 ? 0 : p.st->node_off[d - 1];
+  for (uint64_t x0 = b; x0 < e; x0 += blockDim.x) {
+    const uint64_t x = x0 + tid;
+    const uint32_t f = x < e ? p.pres[x] : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, f != 0);
+    __syncthreads();
+    if (l == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    uint32_t before = base;
+    for (int q = 0; q < w; ++q) before += wsum[q];
+    before += __popc(bal & ((1u << l) - 1));
+    if (f) {
+      if (!ovf) {
+        const uint32_t id = before;
+        const uint64_t par = x / (uint64_t)p.U;
+        p.npar[noff + id] = (uint32_t)par;
+        p.ncode[noff + id] = (uint8_t)(x % (uint64_t)p.U);
+        p.ncls[noff + id] = (uint16_t)(d == 1 ? p.root_cls[par] : p.ncls[poff + par]);
+        p.cid[x] = id;
+      }
+      p.pres[x] = 0;
     }
-    t.v1off = p.v1off[c];
-    t.cell0 = pg.cell_base + p.stage[pg.stage_base + j - 1];
-    t.pred_base_lo = (uint32_t)pg.pred_base;
-    t.pred_base_hi = (uint32_t)(pg.pred_base >> 32);
-    t.pad = 0;
-    slot[x] = t;
+    for (int q = 0; q < nw; ++q) base += wsum[q];
+  }
+  // last CTA: level total and plan
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(&p.st->ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (tid == 0) p.st->ticket = 0;
+  if (ovf) {
+    if (tid == 0) p.st->ovf = 1;
+    return;
+  }
+  uint32_t s = 0;
+  for (int x = tid; x < (int)gridDim.x; x += blockDim.x) s += __ldcg(p.partial + x);
+  const uint32_t total = block_sum_u32(s, sm);
+  // per class: node range (nodes are class-sorted), tiles, table sizes
+  uint32_t* nb = p.nb + (size_t)d * p.n_cls;
+  uint32_t* nK = p.nK + (size_t)d * p.n_cls;
+  const uint16_t* cl = p.ncls + noff;  // written by the other CTAs: read through L2 (__ldcg)
+  for (int c = tid; c < p.n_cls; c += blockDim.x) {
+    uint32_t lo = 0, hi = total;  // lower_bound(c)
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldcg(cl + mid) < c) lo = mid + 1;
+      else hi = mid;
+    }
+    uint32_t lo2 = lo, hi2 = total;  // upper_bound(c)
+    while (lo2 < hi2) {
+      const uint32_t mid = (lo2 + hi2) >> 1;
+      if (__ldcg(cl + mid) <= c) lo2 = mid + 1;
+      else hi2 = mid;
+    }
+    nb[c] = lo;
+    nK[c] = lo2 - lo;
   }
   __syncthreads();
+  if (tid == 0) {
+    p.st->cnt[d] = total;
+    p.st->node_off[d] = noff;
+    uint32_t* tb = p.tbase + (size_t)d * (p.n_cls + 1);
+    uint64_t* vb = p.vbase + (size_t)d * p.n_cls;
+    uint64_t* bb = p.bbase + (size_t)d * p.n_cls;
+    uint32_t tiles = 0;
+    uint64_t vacc = 0, bacc = p.st->bp_bump;
+    for (int c = 0; c < p.n_cls; ++c) {
+      tb[c] = tiles;
+      vb[c] = vacc;
+      bb[c] = bacc;
+      const uint32_t K = nK[c];
+      if (!K) continue;
+      const TrieStage ts = p.tstage[(size_t)c * (p.max_pp + 1) + d + 1];
+      tiles += (K + ts.tn - 1) / ts.tn;
+      if (d < p.cls[c].pp - 1) vacc += (uint64_t)K * ts.n;  // leaves keep argmins only
+      bacc += (uint64_t)K * ts.n;
+    }
+    tb[p.n_cls] = tiles;
+    p.st->ntiles[d] = tiles;
+    p.st->bp_bump = bacc;
+    if (vacc > p.vcap || bacc > p.bpcap) p.st->ovf = 1;
+  }
+}
+
+__global__ void k_level_assign(TrieParams p, int d) {
+  if (p.st->ovf) return;
+  const uint64_t n = *p.n_sig;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = p.sig_key[i];
+    const int pp = p.cls[trie_cls(p, key)].pp;
+    if (pp - 1 < d) continue;
+    const uint32_t node = p.cid[(uint64_t)p.nid[i] * p.U + trie_code(p, key, d - 1)];
+    p.nid[i] = node;
+    if (pp - 1 >= d + 1) p.pres[(uint64_t)node * p.U + trie_code(p, key, d)] = 1;
+  }
+}
+
+// Stage j = d + 1 over the depth-d nodes, one tile per CTA iteration.
+__global__ void __launch_bounds__(kTrieThreads, 4) k_trie_tiles(TrieParams p, int d) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_c;
+  if (p.st->ovf) return;
+  const int tid = threadIdx.x, nt = blockDim.x, L = p.L, LP = L + 1, j = d + 1;
+  const uint32_t ntiles = p.st->ntiles[d];
+  const uint32_t* tb = p.tbase + (size_t)d * (p.n_cls + 1);
+  const uint64_t noff = p.st->node_off[d], poff = d >= 2 ? p.st->node_off[d - 1] : 0;
+  const double* Vprev = p.varena[(d - 1) & 1];
+  double* Vcur = p.varena[d & 1];
   unsigned long long mine = 0;
-  const double* Vprev = p.vals[(j - 1) & 1];
-  double* Vcur = p.vals[j & 1];
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (uint64_t)gridDim.x * blockDim.x) {
-    int lo = 0, hi = nc - 1;  // class slot: last with ibase <= t
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (ibase[mid] <= t) lo = mid;
-      else hi = mid - 1;
-    }
-    const TrieSlot& S = slot[lo];
-    const uint64_t off = t - S.ibase;
-    const uint32_t x = (uint32_t)(off / (uint32_t)S.chunks);
-    const uint32_t n0 = (uint32_t)(off % (uint32_t)S.chunks) * kTrieNB;  // local node
-    const int nn = (int)min((uint32_t)kTrieNB, S.K - n0);
-    const uint2 rec = p.cellrec[S.cell0 + x];
-    const int i = rec.x >> 16, m = rec.x & 0xffff;
-    const uint16_t* q = p.preds + (((uint64_t)S.pred_base_hi << 32) | S.pred_base_lo) + rec.y;
-    const double* Pf = p.prefix + (size_t)S.pair * LP;
-    const double dm = p.domain[(size_t)S.pair * p.nv_stride + m];
-    const double Pi = Pf[i];
-    const double g1 = (double)(S.gas - 1);
-    const double* Vp[kTrieNB];
-    const double* E[kTrieNB];
-    double best[kTrieNB];
-    int bc[kTrieNB];
-#pragma unroll
-    for (int b = 0; b < kTrieNB; ++b) {
-      const uint32_t node = S.nb + n0 + (b < nn ? b : 0);  // pad with the first node
-      const uint64_t key = p.rep_key[p.first[(size_t)d * p.stride + node]];
-      E[b] = p.qtab + ((size_t)S.c * p.n_codes + key_code(p, key, j - 2)) * L;
-      if (j == 2) {
-        Vp[b] = p.v1g + S.v1off;
-      } else {
-        const uint32_t pn = p.parent[(size_t)d * p.stride + node] - S.nb_p;
-        Vp[b] = Vprev + S.vbase_p + pn;
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if (tid == 0) {
+      int lo = 0, hi = p.n_cls - 1;  // last class with tbase <= t
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tb[mid] <= t) lo = mid;
+        else hi = mid - 1;
       }
-      best[b] = CUDART_INF;
-      bc[b] = -1;
+      s_c = lo;
     }
-    const uint32_t Kp = S.K_p;
-#pragma unroll kTrieUnroll
-    for (int cut = j - 1; cut < i; ++cut) {  // pipeline_dp.cpp:114-131
-      const double t2 = Pi - Pf[cut];
-      const double term = t2 > dm ? g1 * (t2 - dm) : 0.0;
-      const size_t idx = (size_t)q[cut - (j - 1)] * Kp;
+    __syncthreads();
+    const int c = s_c;
+    const ClassDev cl = p.cls[c];
+    const TrieStage ts = p.tstage[(size_t)c * (p.max_pp + 1) + j];
+    const TrieStage tp = p.tstage[(size_t)c * (p.max_pp + 1) + j - 1];
+    const uint32_t nbc = p.nb[(size_t)d * p.n_cls + c], Kc = p.nK[(size_t)d * p.n_cls + c];
+    const uint32_t n0 = nbc + (t - tb[c]) * ts.tn;
+    const uint32_t nn = min(ts.tn, nbc + Kc - n0);
+    const bool leaf = d == cl.pp - 1;
+    // parents (consecutive depth-(d-1) nodes) and their stage-(j-1) tables
+    const uint32_t pfirst = d >= 2 ? p.npar[noff + n0] : 0;
+    const uint32_t plast = d >= 2 ? p.npar[noff + n0 + nn - 1] : 0;
+    const int P = (int)(plast - pfirst) + 1;
+    const int Pst = P | 1;  // odd stride (in doubles): rows start on distinct banks
+    const int Np = (int)tp.n, Nj = (int)ts.n;
+    double* sV = reinterpret_cast<double*>(smem_raw);
+    double* sE = sV + (size_t)Np * Pst;
+    double* sPf = sE + (size_t)p.n_codes * L;
+    if (d >= 2) {
+      const uint32_t pnb = p.nb[(size_t)(d - 1) * p.n_cls + c];
+      const double* src = Vprev + p.vbase[(size_t)(d - 1) * p.n_cls + c] + (uint64_t)(pfirst - pnb) * Np;
+      for (int x = tid; x < P * Np; x += nt) {
+        const int pl = x / Np, xp = x - pl * Np;
+        sV[xp * Pst + pl] = src[x];
+      }
+    } else {
+      const double* src = p.v1g + p.v1off[c];
+      for (int x = tid; x < Np; x += nt) sV[x * Pst] = src[x];
+    }
+    int* sNode = reinterpret_cast<int*>(sPf + LP);  // (code << 16) | parent slot
+    const double* qt = p.qtab + (size_t)c * p.n_codes * L;
+    for (int x = tid; x < p.n_codes * L; x += nt) sE[x] = qt[x];
+    for (int x = tid; x < LP; x += nt) sPf[x] = p.prefix[(size_t)cl.pair * LP + x];
+    for (int x = tid; x < (int)nn; x += nt) {
+      const uint64_t node = noff + n0 + x;
+      sNode[x] = ((int)p.ncode[node] << 16) | (d >= 2 ? (int)(p.npar[node] - pfirst) : 0);
+    }
+    __syncthreads();
+    const double g1 = (double)(cl.gas - 1);
+    const double* dom = p.domain + (size_t)cl.pair * p.nv_stride;
+    const ProgDev pg = p.progs[p.class_prog[c]];
+    const uint16_t* pr = p.preds + pg.pred_base;
+    const int G = (int)((nn + kTrieNB - 1) / kTrieNB);
+    const int items = Nj * G;
+    const uint64_t vb = leaf ? 0 : p.vbase[(size_t)d * p.n_cls + c];
+    uint8_t* bpo = p.bparena + p.bbase[(size_t)d * p.n_cls + c];
+    for (int it = tid; it < items; it += nt) {
+      const int x = it / G, g = it - x * G;
+      const uint2 rec = p.cellrec[ts.cell0 + x];
+      const int i = rec.x >> 16, m = rec.x & 0xffff;
+      const uint16_t* q = pr + rec.y;
+      const double dm = dom[m];
+      const double Pi = sPf[i];
+      int pl[kTrieNB];
+      const double* E[kTrieNB];
+      double best[kTrieNB];
+      int bc[kTrieNB];
 #pragma unroll
       for (int b = 0; b < kTrieNB; ++b) {
-        const double g = ((Vp[b][idx] + term) + t2) + E[b][cut];
-        if (g < best[b]) {
-          best[b] = g;
-          bc[b] = cut;
+        const int ln = g * kTrieNB + b < (int)nn ? g * kTrieNB + b : g * kTrieNB;  // pad: repeat
+        const int nd = sNode[ln];
+        pl[b] = nd & 0xffff;
+        E[b] = sE + (nd >> 16) * L;
+        best[b] = CUDART_INF;
+        bc[b] = -1;
+      }
+#pragma unroll 2
+      for (int cut = j - 1; cut < i; ++cut) {  // pipeline_dp.cpp:114-131
+        const double t2 = Pi - sPf[cut];
+        const double term = t2 > dm ? g1 * (t2 - dm) : 0.0;
+        const double* row = sV + (int)q[cut - (j - 1)] * Pst;
+#pragma unroll
+        for (int b = 0; b < kTrieNB; ++b) {
+          const double gv = ((row[pl[b]] + term) + t2) + E[b][cut];
+          if (gv < best[b]) {
+            best[b] = gv;
+            bc[b] = cut;
+          }
         }
       }
-    }
 #pragma unroll
-    for (int b = 0; b < kTrieNB; ++b) {
-      if (b >= nn) break;
-      const uint64_t o = (uint64_t)x * S.K + n0 + b;
-      Vcur[S.vbase + o] = best[b];
-      p.bp[S.bbase + o] = (uint8_t)bc[b];
+      for (int b = 0; b < kTrieNB; ++b) {
+        const int ln = g * kTrieNB + b;
+        if (ln >= (int)nn) break;
+        const uint64_t o = (uint64_t)(n0 - nbc + ln) * Nj + x;
+        if (!leaf) Vcur[vb + o] = best[b];
+        bpo[o] = (uint8_t)bc[b];
+      }
     }
-    mine += (unsigned long long)(i - (j - 1)) * nn;
+    mine += (unsigned long long)nn * ts.iters;
+    __syncthreads();  // smem reuse by the next tile
   }
-  if (exec) {  // executed inner iterations (roofline accounting): one
-               // global atomic per warp (a 64-bit smem atomicAdd is a CAS loop)
-    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(exec, mine);
-  }
+  if (p.exec && tid == 0 && mine) atomicAdd(&p.exec[1], mine);
 }
 
 // One thread per signature: backtrack (pipeline_dp.cpp:134-148) along its
-// trie path and write the cuts of its representative item.
+// trie path and write its cuts.
 __global__ void k_trie_back(TrieParams p) {
-  const uint64_t n = *p.n_rep;
+  if (p.st->ovf) return;
+  const uint64_t n = *p.n_sig;
   const int L = p.L;
-  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
-       r += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t key = p.rep_key[r];
-    if (key == ~0ull) continue;  // failed / pp <= 2 items (K_est)
-    const int c = key_cls(p, key);
-    const ClassDev cl = p.cls[c];
-    const int k = cl.pp;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = p.sig_key[i];
+    const int c = trie_cls(p, key);
+    const int k = p.cls[c].pp;
     const ProgDev pg = p.progs[p.class_prog[c]];
-    const uint32_t* ss = p.stage + pg.stage_base;
-    uint8_t* co = p.repcuts + r * (p.max_pp + 1);  // compact, by signature run
+    const uint16_t* pr = p.preds + pg.pred_base;
+    uint8_t* co = p.repcuts + i * (p.max_pp + 1);
     co[k] = (uint8_t)L;
-    uint32_t x = ss[k - 1];  // N_k = {(L, 0)}
+    uint32_t node = p.nid[i];  // leaf (depth k-1, local id)
+    uint32_t x = 0;            // N_k = {(L, 0)}
     for (int j = k; j >= 2; --j) {
       const int d = j - 1;
-      const uint32_t* rg = p.range + ((size_t)d * p.n_cls + c) * 2;
-      const uint32_t node = p.nid[(size_t)d * p.stride + r] - 1;
-      const uint64_t o = (uint64_t)(x - ss[j - 1]) * (rg[1] - rg[0]) + (node - rg[0]);
-      const int cut = p.bp[p.bbase[(size_t)d * p.n_cls + c] + o];
+      const TrieStage ts = p.tstage[(size_t)c * (p.max_pp + 1) + j];
+      const uint32_t nbc = p.nb[(size_t)d * p.n_cls + c];
+      const int cut = p.bparena[p.bbase[(size_t)d * p.n_cls + c] + (uint64_t)(node - nbc) * ts.n + x];
       co[j - 1] = (uint8_t)cut;
-      const uint2 rec = p.cellrec[pg.cell_base + x];
-      x = ss[j - 2] + p.preds[pg.pred_base + rec.y + (cut - (j - 1))];
+      const uint2 rec = p.cellrec[ts.cell0 + x];
+      x = pr[rec.y + (cut - (j - 1))];
+      if (d >= 2) node = p.npar[p.st->node_off[d] + node];
     }
     co[0] = 0;
   }
+  if (p.exec && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&p.exec[0], (unsigned long long)n);  // one DP instance per signature
 }
 
 // Stage-1 values of every heavy class (pipeline_dp.cpp:102-107), once per

@@ -519,26 +519,57 @@ def test_run_pipe_with_parameter_ceiling_matches_oracle(ceiling, monkeypatch):
         assert (orec["fail_code"] == 3).any() and ok.any()  # AMP_FAIL_CEILING, some pass
 
 
-@pytest.mark.parametrize("min_log2", ["10", "12"])
-def test_small_hash_table_overflow_redo(min_log2, monkeypatch):
-    """The signature table sized from the previous chunk (here forced tiny,
-    AMP_HASH_MIN_LOG2) overflows on a sweep with thousands of signatures:
-    the chunk's inserts are redone with the full-size table (K_place again)
-    and records / top-k equal the default run, also across chunks."""
+SWITCHES = [
+    ("AMP_NO_TRIE", "1"),          # signature-mode K_dp (k_dp_multi over the keys)
+    ("AMP_TRIE_VCAP", "20000"),    # trie capacity exceeded on the device -> same fallback
+    ("AMP_NO_FUSE", "1"),          # K_place places the pp <= 2 tail too
+    ("AMP_NO_FUSE_HASH", "1"),     # separate k_hash_insert launch
+    ("AMP_NO_RUN_SLOT", "1"),      # k_hash_scatter + rep_of lookup in K_est
+    ("AMP_KEEP_WORK", "1"),        # K_place writes work records, K_est reads them
+]
+
+
+@pytest.mark.parametrize("var,val", SWITCHES)
+def test_switch_paths_equal_default(var, val, monkeypatch):
+    """Every comparison switch of the engine gives records and
+    a top-k identical to the default path, across chunks (AMP_CHUNK), and the
+    records equal the memoised oracle."""
     sc = scenario("hetero_cluster")
     enc = P.EncodedProblem.from_scenario(sc)
     outs = []
-    for env in (None, min_log2):
+    monkeypatch.setenv("AMP_CHUNK", "1000000")
+    for env in (None, val):
         if env:
-            monkeypatch.setenv("AMP_HASH_MIN_LOG2", env)
-            monkeypatch.setenv("AMP_CHUNK", "1000000")
+            monkeypatch.setenv(var, env)
         else:
-            monkeypatch.delenv("AMP_HASH_MIN_LOG2", raising=False)
-            monkeypatch.delenv("AMP_CHUNK", raising=False)
-        with planner.Searcher(enc, placements_per_class=40000, seed=6) as s:
+            monkeypatch.delenv(var, raising=False)
+        with planner.Searcher(enc, placements_per_class=30000, seed=6) as s:
             top, allr, _ = s.run(0, s.num_candidates, k=16, want_all=True, details=False)
             st = s.stats()
         outs.append((top, allr, st))
-    assert outs[0][2]["dp_instances"] > 2 ** int(min_log2)  # more signatures than slots
+    monkeypatch.delenv(var, raising=False)
     assert np.array_equal(outs[0][1].view(np.uint8), outs[1][1].view(np.uint8))
     assert np.array_equal(outs[0][0].view(np.uint8), outs[1][0].view(np.uint8))
+    assert outs[0][2]["dp_fallback"] == 0
+    if var == "AMP_TRIE_VCAP":
+        assert outs[1][2]["dp_fallback"] > 0
+    o = B.Oracle(enc, 30000, 6)
+    orec, _ = o.run(threads=8, details=False, memo=True)
+    allr = outs[0][1]
+    assert np.array_equal(allr["fail_code"], orec["fail_code"])
+    ok = orec["fail_code"] == 0
+    assert np.array_equal(allr["total"][ok], orec["total"][ok])
+
+
+def test_trie_dp_stage_timing_and_counts():
+    """The bench's roofline inputs: the trie path reports its executed inner
+    iterations and the CUDA-event time of its stage kernels, and no chunk
+    falls back."""
+    sc = scenario("hetero_cluster")
+    enc = P.EncodedProblem.from_scenario(sc)
+    with planner.Searcher(enc, placements_per_class=200000, seed=0) as s:
+        s.run(0, s.num_candidates, k=10)
+        st = s.stats()
+    assert st["dp_fallback"] == 0
+    assert st["dp_stage_launches"] >= 14 and st["dp_stage_ms"] > 0
+    assert st["dp_inner"] > 0 and st["fp64_ops"] == 7 * st["dp_inner"]
