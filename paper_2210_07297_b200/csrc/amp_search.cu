@@ -173,14 +173,17 @@ struct amp_ctx {
   // DP shared across signature prefixes (amp_trie.cuh)
   bool trie = false;
   int trie_nq = 0, trie_U = 0;
+  int tr_smem = 0;  // K_trie_dp dynamic smem per CTA
+  int tr_build_grid = 0, tr_dp_grid = 0;
   std::vector<uint32_t> stage_h;  // host copy of the program stage starts
   std::vector<uint64_t> prog_stage_inner;  // [prog][L+1] unpadded (cell, cut) pairs of stage j
   std::vector<int32_t> root_cls_h;         // heavy classes (trie roots) in class order
   DevBuf v1off_d, v1g_d, dd_rep_key, dd_nid, tr_state, tr_pres, tr_cid, tr_partial, tr_npar,
-      tr_ncls, tr_ncode, tr_nb, tr_nK, tr_vbase, tr_bbase, tr_tbase, tr_tstage, tr_v0, tr_v1, tr_bp,
+      tr_ncls, tr_ncode, tr_nb, tr_nK, tr_vbase, tr_bbase, tr_rbase, tr_tbase, tr_nxc, tr_tstage, tr_v0, tr_bp,
+      tr_done, tr_tiles,
       tr_rank, tr_rcls;
   uint64_t tr_pres_cap = 0, tr_node_cap = 0, tr_vcap = 0, tr_bpcap = 0;
-  std::vector<cudaEvent_t> tev;  // {before, after} every K_trie_tiles launch of the last run
+  std::vector<cudaEvent_t> tev;  // {before, after} every K_trie_dp launch of the last run
   int tev_used = 0;
   DevBuf ovf_log;                // trie capacity flag of every chunk of the last run
   int ovf_used = 0;
@@ -799,13 +802,12 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   ctx->trie = ctx->dedup && (1 << ctx->code_bits) <= 16 && std::getenv("AMP_NO_TRIE") == nullptr;
   if (ctx->trie) {
     const int NC = (int)ctx->classes.size(), P1 = ctx->max_pp + 1;
-    const size_t budget = kTrieSmem / sizeof(double);
-    std::vector<TrieStage> ts((size_t)NC * P1, TrieStage{0, 0, 0, 1});
+    std::vector<TrieStage> ts((size_t)NC * P1, TrieStage{0, 0, 0, 1, 0});
     std::vector<int32_t> rank(NC, -1), heavy;
     std::vector<uint64_t> v1off(NC, 0);
     uint64_t acc = 0;
     int nq = 1;
-    for (int c = 0; c < NC && ctx->trie; ++c) {
+    for (int c = 0; c < NC; ++c) {
       if (!is_heavy(ctx, c)) continue;
       const int g = ctx->class_prog[c];
       const ProgDev& pg = ctx->progs_h[g];
@@ -820,21 +822,32 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
         t.cell0 = pg.cell_base + sh[j - 1];
         t.n = sh[j] - sh[j - 1];
         t.iters = (uint32_t)ctx->prog_stage_inner[(size_t)g * LP + j];
-        if (j == 1) continue;
-        // tile nodes: parents' tables + edge rows + prefix + node words in
-        // the smem budget; >= 2 (cell, node group) items per thread
-        const double np = ts[(size_t)c * P1 + j - 1].n;
-        const double fixed = (double)ctx->n_codes * L + LP + np;
-        const double per = j == 2 ? 0.5 : np + 0.5;
-        const double room = (double)budget - fixed;
-        int tn = room <= per ? 0 : (int)std::floor(room / per);
-        const int want = kTrieNB * (int)std::ceil(2.0 * kTrieThreads / std::max(1u, t.n));
-        tn = std::min({tn, std::max(kTrieNB, want), 4096});
-        if (tn >= kTrieNB) tn -= tn % kTrieNB;
-        if (tn < 1) ctx->trie = false;  // a parent table does not fit: signature-mode K_dp
-        t.tn = (uint32_t)std::max(tn, 1);
       }
     }
+    // tile shapes (K_trie_dp, one smem budget for all stages): wide stages
+    // (>= 32 cells) take groups of 4 nodes with per-node smem columns when
+    // one group fits kTrieSmem, else a node per thread over the parents'
+    // tables; the budget grows (fewer CTAs / SM) only if a one-node tile
+    // does not fit.  Each class then takes as many nodes as fit (wide: up to
+    // 4 groups; narrow: ~2 items per thread).
+    size_t B = kTrieSmem;
+    for (int c : heavy)
+      for (int j = 2; j <= ctx->classes[c].pp; ++j) {
+        TrieStage& t = ts[(size_t)c * P1 + j];
+        const int Np = (int)ts[(size_t)c * P1 + j - 1].n;
+        t.wide = t.n >= 32 && sizeof(double) * trie_tile_doubles(true, j, 1, Np, L, ctx->n_codes) <= kTrieSmem;
+        B = std::max(B, sizeof(double) * trie_tile_doubles(t.wide, j, 1, Np, L, ctx->n_codes));
+      }
+    if (B > 227 * 1024 || (int)ctx->classes.size() > kTrieMaxCls) ctx->trie = false;
+    ctx->tr_smem = (int)B;
+    for (int c : heavy)
+      for (int j = 2; j <= ctx->classes[c].pp; ++j) {
+        TrieStage& t = ts[(size_t)c * P1 + j];
+        const int Np = (int)ts[(size_t)c * P1 + j - 1].n;
+        int n = t.wide ? 4 : std::min(4096, std::max(1, (2 * kTrieThreads + (int)t.n - 1) / (int)t.n));
+        while (n > 1 && sizeof(double) * trie_tile_doubles(t.wide, j, n, Np, L, ctx->n_codes) > B) --n;
+        t.tn = (uint32_t)(t.wide ? kTrieNB * n : n);
+      }
     if (ctx->trie && heavy.empty()) ctx->trie = false;
     if (ctx->trie) {
       ctx->trie_nq = nq;
@@ -844,12 +857,13 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
       CK(upload(ctx->tr_rank, rank.data(), rank.size()));
       CK(upload(ctx->tr_rcls, heavy.data(), heavy.size()));
       CK(ctx->tr_state.ensure(sizeof(TrieState)));
-      CK(ctx->tr_partial.ensure(sizeof(uint32_t) * kScanGrid));
       CK(ctx->tr_nb.ensure(sizeof(uint32_t) * kTrieMaxD1 * NC));
       CK(ctx->tr_nK.ensure(sizeof(uint32_t) * kTrieMaxD1 * NC));
       CK(ctx->tr_vbase.ensure(sizeof(uint64_t) * kTrieMaxD1 * NC));
       CK(ctx->tr_bbase.ensure(sizeof(uint64_t) * kTrieMaxD1 * NC));
+      CK(ctx->tr_rbase.ensure(sizeof(uint64_t) * kTrieMaxD1 * NC));
       CK(ctx->tr_tbase.ensure(sizeof(uint32_t) * kTrieMaxD1 * (NC + 1)));
+      CK(ctx->tr_nxc.ensure(sizeof(uint32_t) * kTrieMaxD1 * NC));
       CK(upload(ctx->v1off_d, v1off.data(), v1off.size()));
       CK(ctx->v1g_d.ensure(sizeof(double) * (acc + 1)));
       DevBuf d_heavy;
@@ -860,7 +874,16 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
           ctx->domain.as<double>(), ctx->nv_stride, L, d_heavy.as<int32_t>(), (int)heavy.size(),
           ctx->v1off_d.as<uint64_t>(), ctx->v1g_d.as<double>());
       CK(cudaGetLastError());
-      CK(cudaFuncSetAttribute(k_trie_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrieSmem));
+      CK(cudaFuncSetAttribute(k_trie_dp, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->tr_smem));
+      const int bsm = (int)(4 * sizeof(unsigned long long) * NC);
+      CK(cudaFuncSetAttribute(k_trie_build, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm));
+      int ob = 0, od = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k_trie_build, kBuildThreads, bsm));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&od, k_trie_dp, kTrieThreads, ctx->tr_smem));
+      if (ob < 1 || od < 1) return fail(ctx, AMP_E_UNSUPPORTED, "trie kernels do not fit on an SM");
+      ctx->tr_build_grid = std::min(ob, 2) * prop.multiProcessorCount;
+      ctx->tr_dp_grid = od * prop.multiProcessorCount;
+      CK(ctx->tr_partial.ensure(sizeof(uint32_t) * ctx->tr_build_grid));
       CK(cudaStreamSynchronize(ctx->stream));
     }
   }
@@ -1053,17 +1076,17 @@ int run_sig_dp(amp_ctx* ctx, EvalParams& ep, const HashParams& hp) {
   if (ctx->trie) {
     // capacities of the device-side trie (exceeding one raises ovf and the
     // signature-mode K_dp solves the chunk): nodes per level <= signatures
-    // <= heavy items, and <= roots * U^d
+    // <= heavy items, and <= roots * U^d; parents of depth 1 are the roots
     const uint64_t U = tp.U;
-    uint64_t node_b = 0, lvl_b = (uint64_t)tp.n_roots, w = (uint64_t)tp.n_roots;  // parents of depth 1: the roots
+    uint64_t node_b = 0, lvl_b = (uint64_t)tp.n_roots, w = (uint64_t)tp.n_roots;
     for (int d = 1; d <= ctx->trie_nq; ++d) {
       w = std::min<uint64_t>(w * U, C);
       node_b += w;
       lvl_b = std::max(lvl_b, w);
     }
-    const uint64_t node_cap = std::min<uint64_t>(node_b, 16ull << 20);
-    const uint64_t pres_cap = std::min<uint64_t>(lvl_b, 16ull << 20) * U;
-    if (ctx->tr_pres.bytes < pres_cap) {  // marks must start clear (then kept clear)
+    const uint64_t node_cap = std::min<uint64_t>(node_b, 32ull << 20);
+    const uint64_t pres_cap = std::min<uint64_t>(lvl_b, 32ull << 20) * U;
+    if (ctx->tr_pres.bytes < pres_cap) {  // marks start clear (and are kept clear)
       CK(ctx->tr_pres.ensure(pres_cap));
       CK(cudaMemsetAsync(ctx->tr_pres.p, 0, pres_cap, ctx->stream));
     }
@@ -1071,13 +1094,15 @@ int run_sig_dp(amp_ctx* ctx, EvalParams& ep, const HashParams& hp) {
     CK(ctx->tr_npar.ensure(sizeof(uint32_t) * node_cap));
     CK(ctx->tr_ncls.ensure(sizeof(uint16_t) * node_cap));
     CK(ctx->tr_ncode.ensure(node_cap));
-    // value arenas: one level each (64 M doubles; AMP_TRIE_VCAP shrinks them
-    // to exercise the capacity fallback in the tests)
+    // value tables of every depth (256 M doubles; AMP_TRIE_VCAP shrinks them
+    // to exercise the capacity fallback in the tests), argmins, run counters
     const char* vc = std::getenv("AMP_TRIE_VCAP");
-    const uint64_t vcap = vc ? std::strtoull(vc, nullptr, 10) : (64ull << 20), bpcap = 512ull << 20;
-    CK(ctx->tr_v0.ensure(sizeof(double) * vcap));
-    CK(ctx->tr_v1.ensure(sizeof(double) * vcap));
+    const uint64_t vcap = vc ? std::strtoull(vc, nullptr, 10) : (256ull << 20), bpcap = 1ull << 30;
+    const uint64_t run_cap = node_cap, tile_cap = node_cap + (4ull << 20);
+    CK(ctx->tr_v0.ensure(sizeof(double) * std::max<uint64_t>(vcap, 1)));
     CK(ctx->tr_bp.ensure(bpcap));
+    CK(ctx->tr_done.ensure(sizeof(uint32_t) * run_cap));
+    CK(ctx->tr_tiles.ensure(sizeof(TrieTile) * tile_cap));
     CK(ctx->dd_nid.ensure(sizeof(uint32_t) * C));
     tp.nid = ctx->dd_nid.as<uint32_t>();
     tp.root_rank = ctx->tr_rank.as<int32_t>();
@@ -1093,15 +1118,20 @@ int run_sig_dp(amp_ctx* ctx, EvalParams& ep, const HashParams& hp) {
     tp.node_cap = node_cap;
     tp.nb = ctx->tr_nb.as<uint32_t>();
     tp.nK = ctx->tr_nK.as<uint32_t>();
+    tp.nxc = ctx->tr_nxc.as<uint32_t>();
+    tp.tbase = ctx->tr_tbase.as<uint32_t>();
     tp.vbase = ctx->tr_vbase.as<uint64_t>();
     tp.bbase = ctx->tr_bbase.as<uint64_t>();
-    tp.tbase = ctx->tr_tbase.as<uint32_t>();
+    tp.rbase = ctx->tr_rbase.as<uint64_t>();
     tp.tstage = ctx->tr_tstage.as<TrieStage>();
-    tp.varena[0] = ctx->tr_v0.as<double>();
-    tp.varena[1] = ctx->tr_v1.as<double>();
+    tp.varena = ctx->tr_v0.as<double>();
     tp.vcap = vcap;
     tp.bparena = ctx->tr_bp.as<uint8_t>();
     tp.bpcap = bpcap;
+    tp.done = ctx->tr_done.as<uint32_t>();
+    tp.run_cap = run_cap;
+    tp.tiles = ctx->tr_tiles.as<TrieTile>();
+    tp.tile_cap = tile_cap;
     tp.cellrec = ctx->cellrec.as<uint2>();
     tp.preds = ctx->preds.as<uint16_t>();
     tp.progs = ctx->progs_d.as<ProgDev>();
@@ -1113,36 +1143,27 @@ int run_sig_dp(amp_ctx* ctx, EvalParams& ep, const HashParams& hp) {
     tp.qtab = ctx->qtab.as<double>();
     tp.v1g = ctx->v1g_d.as<double>();
     tp.v1off = ctx->v1off_d.as<uint64_t>();
-  }
-  k_sig_init<<<g, 256, 0, ctx->stream>>>(tp);
-  DBG_SYNC("k_sig_init");
-  CK(cudaGetLastError());
-  ctx->launches += 1;
-  if (ctx->trie) {
-    const int tg = ctx->sms * 4;
-    for (int d = 1; d <= ctx->trie_nq; ++d) {
-      k_level_up<<<kScanGrid, kScanThreads, 0, ctx->stream>>>(tp, d);
-      DBG_SYNC("k_level_up");
-      k_level_down<<<kScanGrid, kScanThreads, 0, ctx->stream>>>(tp, d);
-      DBG_SYNC("k_level_down");
-      k_level_assign<<<g, 256, 0, ctx->stream>>>(tp, d);
-      DBG_SYNC("k_level_assign");
-      while ((int)ctx->tev.size() < ctx->tev_used + 2) {
-        cudaEvent_t e;
-        CK(cudaEventCreate(&e));
-        ctx->tev.push_back(e);
-      }
-      CK(cudaEventRecord(ctx->tev[ctx->tev_used++], ctx->stream));
-      k_trie_tiles<<<tg, kTrieThreads, kTrieSmem, ctx->stream>>>(tp, d);
-      DBG_SYNC("k_trie_tiles");
-      CK(cudaEventRecord(ctx->tev[ctx->tev_used++], ctx->stream));
-      CK(cudaGetLastError());
-      ctx->launches += 4;
+    CK(cudaMemsetAsync(ctx->tr_state.p, 0, sizeof(TrieState), ctx->stream));
+    CK(cudaMemsetAsync(ctx->tr_nb.p, 0, sizeof(uint32_t) * kTrieMaxD1 * NC, ctx->stream));
+    CK(cudaMemsetAsync(ctx->tr_nK.p, 0, sizeof(uint32_t) * kTrieMaxD1 * NC, ctx->stream));
+    void* args[] = {&tp};
+    CK(cudaLaunchCooperativeKernel((const void*)k_trie_build, dim3(ctx->tr_build_grid), dim3(kBuildThreads),
+                                   args, 4 * sizeof(unsigned long long) * NC, ctx->stream));
+    DBG_SYNC("k_trie_build");
+    while ((int)ctx->tev.size() < ctx->tev_used + 2) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      ctx->tev.push_back(e);
     }
-    k_trie_back<<<g, 256, 0, ctx->stream>>>(tp);
-    DBG_SYNC("k_trie_back");
+    CK(cudaEventRecord(ctx->tev[ctx->tev_used++], ctx->stream));
+    k_trie_dp<<<ctx->tr_dp_grid, kTrieThreads, ctx->tr_smem, ctx->stream>>>(tp);
+    CK(cudaEventRecord(ctx->tev[ctx->tev_used++], ctx->stream));
     CK(cudaGetLastError());
-    ctx->launches += 1;
+    DBG_SYNC("k_trie_dp");
+    k_trie_back<<<g, 256, 0, ctx->stream>>>(tp);
+    CK(cudaGetLastError());
+    DBG_SYNC("k_trie_back");
+    ctx->launches += 3;
     if ((size_t)(ctx->ovf_used + 1) * sizeof(uint32_t) > ctx->ovf_log.bytes) {
       // (grows between runs only: a run's chunk count is bounded by the first)
       CK(ctx->ovf_log.ensure(sizeof(uint32_t) * std::max(64, 2 * (ctx->ovf_used + 1))));
@@ -1151,6 +1172,11 @@ int run_sig_dp(amp_ctx* ctx, EvalParams& ep, const HashParams& hp) {
                        reinterpret_cast<const char*>(tp.st) + offsetof(TrieState, ovf), sizeof(uint32_t),
                        cudaMemcpyDeviceToDevice, ctx->stream));
     ++ctx->ovf_used;
+  } else {
+    k_sig_list<<<g, 256, 0, ctx->stream>>>(tp);
+    CK(cudaGetLastError());
+    DBG_SYNC("k_sig_list");
+    ctx->launches += 1;
   }
   // signature-mode K_dp: the whole DP when the trie is off; with the trie
   // only if its capacity was exceeded on the device (it exits otherwise)

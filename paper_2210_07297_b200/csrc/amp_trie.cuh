@@ -9,32 +9,28 @@
 // instead of once per signature.  Per cell and cut the operations are those
 // of pipeline_dp.cpp:118-127 (same operands, same order, same strict '<'),
 // so every cut is bit-identical to the reference (tested against the
-// one-DP-per-candidate kernel).
+// one-DP-per-candidate kernel and the oracle).
 //
-// Everything is built and scheduled on the device — no host round trip:
-//   K_sig_init     the hash table's distinct keys -> signature list (hash
-//                  order), slot -> signature map, root of each signature,
-//                  depth-1 child marks
-//   per depth d = 1 .. nq:
-//     K_level_up   per-CTA sums of the child marks          (fixed grid)
-//     K_level_down exclusive scan -> depth-d node ids in (parent, code)
-//                  order: lexicographic, class-contiguous, children of a
-//                  parent adjacent.  The last CTA plans the level: per
-//                  class node range, tiles, value / argmin table bases
-//                  (device bump allocation; capacity overflow raises `ovf`
-//                  and the signature-mode K_dp (amp_dp_multi.cuh) solves the
-//                  chunk instead)
-//     K_level_assign each signature's depth-d node; marks for depth d+1
-//     K_trie_tiles   stage j = d+1.  One CTA per tile = (class, run of <= TN
-//                  consecutive depth-d nodes).  The tile's parents are
-//                  consecutive depth-(d-1) nodes; their stage-(j-1) tables
-//                  are staged in shared memory (transposed, odd stride: the
-//                  lanes of a warp read distinct banks), with the class's
-//                  edge rows and prefix sums.  Thread = (cell of N_j, group
-//                  of 4 nodes): per cut the predecessor index, t2 and the
-//                  tolerance term are shared by the 4 nodes.
-//   K_trie_back    one thread per signature: backtrack (pipeline_dp.cpp:
-//                  134-148) along its trie path, write its cuts.
+// Three kernels per chunk, every count on the device (no host round trip):
+//   K_trie_build (cooperative, grid barriers between phases)
+//     - signature list: the hash table's distinct keys (hash order), slot ->
+//       signature map, the root (class) of each signature, depth-1 marks
+//     - per depth d = 1 .. nq: scan of the child marks -> depth-d node ids in
+//       (parent, code) order: lexicographic, class-contiguous, the children
+//       of a parent adjacent; each signature's depth-d node and its
+//       depth-(d+1) mark; CTA 0 plans the level: per class the node range,
+//       the tiles, the value / argmin table bases (device bump allocation;
+//       exceeding a capacity raises `ovf` and the signature-mode K_dp,
+//       amp_dp_multi.cuh, solves the chunk instead)
+//     - the tile list of all depths
+//   K_trie_dp (persistent, dataflow): CTAs take tiles in depth order from an
+//     atomic counter.  A tile = (class, run of tn consecutive depth-d nodes,
+//     chunk of the cells of N_{d+1}); it waits until the runs holding its
+//     parents are done, stages their stage-d tables and the edge rows in
+//     shared memory, solves its items, publishes its run.  The upper levels
+//     (few nodes, latency-bound) thereby overlap the wide middle levels.
+//   K_trie_back: one thread per signature backtracks (pipeline_dp.cpp:
+//     134-148) along its trie path and writes its cuts.
 #pragma once
 
 #include "amp_common.cuh"
@@ -42,29 +38,40 @@
 
 namespace amp {
 
-constexpr int kTrieMaxD1 = 64;       // depths 0 .. nq (keys are <= 63 bits, >= 1 bit per code)
-constexpr int kTrieThreads = 256;    // K_trie_tiles block
-constexpr int kTrieNB = 4;           // nodes per thread (share the cell's work)
-constexpr int kScanGrid = 296;       // CTAs of the level scans
-constexpr int kScanThreads = 512;
-constexpr int kTrieSmem = 46 * 1024; // K_trie_tiles dynamic smem budget (4 CTAs / SM)
+constexpr int kTrieMaxD1 = 64;        // depths 0 .. nq (keys are <= 63 bits, >= 1 bit per code)
+constexpr int kTrieMaxCls = 1024;     // classes of a trie context (plan arrays in smem)
+constexpr int kTrieThreads = 256;     // K_trie_dp block
+constexpr int kTrieNB = 4;            // nodes per thread in wide stages (share the cell's work)
+constexpr int kTrieSmem = 46 * 1024;  // K_trie_dp smem per CTA (4 CTAs / SM)
+constexpr int kBuildThreads = 512;    // K_trie_build block
 
-// Level state, in device memory (reset by K_sig_init every chunk).
+// Level state, in device memory (zeroed by the host before K_trie_build).
 struct TrieState {
-  uint32_t cnt[kTrieMaxD1];        // nodes per depth (depth 0: the heavy classes)
-  uint64_t node_off[kTrieMaxD1];   // start of depth d's nodes in the node arrays
-  uint32_t ntiles[kTrieMaxD1];     // tiles of stage d+1
-  unsigned long long bp_bump;      // argmin bytes allocated
-  uint32_t ovf;                    // capacity exceeded: signature-mode K_dp instead
-  uint32_t ticket;                 // last-CTA election of K_level_down
+  uint32_t cnt[kTrieMaxD1];         // nodes per depth (depth 0: the heavy classes)
+  uint64_t node_off[kTrieMaxD1];    // start of depth d's nodes in the node arrays
+  uint32_t tile_off[kTrieMaxD1 + 1];  // first tile of depth d; [nq + 1]: all tiles
+  unsigned long long v_bump, bp_bump, run_bump, tile_bump;
+  uint32_t ovf;                     // capacity exceeded: signature-mode K_dp instead
+  uint32_t next_tile;               // K_trie_dp dispenser
+  uint32_t bar_count, bar_gen;      // K_trie_build grid barrier
 };
 
-// Per (class, stage j) facts of the class's pruned program (host-built).
+// Per (class, stage j) facts of the class's pruned program and its tile
+// shape (host-built).
 struct TrieStage {
   uint32_t cell0;   // first cell of N_j in cellrec (absolute)
   uint32_t n;       // |N_j|
   uint32_t iters;   // (cell, cut) pairs of stage j (unpadded)
-  uint32_t tn;      // nodes per K_trie_tiles tile
+  uint32_t tn;      // nodes per tile
+  uint32_t wide;    // 1: groups of 4 nodes, per-node smem columns; 0: node per thread
+};
+
+struct TrieTile {   // one K_trie_dp work item
+  uint32_t n0;      // first node (local id at depth d)
+  uint32_t run;     // node run within (d, c)
+  uint16_t c;       // class
+  uint8_t d, pad;
+  uint16_t nn, x0, x1, pad2;  // nodes, cell range [x0, x1) of N_{d+1}
 };
 
 struct TrieParams {
@@ -81,25 +88,31 @@ struct TrieParams {
   const int32_t* root_rank;         // [n_cls] rank among the roots (-1: not heavy)
   const int32_t* root_cls;          // [n_roots] class of each root
   TrieState* st;
-  uint8_t* pres;                    // child marks [cnt[d-1] * U]
+  uint8_t* pres;                    // child marks [cnt[d-1] * U] (kept clear between uses)
   uint32_t* cid;                    // their scan: child node id
   uint64_t pres_cap;
-  uint32_t* partial;                // [kScanGrid]
+  uint32_t* partial;                // [gridDim of K_trie_build]
   uint32_t* npar;                   // node arrays (absolute index node_off[d] + id)
   uint16_t* ncls;
   uint8_t* ncode;
   uint64_t node_cap;
-  // level plans [kTrieMaxD1][n_cls] (tbase: [kTrieMaxD1][n_cls + 1])
-  uint32_t* nb;
-  uint32_t* nK;
-  uint64_t* vbase;
-  uint64_t* bbase;
-  uint32_t* tbase;
+  // level plans [kTrieMaxD1][n_cls]
+  uint32_t* nb;                     // first node of the class at depth d
+  uint32_t* nK;                     // its node count
+  uint32_t* nxc;                    // cell chunks per node run
+  uint32_t* tbase;                  // [kTrieMaxD1][n_cls + 1] first tile (within the depth)
+  uint64_t* vbase;                  // value table base (doubles, in varena)
+  uint64_t* bbase;                  // argmin table base (bytes, in bparena)
+  uint64_t* rbase;                  // first run counter
   const TrieStage* tstage;          // [n_cls][max_pp + 1]
-  double* varena[2];                // values of depth d in varena[d & 1]
-  uint64_t vcap;                    // doubles per arena
-  uint8_t* bparena;                 // argmins of every depth
+  double* varena;
+  uint64_t vcap;
+  uint8_t* bparena;
   uint64_t bpcap;
+  uint32_t* done;                   // per node run: finished cell chunks
+  uint64_t run_cap;
+  TrieTile* tiles;
+  uint64_t tile_cap;
   // problem tables
   const ClassDev* cls;
   const uint2* cellrec;
@@ -121,31 +134,28 @@ __device__ __forceinline__ int trie_code(const TrieParams& p, uint64_t k, int q)
   return (int)((k >> ((p.nq - 1 - q) * p.cb)) & (uint64_t)(p.U - 1));
 }
 
-// signature list, slot -> signature, roots, depth-1 marks; resets the state
-__global__ void k_sig_init(TrieParams p) {
-  const uint64_t n = *p.n_sig;
-  if (p.st && blockIdx.x == 0 && threadIdx.x == 0) {  // (no state: trie off)
-    p.st->cnt[0] = (uint32_t)p.n_roots;
-    p.st->node_off[0] = 0;
-    p.st->bp_bump = 0;
-    p.st->ovf = 0;
-    p.st->ticket = 0;
-  }
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t s = p.uniq[i];
-    const unsigned long long k = p.tkey[s];
-    const uint64_t key = p.key_shift >= 64 ? k : (k & ((1ull << p.key_shift) - 1));
-    p.sig_key[i] = key;
-    p.rep_item[i] = p.tval[s];
-    p.tval[s] = (uint32_t)i;
-    if (p.pres) {
-      const int c = trie_cls(p, key);
-      const int r = p.root_rank[c];
-      p.nid[i] = (uint32_t)r;
-      if (p.cls[c].pp - 1 >= 1) p.pres[(uint64_t)r * p.U + trie_code(p, key, 0)] = 1;
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+
+// Grid barrier of the cooperative K_trie_build (all CTAs co-resident).
+__device__ __forceinline__ void grid_barrier(TrieState* st) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t g = ld_acquire(&st->bar_gen);
+    __threadfence();
+    if (atomicAdd(&st->bar_count, 1u) == gridDim.x - 1) {
+      st->bar_count = 0;
+      __threadfence();
+      atomicAdd(&st->bar_gen, 1u);
+    } else {
+      while (ld_acquire(&st->bar_gen) == g) __nanosleep(64);
     }
+    __threadfence();
   }
+  __syncthreads();
 }
 
 __device__ __forceinline__ uint32_t block_sum_u32(uint32_t v, uint32_t* sm) {
@@ -159,256 +169,490 @@ __device__ __forceinline__ uint32_t block_sum_u32(uint32_t v, uint32_t* sm) {
   return t;
 }
 
-__device__ __forceinline__ uint64_t level_entries(const TrieParams& p, int d) {
-  const uint64_t n = (uint64_t)p.st->cnt[d - 1] * (uint64_t)p.U;
-  return n < p.pres_cap ? n : p.pres_cap;
+// Exclusive prefix of n values in smem (in place) by one warp; returns the
+// total (valid in that warp).
+__device__ __forceinline__ unsigned long long warp_exscan(unsigned long long* a, int n) {
+  const int l = threadIdx.x & 31;
+  unsigned long long carry = 0;
+  for (int b = 0; b < n; b += 32) {
+    const unsigned long long v = b + l < n ? a[b + l] : 0;
+    unsigned long long incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (l >= o) incl += y;
+    }
+    if (b + l < n) a[b + l] = carry + incl - v;
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  return carry;
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_level_up(TrieParams p, int d) {
-  __shared__ uint32_t sm[32];
-  if (p.st->ovf) return;
-  const uint64_t n = level_entries(p, d);
-  const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
-  const uint64_t b = (uint64_t)blockIdx.x * per, e = b + per < n ? b + per : n;
-  uint32_t s = 0;
-  for (uint64_t x = b + threadIdx.x; x < e; x += blockDim.x) s += p.pres[x];
-  s = block_sum_u32(s, sm);
-  if (threadIdx.x == 0) p.partial[blockIdx.x] = s;
-}
-
-// Scan of the child marks -> depth-d nodes; clears the marks it reads; the
-// last CTA plans the level.
-__global__ void __launch_bounds__(kScanThreads) k_level_down(TrieParams p, int d) {
-  __shared__ uint32_t sm[32], wsum[32];
-  __shared__ uint64_t s_off;
-  __shared__ int s_last;
-  const int tid = threadIdx.x, l = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
-  const uint64_t n = level_entries(p, d);
-  const uint64_t noff = d == 1 ? 0 : p.st->node_off[d - 1] + p.st->cnt[d - 1];
-  const bool ovf = p.st->ovf || noff + n > p.node_cap;
-  const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
-  const uint64_t b = (uint64_t)blockIdx.x * per, e = b + per < n ? b + per : n;
-  uint32_t base = 0;
-  if (!ovf) {
-    uint32_t s = 0;
-    for (int x = tid; x < (int)blockIdx.x; x += blockDim.x) s += p.partial[x];
-    base = block_sum_u32(s, sm);
-  }
-  const uint64_t poff = d == 1 ? 0 : p.st->node_off[d - 1];
-  for (uint64_t x0 = b; x0 < e; x0 += blockDim.x) {
-    const uint64_t x = x0 + tid;
-    const uint32_t f = x < e ? p.pres[x] : 0;
-    const unsigned bal = __ballot_sync(0xffffffffu, f != 0);
-    __syncthreads();
-    if (l == 0) wsum[w] = __popc(bal);
-    __syncthreads();
-    uint32_t before = base;
-    for (int q = 0; q < w; ++q) before += wsum[q];
-    before += __popc(bal & ((1u << l) - 1));
-    if (f) {
-      if (!ovf) {
-        const uint32_t id = before;
-        const uint64_t par = x / (uint64_t)p.U;
-        p.npar[noff + id] = (uint32_t)par;
-        p.ncode[noff + id] = (uint8_t)(x % (uint64_t)p.U);
-        p.ncls[noff + id] = (uint16_t)(d == 1 ? p.root_cls[par] : p.ncls[poff + par]);
-        p.cid[x] = id;
-      }
-      p.pres[x] = 0;
+// CTA 0 of K_trie_build: the plan of depth d (all nodes of depth d written).
+__device__ void plan_level(const TrieParams& p, int d, uint32_t total, uint64_t noff,
+                           unsigned long long* sm4) {
+  __shared__ unsigned long long s_tot[4];
+  const int NC = p.n_cls, tid = threadIdx.x;
+  unsigned long long* s_tiles = sm4;
+  unsigned long long* s_v = sm4 + NC;
+  unsigned long long* s_b = sm4 + 2 * NC;
+  unsigned long long* s_r = sm4 + 3 * NC;
+  const uint16_t* cl = p.ncls + noff;
+  uint32_t* nb = p.nb + (size_t)d * NC;
+  uint32_t* nK = p.nK + (size_t)d * NC;
+  uint32_t* nx = p.nxc + (size_t)d * NC;
+  (void)cl;
+  (void)total;
+  for (int c = tid; c < NC; c += blockDim.x) {
+    // the scan left [first node, end) of the class at depth d in nb / nK
+    // (both zero for a class without nodes)
+    const uint32_t lo = __ldcg(nb + c), K = __ldcg(nK + c) - lo;
+    nK[c] = K;
+    uint32_t runs = 0, chunks = 1;
+    unsigned long long vs = 0, bs = 0;
+    if (K) {
+      const TrieStage ts = p.tstage[(size_t)c * (p.max_pp + 1) + d + 1];
+      runs = (K + ts.tn - 1) / ts.tn;
+      // few node runs (the upper levels): cut the cells into chunks (>= 32
+      // cells) so the level still spreads over the GPU
+      if (ts.wide && runs < 64) chunks = min((64 + runs - 1) / runs, (ts.n + 31) / 32);
+      if (d < p.cls[c].pp - 1) vs = (unsigned long long)K * ts.n;  // leaves keep argmins only
+      bs = (unsigned long long)K * ts.n;
     }
-    for (int q = 0; q < nw; ++q) base += wsum[q];
+    nx[c] = chunks;
+    s_tiles[c] = (unsigned long long)runs * chunks;
+    s_v[c] = vs;
+    s_b[c] = bs;
+    s_r[c] = runs;
   }
-  // last CTA: level total and plan
-  __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = atomicAdd(&p.st->ticket, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  if (tid == 0) p.st->ticket = 0;
-  if (ovf) {
-    if (tid == 0) p.st->ovf = 1;
-    return;
+  const int w = tid >> 5;
+  if (w < 4) {
+    const unsigned long long t = warp_exscan(sm4 + (size_t)w * NC, NC);
+    if ((tid & 31) == 0) s_tot[w] = t;
   }
-  uint32_t s = 0;
-  for (int x = tid; x < (int)gridDim.x; x += blockDim.x) s += __ldcg(p.partial + x);
-  const uint32_t total = block_sum_u32(s, sm);
-  // per class: node range (nodes are class-sorted), tiles, table sizes
-  uint32_t* nb = p.nb + (size_t)d * p.n_cls;
-  uint32_t* nK = p.nK + (size_t)d * p.n_cls;
-  const uint16_t* cl = p.ncls + noff;  // written by the other CTAs: read through L2 (__ldcg)
-  for (int c = tid; c < p.n_cls; c += blockDim.x) {
-    uint32_t lo = 0, hi = total;  // lower_bound(c)
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (__ldcg(cl + mid) < c) lo = mid + 1;
-      else hi = mid;
-    }
-    uint32_t lo2 = lo, hi2 = total;  // upper_bound(c)
-    while (lo2 < hi2) {
-      const uint32_t mid = (lo2 + hi2) >> 1;
-      if (__ldcg(cl + mid) <= c) lo2 = mid + 1;
-      else hi2 = mid;
-    }
-    nb[c] = lo;
-    nK[c] = lo2 - lo;
+  __syncthreads();
+  TrieState* st = p.st;
+  uint32_t* tb = p.tbase + (size_t)d * (NC + 1);
+  uint64_t* vb = p.vbase + (size_t)d * NC;
+  uint64_t* bb = p.bbase + (size_t)d * NC;
+  uint64_t* rb = p.rbase + (size_t)d * NC;
+  for (int c = tid; c < NC; c += blockDim.x) {
+    tb[c] = (uint32_t)s_tiles[c];
+    vb[c] = st->v_bump + s_v[c];
+    bb[c] = st->bp_bump + s_b[c];
+    rb[c] = st->run_bump + s_r[c];
   }
   __syncthreads();
   if (tid == 0) {
-    p.st->cnt[d] = total;
-    p.st->node_off[d] = noff;
-    uint32_t* tb = p.tbase + (size_t)d * (p.n_cls + 1);
-    uint64_t* vb = p.vbase + (size_t)d * p.n_cls;
-    uint64_t* bb = p.bbase + (size_t)d * p.n_cls;
-    uint32_t tiles = 0;
-    uint64_t vacc = 0, bacc = p.st->bp_bump;
-    for (int c = 0; c < p.n_cls; ++c) {
-      tb[c] = tiles;
-      vb[c] = vacc;
-      bb[c] = bacc;
-      const uint32_t K = nK[c];
-      if (!K) continue;
-      const TrieStage ts = p.tstage[(size_t)c * (p.max_pp + 1) + d + 1];
-      tiles += (K + ts.tn - 1) / ts.tn;
-      if (d < p.cls[c].pp - 1) vacc += (uint64_t)K * ts.n;  // leaves keep argmins only
-      bacc += (uint64_t)K * ts.n;
-    }
-    tb[p.n_cls] = tiles;
-    p.st->ntiles[d] = tiles;
-    p.st->bp_bump = bacc;
-    if (vacc > p.vcap || bacc > p.bpcap) p.st->ovf = 1;
+    tb[NC] = (uint32_t)s_tot[0];
+    st->cnt[d] = total;
+    st->node_off[d] = noff;
+    st->tile_off[d] = (uint32_t)st->tile_bump;
+    st->tile_bump += s_tot[0];
+    st->v_bump += s_tot[1];
+    st->bp_bump += s_tot[2];
+    st->run_bump += s_tot[3];
+    if (st->v_bump > p.vcap || st->bp_bump > p.bpcap || st->run_bump > p.run_cap ||
+        st->tile_bump > p.tile_cap)
+      st->ovf = 1;
   }
+  __syncthreads();
 }
 
-__global__ void k_level_assign(TrieParams p, int d) {
-  if (p.st->ovf) return;
+// The trie of the chunk's signatures and the tile list of its DP.
+__global__ void __launch_bounds__(kBuildThreads) k_trie_build(TrieParams p) {
+  extern __shared__ unsigned long long build_sm[];  // [4][n_cls] (CTA 0's plans)
+  __shared__ uint32_t sm[32], wsum[32];
+  TrieState* st = p.st;
+  const int tid = threadIdx.x, l = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+  const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + tid, gstride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t n = *p.n_sig;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t key = p.sig_key[i];
-    const int pp = p.cls[trie_cls(p, key)].pp;
-    if (pp - 1 < d) continue;
-    const uint32_t node = p.cid[(uint64_t)p.nid[i] * p.U + trie_code(p, key, d - 1)];
-    p.nid[i] = node;
-    if (pp - 1 >= d + 1) p.pres[(uint64_t)node * p.U + trie_code(p, key, d)] = 1;
+  // ---- signature list, roots, depth-1 marks --------------------------------
+  for (uint64_t i = gtid; i < n; i += gstride) {
+    const uint32_t s = p.uniq[i];
+    const unsigned long long k = p.tkey[s];
+    const uint64_t key = p.key_shift >= 64 ? k : (k & ((1ull << p.key_shift) - 1));
+    p.sig_key[i] = key;
+    p.rep_item[i] = p.tval[s];
+    p.tval[s] = (uint32_t)i;
+    const int c = trie_cls(p, key);
+    const int r = p.root_rank[c];
+    p.nid[i] = (uint32_t)r;
+    if (p.cls[c].pp - 1 >= 1) p.pres[(uint64_t)r * p.U + trie_code(p, key, 0)] = 1;
   }
-}
-
-// Stage j = d + 1 over the depth-d nodes, one tile per CTA iteration.
-__global__ void __launch_bounds__(kTrieThreads, 4) k_trie_tiles(TrieParams p, int d) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int s_c;
-  if (p.st->ovf) return;
-  const int tid = threadIdx.x, nt = blockDim.x, L = p.L, LP = L + 1, j = d + 1;
-  const uint32_t ntiles = p.st->ntiles[d];
-  const uint32_t* tb = p.tbase + (size_t)d * (p.n_cls + 1);
-  const uint64_t noff = p.st->node_off[d], poff = d >= 2 ? p.st->node_off[d - 1] : 0;
-  const double* Vprev = p.varena[(d - 1) & 1];
-  double* Vcur = p.varena[d & 1];
-  unsigned long long mine = 0;
-  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    if (tid == 0) {
-      int lo = 0, hi = p.n_cls - 1;  // last class with tbase <= t
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (tb[mid] <= t) lo = mid;
-        else hi = mid - 1;
-      }
-      s_c = lo;
+  grid_barrier(st);
+  uint32_t cnt_prev = (uint32_t)p.n_roots;       // nodes of depth d-1
+  uint64_t off_prev = 0, noff = 0;               // node_off of depth d-1, d
+  uint64_t marked = (uint64_t)p.n_roots * p.U;   // mark entries that may be set
+  bool ovf = false;  // (every CTA takes the same decisions: the same inputs)
+  for (int d = 1; d <= p.nq; ++d) {
+    const uint64_t ne = marked;
+    noff = d == 1 ? 0 : off_prev + cnt_prev;
+    if (noff + ne > p.node_cap) {
+      ovf = true;
+      break;
     }
-    __syncthreads();
-    const int c = s_c;
-    const ClassDev cl = p.cls[c];
-    const TrieStage ts = p.tstage[(size_t)c * (p.max_pp + 1) + j];
-    const TrieStage tp = p.tstage[(size_t)c * (p.max_pp + 1) + j - 1];
-    const uint32_t nbc = p.nb[(size_t)d * p.n_cls + c], Kc = p.nK[(size_t)d * p.n_cls + c];
-    const uint32_t n0 = nbc + (t - tb[c]) * ts.tn;
-    const uint32_t nn = min(ts.tn, nbc + Kc - n0);
-    const bool leaf = d == cl.pp - 1;
-    // parents (consecutive depth-(d-1) nodes) and their stage-(j-1) tables
-    const uint32_t pfirst = d >= 2 ? p.npar[noff + n0] : 0;
-    const uint32_t plast = d >= 2 ? p.npar[noff + n0 + nn - 1] : 0;
-    const int P = (int)(plast - pfirst) + 1;
-    const int Pst = P | 1;  // odd stride (in doubles): rows start on distinct banks
-    const int Np = (int)tp.n, Nj = (int)ts.n;
-    double* sV = reinterpret_cast<double*>(smem_raw);
-    double* sE = sV + (size_t)Np * Pst;
-    double* sPf = sE + (size_t)p.n_codes * L;
-    if (d >= 2) {
-      const uint32_t pnb = p.nb[(size_t)(d - 1) * p.n_cls + c];
-      const double* src = Vprev + p.vbase[(size_t)(d - 1) * p.n_cls + c] + (uint64_t)(pfirst - pnb) * Np;
-      for (int x = tid; x < P * Np; x += nt) {
-        const int pl = x / Np, xp = x - pl * Np;
-        sV[xp * Pst + pl] = src[x];
+    // ---- scan of the marks: per-CTA sums -----------------------------------
+    const uint64_t per = (ne + gridDim.x - 1) / gridDim.x;
+    const uint64_t b = (uint64_t)blockIdx.x * per, e = b + per < ne ? b + per : ne;
+    uint32_t s = 0;
+    for (uint64_t x = b + tid; x < e; x += blockDim.x) s += __ldcg(p.pres + x);
+    s = block_sum_u32(s, sm);
+    if (tid == 0) p.partial[blockIdx.x] = s;
+    grid_barrier(st);
+    // ---- node ids: exclusive scan, node arrays, clear the marks ------------
+    uint32_t base = 0, total = 0;
+    {
+      uint32_t a = 0, t = 0;
+      for (int x = tid; x < (int)gridDim.x; x += blockDim.x) {
+        const uint32_t v = __ldcg(p.partial + x);
+        t += v;
+        if (x < (int)blockIdx.x) a += v;
       }
-    } else {
-      const double* src = p.v1g + p.v1off[c];
-      for (int x = tid; x < Np; x += nt) sV[x * Pst] = src[x];
+      base = block_sum_u32(a, sm);
+      total = block_sum_u32(t, sm);
     }
-    int* sNode = reinterpret_cast<int*>(sPf + LP);  // (code << 16) | parent slot
-    const double* qt = p.qtab + (size_t)c * p.n_codes * L;
-    for (int x = tid; x < p.n_codes * L; x += nt) sE[x] = qt[x];
-    for (int x = tid; x < LP; x += nt) sPf[x] = p.prefix[(size_t)cl.pair * LP + x];
-    for (int x = tid; x < (int)nn; x += nt) {
-      const uint64_t node = noff + n0 + x;
-      sNode[x] = ((int)p.ncode[node] << 16) | (d >= 2 ? (int)(p.npar[node] - pfirst) : 0);
-    }
-    __syncthreads();
-    const double g1 = (double)(cl.gas - 1);
-    const double* dom = p.domain + (size_t)cl.pair * p.nv_stride;
-    const ProgDev pg = p.progs[p.class_prog[c]];
-    const uint16_t* pr = p.preds + pg.pred_base;
-    const int G = (int)((nn + kTrieNB - 1) / kTrieNB);
-    const int items = Nj * G;
-    const uint64_t vb = leaf ? 0 : p.vbase[(size_t)d * p.n_cls + c];
-    uint8_t* bpo = p.bparena + p.bbase[(size_t)d * p.n_cls + c];
-    for (int it = tid; it < items; it += nt) {
-      const int x = it / G, g = it - x * G;
-      const uint2 rec = p.cellrec[ts.cell0 + x];
-      const int i = rec.x >> 16, m = rec.x & 0xffff;
-      const uint16_t* q = pr + rec.y;
-      const double dm = dom[m];
-      const double Pi = sPf[i];
-      int pl[kTrieNB];
-      const double* E[kTrieNB];
-      double best[kTrieNB];
-      int bc[kTrieNB];
-#pragma unroll
-      for (int b = 0; b < kTrieNB; ++b) {
-        const int ln = g * kTrieNB + b < (int)nn ? g * kTrieNB + b : g * kTrieNB;  // pad: repeat
-        const int nd = sNode[ln];
-        pl[b] = nd & 0xffff;
-        E[b] = sE + (nd >> 16) * L;
-        best[b] = CUDART_INF;
-        bc[b] = -1;
-      }
-#pragma unroll 2
-      for (int cut = j - 1; cut < i; ++cut) {  // pipeline_dp.cpp:114-131
-        const double t2 = Pi - sPf[cut];
-        const double term = t2 > dm ? g1 * (t2 - dm) : 0.0;
-        const double* row = sV + (int)q[cut - (j - 1)] * Pst;
-#pragma unroll
-        for (int b = 0; b < kTrieNB; ++b) {
-          const double gv = ((row[pl[b]] + term) + t2) + E[b][cut];
-          if (gv < best[b]) {
-            best[b] = gv;
-            bc[b] = cut;
+    for (uint64_t x0 = b; x0 < e; x0 += blockDim.x) {
+      const uint64_t x = x0 + tid;
+      const uint32_t f = x < e ? __ldcg(p.pres + x) : 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, f != 0);
+      __syncthreads();
+      if (l == 0) wsum[w] = __popc(bal);
+      __syncthreads();
+      uint32_t before = base;
+      for (int q = 0; q < w; ++q) before += wsum[q];
+      before += __popc(bal & ((1u << l) - 1));
+      if (x < e) {  // class node ranges at depth d: the prefix at a class's first / after its last parent
+        const uint64_t par = x / (uint64_t)p.U;
+        const uint32_t rem = (uint32_t)(x - par * p.U);
+        if (rem == 0 || rem == (uint32_t)p.U - 1) {
+          int c, cprev = -1, cnext = -1;
+          if (d == 1) {
+            c = p.root_cls[par];
+          } else {
+            const uint16_t* pc = p.ncls + off_prev;
+            c = __ldcg(pc + par);
+            if (rem == 0 && par > 0) cprev = __ldcg(pc + par - 1);
+            if (rem != 0 && par + 1 < cnt_prev) cnext = __ldcg(pc + par + 1);
           }
+          if (rem == 0 && cprev != c) p.nb[(size_t)d * p.n_cls + c] = before;
+          if (rem == (uint32_t)p.U - 1 && cnext != c) p.nK[(size_t)d * p.n_cls + c] = before + f;
         }
       }
+      if (f) {
+        const uint64_t par = x / (uint64_t)p.U;
+        p.npar[noff + before] = (uint32_t)par;
+        p.ncode[noff + before] = (uint8_t)(x % (uint64_t)p.U);
+        p.ncls[noff + before] = (uint16_t)(d == 1 ? p.root_cls[par] : __ldcg(p.ncls + off_prev + par));
+        p.cid[x] = before;
+        p.pres[x] = 0;
+      }
+      for (int q = 0; q < nw; ++q) base += wsum[q];
+    }
+    grid_barrier(st);
+    marked = 0;
+    if (d < p.nq && (uint64_t)total * p.U > p.pres_cap) {
+      ovf = true;
+      break;
+    }
+    // ---- plan of depth d (CTA 0); each signature's node, depth-(d+1) marks
+    if (blockIdx.x == 0) plan_level(p, d, total, noff, build_sm);
+    for (uint64_t i = gtid; i < n; i += gstride) {
+      const uint64_t key = p.sig_key[i];
+      const int pp = p.cls[trie_cls(p, key)].pp;
+      if (pp - 1 < d) continue;
+      const uint32_t node = __ldcg(p.cid + (uint64_t)p.nid[i] * p.U + trie_code(p, key, d - 1));
+      p.nid[i] = node;
+      if (pp - 1 >= d + 1) p.pres[(uint64_t)node * p.U + trie_code(p, key, d)] = 1;
+    }
+    if (d < p.nq) marked = (uint64_t)total * p.U;
+    grid_barrier(st);
+    if (ld_acquire(&st->ovf) != 0) {  // a plan capacity was exceeded
+      ovf = true;
+      break;
+    }
+    off_prev = noff;
+    cnt_prev = total;
+  }
+  if (ovf) {  // clear the marks left behind; the signature-mode K_dp takes over
+    for (uint64_t x = gtid; x < marked; x += gstride) p.pres[x] = 0;
+    if (blockIdx.x == 0 && tid == 0) st->ovf = 1;
+    return;
+  }
+  // ---- tile list of all depths; run counters cleared -----------------------
+  const uint32_t T = (uint32_t)st->tile_bump;
+  if (blockIdx.x == 0 && tid == 0) {
+    st->tile_off[p.nq + 1] = T;
+    st->next_tile = 0;
+  }
+  for (uint64_t r = gtid; r < st->run_bump; r += gstride) p.done[r] = 0;
+  for (uint64_t t = gtid; t < T; t += gstride) {
+    int d = 1;
+    while (d < p.nq && st->tile_off[d + 1] <= t) ++d;
+    const uint32_t tt = (uint32_t)t - st->tile_off[d];
+    const uint32_t* tb = p.tbase + (size_t)d * (p.n_cls + 1);
+    int lo = 0, hi = p.n_cls - 1;  // last class with tbase <= tt
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tb[mid] <= tt) lo = mid;
+      else hi = mid - 1;
+    }
+    const int c = lo;
+    const TrieStage ts = p.tstage[(size_t)c * (p.max_pp + 1) + d + 1];
+    const uint32_t chunks = p.nxc[(size_t)d * p.n_cls + c];
+    const uint32_t lt = tt - tb[c], run = lt / chunks, cc = lt - run * chunks;
+    const uint32_t nbc = p.nb[(size_t)d * p.n_cls + c], K = p.nK[(size_t)d * p.n_cls + c];
+    TrieTile tl;
+    tl.n0 = nbc + run * ts.tn;
+    tl.c = (uint16_t)c;
+    tl.d = (uint8_t)d;
+    tl.pad = 0;
+    tl.nn = (uint16_t)min(ts.tn, nbc + K - tl.n0);
+    const uint32_t xc = (ts.n + chunks - 1) / chunks;
+    tl.x0 = (uint16_t)(cc * xc);
+    tl.x1 = (uint16_t)min(ts.n, (cc + 1) * xc);
+    tl.run = run;
+    tl.pad2 = 0;
+    p.tiles[t] = tl;
+  }
+}
+
+// Wide stages (many cells): the (cell x, group g of 4 nodes) items of one
+// tile.  sV holds, per predecessor cell x' of N_{j-1}, the parent value of
+// every node of the tile (row x', column = node; SINGLE: the one parent's
+// value), sE the edge cost of every node per cut (row cut - (j-1)); rows are
+// TNst doubles (even: a group's 4 nodes are two 16-byte loads).  Per cut the
+// predecessor index, t2 and the tolerance term are shared by the group's 4
+// nodes; each node adds its parent value and its edge
+// (pipeline_dp.cpp:118-127: same operands, same order, strict '<': the
+// lowest cut wins ties).
+template <bool SINGLE>
+__device__ __forceinline__ void tile_wide(const TrieParams& p, const double* __restrict__ sV,
+                                          const double* __restrict__ sE, const double* __restrict__ sPf,
+                                          int TNst, int G, int x0, int x1, int Nj, int j, int nn,
+                                          const TrieStage& ts, const uint16_t* __restrict__ pr,
+                                          const double* __restrict__ dom, double g1, bool leaf,
+                                          double* __restrict__ vout, uint8_t* __restrict__ bpo,
+                                          unsigned long long& mine) {
+  const int items = (x1 - x0) * G;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int xl = it / G, g = it - xl * G, x = x0 + xl;
+    const uint2 rec = p.cellrec[ts.cell0 + x];
+    const int i = rec.x >> 16, m = rec.x & 0xffff;
+    const uint16_t* q = pr + rec.y - (j - 1);
+    const double dm = dom[m];
+    const double Pi = sPf[i];
+    const double* vcol = sV + (SINGLE ? 0 : 4 * g);
+    const double* ecol = sE + 4 * g - (j - 1) * TNst;
+    mine += (unsigned long long)(i - (j - 1)) * (unsigned long long)min(4, nn - 4 * g);
+    double b0 = CUDART_INF, b1 = CUDART_INF, b2 = CUDART_INF, b3 = CUDART_INF;
+    int c0 = -1, c1 = -1, c2 = -1, c3 = -1;
+#pragma unroll 2
+    for (int cut = j - 1; cut < i; ++cut) {  // pipeline_dp.cpp:114-131
+      const double t2 = Pi - sPf[cut];
+      const double term = t2 > dm ? g1 * (t2 - dm) : 0.0;
+      double v0, v1, v2, v3;
+      if (SINGLE) {
+        v0 = v1 = v2 = v3 = vcol[q[cut]];
+      } else {
+        const double2 va = *reinterpret_cast<const double2*>(vcol + (int)q[cut] * TNst);
+        const double2 vb = *reinterpret_cast<const double2*>(vcol + (int)q[cut] * TNst + 2);
+        v0 = va.x;
+        v1 = va.y;
+        v2 = vb.x;
+        v3 = vb.y;
+      }
+      const double2 ea = *reinterpret_cast<const double2*>(ecol + cut * TNst);
+      const double2 eb = *reinterpret_cast<const double2*>(ecol + cut * TNst + 2);
+      const double h0 = ((v0 + term) + t2) + ea.x;
+      const double h1 = ((v1 + term) + t2) + ea.y;
+      const double h2 = ((v2 + term) + t2) + eb.x;
+      const double h3 = ((v3 + term) + t2) + eb.y;
+      if (h0 < b0) { b0 = h0; c0 = cut; }
+      if (h1 < b1) { b1 = h1; c1 = cut; }
+      if (h2 < b2) { b2 = h2; c2 = cut; }
+      if (h3 < b3) { b3 = h3; c3 = cut; }
+    }
+    const double bs[4] = {b0, b1, b2, b3};
+    const int cs[4] = {c0, c1, c2, c3};
 #pragma unroll
-      for (int b = 0; b < kTrieNB; ++b) {
-        const int ln = g * kTrieNB + b;
-        if (ln >= (int)nn) break;
-        const uint64_t o = (uint64_t)(n0 - nbc + ln) * Nj + x;
-        if (!leaf) Vcur[vb + o] = best[b];
-        bpo[o] = (uint8_t)bc[b];
+    for (int b = 0; b < 4; ++b) {
+      const int ln = 4 * g + b;
+      if (ln >= nn) break;
+      const uint64_t o = (uint64_t)ln * Nj + x;
+      if (!leaf) vout[o] = bs[b];
+      bpo[o] = (uint8_t)cs[b];
+    }
+  }
+}
+
+// Narrow stages (few cells, many nodes): one (cell x, node) item per
+// thread.  sV holds the tile's parents' tables once each (row x', column =
+// parent, odd stride), sE the class's edge rows per code (row code).
+__device__ __forceinline__ void tile_narrow(const TrieParams& p, const double* __restrict__ sV,
+                                            const double* __restrict__ sE, const double* __restrict__ sPf,
+                                            const int* __restrict__ sNode, int Pst, int Nj, int j, int nn,
+                                            const TrieStage& ts, const uint16_t* __restrict__ pr,
+                                            const double* __restrict__ dom, double g1, bool leaf,
+                                            double* __restrict__ vout, uint8_t* __restrict__ bpo,
+                                            unsigned long long& mine) {
+  const int L = p.L, items = Nj * nn;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int x = it / nn, ln = it - x * nn;
+    const uint2 rec = p.cellrec[ts.cell0 + x];
+    const int i = rec.x >> 16, m = rec.x & 0xffff;
+    const uint16_t* q = pr + rec.y - (j - 1);
+    const double dm = dom[m];
+    const double Pi = sPf[i];
+    const int nd = sNode[ln];
+    const double* vcol = sV + (nd & 0xffff);
+    const double* E = sE + (nd >> 16) * L;
+    mine += (unsigned long long)(i - (j - 1));
+    double best = CUDART_INF;
+    int bc = -1;
+#pragma unroll 2
+    for (int cut = j - 1; cut < i; ++cut) {  // pipeline_dp.cpp:114-131
+      const double t2 = Pi - sPf[cut];
+      const double term = t2 > dm ? g1 * (t2 - dm) : 0.0;
+      const double h = ((vcol[(int)q[cut] * Pst] + term) + t2) + E[cut];
+      if (h < best) {
+        best = h;
+        bc = cut;
       }
     }
-    mine += (unsigned long long)nn * ts.iters;
-    __syncthreads();  // smem reuse by the next tile
+    const uint64_t o = (uint64_t)ln * Nj + x;
+    if (!leaf) vout[o] = best;
+    bpo[o] = (uint8_t)bc;
   }
-  if (p.exec && tid == 0 && mine) atomicAdd(&p.exec[1], mine);
+}
+
+// All stages of the chunk's trie: persistent CTAs take tiles in depth order;
+// a tile waits for the node runs holding its parents (their stage tables),
+// stages them and the edge rows in shared memory, solves its items and
+// publishes its run.  Parent tables are read through L2 (__ldcg): they were
+// written by other SMs during this launch.
+__global__ void __launch_bounds__(kTrieThreads, 4) k_trie_dp(TrieParams p) {
+  extern __shared__ __align__(16) double smem_d[];
+  __shared__ uint32_t s_t;
+  if (p.st->ovf) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int L = p.L, LP = L + 1, P1 = p.max_pp + 1, NC = p.n_cls;
+  const uint32_t T = p.st->tile_off[p.nq + 1];
+  unsigned long long mine = 0;
+  for (;;) {
+    if (tid == 0) s_t = atomicAdd(&p.st->next_tile, 1u);
+    __syncthreads();
+    const uint32_t t = s_t;
+    if (t >= T) break;
+    const TrieTile tl = p.tiles[t];
+    const int c = tl.c, d = tl.d, j = d + 1, nn = tl.nn;
+    const ClassDev cl = p.cls[c];
+    const TrieStage ts = p.tstage[(size_t)c * P1 + j];
+    const TrieStage tp = p.tstage[(size_t)c * P1 + j - 1];
+    const int Np = (int)tp.n, Nj = (int)ts.n;
+    const uint64_t noff = p.st->node_off[d];
+    const uint32_t nbc = p.nb[(size_t)d * NC + c];
+    const bool leaf = d == cl.pp - 1;
+    const bool single = d < 2;  // depth-1 nodes: one parent, the class's stage-1 table
+    uint32_t pfirst = 0, plast = 0, pnb = 0;
+    uint64_t vbp = 0;
+    if (!single) {
+      pfirst = p.npar[noff + tl.n0];
+      plast = p.npar[noff + tl.n0 + nn - 1];
+      pnb = p.nb[(size_t)(d - 1) * NC + c];
+      vbp = p.vbase[(size_t)(d - 1) * NC + c];
+      // wait for the parents' runs (all their cell chunks)
+      if (warp == 0) {
+        const uint32_t ptn = tp.tn;
+        const uint32_t r0 = (pfirst - pnb) / ptn, r1 = (plast - pnb) / ptn;
+        const uint32_t need = p.nxc[(size_t)(d - 1) * NC + c];
+        const uint32_t* dn = p.done + p.rbase[(size_t)(d - 1) * NC + c];
+        for (uint32_t r = r0 + lane; r <= r1; r += 32)
+          while (ld_acquire(dn + r) < need) __nanosleep(128);
+      }
+      __syncthreads();
+    }
+    const double* qt = p.qtab + (size_t)c * p.n_codes * L;
+    const ProgDev pg = p.progs[p.class_prog[c]];
+    const double* dom = p.domain + (size_t)cl.pair * p.nv_stride;
+    double* vout = p.varena + (leaf ? 0 : p.vbase[(size_t)d * NC + c] + (uint64_t)(tl.n0 - nbc) * Nj);
+    uint8_t* bpo = p.bparena + p.bbase[(size_t)d * NC + c] + (uint64_t)(tl.n0 - nbc) * Nj;
+    const double g1 = (double)(cl.gas - 1);
+    if (ts.wide) {
+      const int G = (nn + 3) >> 2, TW = 4 * G, TNst = TW + 2, ER = L - (j - 1);
+      double* sV = smem_d;
+      double* sE = sV + (single ? ((Np + 1) & ~1) : Np * TNst);
+      double* sPf = sE + ER * TNst;
+      if (single) {
+        const double* src = p.v1g + p.v1off[c];
+        for (int x = tid; x < Np; x += blockDim.x) sV[x] = src[x];
+      } else {
+        for (int ln = warp; ln < TW; ln += nw) {
+          const int lr = ln < nn ? ln : 0;  // padding columns repeat node 0
+          const double* src = p.varena + vbp + (uint64_t)(p.npar[noff + tl.n0 + lr] - pnb) * Np;
+          for (int x = lane; x < Np; x += 32) sV[x * TNst + ln] = __ldcg(src + x);
+        }
+      }
+      for (int ln = warp; ln < TW; ln += nw) {
+        const int lr = ln < nn ? ln : 0;
+        const double* er = qt + (size_t)p.ncode[noff + tl.n0 + lr] * L + (j - 1);
+        for (int r = lane; r < ER; r += 32) sE[r * TNst + ln] = er[r];
+      }
+      for (int x = tid; x < LP; x += blockDim.x) sPf[x] = p.prefix[(size_t)cl.pair * LP + x];
+      __syncthreads();
+      if (single)
+        tile_wide<true>(p, sV, sE, sPf, TNst, G, tl.x0, tl.x1, Nj, j, nn, ts, p.preds + pg.pred_base, dom,
+                        g1, leaf, vout, bpo, mine);
+      else
+        tile_wide<false>(p, sV, sE, sPf, TNst, G, tl.x0, tl.x1, Nj, j, nn, ts, p.preds + pg.pred_base, dom,
+                         g1, leaf, vout, bpo, mine);
+    } else {
+      const int P = single ? 1 : (int)(plast - pfirst) + 1;
+      const int Pst = P | 1;  // odd stride: rows start on distinct banks
+      double* sV = smem_d;
+      double* sE = sV + (size_t)Np * Pst;
+      double* sPf = sE + (size_t)p.n_codes * L;
+      int* sNode = reinterpret_cast<int*>(sPf + LP);  // (code << 16) | parent column
+      if (single) {
+        const double* src = p.v1g + p.v1off[c];
+        for (int x = tid; x < Np; x += blockDim.x) sV[x * Pst] = src[x];
+      } else {
+        const double* src = p.varena + vbp + (uint64_t)(pfirst - pnb) * Np;
+        for (int pl = warp; pl < P; pl += nw)
+          for (int x = lane; x < Np; x += 32) sV[x * Pst + pl] = __ldcg(src + (size_t)pl * Np + x);
+      }
+      for (int x = tid; x < p.n_codes * L; x += blockDim.x) sE[x] = qt[x];
+      for (int x = tid; x < LP; x += blockDim.x) sPf[x] = p.prefix[(size_t)cl.pair * LP + x];
+      for (int x = tid; x < nn; x += blockDim.x) {
+        const uint64_t node = noff + tl.n0 + x;
+        sNode[x] = ((int)p.ncode[node] << 16) | (single ? 0 : (int)(p.npar[node] - pfirst));
+      }
+      __syncthreads();
+      tile_narrow(p, sV, sE, sPf, sNode, Pst, Nj, j, nn, ts, p.preds + pg.pred_base, dom, g1, leaf, vout,
+                  bpo, mine);
+    }
+    // publish: every thread's stores, then the run's chunk count
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(p.done + p.rbase[(size_t)d * NC + c] + tl.run, 1u);
+  }
+  if (p.exec) {  // executed inner iterations (roofline accounting), one atomic per warp
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if (lane == 0 && mine) atomicAdd(&p.exec[1], mine);
+  }
+}
+
+// Shared memory (doubles) of a K_trie_dp tile at stage j (host mirror of the
+// carve-ups above): wide, n groups of 4 nodes; narrow, n nodes (and at most
+// n parents).
+__host__ __device__ inline size_t trie_tile_doubles(bool wide, int j, int n, int Np, int L, int n_codes) {
+  if (wide) {
+    const size_t TNst = 4 * (size_t)n + 2;
+    return (j == 2 ? ((size_t)Np + 1) & ~size_t(1) : (size_t)Np * TNst) + (size_t)(L - (j - 1)) * TNst +
+           (size_t)L + 1;
+  }
+  const size_t Pst = (j == 2 ? 1 : (size_t)n) | 1;
+  return (size_t)Np * Pst + (size_t)n_codes * L + (size_t)L + 1 + ((size_t)n + 1) / 2;
 }
 
 // One thread per signature: backtrack (pipeline_dp.cpp:134-148) along its
@@ -440,7 +684,20 @@ __global__ void k_trie_back(TrieParams p) {
     }
     co[0] = 0;
   }
-  if (p.exec && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&p.exec[0], (unsigned long long)n);  // one DP instance per signature
+  if (p.exec && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&p.exec[0], (unsigned long long)n);
+}
+
+// Signature list only (trie off: the signature-mode K_dp solves the DP).
+__global__ void k_sig_list(TrieParams p) {
+  const uint64_t n = *p.n_sig;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = p.uniq[i];
+    const unsigned long long k = p.tkey[s];
+    p.sig_key[i] = p.key_shift >= 64 ? k : (k & ((1ull << p.key_shift) - 1));
+    p.rep_item[i] = p.tval[s];
+    p.tval[s] = (uint32_t)i;
+  }
 }
 
 // Stage-1 values of every heavy class (pipeline_dp.cpp:102-107), once per

@@ -571,5 +571,5 @@ def test_trie_dp_stage_timing_and_counts():
         s.run(0, s.num_candidates, k=10)
         st = s.stats()
     assert st["dp_fallback"] == 0
-    assert st["dp_stage_launches"] >= 14 and st["dp_stage_ms"] > 0
+    assert st["dp_stage_launches"] == 1 and st["dp_stage_ms"] > 0  # one K_trie_dp per chunk
     assert st["dp_inner"] > 0 and st["fp64_ops"] == 7 * st["dp_inner"]
