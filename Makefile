@@ -8,7 +8,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC,-Wall,-
            -Xptxas -v,-warn-spills --expt-relaxed-constexpr $(EXTRA)
 PKG := paper_2210_07297_b200
 LIB := $(PKG)/libamp_search.so
-SRCS := $(PKG)/csrc/amp_search.cu $(PKG)/csrc/amp_simulate.cpp $(PKG)/csrc/amp_anneal.cpp
+SRCS := $(PKG)/csrc/amp_search.cu $(PKG)/csrc/amp_anneal.cpp
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/amp_search.h
 
 all: lib oracle

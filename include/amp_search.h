@@ -18,7 +18,7 @@
  *   - Per-candidate failures (pp > L, profile miss, parameter ceiling,
  *     invalid bandwidth) are DATA in amp_record.fail_code, never errors —
  *     matching the reference, which catches them per candidate into
- *     CandidateRecord.failure (optimizer.cpp:258-260).
+ *     CandidateRecord.failure (optimizer.cpp:172-174).
  *   - Inputs are copied to the device at create time; the caller may free
  *     them afterwards.  Output buffers are caller-allocated host memory
  *     unless the function name ends in _device.
@@ -99,7 +99,7 @@ typedef struct amp_problem {
 
 /*
  * Candidate space.  Candidates are the reference plan() list
- * (optimizer.cpp:288-293: pp asc, dp asc, tmp = |D|/(pp*dp), mbs in
+ * (optimizer.cpp:202-207: pp asc, dp asc, tmp = |D|/(pp*dp), mbs in
  * divisors(gbs/dp) asc) — the "classes" — crossed with P placements per
  * class in class-major order: index = class * P + p.
  *   p == 0 : the reference heuristic placement (placement.cpp:27-66);
@@ -207,7 +207,7 @@ int amp_search_partition(const amp_ctx* ctx, int32_t n_parts, uint64_t* bounds);
 /* ---- evaluation --------------------------------------------------------- */
 /* Evaluate candidates [begin, end).  Writes the k best under the key
  * (failed, total, index) — the reference rank_records order
- * (optimizer.cpp:264-282) — to topk[0 .. *n_topk).  If `all` is non-NULL
+ * (optimizer.cpp:178-196) — to topk[0 .. *n_topk).  If `all` is non-NULL
  * it receives every record in index order ([end - begin]); `all_details`
  * (nullable) the per-candidate vectors.  Host buffers.                    */
 int amp_search_run(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k,
@@ -316,14 +316,6 @@ typedef struct amp_dp_instance {
 int amp_dp_solve_batch(int32_t device, const amp_dp_instance* instances, int32_t n,
                        int32_t* cuts_out, int32_t cut_stride, double* cost_out,
                        int32_t* status_out);
-
-/* ---- host simulator (plan()'s top-`budget` validation) ---------------- */
-/* simulate() of one strategy (reference simulator.cpp:140-198): writes the
- * iteration time (makespan over replicas + dpsync).  Host code; returns
- * AMP_E_INVALID for an invalid strategy (validate_strategy, types.cpp:191). */
-int amp_simulate(const amp_problem* problem, int32_t pp, int32_t dp, int32_t tmp, int32_t mbs,
-                 const int32_t* rank_to_device, const int32_t* cut_boundaries,
-                 double* iteration_time);
 
 /* Measured FP64 add throughput of `device` (DADD instructions/s over all
  * SMs), for the roofline denominator.                                     */

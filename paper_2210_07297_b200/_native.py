@@ -195,8 +195,6 @@ SIGNATURES = [
     ("amp_search_last_stats", C.c_int, [C.c_void_p, C.POINTER(AmpStats)]),
     ("amp_dp_solve_batch", C.c_int, [C.c_int32, C.POINTER(AmpDpInstance), C.c_int32, _ip, C.c_int32,
                                      _dp, _ip]),
-    ("amp_simulate", C.c_int, [C.POINTER(AmpProblem), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
-                               _ip, _ip, _dp]),
     ("amp_fp64_peak", C.c_int, [C.c_int32, _dp, _dp]),
 ]
 

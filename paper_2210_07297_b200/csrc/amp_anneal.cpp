@@ -1,6 +1,12 @@
 // amp_anneal.cpp — the annealing search over domino-tiling placements
 // (reference placement.cpp:299-398, the paper's Algorithm 2) on the engine.
 //
+// COMPATIBILITY PORT of placement.cpp's host-side chain (device_grid,
+// the backtracking domino tiling, strategy_key, the Metropolis loop): a
+// bit-exact std::mt19937_64 draw sequence forces the reference's control
+// flow and draw order, so this part follows placement.cpp:68-398 closely.
+// The B200 work is the proposals' DP + estimate on the GPU (below).
+//
 // The chain itself is sequential and host-side, as in the reference: the
 // same std::mt19937_64 stream (rng.hpp:25-44), the same draw order (degree
 // flip, mbs, tiling orientations with backtracking, acceptance), the same

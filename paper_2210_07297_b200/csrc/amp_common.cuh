@@ -6,7 +6,7 @@
 //                           index of SegmentTimes/tolerance_domain
 //                           (reference pipeline_dp.cpp:39-91), built once
 //                           per pair instead of once per candidate.
-//   ClassDev[n_cls]         plan() candidate list (optimizer.cpp:288-293)
+//   ClassDev[n_cls]         plan() candidate list (optimizer.cpp:202-207)
 //                           with gas and the pair it uses.
 //   times   [n_pairs][L]    f64 layer times (LayerTimeResolver, cost_model.cpp:74-86)
 //   prefix  [n_pairs][L+1]  f64 prefix sums, left-to-right
@@ -206,7 +206,7 @@ __host__ __device__ inline uint64_t splitmix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
-// Ranking key of rank_records (optimizer.cpp:264-282): non-failed first,
+// Ranking key of rank_records (optimizer.cpp:178-196): non-failed first,
 // then total ascending, then (pp, dp, tmp, mbs[, p]) == candidate index.
 // fail_code < 0 marks an empty slot that sorts after everything.
 __host__ __device__ inline bool rank_less(const amp_record& a, const amp_record& b) {

@@ -462,7 +462,7 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   CK(cudaEventCreate(&ctx->ev2));
 
   tm.mark("stream/events");
-  // ---- classes: the plan() candidate list (optimizer.cpp:288-293) -------
+  // ---- classes: the plan() candidate list (optimizer.cpp:202-207) -------
   std::map<std::pair<int, int>, int> pair_of;
   std::vector<int> pair_tmp, pair_mbs;
   for (int pp : divisors(D))

@@ -123,7 +123,7 @@ PlanResult plan(const ModelGraph& model, const Cluster& cluster, const ProfileTa
   amp_search_destroy(ctx);
   if (rc != AMP_OK) throw std::runtime_error("amp_search_run: " + err);
 
-  // rank_records key (optimizer.cpp:264-282): index order == (pp, dp, tmp, mbs)
+  // rank_records key (optimizer.cpp:178-196): index order == (pp, dp, tmp, mbs)
   std::vector<size_t> order(n);
   std::iota(order.begin(), order.end(), 0);
   std::sort(order.begin(), order.end(), [&](size_t a, size_t b) {

@@ -4,8 +4,8 @@
 declared optimizer.hpp:74-75): same candidate list, same ranking, same
 CandidateRecord/PlanResult shapes and failure texts.  The worker pool +
 evaluate_candidate + rank_records region runs on the GPU through
-libamp_search.so; the simulator validation of the top `budget` runs through
-the engine's host simulator (amp_simulate).
+libamp_search.so; the simulator validation of the top `budget` runs on the
+device too (the engine's batched simulator, simulator.cpp:75-198).
 
 `Searcher` is the thin object over an amp_ctx for the large placement sweep
  and for multi-GPU sharding.
@@ -287,7 +287,7 @@ def records_to_candidates(recs: np.ndarray, bufs: dict, n_layers: int,
 
 
 def rank_order(recs: np.ndarray) -> np.ndarray:
-    """rank_records key (optimizer.cpp:264-282): (failed, total, index)."""
+    """rank_records key (optimizer.cpp:178-196): (failed, total, index)."""
     failed = (recs["fail_code"] != 0).astype(np.int64)
     total = np.where(failed == 1, 0.0, recs["total"])
     return np.lexsort((recs["index"], total, failed))
@@ -301,8 +301,6 @@ def plan(model: ModelGraph, cluster: Cluster, profile: ProfileTable, gbs: int,
     order) — acceptance criterion 5's rank agreement in one pass."""
     import os
     import time
-
-    from . import simulator
 
     tm = {} if os.environ.get("AMP_TIMING") else None
     t = time.perf_counter()

@@ -455,6 +455,6 @@ def enumerate_mbs(gbs: int, dp: int) -> List[int]:
 
 
 def candidate_classes(device_count: int, gbs: int):
-    """plan() candidate list (optimizer.cpp:288-293)."""
+    """plan() candidate list (optimizer.cpp:202-207)."""
     return [(pp, dp, tmp, mbs) for (pp, dp, tmp) in enumerate_degrees(device_count)
             for mbs in enumerate_mbs(gbs, dp)]

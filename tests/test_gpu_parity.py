@@ -205,23 +205,6 @@ def test_run_device_merge_and_partition_invariance():
     assert np.array_equal(merged["total"], whole["total"])
 
 
-def test_simulator_matches_reference():
-    if not B.ref_available():
-        pytest.skip("oracle/_ref not built")
-    from paper_2210_07297_b200 import simulator
-    for name in ("hetero_cluster", "hetero_model"):
-        sc = scenario(name)
-        enc = P.EncodedProblem.from_scenario(sc)
-        res = planner.plan(sc.model, sc.cluster, sc.profile, sc.gbs, P.PlanOptions(budget=0))
-        for c in res.candidates[:40]:
-            if c.failure:
-                continue
-            s = c.strategy
-            mine = simulator.simulate(s, sc.model, sc.cluster, sc.profile, sc.gbs, sc.options.cost_options, enc)
-            ref = B.ref_simulate(enc, s.pp, s.dp, s.tmp, s.mbs, s.placement, s.cut_boundaries)
-            assert mine == ref
-
-
 @pytest.mark.gpu
 @pytest.mark.parametrize("n_shards", [2, 3, 8])
 def test_class_slice_shards_merge_to_single_run(n_shards):
