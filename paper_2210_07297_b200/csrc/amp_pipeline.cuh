@@ -770,9 +770,12 @@ __global__ void __launch_bounds__(kEstWarps * 32, 3) k_est(EvalParams p) {
         }
       }
     }
+    // (the strategy survives the failures raised after it was assigned,
+    // optimizer.cpp:157-171: the parameter ceiling, the all-reduce bandwidth)
+    const bool has_strategy = ok || fc == AMP_FAIL_CEILING || fc == AMP_FAIL_ALLREDUCE_BANDWIDTH;
     if (p.all_cuts) {
       int32_t* o = p.all_cuts + w.out * (maxpp + 1);
-      for (int q = lane; q <= maxpp; q += 32) o[q] = (ok && q <= pp) ? cutsW[q] : -1;
+      for (int q = lane; q <= maxpp; q += 32) o[q] = (has_strategy && q <= pp) ? cutsW[q] : -1;
     }
     if (p.all_stage) {
       double* o = p.all_stage + w.out * maxpp;
@@ -795,7 +798,7 @@ __global__ void __launch_bounds__(kEstWarps * 32, 3) k_est(EvalParams p) {
     }
     if (p.all_place) {
       int32_t* o = p.all_place + w.out * D;
-      for (int x = lane; x < D; x += 32) o[x] = ok ? PL[x] : -1;
+      for (int x = lane; x < D; x += 32) o[x] = has_strategy ? PL[x] : -1;
     }
     __syncwarp();
   }

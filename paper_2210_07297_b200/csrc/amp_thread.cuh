@@ -755,9 +755,13 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
       rec.dpsync_time = ok ? dpsync : CUDART_NAN;
       rec.total = ok ? pipeline + dpsync : CUDART_NAN;
       if (p.all) p.all[w.out] = rec;
+      // the strategy (placement + DP cuts) is kept by the failures raised
+      // after evaluate_candidate assigned it (optimizer.cpp:157-171: the
+      // parameter ceiling, estimate's all-reduce bandwidth)
+      const bool has_strategy = ok || fc == AMP_FAIL_CEILING || fc == AMP_FAIL_ALLREDUCE_BANDWIDTH;
       if (p.all_cuts) {
         int32_t* o = p.all_cuts + w.out * (maxpp + 1);
-        for (int q = 0; q <= maxpp; ++q) o[q] = (ok && q <= pp) ? cuts[q] : -1;
+        for (int q = 0; q <= maxpp; ++q) o[q] = (has_strategy && q <= pp) ? cuts[q] : -1;
       }
       if (p.all_stage) {
         double* o = p.all_stage + w.out * maxpp;
@@ -781,7 +785,7 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
       }
       if (p.all_place) {
         int32_t* o = p.all_place + w.out * D;
-        for (int x = 0; x < D; ++x) o[x] = ok ? nib(perm, x) : -1;
+        for (int x = 0; x < D; ++x) o[x] = has_strategy ? nib(perm, x) : -1;
       }
     }
     // ---- warp top-k (rank_records key): lanes that pass the cheap check

@@ -141,14 +141,19 @@ PlanResult plan(const ModelGraph& model, const Cluster& cluster, const ProfileTa
     c.strategy.degrees = ParallelismDegrees{a.pp, a.dp, a.tmp};
     c.strategy.mbs = a.mbs;
     c.rank = (int)r + 1;
+    // evaluate_candidate assigns record.strategy before the parameter
+    // ceiling and estimate (optimizer.cpp:157-171): those two failures keep
+    // the placement and the DP cuts
+    if (a.fail_code == 0 || a.fail_code == AMP_FAIL_CEILING || a.fail_code == AMP_FAIL_ALLREDUCE_BANDWIDTH) {
+      c.strategy.placement = Placement(
+          c.strategy.degrees, std::vector<int>(place.begin() + i * D, place.begin() + (i + 1) * D));
+      c.strategy.assignment.cut_boundaries.assign(cuts.begin() + i * (max_pp + 1),
+                                                  cuts.begin() + i * (max_pp + 1) + a.pp + 1);
+    }
     if (a.fail_code != 0) {
       c.failure = failure_text(a, model.layer_count());
       continue;
     }
-    c.strategy.placement = Placement(
-        c.strategy.degrees, std::vector<int>(place.begin() + i * D, place.begin() + (i + 1) * D));
-    c.strategy.assignment.cut_boundaries.assign(cuts.begin() + i * (max_pp + 1),
-                                                cuts.begin() + i * (max_pp + 1) + a.pp + 1);
     c.estimated.total = a.total;
     c.estimated.pipeline_time = a.pipeline_time;
     c.estimated.dpsync_time = a.dpsync_time;
