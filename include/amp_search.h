@@ -241,14 +241,22 @@ int amp_search_evaluate_placed(amp_ctx* ctx, const int32_t* classes, const int32
                                const amp_details* details);
 int amp_search_run_device(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k,
                           amp_record* d_topk, void* stream);
-/* Shard `shard` of n_shards (multi-GPU): placements
- * [P*shard/n, P*(shard+1)/n) of EVERY class, so all shards carry the same
- * class mix; the union over shards is the whole space and the merged top-k
- * equals the single-GPU one.  Device-resident like amp_search_run_device.  */
+/* Shard `shard` of n_shards (multi-GPU; replaces the worker split of
+ * optimizer.cpp:212-229 across GPUs): every class is cut into min(P, n)
+ * contiguous placement blocks weighted by its work, and the blocks go
+ * longest-first to the least-loaded shard (deterministic).  With P >= n all
+ * shards carry the same class mix; with P = 1 (plan()) it is an LPT split
+ * of the uneven DP instances.  The union over shards is the whole space and
+ * the merged top-k equals the single-GPU one.  Device-resident like
+ * amp_search_run_device.                                                  */
 int amp_search_run_device_shard(amp_ctx* ctx, int32_t shard, int32_t n_shards, int32_t k,
                                 amp_record* d_topk, void* stream);
 /* Candidates in shard `shard` of n_shards. */
 uint64_t amp_search_shard_size(const amp_ctx* ctx, int32_t shard, int32_t n_shards);
+/* The shard's index ranges [ranges[2i], ranges[2i+1]) in its dispatch
+ * order; *n_ranges = their number (ranges may be NULL to query it).      */
+int amp_search_shard_ranges(const amp_ctx* ctx, int32_t shard, int32_t n_shards, uint64_t* ranges,
+                            int32_t cap, int32_t* n_ranges);
 
 /* Merge n_in device records — n_in / k lists of k records, each sorted by
  * the ranking key and padded at its end (e.g. the all-gathered per-GPU

@@ -166,7 +166,7 @@ oracle_ctx* oracle_create(const amp_problem* p, uint64_t placements_per_class, u
         c->cls[n][1] = dp;
         c->cls[n][2] = tmp;
         c->cls[n][3] = mv[q];
-        if (pp > c->max_pp) c->max_pp = pp;
+        if (pp <= c->L && pp > c->max_pp) c->max_pp = pp; /* (pp > L fails first) */
         ++n;
       }
     }

@@ -171,6 +171,7 @@ SIGNATURES = [
     ("amp_search_abi_version", C.c_int, []),
     ("amp_search_num_candidates", C.c_uint64, [C.c_void_p]),
     ("amp_search_num_classes", C.c_int32, [C.c_void_p]),
+    ("amp_search_shard_ranges", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, _u64p, C.c_int32, _ip]),
     ("amp_search_max_pp", C.c_int32, [C.c_void_p]),
     ("amp_search_class", C.c_int, [C.c_void_p, C.c_int32, _ip, _ip, _ip, _ip]),
     ("amp_search_partition", C.c_int, [C.c_void_p, C.c_int32, _u64p]),

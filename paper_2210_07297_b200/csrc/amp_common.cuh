@@ -185,6 +185,12 @@ struct EvalParams {
   // keys [*n_rep]; run only while *sig_guard != 0 (NULL: always)
   const uint64_t* sig_keys;
   const uint32_t* sig_guard;
+  // node-determined bandwidths (every link a function of its two nodes,
+  // symmetric): make_comm_group's pairwise minimum over the nodes present
+  // in the group instead of over its device pairs (warp K_est), or NULL
+  const int32_t* node_of;     // [D] dense node index of each device
+  const double* nodebw;       // [n_nodes][n_nodes] (diagonal: intra-node links)
+  int32_t n_nodes, node_words;  // node bitmap words (32 nodes each)
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

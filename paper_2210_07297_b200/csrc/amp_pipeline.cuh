@@ -504,6 +504,10 @@ __global__ void __launch_bounds__(kEstWarps * 32, 3) k_est(EvalParams p) {
   sp += sizeof(double) * 2 * maxpp * kEstWarps;
   int* cutsW = reinterpret_cast<int*>(sp) + wib * (maxpp + 2);
   sp += sizeof(int) * (maxpp + 2) * kEstWarps;
+  // node bitmaps of the node-pair all-reduce minimum: present, >= 2 devices
+  unsigned* nodeP = reinterpret_cast<unsigned*>(sp) + wib * 2 * p.node_words;
+  unsigned* nodeM = nodeP + p.node_words;
+  if (p.nodebw) sp += sizeof(unsigned) * 2 * p.node_words * kEstWarps;
   sp = smem_raw + ((sp - smem_raw + 15) & ~15);
   EstWarp* ew = reinterpret_cast<EstWarp*>(sp) + wib;
   sp += sizeof(EstWarp) * kEstWarps;
@@ -683,10 +687,41 @@ __global__ void __launch_bounds__(kEstWarps * 32, 3) k_est(EvalParams p) {
           for (int g = 0; g < ngroups; ++g) {
             const int j = g / tmp, s = g % tmp;
             double b = CUDART_INF;
-            for (int r1 = lane; r1 < dp; r1 += 32) {
-              const int d1 = PL[(j * dp + r1) * tmp + s];
-              for (int r2 = r1 + 1; r2 < dp; ++r2)
-                b = std_min(b, BW[(size_t)d1 * D + PL[(j * dp + r2) * tmp + s]]);
+            if (p.nodebw) {
+              // node-determined symmetric links: the minimum over the device
+              // pairs of the group (cost_model.cpp:23-38) equals the minimum
+              // over its node pairs plus the intra-node link of every node
+              // holding >= 2 of its devices (min is exact in any order)
+              const int NW = p.node_words, NN = p.n_nodes;
+              for (int x = lane; x < NW; x += 32) nodeP[x] = nodeM[x] = 0u;
+              __syncwarp();
+              for (int r = lane; r < dp; r += 32) {
+                const int n = p.node_of[PL[(j * dp + r) * tmp + s]];
+                const unsigned bit = 1u << (n & 31);
+                if (atomicOr(&nodeP[n >> 5], bit) & bit) atomicOr(&nodeM[n >> 5], bit);
+              }
+              __syncwarp();
+              for (int n1 = lane; n1 < NW * 32; n1 += 32) {
+                if (!((nodeP[n1 >> 5] >> (n1 & 31)) & 1u)) continue;
+                const double* row = p.nodebw + (size_t)n1 * NN;
+                if ((nodeM[n1 >> 5] >> (n1 & 31)) & 1u) b = std_min(b, row[n1]);
+                for (int w = n1 >> 5; w < NW; ++w) {
+                  unsigned m = nodeP[w];
+                  if (w == (n1 >> 5)) m &= (n1 & 31) == 31 ? 0u : ~((2u << (n1 & 31)) - 1u);
+                  while (m) {
+                    const int n2 = w * 32 + __ffs(m) - 1;
+                    m &= m - 1;
+                    b = std_min(b, row[n2]);
+                  }
+                }
+              }
+              __syncwarp();
+            } else {
+              for (int r1 = lane; r1 < dp; r1 += 32) {
+                const int d1 = PL[(j * dp + r1) * tmp + s];
+                for (int r2 = r1 + 1; r2 < dp; ++r2)
+                  b = std_min(b, BW[(size_t)d1 * D + PL[(j * dp + r2) * tmp + s]]);
+              }
             }
             for (int o = 16; o > 0; o >>= 1) b = std_min(b, __shfl_xor_sync(0xffffffffu, b, o));
             if (lane == 0) {

@@ -161,6 +161,8 @@ struct amp_ctx {
   int n_codes = 0;
   bool bw_positive = false;  // smallest distinct bandwidth > 0
   DevBuf bwcode, bwval, qtab, cellrec, cut2tab, rsum_t, rsum_p;
+  DevBuf node_of, nodebw;  // node-determined bandwidths (n_nodes > 0)
+  int n_nodes = 0;
   uint64_t n_heavy = 0;  // items of pp >= 3 classes in the current run's dispatch order
   // DP memoisation by signature (amp_dedup.cuh)
   bool dedup = false;
@@ -489,7 +491,7 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
         c.gas = p->gbs / (dp * mbs);
         c.pair = pr;
         ctx->classes.push_back(c);
-        ctx->max_pp = std::max(ctx->max_pp, pp);
+        if (pp <= L) ctx->max_pp = std::max(ctx->max_pp, pp);  // (pp > L fails before any stage)
       }
     }
   if (ctx->classes.empty()) return fail(ctx, AMP_E_INVALID, "no candidates");
@@ -574,6 +576,39 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
         ctx->n_codes = U;
         ctx->bw_positive = vals[0] > 0;
       }
+    }
+  }
+  // ---- node-determined bandwidths (every link a function of its two
+  //      nodes, symmetric, no NaN): the node-pair all-reduce minimum ------
+  {
+    std::vector<int> nodes(p->node_id, p->node_id + D);
+    std::sort(nodes.begin(), nodes.end());
+    nodes.erase(std::unique(nodes.begin(), nodes.end()), nodes.end());
+    const int NN = (int)nodes.size();
+    std::vector<int32_t> nof(D);
+    for (int a = 0; a < D; ++a)
+      nof[a] = (int32_t)(std::lower_bound(nodes.begin(), nodes.end(), p->node_id[a]) - nodes.begin());
+    bool ok = D > 32 && NN <= 4096 && std::getenv("AMP_NO_NODEBW") == nullptr;
+    std::vector<double> nb(ok ? (size_t)NN * NN : 0, NAN);
+    std::vector<uint8_t> set(ok ? (size_t)NN * NN : 0, 0);
+    for (int a = 0; a < D && ok; ++a)
+      for (int b = 0; b < D && ok; ++b) {
+        if (a == b) continue;
+        const double v = bw[(size_t)a * D + b];
+        const size_t x = (size_t)nof[a] * NN + nof[b];
+        if (std::isnan(v)) ok = false;
+        else if (!set[x]) { nb[x] = v; set[x] = 1; }
+        else if (!(nb[x] == v)) ok = false;
+      }
+    for (int n1 = 0; n1 < NN && ok; ++n1)
+      for (int n2 = n1 + 1; n2 < NN && ok; ++n2)
+        if (set[(size_t)n1 * NN + n2] && !(nb[(size_t)n1 * NN + n2] == nb[(size_t)n2 * NN + n1])) ok = false;
+    ctx->n_nodes = ok ? NN : 0;
+    if (ok) {
+      for (size_t x = 0; x < nb.size(); ++x)
+        if (!set[x]) nb[x] = INFINITY;  // (a node with one device: never read)
+      CK(upload(ctx->node_of, nof.data(), nof.size()));
+      CK(upload(ctx->nodebw, nb.data(), nb.size()));
     }
   }
   CK(upload(ctx->param, p->param_count, L));
@@ -1325,7 +1360,14 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   }
   const int D = ctx->D, mp = ctx->max_pp;
   const size_t place_smem = (D <= 32 ? (sizeof(double) + 1) * D * D : 0) + sizeof(int) * 32 * 8;
-  size_t est_smem = (D <= 32 ? sizeof(double) * D * D : 0) +
+  if (ctx->n_nodes > 0) {
+    ep.node_of = ctx->node_of.as<int32_t>();
+    ep.nodebw = ctx->nodebw.as<double>();
+    ep.n_nodes = ctx->n_nodes;
+    ep.node_words = (ctx->n_nodes + 31) / 32;
+  }
+  size_t est_smem = (ep.nodebw ? sizeof(unsigned) * 2 * ep.node_words * kEstWarps : 0) +
+                    (D <= 32 ? sizeof(double) * D * D : 0) +
                     sizeof(double) * 2 * mp * kEstWarps + sizeof(int) * (mp + 2) * kEstWarps;
   est_smem = ((est_smem + 15) & ~size_t(15)) + sizeof(EstWarp) * kEstWarps +
              (kk <= 32 ? sizeof(amp_record) * kk : 0);
@@ -1681,36 +1723,59 @@ int run_device_segs(amp_ctx* ctx, const std::vector<Segment>& segs, int32_t k, a
   return AMP_OK;
 }
 
-// Shard `shard` of n_shards: placements [P*shard/n, P*(shard+1)/n) of every
-// class, so every shard has the same class mix (weak-scaling balance by
-// construction); the union over shards is the whole space.
-std::vector<Segment> make_shard_segments(const amp_ctx* ctx, int32_t shard, int32_t n_shards) {
-  const uint64_t P = ctx->P;
-  const uint64_t p0 = P * (uint64_t)shard / (uint64_t)n_shards;
-  const uint64_t p1 = P * (uint64_t)(shard + 1) / (uint64_t)n_shards;
-  std::vector<std::pair<double, Segment>> v;
-  uint64_t out = 0;
+// Shards: every class is cut into min(P, n) contiguous placement blocks,
+// weighted by its per-candidate work (DP inner iterations of its pruned
+// program + a placement/estimate constant, as amp_search_partition), and
+// the blocks go longest-processing-time-first (by class weight, a class's
+// blocks together) to the least-loaded shard (ties: lowest shard).  With P >= n every shard gets one block of every
+// class (the same class mix); with P = 1 (the plan() space, e.g. C4's 440
+// uneven DP instances) it is LPT over the classes.  Deterministic: every
+// rank computes the same plan.  Mirrored by distributed.lpt_shards.
+std::vector<std::vector<Segment>> shard_plan(const amp_ctx* ctx, int32_t n_shards) {
+  struct Unit {
+    double w, wc;
+    uint64_t c, p0, p1;
+  };
+  const uint64_t P = ctx->P, nb = std::min<uint64_t>(P, (uint64_t)n_shards);
+  std::vector<Unit> units;
   for (uint64_t c = 0; c < ctx->classes.size(); ++c) {
-    if (p1 <= p0) break;
+    const double wc = ctx->class_inner[c] + 128.0 * ctx->D;
+    for (uint64_t b = 0; b < nb; ++b) {
+      const uint64_t p0 = P * b / nb, p1 = P * (b + 1) / nb;
+      if (p1 > p0) units.push_back(Unit{wc * (double)(p1 - p0), wc, c, p0, p1});
+    }
+  }
+  // longest first by the class weight, a class's blocks adjacent (stable)
+  std::stable_sort(units.begin(), units.end(), [](const Unit& a, const Unit& b) { return a.wc > b.wc; });
+  std::vector<double> load(n_shards, 0.0);
+  std::vector<std::vector<std::pair<double, Segment>>> v(n_shards);
+  for (const Unit& u : units) {
+    const int s = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+    load[s] += u.w;
     Segment sg{};
-    sg.first = c * P + p0;
-    sg.count = p1 - p0;
-    sg.out = out;
-    sg.p0 = p0;
-    sg.cls = (int64_t)c;
-    out += sg.count;
-    v.emplace_back(ctx->class_inner[c] + (is_heavy(ctx, c) ? 1e30 : 0.0), sg);
+    sg.first = u.c * P + u.p0;
+    sg.count = u.p1 - u.p0;
+    sg.p0 = u.p0;
+    sg.cls = (int64_t)u.c;
+    // dispatch order within a shard: pp >= 3 classes first, heaviest first
+    v[s].emplace_back(ctx->class_inner[u.c] + (is_heavy(ctx, u.c) ? 1e30 : 0.0), sg);
   }
-  std::stable_sort(v.begin(), v.end(),
-                   [](const auto& a, const auto& b) { return a.first > b.first; });
-  std::vector<Segment> segs;
-  uint64_t off = 0;
-  for (auto& e : v) {
-    e.second.offset = off;
-    off += e.second.count;
-    segs.push_back(e.second);
+  std::vector<std::vector<Segment>> out(n_shards);
+  for (int s = 0; s < n_shards; ++s) {
+    std::stable_sort(v[s].begin(), v[s].end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+    uint64_t off = 0;
+    for (auto& e : v[s]) {
+      e.second.offset = off;
+      e.second.out = off;
+      off += e.second.count;
+      out[s].push_back(e.second);
+    }
   }
-  return segs;
+  return out;
+}
+
+std::vector<Segment> make_shard_segments(const amp_ctx* ctx, int32_t shard, int32_t n_shards) {
+  return shard_plan(ctx, n_shards)[shard];
 }
 
 }  // namespace
@@ -2039,9 +2104,23 @@ int amp_search_run_device_shard(amp_ctx* ctx, int32_t shard, int32_t n_shards, i
 
 uint64_t amp_search_shard_size(const amp_ctx* ctx, int32_t shard, int32_t n_shards) {
   if (!ctx || n_shards < 1 || shard < 0 || shard >= n_shards) return 0;
-  const uint64_t P = ctx->P;
-  return ctx->classes.size() *
-         (P * (uint64_t)(shard + 1) / (uint64_t)n_shards - P * (uint64_t)shard / (uint64_t)n_shards);
+  uint64_t n = 0;
+  for (const Segment& sg : make_shard_segments(ctx, shard, n_shards)) n += sg.count;
+  return n;
+}
+
+int amp_search_shard_ranges(const amp_ctx* ctx, int32_t shard, int32_t n_shards, uint64_t* ranges,
+                            int32_t cap, int32_t* n_ranges) {
+  if (!ctx || n_shards < 1 || shard < 0 || shard >= n_shards || !n_ranges) return AMP_E_INVALID;
+  const auto segs = make_shard_segments(ctx, shard, n_shards);
+  *n_ranges = (int32_t)segs.size();
+  if (!ranges) return AMP_OK;
+  if (cap < (int32_t)segs.size()) return AMP_E_INVALID;
+  for (size_t i = 0; i < segs.size(); ++i) {
+    ranges[2 * i] = segs[i].first;
+    ranges[2 * i + 1] = segs[i].first + segs[i].count;
+  }
+  return AMP_OK;
 }
 
 int amp_search_merge_topk_device(amp_ctx* ctx, const amp_record* d_in, int32_t n_in, int32_t k,

@@ -2,11 +2,13 @@
 
 SURVEY.md §8(e): candidates are independent, so each rank evaluates its own
 part of the class-major index space and keeps its local top-k on the
-device.  Two splits: the per-class placement slice (`search_gpu_sharded`,
-amp_search_run_device_shard: rank r takes placements [P*r/n, P*(r+1)/n) of
-EVERY class, so every rank gets the same class mix — the bench's split) and
-the contiguous work-weighted index range (`search_gpu`,
-amp_search_partition).  The only
+device.  Two splits: the LPT shard plan (`search_gpu_sharded`,
+amp_search_run_device_shard, mirrored by `lpt_shards`: every class cut into
+min(P, n) placement blocks weighted by its work, longest first to the
+least-loaded rank — with P >= n every rank gets the same class mix, the
+bench's split; with P = 1 an LPT split of the plan() DP instances) and the
+contiguous work-weighted index range (`search_gpu`, amp_search_partition).
+The only
 exchange is one all-gather of the k records per rank (NCCL over NVLink on
 GPUs, gloo in the CPU tests) followed by a deterministic merge under the
 reference ranking key (failed, total, index) — identical for any world size.
@@ -78,11 +80,28 @@ def search_gpu_sharded(searcher, k: int, rank: int, world: int, group=None):
     return recs[recs["fail_code"] >= 0]
 
 
-def class_slice_ranges(n_classes: int, P: int, shard: int, n_shards: int) -> List[tuple]:
-    """Index ranges of shard `shard` in the per-class placement split (mirror
-    of amp_search_run_device_shard): [c*P + P*shard/n, c*P + P*(shard+1)/n)."""
-    p0, p1 = P * shard // n_shards, P * (shard + 1) // n_shards
-    return [(c * P + p0, c * P + p1) for c in range(n_classes) if p1 > p0]
+def lpt_shards(class_weights: Sequence[float], P: int, n_shards: int) -> List[List[tuple]]:
+    """The shard plan of amp_search_run_device_shard (amp_search.cu
+    shard_plan): each class c cut into min(P, n) placement blocks of weight
+    class_weights[c] * size, blocks longest-first (stable) to the
+    least-loaded shard (lowest on ties).  Returns each shard's index ranges
+    (in assignment order; the engine dispatches them heaviest class first)."""
+    nb = min(P, n_shards)
+    units = []
+    for c, wc in enumerate(class_weights):
+        for b in range(nb):
+            p0, p1 = P * b // nb, P * (b + 1) // nb
+            if p1 > p0:
+                units.append((wc * (p1 - p0), wc, c, p0, p1))
+    # longest first by the class weight, a class's blocks adjacent (stable)
+    units.sort(key=lambda u: -u[1])
+    load = [0.0] * n_shards
+    out: List[List[tuple]] = [[] for _ in range(n_shards)]
+    for w, _, c, p0, p1 in units:
+        s = min(range(n_shards), key=lambda r: (load[r], r))
+        load[s] += w
+        out[s].append((c * P + p0, c * P + p1))
+    return out
 
 
 def search_host(evaluate: Callable[[int, int], np.ndarray], k: int, bounds: Sequence[int], rank: int,

@@ -238,6 +238,15 @@ class Searcher:
                                                      C.c_void_p(d_topk_ptr), C.c_void_p(stream_ptr)),
                 self.ctx)
 
+    def shard_ranges(self, shard: int, n_shards: int):
+        """Index ranges of shard `shard` (the engine's LPT shard plan)."""
+        n = C.c_int32()
+        N.check(self.lib.amp_search_shard_ranges(self.ctx, shard, n_shards, None, 0, C.byref(n)), self.ctx)
+        r = np.zeros(2 * max(1, n.value), dtype=np.uint64)
+        N.check(self.lib.amp_search_shard_ranges(self.ctx, shard, n_shards, r.ctypes.data_as(N._u64p),
+                                                 n.value, C.byref(n)), self.ctx)
+        return [(int(r[2 * i]), int(r[2 * i + 1])) for i in range(n.value)]
+
     def shard_size(self, shard: int, n_shards: int) -> int:
         return int(self.lib.amp_search_shard_size(self.ctx, shard, n_shards))
 

@@ -352,10 +352,17 @@ def load_scenario(path: str) -> Scenario:
 def synthetic_c4() -> Scenario:
     """96-layer h=12288 transformer on 1024 GPUs
     (128 nodes x 8, three device types), gbs 512, analytic fallback."""
-    h, s, L = 12288, 2048, 96
+    return synthetic_cluster(128, 8, 96, 12288, 512, "synthetic96")
+
+
+def synthetic_cluster(nodes: int, per: int, L: int, h: int, gbs: int, name: str = "") -> Scenario:
+    """The C4 topology at any size: `nodes` x `per`
+    devices, node type = node mod 3, intra {900, 600, 300} GB/s, inter 50
+    GB/s (25 if either node is type 2); an L-layer h-wide transformer chain
+    (s = 2048) on the analytic fallback."""
+    s = 2048
     layers = [LayerSpec(i, "transformer", float(12 * h * h), float(72 * s * h * h)) for i in range(L)]
     model = ModelGraph(layers, [float(2 * s * h)] * (L - 1))
-    nodes, per = 128, 8
     D = nodes * per
     node = np.arange(D) // per
     ntype = node % 3
@@ -367,7 +374,7 @@ def synthetic_c4() -> Scenario:
     devices = [DeviceSpec(i, int(node[i]), ["b200", "h100", "a100"][int(ntype[i])]) for i in range(D)]
     opts = PlanOptions(cost_options=CostModelOptions(
         fallback=AnalyticFallback(True, 1e15, 900e9)))
-    return Scenario("synthetic96", model, Cluster(devices, bw), ProfileTable(), 512, opts)
+    return Scenario(name or f"synthetic{L}_d{D}", model, Cluster(devices, bw), ProfileTable(), gbs, opts)
 
 
 # --------------------------------------------------------------------------

@@ -50,7 +50,7 @@ def _worker(rank, world, port, bounds, k, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("split", ["even", "skewed", "class-slice"])
+@pytest.mark.parametrize("split", ["even", "skewed", "lpt", "lpt-p1"])
 def test_gloo_two_rank_merge_matches_single_process(tmp_path, split):
     from oracle import bindings as B
     from paper_2210_07297_b200 import distributed as Dd
@@ -63,8 +63,12 @@ def test_gloo_two_rank_merge_matches_single_process(tmp_path, split):
     recs, _ = o.run(0, n, threads=4, details=False)
     k = 12
     want = Dd.merge_topk_host(recs, k)
-    if split == "class-slice":  # the bench's split (amp_search_run_device_shard)
-        bounds = [Dd.class_slice_ranges(n // 6, 6, r, 2) for r in range(2)]
+    if split == "lpt":  # the engine's shard plan (amp_search_run_device_shard), uneven weights
+        w = [1.0 + (c % 7) * 3.5 for c in range(n // 6)]
+        bounds = Dd.lpt_shards(w, 6, 2)
+    elif split == "lpt-p1":  # P = 1 would be pure LPT over classes: blocks of one placement
+        w = [float((c * 37) % 11 + 1) for c in range(n)]
+        bounds = Dd.lpt_shards(w, 1, 2)
     else:
         bounds = [0, n // 2, n] if split == "even" else [0, 37, n]
     out = str(tmp_path / "top.npy")
@@ -72,3 +76,20 @@ def test_gloo_two_rank_merge_matches_single_process(tmp_path, split):
     got = np.load(out)
     assert got["index"].tolist() == want["index"].tolist()
     assert np.array_equal(got["total"], want["total"])
+
+
+def test_lpt_shards_cover_space_and_balance():
+    """The shard plan covers every index exactly once for any (P, n) and
+    balances the shards within the largest block, also for uneven
+    single-placement classes (P = 1: the C4 plan() case)."""
+    from paper_2210_07297_b200 import distributed as Dd
+    for n_cls, P_, n in [(70, 100, 8), (440, 1, 8), (35, 3, 4), (5, 1, 8), (12, 7, 3)]:
+        w = [float((c * 2654435761) % 1000 + 1) for c in range(n_cls)]
+        plan = Dd.lpt_shards(w, P_, n)
+        seen = np.zeros(n_cls * P_, dtype=np.int32)
+        for rngs in plan:
+            for lo, hi in rngs:
+                seen[lo:hi] += 1
+        assert (seen == 1).all()
+        loads = [sum(w[lo // P_] * (hi - lo) for lo, hi in r) for r in plan]
+        assert max(loads) - min(loads) <= max(w) * -(-P_ // n) + 1e-9  # greedy: <= the largest block

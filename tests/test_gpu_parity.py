@@ -206,19 +206,27 @@ def test_run_device_merge_and_partition_invariance():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n_shards", [2, 3, 8])
-def test_class_slice_shards_merge_to_single_run(n_shards):
-    """Per-class placement-slice shards (amp_search_run_device_shard, the
-    bench's multi-GPU split) cover the space exactly once and merge to the
+@pytest.mark.parametrize("name,P_,n_shards", [("hetero_cluster", 101, 2), ("hetero_cluster", 101, 3),
+                                              ("hetero_cluster", 101, 8), ("synthetic96", 1, 2),
+                                              ("synthetic96", 1, 4), ("synthetic96", 1, 8)])
+def test_lpt_shards_merge_to_single_run(name, P_, n_shards):
+    """The LPT shard plan (amp_search_run_device_shard, the multi-GPU split;
+    with P = 1 the C4 plan() space's 440 uneven DP instances) covers the
+    space exactly once and the shards' device top-k lists merge to the
     single-run top-k."""
     import torch
-    sc = scenario("hetero_cluster")
+    sc = scenario(name)
     enc = P.EncodedProblem.from_scenario(sc)
     k = 12
-    with planner.Searcher(enc, placements_per_class=101, seed=5) as s:
+    with planner.Searcher(enc, placements_per_class=P_, seed=5) as s:
         N_ = s.num_candidates
         whole, _, _ = s.run(0, N_, k=k)
         assert sum(s.shard_size(r, n_shards) for r in range(n_shards)) == N_
+        seen = np.zeros(N_, dtype=np.int32)
+        for r in range(n_shards):
+            for lo, hi in s.shard_ranges(r, n_shards):
+                seen[lo:hi] += 1
+        assert (seen == 1).all()
         st = torch.cuda.current_stream().cuda_stream
         parts = torch.empty((n_shards, k * 64), dtype=torch.uint8, device="cuda")
         for r in range(n_shards):
@@ -556,3 +564,49 @@ def test_trie_dp_stage_timing_and_counts():
     assert st["dp_fallback"] == 0
     assert st["dp_stage_launches"] == 1 and st["dp_stage_ms"] > 0  # one K_trie_dp per chunk
     assert st["dp_inner"] > 0 and st["fp64_ops"] == 7 * st["dp_inner"]
+
+
+LARGE_D = [(4, 8, 60), (8, 8, 24), (128, 8, 3)]  # (nodes, devices per node, P): |D| = 32, 64, 1024
+
+
+@pytest.mark.parametrize("nodes,per,P_", LARGE_D, ids=["D32", "D64", "D1024"])
+def test_large_cluster_sweep_matches_oracle_and_reference(nodes, per, P_):
+    """|D| > 16 (warp K_place / K_est, generic Fisher-Yates, coded boundary
+    minima, the node-pair all-reduce minimum, memoised signatures with 3-bit
+    codes and the trie at U = 8) on the C4 topology with a 24-layer model
+    and shuffled placements (P > 1): every record equals the memoised
+    oracle, the top-k is its ranking, a strided sample equals the compiled
+    reference (ref_sweep), and the pair-scan all-reduce (AMP_NO_NODEBW=1)
+    gives the same records."""
+    sc = P.synthetic_cluster(nodes, per, 24, 1024, 64)
+    enc = P.EncodedProblem.from_scenario(sc)
+    outs = []
+    for env in (None, "1"):
+        import os
+        if env:
+            os.environ["AMP_NO_NODEBW"] = env
+        try:
+            with planner.Searcher(enc, placements_per_class=P_, seed=5) as s:
+                top, allr, _ = s.run(0, s.num_candidates, k=10, want_all=True, details=False)
+                st = s.stats()
+        finally:
+            os.environ.pop("AMP_NO_NODEBW", None)
+        outs.append((top, allr, st))
+    assert np.array_equal(outs[0][1].view(np.uint8), outs[1][1].view(np.uint8))
+    allr = outs[0][1]
+    assert outs[0][2]["dp_instances"] > 0 and outs[0][2]["dp_fallback"] == 0
+    o = B.Oracle(enc, P_, 5)
+    orec, _ = o.run(threads=16, details=False, memo=True)
+    assert np.array_equal(allr["fail_code"], orec["fail_code"])
+    ok = orec["fail_code"] == 0
+    assert ok.any() and np.array_equal(allr["total"][ok], orec["total"][ok])
+    order = planner.rank_order(orec)[:10]
+    assert outs[0][0]["index"].tolist() == orec["index"][order].tolist()
+    if B.ref_available():
+        idx = np.arange(0, len(allr), max(1, len(allr) // 64), dtype=np.uint64)
+        rrec = B.ref_sweep_indices(enc, P_, 5, idx, 16, o.max_pp)
+        for r, i in zip(rrec, idx):
+            e = allr[int(i)]
+            assert int(r["fail_code"]) == int(e["fail_code"]), int(i)
+            if r["fail_code"] == 0:
+                assert r["total"] == e["total"], int(i)
