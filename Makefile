@@ -16,7 +16,7 @@ all: lib oracle
 lib: $(LIB)
 
 $(LIB): $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> $(PKG)/csrc/ptxas.log || (cat $(PKG)/csrc/ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) -lnccl 2> $(PKG)/csrc/ptxas.log || (cat $(PKG)/csrc/ptxas.log; exit 1)
 	@grep -E "Compiling entry|Used|spill" $(PKG)/csrc/ptxas.log | sed 's/^ptxas info *: //' | head -40
 
 oracle:

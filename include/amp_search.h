@@ -124,7 +124,13 @@ typedef struct amp_search_config {
   int32_t device;                /* CUDA device ordinal                     */
   int32_t max_ctas;              /* 0 = auto (resident CTAs on all SMs)     */
   int32_t flags;                 /* AMP_FLAG_*                              */
-  int32_t reserved;
+  int32_t n_gpus;                /* 0 / 1: one GPU; n > 1: devices device ..
+                                    device+n-1 driven by this one context
+                                    (a thread per GPU, NCCL all-gather of
+                                    the per-GPU top-k): amp_search_run
+                                    shards its range with the LPT plan of
+                                    amp_search_run_device_shard; the other
+                                    entry points use the first device       */
 } amp_search_config;
 
 /* One evaluated candidate: CandidateRecord minus the vectors

@@ -67,7 +67,7 @@ class AmpSearchConfig(C.Structure):
         ("device", C.c_int32),
         ("max_ctas", C.c_int32),
         ("flags", C.c_int32),
-        ("reserved", C.c_int32),
+        ("n_gpus", C.c_int32),
     ]
 
 

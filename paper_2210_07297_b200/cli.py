@@ -96,6 +96,8 @@ def _parser() -> argparse.ArgumentParser:
     p.add_argument("--max-params-per-device", type=float, default=0.0,
                    help="fail candidates whose per-device parameter count exceeds this")
     p.add_argument("--device", type=int, default=0, help="CUDA device (engine option)")
+    p.add_argument("--gpus", type=int, default=1,
+                   help="GPUs driven by the one engine context (devices --device .. +gpus-1)")
     b = sub.add_parser("baseline", help="Megatron-style heuristic candidates")
     _add_common(b)
     b.add_argument("--mode", default="layer-balance", choices=["layer-balance", "param-balance"])
@@ -128,7 +130,7 @@ def cmd_plan(a) -> int:
     opts = P.PlanOptions(budget=a.budget, workers=a.workers, cost_options=_cost_options(a),
                          max_params_per_device=a.max_params_per_device
                          if a.max_params_per_device > 0 else None)
-    res = planner.plan(model, cluster, profile, a.gbs, opts, device=a.device)
+    res = planner.plan(model, cluster, profile, a.gbs, opts, device=a.device, n_gpus=a.gpus)
     st = _abort_if_all_failed(res.candidates)
     if st:
         return st

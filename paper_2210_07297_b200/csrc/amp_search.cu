@@ -6,6 +6,7 @@
 // enumerates classes (integers), encodes the profile map into a dense cube,
 // and schedules work.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -16,6 +17,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <unordered_set>
 #include <vector>
@@ -163,6 +165,11 @@ struct amp_ctx {
   DevBuf bwcode, bwval, qtab, cellrec, cut2tab, rsum_t, rsum_p;
   DevBuf node_of, nodebw;  // node-determined bandwidths (n_nodes > 0)
   int n_nodes = 0;
+  // multi-GPU context (config n_gpus > 1): this context drives the first
+  // device, subs[r - 1] device + r; comms[r] is rank r's NCCL communicator
+  std::vector<amp_ctx*> subs;
+  std::vector<ncclComm_t> comms;
+  DevBuf gathered, mtopk;
   uint64_t n_heavy = 0;  // items of pp >= 3 classes in the current run's dispatch order
   // DP memoisation by signature (amp_dedup.cuh)
   bool dedup = false;
@@ -1731,17 +1738,21 @@ int run_device_segs(amp_ctx* ctx, const std::vector<Segment>& segs, int32_t k, a
 // class (the same class mix); with P = 1 (the plan() space, e.g. C4's 440
 // uneven DP instances) it is LPT over the classes.  Deterministic: every
 // rank computes the same plan.  Mirrored by distributed.lpt_shards.
-std::vector<std::vector<Segment>> shard_plan(const amp_ctx* ctx, int32_t n_shards) {
+std::vector<std::vector<Segment>> shard_plan(const amp_ctx* ctx, int32_t n_shards, uint64_t begin = 0,
+                                             uint64_t end = ~0ull) {
   struct Unit {
     double w, wc;
     uint64_t c, p0, p1;
   };
-  const uint64_t P = ctx->P, nb = std::min<uint64_t>(P, (uint64_t)n_shards);
+  const uint64_t P = ctx->P;
   std::vector<Unit> units;
-  for (uint64_t c = 0; c < ctx->classes.size(); ++c) {
+  for (uint64_t c = 0; c < ctx->classes.size(); ++c) {  // the class's part of [begin, end)
+    const uint64_t lo = std::max(begin, c * P), hi = std::min(end, (c + 1) * P);
+    if (hi <= lo) continue;
+    const uint64_t q0 = lo - c * P, n = hi - lo, nb = std::min<uint64_t>(n, (uint64_t)n_shards);
     const double wc = ctx->class_inner[c] + 128.0 * ctx->D;
     for (uint64_t b = 0; b < nb; ++b) {
-      const uint64_t p0 = P * b / nb, p1 = P * (b + 1) / nb;
+      const uint64_t p0 = q0 + n * b / nb, p1 = q0 + n * (b + 1) / nb;
       if (p1 > p0) units.push_back(Unit{wc * (double)(p1 - p0), wc, c, p0, p1});
     }
   }
@@ -1778,6 +1789,134 @@ std::vector<Segment> make_shard_segments(const amp_ctx* ctx, int32_t shard, int3
   return shard_plan(ctx, n_shards)[shard];
 }
 
+// amp_search_run on a multi-GPU context: the range's LPT shard plan, one
+// host thread per device evaluates its shard (K_place -> K_dp -> K_est, CTA
+// lists -> device top-k), an NCCL all-gather of the k records over NVLink,
+// the device merge on the first device; per-record outputs are copied from
+// each device to their host positions.  Identical to the single-GPU run.
+int run_multi(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k, amp_record* topk, int32_t* n_topk,
+              amp_record* all, const amp_details* det) {
+  const int n = (int)ctx->subs.size() + 1, kk = std::max(1, k);
+  const auto plan = shard_plan(ctx, n, begin, end);
+  const bool want_det = det && (det->cuts || det->stage_times || det->edge_times);
+  const bool want_place = det && det->placement, want_sim = all && det && det->simulated;
+  std::vector<int> rcs(n, AMP_OK);
+  auto dev_ctx = [&](int r) { return r == 0 ? ctx : ctx->subs[r - 1]; };
+  auto on_all = [&](auto&& fn) {  // fn(r) on a thread per device
+    std::vector<std::thread> th;
+    for (int r = 1; r < n; ++r) th.emplace_back([&, r]() { rcs[r] = fn(r); });
+    rcs[0] = fn(0);
+    for (auto& t : th) t.join();
+    for (int r = 0; r < n; ++r)
+      if (rcs[r] != AMP_OK) {
+        if (r) ctx->err = "device " + std::to_string(dev_ctx(r)->device) + ": " + dev_ctx(r)->err;
+        return rcs[r];
+      }
+    return (int)AMP_OK;
+  };
+  // ---- phase 1: every shard to a device top-k (+ per-record outputs) -----
+  int rc = on_all([&](int r) -> int {
+    amp_ctx* c = dev_ctx(r);
+    AllocStream g(c->stream);
+    CK(cudaSetDevice(c->device));
+    const std::vector<Segment>& segs = plan[r];
+    uint64_t nw = 0;
+    for (const Segment& sg : segs) nw += sg.count;
+    c->launches = 0;
+    CK(c->topk.ensure(sizeof(amp_record) * kk));
+    if (nw > 0) {
+      int e = launch_evaluate(c, &segs, nullptr, nw, kk, all != nullptr, want_det, want_place, nullptr, want_sim);
+      if (e) return e;
+      e = launch_merge(c, c->cta_topk.as<amp_record>(), kk * c->n_topk_lists, kk, c->topk.as<amp_record>(),
+                       c->stream);
+      if (e) return e;
+    } else {
+      std::vector<amp_record> pad(kk);
+      for (auto& x : pad) {
+        std::memset(&x, 0, sizeof x);
+        x.index = ~0ull;
+        x.fail_code = -1;
+        x.total = x.pipeline_time = x.dpsync_time = NAN;
+      }
+      CK(cudaMemcpyAsync(c->topk.p, pad.data(), sizeof(amp_record) * kk, cudaMemcpyHostToDevice, c->stream));
+    }
+    const int W = c->max_pp + 1, MP = c->max_pp, D = c->D;
+    for (const Segment& sg : segs) {  // this shard's records to their host positions
+      const uint64_t at = sg.first - begin;
+      if (all)
+        CK(cudaMemcpyAsync(all + at, c->o_all.as<amp_record>() + sg.out, sizeof(amp_record) * sg.count,
+                           cudaMemcpyDeviceToHost, c->stream));
+      if (det && det->cuts)
+        CK(cudaMemcpyAsync(det->cuts + at * W, c->o_cuts.as<int32_t>() + sg.out * W,
+                           sizeof(int32_t) * sg.count * W, cudaMemcpyDeviceToHost, c->stream));
+      if (det && det->stage_times)
+        CK(cudaMemcpyAsync(det->stage_times + at * MP, c->o_stage.as<double>() + sg.out * MP,
+                           sizeof(double) * sg.count * MP, cudaMemcpyDeviceToHost, c->stream));
+      if (det && det->edge_times)
+        CK(cudaMemcpyAsync(det->edge_times + at * MP, c->o_edge.as<double>() + sg.out * MP,
+                           sizeof(double) * sg.count * MP, cudaMemcpyDeviceToHost, c->stream));
+      if (det && det->placement)
+        CK(cudaMemcpyAsync(det->placement + at * D, c->o_place.as<int32_t>() + sg.out * D,
+                           sizeof(int32_t) * sg.count * D, cudaMemcpyDeviceToHost, c->stream));
+      if (want_sim)
+        CK(cudaMemcpyAsync(det->simulated + at, c->o_sim.as<double>() + sg.out, sizeof(double) * sg.count,
+                           cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(c->gathered.ensure(sizeof(amp_record) * kk * n));
+    CK(cudaStreamSynchronize(c->stream));
+    account(c, 0, 0, nullptr, 0, &segs);
+    resolve_kernel_times(c);
+    return AMP_OK;
+  });
+  if (rc) return rc;
+  // ---- phase 2: NCCL all-gather of the k records, merge on device 0 -------
+  rc = on_all([&](int r) -> int {
+    amp_ctx* c = dev_ctx(r);
+    CK(cudaSetDevice(c->device));
+    const ncclResult_t nr = ncclAllGather(c->topk.p, c->gathered.p, sizeof(amp_record) * kk, ncclUint8,
+                                          ctx->comms[r], c->stream);
+    if (nr != ncclSuccess) {
+      c->err = std::string("ncclAllGather: ") + ncclGetErrorString(nr);
+      return AMP_E_CUDA;
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return AMP_OK;
+  });
+  if (rc) return rc;
+  AllocStream g(ctx->stream);
+  CK(cudaSetDevice(ctx->device));
+  CK(ctx->mtopk.ensure(sizeof(amp_record) * kk));
+  rc = launch_merge(ctx, ctx->gathered.as<amp_record>(), kk * n, kk, ctx->mtopk.as<amp_record>(), ctx->stream);
+  if (rc) return rc;
+  std::vector<amp_record> tk(kk);
+  CK(cudaMemcpyAsync(tk.data(), ctx->mtopk.p, sizeof(amp_record) * kk, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  int cnt = 0;
+  for (int i = 0; i < k; ++i)
+    if (tk[i].fail_code >= 0) topk[cnt++] = tk[i];
+  if (n_topk) *n_topk = cnt;
+  // stats: work summed over the devices, times the slowest device's
+  amp_stats agg = ctx->stats;
+  for (amp_ctx* sub : ctx->subs) {
+    const amp_stats& o = sub->stats;
+    agg.candidates += o.candidates;
+    agg.dp_instances += o.dp_instances;
+    agg.dp_inner += o.dp_inner;
+    agg.fp64_ops += o.fp64_ops;
+    agg.dp_cells += o.dp_cells;
+    agg.dp_items += o.dp_items;
+    agg.launches += o.launches;
+    agg.place_ms = std::max(agg.place_ms, o.place_ms);
+    agg.dp_ms = std::max(agg.dp_ms, o.dp_ms);
+    agg.est_ms = std::max(agg.est_ms, o.est_ms);
+    agg.dp_stage_ms = std::max(agg.dp_stage_ms, o.dp_stage_ms);
+    agg.dp_fallback += o.dp_fallback;
+  }
+  agg.kernel_ms = agg.total_ms = std::max(agg.place_ms + agg.dp_ms + agg.est_ms, 0.0);
+  ctx->stats = agg;
+  return AMP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1795,7 +1934,42 @@ int amp_search_create(amp_ctx** out, const amp_problem* problem,
   }
   *out = nullptr;
   amp_ctx* ctx = new amp_ctx();
-  const int rc = setup(ctx, problem, config);
+  int rc = setup(ctx, problem, config);
+  const int n_gpus = config ? config->n_gpus : 1;
+  if (rc == AMP_OK && n_gpus > 1) {
+    // a context per further device (same problem, same candidate space),
+    // set up concurrently, and one NCCL communicator per device
+    std::vector<amp_ctx*> subs(n_gpus - 1, nullptr);
+    std::vector<int> rcs(n_gpus - 1, AMP_OK);
+    std::vector<std::thread> th;
+    for (int r = 1; r < n_gpus; ++r)
+      th.emplace_back([&, r]() {
+        amp_search_config c = *config;
+        c.device = config->device + r;
+        c.n_gpus = 1;
+        AllocStream g(nullptr);
+        subs[r - 1] = new amp_ctx();
+        rcs[r - 1] = setup(subs[r - 1], problem, &c);
+      });
+    for (auto& t : th) t.join();
+    ctx->subs = subs;
+    for (int r = 1; r < n_gpus && rc == AMP_OK; ++r)
+      if (rcs[r - 1] != AMP_OK) {
+        ctx->err = "device " + std::to_string(config->device + r) + ": " + subs[r - 1]->err;
+        rc = rcs[r - 1];
+      }
+    if (rc == AMP_OK) {
+      std::vector<int> devs(n_gpus);
+      for (int r = 0; r < n_gpus; ++r) devs[r] = config->device + r;
+      ctx->comms.assign(n_gpus, nullptr);
+      const ncclResult_t nr = ncclCommInitAll(ctx->comms.data(), n_gpus, devs.data());
+      if (nr != ncclSuccess) {
+        ctx->comms.clear();
+        ctx->err = std::string("ncclCommInitAll: ") + ncclGetErrorString(nr);
+        rc = AMP_E_CUDA;
+      }
+    }
+  }
   if (rc != AMP_OK) {
     g_last_error = ctx->err;
     amp_search_destroy(ctx);
@@ -1807,6 +1981,9 @@ int amp_search_create(amp_ctx** out, const amp_problem* problem,
 
 void amp_search_destroy(amp_ctx* ctx) {
   if (!ctx) return;
+  for (ncclComm_t c : ctx->comms)
+    if (c) ncclCommDestroy(c);
+  for (amp_ctx* sub : ctx->subs) amp_search_destroy(sub);
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -1892,6 +2069,7 @@ int amp_search_run(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k, amp_re
   const uint64_t n = end - begin;
   if (n_topk) *n_topk = 0;
   if (n == 0) return AMP_OK;
+  if (!ctx->subs.empty()) return run_multi(ctx, begin, end, k, topk, n_topk, all, all_details);
   const auto segs = make_segments(ctx, begin, end);
   const bool det = all_details && (all_details->cuts || all_details->stage_times ||
                                    all_details->edge_times);

@@ -101,12 +101,13 @@ void encode(const ModelGraph& model, const Cluster& cluster, const ProfileTable&
 }  // namespace
 
 PlanResult plan(const ModelGraph& model, const Cluster& cluster, const ProfileTable& profile,
-                int gbs, const PlanOptions& options, int device) {
+                int gbs, const PlanOptions& options, int device, int n_gpus) {
   Encoded e;
   encode(model, cluster, profile, gbs, options, e);
   amp_search_config cfg{};
   cfg.placements_per_class = 1;  // the plan() candidate list
   cfg.device = device;
+  cfg.n_gpus = n_gpus;  // > 1: one context drives the GPUs (LPT shards, NCCL all-gather)
   amp_ctx* ctx = nullptr;
   if (int rc = amp_search_create(&ctx, &e.p, &cfg); rc != AMP_OK)
     throw std::runtime_error(std::string("amp_search_create: ") + amp_last_error());

@@ -108,13 +108,13 @@ class Searcher:
 
     def __init__(self, problem: EncodedProblem, placements_per_class: int = 1, seed: int = 0,
                  device: int = 0, max_ctas: int = 0, dense_dp: bool = False,
-                 dedup: bool = True):
+                 dedup: bool = True, n_gpus: int = 1):
         self.lib = N.load()
         self.problem = problem
         cfg = N.AmpSearchConfig(int(placements_per_class), int(seed) & (2**64 - 1), int(device),
                                 int(max_ctas),
                                 (N.AMP_FLAG_DENSE_DP if dense_dp else 0) |
-                                (0 if dedup else N.AMP_FLAG_NO_DEDUP), 0)
+                                (0 if dedup else N.AMP_FLAG_NO_DEDUP), int(n_gpus))
         h = C.c_void_p()
         N.check(self.lib.amp_search_create(C.byref(h), problem.ref(), C.byref(cfg)))
         self.ctx = h
@@ -304,7 +304,7 @@ def rank_order(recs: np.ndarray) -> np.ndarray:
 
 def plan(model: ModelGraph, cluster: Cluster, profile: ProfileTable, gbs: int,
          options: Optional[PlanOptions] = None, device: int = 0, dense_dp: bool = False,
-         simulate_all: bool = False) -> PlanResult:
+         simulate_all: bool = False, n_gpus: int = 1) -> PlanResult:
     """parplan::plan on the GPU (optimizer.cpp:200-251).  simulate_all: also
     return every candidate's simulated time (result.simulated_all, in rank
     order) — acceptance criterion 5's rank agreement in one pass."""
@@ -318,7 +318,7 @@ def plan(model: ModelGraph, cluster: Cluster, profile: ProfileTable, gbs: int,
     if tm is not None:
         tm["encode"] = time.perf_counter() - t
         t = time.perf_counter()
-    with Searcher(enc, placements_per_class=1, device=device, dense_dp=dense_dp) as s:
+    with Searcher(enc, placements_per_class=1, device=device, dense_dp=dense_dp, n_gpus=n_gpus) as s:
         if tm is not None:
             tm["create"] = time.perf_counter() - t
             t = time.perf_counter()

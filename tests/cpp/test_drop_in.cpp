@@ -8,6 +8,7 @@
 // texts and best_index.  Exit status 0 on full agreement.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <string>
@@ -116,7 +117,10 @@ void compare(const PlanResult& a, const PlanResult& b, const char* tag) {
 
 }  // namespace
 
-int main() {
+int main(int argc, char** argv) {
+  // argv[1]: GPUs per context (the drop-in drives devices 0 .. n-1 itself)
+  const int n_gpus = argc > 1 ? std::atoi(argv[1]) : 1;
+  std::printf("n_gpus = %d\n", n_gpus);
   std::mt19937_64 g(2210);
   int worlds = 0;
   for (int trial = 0; trial < 24; ++trial) {
@@ -148,7 +152,7 @@ int main() {
         break;
     }
     const PlanResult ref = parplan::plan(model, cluster, profile, gbs, o);
-    const PlanResult gpu = parplan_gpu::plan(model, cluster, profile, gbs, o);
+    const PlanResult gpu = parplan_gpu::plan(model, cluster, profile, gbs, o, 0, n_gpus);
     char tag[64];
     std::snprintf(tag, sizeof tag, "world%d(L=%d,D=%d)", trial, L, devices);
     compare(gpu, ref, tag);

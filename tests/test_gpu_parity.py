@@ -610,3 +610,27 @@ def test_large_cluster_sweep_matches_oracle_and_reference(nodes, per, P_):
             assert int(r["fail_code"]) == int(e["fail_code"]), int(i)
             if r["fail_code"] == 0:
                 assert r["total"] == e["total"], int(i)
+
+
+@pytest.mark.parametrize("n_gpus", [2, 4])
+@pytest.mark.parametrize("name,P_", [("hetero_cluster", 3000), ("synthetic96", 1)])
+def test_multi_gpu_context_equals_single(name, P_, n_gpus):
+    """One context over n GPUs (config n_gpus: LPT shards, a thread per GPU,
+    NCCL all-gather + device merge, per-record outputs gathered to the
+    host) returns the records, details and top-k of the one-GPU run."""
+    import torch
+    if torch.cuda.device_count() < n_gpus:
+        pytest.skip(f"needs {n_gpus} GPUs")
+    sc = scenario(name)
+    enc = P.EncodedProblem.from_scenario(sc)
+    outs = []
+    for g in (1, n_gpus):
+        with planner.Searcher(enc, placements_per_class=P_, seed=3, n_gpus=g) as s:
+            top, allr, bufs = s.run(0, s.num_candidates, k=12, want_all=True, details=True)
+            top2, _, _ = s.run(s.num_candidates // 3, s.num_candidates, k=7)  # a sub-range
+        outs.append((top, allr, bufs, top2))
+    for a, b in zip(outs[0][:2], outs[1][:2]):
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
+    for key in ("cuts", "stage_times", "edge_times", "placement"):
+        assert np.array_equal(outs[0][2][key], outs[1][2][key], equal_nan=key != "cuts" and key != "placement"), key
+    assert np.array_equal(outs[0][3].view(np.uint8), outs[1][3].view(np.uint8))
