@@ -12,15 +12,23 @@ x P placements, N_PER_GPU candidates per GPU per step
 (weak scaling).  Inputs (problem tables) are resident in HBM; the per-step
 outputs are a k-record top-k.
 
+Roofline: the DP is the FP64 part of the path; its
+headline figure is 7 FP64 ops per executed (cell, cut) iteration of the
+memoised, prefix-shared DP over the CUDA-event time of the DP stage kernel
+(k_trie_dp), against the measured FP64 DADD peak.  The per-candidate
+kernels (K_place / K_est: integer placement shuffle + estimate) are reported
+by their HBM fraction and, secondarily, their issue-slot utilisation from
+the ncu counts of THIS build (profiles/<round>_kernel_counts.json, checked
+against the library's sha256; stale counts are dropped, not used).
+
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
-import math
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -34,13 +42,12 @@ SCENARIO = "hetero_cluster"
 DEFAULT_N_PER_GPU = 100_000_000
 TOPK = 10
 METRIC = "candidate strategies/sec"
-# ncu --set full of one k_dp_multi launch (profiles/r1b_k_dp_multi_ncu.txt):
-# dram__bytes_read.sum + dram__bytes_write.sum / candidates of that launch
-TRAFFIC_BYTES_PER_DP_ITEM = 66.5  # 66.54 MB over the 1,000,000 items of launch 3
-# ncu instructions / DRAM bytes per item of the per-candidate kernels on this
-# workload (tools/gpu_round.sh -> tools/summarize_profiles.py)
-KERNEL_COUNTS = os.path.join(ROOT, "profiles", "r1k_kernel_counts.json")
 UNIT = "candidates/s"
+LIB = os.path.join(ROOT, "paper_2210_07297_b200", "libamp_search.so")
+# ncu counts of this build's kernels on this workload (tools/profile_round.py)
+KERNEL_COUNTS = os.path.join(ROOT, "profiles", "r2_kernel_counts.json")
+SWEEP_N = [10_000, 100_000, 1_000_000, 10_000_000, 100_000_000, 1_000_000_000]
+CPU_FULL_MAX = 1_000_000  # the CPU arm runs the sweep in full up to here, then extrapolates
 
 
 def parse():
@@ -57,6 +64,7 @@ def parse():
     ap.add_argument("--no-dense", action="store_true", help="skip the dense-DP comparison leg")
     ap.add_argument("--no-wall-time", action="store_true",
                     help="skip the C1-C4 plan() wall-time leg (ours vs the reference)")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the configs[4] N sweep")
     return ap.parse_args()
 
 
@@ -72,10 +80,28 @@ def workload(n_per_gpu, world):
     return n_total, P_
 
 
+def lib_sha256():
+    h = hashlib.sha256()
+    with open(LIB, "rb") as f:
+        h.update(f.read())
+    return h.hexdigest()
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled through NVML every
     millisecond while the timed region runs (nvidia-smi's 100 ms loop would
-    see no sample of a ~25 ms region); nvidia-smi is the fallback."""
+    see no sample of a ~25 ms region)."""
 
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap"}
@@ -138,7 +164,7 @@ class ClockSampler:
                 "samples": len(self.rows), "source": "nvml, 1 ms"}
 
 
-def cpu_sample_indices(n_total, P_, sample):
+def cpu_sample_indices(n_total, sample):
     """Strided sample across the whole class-major range (all classes)."""
     stride = max(1, n_total // sample)
     return np.arange(0, n_total, stride, dtype=np.uint64)[:sample]
@@ -146,11 +172,12 @@ def cpu_sample_indices(n_total, P_, sample):
 
 def run_cpu_reference(sc, n_total, P_, sample, threads):
     """The reference's own CPU call chain (oracle/_ref, compiled from the
-    unmodified reference sources) over a bounded strided sample."""
+    unmodified reference sources) over a bounded strided sample, or over
+    the full range when sample >= n_total."""
     from oracle import bindings as B
     from paper_2210_07297_b200 import problem as P
     enc = P.EncodedProblem.from_scenario(sc)
-    idx = cpu_sample_indices(n_total, P_, sample)
+    idx = np.arange(n_total, dtype=np.uint64) if sample >= n_total else cpu_sample_indices(n_total, sample)
     max_pp = 16
     if B.ref_available():
         t0 = time.perf_counter()
@@ -158,9 +185,10 @@ def run_cpu_reference(sc, n_total, P_, sample, threads):
         dt = time.perf_counter() - t0
         kind = "reference"
     else:  # the plain-C port of the same path
+        from paper_2210_07297_b200.planner import RECORD_DTYPE
         o = B.Oracle(enc, P_, 0)
+        rec = np.zeros(1, dtype=RECORD_DTYPE)
         t0 = time.perf_counter()
-        rec = np.zeros(1, dtype=__import__("paper_2210_07297_b200.planner", fromlist=["x"]).RECORD_DTYPE)
         for i in idx:
             o.lib.oracle_evaluate(o.h, int(i), rec.ctypes.data_as(B._recp), None, None, None)
         dt = time.perf_counter() - t0
@@ -192,7 +220,7 @@ def reference_arm(args):
         "config": {"workload": f"{SCENARIO} sweep (C2 classes x placements)", "scenario": SCENARIO,
                    "candidates_per_step": n_total, "placements_per_class": P_,
                    "sample": f"{ns} strided candidates of the {n_total}-candidate space"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": th, "kind": kind,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": th, "kind": kind, "cpu": cpu_model(),
                          "sample": f"{ns} strided candidates, reference call chain "
                                    "(heuristic/shuffled placement, optimal_assignment, estimate)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -200,12 +228,13 @@ def reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
-def search_wall_time(budget=10):
+def search_wall_time(budget=10, runs=10, ref_runs_c4=5):
     """The metric's second half: AMP search wall time of plan() for C1-C4 —
     the drop-in (planner.plan: create from host arrays, K0/K0b, evaluate,
     rank, simulate the top `budget`) vs the reference parplan::plan
-    (oracle/_ref, all host threads), same inputs; the argmin and the whole
-    ranking must be identical."""
+    (oracle/_ref, all host threads), same inputs; median of `runs` after a
+    warm-up; the argmin and the whole ranking must be identical.  C4 also
+    reports its plan() phase times."""
     from oracle import bindings as B
     from paper_2210_07297_b200 import planner, problem as P
     out = {}
@@ -216,23 +245,31 @@ def search_wall_time(budget=10):
         opts = P.PlanOptions(budget=budget, cost_options=sc.options.cost_options,
                              max_params_per_device=sc.options.max_params_per_device)
         planner.plan(sc.model, sc.cluster, sc.profile, sc.gbs, opts)  # warm-up
-        ts = []
-        for _ in range(5 if tag != "C4" else 3):
+        ts, phases = [], []
+        for _ in range(runs):
+            tm = {}
             t0 = time.perf_counter()
-            res = planner.plan(sc.model, sc.cluster, sc.profile, sc.gbs, opts)
+            res = planner.plan(sc.model, sc.cluster, sc.profile, sc.gbs, opts, timing=tm)
             ts.append(time.perf_counter() - t0)
-        e = {"workload": name, "candidates": len(res.candidates), "budget": budget,
-             "ours_s": min(ts), "best": list(res.candidates[res.best_index].strategy.degrees)
-             if res.best_index >= 0 else None}
+            phases.append(tm)
+        e = {"workload": name, "candidates": len(res.candidates), "budget": budget, "runs": runs,
+             "ours_s": float(np.median(ts)), "ours_min_s": float(min(ts)),
+             "best": list(res.candidates[res.best_index].strategy.degrees) if res.best_index >= 0 else None}
+        if tag == "C4":
+            e["ours_phases_ms"] = {k: round(1e3 * float(np.median([p[k] for p in phases])), 3)
+                                   for k in phases[0]}
         if B.ref_available():
             enc = P.EncodedProblem.from_scenario(sc, opts)
             max_pp = max(c[0] for c in P.candidate_classes(sc.cluster.device_count(), sc.gbs))
             rs = []
-            for _ in range(3 if tag != "C4" else 1):
+            n_ref = ref_runs_c4 if tag == "C4" else runs
+            B.ref_plan(enc, max_pp, budget=budget, workers=os.cpu_count() or 1)  # warm-up
+            for _ in range(n_ref):
                 t0 = time.perf_counter()
                 r = B.ref_plan(enc, max_pp, budget=budget, workers=os.cpu_count() or 1)
                 rs.append(time.perf_counter() - t0)
-            e["reference_s"] = min(rs)
+            e["reference_s"] = float(np.median(rs))
+            e["reference_runs"] = n_ref
             e["reference_threads"] = os.cpu_count()
             e["same_argmin"] = bool(r["best_index"] == res.best_index)
             e["same_ranking"] = bool([int(x) for x in r["records"]["index"]] ==
@@ -246,10 +283,25 @@ def l2_flush(buf):
     buf.add_(1)  # write a buffer larger than L2 (126 MB)
 
 
+def kernel_counts():
+    """ncu counts of this build (None when absent or for another build)."""
+    try:
+        with open(KERNEL_COUNTS) as f:
+            kc = json.load(f)
+    except OSError:
+        return None, "absent"
+    if kc.get("lib_sha256") != lib_sha256():
+        return None, f"stale ({os.path.relpath(KERNEL_COUNTS, ROOT)} is for another build)"
+    return kc, os.path.relpath(KERNEL_COUNTS, ROOT)
+
+
 def our_arm(args):
+    import ctypes as C
+
     import torch
     import torch.distributed as dist
 
+    from paper_2210_07297_b200 import _native as N
     from paper_2210_07297_b200 import problem as P
     from paper_2210_07297_b200.planner import RECORD_DTYPE, Searcher
 
@@ -265,8 +317,8 @@ def our_arm(args):
     enc = P.EncodedProblem.from_scenario(sc)
     s = Searcher(enc, placements_per_class=P_, seed=0, device=local)
     # the whole class-major space (70 classes x P_ placements, >= n_total);
-    # rank r evaluates placements [P*r/N, P*(r+1)/N) of every class
-    # (amp_search_run_device_shard): every rank gets the same class mix
+    # rank r evaluates its LPT shard (amp_search_run_device_shard: one block
+    # of every class when P >= world)
     n_total = s.num_candidates
     n_mine = s.shard_size(rank, world)
     stream = torch.cuda.current_stream()
@@ -290,17 +342,16 @@ def our_arm(args):
     torch.cuda.synchronize()
     if distributed:
         dist.barrier()
-    times = []
-    kernel_ms = []
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
+    kstats = []
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             l2_flush(flush)
             ev[i][0].record(stream)
             step()
             ev[i][1].record(stream)
-            kernel_ms.append(s.stats())  # per-kernel events on the engine stream
+            kstats.append(s.stats())  # per-kernel events on the engine stream
         torch.cuda.synchronize()
     times = [a.elapsed_time(b) for a, b in ev]
     my_ms = float(sum(times))
@@ -311,62 +362,74 @@ def our_arm(args):
         dist.barrier()
     ms_per_step = my_ms / args.steps
     value = n_total / (ms_per_step * 1e-3)
-    st = s.stats()
+    st = kstats[-1]
     top = np.frombuffer(final.cpu().numpy().tobytes(), dtype=RECORD_DTYPE)
 
-    # ---- roofline of the dominant kernel (K1+K2 evaluate) ---------------
-    from paper_2210_07297_b200 import _native as N
-    import ctypes as C
+    # ---- rooflines ---------------------------------------------------------
     peak = C.c_double()
     pms = C.c_double()
     N.check(N.load().amp_fp64_peak(local, C.byref(peak), C.byref(pms)))
-    dp_ms = float(np.mean([x["dp_ms"] for x in kernel_ms]))
-    place_ms = float(np.mean([x["place_ms"] for x in kernel_ms]))
-    est_ms = float(np.mean([x["est_ms"] for x in kernel_ms]))
-    kern_ms = dp_ms
-    achieved = st["fp64_ops"] / (kern_ms * 1e-3) / 1e12
     peak_t = peak.value / 1e12
+    med = lambda key: float(np.median([x[key] for x in kstats]))  # noqa: E731
+    dp_stage_ms, dp_ms, place_ms, est_ms = med("dp_stage_ms"), med("dp_ms"), med("place_ms"), med("est_ms")
+    fp64 = st["fp64_ops"]  # 7 per executed (cell, cut) iteration, this step's DP (device counters)
+    ach_stage = fp64 / (dp_stage_ms * 1e-3) / 1e12
+    ach_span = fp64 / (dp_ms * 1e-3) / 1e12
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6537.0))
+    kc, kc_src = kernel_counts()
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    csum = clk.summary()
+    mhz = csum.get("sm_mhz") or csum.get("sm_max_mhz") or 1965.0
+    issue_peak = sms * 4 * mhz * 1e6
+
+    def counted(name, ms):
+        c = (kc or {}).get(name)
+        if not c:
+            return {}
+        per_launch = c["dram_bytes"] / c["launches"]
+        gbs = c["dram_bytes"] / c["runs"] / (ms * 1e-3) / 1e9
+        return {"traffic_per_launch": per_launch, "dram_gbs": gbs, "hbm_frac": gbs / hbm_peak,
+                "issue_frac": c["warp_inst"] / c["runs"] / (ms * 1e-3) / issue_peak,
+                "counts": kc_src}
+
+    k_dp = {"bound": "fp64", "kernel": "k_trie_dp (layer-partition DP, all stages: memoised by signature, "
+                                       "prefix-shared trie, smem-staged parent tables)",
+            "achieved": ach_stage, "peak": peak_t, "unit": "TFLOP/s", "frac": ach_stage / peak_t,
+            "ms_per_step": dp_stage_ms, "launches_per_step": int(st["dp_stage_launches"]),
+            "traffic": None,
+            "def": "7 FP64 ops per executed (cell, cut) iteration (SURVEY.md 8(d)), device-counted, over "
+                   "the CUDA-event time of k_trie_dp; peak = measured DADD throughput (amp_fp64_peak)"}
+    c = (kc or {}).get("k_trie_dp")
+    if c:
+        k_dp["traffic"] = c["dram_bytes"] / c["launches"]
+        k_dp["traffic_unit"] = "bytes per launch (ncu dram__bytes_read+write, " + kc_src + ")"
+    rooflines = {
+        "k_dp": k_dp,
+        "k_dp_span": {"bound": "fp64", "achieved": ach_span, "peak": peak_t, "unit": "TFLOP/s",
+                      "frac": ach_span / peak_t, "ms_per_step": dp_ms,
+                      "note": "the whole DP phase: signature list + trie build + k_trie_dp + backtrack + "
+                              "per-signature estimate"},
+        "k_est": dict({"bound": "hbm/issue", "ms_per_step": est_ms}, **counted("k_est_t", est_ms)),
+        "k_place": dict({"bound": "hbm/issue", "ms_per_step": place_ms}, **counted("k_place_t", place_ms)),
+    }
 
     # ---- e2e through the C-ABI with host buffers ------------------------
     e2e = None
     if not args.no_e2e:
         e2e = e2e_arm(args, enc, P_, n_total, world, rank, local, distributed)
 
-    dense = per_cand = None
+    dense = per_cand = sweep = None
     if world == 1 and not args.no_dense:
         dense = dense_leg(enc, local)
         per_cand = per_candidate_leg(enc, local, P_, n_total)
-
-    # ---- rooflines of the three kernels of a step ---------------------------
-    #   k_dp: FP64 pipe (algorithmic ops of the DP instances solved);
-    #   k_est / k_place: instruction issue (thread per candidate, integer and
-    #   FP64 mix) — ncu instructions per item x items / measured time, against
-    #   148 SMs x 4 warp-instructions/clk at the sampled SM clock
-    rooflines = {"k_dp": {"bound": "fp64", "achieved": achieved, "peak": peak_t,
-                          "unit": "TFLOP/s", "frac": achieved / peak_t, "ms_per_step": dp_ms}}
-    try:
-        with open(KERNEL_COUNTS) as f:
-            kc = json.load(f)
-    except OSError:
-        kc = {}
-    import torch
-    sms = torch.cuda.get_device_properties(local).multi_processor_count
-    csum = clk.summary() if hasattr(clk, "summary") else {}
-    mhz = csum.get("sm_mhz") or csum.get("sm_max_mhz") or 1965.0
-    issue_peak = sms * 4 * mhz * 1e6
-    # K_place_t covers the pp >= 3 classes (the pp <= 2 tail is placed in K_est)
-    cls_list = s.classes()
-    heavy = sum(1 for c in cls_list if c[0] >= 3) * (n_mine // len(cls_list))
-    for name, ms, items in (("k_est", est_ms, n_mine), ("k_place", place_ms, heavy)):
-        c = kc.get(name + "_t")
-        if not c or not items:
-            continue
-        ach = c["warp_inst_per_item"] * items / (ms * 1e-3)
-        rooflines[name] = {"bound": "issue", "achieved": ach, "peak": issue_peak,
-                           "unit": "warp-inst/s", "frac": ach / issue_peak, "ms_per_step": ms,
-                           "traffic": c["dram_bytes_per_item"] * items / max(1, st["dp_launches"]),
-                           "counts": os.path.relpath(KERNEL_COUNTS, ROOT)}
-    dominant = max(("k_dp", dp_ms), ("k_est", est_ms), ("k_place", place_ms), key=lambda t: t[1])[0]
+    if world == 1 and not args.no_sweep:
+        sweep = sweep_leg(sc, enc, local, args)
 
     if rank == 0:
         line = {
@@ -378,32 +441,24 @@ def our_arm(args):
                        "candidates_per_gpu": args.n_per_gpu, "placements_per_class": P_,
                        "topk": k, "l2": "flushed (256 MiB write) before every timed step",
                        "candidates_this_rank": n_mine,
-                       "parallelism": f"per-class placement-slice shards x{world} "
-                                      "(amp_search_run_device_shard), NCCL all-gather of the "
-                                      "k-record top-k + device merge"},
-            "roofline": dict(rooflines[dominant], kernel={
-                "k_est": "k_est_t (thread per candidate: pp<=2 placement + estimate, "
-                         "replica edges, dpsync, CTA top-k)",
-                "k_place": "k_place_t (thread per candidate: Fisher-Yates placement, "
-                           "boundary bandwidth codes)",
-                "k_dp": "memoised + prefix-shared layer-partition DP (dedup sort, trie stages)",
-            }[dominant], dominant_of=["k_place", "k_dp", "k_est"]),
+                       "parallelism": f"LPT shards x{world} (amp_search_run_device_shard), NCCL "
+                                      "all-gather of the k-record top-k + device merge"},
+            "roofline": rooflines["k_dp"],
             "rooflines": rooflines,
             "dp_detail": {
-                "traffic": TRAFFIC_BYTES_PER_DP_ITEM * st["dp_items"] / max(1, st["dp_launches"]),
-                "fp64_ops_def": "7 per executed inner iteration (SURVEY.md 8(d)) over the pruned "
-                                "program's iterations actually executed (memoised by signature, "
-                                "stage tables shared by code prefix)",
                 "dp_memoisation": {"candidates": n_total, "dp_instances_solved": st["dp_instances"]},
-                "pipeline_ms_per_step": {"k_place": place_ms, "k_dp": dp_ms, "k_est": est_ms},
-                "fp64_ops_per_step": st["fp64_ops"], "dp_inner_per_step": st["dp_inner"],
-                "peak_source": "measured live: amp_fp64_peak DADD throughput (no FP64 entry "
-                               "in MEASURED_PEAKS.json)"},
+                "pipeline_ms_per_step": {"k_place": place_ms, "k_dp_span": dp_ms, "k_dp_stage": dp_stage_ms,
+                                         "k_est": est_ms},
+                "fp64_ops_per_step": fp64, "dp_inner_per_step": st["dp_inner"],
+                "dp_fallback_chunks": st["dp_fallback"],
+                "peak_source": "measured live: amp_fp64_peak DADD throughput (MEASURED_PEAKS.json has "
+                               "no FP64 entry)"},
             "gpu_launches": int(args.steps * (st["launches"] + (1 if distributed else 0))),
             "best": {"index": int(top[0]["index"]), "total": float(top[0]["total"]),
                      "degrees": [int(top[0]["pp"]), int(top[0]["dp"]), int(top[0]["tmp"])],
                      "mbs": int(top[0]["mbs"])},
-            "clocks": clk.summary(),
+            "clocks": csum,
+            "lib_sha256": lib_sha256(),
         }
         if e2e:
             line["e2e"] = e2e
@@ -411,17 +466,64 @@ def our_arm(args):
             line["per_candidate_dp"] = per_cand
         if dense:
             line["dense_dp"] = dense
+        if sweep:
+            line["sweep"] = sweep
         if world == 1 and not args.no_wall_time:
             line["search_wall_time"] = search_wall_time()
         if world == 1 and not args.no_cpu_baseline:
-            v, dt, kind, th, ns = run_cpu_reference(sc, n_total, P_, args.cpu_sample, os.cpu_count() or 1)
-            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": th, "kind": kind,
+            th = os.cpu_count() or 1
+            v, dt, kind, th, ns = run_cpu_reference(sc, n_total, P_, args.cpu_sample, th)
+            v1, dt1, _, _, ns1 = run_cpu_reference(sc, n_total, P_, max(2000, args.cpu_sample // 40), 1)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": th, "kind": kind, "cpu": cpu_model(),
                                     "sample": f"{ns} strided candidates of the same sweep, "
-                                              f"{dt:.1f} s on {th} host threads"}
+                                              f"{dt:.1f} s on {th} host threads",
+                                    "one_thread": {"value": v1, "sample": f"{ns1} strided candidates, "
+                                                                          f"{dt1:.1f} s on 1 thread"}}
         print(json.dumps(line), flush=True)
     s.close()
     if distributed:
         dist.destroy_process_group()
+
+
+def sweep_leg(sc, enc, local, args):
+    """configs[4]: N in 1e4 .. 1e9 candidates (C2 classes x placements): the
+    device figure (one run's CUDA-event time, warm context), the e2e figure
+    (create from host arrays + run + host top-k + destroy, wall clock), and
+    the reference CPU path on all host threads — in full up to 1e6
+    candidates, a >= 1e6 prefix-equivalent strided sample beyond that,
+    labelled extrapolated."""
+    from paper_2210_07297_b200.planner import Searcher
+    out = []
+    th = os.cpu_count() or 1
+    cpu_rate = None
+    for n in SWEEP_N:
+        P_ = -(-n // 70)
+        with Searcher(enc, placements_per_class=P_, seed=0, device=local) as s:
+            s.run(0, n, k=TOPK)  # warm
+            ms = []
+            for _ in range(3 if n >= 10**9 else 5):
+                s.run(0, n, k=TOPK)
+                ms.append(s.stats()["total_ms"])
+        dev = float(np.median(ms))
+        walls = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            with Searcher(enc, placements_per_class=P_, seed=0, device=local) as s:
+                s.run(0, n, k=TOPK)
+            walls.append(time.perf_counter() - t0)
+        e = {"n": n, "placements_per_class": P_, "device_ms": dev, "device_value": n / (dev * 1e-3),
+             "e2e_s": float(np.median(walls)), "e2e_value": n / float(np.median(walls))}
+        if not args.no_cpu_baseline:
+            if n <= CPU_FULL_MAX:
+                v, dt, kind, thr, ns = run_cpu_reference(sc, n, P_, n, th)
+                cpu_rate = (v, kind, thr)
+                e["cpu"] = {"value": v, "s": dt, "kind": kind, "cores": thr, "measured": "full"}
+            else:
+                v, kind, thr = cpu_rate
+                e["cpu"] = {"value": v, "s": n / v, "kind": kind, "cores": thr,
+                            "measured": f"extrapolated from the full N={CPU_FULL_MAX} run's rate"}
+        out.append(e)
+    return {"points": out, "unit": UNIT, "workload": f"{SCENARIO}: 70 classes x P placements"}
 
 
 def per_candidate_leg(enc, local, P_, n):
@@ -486,7 +588,9 @@ def e2e_arm(args, enc, P_, n_total, world, rank, local, distributed):
     """Same metric through the public API per step, from HOST arrays to a
     HOST top-k: amp_search_create (H2D of the problem, K0 tables), the
     sharded run + NCCL all-gather + device merge (distributed.search_gpu_sharded),
-    the D2H of the k-record result, destroy — wall clock, max over ranks."""
+    the D2H of the k-record result, destroy — wall clock, max over ranks;
+    median of the timed steps after one warm-up step, the first (cold-context)
+    call reported separately."""
     import torch
     import torch.distributed as dist
 
@@ -496,7 +600,8 @@ def e2e_arm(args, enc, P_, n_total, world, rank, local, distributed):
     h2d = (enc.param.nbytes + enc.flops.nbytes + enc.flops_ok.nbytes + enc.act.nbytes +
            enc.node.nbytes + enc.bw.nbytes + enc.p_layer.nbytes * 3 + enc.p_sec.nbytes)
     d2h = k * 64
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, min(args.steps, 5))
+    walls = []
     for i in range(1 + steps):
         if distributed:
             dist.barrier()
@@ -505,20 +610,20 @@ def e2e_arm(args, enc, P_, n_total, world, rank, local, distributed):
         top = Dd.search_gpu_sharded(s, k, rank, world)
         s.close()
         dt = time.perf_counter() - t0
-        if i == 0:
-            continue  # warm-up
         if distributed:
             t = torch.tensor([dt], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
-        if i == 1:
-            best = dt
-        best = min(best, dt)
-    return {"value": n_total / best, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "s_per_step": best,
+        walls.append(dt)
+    med = float(np.median(walls[1:]))
+    return {"value": n_total / med, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "s_per_step": med, "steps": steps,
+            "first_call_s": walls[0],
             "best_index": int(top[0]["index"]) if len(top) else None,
             "note": "wall clock per step: amp_search_create (host arrays -> HBM, K0 tables) + "
-                    "sharded run + all-gather/merge + host top-k + destroy"}
+                    "sharded run + all-gather/merge + host top-k + destroy; median of the steps "
+                    "after the first (first_call_s: the first context of the measurement, in a "
+                    "process whose CUDA context and memory pool are already up)"}
 
 
 def main():

@@ -304,14 +304,16 @@ def rank_order(recs: np.ndarray) -> np.ndarray:
 
 def plan(model: ModelGraph, cluster: Cluster, profile: ProfileTable, gbs: int,
          options: Optional[PlanOptions] = None, device: int = 0, dense_dp: bool = False,
-         simulate_all: bool = False, n_gpus: int = 1) -> PlanResult:
+         simulate_all: bool = False, n_gpus: int = 1, timing: Optional[dict] = None) -> PlanResult:
     """parplan::plan on the GPU (optimizer.cpp:200-251).  simulate_all: also
     return every candidate's simulated time (result.simulated_all, in rank
-    order) — acceptance criterion 5's rank agreement in one pass."""
+    order) — acceptance criterion 5's rank agreement in one pass.  timing:
+    a dict filled with the host phase times (s): encode, create, run,
+    destroy, decode, simulate."""
     import os
     import time
 
-    tm = {} if os.environ.get("AMP_TIMING") else None
+    tm = timing if timing is not None else ({} if os.environ.get("AMP_TIMING") else None)
     t = time.perf_counter()
     options = options or PlanOptions()
     enc = EncodedProblem(model, cluster, profile, gbs, options)
@@ -357,5 +359,6 @@ def plan(model: ModelGraph, cluster: Cluster, profile: ProfileTable, gbs: int,
                                 for i, c in enumerate(cands)]
     if tm is not None:
         tm["simulate"] = time.perf_counter() - t
-        print("plan timing (ms):", {k: round(v * 1e3, 3) for k, v in tm.items()})
+        if timing is None:
+            print("plan timing (ms):", {k: round(v * 1e3, 3) for k, v in tm.items()})
     return result
