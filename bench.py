@@ -279,6 +279,40 @@ def search_wall_time(budget=10, runs=10, ref_runs_c4=5):
     return out
 
 
+def anneal_wall_time(iterations=200, seed=17, runs=5):
+    """the annealing chain (placement.cpp:299-398) —
+    ours (anneal.anneal: the chain on the host, every proposal's DP +
+    estimate on the GPU, speculative accept/reject branches batched per
+    call) vs the reference parplan::anneal (oracle/_ref), C1-C3, median of
+    `runs`; the initial and best costs must be identical."""
+    from oracle import bindings as B
+    from paper_2210_07297_b200 import anneal as A, problem as P
+    out = {}
+    for tag, name in {"C1": "homogeneous", "C2": "hetero_cluster", "C3": "hetero_model"}.items():
+        sc = P.load_scenario(os.path.join(ROOT, "tests", "golden", "scenarios", name + ".json"))
+        o = A.AnnealOptions(iterations=iterations, seed=seed, cost_options=sc.options.cost_options)
+        A.anneal(sc.model, sc.cluster, sc.profile, sc.gbs, o, simulate_top=False)  # warm-up
+        ts = []
+        for _ in range(runs):
+            t0 = time.perf_counter()
+            r = A.anneal(sc.model, sc.cluster, sc.profile, sc.gbs, o, simulate_top=False)
+            ts.append(time.perf_counter() - t0)
+        e = {"iterations": iterations, "ours_s": float(np.median(ts)), "initial_cost": r.initial_cost,
+             "best_cost": r.best_cost}
+        if B.ref_available():
+            enc = P.EncodedProblem.from_scenario(sc)
+            rs = []
+            for _ in range(runs):
+                t0 = time.perf_counter()
+                ic, bc, _ = B.ref_anneal(enc, iterations, seed)
+                rs.append(time.perf_counter() - t0)
+            e["reference_s"] = float(np.median(rs))
+            e["same_result"] = bool(ic == r.initial_cost and bc == r.best_cost)
+            e["speedup"] = e["reference_s"] / e["ours_s"]
+        out[tag] = e
+    return out
+
+
 def l2_flush(buf):
     buf.add_(1)  # write a buffer larger than L2 (126 MB)
 
@@ -470,6 +504,7 @@ def our_arm(args):
             line["sweep"] = sweep
         if world == 1 and not args.no_wall_time:
             line["search_wall_time"] = search_wall_time()
+            line["anneal_wall_time"] = anneal_wall_time()
         if world == 1 and not args.no_cpu_baseline:
             th = os.cpu_count() or 1
             v, dt, kind, th, ns = run_cpu_reference(sc, n_total, P_, args.cpu_sample, th)

@@ -78,6 +78,8 @@ def load_ref() -> C.CDLL:
             "ref_sweep_indices": (C.c_int, [C.POINTER(N.AmpProblem), C.c_uint64, C.c_uint64, _u64p, C.c_int64,
                                             C.c_int32, _recp, C.c_int32]),
             "ref_optimal_assignment": (C.c_int, [_dp, C.c_int32, C.c_int32, C.c_int32, _dp, _ip, _dp]),
+            "ref_anneal": (C.c_int, [C.POINTER(N.AmpProblem), C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
+                                     _dp, _dp, _ip]),
             "ref_brute_force": (C.c_int, [_dp, C.c_int32, C.c_int32, C.c_int32, _dp, _ip, _dp]),
             "ref_tolerance_domain": (C.c_int, [_dp, C.c_int32, _dp]),
             "ref_estimate": (C.c_int, [C.POINTER(N.AmpProblem), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
@@ -254,3 +256,14 @@ def ref_simulate(enc, pp, dp, tmp, mbs, placement, cuts):
                         C.byref(out)):
         raise ValueError("invalid strategy")
     return out.value
+
+
+def ref_anneal(enc, iterations: int, seed: int, budget: int = 10, record_all: bool = False):
+    """The reference anneal chain (parplan::anneal): (initial cost, best cost,
+    recorded states)."""
+    lib = load_ref()
+    ic, bc, nr = C.c_double(), C.c_double(), C.c_int32()
+    if lib.ref_anneal(enc.ref(), iterations, seed & (2**64 - 1), budget, int(record_all), C.byref(ic),
+                      C.byref(bc), C.byref(nr)):
+        raise RuntimeError("ref_anneal failed")
+    return ic.value, bc.value, nr.value

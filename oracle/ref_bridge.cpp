@@ -369,3 +369,30 @@ int ref_simulate(const amp_problem* p, int32_t pp, int32_t dp, int32_t tmp, int3
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// parplan::anneal on the problem (placement.cpp:299-398, the unmodified
+// reference chain): initial and best cost, recorded states; 0 on success,
+// -1 if the reference threw.
+int ref_anneal(const amp_problem* p, int32_t iterations, uint64_t seed, int32_t budget,
+               int32_t record_all, double* initial_cost, double* best_cost, int32_t* n_record) {
+  try {
+    World w = make_world(p);
+    AnnealOptions o;
+    o.iterations = iterations;
+    o.seed = seed;
+    o.budget = budget;
+    o.record_all = record_all != 0;
+    o.cost_options = w.cost;
+    const AnnealResult r = anneal(w.model, w.cluster, w.profile, w.gbs, o);
+    if (initial_cost) *initial_cost = r.initial_cost;
+    if (best_cost) *best_cost = r.best_cost;
+    if (n_record) *n_record = (int32_t)r.record.size();
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+}  // extern "C"

@@ -197,6 +197,32 @@ struct Engine {
   // (placement.cpp:252-259, cost_model.cpp:176-212).  Returns AMP_OK, an
   // engine error, or AMP_E_CANDIDATE with the failing record in `failed`
   // (the reference throws out of anneal there).
+  // Batch evaluation of speculative proposals: records (failures as data)
+  // and cuts for every entry; the caller decides which one was on the
+  // chain's path (the reference throws only there).
+  int evaluate_all(std::vector<Strat*>& v, std::vector<amp_record>& out) {
+    const int n = (int)v.size();
+    out.assign(n, amp_record{});
+    if (n == 0) return AMP_OK;
+    std::vector<int32_t> c(n), pl((size_t)n * D), cu((size_t)n * (max_pp + 1), -1);
+    for (int i = 0; i < n; ++i) {
+      auto it = cls.find({v[i]->deg.pp, v[i]->deg.dp, v[i]->deg.tmp, v[i]->mbs});
+      if (it == cls.end()) return AMP_E_INVALID;
+      c[i] = it->second;
+      std::copy(v[i]->place.begin(), v[i]->place.end(), pl.begin() + (size_t)i * D);
+    }
+    amp_details det{};
+    det.cuts = cu.data();
+    const int rc = amp_search_evaluate_placed(ctx, c.data(), pl.data(), nullptr, n, out.data(), &det);
+    if (rc != AMP_OK) return rc;
+    for (int i = 0; i < n; ++i) {
+      v[i]->est = out[i];
+      v[i]->cuts.assign(cu.begin() + (size_t)i * (max_pp + 1),
+                        cu.begin() + (size_t)i * (max_pp + 1) + v[i]->deg.pp + 1);
+    }
+    return AMP_OK;
+  }
+
   int evaluate(std::vector<Strat*>& v) {
     const int n = (int)v.size();
     if (n == 0) return AMP_OK;
@@ -354,44 +380,111 @@ extern "C" int amp_search_anneal(amp_ctx* ctx, const amp_problem* problem,
   };
   *initial_cost = current.est.total;
   if (record_state(current, 0, true) != AMP_OK) return AMP_E_INVALID;
+  // The chain, speculatively: the mt19937_64 stream is the same on the
+  // accept and the reject branch (the acceptance draw happens either way),
+  // and a proposal depends only on the current state and that stream — not
+  // on any cost.  So the proposals of every branch of the next `depth`
+  // iterations (a binary tree: accept / reject) are generated on the host
+  // first, evaluated in ONE batched GPU call (amp_search_evaluate_placed),
+  // and the chain then walks the tree with the real costs: bit-identical to
+  // the sequential chain, `depth` iterations per GPU round trip.
+  // AMP_ANNEAL_DEPTH (default 6; 1 = the sequential chain).
   double temperature = cfg->initial_temperature;
   const int n = P.D;
-  for (int i = 1; i <= cfg->iterations; ++i) {
-    temperature = std::max(temperature * cfg->cooling, cfg->min_temperature);
+  const char* dv = std::getenv("AMP_ANNEAL_DEPTH");
+  const int spec = std::max(1, std::min(12, dv ? std::atoi(dv) : 6));
+  struct Node {
+    Strat cur;                  // state entering the iteration (degrees, mbs, placement)
+    Rng rng_in, rng_out;        // the stream entering / leaving the iteration
+    std::optional<Strat> next;  // its proposal (none: every attempt failed)
+    double u = 0.0;             // the acceptance draw
+    int child[2] = {-1, -1};    // [reject, accept] (no proposal: child[0] only)
+  };
+  auto propose = [&](const Strat& cur, Rng& r) {  // placement.cpp:329-359
     std::optional<Strat> next;
     for (int attempt = 0; attempt < cfg->neighbor_retries && !next; ++attempt) {
-      Deg deg = current.deg;
-      if (rng.uniform() > 0.5) {
+      Deg deg = cur.deg;
+      if (r.uniform() > 0.5) {
         const auto choices = divisors(n / deg.dp);
-        deg.tmp = choices[rng.below(static_cast<int>(choices.size()))];
+        deg.tmp = choices[r.below(static_cast<int>(choices.size()))];
       } else {
         const auto choices = divisors(n / deg.tmp);
-        deg.dp = choices[rng.below(static_cast<int>(choices.size()))];
+        deg.dp = choices[r.below(static_cast<int>(choices.size()))];
       }
       deg.pp = n / (deg.dp * deg.tmp);
       if (deg.pp > P.L) continue;
       const auto mbs_options = enumerate_mbs(P.gbs, deg.dp);
       if (mbs_options.empty()) continue;
-      const int mbs = mbs_options[rng.below(static_cast<int>(mbs_options.size()))];
-      auto place = sample_placement(deg, grid, rng);
+      const int mbs = mbs_options[r.below(static_cast<int>(mbs_options.size()))];
+      auto place = sample_placement(deg, grid, r);
       if (!place) continue;
-      Strat s;
-      s.deg = deg;
-      s.mbs = mbs;
-      s.place = std::move(*place);
-      next = std::move(s);
+      Strat st;
+      st.deg = deg;
+      st.mbs = mbs;
+      st.place = std::move(*place);
+      next = std::move(st);
     }
-    if (!next) continue;  // keep the current state
-    std::vector<Strat*> one{&*next};
-    const int rc = E.evaluate(one);  // solve_candidate + estimate
+    return next;
+  };
+  for (int i = 1; i <= cfg->iterations;) {
+    const int depth = std::min(spec, cfg->iterations - i + 1);
+    std::vector<Node> tree;
+    tree.reserve((size_t)2 << depth);
+    tree.push_back(Node{current, rng, rng, std::nullopt});
+    std::vector<int> level{0};
+    for (int l = 0; l < depth; ++l) {
+      std::vector<int> nxt;
+      for (int id : level) {
+        Rng r = tree[id].rng_in;
+        std::optional<Strat> prop = propose(tree[id].cur, r);
+        if (prop) tree[id].u = r.uniform();  // drawn on both branches
+        tree[id].rng_out = r;
+        tree[id].next = std::move(prop);
+        if (l + 1 == depth) continue;
+        const Strat cur = tree[id].cur;
+        const std::optional<Strat> acc = tree[id].next;
+        tree[id].child[0] = (int)tree.size();
+        tree.push_back(Node{cur, r, r, std::nullopt});
+        nxt.push_back(tree[id].child[0]);
+        if (acc) {
+          tree[id].child[1] = (int)tree.size();
+          tree.push_back(Node{*acc, r, r, std::nullopt});
+          nxt.push_back(tree[id].child[1]);
+        }
+      }
+      level = std::move(nxt);
+    }
+    std::vector<Strat*> props;
+    for (Node& nd : tree)
+      if (nd.next) props.push_back(&*nd.next);
+    std::vector<amp_record> recs;
+    const int rc = E.evaluate_all(props, recs);  // solve_candidate + estimate, every branch
     if (rc != AMP_OK) return fail_out(rc);
-    const double acc_prob =
-        std::exp(std::min(current.est.total - next->est.total, 0.0) / temperature);
-    if (rng.uniform() < acc_prob) {
-      current = std::move(*next);
-      if (record_state(current, i, true) != AMP_OK) return AMP_E_INVALID;
-    } else if (cfg->record_all) {
-      if (record_state(*next, i, false) != AMP_OK) return AMP_E_INVALID;
+    // walk the tree with the real costs (placement.cpp:360-370)
+    int id = 0;
+    for (int l = 0; l < depth; ++l, ++i) {
+      temperature = std::max(temperature * cfg->cooling, cfg->min_temperature);
+      Node& nd = tree[id];
+      rng = nd.rng_out;
+      if (!nd.next) {  // keep the current state
+        if (l + 1 < depth) id = nd.child[0];
+        continue;
+      }
+      Strat& nx = *nd.next;
+      if (nx.est.fail_code != AMP_FAIL_NONE) {  // the reference throws here
+        E.failed = nx.est;
+        E.has_failed = true;
+        return fail_out(AMP_E_CANDIDATE);
+      }
+      const double acc_prob = std::exp(std::min(current.est.total - nx.est.total, 0.0) / temperature);
+      const bool accept = nd.u < acc_prob;
+      if (accept) {
+        current = nx;
+        if (record_state(current, i, true) != AMP_OK) return AMP_E_INVALID;
+      } else if (cfg->record_all) {
+        if (record_state(nx, i, false) != AMP_OK) return AMP_E_INVALID;
+      }
+      if (l + 1 < depth) id = nd.child[accept ? 1 : 0];
     }
   }
   *n_record = nrec;

@@ -191,6 +191,10 @@ struct EvalParams {
   const int32_t* node_of;     // [D] dense node index of each device
   const double* nodebw;       // [n_nodes][n_nodes] (diagonal: intra-node links)
   int32_t n_nodes, node_words;  // node bitmap words (32 nodes each)
+  // |D| = 16: placement of every placement index p < perm_n (k_perm_table),
+  // shared by the classes, or NULL
+  const uint64_t* perm_tab;
+  uint64_t perm_n;
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

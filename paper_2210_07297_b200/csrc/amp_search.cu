@@ -165,6 +165,8 @@ struct amp_ctx {
   DevBuf bwcode, bwval, qtab, cellrec, cut2tab, rsum_t, rsum_p;
   DevBuf node_of, nodebw;  // node-determined bandwidths (n_nodes > 0)
   int n_nodes = 0;
+  DevBuf perm_tab;         // placements of p in [0, perm_n) (|D| = 16), built on first use
+  uint64_t perm_n = 0;
   // multi-GPU context (config n_gpus > 1): this context drives the first
   // device, subs[r - 1] device + r; comms[r] is rank r's NCCL communicator
   std::vector<amp_ctx*> subs;
@@ -1409,10 +1411,30 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
       ep.sig_code_bits = ctx->code_bits;
     }
   }
+  // the placement table: the shuffle of placement p is the same for every
+  // class, so it is computed once per context (P placements) and read by
+  // K_place_t / K_est_t (AMP_NO_PERM_TAB=1: every candidate shuffles)
+  ep.perm_tab = nullptr;
+  ep.perm_n = 0;
+  if (thread_mode && ctx->D == 16 && !d_given_place && ctx->P > 1 && ctx->P <= (64ull << 20) &&
+      std::getenv("AMP_NO_PERM_TAB") == nullptr) {
+    if (ctx->perm_n != ctx->P) {
+      CK(ctx->perm_tab.ensure(sizeof(uint64_t) * ctx->P));
+      const int gp = (int)std::min<uint64_t>((ctx->P + 255) / 256, (uint64_t)ctx->sms * 8);
+      k_perm_table<<<gp, 256, 0, ctx->stream>>>(ep, ctx->perm_tab.as<uint64_t>(), ctx->P);
+      CK(cudaGetLastError());
+      DBG_SYNC("k_perm_table");
+      ctx->launches += 1;
+      ctx->perm_n = ctx->P;
+    }
+    ep.perm_tab = ctx->perm_tab.as<uint64_t>();
+    ep.perm_n = ctx->perm_n;
+  }
   // unrolled shape kernels in K_est_t: |D| == 16, every class a full
   // pp * dp * tmp == 16 shape, positive coded bandwidths, the range / 2-stage
   // tables, records only (AMP_NO_SHAPE=1 keeps the generic body)
-  bool shape16 = thread_mode && ctx->D == 16 && ep.bw_positive && std::getenv("AMP_NO_SHAPE") == nullptr;
+  bool shape16 = thread_mode && ctx->D == 16 && ep.bw_positive && std::getenv("AMP_NO_SHAPE") == nullptr &&
+                 (ctx->P == 1 || ep.perm_tab != nullptr) && !d_given_place;
   for (const auto& c : ctx->classes) shape16 = shape16 && c.pp * c.dp * c.tmp == 16;
   ep.est_fast = shape16 && est_thread && ep.cut2tab && ep.rsum_t && !ep.all_cuts && !ep.all_stage &&
                 !ep.all_edge && !ep.all_place && !d_given_cuts;

@@ -123,7 +123,11 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
   if (fc == 0 && !DECODE_ONLY) {
     // ---- placement: heuristic order (placement.cpp:37-49); p >= 1:
     //      Fisher-Yates driven by splitmix64(seed ^ p) ----------------------
-    if (p.given_place) {  // caller placement (anneal proposals, evaluate_placed)
+    if constexpr (FAST) {
+      // (the shape kernels run only with the placement table: P = 1 or the
+      //  table of every placement index; no per-candidate shuffle)
+      if (pl != 0 && (store || pp != 1 || dp != 1)) perm = p.perm_tab[pl];
+    } else if (p.given_place) {  // caller placement (anneal proposals, evaluate_placed)
       const int32_t* g = p.given_place + (p.t0 + u) * D;
       perm = 0;
       for (int x = 0; x < D; ++x) perm |= (uint64_t)g[x] << (4 * x);
@@ -131,6 +135,9 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
       // (a fused pp = dp = 1 item's estimate does not depend on where its
       //  single stage sits: no edges, no all-reduce group — the shuffle is
       //  skipped when nothing stores the placement)
+      if (p.perm_tab && pl < p.perm_n) {
+        perm = p.perm_tab[pl];  // the shuffle of placement pl, shared by every class
+      } else {
       uint64_t r = splitmix64(p.seed ^ pl);
       if (DT > 0) {
 #pragma unroll
@@ -150,6 +157,7 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
           perm ^= (x << (4 * kk)) | (x << (4 * jj));
           r = splitmix64(r);
         }
+      }
       }
     }
     if (store && p.placep) p.placep[u] = perm;
@@ -268,6 +276,38 @@ __global__ void AMP_PLACE_BOUNDS k_place_t(EvalParams p) {
     int code0;
     place_one<DT, FAST>(p, S, u, true, w, perm, code0, nullptr, &hint);
     if (!p.skip_work) p.work[u] = w;
+  }
+}
+
+// The placement of every placement index p in [0, n) as 16 x 4-bit
+// nibbles (p = 0 the heuristic order, p >= 1 its
+// Fisher-Yates shuffle driven by splitmix64(seed ^ p)).  It depends on p
+// only — not on the class — so K_place / K_est of every class read it here
+// instead of redoing the 15-step shuffle per candidate.  |D| = 16.
+__global__ void k_perm_table(EvalParams p, uint64_t* out, uint64_t n) {
+  __shared__ uint64_t base;
+  if (threadIdx.x == 0) {
+    uint64_t v = 0;
+    for (int x = 0; x < p.D; ++x) v |= (uint64_t)p.base_order[x] << (4 * x);
+    base = v;
+  }
+  __syncthreads();
+  for (uint64_t pl = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; pl < n;
+       pl += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t perm = base;
+    if (pl != 0) {
+      uint64_t r = splitmix64(p.seed ^ pl);
+#pragma unroll
+      for (int kk = 15; kk >= 1; --kk) {
+        const uint32_t d = (uint32_t)kk + 1u;
+        const uint32_t t32 = (uint32_t)(0x100000000ull % d);
+        const uint32_t jj = (uint32_t)((((uint32_t)(r >> 32) % d) * t32 + ((uint32_t)r % d)) % d);
+        const uint64_t x = ((perm >> (4 * kk)) ^ (perm >> (4 * jj))) & 0xf;
+        perm ^= (x << (4 * kk)) | (x << (4 * jj));
+        r = splitmix64(r);
+      }
+    }
+    out[pl] = perm;
   }
 }
 

@@ -635,3 +635,28 @@ def test_multi_gpu_context_equals_single(name, P_, n_gpus):
     for key, v in outs[0][2].items():
         assert np.array_equal(v, outs[1][2][key], equal_nan=v.dtype.kind == "f"), key
     assert np.array_equal(outs[0][3].view(np.uint8), outs[1][3].view(np.uint8))
+
+
+@pytest.mark.parametrize("name,seed,record_all", [("homogeneous", 3, False), ("hetero_cluster", 17, True),
+                                                  ("hetero_model", 101, False)])
+def test_speculative_anneal_equals_sequential_and_reference(name, seed, record_all, monkeypatch):
+    """the batched anneal (accept / reject branches of the
+    next iterations evaluated in one GPU call, AMP_ANNEAL_DEPTH) walks the
+    same chain as the sequential one (depth 1) — every recorded state,
+    iteration and acceptance — and its initial / best costs equal the
+    reference parplan::anneal's."""
+    from paper_2210_07297_b200 import anneal as A
+    sc = scenario(name)
+    o = A.AnnealOptions(iterations=150, seed=seed, record_all=record_all, cost_options=sc.options.cost_options)
+    runs = []
+    for depth in ("1", "4", "9"):
+        monkeypatch.setenv("AMP_ANNEAL_DEPTH", depth)
+        runs.append(A.anneal(sc.model, sc.cluster, sc.profile, sc.gbs, o, simulate_top=False))
+    monkeypatch.delenv("AMP_ANNEAL_DEPTH", raising=False)
+    key = lambda r: [(e.iteration, e.accepted, e.strategy.placement, e.strategy.cut_boundaries,  # noqa: E731
+                      e.estimated.total) for e in r.record]
+    assert key(runs[0]) == key(runs[1]) == key(runs[2])
+    if B.ref_available():
+        enc = P.EncodedProblem.from_scenario(sc)
+        ic, bc, nrec = B.ref_anneal(enc, 150, seed, record_all=record_all)
+        assert (ic, bc, nrec) == (runs[0].initial_cost, runs[0].best_cost, len(runs[0].record))

@@ -87,8 +87,8 @@ for r in data:
     c = counts.setdefault(k, {"launches": 0, "runs": 1, "duration_ms": 0.0, "dram_bytes": 0.0,
                               "warp_inst": 0.0, "fp64_pipe_pct": []})
     c["launches"] += 1
-    c["duration_ms"] += num(r, "gpu__time_duration.sum") / 1e6 if units[ix["gpu__time_duration.sum"]] == "ns" \
-        else num(r, "gpu__time_duration.sum") / 1e3
+    c["duration_ms"] += num(r, "gpu__time_duration.sum") * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
+                                                             "second": 1e3}.get(units[ix["gpu__time_duration.sum"]], 1e-6)
     mul = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         c["dram_bytes"] += num(r, m) * mul.get(units[ix[m]], 1)
