@@ -484,7 +484,7 @@ struct EstWarp {
   int place[32];
 };
 
-__global__ void __launch_bounds__(kEstWarps * 32, 3) k_est(EvalParams p) {
+__global__ void __launch_bounds__(kEstWarps * 32, 2) k_est(EvalParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int lock;
   __shared__ int n_top;

@@ -519,7 +519,7 @@ constexpr int kEstTWarps = 8;
 
 template <int DT, bool FAST = false>
 #ifndef AMP_EST_MINB
-#define AMP_EST_MINB 4
+#define AMP_EST_MINB 3
 #endif
 __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalParams p) {
   __shared__ PlaceSmem PS;
@@ -551,7 +551,8 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
   // from the previous chunk (an item that cannot beat it cannot reach the
   // CTA's top-k), else nothing (w_kf = 2).  The exact key (index included)
   // matters: a chunk of failing candidates would otherwise pass every item.
-  int w_n = 0, w_kf = 2;
+  int w_kf = 2;  // (the warp list's count lives in wcount[wib]: one register less)
+  if (lane == 0) wcount[wib] = 0;
   double w_kt = CUDART_INF;
   uint64_t w_ki = ~0ull;
   if (p.k > 0 && n_top == p.k) {
@@ -844,21 +845,20 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
         while (m) {
           const int b = __ffs(m) - 1;
           m &= m - 1;
-          topk_insert(wtop[wib], w_n, p.k, stage_rec[wib][b]);
+          topk_insert(wtop[wib], wcount[wib], p.k, stage_rec[wib][b]);
         }
-        if (w_n == p.k) {
+        if (wcount[wib] == p.k) {
           w_kf = wtop[wib][p.k - 1].fail_code != 0;
           w_kt = wtop[wib][p.k - 1].total;
           w_ki = wtop[wib][p.k - 1].index;
         }
       }
-      w_n = __shfl_sync(0xffffffffu, w_n, 0);
       w_kf = __shfl_sync(0xffffffffu, w_kf, 0);
       w_kt = __shfl_sync(0xffffffffu, w_kt, 0);
       w_ki = __shfl_sync(0xffffffffu, w_ki, 0);
     }
   }
-  if (lane == 0) wcount[wib] = w_n;
+  __syncwarp();
   __syncthreads();
   if (threadIdx.x == 0 && p.k > 0) {  // CTA list (+ the persisted one) <- warp lists
     int n = n_top;
