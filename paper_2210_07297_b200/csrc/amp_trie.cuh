@@ -66,6 +66,21 @@ struct TrieStage {
   uint32_t wide;    // 1: groups of 4 nodes, per-node smem columns; 0: node per thread
 };
 
+// Value-table row stride (doubles) of a stage of n cells: whole 128-byte
+// lines, so no L1 line spans two nodes' rows — a row is read (through L1,
+// by cp.async) only after the run that wrote it is published, and no SM can
+// hold a stale copy of it from an earlier read of a neighbouring row.
+__host__ __device__ inline uint32_t vrow(uint32_t n) { return (n + 15u) & ~15u; }
+
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 struct TrieTile {   // one K_trie_dp work item
   uint32_t n0;      // first node (local id at depth d)
   uint32_t run;     // node run within (d, c)
@@ -215,7 +230,7 @@ __device__ void plan_level(const TrieParams& p, int d, uint32_t total, uint64_t 
       // few node runs (the upper levels): cut the cells into chunks (>= 32
       // cells) so the level still spreads over the GPU
       if (ts.wide && runs < 64) chunks = min((64 + runs - 1) / runs, (ts.n + 31) / 32);
-      if (d < p.cls[c].pp - 1) vs = (unsigned long long)K * ts.n;  // leaves keep argmins only
+      if (d < p.cls[c].pp - 1) vs = (unsigned long long)K * vrow(ts.n);  // leaves keep argmins only
       bs = (unsigned long long)K * ts.n;
     }
     nx[c] = chunks;
@@ -429,7 +444,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_trie_build(TrieParams p) {
 template <bool SINGLE>
 __device__ __forceinline__ void tile_wide(const TrieParams& p, const double* __restrict__ sV,
                                           const double* __restrict__ sE, const double* __restrict__ sPf,
-                                          int TNst, int G, int x0, int x1, int Nj, int j, int nn,
+                                          int TNst, int G, int x0, int x1, int Nj, int VS, int j, int nn,
                                           const TrieStage& ts, const uint16_t* __restrict__ pr,
                                           const double* __restrict__ dom, double g1, bool leaf,
                                           double* __restrict__ vout, uint8_t* __restrict__ bpo,
@@ -479,9 +494,8 @@ __device__ __forceinline__ void tile_wide(const TrieParams& p, const double* __r
     for (int b = 0; b < 4; ++b) {
       const int ln = 4 * g + b;
       if (ln >= nn) break;
-      const uint64_t o = (uint64_t)ln * Nj + x;
-      if (!leaf) vout[o] = bs[b];
-      bpo[o] = (uint8_t)cs[b];
+      if (!leaf) vout[(uint64_t)ln * VS + x] = bs[b];
+      bpo[(uint64_t)ln * Nj + x] = (uint8_t)cs[b];
     }
   }
 }
@@ -491,7 +505,7 @@ __device__ __forceinline__ void tile_wide(const TrieParams& p, const double* __r
 // parent, odd stride), sE the class's edge rows per code (row code).
 __device__ __forceinline__ void tile_narrow(const TrieParams& p, const double* __restrict__ sV,
                                             const double* __restrict__ sE, const double* __restrict__ sPf,
-                                            const int* __restrict__ sNode, int Pst, int Nj, int j, int nn,
+                                            const int* __restrict__ sNode, int Pst, int Nj, int VS, int j, int nn,
                                             const TrieStage& ts, const uint16_t* __restrict__ pr,
                                             const double* __restrict__ dom, double g1, bool leaf,
                                             double* __restrict__ vout, uint8_t* __restrict__ bpo,
@@ -520,9 +534,8 @@ __device__ __forceinline__ void tile_narrow(const TrieParams& p, const double* _
         bc = cut;
       }
     }
-    const uint64_t o = (uint64_t)ln * Nj + x;
-    if (!leaf) vout[o] = best;
-    bpo[o] = (uint8_t)bc;
+    if (!leaf) vout[(uint64_t)ln * VS + x] = best;
+    bpo[(uint64_t)ln * Nj + x] = (uint8_t)bc;
   }
 }
 
@@ -549,7 +562,7 @@ __global__ void __launch_bounds__(kTrieThreads, 4) k_trie_dp(TrieParams p) {
     const ClassDev cl = p.cls[c];
     const TrieStage ts = p.tstage[(size_t)c * P1 + j];
     const TrieStage tp = p.tstage[(size_t)c * P1 + j - 1];
-    const int Np = (int)tp.n, Nj = (int)ts.n;
+    const int Np = (int)tp.n, Nj = (int)ts.n, VS = (int)vrow(ts.n), VSp = (int)vrow(tp.n);
     const uint64_t noff = p.st->node_off[d];
     const uint32_t nbc = p.nb[(size_t)d * NC + c];
     const bool leaf = d == cl.pp - 1;
@@ -575,7 +588,7 @@ __global__ void __launch_bounds__(kTrieThreads, 4) k_trie_dp(TrieParams p) {
     const double* qt = p.qtab + (size_t)c * p.n_codes * L;
     const ProgDev pg = p.progs[p.class_prog[c]];
     const double* dom = p.domain + (size_t)cl.pair * p.nv_stride;
-    double* vout = p.varena + (leaf ? 0 : p.vbase[(size_t)d * NC + c] + (uint64_t)(tl.n0 - nbc) * Nj);
+    double* vout = p.varena + (leaf ? 0 : p.vbase[(size_t)d * NC + c] + (uint64_t)(tl.n0 - nbc) * VS);
     uint8_t* bpo = p.bparena + p.bbase[(size_t)d * NC + c] + (uint64_t)(tl.n0 - nbc) * Nj;
     const double g1 = (double)(cl.gas - 1);
     if (ts.wide) {
@@ -589,8 +602,8 @@ __global__ void __launch_bounds__(kTrieThreads, 4) k_trie_dp(TrieParams p) {
       } else {
         for (int ln = warp; ln < TW; ln += nw) {
           const int lr = ln < nn ? ln : 0;  // padding columns repeat node 0
-          const double* src = p.varena + vbp + (uint64_t)(p.npar[noff + tl.n0 + lr] - pnb) * Np;
-          for (int x = lane; x < Np; x += 32) sV[x * TNst + ln] = __ldcg(src + x);
+          const double* src = p.varena + vbp + (uint64_t)(p.npar[noff + tl.n0 + lr] - pnb) * VSp;
+          for (int x = lane; x < Np; x += 32) cp_async8(sV + x * TNst + ln, src + x);
         }
       }
       for (int ln = warp; ln < TW; ln += nw) {
@@ -599,12 +612,13 @@ __global__ void __launch_bounds__(kTrieThreads, 4) k_trie_dp(TrieParams p) {
         for (int r = lane; r < ER; r += 32) sE[r * TNst + ln] = er[r];
       }
       for (int x = tid; x < LP; x += blockDim.x) sPf[x] = p.prefix[(size_t)cl.pair * LP + x];
+      cp_async_wait_all();
       __syncthreads();
       if (single)
-        tile_wide<true>(p, sV, sE, sPf, TNst, G, tl.x0, tl.x1, Nj, j, nn, ts, p.preds + pg.pred_base, dom,
+        tile_wide<true>(p, sV, sE, sPf, TNst, G, tl.x0, tl.x1, Nj, VS, j, nn, ts, p.preds + pg.pred_base, dom,
                         g1, leaf, vout, bpo, mine);
       else
-        tile_wide<false>(p, sV, sE, sPf, TNst, G, tl.x0, tl.x1, Nj, j, nn, ts, p.preds + pg.pred_base, dom,
+        tile_wide<false>(p, sV, sE, sPf, TNst, G, tl.x0, tl.x1, Nj, VS, j, nn, ts, p.preds + pg.pred_base, dom,
                          g1, leaf, vout, bpo, mine);
     } else {
       const int P = single ? 1 : (int)(plast - pfirst) + 1;
@@ -617,9 +631,9 @@ __global__ void __launch_bounds__(kTrieThreads, 4) k_trie_dp(TrieParams p) {
         const double* src = p.v1g + p.v1off[c];
         for (int x = tid; x < Np; x += blockDim.x) sV[x * Pst] = src[x];
       } else {
-        const double* src = p.varena + vbp + (uint64_t)(pfirst - pnb) * Np;
+        const double* src = p.varena + vbp + (uint64_t)(pfirst - pnb) * VSp;
         for (int pl = warp; pl < P; pl += nw)
-          for (int x = lane; x < Np; x += 32) sV[x * Pst + pl] = __ldcg(src + (size_t)pl * Np + x);
+          for (int x = lane; x < Np; x += 32) cp_async8(sV + x * Pst + pl, src + (size_t)pl * VSp + x);
       }
       for (int x = tid; x < p.n_codes * L; x += blockDim.x) sE[x] = qt[x];
       for (int x = tid; x < LP; x += blockDim.x) sPf[x] = p.prefix[(size_t)cl.pair * LP + x];
@@ -627,8 +641,9 @@ __global__ void __launch_bounds__(kTrieThreads, 4) k_trie_dp(TrieParams p) {
         const uint64_t node = noff + tl.n0 + x;
         sNode[x] = ((int)p.ncode[node] << 16) | (single ? 0 : (int)(p.npar[node] - pfirst));
       }
+      cp_async_wait_all();
       __syncthreads();
-      tile_narrow(p, sV, sE, sPf, sNode, Pst, Nj, j, nn, ts, p.preds + pg.pred_base, dom, g1, leaf, vout,
+      tile_narrow(p, sV, sE, sPf, sNode, Pst, Nj, VS, j, nn, ts, p.preds + pg.pred_base, dom, g1, leaf, vout,
                   bpo, mine);
     }
     // publish: every thread's stores, then the run's chunk count

@@ -35,8 +35,17 @@ for cb in cubins:
 rows = list(csv.reader(open(sass_csv)))
 hdr = rows[1]
 ix = {h: i for i, h in enumerate(hdr)}
-data = [r for r in rows[2:] if len(r) == len(hdr)]
+data = [r for r in rows[2:] if len(r) == len(hdr) and r[ix["Address"]] != "Address"]
+# (a capture with several launches lists the kernel once per launch: keep the first)
 base = int(data[0][ix["Address"]], 16)
+seen, first = set(), []
+for r in data:
+    a = r[ix["Address"]]
+    if a in seen:
+        break
+    seen.add(a)
+    first.append(r)
+data = first
 def f(r, k):
     try:
         return float(r[ix[k]] or 0)
