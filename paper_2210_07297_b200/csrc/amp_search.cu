@@ -1130,9 +1130,9 @@ int run_sig_dp(amp_ctx* ctx, EvalParams& ep, const HashParams& hp) {
     }
     const uint64_t node_cap = std::min<uint64_t>(node_b, 32ull << 20);
     const uint64_t pres_cap = std::min<uint64_t>(lvl_b, 32ull << 20) * U;
-    if (ctx->tr_pres.bytes < pres_cap) {  // marks start clear (and are kept clear)
-      CK(ctx->tr_pres.ensure(pres_cap));
-      CK(cudaMemsetAsync(ctx->tr_pres.p, 0, pres_cap, ctx->stream));
+    if (ctx->tr_pres.bytes < pres_cap + 16) {  // marks start clear (and are kept clear); read as 16-byte vectors
+      CK(ctx->tr_pres.ensure(pres_cap + 16));
+      CK(cudaMemsetAsync(ctx->tr_pres.p, 0, pres_cap + 16, ctx->stream));
     }
     CK(ctx->tr_cid.ensure(sizeof(uint32_t) * pres_cap));
     CK(ctx->tr_npar.ensure(sizeof(uint32_t) * node_cap));

@@ -44,6 +44,7 @@ constexpr int kTrieThreads = 256;     // K_trie_dp block
 constexpr int kTrieNB = 4;            // nodes per thread in wide stages (share the cell's work)
 constexpr int kTrieSmem = 46 * 1024;  // K_trie_dp smem per CTA (4 CTAs / SM)
 constexpr int kBuildThreads = 512;    // K_trie_build block
+constexpr int kBuildReg = 4;          // signatures per thread K_trie_build keeps in registers
 
 // Level state, in device memory (zeroed by the host before K_trie_build).
 struct TrieState {
@@ -53,7 +54,7 @@ struct TrieState {
   unsigned long long v_bump, bp_bump, run_bump, tile_bump;
   uint32_t ovf;                     // capacity exceeded: signature-mode K_dp instead
   uint32_t next_tile;               // K_trie_dp dispenser
-  uint32_t bar_count, bar_gen;      // K_trie_build grid barrier
+  uint32_t bar_count, bar_pad;      // K_trie_build grid barrier (arrivals)
 };
 
 // Per (class, stage j) facts of the class's pruned program and its tile
@@ -155,18 +156,16 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* a) {
   return v;
 }
 
-// Grid barrier of the cooperative K_trie_build (all CTAs co-resident).
-__device__ __forceinline__ void grid_barrier(TrieState* st) {
+// Grid barrier of the cooperative K_trie_build (all CTAs co-resident): one
+// monotonic arrival counter (zeroed per launch); CTA thread 0 adds its
+// arrival with release semantics and polls until all CTAs of this phase
+// arrived.
+__device__ __forceinline__ void grid_barrier(TrieState* st, uint32_t& phase) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t g = ld_acquire(&st->bar_gen);
-    __threadfence();
-    if (atomicAdd(&st->bar_count, 1u) == gridDim.x - 1) {
-      st->bar_count = 0;
-      __threadfence();
-      atomicAdd(&st->bar_gen, 1u);
-    } else {
-      while (ld_acquire(&st->bar_gen) == g) __nanosleep(64);
+    const uint32_t target = ++phase * gridDim.x;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&st->bar_count) : "memory");
+    while (ld_acquire(&st->bar_count) < target) {
     }
     __threadfence();
   }
@@ -282,8 +281,14 @@ __global__ void __launch_bounds__(kBuildThreads) k_trie_build(TrieParams p) {
   const int tid = threadIdx.x, l = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
   const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + tid, gstride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t n = *p.n_sig;
+  uint32_t phase = 0;  // grid barriers passed
   // ---- signature list, roots, depth-1 marks --------------------------------
-  for (uint64_t i = gtid; i < n; i += gstride) {
+  // (a thread's first kBuildReg signatures keep key, depth and node in
+  // registers over the levels; the rest go through sig_key / nid)
+  uint64_t rkey[kBuildReg];
+  uint32_t rnid[kBuildReg];
+  int rdep[kBuildReg];
+  for (uint64_t i = gtid, r = 0; i < n; i += gstride, ++r) {
     const uint32_t s = p.uniq[i];
     const unsigned long long k = p.tkey[s];
     const uint64_t key = p.key_shift >= 64 ? k : (k & ((1ull << p.key_shift) - 1));
@@ -291,11 +296,22 @@ __global__ void __launch_bounds__(kBuildThreads) k_trie_build(TrieParams p) {
     p.rep_item[i] = p.tval[s];
     p.tval[s] = (uint32_t)i;
     const int c = trie_cls(p, key);
-    const int r = p.root_rank[c];
-    p.nid[i] = (uint32_t)r;
-    if (p.cls[c].pp - 1 >= 1) p.pres[(uint64_t)r * p.U + trie_code(p, key, 0)] = 1;
+    const int rt = p.root_rank[c];
+    const int dep = p.cls[c].pp - 1;  // depth of the signature's leaf
+    p.nid[i] = (uint32_t)rt;
+    if (dep >= 1) p.pres[(uint64_t)rt * p.U + trie_code(p, key, 0)] = 1;
+#pragma unroll
+    for (int q = 0; q < kBuildReg; ++q)
+      if (r == q) {
+        rkey[q] = key;
+        rnid[q] = (uint32_t)rt;
+        rdep[q] = dep;
+      }
   }
-  grid_barrier(st);
+#pragma unroll
+  for (int q = 0; q < kBuildReg; ++q)
+    if (gtid + q * gstride >= n) rdep[q] = -1;
+  grid_barrier(st, phase);
   uint32_t cnt_prev = (uint32_t)p.n_roots;       // nodes of depth d-1
   uint64_t off_prev = 0, noff = 0;               // node_off of depth d-1, d
   uint64_t marked = (uint64_t)p.n_roots * p.U;   // mark entries that may be set
@@ -314,7 +330,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_trie_build(TrieParams p) {
     for (uint64_t x = b + tid; x < e; x += blockDim.x) s += __ldcg(p.pres + x);
     s = block_sum_u32(s, sm);
     if (tid == 0) p.partial[blockIdx.x] = s;
-    grid_barrier(st);
+    grid_barrier(st, phase);
     // ---- node ids: exclusive scan, node arrays, clear the marks ------------
     uint32_t base = 0, total = 0;
     {
@@ -364,7 +380,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_trie_build(TrieParams p) {
       }
       for (int q = 0; q < nw; ++q) base += wsum[q];
     }
-    grid_barrier(st);
+    grid_barrier(st, phase);
     marked = 0;
     if (d < p.nq && (uint64_t)total * p.U > p.pres_cap) {
       ovf = true;
@@ -372,7 +388,14 @@ __global__ void __launch_bounds__(kBuildThreads) k_trie_build(TrieParams p) {
     }
     // ---- plan of depth d (CTA 0); each signature's node, depth-(d+1) marks
     if (blockIdx.x == 0) plan_level(p, d, total, noff, build_sm);
-    for (uint64_t i = gtid; i < n; i += gstride) {
+#pragma unroll
+    for (int q = 0; q < kBuildReg; ++q) {
+      if (rdep[q] < d) continue;
+      const uint32_t node = __ldcg(p.cid + (uint64_t)rnid[q] * p.U + trie_code(p, rkey[q], d - 1));
+      rnid[q] = node;
+      if (rdep[q] >= d + 1) p.pres[(uint64_t)node * p.U + trie_code(p, rkey[q], d)] = 1;
+    }
+    for (uint64_t i = gtid + kBuildReg * gstride; i < n; i += gstride) {
       const uint64_t key = p.sig_key[i];
       const int pp = p.cls[trie_cls(p, key)].pp;
       if (pp - 1 < d) continue;
@@ -381,7 +404,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_trie_build(TrieParams p) {
       if (pp - 1 >= d + 1) p.pres[(uint64_t)node * p.U + trie_code(p, key, d)] = 1;
     }
     if (d < p.nq) marked = (uint64_t)total * p.U;
-    grid_barrier(st);
+    grid_barrier(st, phase);
     if (ld_acquire(&st->ovf) != 0) {  // a plan capacity was exceeded
       ovf = true;
       break;
@@ -394,6 +417,9 @@ __global__ void __launch_bounds__(kBuildThreads) k_trie_build(TrieParams p) {
     if (blockIdx.x == 0 && tid == 0) st->ovf = 1;
     return;
   }
+#pragma unroll
+  for (int q = 0; q < kBuildReg; ++q)
+    if (rdep[q] >= 0) p.nid[gtid + q * gstride] = rnid[q];
   // ---- tile list of all depths; run counters cleared -----------------------
   const uint32_t T = (uint32_t)st->tile_bump;
   if (blockIdx.x == 0 && tid == 0) {
