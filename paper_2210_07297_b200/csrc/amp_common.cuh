@@ -185,6 +185,11 @@ struct EvalParams {
   // keys [*n_rep]; run only while *sig_guard != 0 (NULL: always)
   const uint64_t* sig_keys;
   const uint32_t* sig_guard;
+  // hashed signature keys (class + codes wider than 63 bits): set when an
+  // item's class / codes differ from its signature representative's (a
+  // hash collision); K_est then reads the per-item cuts of the guarded
+  // per-item K_dp instead of the signature's (NULL: exact keys)
+  const uint32_t* memo_bad;
   // node-determined bandwidths (every link a function of its two nodes,
   // symmetric): make_comm_group's pairwise minimum over the nodes present
   // in the group instead of over its device pairs (warp K_est), or NULL

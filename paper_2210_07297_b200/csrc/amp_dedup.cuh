@@ -34,6 +34,7 @@ struct HashParams {
   const uint8_t* bwcb;
   uint64_t n;              // heavy items
   int32_t max_pp, code_bits;
+  int32_t wide, pad1;      // hashed keys (sig_key_wide)
   uint64_t mask;           // table size - 1
   uint64_t max_probe;      // probe bound (hash_insert_warp)
   uint64_t epoch;          // this run's tag (> 0)
@@ -55,6 +56,30 @@ __device__ __forceinline__ uint64_t sig_key(const CandWork& w, const ClassDev* c
   uint64_t key = (uint64_t)w.cls;
   for (int q = 0; q < max_pp - 1; ++q) key = (key << cb) | (q < cl.pp - 1 ? (uint64_t)codes[q] : 0ull);
   return key;
+}
+
+// Hashed key (the exact key would exceed 63 bits: |D| = 1024 with pp up to
+// 64): a 64-bit mix of the class and the codes.  Equal signatures get equal
+// keys; distinct ones may collide, which k_hash_verify detects exactly (the
+// memoisation is then dropped for the chunk, see memo_bad).
+__device__ __forceinline__ uint64_t sig_key_wide(const CandWork& w, const ClassDev* cls,
+                                                 const uint8_t* codes) {
+  if (w.fail_code != 0) return kHashEmpty;
+  const ClassDev cl = cls[w.cls];
+  if (cl.pp < 3) return kHashEmpty;
+  uint64_t h = splitmix64((uint64_t)w.cls);
+  const int nq = cl.pp - 1;
+  for (int q0 = 0; q0 < nq; q0 += 8) {
+    uint64_t word = 0;
+    for (int q = q0; q < nq && q < q0 + 8; ++q) word |= (uint64_t)codes[q] << ((q - q0) * 8);
+    h = splitmix64(h ^ word);
+  }
+  return h == kHashEmpty ? h - 1 : h;
+}
+
+// (the tests keep fewer hash bits to force collisions)
+__device__ __forceinline__ uint64_t wide_bits(uint64_t k, int bits) {
+  return (bits >= 64 || k == kHashEmpty) ? k : (k & ((1ull << bits) - 1));
 }
 
 // Table entries carry the run's epoch above the key bits (epoch_shift), so
@@ -118,6 +143,7 @@ __global__ void k_hash_insert(HashParams p) {
     const bool live = u < p.n;
     const uint64_t key = !live ? kHashEmpty
                          : p.sigkey ? p.sigkey[u]
+                         : p.wide   ? wide_bits(sig_key_wide(p.work[u], p.cls, p.bwcb + u * p.max_pp), p.wide)
                                     : sig_key(p.work[u], p.cls, p.bwcb + u * p.max_pp, p.max_pp,
                                               p.code_bits);
     const uint32_t slot = hash_insert_warp(key, u, lane, p.tkey, p.tval, p.uniq, p.n_uniq, p.mask,
@@ -140,6 +166,26 @@ __global__ void k_hash_scatter(HashParams p) {
     if (lane == leader && s != ~0u) r = p.tval[s];
     r = __shfl_sync(0xffffffffu, r, leader);
     if (live) p.rep_of[u] = r;
+  }
+}
+
+// Hashed keys: every item's class and codes against its signature
+// representative's (rep_of after k_hash_scatter, rep_list from K_sig_list);
+// any difference is a collision and sets *bad.
+__global__ void k_hash_verify(HashParams p, const uint32_t* rep_list, uint32_t* bad) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < p.n; u += stride) {
+    if (p.slot_of[u] == ~0u) continue;
+    const uint64_t r = rep_list[p.rep_of[u]];
+    if (r == u) continue;
+    const CandWork& a = p.work[u];
+    const CandWork& b = p.work[r];
+    bool same = a.cls == b.cls && b.fail_code == 0;
+    const int nq = p.cls[a.cls].pp - 1;
+    const uint8_t* ca = p.bwcb + u * p.max_pp;
+    const uint8_t* cb = p.bwcb + r * p.max_pp;
+    for (int q = 0; same && q < nq; ++q) same = ca[q] == cb[q];
+    if (!same) atomicOr(bad, 1u);
   }
 }
 

@@ -295,6 +295,11 @@ __global__ void __launch_bounds__(MODE == kSparseG ? 1024 : (MODE == kSparseS ? 
   // (integer offset from smem_raw keeps the shared address space visible)
   uint16_t* seg = reinterpret_cast<uint16_t*>(smem_raw + ((sp - smem_raw + 15) & ~15));
 
+  // memoised runs (p.rep_list): slot s solves signature s through its
+  // representative item rep_list[s] and writes its cuts at repcuts[s]; a
+  // guarded launch (sig_guard) runs only while *sig_guard != 0
+  if (p.sig_guard && *p.sig_guard == 0) return;
+  const uint64_t n_items = p.rep_list ? *p.n_rep : p.n_dp;
   if (tid == 0) {
     sh.cls = -1;
     sh.pair = -1;
@@ -308,22 +313,30 @@ __global__ void __launch_bounds__(MODE == kSparseG ? 1024 : (MODE == kSparseS ? 
       if (tid == 0) {
         const unsigned long long u0 = atomicAdd(p.counter, (unsigned long long)kDpBatch);
         sh.u = u0;
-        sh.done = u0 >= p.n_dp;  // items [n_dp, n_chunk) are pp <= 2 (K_est)
+        sh.done = u0 >= n_items;  // items [n_dp, n_chunk) are pp <= 2 (K_est)
       }
       __syncthreads();
       if (sh.done) break;
       bbase = sh.u;
-      bn = p.n_dp - bbase < (uint64_t)kDpBatch ? (int)(p.n_dp - bbase) : kDpBatch;
+      bn = n_items - bbase < (uint64_t)kDpBatch ? (int)(n_items - bbase) : kDpBatch;
       bi = 0;
-      const uint64_t* src = reinterpret_cast<const uint64_t*>(p.work + bbase);
+      constexpr int WW = (int)(sizeof(CandWork) / 8);
       uint64_t* dst = reinterpret_cast<uint64_t*>(wq);
-      for (int x = tid; x < bn * (int)(sizeof(CandWork) / 8); x += nt) dst[x] = src[x];
+      for (int x = tid; x < bn * WW; x += nt) {
+        const uint64_t it = p.rep_list ? p.rep_list[bbase + x / WW] : bbase + x / WW;
+        dst[x] = reinterpret_cast<const uint64_t*>(p.work + it)[x % WW];
+      }
       __syncthreads();
     }
     const int my = bi++;
     const CandWork& w = wq[my];
     if (w.fail_code != 0) continue;  // failed before the DP (uniform)
-    const uint64_t u = bbase + my;
+    const uint64_t slot = bbase + my;
+    const uint64_t u = p.rep_list ? p.rep_list[slot] : slot;
+    if (p.exec_counters && tid == 0) {  // executed work (roofline accounting)
+      atomicAdd(&p.exec_counters[0], 1ull);
+      atomicAdd(&p.exec_counters[1], (unsigned long long)p.prog_inner[p.class_prog[w.cls]]);
+    }
     if (w.cls != sh.cls) {  // uniform: everybody reads the same smem
       __syncthreads();
       if (tid == 0) {
@@ -356,7 +369,7 @@ __global__ void __launch_bounds__(MODE == kSparseG ? 1024 : (MODE == kSparseS ? 
     } else {
       dp_solve(L, pp, cl.gas, M, Pf, Dm, seg, ef, C, W, E, pr.monotone != 0, bp, cuts);
     }
-    uint8_t* co = p.cutsb + u * (maxpp + 1);
+    uint8_t* co = p.repcuts ? p.repcuts + slot * (maxpp + 1) : p.cutsb + u * (maxpp + 1);
     for (int q = tid; q <= pp; q += nt) co[q] = (uint8_t)cuts[q];
     __syncthreads();
   }
@@ -553,7 +566,7 @@ __global__ void __launch_bounds__(kEstWarps * 32, 2) k_est(EvalParams p) {
       if (pp >= 3 || p.cuts_given) {
         // (memoised DP: the cuts of this candidate's signature representative)
         // (memoised DP: the cuts of this candidate's signature run)
-        const uint8_t* ci = (p.rep_of && !p.cuts_given && u < p.n_dp)
+        const uint8_t* ci = (p.rep_of && !p.cuts_given && u < p.n_dp && !(p.memo_bad && *p.memo_bad))
                                 ? p.repcuts + (uint64_t)p.rep_of[u] * (maxpp + 1)
                                 : p.cutsb + u * (maxpp + 1);
         for (int q = lane; q <= pp; q += 32) cutsW[q] = ci[q];

@@ -175,8 +175,10 @@ struct amp_ctx {
   uint64_t n_heavy = 0;  // items of pp >= 3 classes in the current run's dispatch order
   // DP memoisation by signature (amp_dedup.cuh)
   bool dedup = false;
+  bool wide = false;   // hashed signature keys (exact key > 63 bits), verified per chunk
+  int wide_bits = 64;  // hash bits kept (AMP_WIDE_HASH_BITS: forced collisions in the tests)
   int code_bits = 0, key_bits = 0;
-  DevBuf dd_rep_list, dd_rep_of;
+  DevBuf dd_rep_list, dd_rep_of, dd_bad;
   DevBuf dd_runpipe;  // per-run pipeline time of dp == 1 classes (k_run_pipe)
   DevBuf dd_counters, prog_inner_d, dd_repcuts;
   DevBuf dd_tkey, dd_tval, dd_slot, dd_uniq, dd_nuniq, dd_sigkey;  // hash dedup
@@ -327,6 +329,8 @@ int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
   CK(cudaMemcpyAsync(pin.data(), d_inner_n.p, sizeof(uint64_t) * pin.size(),
                      cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  PhaseTimer tm;
+  tm.mark("K0b count pass");
   ctx->prog_inner_raw.assign(n, 0.0);
   ctx->prog_stage_inner = pin;
   // layout
@@ -399,9 +403,20 @@ int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
   bp.preds = ctx->preds.as<uint16_t>();
   bp.stage = ctx->stage_d.as<uint32_t>();
   bp.pred_start = d_pst.as<uint64_t>();
+  tm.mark("K0b layout+alloc");
   k_build_progs<<<n, 512, smem, ctx->stream>>>(bp);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(ctx->stream));
+  tm.mark("K0b build pass");
+  if (tm.on) {
+    int kmax = 0, Mmax = 0;
+    for (int g = 0; g < n; ++g) {
+      kmax = std::max(kmax, pk[g]);
+      Mmax = std::max(Mmax, ctx->pairs[ppair[g]].M);
+    }
+    std::fprintf(stderr, "[amp create] K0b: %d programs, k <= %d, M <= %d, cells %llu, preds %llu, max |N_j| %d\n", n,
+                 kmax, Mmax, (unsigned long long)cell_total, (unsigned long long)pred_total, max_cells);
+  }
   ctx->progs_h = progs;
   return AMP_OK;
 }
@@ -799,17 +814,23 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   }
   // ---- DP memoisation by signature: key = class | codes ------
   ctx->dedup = false;
-  if (ctx->multi_b && ctx->n_codes > 0 && !(cfg && (cfg->flags & AMP_FLAG_NO_DEDUP)) &&
+  if (ctx->sparse && ctx->n_codes > 0 && !(cfg && (cfg->flags & AMP_FLAG_NO_DEDUP)) &&
       std::getenv("AMP_NO_DEDUP") == nullptr) {
     int cb = 1;
     while ((1 << cb) < ctx->n_codes) ++cb;
     int clsb = 1;
     while ((1ull << clsb) < ctx->classes.size()) ++clsb;
     const int kb = clsb + (ctx->max_pp - 1) * cb;
-    if (kb <= 63) {
+    // keys wider than 63 bits (|D| = 1024: pp up to 64) are hashed and every
+    // item verified against its representative (AMP_WIDE_MEMO=1 forces the
+    // hashed keys, AMP_NO_WIDE_MEMO=1 disables them)
+    const bool wide = kb > 63 || std::getenv("AMP_WIDE_MEMO") != nullptr;
+    if (!wide || std::getenv("AMP_NO_WIDE_MEMO") == nullptr) {
       ctx->dedup = true;
+      ctx->wide = wide;
+      if (const char* wb = std::getenv("AMP_WIDE_HASH_BITS")) ctx->wide_bits = std::max(1, std::min(64, std::atoi(wb)));
       ctx->code_bits = cb;
-      ctx->key_bits = kb;
+      ctx->key_bits = wide ? 64 : kb;
       std::vector<double> pin(ctx->prog_inner_raw.begin(), ctx->prog_inner_raw.end());
       if (pin.empty()) pin.push_back(0.0);
       CK(upload(ctx->prog_inner_d, pin.data(), pin.size()));
@@ -843,7 +864,7 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
     CK(cudaGetLastError());
   }
   // ---- prefix-shared DP (amp_trie.cuh): static per-class stage facts ------
-  ctx->trie = ctx->dedup && (1 << ctx->code_bits) <= 16 && std::getenv("AMP_NO_TRIE") == nullptr;
+  ctx->trie = ctx->dedup && ctx->multi_b && !ctx->wide && (1 << ctx->code_bits) <= 16 && std::getenv("AMP_NO_TRIE") == nullptr;
   if (ctx->trie) {
     const int NC = (int)ctx->classes.size(), P1 = ctx->max_pp + 1;
     std::vector<TrieStage> ts((size_t)NC * P1, TrieStage{0, 0, 0, 1, 0});
@@ -1225,12 +1246,15 @@ int run_sig_dp(amp_ctx* ctx, EvalParams& ep, const HashParams& hp) {
   // signature-mode K_dp: the whole DP when the trie is off; with the trie
   // only if its capacity was exceeded on the device (it exits otherwise)
   EvalParams es = ep;
-  es.sig_keys = ctx->dd_rep_key.as<uint64_t>();
+  // (hashed keys, or the per-candidate K_dp of programs too large for
+  // k_dp_multi: class and codes of each signature's representative item)
+  const bool by_rep = ctx->wide || !ctx->multi_b;
+  es.sig_keys = by_rep ? nullptr : ctx->dd_rep_key.as<uint64_t>();
   es.sig_guard = ctx->trie ? reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(tp.st) +
                                                                offsetof(TrieState, ovf))
                           : nullptr;
   es.n_rep = reinterpret_cast<const uint64_t*>(hp.n_uniq);
-  es.rep_list = nullptr;
+  es.rep_list = by_rep ? ctx->dd_rep_list.as<uint32_t>() : nullptr;
   es.repcuts = ctx->dd_repcuts.as<uint8_t>();
   es.sig_code_bits = ctx->code_bits;
   void* args[] = {&es};
@@ -1405,7 +1429,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   if (thread_mode) {
     CK(ctx->c_placep.ensure(sizeof(uint64_t) * C));
     ep.placep = ctx->c_placep.as<uint64_t>();
-    if (ctx->dedup && !d_given_cuts) {  // K_place_t writes the DP signature keys
+    if (ctx->dedup && !ctx->wide && !d_given_cuts) {  // K_place_t writes the DP signature keys
       CK(ctx->dd_sigkey.ensure(sizeof(uint64_t) * C));
       ep.sigkey = ctx->dd_sigkey.as<uint64_t>();
       ep.sig_code_bits = ctx->code_bits;
@@ -1437,7 +1461,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
                  (ctx->P == 1 || ep.perm_tab != nullptr) && !d_given_place;
   for (const auto& c : ctx->classes) shape16 = shape16 && c.pp * c.dp * c.tmp == 16;
   ep.est_fast = shape16 && est_thread && ep.cut2tab && ep.rsum_t && !ep.all_cuts && !ep.all_stage &&
-                !ep.all_edge && !ep.all_place && !d_given_cuts;
+                !ep.all_edge && !ep.all_place && !d_given_cuts && !ctx->wide;
   // the boundary codes are read by K_dp without the trie, the sort dedup
   // path and K_est's pp == 2 items placed by K_place; with the hash dedup on
   // K_place's signature keys, the trie and the fused light path, nothing
@@ -1508,6 +1532,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     hp.n = ep.n_dp;
     hp.max_pp = ctx->max_pp;
     hp.code_bits = ctx->code_bits;
+    hp.wide = ctx->wide ? ctx->wide_bits : 0;
     hp.mask = T - 1;
     hp.max_probe = T;
     hp.epoch = ctx->hash_epoch;
@@ -1524,7 +1549,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   const bool fuse_hash_ok = thread_mode && ep.sigkey && ctx->dedup && !d_given_cuts &&
                             std::getenv("AMP_NO_FUSE_HASH") == nullptr;
   HashParams fused_hp{};
-  ep.skip_work = ep.est_fast && ctx->dedup && fuse_hash_ok && ep.fuse_light &&
+  ep.skip_work = ep.est_fast && ctx->dedup && ctx->multi_b && fuse_hash_ok && ep.fuse_light &&
                  std::getenv("AMP_KEEP_WORK") == nullptr;
   if (overlap) {
     CK(cudaEventRecord(ctx->aux_start, ctx->stream));
@@ -1598,6 +1623,7 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
     CK(cudaEventRecord(ev[1], ctx->stream));
     ep.rep_list = nullptr;
     ep.rep_of = nullptr;
+    ep.memo_bad = nullptr;
     ep.n_rep = nullptr;
     ep.repcuts = nullptr;
     ep.run_slot = nullptr;
@@ -1630,6 +1656,31 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
         DBG_SYNC("k_hash_scatter");
         ctx->launches += 1;
         ep.rep_of = hp.rep_of;
+      }
+      if (ctx->wide) {
+        // hashed keys: verify every item against its representative; on a
+        // collision (*bad) a guarded per-item K_dp writes every item's cuts
+        // and K_est reads those instead
+        CK(ctx->dd_bad.ensure(sizeof(uint32_t)));
+        CK(cudaMemsetAsync(ctx->dd_bad.p, 0, sizeof(uint32_t), ctx->stream));
+        k_hash_verify<<<g, 256, 0, ctx->stream>>>(hp, ctx->dd_rep_list.as<uint32_t>(), ctx->dd_bad.as<uint32_t>());
+        DBG_SYNC("k_hash_verify");
+        CK(cudaGetLastError());
+        EvalParams eg = ep;
+        eg.sig_guard = ctx->dd_bad.as<uint32_t>();
+        eg.sig_keys = nullptr;
+        eg.rep_list = nullptr;
+        eg.n_rep = nullptr;
+        eg.repcuts = nullptr;
+        eg.exec_counters = nullptr;
+        CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), ctx->stream));
+        void* gargs[] = {&eg};
+        CK(cudaLaunchKernel(ctx->eval_fn, dim3(ctx->n_ctas), dim3(ctx->eval_threads), gargs, ctx->smem_bytes,
+                            ctx->stream));
+        CK(cudaGetLastError());
+        DBG_SYNC("k_dp_multi (collision fallback)");
+        ctx->launches += 2;
+        ep.memo_bad = ctx->dd_bad.as<uint32_t>();
       }
       ep.repcuts = ctx->dd_repcuts.as<uint8_t>();
       if (ep.est_fast && std::getenv("AMP_NO_RUN_PIPE") == nullptr) {

@@ -612,7 +612,7 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
         //      the k <= 2 DP here (light_cut2's operations, sequential) ---
         if (pp >= 3 || p.cuts_given) {
           // (memoised DP: the cuts of this candidate's signature run)
-          const uint8_t* ci = (p.rep_of && !p.cuts_given && u < p.n_dp)
+          const uint8_t* ci = (p.rep_of && !p.cuts_given && u < p.n_dp && !(p.memo_bad && *p.memo_bad))
                                   ? p.repcuts + (uint64_t)p.rep_of[u] * (maxpp + 1)
                                   : p.cutsb + u * (maxpp + 1);
           for (int q = 0; q <= pp; ++q) cuts[q] = ci[q];

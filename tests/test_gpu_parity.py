@@ -517,6 +517,7 @@ SWITCHES = [
     ("AMP_NO_FUSE_HASH", "1"),     # separate k_hash_insert launch
     ("AMP_NO_RUN_SLOT", "1"),      # k_hash_scatter + rep_of lookup in K_est
     ("AMP_KEEP_WORK", "1"),        # K_place writes work records, K_est reads them
+    ("AMP_WIDE_MEMO", "1"),        # hashed signature keys (the |D| = 1024 path), verified
 ]
 
 
@@ -550,6 +551,35 @@ def test_switch_paths_equal_default(var, val, monkeypatch):
     assert np.array_equal(allr["fail_code"], orec["fail_code"])
     ok = orec["fail_code"] == 0
     assert np.array_equal(allr["total"][ok], orec["total"][ok])
+
+
+@pytest.mark.parametrize("bits", ["64", "3"])
+def test_hashed_signature_keys_exact_under_collisions(bits, monkeypatch):
+    """Hashed signature keys (AMP_WIDE_MEMO: the keys of |D| = 1024 exceed 63
+    bits) with the full hash and with 3 hash bits (every class collides):
+    k_hash_verify catches each collision and the per-item K_dp takes over,
+    so the records equal the exact-key run and the memoised oracle."""
+    sc = scenario("hetero_cluster")
+    enc = P.EncodedProblem.from_scenario(sc)
+    with planner.Searcher(enc, placements_per_class=3000, seed=6) as s:
+        top0, all0, _ = s.run(0, s.num_candidates, k=16, want_all=True, details=True)
+        st0 = s.stats()
+    monkeypatch.setenv("AMP_WIDE_MEMO", "1")
+    monkeypatch.setenv("AMP_WIDE_HASH_BITS", bits)
+    with planner.Searcher(enc, placements_per_class=3000, seed=6) as s:
+        top1, all1, _ = s.run(0, s.num_candidates, k=16, want_all=True, details=True)
+        st1 = s.stats()
+    monkeypatch.delenv("AMP_WIDE_MEMO")
+    monkeypatch.delenv("AMP_WIDE_HASH_BITS")
+    assert np.array_equal(all0.view(np.uint8), all1.view(np.uint8))
+    assert np.array_equal(top0.view(np.uint8), top1.view(np.uint8))
+    if bits == "64":  # no collision: one DP per distinct signature, as with exact keys
+        assert st1["dp_instances"] == st0["dp_instances"]
+    o = B.Oracle(enc, 3000, 6)
+    orec, _ = o.run(threads=8, details=False, memo=True)
+    ok = orec["fail_code"] == 0
+    assert np.array_equal(all1["fail_code"], orec["fail_code"])
+    assert np.array_equal(all1["total"][ok], orec["total"][ok])
 
 
 def test_trie_dp_stage_timing_and_counts():
