@@ -16,7 +16,7 @@
 // the closure is 1.7-5% of the dense table (measured).
 //
 // "Program" of one (pair, k), built on the device once per search context
-// (K0b, two passes: count, then build):
+// (K0b):
 //   cells[]     u32 (i << 16 | m) of N_1 .. N_k, each stage ordered by row
 //               descending then m ascending (equal cut counts are adjacent)
 //   cellpred[]  u32 per cell of N_j (j >= 2): offset of its predecessor list
@@ -26,6 +26,14 @@
 //               padding entries hold |N_{j-1}| (sentinel slot)
 //   stage[]     u32 k+1 entries: start of N_j (j = 1..k) within the program's
 //               cells, then the end
+// Two kernels: K0b-closure (one CTA per program, sequential over the stages)
+// computes each N_j as a bitmap [row][m / 32] word-parallel:
+//   row c of N_{j-1} = OR over the rows i > c of N_j of
+//       (row i's bits above seg(c,i))  |  (bit seg(c,i) if row i has a bit <= seg(c,i))
+// (= { max(seg(c,i), m) : (i, m) in N_j }), stores every stage's bitmap and
+// its sizes; K0b-emit (one CTA per (program, stage, slice of 4096 cells),
+// all in parallel) writes the cells, their list offsets and the predecessor
+// indices (rank of (c, mp) in N_{j-1}: a word prefix plus a popcount).
 #pragma once
 
 #include "amp_common.cuh"
@@ -45,24 +53,25 @@ struct ProgDev {
 };
 
 struct ProgBuildParams {
-  int32_t L, n_progs, count_only, pad;
+  int32_t L, n_progs;
   const int32_t* prog_k;     // [n_progs]
   const int32_t* prog_pair;  // [n_progs]
   const PairDev* pairs;
   const uint16_t* seg;       // [n_pairs][(L+1)^2]
-  uint32_t* scratch;         // [n_progs][2 * (L+1) * max_M] cell lists
-  uint64_t scratch_stride;
-  // count pass outputs
+  uint32_t* bm;              // stage bitmaps: program g, stage j at bm_off[g] + (j-1) * (L+1) * W_g
+  const uint64_t* bm_off;    // [n_progs]
+  // closure outputs
   uint32_t* stage_sizes;     // [n_progs][L+1]  |N_j| at [j]
   uint64_t* stage_preds;     // [n_progs][L+1]  predecessor entries of stage j (padded)
   uint64_t* stage_inner;     // [n_progs][L+1]  inner iterations of stage j (unpadded)
-  // build pass inputs/outputs
+  // emit inputs / outputs
   const ProgDev* progs;
   uint32_t* cells;
   uint32_t* cellpred;
   uint16_t* preds;
-  const uint32_t* stage;     // stage starts (host-computed from the count pass)
+  const uint32_t* stage;     // stage starts (host-computed from the closure sizes)
   const uint64_t* pred_start;  // [n_progs][L+1] start of stage j's preds (relative)
+  const uint4* items;        // emit work list {g, j, first cell, end cell}
 };
 
 // Exclusive block scan over n items in chunks of blockDim; emit(x, prefix)
@@ -98,123 +107,244 @@ __device__ uint64_t block_scan(int n, F value, G emit, uint64_t* sm) {
   return carry;
 }
 
-// K0b: one CTA per program.  Dynamic smem: bitmap [(L+1) * W] u32 and its
-// exclusive word prefix [(L+1) * W] u32 in row-descending scan order, plus
-// the segment table [(L+1)^2] u16.
-__global__ void k_build_progs(ProgBuildParams p) {
+constexpr uint32_t kEmitSlice = 4096;  // cells per K0b-emit CTA
+
+__device__ __forceinline__ int pad4(int x) { return (x + 3) & ~3; }
+
+// Bits of word w (m = 32 w .. 32 w + 31) strictly above m = s.
+__device__ __forceinline__ uint32_t bits_above(int s, int w) {
+  const int lo = w << 5;
+  if (s < lo) return ~0u;
+  if (s >= lo + 31) return 0u;
+  return ~((2u << (s - lo)) - 1u);
+}
+
+// Exclusive word prefix of a stage bitmap in rank order (rows descending,
+// words ascending): wpre[row * W + w] = cells before that word.  Returns the
+// stage size.
+__device__ uint32_t bitmap_rank(const uint32_t* bm, uint32_t* wpre, int L, int W, uint64_t* sm) {
+  const int nw = (L + 1) * W;
+  return (uint32_t)block_scan(
+      nw, [&](int o) { return (uint64_t)__popc(bm[(L - o / W) * W + (o % W)]); },
+      [&](int o, uint64_t before) { wpre[(L - o / W) * W + (o % W)] = (uint32_t)before; }, sm);
+}
+
+// K0b-closure: one CTA per program.  Dynamic smem: two stage bitmaps
+// [(L+1) * W] u32, the segment table [(L+1)^2] u16, the non-empty rows of
+// the current stage and their lowest m.
+__global__ void __launch_bounds__(512) k_prog_closure(ProgBuildParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ uint64_t scan_sm[64];
-  __shared__ uint64_t red64[32];
-  const int pg = blockIdx.x, L = p.L, LP = L + 1, tid = threadIdx.x, nt = blockDim.x;
-  const int k = p.prog_k[pg];
-  const PairDev pr = p.pairs[p.prog_pair[pg]];
-  const int M = pr.M;
-  const int W = (M + 31) >> 5;
-  const int nw = LP * W;
-  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw);
-  uint32_t* wpre = bm + nw;
-  uint16_t* seg = reinterpret_cast<uint16_t*>(wpre + nw);
-  const uint16_t* gseg = p.seg + (size_t)p.prog_pair[pg] * LP * LP;
+  __shared__ uint64_t red[3][32];
+  __shared__ int n_rows;
+  const int g = blockIdx.x, L = p.L, LP = L + 1, tid = threadIdx.x, nt = blockDim.x;
+  const int k = p.prog_k[g];
+  const int M = p.pairs[p.prog_pair[g]].M;
+  const int W = (M + 31) >> 5, nw = LP * W;
+  uint32_t* cur = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* nxt = cur + nw;
+  uint16_t* seg = reinterpret_cast<uint16_t*>(nxt + nw);
+  int* rows = reinterpret_cast<int*>(seg + ((LP * LP + 1) & ~1));  // [LP] non-empty rows, ascending
+  int* rmin = rows + LP;                                            // [LP] lowest m of each listed row
+  int* rlo = rmin + LP;                                             // [LP] lowest m of row i (-1: empty)
+  const uint16_t* gseg = p.seg + (size_t)p.prog_pair[g] * LP * LP;
   for (int x = tid; x < LP * LP; x += nt) seg[x] = gseg[x];
-  uint32_t* A = p.scratch + (size_t)pg * p.scratch_stride;
-  uint32_t* B = A + p.scratch_stride / 2;
-  if (tid == 0) A[0] = (uint32_t)L << 16;  // N_k = {(L, 0)}
-  int n = 1;
-  ProgDev pd{};
-  if (!p.count_only) pd = p.progs[pg];
+  for (int x = tid; x < nw; x += nt) cur[x] = 0;
+  __syncthreads();
+  if (tid == 0) cur[L * W] = 1u;  // N_k = {(L, 0)}
   __syncthreads();
   for (int j = k; j >= 1; --j) {
-    if (p.count_only) {
-      if (tid == 0) p.stage_sizes[(size_t)pg * LP + j] = n;
-    } else {
-      // write N_j (already in rank order) into the program
-      uint32_t* out = p.cells + pd.cell_base + p.stage[pd.stage_base + j - 1];
-      for (int x = tid; x < n; x += nt) out[x] = A[x];
-    }
-    if (j == 1) break;
-    // ---- mark N_{j-1} ----------------------------------------------------
-    for (int x = tid; x < nw; x += nt) bm[x] = 0;
-    __syncthreads();
-    uint64_t my_preds = 0, my_inner = 0;
-    for (int x = tid; x < n; x += nt) {
-      const uint32_t cell = A[x];
-      const int i = cell >> 16, m = cell & 0xffff;
-      my_preds += (uint64_t)((i - j + 1 + 3) & ~3);  // lists padded to 4 (8-byte loads)
-      my_inner += (uint64_t)(i - j + 1);
-      for (int c = j - 1; c < i; ++c) {
-        const int s = seg[c * LP + i];
-        const int mp = s > m ? s : m;
-        atomicOr(&bm[c * W + (mp >> 5)], 1u << (mp & 31));
+    uint32_t* out = p.bm + p.bm_off[g] + (size_t)(j - 1) * nw;
+    for (int x = tid; x < nw; x += nt) out[x] = cur[x];
+    // sizes of N_j: cells, padded and unpadded predecessor entries
+    uint64_t cn = 0, pn = 0, in = 0;
+    for (int i = tid; i <= L; i += nt) {
+      uint32_t c = 0;
+      int lo = -1;
+      for (int w = 0; w < W; ++w) {
+        const uint32_t b = cur[i * W + w];
+        if (b && lo < 0) lo = (w << 5) + __ffs(b) - 1;
+        c += __popc(b);
+      }
+      rlo[i] = lo;
+      cn += c;
+      if (i >= j) {
+        pn += (uint64_t)c * pad4(i - j + 1);
+        in += (uint64_t)c * (i - j + 1);
       }
     }
-    // total predecessor entries of stage j
     for (int o = 16; o > 0; o >>= 1) {
-      my_preds += __shfl_xor_sync(0xffffffffu, my_preds, o);
-      my_inner += __shfl_xor_sync(0xffffffffu, my_inner, o);
+      cn += __shfl_xor_sync(0xffffffffu, cn, o);
+      pn += __shfl_xor_sync(0xffffffffu, pn, o);
+      in += __shfl_xor_sync(0xffffffffu, in, o);
     }
     if ((tid & 31) == 0) {
-      red64[tid >> 5] = my_preds;
-      red64[16 + (tid >> 5)] = my_inner;
+      red[0][tid >> 5] = cn;
+      red[1][tid >> 5] = pn;
+      red[2][tid >> 5] = in;
     }
     __syncthreads();
     if (tid == 0) {
-      uint64_t t = 0, ti = 0;
+      uint64_t a = 0, b = 0, c = 0;
       for (int w = 0; w < (nt >> 5); ++w) {
-        t += red64[w];
-        ti += red64[16 + w];
+        a += red[0][w];
+        b += red[1][w];
+        c += red[2][w];
       }
-      if (p.count_only) {
-        p.stage_preds[(size_t)pg * LP + j] = t;
-        p.stage_inner[(size_t)pg * LP + j] = ti;
+      p.stage_sizes[(size_t)g * LP + j] = (uint32_t)a;
+      if (j >= 2) {
+        p.stage_preds[(size_t)g * LP + j] = b;
+        p.stage_inner[(size_t)g * LP + j] = c;
       }
     }
-    // ---- rank structure: words in row-descending order ------------------
-    // scan position o = (L - row) * W + w
-    const uint64_t n_next = block_scan(
-        nw, [&](int o) { return (uint64_t)__popc(bm[(L - o / W) * W + (o % W)]); },
-        [&](int o, uint64_t before) { wpre[(L - o / W) * W + (o % W)] = (uint32_t)before; }, scan_sm);
-    __syncthreads();
-    // ---- predecessor lists of N_j (build pass) ---------------------------
-    if (!p.count_only) {
-      const uint64_t pbase = pd.pred_base + p.pred_start[(size_t)pg * LP + j];
-      uint32_t* cpo = p.cellpred + pd.cell_base + p.stage[pd.stage_base + j - 1];
-      block_scan(
-          n, [&](int x) { return (uint64_t)(((A[x] >> 16) - j + 1 + 3) & ~3u); },
-          [&](int x, uint64_t before) {
-            const uint32_t cell = A[x];
-            const int i = cell >> 16, m = cell & 0xffff;
-            cpo[x] = (uint32_t)(p.pred_start[(size_t)pg * LP + j] + before);
-            uint16_t* q = p.preds + pbase + before;
-            for (int c = j - 1; c < i; ++c) {
-              const int s = seg[c * LP + i];
-              const int mp = s > m ? s : m;
-              const int wi = c * W + (mp >> 5);
-              const uint32_t below = bm[wi] & ((1u << (mp & 31)) - 1u);
-              q[c - (j - 1)] = (uint16_t)(wpre[wi] + __popc(below));
-            }
-            // padding entries name the sentinel slot |N_{j-1}| (a +inf
-            // value in K_dp multi, so padded cuts never win)
-            for (int t = i - (j - 1); t < (((i - j + 1) + 3) & ~3); ++t)
-              q[t] = (uint16_t)n_next;
-          },
-          scan_sm);
-    }
-    // ---- N_{j-1} list in rank order -------------------------------------
-    for (int wi = tid; wi < nw; wi += nt) {
-      uint32_t bits = bm[wi];
-      uint32_t pos = wpre[wi];
-      const int row = wi / W, m0 = (wi % W) << 5;
-      while (bits) {
-        const int b = __ffs(bits) - 1;
-        bits &= bits - 1;
-        B[pos++] = ((uint32_t)row << 16) | (uint32_t)(m0 + b);
+    if (tid < 32) {  // the non-empty rows (ascending) and their lowest m
+      int nr = 0;
+      for (int b = 0; b <= L; b += 32) {
+        const int i = b + (tid & 31);
+        const bool ne = i <= L && rlo[i] >= 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, ne);
+        if (ne) {
+          const int at = nr + __popc(bal & ((1u << (tid & 31)) - 1u));
+          rows[at] = i;
+          rmin[at] = rlo[i];
+        }
+        nr += __popc(bal);
       }
+      if (tid == 0) n_rows = nr;
     }
     __syncthreads();
-    uint32_t* t = A;
-    A = B;
-    B = t;
-    n = (int)n_next;
+    if (j == 1) break;
+    // N_{j-1}: rows c in [j-1, L-1], word-parallel
+    const int nr = n_rows;
+    for (int x = tid; x < nw; x += nt) {
+      const int c = x / W, w = x - c * W;
+      uint32_t word = 0;
+      if (c >= j - 1 && c < L) {
+        for (int r = 0; r < nr; ++r) {
+          const int i = rows[r];
+          if (i <= c) continue;
+          const int s = seg[c * LP + i];
+          word |= cur[i * W + w] & bits_above(s, w);
+          if ((s >> 5) == w && rmin[r] <= s) word |= 1u << (s & 31);
+        }
+      }
+      nxt[x] = word;
+    }
+    __syncthreads();
+    uint32_t* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+}
+
+// K0b-emit: one CTA per work item {g, j, x0, x1}: the cells of N_j with rank
+// in [x0, x1), their predecessor-list offsets and (j >= 2) the lists.
+// Dynamic smem: bitmap + word prefix of N_j and of N_{j-1} [(L+1) * W] u32
+// each, the segment table, the per-row list offsets of N_j.
+__global__ void __launch_bounds__(512) k_prog_emit(ProgBuildParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint64_t scan_sm[64];
+  const uint4 it = p.items[blockIdx.x];
+  const int g = (int)it.x, j = (int)it.y;
+  const uint32_t x0 = it.z, x1 = it.w;
+  const int L = p.L, LP = L + 1, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+  const int M = p.pairs[p.prog_pair[g]].M;
+  const int W = (M + 31) >> 5, nw = LP * W;
+  uint32_t* bmj = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* wpj = bmj + nw;
+  uint32_t* bmp = wpj + nw;
+  uint32_t* wpp = bmp + nw;
+  uint64_t* rowoff = reinterpret_cast<uint64_t*>(wpp + nw);  // (4 nw words: 8-byte aligned)  // [LP] first pred entry of row i's cells
+  uint32_t* scell = reinterpret_cast<uint32_t*>(rowoff + LP);  // [kEmitSlice] the slice's cells
+  uint32_t* scpo = scell + kEmitSlice;                           // [kEmitSlice] their list offsets
+  uint16_t* seg = reinterpret_cast<uint16_t*>(scpo + kEmitSlice);
+  const uint32_t* gbm = p.bm + p.bm_off[g] + (size_t)(j - 1) * nw;
+  for (int x = tid; x < nw; x += nt) bmj[x] = gbm[x];
+  if (j >= 2) {
+    for (int x = tid; x < nw; x += nt) bmp[x] = gbm[x - nw];
+    const uint16_t* gseg = p.seg + (size_t)p.prog_pair[g] * LP * LP;
+    for (int x = tid; x < LP * LP; x += nt) seg[x] = gseg[x];
+  }
+  __syncthreads();
+  const uint32_t n_cur = bitmap_rank(bmj, wpj, L, W, scan_sm);
+  __syncthreads();
+  uint32_t n_prev = 0;
+  if (j >= 2) {
+    n_prev = bitmap_rank(bmp, wpp, L, W, scan_sm);
+    if (tid < 32) {  // rows descending: padded entries before each row's cells
+      uint64_t carry = 0;
+      for (int b = 0; b <= L; b += 32) {
+        const int i = L - (b + lane);
+        uint64_t v = 0;
+        if (i >= j) {  // row i's cells: ranks [first(i), first(i - 1))
+          const uint32_t c = (i > 0 ? wpj[(i - 1) * W] : n_cur) - wpj[i * W];
+          v = (uint64_t)c * pad4(i - j + 1);
+        }
+        uint64_t incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (i >= 0) rowoff[i] = carry + incl - v;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+  }
+  __syncthreads();
+  const ProgDev pd = p.progs[g];
+  const uint32_t sbase = p.stage[pd.stage_base + j - 1];  // start of N_j within the program's cells
+  uint32_t* cells = p.cells + pd.cell_base + sbase;
+  uint32_t* cpo = p.cellpred + pd.cell_base + sbase;
+  const uint64_t pstart = j >= 2 ? p.pred_start[(size_t)g * LP + j] : 0;
+  // cells with rank in [x0, x1) (and their list offsets)
+  for (int wi = tid; wi < nw; wi += nt) {
+    uint32_t bits = bmj[wi];
+    uint32_t pos = wpj[wi];
+    if (!bits || pos >= x1 || pos + __popc(bits) <= x0) continue;
+    const int row = wi / W, m0 = (wi % W) << 5;
+    const uint32_t rfirst = wpj[row * W];  // rank of the row's first cell
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      if (pos >= x0 && pos < x1) {
+        scell[pos - x0] = ((uint32_t)row << 16) | (uint32_t)(m0 + b);
+        if (j >= 2) scpo[pos - x0] = (uint32_t)(pstart + rowoff[row] + (uint64_t)(pos - rfirst) * pad4(row - j + 1));
+      }
+      ++pos;
+    }
+  }
+  __syncthreads();
+  for (uint32_t x = x0 + tid; x < x1; x += nt) {
+    cells[x] = scell[x - x0];
+    if (j >= 2) cpo[x] = scpo[x - x0];
+  }
+  if (j < 2) return;
+  // predecessor lists: 8 lanes per cell (4 cells per warp), each lane 4
+  // cuts per pass (one 8-byte store)
+  uint16_t* pbase = p.preds + pd.pred_base;
+  const int sub = lane & 7;
+  for (uint32_t x = x0 + (tid >> 3); x < x1; x += nt >> 3) {
+    const uint32_t cell = scell[x - x0];
+    const int i = cell >> 16, m = cell & 0xffff;
+    const int n = i - j + 1, np = pad4(n);
+    uint16_t* q = pbase + scpo[x - x0];
+    for (int t0 = sub * 4; t0 < np; t0 += 32) {
+      uint16_t v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int t = t0 + e;
+        if (t < n) {
+          const int c = j - 1 + t;
+          const int s = seg[c * LP + i];
+          const int mp = s > m ? s : m;
+          const int wi = c * W + (mp >> 5);
+          v[e] = (uint16_t)(wpp[wi] + __popc(bmp[wi] & ((1u << (mp & 31)) - 1u)));
+        } else {
+          v[e] = (uint16_t)n_prev;
+        }
+      }
+      *reinterpret_cast<uint2*>(q + t0) =
+          make_uint2((uint32_t)v[0] | ((uint32_t)v[1] << 16), (uint32_t)v[2] | ((uint32_t)v[3] << 16));
+    }
   }
 }
 

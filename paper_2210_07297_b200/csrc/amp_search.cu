@@ -287,11 +287,26 @@ int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
     CK(upload(ctx->class_prog_d, ctx->class_prog.data(), ctx->class_prog.size()));
     return AMP_OK;
   }
-  DevBuf d_k, d_pair, d_scratch, d_sizes, d_preds_n, d_inner_n, d_pstart;
+  DevBuf d_k, d_pair, d_bm, d_bmoff, d_sizes, d_preds_n, d_inner_n, d_items;
   CK(upload(d_k, pk.data(), pk.size()));
   CK(upload(d_pair, ppair.data(), ppair.size()));
-  const uint64_t scratch_stride = 2ull * LP * ctx->max_M;
-  CK(d_scratch.ensure(sizeof(uint32_t) * scratch_stride * n));
+  // stage bitmaps of every program ([k][(L+1) * W] u32 each)
+  std::vector<uint64_t> bmoff(n);
+  uint64_t bm_total = 0;
+  for (int g = 0; g < n; ++g) {
+    bmoff[g] = bm_total;
+    bm_total += (uint64_t)pk[g] * LP * ((ctx->pairs[ppair[g]].M + 31) / 32);
+  }
+  const int W = (ctx->max_M + 31) / 32;
+  const size_t nw = (size_t)LP * W;
+  const size_t smem_c = sizeof(uint32_t) * 2 * nw + sizeof(uint16_t) * ((LP * LP + 1) & ~1) + sizeof(int) * 3 * LP;
+  const size_t smem_e = sizeof(uint32_t) * (4 * nw + 2 * kEmitSlice) + sizeof(uint64_t) * LP + sizeof(uint16_t) * LP * LP;
+  if (smem_c > 227 * 1024 || smem_e > 227 * 1024 || bm_total > (4ull << 30)) {
+    ctx->progs_ok = false;
+    return AMP_OK;
+  }
+  CK(d_bm.ensure(sizeof(uint32_t) * bm_total));
+  CK(upload(d_bmoff, bmoff.data(), bmoff.size()));
   CK(d_sizes.ensure(sizeof(uint32_t) * (size_t)n * LP));
   CK(d_preds_n.ensure(sizeof(uint64_t) * (size_t)n * LP));
   CK(d_inner_n.ensure(sizeof(uint64_t) * (size_t)n * LP));
@@ -301,24 +316,18 @@ int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
   ProgBuildParams bp{};
   bp.L = L;
   bp.n_progs = n;
-  bp.count_only = 1;
   bp.prog_k = d_k.as<int32_t>();
   bp.prog_pair = d_pair.as<int32_t>();
   bp.pairs = ctx->pairs_d.as<PairDev>();
   bp.seg = ctx->seg.as<uint16_t>();
-  bp.scratch = d_scratch.as<uint32_t>();
-  bp.scratch_stride = scratch_stride;
+  bp.bm = d_bm.as<uint32_t>();
+  bp.bm_off = d_bmoff.as<uint64_t>();
   bp.stage_sizes = d_sizes.as<uint32_t>();
   bp.stage_preds = d_preds_n.as<uint64_t>();
   bp.stage_inner = d_inner_n.as<uint64_t>();
-  const int W = (ctx->max_M + 31) / 32;
-  const size_t smem = sizeof(uint32_t) * 2 * (size_t)LP * W + sizeof(uint16_t) * LP * LP;
-  if (smem > 227 * 1024) {
-    ctx->progs_ok = false;
-    return AMP_OK;
-  }
-  CK(cudaFuncSetAttribute(k_build_progs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_build_progs<<<n, 512, smem, ctx->stream>>>(bp);
+  PhaseTimer tm;
+  CK(cudaFuncSetAttribute(k_prog_closure, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
+  k_prog_closure<<<n, 512, smem_c, ctx->stream>>>(bp);
   CK(cudaGetLastError());
   std::vector<uint32_t> sizes((size_t)n * LP);
   std::vector<uint64_t> pn((size_t)n * LP), pin((size_t)n * LP);
@@ -329,14 +338,14 @@ int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
   CK(cudaMemcpyAsync(pin.data(), d_inner_n.p, sizeof(uint64_t) * pin.size(),
                      cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  PhaseTimer tm;
-  tm.mark("K0b count pass");
+  tm.mark("K0b closure");
   ctx->prog_inner_raw.assign(n, 0.0);
   ctx->prog_stage_inner = pin;
   // layout
   std::vector<ProgDev> progs(n);
   std::vector<uint32_t> stage;
   std::vector<uint64_t> pstart((size_t)n * LP, 0);
+  std::vector<uint4> items;  // emit work: {g, j, first cell, end cell}
   uint64_t cell_total = 0, pred_total = 0;
   int max_cells = 1;
   uint64_t max_prog_cells = 1;
@@ -352,6 +361,8 @@ int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
     for (int j = 1; j <= k; ++j) {
       stage.push_back(acc);
       const uint32_t sz = sizes[(size_t)g * LP + j];
+      for (uint32_t x = 0; x < sz; x += kEmitSlice)
+        items.push_back(make_uint4((uint32_t)g, (uint32_t)j, x, std::min(sz, x + kEmitSlice)));
       acc += sz;
       mx = std::max(mx, sz);
     }
@@ -393,30 +404,26 @@ int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
   CK(upload(ctx->class_prog_d, ctx->class_prog.data(), ctx->class_prog.size()));
   DevBuf d_pst;
   CK(upload(d_pst, pstart.data(), pstart.size()));
+  CK(upload(d_items, items.data(), items.size()));
   CK(ctx->cells.ensure(sizeof(uint32_t) * cell_total));
   CK(ctx->cellpred.ensure(sizeof(uint32_t) * cell_total));
   CK(ctx->preds.ensure(sizeof(uint16_t) * (pred_total + 8)));
-  bp.count_only = 0;
   bp.progs = ctx->progs_d.as<ProgDev>();
   bp.cells = ctx->cells.as<uint32_t>();
   bp.cellpred = ctx->cellpred.as<uint32_t>();
   bp.preds = ctx->preds.as<uint16_t>();
   bp.stage = ctx->stage_d.as<uint32_t>();
   bp.pred_start = d_pst.as<uint64_t>();
+  bp.items = d_items.as<uint4>();
   tm.mark("K0b layout+alloc");
-  k_build_progs<<<n, 512, smem, ctx->stream>>>(bp);
+  CK(cudaFuncSetAttribute(k_prog_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e));
+  if (!items.empty()) k_prog_emit<<<(unsigned)items.size(), 512, smem_e, ctx->stream>>>(bp);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(ctx->stream));
-  tm.mark("K0b build pass");
-  if (tm.on) {
-    int kmax = 0, Mmax = 0;
-    for (int g = 0; g < n; ++g) {
-      kmax = std::max(kmax, pk[g]);
-      Mmax = std::max(Mmax, ctx->pairs[ppair[g]].M);
-    }
-    std::fprintf(stderr, "[amp create] K0b: %d programs, k <= %d, M <= %d, cells %llu, preds %llu, max |N_j| %d\n", n,
-                 kmax, Mmax, (unsigned long long)cell_total, (unsigned long long)pred_total, max_cells);
-  }
+  tm.mark("K0b emit");
+  if (tm.on)
+    std::fprintf(stderr, "[amp create] K0b: %d programs, cells %llu, preds %llu, max |N_j| %d, %zu emit CTAs\n", n,
+                 (unsigned long long)cell_total, (unsigned long long)pred_total, max_cells, items.size());
   ctx->progs_h = progs;
   return AMP_OK;
 }
