@@ -566,7 +566,11 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
     std::vector<double> vals;
     bool nan = false;
     {
+      // (runs of equal links are the common case: compare with the previous
+      // link before the set lookup)
       std::unordered_set<uint64_t> seen;
+      uint64_t last_bits = 0;
+      bool have_last = false;
       for (double v : bw) {
         if (std::isnan(v)) {
           nan = true;
@@ -575,6 +579,9 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
         uint64_t bits;
         std::memcpy(&bits, &v, sizeof bits);
         if (v == 0.0) bits = 0;  // +0 / -0 are one value
+        if (have_last && bits == last_bits) continue;
+        last_bits = bits;
+        have_last = true;
         if (seen.insert(bits).second) vals.push_back(v == 0.0 ? 0.0 : v);
         if (vals.size() > 255) break;  // codes disabled anyway
       }
@@ -622,15 +629,24 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
     bool ok = D > 32 && NN <= 4096 && std::getenv("AMP_NO_NODEBW") == nullptr;
     std::vector<double> nb(ok ? (size_t)NN * NN : 0, NAN);
     std::vector<uint8_t> set(ok ? (size_t)NN * NN : 0, 0);
-    for (int a = 0; a < D && ok; ++a)
-      for (int b = 0; b < D && ok; ++b) {
+    for (int a = 0; a < D && ok; ++a) {
+      const double* row = bw.data() + (size_t)a * D;
+      double* nrow = nb.data() + (size_t)nof[a] * NN;
+      uint8_t* srow = set.data() + (size_t)nof[a] * NN;
+      for (int b = 0; b < D; ++b) {
         if (a == b) continue;
-        const double v = bw[(size_t)a * D + b];
-        const size_t x = (size_t)nof[a] * NN + nof[b];
-        if (std::isnan(v)) ok = false;
-        else if (!set[x]) { nb[x] = v; set[x] = 1; }
-        else if (!(nb[x] == v)) ok = false;
+        const double v = row[b];
+        const int x = nof[b];
+        if (srow[x]) {
+          if (!(nrow[x] == v)) ok = false;  // (NaN != NaN: rejected too)
+        } else if (std::isnan(v)) {
+          ok = false;
+        } else {
+          nrow[x] = v;
+          srow[x] = 1;
+        }
       }
+    }
     for (int n1 = 0; n1 < NN && ok; ++n1)
       for (int n2 = n1 + 1; n2 < NN && ok; ++n2)
         if (set[(size_t)n1 * NN + n2] && !(nb[(size_t)n1 * NN + n2] == nb[(size_t)n2 * NN + n1])) ok = false;
