@@ -54,10 +54,10 @@ struct PhaseTimer {
 
 // Device buffers come from the device's stream-ordered memory pool, kept
 // warm across contexts (release threshold = max), so a create/run/destroy
-// cycle does not pay cudaMalloc/cudaFree.  Allocation and free are ordered
-// on the stream of the API call in flight (g_alloc_stream: the context's
-// stream); a fresh allocation is synchronised once so synchronous copies on
-// other streams may use it.
+// cycle does not pay cudaMalloc/cudaFree.  Allocation, free and every use
+// (uploads, memsets, kernels) are ordered on the stream of the API call in
+// flight (g_alloc_stream: the context's stream), so no allocation needs a
+// host synchronisation; an API call synchronises once before it returns.
 thread_local cudaStream_t g_alloc_stream = nullptr;
 
 void warm_pool(int device) {
@@ -88,7 +88,6 @@ struct DevBuf {
     release();
     s = g_alloc_stream;
     cudaError_t e = cudaMallocAsync(&p, n ? n : 16, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e == cudaSuccess) bytes = n;
     else p = nullptr;
     return e;
@@ -105,6 +104,24 @@ struct AllocStream {
   explicit AllocStream(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
   ~AllocStream() { g_alloc_stream = prev; }
 };
+
+// Per-device hand-over between contexts (the common create / run / destroy
+// cycle of plan() and of the e2e path): a destroyed context leaves its
+// (idle) stream, its signature hash table with its epoch state, and its trie
+// mark array (kept clear by every run) to the next context created on the
+// device, which then needs no stream creation and no table clearing.
+struct Recycled {
+  bool used = false;
+  cudaStream_t stream = nullptr;
+  void* tkey = nullptr;
+  size_t tkey_bytes = 0;
+  uint64_t T = 0, epoch = 0;
+  int esh = -1;
+  void* pres = nullptr;
+  size_t pres_bytes = 0;
+};
+std::mutex g_rec_mu;
+std::map<int, Recycled> g_rec;
 
 std::vector<int> divisors(int n) {
   std::vector<int> out;
@@ -183,6 +200,7 @@ struct amp_ctx {
   DevBuf dd_counters, prog_inner_d, dd_repcuts;
   DevBuf dd_tkey, dd_tval, dd_slot, dd_uniq, dd_nuniq, dd_sigkey;  // hash dedup
   uint64_t hash_epoch = 0, hash_T = 0;
+  int hash_esh = -1;  // epoch shift the table's tags were written with
   // DP shared across signature prefixes (amp_trie.cuh)
   bool trie = false;
   int trie_nq = 0, trie_U = 0;
@@ -254,7 +272,10 @@ template <class T>
 cudaError_t upload(DevBuf& b, const T* src, size_t n) {
   cudaError_t e = b.ensure(sizeof(T) * n);
   if (e != cudaSuccess) return e;
-  if (n) e = cudaMemcpy(b.p, src, sizeof(T) * n, cudaMemcpyHostToDevice);
+  // (stream-ordered after the allocation; a pageable source is staged
+  // before the call returns, a pinned one is read before the API call's
+  // final synchronisation)
+  if (n) e = cudaMemcpyAsync(b.p, src, sizeof(T) * n, cudaMemcpyHostToDevice, g_alloc_stream);
   return e;
 }
 
@@ -419,7 +440,7 @@ int build_programs(amp_ctx* ctx, const std::vector<uint16_t>& seg_h) {
   CK(cudaFuncSetAttribute(k_prog_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e));
   if (!items.empty()) k_prog_emit<<<(unsigned)items.size(), 512, smem_e, ctx->stream>>>(bp);
   CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(ctx->stream));
+  if (tm.on) CK(cudaStreamSynchronize(ctx->stream));
   tm.mark("K0b emit");
   if (tm.on)
     std::fprintf(stderr, "[amp create] K0b: %d programs, cells %llu, preds %llu, max |N_j| %d, %zu emit CTAs\n", n,
@@ -488,7 +509,24 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
                 "device is sm_" + std::to_string(prop.major * 10 + prop.minor) +
                     "; this build contains sm_100a kernels only");
   warm_pool(ctx->device);
-  CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  {
+    std::lock_guard<std::mutex> lk(g_rec_mu);
+    Recycled& r = g_rec[ctx->device];
+    if (r.used && std::getenv("AMP_NO_RECYCLE") == nullptr) {
+      ctx->stream = r.stream;
+      ctx->dd_tkey.p = r.tkey;
+      ctx->dd_tkey.bytes = r.tkey_bytes;
+      ctx->dd_tkey.s = r.stream;
+      ctx->hash_T = r.T;
+      ctx->hash_epoch = r.epoch;
+      ctx->hash_esh = r.esh;
+      ctx->tr_pres.p = r.pres;
+      ctx->tr_pres.bytes = r.pres_bytes;
+      ctx->tr_pres.s = r.stream;
+      r = Recycled{};
+    }
+  }
+  if (!ctx->stream) CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   g_alloc_stream = ctx->stream;
   CK(cudaEventCreate(&ctx->ev0));
   CK(cudaEventCreate(&ctx->ev1));
@@ -972,7 +1010,6 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
       ctx->tr_build_grid = std::min(ob, 2) * prop.multiProcessorCount;
       ctx->tr_dp_grid = od * prop.multiProcessorCount;
       CK(ctx->tr_partial.ensure(sizeof(uint32_t) * ctx->tr_build_grid));
-      CK(cudaStreamSynchronize(ctx->stream));
     }
   }
   if (ctx->multi_b == 2) ctx->eval_fn = (const void*)k_dp_multi<2>;
@@ -1010,6 +1047,7 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   if (!sparse && !ctx->w_in_smem) CK(ctx->wtab.ensure(w_b * n_ctas));
   if (ctx->v_stride) CK(ctx->vbuf.ensure(sizeof(double) * ctx->v_stride * n_ctas));
   CK(ctx->counter.ensure(sizeof(unsigned long long)));
+  CK(cudaStreamSynchronize(ctx->stream));  // (the caller's arrays are read before create returns)
   tm.mark("launch shape+scratch");
   return AMP_OK;
 }
@@ -1540,13 +1578,14 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
       CK(cudaMemsetAsync(ctx->dd_tkey.p, 0xff, sizeof(uint64_t) * T, ctx->stream));
     } else {
       const uint64_t max_epoch = (1ull << (64 - esh)) - 1;
-      if (grown || ctx->hash_T != T || ctx->hash_epoch >= max_epoch) {
+      if (grown || ctx->hash_T != T || ctx->hash_esh != esh || ctx->hash_epoch >= max_epoch) {
         CK(cudaMemsetAsync(ctx->dd_tkey.p, 0, sizeof(uint64_t) * T, ctx->stream));
         ctx->hash_epoch = 0;
       }
       ++ctx->hash_epoch;
     }
     ctx->hash_T = T;
+    ctx->hash_esh = esh;
     CK(cudaMemsetAsync(ctx->dd_nuniq.p, 0, 2 * sizeof(unsigned long long), ctx->stream));
     hp = HashParams{};
     hp.work = ep.work;
@@ -2086,11 +2125,33 @@ void amp_search_destroy(amp_ctx* ctx) {
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->ev2) cudaEventDestroy(ctx->ev2);
   for (cudaEvent_t e : ctx->kev) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->tev) cudaEventDestroy(e);
   if (ctx->aux) cudaStreamSynchronize(ctx->aux);
   if (ctx->aux_start) cudaEventDestroy(ctx->aux_start);
   if (ctx->aux_done) cudaEventDestroy(ctx->aux_done);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   cudaStream_t st = ctx->stream;
+  if (st && ctx->err.empty() && std::getenv("AMP_NO_RECYCLE") == nullptr) {
+    // hand the stream, hash table and clear trie marks to the device's next context
+    std::lock_guard<std::mutex> lk(g_rec_mu);
+    Recycled& r = g_rec[ctx->device];
+    if (!r.used) {
+      r.used = true;
+      r.stream = st;
+      r.tkey = ctx->dd_tkey.p;
+      r.tkey_bytes = ctx->dd_tkey.bytes;
+      r.T = ctx->hash_T;
+      r.epoch = ctx->hash_epoch;
+      r.esh = ctx->hash_esh;
+      r.pres = ctx->tr_pres.p;
+      r.pres_bytes = ctx->tr_pres.bytes;
+      ctx->dd_tkey.p = nullptr;
+      ctx->dd_tkey.bytes = 0;
+      ctx->tr_pres.p = nullptr;
+      ctx->tr_pres.bytes = 0;
+      st = nullptr;
+    }
+  }
   delete ctx;  // buffers return to the pool, ordered on the context stream
   if (st) cudaStreamDestroy(st);
 }
