@@ -37,7 +37,8 @@ struct PairDev {
 struct ClassDev {
   int32_t pp, dp, tmp, mbs;
   int32_t gas, pair;
-  int32_t pad0, pad1;
+  int32_t crow;  // row of the class's shape in the code table (EvalParams::ctab), -1: none
+  int32_t pad1;
 };
 
 // Contiguous run of candidate indices of one class, handed out
@@ -200,6 +201,12 @@ struct EvalParams {
   // shared by the classes, or NULL
   const uint64_t* perm_tab;
   uint64_t perm_n;
+  // |D| = 16 full shapes, codes < 16: the link codes of placement pl under
+  // the shape of row crow, ctab[crow * perm_n + pl] = {x: the edge code of
+  // every (boundary q, replica r) at 4 bits (q * dp + r) (min over shards),
+  // y: the all-reduce group code of every stage j at 4 bits j (min over the
+  // group's pairs)} (k_code_table), or NULL
+  const ulonglong2* ctab;
 };
 
 // std::min(a, b) with the reference's argument order: (b < a) ? b : a.

@@ -181,6 +181,9 @@ struct amp_ctx {
   bool bw_positive = false;  // smallest distinct bandwidth > 0
   DevBuf bwcode, bwval, qtab, cellrec, cut2tab, rsum_t, rsum_p;
   DevBuf node_of, nodebw;  // node-determined bandwidths (n_nodes > 0)
+  std::vector<int32_t> row_shape;  // code-table row -> shape key pp * 1024 + dp * 32 + tmp
+  DevBuf row_shape_d, ctab;        // the code table (k_code_table), built for ctab_P placements
+  uint64_t ctab_P = 0;
   int n_nodes = 0;
   DevBuf perm_tab;         // placements of p in [0, perm_n) (|D| = 16), built on first use
   uint64_t perm_n = 0;
@@ -700,6 +703,18 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   CK(upload(ctx->act, act.data(), act.size()));
   CK(upload(ctx->bw, bw.data(), bw.size()));
   CK(upload(ctx->base_order, order.data(), order.size()));
+  // code-table rows: the distinct full 16-device shapes (K_place / K_est
+  // shape kernels read the placement's link codes by (shape, placement))
+  ctx->row_shape.clear();
+  for (ClassDev& c : ctx->classes) {
+    c.crow = -1;
+    if (D != 16 || c.pp * c.dp * c.tmp != 16) continue;
+    const int key = c.pp * 1024 + c.dp * 32 + c.tmp;
+    auto it = std::find(ctx->row_shape.begin(), ctx->row_shape.end(), key);
+    c.crow = (int32_t)(it - ctx->row_shape.begin());
+    if (it == ctx->row_shape.end()) ctx->row_shape.push_back(key);
+  }
+  if (!ctx->row_shape.empty()) CK(upload(ctx->row_shape_d, ctx->row_shape.data(), ctx->row_shape.size()));
   CK(upload(ctx->cls_d, ctx->classes.data(), ctx->classes.size()));
 
   tm.mark("encode+uploads");
@@ -1523,6 +1538,30 @@ int launch_evaluate(amp_ctx* ctx, const std::vector<Segment>* segs, const uint64
   for (const auto& c : ctx->classes) shape16 = shape16 && c.pp * c.dp * c.tmp == 16;
   ep.est_fast = shape16 && est_thread && ep.cut2tab && ep.rsum_t && !ep.all_cuts && !ep.all_stage &&
                 !ep.all_edge && !ep.all_place && !d_given_cuts && !ctx->wide;
+  // the code table of every (shape, placement): the shape kernels need it;
+  // codes < 16 (4 bits each), at most 4 GB (else the generic bodies run)
+  ep.ctab = nullptr;
+  if (ep.est_fast) {
+    const uint64_t tb = sizeof(ulonglong2) * (uint64_t)ctx->row_shape.size() * ctx->P;
+    if (ctx->n_codes <= 16 && tb <= (4ull << 30) && !ctx->row_shape.empty() &&
+        std::getenv("AMP_NO_CTAB") == nullptr) {
+      if (ctx->ctab_P != ctx->P) {
+        CK(ctx->ctab.ensure(tb));
+        const uint64_t n = (uint64_t)ctx->row_shape.size() * ctx->P;
+        const int gc = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->sms * 8);
+        k_code_table<<<gc, 256, 0, ctx->stream>>>(ep, ctx->row_shape_d.as<int32_t>(), (int)ctx->row_shape.size(),
+                                                   ctx->ctab.as<ulonglong2>());
+        CK(cudaGetLastError());
+        DBG_SYNC("k_code_table");
+        ctx->launches += 1;
+        ctx->ctab_P = ctx->P;
+      }
+      ep.ctab = ctx->ctab.as<ulonglong2>();
+      ep.placep = nullptr;  // (K_est reads the codes, not the placement)
+    } else {
+      ep.est_fast = false;
+    }
+  }
   // the boundary codes are read by K_dp without the trie, the sort dedup
   // path and K_est's pp == 2 items placed by K_place; with the hash dedup on
   // K_place's signature keys, the trie and the fused light path, nothing

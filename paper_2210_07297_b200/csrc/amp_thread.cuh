@@ -69,17 +69,26 @@ __device__ void place_smem_init(const EvalParams& p, PlaceSmem& S) {
 // signature key.  Positive bandwidths only (no boundary can fail).
 template <int PP, int DPn, int TMP>
 __device__ __forceinline__ uint64_t codes_shape(const EvalParams& p, const uint8_t* code, uint64_t perm,
-                                                uint64_t u, bool store, uint64_t key, int& code0) {
+                                                bool has_cw, ulonglong2 cw, uint64_t u, bool store,
+                                                uint64_t key, int& code0) {
 #pragma unroll
   for (int q = 0; q < PP - 1; ++q) {
     int cm = 255;
+    if (has_cw) {  // the placement's per-replica edge codes (k_code_table)
 #pragma unroll
-    for (int r = 0; r < DPn && cm; ++r)
-#pragma unroll
-      for (int s = 0; s < TMP && cm; ++s) {
-        const int cc = code[nib(perm, (q * DPn + r) * TMP + s) * 16 + nib(perm, ((q + 1) * DPn + r) * TMP + s)];
+      for (int r = 0; r < DPn; ++r) {
+        const int cc = (int)((cw.x >> (4 * (q * DPn + r))) & 0xf);
         cm = cc < cm ? cc : cm;
       }
+    } else {
+#pragma unroll
+      for (int r = 0; r < DPn && cm; ++r)
+#pragma unroll
+        for (int s = 0; s < TMP && cm; ++s) {
+          const int cc = code[nib(perm, (q * DPn + r) * TMP + s) * 16 + nib(perm, ((q + 1) * DPn + r) * TMP + s)];
+          cm = cc < cm ? cc : cm;
+        }
+    }
     if (q == 0) code0 = cm;
     key = (key << p.sig_code_bits) | (uint64_t)cm;
     if (store) {
@@ -88,6 +97,44 @@ __device__ __forceinline__ uint64_t codes_shape(const EvalParams& p, const uint8
     }
   }
   return key;
+}
+
+// The code-table entry of a placement under shape (PP, DPn, TMP): x = the
+// edge code of every (boundary q, replica r), min over the shards
+// (cost_model.cpp:164-174 before the min over replicas), y = the all-reduce
+// group code of every stage (min over the group's device pairs,
+// cost_model.cpp:122-143).  Codes < 16.
+template <int PP, int DPn, int TMP>
+__device__ __forceinline__ ulonglong2 ctab_entry(const uint8_t* code, uint64_t perm) {
+  uint64_t x = 0, y = 0;
+#pragma unroll
+  for (int q = 0; q < PP - 1; ++q)
+#pragma unroll
+    for (int r = 0; r < DPn; ++r) {
+      int cm = 255;
+#pragma unroll
+      for (int s = 0; s < TMP; ++s) {
+        const int cc = code[nib(perm, (q * DPn + r) * TMP + s) * 16 + nib(perm, ((q + 1) * DPn + r) * TMP + s)];
+        cm = cc < cm ? cc : cm;
+      }
+      x |= (uint64_t)cm << (4 * (q * DPn + r));
+    }
+  if (DPn > 1)
+#pragma unroll
+    for (int j = 0; j < PP; ++j) {
+      int cm = 255;
+#pragma unroll
+      for (int s = 0; s < TMP; ++s)
+#pragma unroll
+        for (int r1 = 0; r1 < DPn; ++r1)
+#pragma unroll
+          for (int r2 = r1 + 1; r2 < DPn; ++r2) {
+            const int cc = code[nib(perm, (j * DPn + r1) * TMP + s) * 16 + nib(perm, (j * DPn + r2) * TMP + s)];
+            cm = cc < cm ? cc : cm;
+          }
+      y |= (uint64_t)cm << (4 * j);
+    }
+  return make_ulonglong2(x, y);
 }
 
 // K_place's work for chunk item u: decode, early failures, placement,
@@ -100,7 +147,8 @@ __device__ __forceinline__ uint64_t codes_shape(const EvalParams& p, const uint8
 template <int DT, bool FAST = false, bool DECODE_ONLY = false>
 __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& S, uint64_t u,
                                           bool store, CandWork& w, uint64_t& perm, int& code0,
-                                          uint64_t* sig = nullptr, int* seg_hint = nullptr) {
+                                          uint64_t* sig = nullptr, int* seg_hint = nullptr,
+                                          ulonglong2* cwo = nullptr) {
   if (sig) *sig = ~0ull;
   const int D = DT > 0 ? DT : p.D, maxpp = p.max_pp;
   uint64_t index, out, pl;
@@ -126,7 +174,7 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
     if constexpr (FAST) {
       // (the shape kernels run only with the placement table: P = 1 or the
       //  table of every placement index; no per-candidate shuffle)
-      if (pl != 0 && (store || pp != 1 || dp != 1)) perm = p.perm_tab[pl];
+      if (pl != 0 && !p.ctab && (store || pp != 1 || dp != 1)) perm = p.perm_tab[pl];
     } else if (p.given_place) {  // caller placement (anneal proposals, evaluate_placed)
       const int32_t* g = p.given_place + (p.t0 + u) * D;
       perm = 0;
@@ -161,6 +209,12 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
       }
     }
     if (store && p.placep) p.placep[u] = perm;
+    ulonglong2 cwv = make_ulonglong2(0, 0);
+    const bool has_cw = FAST && p.ctab != nullptr;
+    if (has_cw) {
+      if (pp > 1 || dp > 1) cwv = p.ctab[(uint64_t)cl.crow * p.P + pl];
+      if (cwo) *cwo = cwv;
+    }
     if (store && p.need_place_rows) {
       int32_t* prow = p.placeb + u * D;
       for (int x = 0; x < D; ++x) prow[x] = nib(perm, x);
@@ -175,7 +229,7 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
       switch (pp * 1024 + dp * 32 + tmp) {
 #define AMP_SHAPE(a, b, c)                                                        \
   case a * 1024 + b * 32 + c:                                                     \
-    key = codes_shape<a, b, c>(p, S.code, perm, u, store, key, code0); \
+    key = codes_shape<a, b, c>(p, S.code, perm, has_cw, cwv, u, store, key, code0); \
     break;
         AMP_SHAPE(1, 1, 16) AMP_SHAPE(1, 2, 8) AMP_SHAPE(1, 4, 4) AMP_SHAPE(1, 8, 2) AMP_SHAPE(1, 16, 1)
         AMP_SHAPE(2, 1, 8) AMP_SHAPE(2, 2, 4) AMP_SHAPE(2, 4, 2) AMP_SHAPE(2, 8, 1)
@@ -311,6 +365,39 @@ __global__ void k_perm_table(EvalParams p, uint64_t* out, uint64_t n) {
   }
 }
 
+// The code table (EvalParams::ctab): for every shape row and placement
+// index, the placement's edge and all-reduce group codes (ctab_entry), so
+// K_place / K_est of every class of that shape read one 16-byte entry
+// instead of redoing the code minima per candidate.  |D| = 16, full shapes.
+__global__ void k_code_table(EvalParams p, const int32_t* row_shape, int n_rows, ulonglong2* out) {
+  __shared__ PlaceSmem S;
+  place_smem_init(p, S);
+  __syncthreads();
+  const uint64_t P = p.P, n = (uint64_t)n_rows * P;
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(x / P);
+    const uint64_t pl = x - (uint64_t)row * P;
+    const uint64_t perm = pl == 0 ? S.base_perm : p.perm_tab[pl];
+    ulonglong2 e = make_ulonglong2(0, 0);
+    switch (row_shape[row]) {
+#define AMP_SHAPE(a, b, c)            \
+  case a * 1024 + b * 32 + c:         \
+    e = ctab_entry<a, b, c>(S.code, perm); \
+    break;
+      AMP_SHAPE(1, 1, 16) AMP_SHAPE(1, 2, 8) AMP_SHAPE(1, 4, 4) AMP_SHAPE(1, 8, 2) AMP_SHAPE(1, 16, 1)
+      AMP_SHAPE(2, 1, 8) AMP_SHAPE(2, 2, 4) AMP_SHAPE(2, 4, 2) AMP_SHAPE(2, 8, 1)
+      AMP_SHAPE(4, 1, 4) AMP_SHAPE(4, 2, 2) AMP_SHAPE(4, 4, 1)
+      AMP_SHAPE(8, 1, 2) AMP_SHAPE(8, 2, 1)
+      AMP_SHAPE(16, 1, 1)
+#undef AMP_SHAPE
+      default:
+        break;
+    }
+    out[x] = e;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K_est shape kernels: the estimate of one candidate of class shape
 // (PP, DPn, TMP) (pp * dp * tmp == 16) with every loop unrolled — nibble
@@ -323,10 +410,9 @@ __global__ void k_perm_table(EvalParams p, uint64_t* out, uint64_t n) {
 // chain of the slowest replica, the parameter ceiling and dpsync_time: each
 // keeps its own sequential order, they only share the stage's two loads.
 template <int PP, int DPn, int TMP>
-__device__ __forceinline__ void est_shape(const EvalParams& p, const uint8_t* codeS, const CandWork& w,
-                                          const ClassDev& cl, uint64_t u, bool fused, uint64_t perm,
-                                          int code0, int& fc, double& pipeline, double& dpsync) {
-  constexpr int D = 16;
+__device__ __forceinline__ void est_shape(const EvalParams& p, const ulonglong2 cw, const CandWork& w,
+                                          const ClassDev& cl, uint64_t u, bool fused, int code0, int& fc,
+                                          double& pipeline, double& dpsync) {
   const int L = p.L, LP = L + 1, maxpp = p.max_pp;
   int cuts[PP + 1];
   if (PP >= 3) {  // the signature run's cuts (memoised DP) or this item's
@@ -364,12 +450,7 @@ __device__ __forceinline__ void est_shape(const EvalParams& p, const uint8_t* co
     double esum = 0.0;
 #pragma unroll
     for (int q = 0; q < PP - 1; ++q) {
-      int cm = 255;
-#pragma unroll
-      for (int s = 0; s < TMP; ++s) {
-        const int cc = codeS[nib(perm, (q * DPn + r) * TMP + s) * D + nib(perm, ((q + 1) * DPn + r) * TMP + s)];
-        cm = cc < cm ? cc : cm;
-      }
+      const int cm = (int)((cw.x >> (4 * (q * DPn + r))) & 0xf);  // (min over the shards)
       esum = esum + qt[(size_t)cm * L + cuts[q + 1]];
     }
     emax = emax < esum ? esum : emax;
@@ -390,16 +471,7 @@ __device__ __forceinline__ void est_shape(const EvalParams& p, const uint8_t* co
     sum = sum + stj;
     if (p.has_ceiling) worst_p = std_max(worst_p, spj / TMP);
     if (DPn != 1) {  // dpsync: the stage's minimum-bandwidth group (bw_positive)
-      int cm = 255;
-#pragma unroll
-      for (int s = 0; s < TMP && cm; ++s)
-#pragma unroll
-        for (int r1 = 0; r1 < DPn && cm; ++r1)
-#pragma unroll
-          for (int r2 = r1 + 1; r2 < DPn && cm; ++r2) {
-            const int cc = codeS[nib(perm, (j * DPn + r1) * TMP + s) * D + nib(perm, (j * DPn + r2) * TMP + s)];
-            cm = cc < cm ? cc : cm;
-          }
+      const int cm = (int)((cw.y >> (4 * j)) & 0xf);
       const double b = p.bwval[cm];
       const double message = spj * p.bpp / TMP;
       worst = std_max(worst, 2.0 * (double)(DPn - 1) * message / ((double)DPn * b));
@@ -463,7 +535,8 @@ __device__ __forceinline__ void est_fast_item(const EvalParams& p, const PlaceSm
   CandWork w;
   uint64_t perm = 0;
   int code0 = 0;
-  if (fused) place_one<DT, true>(p, PS, u, false, w, perm, code0, nullptr, seg_hint);
+  ulonglong2 cw = make_ulonglong2(0, 0);  // the placement's link codes (k_code_table)
+  if (fused) place_one<DT, true>(p, PS, u, false, w, perm, code0, nullptr, seg_hint, &cw);
   else if (p.skip_work) place_one<DT, true, true>(p, PS, u, false, w, perm, code0, nullptr, seg_hint);
   else w = p.work[u];
   const ClassDev cl = p.cls[w.cls];
@@ -471,11 +544,12 @@ __device__ __forceinline__ void est_fast_item(const EvalParams& p, const PlaceSm
   double pipeline = CUDART_NAN, dpsync = CUDART_NAN;
   if (fc == 0) {
     // (a dp == 1, pp >= 3 item with the per-run estimate needs no placement)
-    if (!fused && !(p.run_pipe && cl.dp == 1 && cl.pp >= 3)) perm = p.placep[u];
+    if (!fused && !(p.run_pipe && cl.dp == 1 && cl.pp >= 3))
+      cw = p.ctab[(uint64_t)cl.crow * p.P + (w.index - (uint64_t)w.cls * p.P)];
     switch (cl.pp * 1024 + cl.dp * 32 + cl.tmp) {
-#define AMP_SHAPE(a, b, c)                                                                  \
-  case a * 1024 + b * 32 + c:                                                               \
-    est_shape<a, b, c>(p, PS.code, w, cl, u, fused, perm, code0, fc, pipeline, dpsync); \
+#define AMP_SHAPE(a, b, c)                                                    \
+  case a * 1024 + b * 32 + c:                                                 \
+    est_shape<a, b, c>(p, cw, w, cl, u, fused, code0, fc, pipeline, dpsync); \
     break;
       AMP_SHAPE(1, 1, 16) AMP_SHAPE(1, 2, 8) AMP_SHAPE(1, 4, 4) AMP_SHAPE(1, 8, 2) AMP_SHAPE(1, 16, 1)
       AMP_SHAPE(2, 1, 8) AMP_SHAPE(2, 2, 4) AMP_SHAPE(2, 4, 2) AMP_SHAPE(2, 8, 1)
