@@ -212,6 +212,8 @@ struct amp_ctx {
   std::vector<uint32_t> stage_h;  // host copy of the program stage starts
   std::vector<uint64_t> prog_stage_inner;  // [prog][L+1] unpadded (cell, cut) pairs of stage j
   std::vector<int32_t> root_cls_h;         // heavy classes (trie roots) in class order
+  DevBuf tr_ghist, tr_gpart, tr_sortk, tr_sortv;  // k_trie_build_sorted scratch
+  bool tr_sorted = true;                            // sorted-key trie build (AMP_TRIE_LEVELS=1: level build)
   DevBuf v1off_d, v1g_d, dd_rep_key, dd_nid, tr_state, tr_pres, tr_cid, tr_partial, tr_npar,
       tr_ncls, tr_ncode, tr_nb, tr_nK, tr_vbase, tr_bbase, tr_rbase, tr_tbase, tr_nxc, tr_tstage, tr_v0, tr_bp,
       tr_done, tr_tiles,
@@ -1018,13 +1020,20 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
       CK(cudaFuncSetAttribute(k_trie_dp, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->tr_smem));
       const int bsm = (int)(4 * sizeof(unsigned long long) * NC);
       CK(cudaFuncSetAttribute(k_trie_build, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm));
+      CK(cudaFuncSetAttribute(k_trie_build_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm));
       int ob = 0, od = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k_trie_build, kBuildThreads, bsm));
+      int ob2 = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob2, k_trie_build_sorted, kBuildThreads, bsm));
+      ob = std::min(ob, ob2);
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&od, k_trie_dp, kTrieThreads, ctx->tr_smem));
       if (ob < 1 || od < 1) return fail(ctx, AMP_E_UNSUPPORTED, "trie kernels do not fit on an SM");
       ctx->tr_build_grid = std::min(ob, 2) * prop.multiProcessorCount;
       ctx->tr_dp_grid = od * prop.multiProcessorCount;
       CK(ctx->tr_partial.ensure(sizeof(uint32_t) * ctx->tr_build_grid));
+      CK(ctx->tr_ghist.ensure(sizeof(uint32_t) * 256 * ctx->tr_build_grid));
+      CK(ctx->tr_gpart.ensure(sizeof(uint32_t) * kTrieMaxD1 * ctx->tr_build_grid));
+      ctx->tr_sorted = std::getenv("AMP_TRIE_LEVELS") == nullptr;
     }
   }
   if (ctx->multi_b == 2) ctx->eval_fn = (const void*)k_dp_multi<2>;
@@ -1253,6 +1262,19 @@ int run_sig_dp(amp_ctx* ctx, EvalParams& ep, const HashParams& hp) {
     tp.cid = ctx->tr_cid.as<uint32_t>();
     tp.pres_cap = pres_cap;
     tp.partial = ctx->tr_partial.as<uint32_t>();
+    if (ctx->tr_sorted) {
+      CK(ctx->tr_sortk.ensure(sizeof(uint64_t) * 2 * C));
+      CK(ctx->tr_sortv.ensure(sizeof(uint32_t) * 2 * C));
+      tp.sk[0] = ctx->tr_sortk.as<uint64_t>();
+      tp.sk[1] = tp.sk[0] + C;
+      tp.sv[0] = ctx->tr_sortv.as<uint32_t>();
+      tp.sv[1] = tp.sv[0] + C;
+      tp.ghist = ctx->tr_ghist.as<uint32_t>();
+      tp.gpart = ctx->tr_gpart.as<uint32_t>();
+      int clsb = 0;
+      while ((1 << clsb) < NC) ++clsb;
+      tp.kbits = tp.nq * tp.cb + clsb;
+    }
     tp.npar = ctx->tr_npar.as<uint32_t>();
     tp.ncls = ctx->tr_ncls.as<uint16_t>();
     tp.ncode = ctx->tr_ncode.as<uint8_t>();
@@ -1288,7 +1310,8 @@ int run_sig_dp(amp_ctx* ctx, EvalParams& ep, const HashParams& hp) {
     CK(cudaMemsetAsync(ctx->tr_nb.p, 0, sizeof(uint32_t) * kTrieMaxD1 * NC, ctx->stream));
     CK(cudaMemsetAsync(ctx->tr_nK.p, 0, sizeof(uint32_t) * kTrieMaxD1 * NC, ctx->stream));
     void* args[] = {&tp};
-    CK(cudaLaunchCooperativeKernel((const void*)k_trie_build, dim3(ctx->tr_build_grid), dim3(kBuildThreads),
+    CK(cudaLaunchCooperativeKernel(ctx->tr_sorted ? (const void*)k_trie_build_sorted : (const void*)k_trie_build,
+                                   dim3(ctx->tr_build_grid), dim3(kBuildThreads),
                                    args, 4 * sizeof(unsigned long long) * NC, ctx->stream));
     DBG_SYNC("k_trie_build");
     while ((int)ctx->tev.size() < ctx->tev_used + 2) {

@@ -55,6 +55,7 @@ struct TrieState {
   uint32_t ovf;                     // capacity exceeded: signature-mode K_dp instead
   uint32_t next_tile;               // K_trie_dp dispenser
   uint32_t bar_count, bar_pad;      // K_trie_build grid barrier (arrivals)
+  unsigned long long dtot[kTrieMaxD1][4];  // per-depth plan totals: tiles, values, argmins, runs
 };
 
 // Per (class, stage j) facts of the class's pruned program and its tile
@@ -93,7 +94,7 @@ struct TrieTile {   // one K_trie_dp work item
 struct TrieParams {
   // signatures: the distinct keys of the chunk's hash table
   const unsigned long long* n_sig;  // device count
-  const uint32_t* uniq;             // [n_sig] slots
+  uint32_t* uniq;                   // [n_sig] slots (the sorted build rewrites it: slot of signature i)
   const unsigned long long* tkey;
   uint32_t* tval;                   // slot -> first item, rewritten to slot -> signature
   int32_t key_shift;                // epoch tag position (64: none)
@@ -143,6 +144,13 @@ struct TrieParams {
   const uint64_t* v1off;
   uint8_t* repcuts;                 // [n_sig][max_pp + 1] cuts per signature
   unsigned long long* exec;         // [2]: DP instances, inner iterations (or NULL)
+  // k_trie_build_sorted: radix-sort ping-pong buffers [n], per-CTA digit
+  // histograms [grid][256] and per-depth start counts [grid][64]
+  uint64_t* sk[2];
+  uint32_t* sv[2];
+  uint32_t* ghist;
+  uint32_t* gpart;
+  int32_t kbits, pad_s;             // significant key bits (class + codes)
 };
 
 __device__ __forceinline__ int trie_cls(const TrieParams& p, uint64_t k) { return (int)(k >> (p.nq * p.cb)); }
@@ -273,7 +281,49 @@ __device__ void plan_level(const TrieParams& p, int d, uint32_t total, uint64_t 
   __syncthreads();
 }
 
-// The trie of the chunk's signatures and the tile list of its DP.
+// The tile list of all depths (after the level plans); run counters cleared.
+__device__ void build_tile_list(const TrieParams& p, uint64_t gtid, uint64_t gstride) {
+  TrieState* st = p.st;
+  const uint32_t T = (uint32_t)st->tile_bump;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->tile_off[p.nq + 1] = T;
+    st->next_tile = 0;
+  }
+  for (uint64_t r = gtid; r < st->run_bump; r += gstride) p.done[r] = 0;
+  for (uint64_t t = gtid; t < T; t += gstride) {
+    int d = 1;
+    while (d < p.nq && st->tile_off[d + 1] <= t) ++d;
+    const uint32_t tt = (uint32_t)t - st->tile_off[d];
+    const uint32_t* tb = p.tbase + (size_t)d * (p.n_cls + 1);
+    int lo = 0, hi = p.n_cls - 1;  // last class with tbase <= tt
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tb[mid] <= tt) lo = mid;
+      else hi = mid - 1;
+    }
+    const int c = lo;
+    const TrieStage ts = p.tstage[(size_t)c * (p.max_pp + 1) + d + 1];
+    const uint32_t chunks = p.nxc[(size_t)d * p.n_cls + c];
+    const uint32_t lt = tt - tb[c], run = lt / chunks, cc = lt - run * chunks;
+    const uint32_t nbc = p.nb[(size_t)d * p.n_cls + c], K = p.nK[(size_t)d * p.n_cls + c];
+    TrieTile tl;
+    tl.n0 = nbc + run * ts.tn;
+    tl.c = (uint16_t)c;
+    tl.d = (uint8_t)d;
+    tl.pad = 0;
+    tl.nn = (uint16_t)min(ts.tn, nbc + K - tl.n0);
+    const uint32_t xc = (ts.n + chunks - 1) / chunks;
+    tl.x0 = (uint16_t)(cc * xc);
+    tl.x1 = (uint16_t)min(ts.n, (cc + 1) * xc);
+    tl.run = run;
+    tl.pad2 = 0;
+    p.tiles[t] = tl;
+  }
+}
+
+// The trie of the chunk's signatures and the tile list of its DP, level by
+// level (the comparison path, AMP_TRIE_LEVELS=1; the default is
+// k_trie_build_sorted below).
 __global__ void __launch_bounds__(kBuildThreads) k_trie_build(TrieParams p) {
   extern __shared__ unsigned long long build_sm[];  // [4][n_cls] (CTA 0's plans)
   __shared__ uint32_t sm[32], wsum[32];
@@ -420,42 +470,318 @@ __global__ void __launch_bounds__(kBuildThreads) k_trie_build(TrieParams p) {
 #pragma unroll
   for (int q = 0; q < kBuildReg; ++q)
     if (rdep[q] >= 0) p.nid[gtid + q * gstride] = rnid[q];
-  // ---- tile list of all depths; run counters cleared -----------------------
-  const uint32_t T = (uint32_t)st->tile_bump;
-  if (blockIdx.x == 0 && tid == 0) {
-    st->tile_off[p.nq + 1] = T;
-    st->next_tile = 0;
-  }
-  for (uint64_t r = gtid; r < st->run_bump; r += gstride) p.done[r] = 0;
-  for (uint64_t t = gtid; t < T; t += gstride) {
-    int d = 1;
-    while (d < p.nq && st->tile_off[d + 1] <= t) ++d;
-    const uint32_t tt = (uint32_t)t - st->tile_off[d];
-    const uint32_t* tb = p.tbase + (size_t)d * (p.n_cls + 1);
-    int lo = 0, hi = p.n_cls - 1;  // last class with tbase <= tt
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (tb[mid] <= tt) lo = mid;
-      else hi = mid - 1;
+  build_tile_list(p, gtid, gstride);
+}
+
+// k_trie_build_sorted, the plan of depth d relative to the depth's own
+// bases (the depths are planned in parallel, one CTA each): per class the
+// node runs, cell chunks, tiles and table sizes; the per-depth totals go to
+// st->dtot[d].
+__device__ void plan_depth(const TrieParams& p, int d, unsigned long long* sm4) {
+  const int NC = p.n_cls, tid = threadIdx.x;
+  unsigned long long* s_tiles = sm4;
+  unsigned long long* s_v = sm4 + NC;
+  unsigned long long* s_b = sm4 + 2 * NC;
+  unsigned long long* s_r = sm4 + 3 * NC;
+  uint32_t* nb = p.nb + (size_t)d * NC;
+  uint32_t* nK = p.nK + (size_t)d * NC;
+  uint32_t* nx = p.nxc + (size_t)d * NC;
+  for (int c = tid; c < NC; c += blockDim.x) {
+    const uint32_t lo = __ldcg(nb + c), K = __ldcg(nK + c) - lo;  // [first node, end) -> count
+    nK[c] = K;
+    uint32_t runs = 0, chunks = 1;
+    unsigned long long vs = 0, bs = 0;
+    if (K) {
+      const TrieStage ts = p.tstage[(size_t)c * (p.max_pp + 1) + d + 1];
+      runs = (K + ts.tn - 1) / ts.tn;
+      if (ts.wide && runs < 64) chunks = min((64 + runs - 1) / runs, (ts.n + 31) / 32);
+      if (d < p.cls[c].pp - 1) vs = (unsigned long long)K * vrow(ts.n);  // leaves keep argmins only
+      bs = (unsigned long long)K * ts.n;
     }
-    const int c = lo;
-    const TrieStage ts = p.tstage[(size_t)c * (p.max_pp + 1) + d + 1];
-    const uint32_t chunks = p.nxc[(size_t)d * p.n_cls + c];
-    const uint32_t lt = tt - tb[c], run = lt / chunks, cc = lt - run * chunks;
-    const uint32_t nbc = p.nb[(size_t)d * p.n_cls + c], K = p.nK[(size_t)d * p.n_cls + c];
-    TrieTile tl;
-    tl.n0 = nbc + run * ts.tn;
-    tl.c = (uint16_t)c;
-    tl.d = (uint8_t)d;
-    tl.pad = 0;
-    tl.nn = (uint16_t)min(ts.tn, nbc + K - tl.n0);
-    const uint32_t xc = (ts.n + chunks - 1) / chunks;
-    tl.x0 = (uint16_t)(cc * xc);
-    tl.x1 = (uint16_t)min(ts.n, (cc + 1) * xc);
-    tl.run = run;
-    tl.pad2 = 0;
-    p.tiles[t] = tl;
+    nx[c] = chunks;
+    s_tiles[c] = (unsigned long long)runs * chunks;
+    s_v[c] = vs;
+    s_b[c] = bs;
+    s_r[c] = runs;
   }
+  __syncthreads();
+  const int w = tid >> 5;
+  if (w < 4) {
+    const unsigned long long t = warp_exscan(sm4 + (size_t)w * NC, NC);
+    if ((tid & 31) == 0) p.st->dtot[d][w] = t;
+  }
+  __syncthreads();
+  uint32_t* tb = p.tbase + (size_t)d * (NC + 1);
+  uint64_t* vb = p.vbase + (size_t)d * NC;
+  uint64_t* bb = p.bbase + (size_t)d * NC;
+  uint64_t* rb = p.rbase + (size_t)d * NC;
+  for (int c = tid; c < NC; c += blockDim.x) {
+    tb[c] = (uint32_t)s_tiles[c];
+    vb[c] = s_v[c];
+    bb[c] = s_b[c];
+    rb[c] = s_r[c];
+  }
+  if (tid == 0) tb[NC] = (uint32_t)p.st->dtot[d][0];
+  __syncthreads();
+}
+
+// The trie of the chunk's signatures from their sorted keys (one pass for
+// all depths) and the tile list of its DP.  Node ids are those of the level
+// build (k_trie_build): the depth-d nodes are the distinct (class, c_0 ..
+// c_{d-1}) prefixes in lexicographic order, so in key order a signature
+// starts a new node at every depth past the length of its common prefix
+// with the previous signature (a different class: every depth), and its
+// depth-d node is the count of such starts so far, minus one.
+//   1. LSD radix sort of the signature keys (8-bit digits; per pass a digit
+//      histogram per CTA, one grid barrier, the scatter ranked stably by
+//      warp match + per-warp counts in smem, one grid barrier);
+//   2. per-CTA start counts per depth, one grid barrier, then in key order:
+//      node ids by ballot prefixes per depth, the node arrays, the class
+//      node ranges, each signature's leaf node, the slot -> signature map;
+//   3. the level plans (one CTA per depth, in parallel), their offsets
+//      across depths, the tile list.
+__global__ void __launch_bounds__(kBuildThreads) k_trie_build_sorted(TrieParams p) {
+  extern __shared__ unsigned long long build_sm[];  // [4][n_cls] (plans)
+  constexpr int NW = kBuildThreads / 32;
+  __shared__ uint32_t s_hist[256], s_base[256];
+  __shared__ uint16_t s_wc[NW][256];
+  __shared__ uint32_t s_wd[NW][kTrieMaxD1];  // per-warp start counts, then their exclusive prefix
+  __shared__ uint32_t s_run[kTrieMaxD1];     // starts before the current chunk (per depth)
+  __shared__ uint64_t s_noff[kTrieMaxD1 + 1];
+  __shared__ int s_ovf;
+  TrieState* st = p.st;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, G = gridDim.x, bid = blockIdx.x;
+  const uint64_t gtid = (uint64_t)bid * blockDim.x + tid, gstride = (uint64_t)G * blockDim.x;
+  const uint64_t n = *p.n_sig;
+  const int nq = p.nq, cb = p.cb;
+  const uint64_t TS = (n + G - 1) / G, b0 = min((uint64_t)bid * TS, n), b1 = min(b0 + TS, n);
+  const unsigned lt_mask = (1u << lane) - 1u;
+  uint32_t phase = 0;
+  // ---- keys of the chunk's distinct signatures ------------------------------
+  for (uint64_t i = gtid; i < n; i += gstride) {
+    const uint32_t sl = p.uniq[i];
+    const unsigned long long k = p.tkey[sl];
+    p.sk[0][i] = p.key_shift >= 64 ? k : (k & ((1ull << p.key_shift) - 1));
+    p.sv[0][i] = sl;
+  }
+  grid_barrier(st, phase);
+  // ---- 1. LSD radix sort, 8-bit digits ---------------------------------------
+  int cur = 0;
+  for (int sh = 0; sh < p.kbits; sh += 8, cur ^= 1) {
+    const uint64_t* sk = p.sk[cur];
+    const uint32_t* sv = p.sv[cur];
+    for (int x = tid; x < 256; x += blockDim.x) s_hist[x] = 0;
+    __syncthreads();
+    for (uint64_t i = b0 + tid; i < b1; i += blockDim.x) atomicAdd(&s_hist[(sk[i] >> sh) & 255], 1u);
+    __syncthreads();
+    for (int x = tid; x < 256; x += blockDim.x) p.ghist[(size_t)bid * 256 + x] = s_hist[x];
+    grid_barrier(st, phase);
+    // this CTA's first position of every digit: all CTAs' counts of smaller
+    // digits plus the earlier CTAs' counts of the digit
+    if (tid < 256) {
+      uint32_t tot = 0, pre = 0;
+      for (int b = 0; b < G; ++b) {
+        const uint32_t v = __ldcg(p.ghist + (size_t)b * 256 + tid);
+        tot += v;
+        if (b < bid) pre += v;
+      }
+      s_hist[tid] = tot;
+      s_base[tid] = pre;
+    }
+    __syncthreads();
+    if (w == 0) {  // exclusive scan of the digit totals
+      uint32_t carry = 0;
+      for (int b = 0; b < 256; b += 32) {
+        const uint32_t v = s_hist[b + lane];
+        uint32_t incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        s_base[b + lane] += carry + incl - v;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+    // stable scatter, blockDim items at a time in order
+    uint64_t* dk = p.sk[cur ^ 1];
+    uint32_t* dv = p.sv[cur ^ 1];
+    for (uint64_t c0 = b0; c0 < b1; c0 += blockDim.x) {
+      for (int x = tid; x < NW * 256; x += blockDim.x) (&s_wc[0][0])[x] = 0;
+      __syncthreads();
+      const uint64_t i = c0 + tid;
+      const bool live = i < b1;
+      uint64_t key = 0;
+      uint32_t val = 0;
+      int dig = 256;  // (dead lanes: a digit no live lane has)
+      if (live) {
+        key = sk[i];
+        val = sv[i];
+        dig = (int)((key >> sh) & 255);
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, dig);
+      const int rank = __popc(peers & lt_mask);
+      if (live && rank == 0) s_wc[w][dig] = (uint16_t)__popc(peers);
+      __syncthreads();
+      if (live) {
+        uint32_t pos = s_base[dig] + rank;
+        for (int q = 0; q < w; ++q) pos += s_wc[q][dig];
+        dk[pos] = key;
+        dv[pos] = val;
+      }
+      __syncthreads();
+      if (tid < 256) {
+        uint32_t t = 0;
+        for (int q = 0; q < NW; ++q) t += s_wc[q][tid];
+        s_base[tid] += t;
+      }
+      __syncthreads();
+    }
+    grid_barrier(st, phase);
+  }
+  const uint64_t* K = p.sk[cur];
+  const uint32_t* V = p.sv[cur];
+  const int cshift = nq * cb;
+  const uint64_t cmask = cshift >= 64 ? ~0ull : ((1ull << cshift) - 1);
+  // common-prefix length (codes) with the previous key; 0 at a class change
+  auto lcp_of = [&](uint64_t i, uint64_t key) -> int {
+    if (i == 0) return 0;
+    const uint64_t prev = K[i - 1];
+    if ((prev >> cshift) != (key >> cshift)) return 0;
+    const uint64_t x = (prev ^ key) & cmask;  // != 0: keys are distinct
+    return (__clzll((long long)x) - (64 - cshift)) / cb;
+  };
+  // ---- the signature list in key order (also for the capacity fallback) ---
+  for (uint64_t i = b0 + tid; i < b1; i += blockDim.x) {
+    const uint32_t sl = V[i];
+    p.uniq[i] = sl;  // (signature -> slot, read by k_run_pipe)
+    p.sig_key[i] = K[i];
+    p.rep_item[i] = p.tval[sl];
+    p.tval[sl] = (uint32_t)i;
+  }
+  // ---- 2. node starts per depth: per-CTA counts ------------------------------
+  for (int x = tid; x < kTrieMaxD1; x += blockDim.x) s_run[x] = 0;
+  __syncthreads();
+  for (uint64_t i = b0 + tid; i < b1; i += blockDim.x) {
+    const uint64_t key = K[i];
+    const int dep = p.cls[key >> cshift].pp - 1;
+    for (int d = lcp_of(i, key) + 1; d <= dep; ++d) atomicAdd(&s_run[d], 1u);
+  }
+  __syncthreads();
+  for (int x = tid; x < kTrieMaxD1; x += blockDim.x) p.gpart[(size_t)bid * kTrieMaxD1 + x] = s_run[x];
+  grid_barrier(st, phase);
+  if (tid < kTrieMaxD1) {
+    uint32_t tot = 0, pre = 0;
+    for (int b = 0; b < G; ++b) {
+      const uint32_t v = __ldcg(p.gpart + (size_t)b * kTrieMaxD1 + tid);
+      tot += v;
+      if (b < bid) pre += v;
+    }
+    s_run[tid] = pre;
+    s_wd[0][tid] = tot;  // (depth totals, consumed below)
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t off = 0;
+    for (int d = 1; d <= nq; ++d) {
+      s_noff[d] = off;
+      off += s_wd[0][d];
+    }
+    s_noff[nq + 1] = off;
+    s_ovf = off > p.node_cap;
+    if (bid == 0) {
+      for (int d = 1; d <= nq; ++d) {
+        st->cnt[d] = s_wd[0][d];
+        st->node_off[d] = s_noff[d];
+      }
+      if (s_ovf) st->ovf = 1;
+    }
+  }
+  __syncthreads();
+  if (s_ovf) return;  // (uniform: every CTA read the same totals)
+  for (uint64_t c0 = b0; c0 < b1; c0 += blockDim.x) {
+    const uint64_t i = c0 + tid;
+    const bool live = i < b1;
+    uint64_t key = 0;
+    int lcp = 0, dep = -1, c = 0;
+    if (live) {
+      key = K[i];
+      c = (int)(key >> cshift);
+      dep = p.cls[c].pp - 1;
+      lcp = lcp_of(i, key);
+    }
+    for (int d = 1; d <= nq; ++d) {  // per-warp start counts
+      const unsigned b = __ballot_sync(0xffffffffu, live && d > lcp && d <= dep);
+      if (lane == 0) s_wd[w][d] = __popc(b);
+    }
+    __syncthreads();
+    if (tid >= 1 && tid <= nq) {  // exclusive prefix over the warps, per depth
+      uint32_t a = 0;
+      for (int q = 0; q < NW; ++q) {
+        const uint32_t v = s_wd[q][tid];
+        s_wd[q][tid] = a;
+        a += v;
+      }
+      s_base[tid] = a;  // (this chunk's starts at depth tid)
+    }
+    __syncthreads();
+    const bool first = live && (i == 0 || (K[i - 1] >> cshift) != (uint64_t)c);
+    const bool last = live && (i + 1 == n || (K[i + 1] >> cshift) != (uint64_t)c);
+    uint32_t par = live ? (uint32_t)p.root_rank[c] : 0u;
+    for (int d = 1; d <= nq; ++d) {  // (uniform trip count: the ballots)
+      const bool f = live && d > lcp && d <= dep;
+      const unsigned b = __ballot_sync(0xffffffffu, f);
+      if (live && d <= dep) {
+        // inclusive count of the starts at depth d up to this signature
+        const uint32_t node = s_run[d] + s_wd[w][d] + __popc(b & lt_mask) + (f ? 1u : 0u) - 1u;
+        if (f) {  // this signature starts the node
+          const uint64_t at = s_noff[d] + node;
+          p.npar[at] = par;
+          p.ncode[at] = (uint8_t)((key >> ((nq - d) * cb)) & (uint64_t)(p.U - 1));
+          p.ncls[at] = (uint16_t)c;
+        }
+        if (first) p.nb[(size_t)d * p.n_cls + c] = node;
+        if (last) p.nK[(size_t)d * p.n_cls + c] = node + 1;
+        par = node;
+      }
+    }
+    if (live) p.nid[i] = par;  // leaf node
+    __syncthreads();
+    if (tid >= 1 && tid <= nq) s_run[tid] += s_base[tid];
+    __syncthreads();
+  }
+  grid_barrier(st, phase);
+  // ---- 3. level plans (CTA d-1 plans depth d), offsets across depths ---------
+  for (int d = bid + 1; d <= nq; d += G) plan_depth(p, d, build_sm);
+  grid_barrier(st, phase);
+  for (int d = bid + 1; d <= nq; d += G) {
+    unsigned long long off[4] = {0, 0, 0, 0};
+    for (int e = 1; e < d; ++e)
+      for (int q = 0; q < 4; ++q) off[q] += __ldcg(&st->dtot[e][q]);
+    const int NC = p.n_cls;
+    uint64_t* vb = p.vbase + (size_t)d * NC;
+    uint64_t* bb = p.bbase + (size_t)d * NC;
+    uint64_t* rb = p.rbase + (size_t)d * NC;
+    for (int c = tid; c < NC; c += blockDim.x) {
+      vb[c] += off[1];
+      bb[c] += off[2];
+      rb[c] += off[3];
+    }
+    if (tid == 0) {
+      st->tile_off[d] = (uint32_t)off[0];
+      if (d == nq) {
+        st->tile_bump = off[0] + __ldcg(&st->dtot[d][0]);
+        st->v_bump = off[1] + __ldcg(&st->dtot[d][1]);
+        st->bp_bump = off[2] + __ldcg(&st->dtot[d][2]);
+        st->run_bump = off[3] + __ldcg(&st->dtot[d][3]);
+        if (st->v_bump > p.vcap || st->bp_bump > p.bpcap || st->run_bump > p.run_cap ||
+            st->tile_bump > p.tile_cap)
+          st->ovf = 1;
+      }
+    }
+  }
+  grid_barrier(st, phase);
+  if (ld_acquire(&st->ovf) != 0) return;
+  build_tile_list(p, gtid, gstride);
 }
 
 // Wide stages (many cells): the (cell x, group g of 4 nodes) items of one

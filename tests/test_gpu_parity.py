@@ -518,6 +518,7 @@ SWITCHES = [
     ("AMP_NO_RUN_SLOT", "1"),      # k_hash_scatter + rep_of lookup in K_est
     ("AMP_KEEP_WORK", "1"),        # K_place writes work records, K_est reads them
     ("AMP_WIDE_MEMO", "1"),        # hashed signature keys (the |D| = 1024 path), verified
+    ("AMP_TRIE_LEVELS", "1"),      # level-by-level trie build instead of the sorted-key build
 ]
 
 
