@@ -578,15 +578,26 @@ __global__ void __launch_bounds__(kBuildThreads) k_trie_build_sorted(TrieParams 
     grid_barrier(st, phase);
     // this CTA's first position of every digit: all CTAs' counts of smaller
     // digits plus the earlier CTAs' counts of the digit
-    if (tid < 256) {
+    {  // (thread = digit, the two halves of the block over the two halves of the CTAs)
+      const int dg = tid & 255, half = tid >> 8, bh = (G + 1) >> 1;
+      const int bb0 = half ? bh : 0, bb1 = half ? G : bh;
       uint32_t tot = 0, pre = 0;
-      for (int b = 0; b < G; ++b) {
-        const uint32_t v = __ldcg(p.ghist + (size_t)b * 256 + tid);
+#pragma unroll 8
+      for (int b = bb0; b < bb1; ++b) {
+        const uint32_t v = __ldcg(p.ghist + (size_t)b * 256 + dg);
         tot += v;
-        if (b < bid) pre += v;
+        pre += b < bid ? v : 0u;
       }
-      s_hist[tid] = tot;
-      s_base[tid] = pre;
+      if (half) {
+        // (s_wc as u32 scratch for the upper half's sums; cleared before the scatter)
+        reinterpret_cast<uint32_t*>(&s_wc[0][0])[dg] = tot;
+        reinterpret_cast<uint32_t*>(&s_wc[0][0])[256 + dg] = pre;
+      }
+      __syncthreads();
+      if (!half) {
+        s_hist[dg] = tot + reinterpret_cast<uint32_t*>(&s_wc[0][0])[dg];
+        s_base[dg] = pre + reinterpret_cast<uint32_t*>(&s_wc[0][0])[256 + dg];
+      }
     }
     __syncthreads();
     if (w == 0) {  // exclusive scan of the digit totals
