@@ -833,8 +833,9 @@ __device__ __forceinline__ void tile_wide(const TrieParams& p, const double* __r
       if (SINGLE) {
         v0 = v1 = v2 = v3 = vcol[q[cut]];
       } else {
-        const double2 va = *reinterpret_cast<const double2*>(vcol + (int)q[cut] * TNst);
-        const double2 vb = *reinterpret_cast<const double2*>(vcol + (int)q[cut] * TNst + 2);
+        const int qq = q[cut];
+        const double2 va = *reinterpret_cast<const double2*>(vcol + qq * TNst);
+        const double2 vb = *reinterpret_cast<const double2*>(vcol + qq * TNst + 2);
         v0 = va.x;
         v1 = va.y;
         v2 = vb.x;
@@ -915,11 +916,16 @@ __global__ void __launch_bounds__(kTrieThreads, 4) k_trie_dp(TrieParams p) {
   const int L = p.L, LP = L + 1, P1 = p.max_pp + 1, NC = p.n_cls;
   const uint32_t T = p.st->tile_off[p.nq + 1];
   unsigned long long mine = 0;
+  // the next tile is taken while this one is solved (its index is read at
+  // the publish barrier); a CTA never waits on its own prefetched tile, and
+  // every tile it waits on has a smaller index than its current one
+  if (tid == 0) s_t = atomicAdd(&p.st->next_tile, 1u);
+  __syncthreads();
+  uint32_t t = s_t;
   for (;;) {
-    if (tid == 0) s_t = atomicAdd(&p.st->next_tile, 1u);
-    __syncthreads();
-    const uint32_t t = s_t;
     if (t >= T) break;
+    uint32_t tnext = 0;
+    if (tid == 0) tnext = atomicAdd(&p.st->next_tile, 1u);
     const TrieTile tl = p.tiles[t];
     const int c = tl.c, d = tl.d, j = d + 1, nn = tl.nn;
     const ClassDev cl = p.cls[c];
@@ -1009,10 +1015,14 @@ __global__ void __launch_bounds__(kTrieThreads, 4) k_trie_dp(TrieParams p) {
       tile_narrow(p, sV, sE, sPf, sNode, Pst, Nj, VS, j, nn, ts, p.preds + pg.pred_base, dom, g1, leaf, vout,
                   bpo, mine);
     }
-    // publish: every thread's stores, then the run's chunk count
-    __threadfence();
+    // publish: the CTA's stores (ordered before thread 0 by the barrier),
+    // then the run's chunk count with release semantics
+    if (tid == 0) s_t = tnext;
     __syncthreads();
-    if (tid == 0) atomicAdd(p.done + p.rbase[(size_t)d * NC + c] + tl.run, 1u);
+    if (tid == 0)
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.done + p.rbase[(size_t)d * NC + c] + tl.run)
+                   : "memory");
+    t = s_t;
   }
   if (p.exec) {  // executed inner iterations (roofline accounting), one atomic per warp
     for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
