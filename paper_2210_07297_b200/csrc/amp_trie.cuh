@@ -83,12 +83,20 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
-struct TrieTile {   // one K_trie_dp work item
-  uint32_t n0;      // first node (local id at depth d)
-  uint32_t run;     // node run within (d, c)
+// One K_trie_dp work item, with everything its prologue needs resolved by
+// the build (one 64-byte load instead of a chain of dependent lookups).
+struct alignas(16) TrieTile {
+  uint32_t node;    // absolute index of the first node (node_off[d] + local id)
+  uint32_t pub;     // done[] counter of the tile's node run
   uint16_t c;       // class
-  uint8_t d, pad;
-  uint16_t nn, x0, x1, pad2;  // nodes, cell range [x0, x1) of N_{d+1}
+  uint8_t d, leaf;  // depth; 1: leaf depth (argmins only)
+  uint16_t nn, x0, x1, pad;  // nodes, cell range [x0, x1) of N_{d+1}
+  uint32_t pfirst, pn;  // parents: first (local id at depth d - 1), count
+  uint32_t w0, w1;      // done[] counters of the parents' runs [w0, w1]
+  uint32_t need;        // cell chunks per parent run
+  int64_t vpar;         // value arena: row of parent P at vpar + P * vrow(N_d)
+  uint64_t vout;        // value arena: the tile's first row
+  uint64_t bout;        // argmin arena: the tile's first row
 };
 
 struct TrieParams {
@@ -307,16 +315,35 @@ __device__ void build_tile_list(const TrieParams& p, uint64_t gtid, uint64_t gst
     const uint32_t lt = tt - tb[c], run = lt / chunks, cc = lt - run * chunks;
     const uint32_t nbc = p.nb[(size_t)d * p.n_cls + c], K = p.nK[(size_t)d * p.n_cls + c];
     TrieTile tl;
-    tl.n0 = nbc + run * ts.tn;
+    const uint32_t n0 = nbc + run * ts.tn;
+    const uint64_t noff = st->node_off[d];
+    const int NC = p.n_cls;
+    tl.node = (uint32_t)(noff + n0);
+    tl.pub = (uint32_t)(p.rbase[(size_t)d * NC + c] + run);
     tl.c = (uint16_t)c;
     tl.d = (uint8_t)d;
-    tl.pad = 0;
-    tl.nn = (uint16_t)min(ts.tn, nbc + K - tl.n0);
+    tl.leaf = d == p.cls[c].pp - 1;
+    tl.nn = (uint16_t)min(ts.tn, nbc + K - n0);
     const uint32_t xc = (ts.n + chunks - 1) / chunks;
     tl.x0 = (uint16_t)(cc * xc);
     tl.x1 = (uint16_t)min(ts.n, (cc + 1) * xc);
-    tl.run = run;
-    tl.pad2 = 0;
+    tl.pad = 0;
+    tl.vout = tl.leaf ? 0 : p.vbase[(size_t)d * NC + c] + (uint64_t)(n0 - nbc) * vrow(ts.n);
+    tl.bout = p.bbase[(size_t)d * NC + c] + (uint64_t)(n0 - nbc) * ts.n;
+    tl.pfirst = tl.pn = tl.w0 = tl.w1 = tl.need = 0;
+    tl.vpar = 0;
+    if (d >= 2) {  // (depth 1: the class's stage-1 table)
+      const TrieStage tp = p.tstage[(size_t)c * (p.max_pp + 1) + d];
+      const uint32_t pfirst = p.npar[noff + n0], plast = p.npar[noff + n0 + tl.nn - 1];
+      const uint32_t pnb = p.nb[(size_t)(d - 1) * NC + c];
+      const uint64_t rb = p.rbase[(size_t)(d - 1) * NC + c];
+      tl.pfirst = pfirst;
+      tl.pn = plast - pfirst + 1;
+      tl.w0 = (uint32_t)(rb + (pfirst - pnb) / tp.tn);
+      tl.w1 = (uint32_t)(rb + (plast - pnb) / tp.tn);
+      tl.need = p.nxc[(size_t)(d - 1) * NC + c];
+      tl.vpar = (int64_t)p.vbase[(size_t)(d - 1) * NC + c] - (int64_t)pnb * (int64_t)vrow(tp.n);
+    }
     p.tiles[t] = tl;
   }
 }
@@ -913,7 +940,7 @@ __global__ void __launch_bounds__(kTrieThreads, 4) k_trie_dp(TrieParams p) {
   __shared__ uint32_t s_t;
   if (p.st->ovf) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int L = p.L, LP = L + 1, P1 = p.max_pp + 1, NC = p.n_cls;
+  const int L = p.L, LP = L + 1, P1 = p.max_pp + 1;
   const uint32_t T = p.st->tile_off[p.nq + 1];
   unsigned long long mine = 0;
   // the next tile is taken while this one is solved (its index is read at
@@ -928,37 +955,24 @@ __global__ void __launch_bounds__(kTrieThreads, 4) k_trie_dp(TrieParams p) {
     if (tid == 0) tnext = atomicAdd(&p.st->next_tile, 1u);
     const TrieTile tl = p.tiles[t];
     const int c = tl.c, d = tl.d, j = d + 1, nn = tl.nn;
+    const bool leaf = tl.leaf;
+    const bool single = d < 2;  // depth-1 nodes: one parent, the class's stage-1 table
+    if (!single) {  // wait for the parents' runs (all their cell chunks)
+      if (warp == 0)
+        for (uint32_t r = tl.w0 + lane; r <= tl.w1; r += 32)
+          while (ld_acquire(p.done + r) < tl.need) __nanosleep(128);
+    }
     const ClassDev cl = p.cls[c];
     const TrieStage ts = p.tstage[(size_t)c * P1 + j];
-    const TrieStage tp = p.tstage[(size_t)c * P1 + j - 1];
-    const int Np = (int)tp.n, Nj = (int)ts.n, VS = (int)vrow(ts.n), VSp = (int)vrow(tp.n);
-    const uint64_t noff = p.st->node_off[d];
-    const uint32_t nbc = p.nb[(size_t)d * NC + c];
-    const bool leaf = d == cl.pp - 1;
-    const bool single = d < 2;  // depth-1 nodes: one parent, the class's stage-1 table
-    uint32_t pfirst = 0, plast = 0, pnb = 0;
-    uint64_t vbp = 0;
-    if (!single) {
-      pfirst = p.npar[noff + tl.n0];
-      plast = p.npar[noff + tl.n0 + nn - 1];
-      pnb = p.nb[(size_t)(d - 1) * NC + c];
-      vbp = p.vbase[(size_t)(d - 1) * NC + c];
-      // wait for the parents' runs (all their cell chunks)
-      if (warp == 0) {
-        const uint32_t ptn = tp.tn;
-        const uint32_t r0 = (pfirst - pnb) / ptn, r1 = (plast - pnb) / ptn;
-        const uint32_t need = p.nxc[(size_t)(d - 1) * NC + c];
-        const uint32_t* dn = p.done + p.rbase[(size_t)(d - 1) * NC + c];
-        for (uint32_t r = r0 + lane; r <= r1; r += 32)
-          while (ld_acquire(dn + r) < need) __nanosleep(128);
-      }
-      __syncthreads();
-    }
+    const int Np = (int)p.tstage[(size_t)c * P1 + j - 1].n, Nj = (int)ts.n, VS = (int)vrow(ts.n),
+              VSp = (int)vrow((uint32_t)Np);
     const double* qt = p.qtab + (size_t)c * p.n_codes * L;
     const ProgDev pg = p.progs[p.class_prog[c]];
     const double* dom = p.domain + (size_t)cl.pair * p.nv_stride;
-    double* vout = p.varena + (leaf ? 0 : p.vbase[(size_t)d * NC + c] + (uint64_t)(tl.n0 - nbc) * VS);
-    uint8_t* bpo = p.bparena + p.bbase[(size_t)d * NC + c] + (uint64_t)(tl.n0 - nbc) * Nj;
+    double* vout = p.varena + tl.vout;
+    uint8_t* bpo = p.bparena + tl.bout;
+    const double* vpar = p.varena + tl.vpar;
+    if (!single) __syncthreads();
     const double g1 = (double)(cl.gas - 1);
     if (ts.wide) {
       const int G = (nn + 3) >> 2, TW = 4 * G, TNst = TW + 2, ER = L - (j - 1);
@@ -971,13 +985,13 @@ __global__ void __launch_bounds__(kTrieThreads, 4) k_trie_dp(TrieParams p) {
       } else {
         for (int ln = warp; ln < TW; ln += nw) {
           const int lr = ln < nn ? ln : 0;  // padding columns repeat node 0
-          const double* src = p.varena + vbp + (uint64_t)(p.npar[noff + tl.n0 + lr] - pnb) * VSp;
+          const double* src = vpar + (uint64_t)p.npar[tl.node + lr] * VSp;
           for (int x = lane; x < Np; x += 32) cp_async8(sV + x * TNst + ln, src + x);
         }
       }
       for (int ln = warp; ln < TW; ln += nw) {
         const int lr = ln < nn ? ln : 0;
-        const double* er = qt + (size_t)p.ncode[noff + tl.n0 + lr] * L + (j - 1);
+        const double* er = qt + (size_t)p.ncode[tl.node + lr] * L + (j - 1);
         for (int r = lane; r < ER; r += 32) sE[r * TNst + ln] = er[r];
       }
       for (int x = tid; x < LP; x += blockDim.x) sPf[x] = p.prefix[(size_t)cl.pair * LP + x];
@@ -990,7 +1004,7 @@ __global__ void __launch_bounds__(kTrieThreads, 4) k_trie_dp(TrieParams p) {
         tile_wide<false>(p, sV, sE, sPf, TNst, G, tl.x0, tl.x1, Nj, VS, j, nn, ts, p.preds + pg.pred_base, dom,
                          g1, leaf, vout, bpo, mine);
     } else {
-      const int P = single ? 1 : (int)(plast - pfirst) + 1;
+      const int P = single ? 1 : (int)tl.pn;
       const int Pst = P | 1;  // odd stride: rows start on distinct banks
       double* sV = smem_d;
       double* sE = sV + (size_t)Np * Pst;
@@ -1000,15 +1014,15 @@ __global__ void __launch_bounds__(kTrieThreads, 4) k_trie_dp(TrieParams p) {
         const double* src = p.v1g + p.v1off[c];
         for (int x = tid; x < Np; x += blockDim.x) sV[x * Pst] = src[x];
       } else {
-        const double* src = p.varena + vbp + (uint64_t)(pfirst - pnb) * VSp;
+        const double* src = vpar + (uint64_t)tl.pfirst * VSp;
         for (int pl = warp; pl < P; pl += nw)
           for (int x = lane; x < Np; x += 32) cp_async8(sV + x * Pst + pl, src + (size_t)pl * VSp + x);
       }
       for (int x = tid; x < p.n_codes * L; x += blockDim.x) sE[x] = qt[x];
       for (int x = tid; x < LP; x += blockDim.x) sPf[x] = p.prefix[(size_t)cl.pair * LP + x];
       for (int x = tid; x < nn; x += blockDim.x) {
-        const uint64_t node = noff + tl.n0 + x;
-        sNode[x] = ((int)p.ncode[node] << 16) | (single ? 0 : (int)(p.npar[node] - pfirst));
+        const uint64_t node = (uint64_t)tl.node + x;
+        sNode[x] = ((int)p.ncode[node] << 16) | (single ? 0 : (int)(p.npar[node] - tl.pfirst));
       }
       cp_async_wait_all();
       __syncthreads();
@@ -1020,8 +1034,7 @@ __global__ void __launch_bounds__(kTrieThreads, 4) k_trie_dp(TrieParams p) {
     if (tid == 0) s_t = tnext;
     __syncthreads();
     if (tid == 0)
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.done + p.rbase[(size_t)d * NC + c] + tl.run)
-                   : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.done + tl.pub) : "memory");
     t = s_t;
   }
   if (p.exec) {  // executed inner iterations (roofline accounting), one atomic per warp
