@@ -40,9 +40,13 @@ namespace amp {
 
 constexpr int kTrieMaxD1 = 64;        // depths 0 .. nq (keys are <= 63 bits, >= 1 bit per code)
 constexpr int kTrieMaxCls = 1024;     // classes of a trie context (plan arrays in smem)
+#ifndef AMP_TRIE_MINB
+#define AMP_TRIE_MINB 4       // K_trie_dp CTAs per SM
+#define AMP_TRIE_SMEM_KB 46   // K_trie_dp smem per CTA
+#endif
 constexpr int kTrieThreads = 256;     // K_trie_dp block
 constexpr int kTrieNB = 4;            // nodes per thread in wide stages (share the cell's work)
-constexpr int kTrieSmem = 46 * 1024;  // K_trie_dp smem per CTA (4 CTAs / SM)
+constexpr int kTrieSmem = AMP_TRIE_SMEM_KB * 1024;  // K_trie_dp smem per CTA
 constexpr int kBuildThreads = 512;    // K_trie_build block
 constexpr int kBuildReg = 4;          // signatures per thread K_trie_build keeps in registers
 
@@ -935,7 +939,7 @@ __device__ __forceinline__ void tile_narrow(const TrieParams& p, const double* _
 // stages them and the edge rows in shared memory, solves its items and
 // publishes its run.  Parent tables are read through L2 (__ldcg): they were
 // written by other SMs during this launch.
-__global__ void __launch_bounds__(kTrieThreads, 4) k_trie_dp(TrieParams p) {
+__global__ void __launch_bounds__(kTrieThreads, AMP_TRIE_MINB) k_trie_dp(TrieParams p) {
   extern __shared__ __align__(16) double smem_d[];
   __shared__ uint32_t s_t;
   if (p.st->ovf) return;
