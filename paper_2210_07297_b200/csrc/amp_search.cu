@@ -1935,6 +1935,15 @@ int run_device_segs(amp_ctx* ctx, const std::vector<Segment>& segs, int32_t k, a
 // class (the same class mix); with P = 1 (the plan() space, e.g. C4's 440
 // uneven DP instances) it is LPT over the classes.  Deterministic: every
 // rank computes the same plan.  Mirrored by distributed.lpt_shards.
+//
+// Signature-disjoint variant (n > 1, P >= n, enough pp <= 2 work to fill):
+// every DP class (pp >= 3) is one unit — a signature contains its class, so
+// no two shards solve the same DP instance, and the memoised DP work is
+// split across the shards instead of repeated on each — dealt first, the
+// largest DP programs first (round robin at equal weights); the pp <= 2
+// classes (no DP) in min(P, n) blocks then balance the per-candidate load.
+// Weights: 2 units per DP-class candidate (K_place + K_est), 1 per pp <= 2
+// candidate (K_est only), times 128 D.
 std::vector<std::vector<Segment>> shard_plan(const amp_ctx* ctx, int32_t n_shards, uint64_t begin = 0,
                                              uint64_t end = ~0ull) {
   struct Unit {
@@ -1943,14 +1952,28 @@ std::vector<std::vector<Segment>> shard_plan(const amp_ctx* ctx, int32_t n_shard
   };
   const uint64_t P = ctx->P;
   std::vector<Unit> units;
+  double heavy_max = 0, light_w = 0;
+  for (uint64_t c = 0; c < ctx->classes.size(); ++c) {
+    const uint64_t lo = std::max(begin, c * P), hi = std::min(end, (c + 1) * P);
+    if (hi <= lo) continue;
+    if (is_heavy(ctx, c)) heavy_max = std::max(heavy_max, 2.0 * (double)(hi - lo));
+    else light_w += (double)(hi - lo);
+  }
+  const bool disjoint = n_shards > 1 && P >= (uint64_t)n_shards && heavy_max > 0 &&
+                        light_w >= heavy_max * n_shards && std::getenv("AMP_SHARD_BLOCKS") == nullptr;
   for (uint64_t c = 0; c < ctx->classes.size(); ++c) {  // the class's part of [begin, end)
     const uint64_t lo = std::max(begin, c * P), hi = std::min(end, (c + 1) * P);
     if (hi <= lo) continue;
-    const uint64_t q0 = lo - c * P, n = hi - lo, nb = std::min<uint64_t>(n, (uint64_t)n_shards);
-    const double wc = ctx->class_inner[c] + 128.0 * ctx->D;
+    const bool whole = disjoint && is_heavy(ctx, c);
+    const uint64_t q0 = lo - c * P, n = hi - lo, nb = whole ? 1 : std::min<uint64_t>(n, (uint64_t)n_shards);
+    // sort key: LPT by class weight (disjoint: DP classes first, largest
+    // program first), a class's blocks adjacent
+    const double wc = disjoint ? (whole ? 1e12 + ctx->class_inner[c] : 128.0 * ctx->D)
+                               : ctx->class_inner[c] + 128.0 * ctx->D;
+    const double wu = disjoint ? (whole ? 2.0 : 1.0) * 128.0 * ctx->D : wc;  // per-candidate load
     for (uint64_t b = 0; b < nb; ++b) {
       const uint64_t p0 = q0 + n * b / nb, p1 = q0 + n * (b + 1) / nb;
-      if (p1 > p0) units.push_back(Unit{wc * (double)(p1 - p0), wc, c, p0, p1});
+      if (p1 > p0) units.push_back(Unit{wu * (double)(p1 - p0), wc, c, p0, p1});
     }
   }
   // longest first by the class weight, a class's blocks adjacent (stable)

@@ -5,8 +5,9 @@ part of the class-major index space and keeps its local top-k on the
 device.  Two splits: the LPT shard plan (`search_gpu_sharded`,
 amp_search_run_device_shard, mirrored by `lpt_shards`: every class cut into
 min(P, n) placement blocks weighted by its work, longest first to the
-least-loaded rank — with P >= n every rank gets the same class mix, the
-bench's split; with P = 1 an LPT split of the plan() DP instances) and the
+least-loaded rank — with P >= n and enough pp <= 2 work the DP classes stay
+whole, so the ranks solve disjoint signatures and the pp <= 2 blocks balance
+the load; with P = 1 an LPT split of the plan() DP instances) and the
 contiguous work-weighted index range (`search_gpu`, amp_search_partition).
 The only
 exchange is one all-gather of the k records per rank (NCCL over NVLink on
@@ -80,19 +81,33 @@ def search_gpu_sharded(searcher, k: int, rank: int, world: int, group=None):
     return recs[recs["fail_code"] >= 0]
 
 
-def lpt_shards(class_weights: Sequence[float], P: int, n_shards: int) -> List[List[tuple]]:
+def lpt_shards(class_weights: Sequence[float], P: int, n_shards: int,
+               heavy: Optional[Sequence[bool]] = None) -> List[List[tuple]]:
     """The shard plan of amp_search_run_device_shard (amp_search.cu
     shard_plan): each class c cut into min(P, n) placement blocks of weight
     class_weights[c] * size, blocks longest-first (stable) to the
-    least-loaded shard (lowest on ties).  Returns each shard's index ranges
-    (in assignment order; the engine dispatches them heaviest class first)."""
+    least-loaded shard (lowest on ties).  With `heavy` (the DP classes,
+    pp >= 3) the signature-disjoint variant applies when n > 1, P >= n and
+    the pp <= 2 candidates are at least n times the largest DP class's
+    doubled size: every DP class is one unit of weight 2 * P (dealt first,
+    the largest class_weights first), the others min(P, n) blocks of weight
+    1 * size.  Returns each shard's index ranges (in assignment order; the
+    engine dispatches them heaviest class first)."""
     nb = min(P, n_shards)
+    disjoint = False
+    if heavy is not None and n_shards > 1 and P >= n_shards and any(heavy):
+        light = sum(P for h in heavy if not h)
+        disjoint = light >= 2.0 * P * n_shards
     units = []
     for c, wc in enumerate(class_weights):
-        for b in range(nb):
-            p0, p1 = P * b // nb, P * (b + 1) // nb
+        whole = disjoint and heavy[c]
+        nbc = 1 if whole else nb
+        key = (1e12 + wc) if whole else (1.0 if disjoint else wc)
+        for b in range(nbc):
+            p0, p1 = P * b // nbc, P * (b + 1) // nbc
             if p1 > p0:
-                units.append((wc * (p1 - p0), wc, c, p0, p1))
+                wu = (2.0 if whole else 1.0) if disjoint else wc
+                units.append((wu * (p1 - p0), key, c, p0, p1))
     # longest first by the class weight, a class's blocks adjacent (stable)
     units.sort(key=lambda u: -u[1])
     load = [0.0] * n_shards

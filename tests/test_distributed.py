@@ -93,3 +93,32 @@ def test_lpt_shards_cover_space_and_balance():
         assert (seen == 1).all()
         loads = [sum(w[lo // P_] * (hi - lo) for lo, hi in r) for r in plan]
         assert max(loads) - min(loads) <= max(w) * -(-P_ // n) + 1e-9  # greedy: <= the largest block
+
+
+def test_signature_disjoint_shards():
+    """The signature-disjoint plan (P >= n, enough pp <= 2 work): every DP
+    class lies in exactly one shard (no signature is solved twice), every
+    index is covered once, and the per-candidate load (2 per DP-class
+    candidate, 1 otherwise) is balanced within one pp <= 2 block."""
+    from paper_2210_07297_b200 import distributed as Dd
+    for n_cls, n_heavy, P_, n in [(70, 32, 1000, 4), (70, 32, 1000, 8), (40, 6, 64, 2), (20, 2, 9, 3)]:
+        heavy = [c >= n_cls - n_heavy for c in range(n_cls)]
+        w = [float(c) for c in range(n_cls)]
+        plan = Dd.lpt_shards(w, P_, n, heavy)
+        seen = np.zeros(n_cls * P_, dtype=np.int32)
+        owner = {}
+        for r, rngs in enumerate(plan):
+            for lo, hi in rngs:
+                seen[lo:hi] += 1
+                c = lo // P_
+                assert (hi - 1) // P_ == c
+                if heavy[c]:
+                    assert c not in owner
+                    owner[c] = r
+                    assert hi - lo == P_
+        assert (seen == 1).all() and len(owner) == n_heavy
+        loads = [sum((2.0 if heavy[lo // P_] else 1.0) * (hi - lo) for lo, hi in r) for r in plan]
+        assert max(loads) - min(loads) <= -(-P_ // n) + 1e-9
+    # not enough pp <= 2 work: the block plan (every class in min(P, n) blocks)
+    plan = Dd.lpt_shards([1.0] * 10, 100, 4, [c < 8 for c in range(10)])
+    assert sum(len(r) for r in plan) == 40
