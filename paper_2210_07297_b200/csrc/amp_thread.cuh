@@ -625,16 +625,22 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
   // from the previous chunk (an item that cannot beat it cannot reach the
   // CTA's top-k), else nothing (w_kf = 2).  The exact key (index included)
   // matters: a chunk of failing candidates would otherwise pass every item.
-  int w_kf = 2;  // (the warp list's count lives in wcount[wib]: one register less)
-  if (lane == 0) wcount[wib] = 0;
+  // (the warp list's count and the threshold's index live in shared memory:
+  // registers are the kernel's occupancy limit)
+  __shared__ unsigned long long w_ki[kEstTWarps];
+  int w_kf = 2;
   double w_kt = CUDART_INF;
-  uint64_t w_ki = ~0ull;
+  if (lane == 0) {
+    wcount[wib] = 0;
+    w_ki[wib] = ~0ull;
+  }
   if (p.k > 0 && n_top == p.k) {
     const amp_record& e = mytop[p.k - 1];
     w_kf = e.fail_code < 0 ? 2 : (e.fail_code != 0 ? 1 : 0);
     w_kt = e.total;
-    w_ki = e.index;
+    if (lane == 0) w_ki[wib] = e.index;
   }
+  __syncwarp();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   int seg_hint = -1;  // (decode_item: this thread's previous segment)
   // uniform trip count per warp (the top-k hand-off is warp-synchronous)
@@ -910,7 +916,7 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
       bool cand = false;
       if (live) {
         const int rf = ok ? 0 : 1;
-        cand = rf != w_kf ? rf < w_kf : (rf == 0 && rec.total != w_kt ? rec.total < w_kt : rec.index < w_ki);
+        cand = rf != w_kf ? rf < w_kf : (rf == 0 && rec.total != w_kt ? rec.total < w_kt : rec.index < w_ki[wib]);
         if (cand) stage_rec[wib][lane] = rec;
       }
       unsigned m = __ballot_sync(0xffffffffu, cand);
@@ -924,12 +930,12 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
         if (wcount[wib] == p.k) {
           w_kf = wtop[wib][p.k - 1].fail_code != 0;
           w_kt = wtop[wib][p.k - 1].total;
-          w_ki = wtop[wib][p.k - 1].index;
+          w_ki[wib] = wtop[wib][p.k - 1].index;
         }
       }
       w_kf = __shfl_sync(0xffffffffu, w_kf, 0);
       w_kt = __shfl_sync(0xffffffffu, w_kt, 0);
-      w_ki = __shfl_sync(0xffffffffu, w_ki, 0);
+      __syncwarp();
     }
   }
   __syncwarp();
