@@ -17,6 +17,10 @@ lib: $(LIB)
 
 $(LIB): $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) -lnccl 2> $(PKG)/csrc/ptxas.log || (cat $(PKG)/csrc/ptxas.log; exit 1)
+	@# host symbol table out: nvcc names the TU's static initialiser after its
+	@# pid-stamped temp file, so an unstripped build differs on every run; the
+	@# stripped .so is reproducible (profiles/ counts are keyed by its sha256)
+	strip --strip-unneeded $@
 	@grep -E "Compiling entry|Used|spill" $(PKG)/csrc/ptxas.log | sed 's/^ptxas info *: //' | head -40
 
 oracle:
