@@ -21,6 +21,25 @@
 
 namespace amp {
 
+// Bounds assertions of the debug build (make lib EXTRA=-DAMP_BOUNDS): a
+// failing check prints its site and traps.  compute-sanitizer is not
+// available on the GPU pool; tools/gpu_bounds.sh runs the GPU tests on this
+// build instead.
+#ifdef AMP_BOUNDS
+#define AMP_CHECK(cond, what)                                                      \
+  do {                                                                             \
+    if (!(cond)) {                                                                 \
+      printf("AMP_BOUNDS %s:%d %s (block %d thread %d)\n", __FILE__, __LINE__, what, \
+             (int)blockIdx.x, (int)threadIdx.x);                                   \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
+#else
+#define AMP_CHECK(cond, what) \
+  do {                        \
+  } while (0)
+#endif
+
 constexpr int kMaxLayers = 180;        // (L(L+1)/2 + 1) <= 16384 for the smem sort
 constexpr int kSortCap = 16384;        // padded domain capacity (pow2)
 constexpr int kEvalThreads = 384;      // evaluate kernel max block size

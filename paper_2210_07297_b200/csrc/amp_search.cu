@@ -1262,6 +1262,7 @@ int run_sig_dp(amp_ctx* ctx, EvalParams& ep, const HashParams& hp) {
     tp.cid = ctx->tr_cid.as<uint32_t>();
     tp.pres_cap = pres_cap;
     tp.partial = ctx->tr_partial.as<uint32_t>();
+    tp.smem_bytes = ctx->tr_smem;
     if (ctx->tr_sorted) {
       CK(ctx->tr_sortk.ensure(sizeof(uint64_t) * 2 * C));
       CK(ctx->tr_sortv.ensure(sizeof(uint32_t) * 2 * C));

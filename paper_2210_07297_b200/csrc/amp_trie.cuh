@@ -162,7 +162,7 @@ struct TrieParams {
   uint32_t* sv[2];
   uint32_t* ghist;
   uint32_t* gpart;
-  int32_t kbits, pad_s;             // significant key bits (class + codes)
+  int32_t kbits, smem_bytes;        // significant key bits (class + codes); K_trie_dp dynamic smem
 };
 
 __device__ __forceinline__ int trie_cls(const TrieParams& p, uint64_t k) { return (int)(k >> (p.nq * p.cb)); }
@@ -348,6 +348,10 @@ __device__ void build_tile_list(const TrieParams& p, uint64_t gtid, uint64_t gst
       tl.need = p.nxc[(size_t)(d - 1) * NC + c];
       tl.vpar = (int64_t)p.vbase[(size_t)(d - 1) * NC + c] - (int64_t)pnb * (int64_t)vrow(tp.n);
     }
+    AMP_CHECK(t < p.tile_cap && tl.pub < p.run_cap && (d < 2 || tl.w1 < p.run_cap), "tile / run counters");
+    AMP_CHECK(tl.bout + (uint64_t)tl.nn * ts.n <= p.bpcap, "tile argmin rows");
+    AMP_CHECK(tl.leaf || tl.vout + (uint64_t)tl.nn * vrow(ts.n) <= p.vcap, "tile value rows");
+    AMP_CHECK(tl.node + tl.nn <= p.node_cap, "tile nodes");
     p.tiles[t] = tl;
   }
 }
@@ -667,6 +671,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_trie_build_sorted(TrieParams 
       if (live) {
         uint32_t pos = s_base[dig] + rank;
         for (int q = 0; q < w; ++q) pos += s_wc[q][dig];
+        AMP_CHECK(pos < n, "radix scatter");
         dk[pos] = key;
         dv[pos] = val;
       }
@@ -777,6 +782,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_trie_build_sorted(TrieParams 
         const uint32_t node = s_run[d] + s_wd[w][d] + __popc(b & lt_mask) + (f ? 1u : 0u) - 1u;
         if (f) {  // this signature starts the node
           const uint64_t at = s_noff[d] + node;
+          AMP_CHECK(at < p.node_cap, "node arrays");
           p.npar[at] = par;
           p.ncode[at] = (uint8_t)((key >> ((nq - d) * cb)) & (uint64_t)(p.U - 1));
           p.ncls[at] = (uint16_t)c;
@@ -889,6 +895,8 @@ __device__ __forceinline__ void tile_wide(const TrieParams& p, const double* __r
     for (int b = 0; b < 4; ++b) {
       const int ln = 4 * g + b;
       if (ln >= nn) break;
+      AMP_CHECK(bpo + (uint64_t)ln * Nj + x < p.bparena + p.bpcap, "wide argmin");
+      AMP_CHECK(leaf || vout + (uint64_t)ln * VS + x < p.varena + p.vcap, "wide value");
       if (!leaf) vout[(uint64_t)ln * VS + x] = bs[b];
       bpo[(uint64_t)ln * Nj + x] = (uint8_t)cs[b];
     }
@@ -929,6 +937,8 @@ __device__ __forceinline__ void tile_narrow(const TrieParams& p, const double* _
         bc = cut;
       }
     }
+    AMP_CHECK(bpo + (uint64_t)ln * Nj + x < p.bparena + p.bpcap, "narrow argmin");
+    AMP_CHECK(leaf || vout + (uint64_t)ln * VS + x < p.varena + p.vcap, "narrow value");
     if (!leaf) vout[(uint64_t)ln * VS + x] = best;
     bpo[(uint64_t)ln * Nj + x] = (uint8_t)bc;
   }
@@ -983,6 +993,7 @@ __global__ void __launch_bounds__(kTrieThreads, AMP_TRIE_MINB) k_trie_dp(TriePar
       double* sV = smem_d;
       double* sE = sV + (single ? ((Np + 1) & ~1) : Np * TNst);
       double* sPf = sE + ER * TNst;
+      AMP_CHECK((size_t)(sPf + LP - smem_d) * sizeof(double) <= (size_t)p.smem_bytes, "wide tile smem");
       if (single) {
         const double* src = p.v1g + p.v1off[c];
         for (int x = tid; x < Np; x += blockDim.x) sV[x] = src[x];
@@ -990,6 +1001,7 @@ __global__ void __launch_bounds__(kTrieThreads, AMP_TRIE_MINB) k_trie_dp(TriePar
         for (int ln = warp; ln < TW; ln += nw) {
           const int lr = ln < nn ? ln : 0;  // padding columns repeat node 0
           const double* src = vpar + (uint64_t)p.npar[tl.node + lr] * VSp;
+          AMP_CHECK(src >= p.varena && src + Np <= p.varena + p.vcap, "wide parent row");
           for (int x = lane; x < Np; x += 32) cp_async8(sV + x * TNst + ln, src + x);
         }
       }
@@ -1014,11 +1026,14 @@ __global__ void __launch_bounds__(kTrieThreads, AMP_TRIE_MINB) k_trie_dp(TriePar
       double* sE = sV + (size_t)Np * Pst;
       double* sPf = sE + (size_t)p.n_codes * L;
       int* sNode = reinterpret_cast<int*>(sPf + LP);  // (code << 16) | parent column
+      AMP_CHECK((size_t)((char*)(sNode + nn) - (char*)smem_d) <= (size_t)p.smem_bytes, "narrow tile smem");
       if (single) {
         const double* src = p.v1g + p.v1off[c];
         for (int x = tid; x < Np; x += blockDim.x) sV[x * Pst] = src[x];
       } else {
         const double* src = vpar + (uint64_t)tl.pfirst * VSp;
+        AMP_CHECK(single || (src >= p.varena && src + (uint64_t)(P - 1) * VSp + Np <= p.varena + p.vcap),
+                  "narrow parent rows");
         for (int pl = warp; pl < P; pl += nw)
           for (int x = lane; x < Np; x += 32) cp_async8(sV + x * Pst + pl, src + (size_t)pl * VSp + x);
       }
@@ -1081,6 +1096,7 @@ __global__ void k_trie_back(TrieParams p) {
       const int d = j - 1;
       const TrieStage ts = p.tstage[(size_t)c * (p.max_pp + 1) + j];
       const uint32_t nbc = p.nb[(size_t)d * p.n_cls + c];
+      AMP_CHECK(p.bbase[(size_t)d * p.n_cls + c] + (uint64_t)(node - nbc) * ts.n + x < p.bpcap, "backtrack argmin");
       const int cut = p.bparena[p.bbase[(size_t)d * p.n_cls + c] + (uint64_t)(node - nbc) * ts.n + x];
       co[j - 1] = (uint8_t)cut;
       const uint2 rec = p.cellrec[ts.cell0 + x];
