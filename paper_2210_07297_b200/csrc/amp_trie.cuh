@@ -12,23 +12,24 @@
 // one-DP-per-candidate kernel and the oracle).
 //
 // Three kernels per chunk, every count on the device (no host round trip):
-//   K_trie_build (cooperative, grid barriers between phases)
-//     - signature list: the hash table's distinct keys (hash order), slot ->
-//       signature map, the root (class) of each signature, depth-1 marks
-//     - per depth d = 1 .. nq: scan of the child marks -> depth-d node ids in
-//       (parent, code) order: lexicographic, class-contiguous, the children
-//       of a parent adjacent; each signature's depth-d node and its
-//       depth-(d+1) mark; CTA 0 plans the level: per class the node range,
-//       the tiles, the value / argmin table bases (device bump allocation;
-//       exceeding a capacity raises `ovf` and the signature-mode K_dp,
-//       amp_dp_multi.cuh, solves the chunk instead)
-//     - the tile list of all depths
+//   K_trie_build_sorted (cooperative, grid barriers between phases): the
+//     chunk's distinct signature keys radix-sorted; in key order a signature
+//     starts a node at every depth past its common prefix with the previous
+//     key, so the depth-d node ids (lexicographic, class-contiguous, the
+//     children of a parent adjacent) are prefix counts of those starts; the
+//     node arrays, each class's node range per depth, the level plans (tiles,
+//     value / argmin table bases by device bump allocation; exceeding a
+//     capacity raises `ovf` and the signature-mode K_dp, amp_dp_multi.cuh,
+//     solves the chunk instead) and the tile descriptors.  K_trie_build, the
+//     level-by-level build of the same trie (a scan of child marks per
+//     depth), is the comparison path (AMP_TRIE_LEVELS=1).
 //   K_trie_dp (persistent, dataflow): CTAs take tiles in depth order from an
-//     atomic counter.  A tile = (class, run of tn consecutive depth-d nodes,
-//     chunk of the cells of N_{d+1}); it waits until the runs holding its
-//     parents are done, stages their stage-d tables and the edge rows in
-//     shared memory, solves its items, publishes its run.  The upper levels
-//     (few nodes, latency-bound) thereby overlap the wide middle levels.
+//     atomic counter (the next one while the current one is solved).  A tile
+//     = (class, run of tn consecutive depth-d nodes, chunk of the cells of
+//     N_{d+1}); it waits until the runs holding its parents are done, stages
+//     their stage-d tables and the edge rows in shared memory, solves its
+//     items, publishes its run.  The upper levels (few nodes, latency-bound)
+//     thereby overlap the wide middle levels.
 //   K_trie_back: one thread per signature backtracks (pipeline_dp.cpp:
 //     134-148) along its trie path and writes its cuts.
 #pragma once
