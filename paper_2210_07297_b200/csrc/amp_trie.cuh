@@ -45,7 +45,10 @@ constexpr int kTrieMaxCls = 1024;     // classes of a trie context (plan arrays 
 #define AMP_TRIE_MINB 4       // K_trie_dp CTAs per SM
 #define AMP_TRIE_SMEM_KB 46   // K_trie_dp smem per CTA
 #endif
-constexpr int kTrieThreads = 256;     // K_trie_dp block
+#ifndef AMP_TRIE_THREADS
+#define AMP_TRIE_THREADS 256  // K_trie_dp block
+#endif
+constexpr int kTrieThreads = AMP_TRIE_THREADS;
 constexpr int kTrieNB = 4;            // nodes per thread in wide stages (share the cell's work)
 constexpr int kTrieSmem = AMP_TRIE_SMEM_KB * 1024;  // K_trie_dp smem per CTA
 constexpr int kBuildThreads = 512;    // K_trie_build block
