@@ -121,6 +121,14 @@ struct Recycled {
   size_t pres_bytes = 0;
 };
 std::mutex g_rec_mu;
+
+// NCCL communicators of a device set, handed from a destroyed multi-GPU
+// context to the next one on the same devices (ncclCommInitAll and the
+// connection setup of a communicator's first collective cost 0.1-1 s; a
+// plan() creates a context per call).  A set is owned by one context at a
+// time (checked out at create, returned at destroy).
+std::mutex g_comm_mu;
+std::map<std::vector<int>, std::vector<std::vector<ncclComm_t>>> g_comm_pool;
 std::map<int, Recycled> g_rec;
 
 std::vector<int> divisors(int n) {
@@ -191,6 +199,7 @@ struct amp_ctx {
   // device, subs[r - 1] device + r; comms[r] is rank r's NCCL communicator
   std::vector<amp_ctx*> subs;
   std::vector<ncclComm_t> comms;
+  std::vector<int> comm_devs;  // the devices of comms (the pool key)
   DevBuf gathered, mtopk;
   uint64_t n_heavy = 0;  // items of pp >= 3 classes in the current run's dispatch order
   // DP memoisation by signature (amp_dedup.cuh)
@@ -2061,30 +2070,38 @@ int run_multi(amp_ctx* ctx, uint64_t begin, uint64_t end, int32_t k, amp_record*
       }
       CK(cudaMemcpyAsync(c->topk.p, pad.data(), sizeof(amp_record) * kk, cudaMemcpyHostToDevice, c->stream));
     }
+    // this shard's per-record outputs: one bulk copy per array (the shard's
+    // records are contiguous on the device, segment after segment), then
+    // each segment to its host position (P = 1 shards have a segment per
+    // class: hundreds of small device copies otherwise)
     const int W = c->max_pp + 1, MP = c->max_pp, D = c->D;
-    for (const Segment& sg : segs) {  // this shard's records to their host positions
-      const uint64_t at = sg.first - begin;
-      if (all)
-        CK(cudaMemcpyAsync(all + at, c->o_all.as<amp_record>() + sg.out, sizeof(amp_record) * sg.count,
-                           cudaMemcpyDeviceToHost, c->stream));
-      if (det && det->cuts)
-        CK(cudaMemcpyAsync(det->cuts + at * W, c->o_cuts.as<int32_t>() + sg.out * W,
-                           sizeof(int32_t) * sg.count * W, cudaMemcpyDeviceToHost, c->stream));
-      if (det && det->stage_times)
-        CK(cudaMemcpyAsync(det->stage_times + at * MP, c->o_stage.as<double>() + sg.out * MP,
-                           sizeof(double) * sg.count * MP, cudaMemcpyDeviceToHost, c->stream));
-      if (det && det->edge_times)
-        CK(cudaMemcpyAsync(det->edge_times + at * MP, c->o_edge.as<double>() + sg.out * MP,
-                           sizeof(double) * sg.count * MP, cudaMemcpyDeviceToHost, c->stream));
-      if (det && det->placement)
-        CK(cudaMemcpyAsync(det->placement + at * D, c->o_place.as<int32_t>() + sg.out * D,
-                           sizeof(int32_t) * sg.count * D, cudaMemcpyDeviceToHost, c->stream));
-      if (want_sim)
-        CK(cudaMemcpyAsync(det->simulated + at, c->o_sim.as<double>() + sg.out, sizeof(double) * sg.count,
-                           cudaMemcpyDeviceToHost, c->stream));
-    }
+    struct Out {
+      bool on;
+      const void* src;
+      void* dst;
+      size_t rec;  // bytes per record
+      std::vector<unsigned char> h;
+    };
+    Out outs[] = {
+        {all != nullptr, c->o_all.p, all, sizeof(amp_record), {}},
+        {det && det->cuts, c->o_cuts.p, det ? det->cuts : nullptr, sizeof(int32_t) * W, {}},
+        {det && det->stage_times, c->o_stage.p, det ? det->stage_times : nullptr, sizeof(double) * MP, {}},
+        {det && det->edge_times, c->o_edge.p, det ? det->edge_times : nullptr, sizeof(double) * MP, {}},
+        {det && det->placement, c->o_place.p, det ? det->placement : nullptr, sizeof(int32_t) * D, {}},
+        {want_sim, c->o_sim.p, want_sim ? det->simulated : nullptr, sizeof(double), {}},
+    };
+    for (Out& o : outs)
+      if (o.on && nw) {
+        o.h.resize(o.rec * nw);
+        CK(cudaMemcpyAsync(o.h.data(), o.src, o.rec * nw, cudaMemcpyDeviceToHost, c->stream));
+      }
     CK(c->gathered.ensure(sizeof(amp_record) * kk * n));
     CK(cudaStreamSynchronize(c->stream));
+    for (Out& o : outs)
+      if (o.on && nw)
+        for (const Segment& sg : segs)
+          std::memcpy(static_cast<unsigned char*>(o.dst) + (sg.first - begin) * o.rec, o.h.data() + sg.out * o.rec,
+                      sg.count * o.rec);
     account(c, 0, 0, nullptr, 0, &segs);
     resolve_kernel_times(c);
     return AMP_OK;
@@ -2182,12 +2199,23 @@ int amp_search_create(amp_ctx** out, const amp_problem* problem,
     if (rc == AMP_OK) {
       std::vector<int> devs(n_gpus);
       for (int r = 0; r < n_gpus; ++r) devs[r] = config->device + r;
-      ctx->comms.assign(n_gpus, nullptr);
-      const ncclResult_t nr = ncclCommInitAll(ctx->comms.data(), n_gpus, devs.data());
-      if (nr != ncclSuccess) {
-        ctx->comms.clear();
-        ctx->err = std::string("ncclCommInitAll: ") + ncclGetErrorString(nr);
-        rc = AMP_E_CUDA;
+      ctx->comm_devs = devs;
+      {
+        std::lock_guard<std::mutex> lk(g_comm_mu);
+        auto it = g_comm_pool.find(devs);
+        if (it != g_comm_pool.end() && !it->second.empty()) {
+          ctx->comms = it->second.back();
+          it->second.pop_back();
+        }
+      }
+      if (ctx->comms.empty()) {
+        ctx->comms.assign(n_gpus, nullptr);
+        const ncclResult_t nr = ncclCommInitAll(ctx->comms.data(), n_gpus, devs.data());
+        if (nr != ncclSuccess) {
+          ctx->comms.clear();
+          ctx->err = std::string("ncclCommInitAll: ") + ncclGetErrorString(nr);
+          rc = AMP_E_CUDA;
+        }
       }
     }
   }
@@ -2202,8 +2230,18 @@ int amp_search_create(amp_ctx** out, const amp_problem* problem,
 
 void amp_search_destroy(amp_ctx* ctx) {
   if (!ctx) return;
-  for (ncclComm_t c : ctx->comms)
-    if (c) ncclCommDestroy(c);
+  if (!ctx->comms.empty()) {
+    bool kept = false;
+    if (ctx->err.empty() && std::getenv("AMP_NO_RECYCLE") == nullptr) {  // to the next context
+      std::lock_guard<std::mutex> lk(g_comm_mu);
+      g_comm_pool[ctx->comm_devs].push_back(ctx->comms);
+      kept = true;
+    }
+    if (!kept)
+      for (ncclComm_t c : ctx->comms)
+        if (c) ncclCommDestroy(c);
+    ctx->comms.clear();
+  }
   for (amp_ctx* sub : ctx->subs) amp_search_destroy(sub);
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
