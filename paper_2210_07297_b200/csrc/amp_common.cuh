@@ -205,6 +205,15 @@ struct EvalParams {
   // keys [*n_rep]; run only while *sig_guard != 0 (NULL: always)
   const uint64_t* sig_keys;
   const uint32_t* sig_guard;
+  // gangs (k_dp<kSparseG>): each DP instance whose program has >= gang_min
+  // inner iterations is solved by G CTAs (stage cells split G ways, one
+  // cross-CTA barrier per stage); listed by k_gang_plan (NULL: off)
+  uint32_t* gang_hdr;   // [0] gangs, [1] units, [2] unit dispenser
+  uint32_t* gang_slot;  // [gangs] item slot (rep_list index, or item)
+  uint32_t* gang_off;   // [gangs + 1] first unit of each gang
+  uint32_t* gang_sync;  // [gangs][2] leader CTA (~0: not yet), stage parts finished
+  double gang_min, gang_unit;
+  int32_t gang_max, pad_gang;
   // hashed signature keys (class + codes wider than 63 bits): set when an
   // item's class / codes differ from its signature representative's (a
   // hash collision); K_est then reads the per-item cuts of the guarded

@@ -490,4 +490,140 @@ __device__ double sparse_solve(const int L, const int k, const int gas,
   return cost;
 }
 
+// Gang version of sparse_solve: part g of G CTAs solves the cells
+// [n g / G, n (g+1) / G) of every stage of one instance; the stage values
+// V0 / V1 and the argmins bpS are the leader CTA's global scratch, shared by
+// the gang (read through L2: other SMs write them), and *cnt counts the
+// finished (part, stage) pairs: stage j starts once G (j - 1) are done
+// (release add after the CTA barrier, acquire poll).  The leader (g = 0)
+// backtracks after the last stage and returns the cost; the same cells,
+// cuts and operations as sparse_solve, so the result is bit-identical.
+__device__ __forceinline__ void gang_stage_done(uint32_t* cnt, uint32_t target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+      if (v >= target) break;
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+template <class EdgeFn>
+__device__ double sparse_solve_gang(const int L, const int k, const int gas,
+                                    const double* __restrict__ Pf, const double* __restrict__ Dm,
+                                    const ProgDev& pg, const uint32_t* __restrict__ cells,
+                                    const uint32_t* __restrict__ cellpred,
+                                    const uint16_t* __restrict__ preds,
+                                    const uint32_t* __restrict__ stage, const EdgeFn& edge,
+                                    double* V0, double* V1, double2* PE0, double2* PE1,
+                                    uint8_t* bpS, int* cuts, int g, int G, uint32_t* cnt) {
+  const double g1 = (double)(gas - 1);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const uint32_t* cl = cells + pg.cell_base;
+  const uint32_t* cpd = cellpred + pg.cell_base;
+  const uint16_t* pd = preds + pg.pred_base;
+  const uint32_t* ss = stage + pg.stage_base;
+  {  // stage 1 (pipeline_dp.cpp:102-107), this part's cells of N_1
+    const uint32_t n = ss[1] - ss[0], a = ss[0] + (uint32_t)((uint64_t)n * g / G),
+                   b = ss[0] + (uint32_t)((uint64_t)n * (g + 1) / G);
+    for (uint32_t x = a + tid; x < b; x += nt) {
+      const uint32_t cell = cl[x];
+      const int i = cell >> 16, m = cell & 0xffff;
+      const double t1 = Pf[i] - Pf[0];
+      V1[x - ss[0]] = g1 * max0(t1 - Dm[m]) + t1;
+    }
+  }
+  if (k >= 2)
+    for (int c = 1 + tid; c < L; c += nt) PE0[c] = make_double2(Pf[c], edge(c, 0));  // stage 2
+  gang_stage_done(cnt, (uint32_t)G);
+  for (int j = 2; j <= k; ++j) {
+    const double* Vp = (j & 1) ? V0 : V1;
+    double* Vc = (j & 1) ? V1 : V0;
+    const double2* PE = (j & 1) ? PE1 : PE0;
+    if (j < k) {
+      double2* PN = (j & 1) ? PE0 : PE1;
+      for (int c = j + tid; c < L; c += nt) PN[c] = make_double2(Pf[c], edge(c, j - 1));
+    }
+    const uint32_t s0 = ss[j - 1], n = ss[j] - s0;
+    const uint32_t a = s0 + (uint32_t)((uint64_t)n * g / G), b = s0 + (uint32_t)((uint64_t)n * (g + 1) / G);
+    const int c0 = j - 1, np = (int)(b - a);
+    if (np * 2 > nt) {
+      for (uint32_t x = a + tid; x < b; x += nt) {
+        const uint32_t cell = cl[x];
+        const int i = cell >> 16, m = cell & 0xffff;
+        const double dm = Dm[m], Pi = Pf[i];
+        const uint2* q = reinterpret_cast<const uint2*>(pd + cpd[x]);
+        double best = CUDART_INF;
+        int bc = -1;
+        int c = c0;
+        for (; c + 3 < i; c += 4, ++q) {
+          const uint2 w = __ldg(q);
+          cut_step(__ldcg(Vp + (w.x & 0xffff)), Pi, PE[c], dm, g1, c, best, bc);
+          cut_step(__ldcg(Vp + (w.x >> 16)), Pi, PE[c + 1], dm, g1, c + 1, best, bc);
+          cut_step(__ldcg(Vp + (w.y & 0xffff)), Pi, PE[c + 2], dm, g1, c + 2, best, bc);
+          cut_step(__ldcg(Vp + (w.y >> 16)), Pi, PE[c + 3], dm, g1, c + 3, best, bc);
+        }
+        if (c < i) {
+          const uint2 w = __ldg(q);
+          cut_step(__ldcg(Vp + (w.x & 0xffff)), Pi, PE[c], dm, g1, c, best, bc);
+          if (c + 1 < i) cut_step(__ldcg(Vp + (w.x >> 16)), Pi, PE[c + 1], dm, g1, c + 1, best, bc);
+          if (c + 2 < i) cut_step(__ldcg(Vp + (w.y & 0xffff)), Pi, PE[c + 2], dm, g1, c + 2, best, bc);
+        }
+        Vc[x - s0] = best;
+        bpS[x] = (uint8_t)bc;
+      }
+    } else {
+      int GL = 2;  // lanes per cell (sparse_solve's few-cells branch)
+      while (GL < 32 && np * GL * 2 <= nt) GL <<= 1;
+      const int gl = tid & (GL - 1);
+      const int per = nt / GL;
+      for (int base = 0; base < np; base += per) {
+        const int xi = base + tid / GL;
+        double best = CUDART_INF;
+        int bc = -1;
+        if (xi < np) {
+          const uint32_t x = a + xi;
+          const uint32_t cell = cl[x];
+          const int i = cell >> 16, m = cell & 0xffff;
+          const double dm = Dm[m], Pi = Pf[i];
+          const uint16_t* q = pd + cpd[x] + gl;
+          for (int c = c0 + gl; c < i; c += GL, q += GL)
+            cut_step(__ldcg(Vp + __ldg(q)), Pi, PE[c], dm, g1, c, best, bc);
+        }
+        for (int o = GL >> 1; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+          if (ov < best || (ov == best && oc < bc)) {
+            best = ov;
+            bc = oc;
+          }
+        }
+        if (xi < np && gl == 0) {
+          Vc[a + xi - s0] = best;
+          bpS[a + xi] = (uint8_t)bc;
+        }
+      }
+    }
+    gang_stage_done(cnt, (uint32_t)G * (uint32_t)j);
+  }
+  double cost = 0.0;
+  if (g == 0 && tid == 0) {
+    cost = __ldcg(((k & 1) ? V1 : V0));
+    cuts[k] = L;
+    uint32_t x = ss[k - 1];
+    for (int j = k; j >= 2; --j) {
+      const int c = __ldcg(reinterpret_cast<const unsigned char*>(bpS) + x);
+      cuts[j - 1] = c;
+      x = ss[j - 2] + pd[cpd[x] + (c - (j - 1))];
+    }
+    cuts[0] = 0;
+  }
+  __syncthreads();
+  return cost;
+}
+
 }  // namespace amp

@@ -229,7 +229,76 @@ struct DpShared {
   int cls, pair;
   ClassDev cl;
   PairDev pr;
+  uint32_t leader, pad;
 };
+
+// The gang list of a K_dp launch: every item whose program has >= gang_min
+// inner iterations, with G = clamp(inner / gang_unit, 2, gang_max) parts;
+// units (gang, part) numbered gang-major (one CTA).
+__global__ void __launch_bounds__(1024) k_gang_plan(EvalParams p) {
+  __shared__ uint32_t s_c[32], s_g[32], s_nb, s_nu;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+  const uint64_t n_items = (p.sig_guard && *p.sig_guard == 0) ? 0 : (p.rep_list ? *p.n_rep : p.n_dp);
+  if (tid == 0) s_nb = s_nu = 0;
+  __syncthreads();
+  for (uint64_t base = 0; base < n_items; base += blockDim.x) {
+    const uint64_t slot = base + tid;
+    uint32_t G = 0;
+    if (slot < n_items) {
+      const uint64_t u = p.rep_list ? p.rep_list[slot] : slot;
+      const CandWork& wk = p.work[u];
+      if (wk.fail_code == 0) {
+        const double inner = p.prog_inner[p.class_prog[wk.cls]];
+        if (inner >= p.gang_min)
+          G = (uint32_t)min(p.gang_max, max(2, (int)(inner / p.gang_unit)));
+      }
+    }
+    // block exclusive scans of (G > 0) and G
+    uint32_t c = G ? 1u : 0u, gi = G;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, c, o), z = __shfl_up_sync(0xffffffffu, gi, o);
+      if (lane >= o) {
+        c += y;
+        gi += z;
+      }
+    }
+    if (lane == 31) {
+      s_c[w] = c;
+      s_g[w] = gi;
+    }
+    __syncthreads();
+    uint32_t pc = 0, pgi = 0, tc = 0, tg = 0;
+    for (int x = 0; x < nw; ++x) {
+      if (x < w) {
+        pc += s_c[x];
+        pgi += s_g[x];
+      }
+      tc += s_c[x];
+      tg += s_g[x];
+    }
+    if (G) {
+      const uint32_t b = s_nb + pc + c - 1;
+      p.gang_slot[b] = (uint32_t)slot;
+      p.gang_off[b] = s_nu + pgi + gi - G;
+      p.gang_sync[2 * b] = ~0u;
+      p.gang_sync[2 * b + 1] = 0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      s_nb += tc;
+      s_nu += tg;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    p.gang_off[s_nb] = s_nu;
+    p.gang_hdr[0] = s_nb;
+    p.gang_hdr[1] = s_nu;
+    p.gang_hdr[2] = 0;
+  }
+}
+
+
 
 // MODE selects the DP implementation and where its working set lives
 // (compile-time so the compiler emits LDS/STS instead of generic loads):
@@ -304,6 +373,81 @@ __global__ void __launch_bounds__(MODE == kSparseG ? 1024 : (MODE == kSparseS ? 
     sh.cls = -1;
     sh.pair = -1;
   }
+  // ---- gangs first (k_gang_plan): units (gang, part) in gang-major order
+  //      from their own counter; the first part of a gang publishes its CTA,
+  //      whose scratch holds the gang's stage values and argmins.  Every
+  //      CTA a part waits on holds a unit of the same gang, and only the
+  //      last gang being dealt can lack parts, so the gangs cannot deadlock.
+  if constexpr (MODE == kSparseG) {
+    if (p.gang_hdr) {
+      const uint32_t NB = p.gang_hdr[0], NU = p.gang_hdr[1];
+      for (;;) {
+        if (tid == 0) sh.u = atomicAdd(&p.gang_hdr[2], 1u);
+        __syncthreads();
+        const uint32_t un = (uint32_t)sh.u;
+        if (un >= NU) break;
+        int lo = 0, hi = (int)NB - 1;  // the last gang whose first unit is <= un
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (p.gang_off[mid] <= un) lo = mid;
+          else hi = mid - 1;
+        }
+        const int g = (int)(un - p.gang_off[lo]), G = (int)(p.gang_off[lo + 1] - p.gang_off[lo]);
+        const uint64_t slot = p.gang_slot[lo];
+        const uint64_t u = p.rep_list ? p.rep_list[slot] : slot;
+        const CandWork w = p.work[u];
+        uint32_t* gs = p.gang_sync + 2 * (size_t)lo;
+        if (tid == 0) {
+          uint32_t ld = blockIdx.x;
+          if (g == 0) {
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gs), "r"(ld) : "memory");
+          } else {
+            for (;;) {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(ld) : "l"(gs) : "memory");
+              if (ld != ~0u) break;
+              __nanosleep(64);
+            }
+          }
+          sh.leader = ld;
+        }
+        if (w.cls != sh.cls) {
+          __syncthreads();
+          if (tid == 0) {
+            sh.cls = w.cls;
+            sh.cl = p.cls[w.cls];
+            sh.pr = p.pairs[sh.cl.pair];
+          }
+        }
+        __syncthreads();
+        const ClassDev cl = sh.cl;
+        const int pp = cl.pp;
+        if (sh.pair != cl.pair) {
+          const double* gdom = p.domain + (size_t)cl.pair * p.nv_stride;
+          for (int x = tid; x < sh.pr.M; x += nt) Dm[x] = gdom[x];
+          for (int x = tid; x < LP; x += nt) Pf[x] = p.prefix[(size_t)cl.pair * LP + x];
+          __syncthreads();
+          if (tid == 0) sh.pair = cl.pair;
+        }
+        const uint32_t ldr = sh.leader;
+        double* GV0 = p.vbuf + (size_t)ldr * 2 * p.max_cells;
+        uint8_t* gbp = p.bp + (size_t)ldr * p.bp_stride;
+        EdgeFromBandwidth ef{p.act, p.bwqb + u * maxpp, cl.mbs};
+        const ProgDev pg = p.progs[p.class_prog[w.cls]];
+        sparse_solve_gang(L, pp, cl.gas, Pf, Dm, pg, p.cells, p.cellpred, p.preds, p.stage, ef, GV0,
+                          GV0 + p.max_cells, reinterpret_cast<double2*>(E), reinterpret_cast<double2*>(E) + L,
+                          gbp, cuts, g, G, gs + 1);
+        if (g == 0) {
+          uint8_t* co = p.repcuts ? p.repcuts + slot * (maxpp + 1) : p.cutsb + u * (maxpp + 1);
+          for (int q = tid; q <= pp; q += nt) co[q] = (uint8_t)cuts[q];
+          if (p.exec_counters && tid == 0) {
+            atomicAdd(&p.exec_counters[0], 1ull);
+            atomicAdd(&p.exec_counters[1], (unsigned long long)p.prog_inner[p.class_prog[w.cls]]);
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
   // work is taken kDpBatch items at a time: one atomic and one coalesced
   // load of the work records and bandwidth rows per batch
   int bi = 0, bn = 0;
@@ -331,6 +475,8 @@ __global__ void __launch_bounds__(MODE == kSparseG ? 1024 : (MODE == kSparseS ? 
     const int my = bi++;
     const CandWork& w = wq[my];
     if (w.fail_code != 0) continue;  // failed before the DP (uniform)
+    if (MODE == kSparseG && p.gang_hdr && p.prog_inner[p.class_prog[w.cls]] >= p.gang_min)
+      continue;  // solved by its gang (above)
     const uint64_t slot = bbase + my;
     const uint64_t u = p.rep_list ? p.rep_list[slot] : slot;
     if (p.exec_counters && tid == 0) {  // executed work (roofline accounting)

@@ -180,6 +180,12 @@ struct amp_ctx {
   int max_n1 = 1, max_v = 1, max_rest = 1;
   int multi_b = 0;                 // K_dp multi: candidates per group (0: per-candidate k_dp)
   std::vector<double> prog_inner_raw;  // unpadded inner iterations per program
+  // gangs: DP instances of programs >= gang_min inner iterations solved by
+  // several CTAs (k_gang_plan + the gang phase of k_dp<kSparseG>)
+  bool gang_on = false;
+  double gang_min = 5e5, gang_unit = 4e6;  // (C4: DP 12.8 -> 3.4 ms; smaller parts lose to the per-stage barrier)
+  int gang_max = 32;
+  DevBuf gang_hdr, gang_slot, gang_off, gang_sync;
   size_t v_stride = 0;
   DevBuf progs_d, stage_d, class_prog_d, cells, cellpred, preds, vbuf;
   DevBuf c_work, c_place, c_bwq, c_cuts, c_bwc, c_placep;  // pipeline chunk buffers
@@ -843,6 +849,14 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
                        (((size_t)ctx->max_prog_cells + 15) & ~size_t(15));
     const bool v_smem = small + v_b <= 64 * 1024;
     mode = v_smem ? kSparseS : kSparseG;
+    if (mode == kSparseG && std::getenv("AMP_NO_GANG") == nullptr) {
+      // (C4: a few instances hold most of the DP — pp = 64 programs of
+      // ~1e7 iterations — and would each bound the launch on one SM)
+      if (const char* e = std::getenv("AMP_GANG_MIN")) ctx->gang_min = std::atof(e);
+      if (const char* e = std::getenv("AMP_GANG_UNIT")) ctx->gang_unit = std::atof(e);
+      if (const char* e = std::getenv("AMP_GANG_MAX")) ctx->gang_max = std::max(2, std::atoi(e));
+      for (double x : ctx->prog_inner_raw) ctx->gang_on = ctx->gang_on || x >= ctx->gang_min;
+    }
     ctx->smem_bytes = small + (v_smem ? v_b : 0);
     ctx->eval_threads = v_smem ? 128 : 1024;
     ctx->bp_stride = v_smem ? 0 : (((size_t)ctx->max_prog_cells + 255) & ~size_t(255));
@@ -1366,6 +1380,23 @@ int run_sig_dp(amp_ctx* ctx, EvalParams& ep, const HashParams& hp) {
   es.rep_list = by_rep ? ctx->dd_rep_list.as<uint32_t>() : nullptr;
   es.repcuts = ctx->dd_repcuts.as<uint8_t>();
   es.sig_code_bits = ctx->code_bits;
+  if (ctx->gang_on && ctx->eval_fn == (const void*)k_dp<kSparseG>) {
+    CK(ctx->gang_hdr.ensure(4 * sizeof(uint32_t)));
+    CK(ctx->gang_slot.ensure(sizeof(uint32_t) * C));
+    CK(ctx->gang_off.ensure(sizeof(uint32_t) * (C + 1)));
+    CK(ctx->gang_sync.ensure(2 * sizeof(uint32_t) * C));
+    es.gang_hdr = ctx->gang_hdr.as<uint32_t>();
+    es.gang_slot = ctx->gang_slot.as<uint32_t>();
+    es.gang_off = ctx->gang_off.as<uint32_t>();
+    es.gang_sync = ctx->gang_sync.as<uint32_t>();
+    es.gang_min = ctx->gang_min;
+    es.gang_unit = ctx->gang_unit;
+    es.gang_max = std::min(ctx->gang_max, ctx->n_ctas);  // a gang's parts must be co-resident
+    k_gang_plan<<<1, 1024, 0, ctx->stream>>>(es);
+    CK(cudaGetLastError());
+    DBG_SYNC("k_gang_plan");
+    ctx->launches += 1;
+  }
   void* args[] = {&es};
   CK(cudaLaunchKernel(ctx->eval_fn, dim3(ctx->n_ctas), dim3(ctx->eval_threads), args, ctx->smem_bytes,
                       ctx->stream));
