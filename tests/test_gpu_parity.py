@@ -691,3 +691,29 @@ def test_speculative_anneal_equals_sequential_and_reference(name, seed, record_a
         enc = P.EncodedProblem.from_scenario(sc)
         ic, bc, nrec = B.ref_anneal(enc, 150, seed, record_all=record_all)
         assert (ic, bc, nrec) == (runs[0].initial_cost, runs[0].best_cost, len(runs[0].record))
+
+
+@pytest.mark.parametrize("env", [{"AMP_NO_GANG": "1"}, {"AMP_GANG_UNIT": "1e5", "AMP_GANG_MIN": "1e5"}])
+def test_gang_dp_equals_single_cta(env, monkeypatch):
+    """C4's large DP instances solved by CTA gangs (k_gang_plan + the gang
+    phase of k_dp<kSparseG>; the pp = 64 programs must be
+    multi-CTA) give every record, cut and stage time of the one-CTA-per-
+    instance path (AMP_NO_GANG=1) and of many small gangs, on the C4 plan()
+    space and a P = 3 sweep (more instances per program)."""
+    sc = P.synthetic_c4()
+    enc = P.EncodedProblem.from_scenario(sc)
+    for P_ in (1, 3):
+        outs = []
+        for e in ({}, env):
+            for k in ("AMP_NO_GANG", "AMP_GANG_UNIT", "AMP_GANG_MIN"):
+                monkeypatch.delenv(k, raising=False)
+            for k, v in e.items():
+                monkeypatch.setenv(k, v)
+            with planner.Searcher(enc, placements_per_class=P_, seed=4) as s:
+                top, allr, bufs = s.run(0, s.num_candidates, k=10, want_all=True, details=True)
+                outs.append((top, allr, bufs, s.stats()))
+        assert np.array_equal(outs[0][1].view(np.uint8), outs[1][1].view(np.uint8))
+        assert np.array_equal(outs[0][0].view(np.uint8), outs[1][0].view(np.uint8))
+        for key in ("cuts", "stage_times"):
+            assert np.array_equal(outs[0][2][key], outs[1][2][key], equal_nan=True)
+        assert outs[0][3]["dp_instances"] == outs[1][3]["dp_instances"] > 0
