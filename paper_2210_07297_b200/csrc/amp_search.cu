@@ -2203,25 +2203,26 @@ int amp_search_create(amp_ctx** out, const amp_problem* problem,
   }
   *out = nullptr;
   amp_ctx* ctx = new amp_ctx();
-  int rc = setup(ctx, problem, config);
   const int n_gpus = config ? config->n_gpus : 1;
+  // a context per further device (same problem, same candidate space), set
+  // up by a thread each while this thread sets up the first device's
+  std::vector<amp_ctx*> subs(n_gpus > 1 ? n_gpus - 1 : 0, nullptr);
+  std::vector<int> rcs(subs.size(), AMP_OK);
+  std::vector<std::thread> th;
+  for (int r = 1; r < n_gpus; ++r)
+    th.emplace_back([&, r]() {
+      amp_search_config c = *config;
+      c.device = config->device + r;
+      c.n_gpus = 1;
+      AllocStream g(nullptr);
+      subs[r - 1] = new amp_ctx();
+      rcs[r - 1] = setup(subs[r - 1], problem, &c);
+    });
+  int rc = setup(ctx, problem, config);
+  for (auto& t : th) t.join();
+  if (n_gpus > 1) ctx->subs = subs;
   if (rc == AMP_OK && n_gpus > 1) {
-    // a context per further device (same problem, same candidate space),
-    // set up concurrently, and one NCCL communicator per device
-    std::vector<amp_ctx*> subs(n_gpus - 1, nullptr);
-    std::vector<int> rcs(n_gpus - 1, AMP_OK);
-    std::vector<std::thread> th;
-    for (int r = 1; r < n_gpus; ++r)
-      th.emplace_back([&, r]() {
-        amp_search_config c = *config;
-        c.device = config->device + r;
-        c.n_gpus = 1;
-        AllocStream g(nullptr);
-        subs[r - 1] = new amp_ctx();
-        rcs[r - 1] = setup(subs[r - 1], problem, &c);
-      });
-    for (auto& t : th) t.join();
-    ctx->subs = subs;
+    // and one NCCL communicator per device
     for (int r = 1; r < n_gpus && rc == AMP_OK; ++r)
       if (rcs[r - 1] != AMP_OK) {
         ctx->err = "device " + std::to_string(config->device + r) + ": " + subs[r - 1]->err;
