@@ -1398,8 +1398,12 @@ int run_sig_dp(amp_ctx* ctx, EvalParams& ep, const HashParams& hp) {
     ctx->launches += 1;
   }
   void* args[] = {&es};
-  CK(cudaLaunchKernel(ctx->eval_fn, dim3(ctx->n_ctas), dim3(ctx->eval_threads), args, ctx->smem_bytes,
-                      ctx->stream));
+  if (es.gang_hdr)  // a gang's parts wait on each other: co-residency guaranteed by a cooperative launch
+    CK(cudaLaunchCooperativeKernel(ctx->eval_fn, dim3(ctx->n_ctas), dim3(ctx->eval_threads), args,
+                                   ctx->smem_bytes, ctx->stream));
+  else
+    CK(cudaLaunchKernel(ctx->eval_fn, dim3(ctx->n_ctas), dim3(ctx->eval_threads), args, ctx->smem_bytes,
+                        ctx->stream));
   CK(cudaGetLastError());
   DBG_SYNC("k_dp_multi (signatures)");
   ctx->launches += 1;
