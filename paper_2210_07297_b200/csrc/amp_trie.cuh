@@ -257,7 +257,7 @@ __device__ void plan_level(const TrieParams& p, int d, uint32_t total, uint64_t 
       bs = (unsigned long long)K * ts.n;
     }
     nx[c] = chunks;
-    s_tiles[c] = (unsigned long long)runs * chunks;
+    s_tiles[NC - 1 - c] = (unsigned long long)runs * chunks;  // (dispense order: last class first)
     s_v[c] = vs;
     s_b[c] = bs;
     s_r[c] = runs;
@@ -311,16 +311,19 @@ __device__ void build_tile_list(const TrieParams& p, uint64_t gtid, uint64_t gst
     while (d < p.nq && st->tile_off[d + 1] <= t) ++d;
     const uint32_t tt = (uint32_t)t - st->tile_off[d];
     const uint32_t* tb = p.tbase + (size_t)d * (p.n_cls + 1);
-    int lo = 0, hi = p.n_cls - 1;  // last class with tbase <= tt
+    // within a depth the classes are dealt last class first (the plan()
+    // list ends with the deepest pipelines, whose chain of levels is the
+    // launch's critical path): tbase is by dispense position
+    int lo = 0, hi = p.n_cls - 1;  // last position with tbase <= tt
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
       if (tb[mid] <= tt) lo = mid;
       else hi = mid - 1;
     }
-    const int c = lo;
+    const int c = p.n_cls - 1 - lo;
     const TrieStage ts = p.tstage[(size_t)c * (p.max_pp + 1) + d + 1];
     const uint32_t chunks = p.nxc[(size_t)d * p.n_cls + c];
-    const uint32_t lt = tt - tb[c], run = lt / chunks, cc = lt - run * chunks;
+    const uint32_t lt = tt - tb[lo], run = lt / chunks, cc = lt - run * chunks;
     const uint32_t nbc = p.nb[(size_t)d * p.n_cls + c], K = p.nK[(size_t)d * p.n_cls + c];
     TrieTile tl;
     const uint32_t n0 = nbc + run * ts.tn;
@@ -538,7 +541,7 @@ __device__ void plan_depth(const TrieParams& p, int d, unsigned long long* sm4) 
       bs = (unsigned long long)K * ts.n;
     }
     nx[c] = chunks;
-    s_tiles[c] = (unsigned long long)runs * chunks;
+    s_tiles[NC - 1 - c] = (unsigned long long)runs * chunks;  // (dispense order: last class first)
     s_v[c] = vs;
     s_b[c] = bs;
     s_r[c] = runs;
