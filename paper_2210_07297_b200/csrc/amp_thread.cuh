@@ -155,6 +155,11 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
   int c;
   decode_item(p, p.t0 + u, index, out, c, pl, seg_hint);
   const ClassDev cl = p.cls[c];
+  // the placement's code-table entry, issued with the pair load (it is used
+  // only when the item does not fail early, but its address is valid)
+  const bool has_cw = FAST && p.ctab != nullptr;
+  ulonglong2 cwv = make_ulonglong2(0, 0);
+  if (has_cw && (cl.pp > 1 || cl.dp > 1) && cl.crow >= 0) cwv = p.ctab[(uint64_t)cl.crow * p.P + pl];
   const PairDev pr = p.pairs[cl.pair];
   const int pp = cl.pp, dp = cl.dp, tmp = cl.tmp;
   int fc = 0, flayer = -1;
@@ -209,12 +214,7 @@ __device__ __forceinline__ void place_one(const EvalParams& p, const PlaceSmem& 
       }
     }
     if (store && p.placep) p.placep[u] = perm;
-    ulonglong2 cwv = make_ulonglong2(0, 0);
-    const bool has_cw = FAST && p.ctab != nullptr;
-    if (has_cw) {
-      if (pp > 1 || dp > 1) cwv = p.ctab[(uint64_t)cl.crow * p.P + pl];
-      if (cwo) *cwo = cwv;
-    }
+    if (has_cw && cwo) *cwo = cwv;
     if (store && p.need_place_rows) {
       int32_t* prow = p.placeb + u * D;
       for (int x = 0; x < D; ++x) prow[x] = nib(perm, x);
