@@ -412,7 +412,7 @@ __global__ void k_code_table(EvalParams p, const int32_t* row_shape, int n_rows,
 template <int PP, int DPn, int TMP>
 __device__ __forceinline__ void est_shape(const EvalParams& p, const ulonglong2 cw, const CandWork& w,
                                           const ClassDev& cl, uint64_t u, bool fused, int code0, int& fc,
-                                          double& pipeline, double& dpsync) {
+                                          double& pipeline, double& dpsync, uint32_t rs) {
   const int L = p.L, LP = L + 1, maxpp = p.max_pp;
   int cuts[PP + 1];
   if (PP >= 3) {  // the signature run's cuts (memoised DP) or this item's
@@ -420,7 +420,7 @@ __device__ __forceinline__ void est_shape(const EvalParams& p, const ulonglong2 
       // one replica whose boundary codes are the signature's: the whole
       // estimate is a function of the run (k_run_pipe, same operations),
       // stored by hash slot when the shape kernels look runs up by slot
-      const double v = p.run_slot ? p.run_pipe[p.run_slot[u]]
+      const double v = p.run_slot ? p.run_pipe[rs]
                                   : p.run_pipe[p.rep_of ? p.rep_of[u] : 0u];
       if (v != v) {
         fc = AMP_FAIL_CEILING;
@@ -430,7 +430,7 @@ __device__ __forceinline__ void est_shape(const EvalParams& p, const ulonglong2 
       }
       return;
     }
-    const uint64_t run = p.run_slot ? p.run_of_slot[p.run_slot[u]] : p.rep_of ? p.rep_of[u] : ~0ull;
+    const uint64_t run = p.run_slot ? p.run_of_slot[rs] : p.rep_of ? p.rep_of[u] : ~0ull;
     const uint8_t* ci = run != ~0ull ? p.repcuts + run * (maxpp + 1) : p.cutsb + u * (maxpp + 1);
 #pragma unroll
     for (int q = 0; q <= PP; ++q) cuts[q] = ci[q];
@@ -532,6 +532,9 @@ template <int DT>
 __device__ __forceinline__ void est_fast_item(const EvalParams& p, const PlaceSmem& PS, uint64_t u,
                                               amp_record& rec, bool& ok, int* seg_hint) {
   const bool fused = p.fuse_light && u >= p.n_dp;
+  // a heavy item's signature-run slot, issued before its decode (the run's
+  // cuts / estimate lookups hang off it)
+  const uint32_t rs = (!fused && p.run_slot && u < p.n_dp) ? p.run_slot[u] : 0u;
   CandWork w;
   uint64_t perm = 0;
   int code0 = 0;
@@ -549,7 +552,7 @@ __device__ __forceinline__ void est_fast_item(const EvalParams& p, const PlaceSm
     switch (cl.pp * 1024 + cl.dp * 32 + cl.tmp) {
 #define AMP_SHAPE(a, b, c)                                                    \
   case a * 1024 + b * 32 + c:                                                 \
-    est_shape<a, b, c>(p, cw, w, cl, u, fused, code0, fc, pipeline, dpsync); \
+    est_shape<a, b, c>(p, cw, w, cl, u, fused, code0, fc, pipeline, dpsync, rs); \
     break;
       AMP_SHAPE(1, 1, 16) AMP_SHAPE(1, 2, 8) AMP_SHAPE(1, 4, 4) AMP_SHAPE(1, 8, 2) AMP_SHAPE(1, 16, 1)
       AMP_SHAPE(2, 1, 8) AMP_SHAPE(2, 2, 4) AMP_SHAPE(2, 4, 2) AMP_SHAPE(2, 8, 1)
