@@ -1079,7 +1079,7 @@ int setup(amp_ctx* ctx, const amp_problem* p, const amp_search_config* cfg) {
   ctx->n_ctas = n_ctas;
   ctx->sms = prop.multiProcessorCount;
   const char* ec = std::getenv("AMP_EST_CTAS_PER_SM");
-  ctx->est_ctas = prop.multiProcessorCount * (ec ? std::atoi(ec) : 3);  // 8-warp estimate CTAs per SM (80 regs)
+  ctx->est_ctas = prop.multiProcessorCount * (ec ? std::atoi(ec) : 4);  // 8-warp estimate CTAs per SM (64 regs)
   // chunk size: keep the per-chunk buffers within ~256 MB
   const size_t per_item = sizeof(CandWork) + sizeof(int32_t) * D + sizeof(double) * ctx->max_pp +
                           (ctx->max_pp + 1);

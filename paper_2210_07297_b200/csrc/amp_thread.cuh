@@ -596,7 +596,7 @@ constexpr int kEstTWarps = 8;
 
 template <int DT, bool FAST = false>
 #ifndef AMP_EST_MINB
-#define AMP_EST_MINB 3
+#define AMP_EST_MINB 4  // (64 registers: 4 CTAs x 8 warps per SM)
 #endif
 __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalParams p) {
   __shared__ PlaceSmem PS;
@@ -628,20 +628,22 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
   // from the previous chunk (an item that cannot beat it cannot reach the
   // CTA's top-k), else nothing (w_kf = 2).  The exact key (index included)
   // matters: a chunk of failing candidates would otherwise pass every item.
-  // (the warp list's count and the threshold's index live in shared memory:
+  // (the warp list's count and threshold live in shared memory:
   // registers are the kernel's occupancy limit)
   __shared__ unsigned long long w_ki[kEstTWarps];
-  int w_kf = 2;
-  double w_kt = CUDART_INF;
+  __shared__ double w_kt[kEstTWarps];
+  __shared__ int w_kf[kEstTWarps];
   if (lane == 0) {
     wcount[wib] = 0;
+    w_kf[wib] = 2;
+    w_kt[wib] = CUDART_INF;
     w_ki[wib] = ~0ull;
-  }
-  if (p.k > 0 && n_top == p.k) {
-    const amp_record& e = mytop[p.k - 1];
-    w_kf = e.fail_code < 0 ? 2 : (e.fail_code != 0 ? 1 : 0);
-    w_kt = e.total;
-    if (lane == 0) w_ki[wib] = e.index;
+    if (p.k > 0 && n_top == p.k) {
+      const amp_record& e = mytop[p.k - 1];
+      w_kf[wib] = e.fail_code < 0 ? 2 : (e.fail_code != 0 ? 1 : 0);
+      w_kt[wib] = e.total;
+      w_ki[wib] = e.index;
+    }
   }
   __syncwarp();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -919,7 +921,9 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
       bool cand = false;
       if (live) {
         const int rf = ok ? 0 : 1;
-        cand = rf != w_kf ? rf < w_kf : (rf == 0 && rec.total != w_kt ? rec.total < w_kt : rec.index < w_ki[wib]);
+        const int kf = w_kf[wib];
+        const double kt = w_kt[wib];
+        cand = rf != kf ? rf < kf : (rf == 0 && rec.total != kt ? rec.total < kt : rec.index < w_ki[wib]);
         if (cand) stage_rec[wib][lane] = rec;
       }
       unsigned m = __ballot_sync(0xffffffffu, cand);
@@ -931,13 +935,11 @@ __global__ void __launch_bounds__(kEstTWarps * 32, AMP_EST_MINB) k_est_t(EvalPar
           topk_insert(wtop[wib], wcount[wib], p.k, stage_rec[wib][b]);
         }
         if (wcount[wib] == p.k) {
-          w_kf = wtop[wib][p.k - 1].fail_code != 0;
-          w_kt = wtop[wib][p.k - 1].total;
+          w_kf[wib] = wtop[wib][p.k - 1].fail_code != 0;
+          w_kt[wib] = wtop[wib][p.k - 1].total;
           w_ki[wib] = wtop[wib][p.k - 1].index;
         }
       }
-      w_kf = __shfl_sync(0xffffffffu, w_kf, 0);
-      w_kt = __shfl_sync(0xffffffffu, w_kt, 0);
       __syncwarp();
     }
   }
